@@ -1,0 +1,205 @@
+/*
+ * specden_b200.h — C-ABI of the B200-native SLQ hot path (HessFormer, arxiv
+ * 2505.11564). Implemented by paper_2505_11564_b200/libspecden_b200.so
+ * (hand-written sm_100a CUDA kernels + a C++ host engine).
+ *
+ * Conventions
+ *  - Every entry point returns sd_status; on failure sd_last_error() holds a
+ *    thread-local message. Codes 1-6 are the six classes of
+ *    proj/include/specden/errors.hpp:13-41; 7/8 are CUDA / NCCL failures.
+ *  - Device buffers are CALLER-OWNED (plain pointers + element counts).
+ *    Launchers ("sd_k_*") never allocate, never synchronise, and are ordered
+ *    on the caller's stream. Engine calls that need scratch take a caller
+ *    workspace sized by a matching *_workspace_bytes query.
+ *  - prec: SD_F32 (float* storage) or SD_F64 (double* storage), the
+ *    Precision of proj/include/specden/precision.hpp:15-19. Scalars (dots,
+ *    alpha, beta) are always f64 (precision.hpp:9-14).
+ *  - Shards: a rank owns [begin, end) of a logical vector of length `total`
+ *    (ShardLayout, proj/include/specden/layout.hpp:12-72); pointers passed
+ *    for a shard point at its first owned element.
+ */
+#ifndef SPECDEN_B200_H
+#define SPECDEN_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* sd_stream; /* == cudaStream_t */
+
+typedef enum {
+  SD_OK = 0,
+  SD_CONFIG_ERROR = 1,    /* config_error   errors.hpp:13-17 */
+  SD_LAYOUT_ERROR = 2,    /* layout_error   errors.hpp:19-22 */
+  SD_ARGUMENT_ERROR = 3,  /* argument_error errors.hpp:24-27 */
+  SD_NUMERICAL_ERROR = 4, /* numerical_error errors.hpp:29-32 */
+  SD_STATE_ERROR = 5,     /* state_error    errors.hpp:34-38 */
+  SD_PROTOCOL_ERROR = 6,  /* protocol_error errors.hpp:40-43 */
+  SD_CUDA_ERROR = 7,
+  SD_NCCL_ERROR = 8
+} sd_status;
+
+enum { SD_F32 = 0, SD_F64 = 1 };
+enum { SD_GAUSSIAN = 0, SD_RADEMACHER = 1, SD_ONE_HOT = 2 }; /* ProbeDist, sharded.hpp:34 */
+enum { SD_REORTH_NONE = 0, SD_REORTH_FULL = 1, SD_REORTH_SELECTIVE = 2 };
+
+const char* sd_last_error(void);
+int sd_abi_version(void);
+
+/* ---------------------------------------------------------------- RNG (host)
+ * Replaces mix64/keyed_counter/uniform01/gaussian/rademacher/uniform_index,
+ * proj/include/specden/rng.hpp:17-52 (host copies for bookkeeping/tests). */
+uint64_t sd_keyed_counter(uint64_t seed, uint64_t counter);
+double sd_rademacher(uint64_t seed, uint64_t i);
+uint64_t sd_uniform_index(uint64_t seed, uint64_t i, uint64_t n);
+
+/* ------------------------------------------------------------- layout (host)
+ * split_evenly (layout.hpp:59-72), validate_layout (layout.hpp:45-55),
+ * ShardLayout::owner (layout.hpp:28-32). `begins/ends` hold >= n entries. */
+sd_status sd_split_evenly(uint64_t dim, uint64_t n, uint64_t* begins, uint64_t* ends, uint64_t* count);
+sd_status sd_validate_layout(uint64_t total, uint64_t n, const uint64_t* begins, const uint64_t* ends);
+sd_status sd_layout_owner(uint64_t n, const uint64_t* ends, uint64_t i, uint64_t* owner);
+
+/* ------------------------------------------------- blocked partials (host)
+ * Shape of one rank's BlockedPartial (reduction.hpp:40-71) on the fixed
+ * 1024-block global grid: n_head raw terms, n_sums block folds, n_tail raw
+ * terms. Device partial buffers store them contiguously as f64
+ * [head | sums | tail]; sd_partial_len = n_head + n_sums + n_tail. */
+sd_status sd_partial_shape(uint64_t begin, uint64_t end, uint64_t total, uint64_t* n_head, uint64_t* n_sums,
+                           uint64_t* n_tail);
+uint64_t sd_partial_len(uint64_t begin, uint64_t end, uint64_t total);
+/* Host fold of per-rank partials in rank order (combine_blocked,
+ * reduction.hpp:76-107): parts[r] points at rank r's [head|sums|tail]. */
+sd_status sd_combine_partials_host(uint64_t nranks, const uint64_t* begins, const uint64_t* ends, uint64_t total,
+                                   const double* const* parts, double* out);
+
+/* ----------------------------------------------------- vector kernels (GPU)
+ * draw_probe fill (sharded.cpp:59-76, unnormalised): x[i-begin] =
+ * round(dist(seed, i)) for i in [begin, end). */
+sd_status sd_k_probe_fill(void* x, uint64_t begin, uint64_t end, uint64_t seed, int dist, uint64_t one_hot_index,
+                          int prec, sd_stream s);
+/* Blocked dot partial of a[i]*b[i] over this rank's shard (dot, sharded.cpp:85-100). */
+sd_status sd_k_dot_partial(const void* a, const void* b, uint64_t begin, uint64_t end, uint64_t total, int prec,
+                           double* partial, sd_stream s);
+/* m independent partial sets folded in rank order on the device:
+ * partials laid out [rank][seq][plen_r]; out[seq] = combine_blocked. */
+sd_status sd_k_combine(uint64_t nranks, const uint64_t* begins, const uint64_t* ends, uint64_t total, uint64_t m,
+                       const double* partials, double* out, sd_stream s);
+/* y = round(y + alpha*x) with alpha = sign * (*alpha_dev) (axpy, sharded.cpp:106-118). */
+sd_status sd_k_axpy(const void* x, void* y, uint64_t n, const double* alpha_dev, double sign, int prec, sd_stream s);
+/* out = round(c*x), c = (*c_dev) or, with reciprocal, 1.0/(*c_dev) (scale, sharded.cpp:120-130). */
+sd_status sd_k_scale(const void* x, void* out, uint64_t n, const double* c_dev, int reciprocal, int prec,
+                     sd_stream s);
+/* Fused recurrence pass: y = round(y - (*coef)*x) (skipped if x == NULL),
+ * then the blocked partial of dot(z, y) (z == NULL: dot(y, y)). */
+sd_status sd_k_axpy_dot(const void* x, void* y, const void* z, const double* coef, uint64_t begin, uint64_t end,
+                        uint64_t total, int prec, double* partial, sd_stream s);
+/* Classical Gram-Schmidt pass over j stored columns Q[i] = Q + i*ldq:
+ *   if coef: r = round(...round(r - coef[0] Q[0]) ... - coef[j-1] Q[j-1]) per element,
+ *   then mode 0: no dots, 1: partials of dot(Q[i], r) for all i ([i][plen]),
+ *   2: partial of dot(r, r). */
+sd_status sd_k_cgs(const void* Q, uint64_t ldq, uint64_t j, void* r, const double* coef, int mode, uint64_t begin,
+                   uint64_t end, uint64_t total, int prec, double* partials, sd_stream s);
+/* Dense symmetric apply (dense_operator, operators.cpp:26-48): row i of this
+ * shard = round(sum_j a[i*n+j] * x_full[j]), serial f64 fold; a is row-major
+ * n x n f64 on device; rows [row_begin, row_end). */
+sd_status sd_k_dense_apply(const double* a, uint64_t n, const void* x_full, void* y, uint64_t row_begin,
+                           uint64_t row_end, int prec, sd_stream s);
+
+/* ------------------------------------------------------- quadrature (host)
+ * ritz_decompose: implicit-shift QL, f64. values ascending;
+ * weights = squared first eigenvector components. resid (optional) receives
+ * max_i ||T y_i - theta_i y_i|| / ||T||. */
+sd_status sd_ritz_decompose(uint64_t k, const double* alphas, const double* betas, double* values, double* weights,
+                            double* resid);
+/* smooth_density; sigma <= 0 selects (max-min)/100. */
+sd_status sd_smooth_density(uint64_t k, const double* values, const double* weights, double sigma, uint64_t npts,
+                            double* grid, double* density, double* sigma_used);
+
+/* Dense test operators built on the host (wigner_dense / spiked_dense,
+ * operators.cpp:50-102); out is row-major n x n f64. */
+sd_status sd_wigner_dense(uint64_t n, double sigma, uint64_t seed, double* out);
+sd_status sd_spiked_dense(uint64_t n, double sigma, const double* spikes, uint64_t n_spikes, uint64_t seed,
+                          double* out);
+
+/* ------------------------------------------------------ communication
+ * One process per GPU. An sd_comm carries the rank/size and the collectives
+ * the engine needs; sd_comm_nccl_* builds one over NCCL (NVLink/NVSwitch). */
+typedef struct sd_comm_s* sd_comm;
+sd_status sd_nccl_unique_id(unsigned char out_id[128]);
+sd_status sd_comm_nccl_create(const unsigned char id[128], int nranks, int rank, sd_comm* out);
+sd_status sd_comm_destroy(sd_comm c);
+/* In-place sum all-reduce of n floats (data-sharded HVP, C1 of SURVEY §2.1). */
+sd_status sd_comm_allreduce_f32(sd_comm c, float* buf, uint64_t n, sd_stream s);
+/* All-gather of `bytes` per rank (ordered scalar partial exchange). */
+sd_status sd_comm_allgather(sd_comm c, const void* send, void* recv, uint64_t bytes, sd_stream s);
+
+/* ------------------------------------------------------------ operators
+ * OperatorHandle (operators.hpp:15-21): apply(x, y) on this rank's shard.
+ * x_full is the gathered logical vector when the operator needs it. */
+typedef sd_status (*sd_apply_fn)(void* ctx, const void* x, void* y, sd_stream s);
+typedef struct sd_operator_s* sd_operator;
+sd_status sd_operator_custom(uint64_t dim, sd_apply_fn fn, void* ctx, sd_operator* out);
+/* dense_operator (operators.cpp:26-48); `a` host row-major n x n f64, uploaded. */
+sd_status sd_operator_dense(uint64_t n, const double* a_host, sd_operator* out);
+/* Diagonal test operator y = round(d * x); d is caller-owned device memory
+ * holding this rank's shard of the diagonal (prec storage). */
+sd_status sd_operator_diag(uint64_t dim, const void* d_dev, int prec, sd_operator* out);
+sd_status sd_operator_apply(sd_operator op, const void* x, void* y, int prec, sd_stream s);
+uint64_t sd_operator_dim(sd_operator op);
+sd_status sd_operator_destroy(sd_operator op);
+
+/* -------------------------------------------------------------- Lanczos
+ * lanczos_run (Alg. 2) on device. Vectors are this
+ * rank's shard [begin,end) of `total`; scalar partials are exchanged through
+ * `comm` (NULL: single rank) and folded in rank order, so alpha/beta are
+ * bit-identical to the reference fold for any rank count. Full reorth = two
+ * classical Gram-Schmidt passes over all stored columns. */
+typedef struct {
+  uint64_t k_max;
+  double eps; /* <= 0: 1e-12 (f64) / 1e-7 (f32) */
+  int reorth; /* SD_REORTH_* */
+  int prec;
+  uint64_t probe_seed;
+  int probe_dist;
+  uint64_t selective_window; /* SD_REORTH_SELECTIVE: columns kept (most recent) */
+} sd_lanczos_config;
+
+typedef struct {
+  uint64_t n_alpha, n_beta;
+  int breakdown;         /* beta < eps: benign truncation */
+  int numerical_failure; /* non-finite alpha/beta: partial T returned */
+  double ms_apply, ms_recurrence, ms_reorth, ms_comm; /* CUDA-event phase times */
+} sd_lanczos_info;
+
+/* Layout: begins/ends hold every rank's shard (comm size entries; NULL comm =
+ * one rank), this rank = comm rank. */
+uint64_t sd_lanczos_workspace_bytes(const uint64_t* begins, const uint64_t* ends, uint64_t total,
+                                    const sd_lanczos_config* cfg, int nranks, int rank);
+/* alphas/betas: host arrays of k_max. */
+sd_status sd_lanczos_run(sd_operator op, sd_comm comm, const uint64_t* begins, const uint64_t* ends, uint64_t total,
+                         const sd_lanczos_config* cfg, void* workspace, uint64_t workspace_bytes, double* alphas,
+                         double* betas, sd_lanczos_info* info, sd_stream s);
+
+/* Step-level engine (what bench.py times): state lives in the workspace. */
+typedef struct sd_lanczos_s* sd_lanczos;
+sd_status sd_lanczos_begin(sd_operator op, sd_comm comm, const uint64_t* begins, const uint64_t* ends, uint64_t total,
+                           const sd_lanczos_config* cfg, void* workspace, uint64_t workspace_bytes, sd_stream s,
+                           sd_lanczos* out);
+/* One Lanczos step (apply + recurrence + reorth). *done = 1 once the run
+ * stopped (k_max reached, benign breakdown, or numerical failure). */
+sd_status sd_lanczos_step(sd_lanczos L, int* done);
+sd_status sd_lanczos_result(sd_lanczos L, double* alphas, double* betas, sd_lanczos_info* info);
+/* Device pointers: current Lanczos vector q_k and the stored basis
+ * (column-major, ld = shard length; *ncols columns; NULL if not stored). */
+const void* sd_lanczos_current(sd_lanczos L);
+sd_status sd_lanczos_basis(sd_lanczos L, const void** basis, uint64_t* ncols);
+sd_status sd_lanczos_end(sd_lanczos L);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPECDEN_B200_H */

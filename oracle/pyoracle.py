@@ -207,6 +207,15 @@ class Oracle:
             res["basis"] = Q[:info[4]].copy()
         return res
 
+    def lanczos_diag(self, d, k_max, eps=-1.0, reorth=False, seed=42, dist=RADEMACHER, prec=F32):
+        d = np.ascontiguousarray(d, np.float64)
+        al = np.zeros(k_max, np.float64)
+        be = np.zeros(k_max, np.float64)
+        info = np.zeros(4, np.int64)
+        self._chk(self.lib.oracle_lanczos_diag(_ll(d.size), _p(d), _ll(k_max), _d(eps), int(reorth), _ull(seed), dist,
+                                               prec, _p(al), _p(be), _pl(info)))
+        return {"alphas": al[:info[0]].copy(), "betas": be[:info[1]].copy(), "breakdown": bool(info[2])}
+
     def ritz(self, alphas, betas):
         al = np.ascontiguousarray(alphas, np.float64)
         be = np.ascontiguousarray(betas, np.float64)

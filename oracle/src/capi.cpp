@@ -219,6 +219,32 @@ int oracle_lanczos_dense(long long n, const double* a, long long k_max, double e
   })
 }
 
+// Lanczos over the diagonal operator y_i = round(d_i * x_i) (exact product, one rounding).
+int oracle_lanczos_diag(long long n, const double* d, long long k_max, double eps, int reorth, unsigned long long seed,
+                        int dist, int prec, double* out_alpha, double* out_beta, long long* info) {
+  ORACLE_TRY({
+    LanczosConfig cfg;
+    cfg.k_max = size_t(k_max);
+    cfg.eps = eps;
+    cfg.reorth = Reorth(reorth);
+    cfg.probe.seed = seed;
+    cfg.probe.dist = ProbeDist(dist);
+    cfg.prec = Precision(prec);
+    const LanczosResult r = lanczos_run(
+        size_t(n),
+        [&](const Vec& x, Vec& y) {
+          for (size_t i = 0; i < x.dim(); ++i) y.x[i] = round_elem(d[i] * x.x[i], x.prec);
+        },
+        cfg);
+    for (size_t i = 0; i < r.alphas.size(); ++i) out_alpha[i] = r.alphas[i];
+    for (size_t i = 0; i < r.betas.size(); ++i) out_beta[i] = r.betas[i];
+    info[0] = (long long)r.alphas.size();
+    info[1] = (long long)r.betas.size();
+    info[2] = r.breakdown;
+    info[3] = r.numerical_failure;
+  })
+}
+
 int oracle_ritz(long long k, const double* alphas, const double* betas, double* values, double* weights) {
   ORACLE_TRY({
     const Ritz r = ritz_decompose(std::vector<double>(alphas, alphas + k), std::vector<double>(betas, betas + (k - 1)));

@@ -1,0 +1,473 @@
+// Host side of libspecden_b200: error plumbing, layout bookkeeping, the
+// tridiagonal eigensolve + quadrature (stays on the host),
+// NCCL communicators, operator handles and the device Lanczos engine
+// (Alg. 2) that drives the kernels of sd_vector.cu.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "sd_common.cuh"
+#include "sd_engine.h"
+
+namespace sd {
+
+static thread_local std::string g_last_error;
+void set_last_error(const std::string& m) { g_last_error = m; }
+
+// ------------------------------------------------------------------ layout
+static void validate(uint64_t total, uint64_t n, const uint64_t* b, const uint64_t* e) {
+  if (total == 0) fail(SD_LAYOUT_ERROR, "layout covers zero dimensions");
+  if (n == 0) fail(SD_LAYOUT_ERROR, "layout has no shards");
+  uint64_t at = 0;
+  for (uint64_t w = 0; w < n; ++w) {
+    if (b[w] != at) fail(SD_LAYOUT_ERROR, "shard bounds leave a gap or overlap");
+    if (!(e[w] > b[w])) fail(SD_LAYOUT_ERROR, "empty shard range");
+    at = e[w];
+  }
+  if (at != total) fail(SD_LAYOUT_ERROR, "shard bounds do not cover total_dim");
+}
+
+// ------------------------------------------------------------- quadrature
+// Implicit-shift QL on the symmetric tridiagonal with accumulated rotations
+// (the textbook tql2/tqli iteration), f64. Returns eigenvalues ascending and
+// the full eigenvector matrix (column-major k x k).
+static void tridiag_ql(std::vector<double>& d, std::vector<double> e, std::vector<double>& z) {
+  const size_t k = d.size();
+  z.assign(k * k, 0.0);
+  for (size_t i = 0; i < k; ++i) z[i * k + i] = 1.0;
+  e.resize(k, 0.0);
+  for (size_t l = 0; l < k; ++l) {
+    int iter = 0;
+    size_t m;
+    do {
+      for (m = l; m + 1 < k; ++m) {
+        const double dd = std::fabs(d[m]) + std::fabs(d[m + 1]);
+        if (std::fabs(e[m]) <= std::numeric_limits<double>::epsilon() * dd) break;
+      }
+      if (m != l) {
+        if (iter++ == 200) fail(SD_NUMERICAL_ERROR, "tridiagonal QL did not converge");
+        double g = (d[l + 1] - d[l]) / (2.0 * e[l]);
+        double r = std::hypot(g, 1.0);
+        g = d[m] - d[l] + e[l] / (g + std::copysign(r, g));
+        double s = 1.0, c = 1.0, p = 0.0;
+        bool early = false;
+        for (size_t ii = m; ii-- > l;) {
+          double f = s * e[ii];
+          const double b = c * e[ii];
+          r = std::hypot(f, g);
+          e[ii + 1] = r;
+          if (r == 0.0) {
+            d[ii + 1] -= p;
+            e[m] = 0.0;
+            early = true;
+            break;
+          }
+          s = f / r;
+          c = g / r;
+          g = d[ii + 1] - p;
+          r = (d[ii] - g) * s + 2.0 * c * b;
+          p = s * r;
+          d[ii + 1] = g + p;
+          g = c * r - b;
+          for (size_t row = 0; row < k; ++row) {  // column-major: z[col*k + row]
+            f = z[(ii + 1) * k + row];
+            z[(ii + 1) * k + row] = s * z[ii * k + row] + c * f;
+            z[ii * k + row] = c * z[ii * k + row] - s * f;
+          }
+        }
+        if (early) continue;
+        d[l] -= p;
+        e[l] = g;
+        e[m] = 0.0;
+      }
+    } while (m != l);
+  }
+}
+
+void ritz(uint64_t k, const double* al, const double* be, double* vals, double* wts, double* resid) {
+  if (k == 0) fail(SD_ARGUMENT_ERROR, "ritz_decompose needs k >= 1");
+  for (uint64_t i = 0; i < k; ++i)
+    if (!std::isfinite(al[i]) || (i + 1 < k && !std::isfinite(be[i])))
+      fail(SD_NUMERICAL_ERROR, "non-finite tridiagonal entry");
+  std::vector<double> d(al, al + k), e(be, be + (k - 1)), z;
+  tridiag_ql(d, e, z);
+  std::vector<size_t> idx(k);
+  for (size_t i = 0; i < k; ++i) idx[i] = i;
+  std::sort(idx.begin(), idx.end(), [&](size_t a, size_t b) { return d[a] < d[b]; });
+  double tnorm = 0.0;
+  for (uint64_t i = 0; i < k; ++i)
+    tnorm = std::max(tnorm, std::fabs(al[i]) + (i ? std::fabs(be[i - 1]) : 0.0) + (i + 1 < k ? std::fabs(be[i]) : 0.0));
+  double worst = 0.0;
+  for (size_t o = 0; o < k; ++o) {
+    const size_t c = idx[o];
+    const double* y = &z[c * k];
+    double n2 = 0.0;
+    for (size_t r = 0; r < k; ++r) n2 += y[r] * y[r];
+    vals[o] = d[c];
+    wts[o] = y[0] * y[0] / n2;
+    double res = 0.0;
+    for (size_t r = 0; r < k; ++r) {
+      double ty = al[r] * y[r];
+      if (r > 0) ty += be[r - 1] * y[r - 1];
+      if (r + 1 < k) ty += be[r] * y[r + 1];
+      const double dlt = ty - d[c] * y[r];
+      res += dlt * dlt;
+    }
+    worst = std::max(worst, std::sqrt(res / n2));
+  }
+  if (resid) *resid = tnorm > 0 ? worst / tnorm : worst;
+}
+
+void density(uint64_t k, const double* v, const double* w, double sigma, uint64_t npts, double* grid, double* dens,
+             double* sig_used) {
+  if (k == 0) fail(SD_ARGUMENT_ERROR, "degenerate spectrum (k = 0)");
+  if (npts < 2) fail(SD_ARGUMENT_ERROR, "grid_points must be >= 2");
+  const double lo = *std::min_element(v, v + k), hi = *std::max_element(v, v + k);
+  if (!(sigma > 0)) sigma = (hi - lo) / 100.0;
+  if (!(sigma > 0)) sigma = 1.0;
+  const double a = lo - 5 * sigma, b = hi + 5 * sigma;
+  const double norm = 1.0 / (sigma * std::sqrt(2.0 * M_PI));
+  for (uint64_t g = 0; g < npts; ++g) {
+    const double x = a + (b - a) * double(g) / double(npts - 1);
+    double acc = 0.0;
+    for (uint64_t i = 0; i < k; ++i) {
+      const double t = (x - v[i]) / sigma;
+      acc += w[i] * norm * std::exp(-0.5 * t * t);
+    }
+    grid[g] = x;
+    dens[g] = acc;
+  }
+  if (sig_used) *sig_used = sigma;
+}
+
+// ------------------------------------------------------------------- NCCL
+// NCCL is resolved at run time from the process (torch has usually loaded
+// libnccl.so.2 already); the library never links a second copy.
+struct NcclApi {
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+static NcclApi& nccl() {
+  static NcclApi api = [] {
+    NcclApi a;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return a;
+    a.GetUniqueId = (decltype(a.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+    a.CommInitRank = (decltype(a.CommInitRank))dlsym(h, "ncclCommInitRank");
+    a.CommDestroy = (decltype(a.CommDestroy))dlsym(h, "ncclCommDestroy");
+    a.AllReduce = (decltype(a.AllReduce))dlsym(h, "ncclAllReduce");
+    a.AllGather = (decltype(a.AllGather))dlsym(h, "ncclAllGather");
+    a.GetErrorString = (decltype(a.GetErrorString))dlsym(h, "ncclGetErrorString");
+    return a;
+  }();
+  if (!api.CommInitRank) fail(SD_NCCL_ERROR, "libnccl.so.2 not loadable");
+  return api;
+}
+static void nccl_check(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess) fail(SD_NCCL_ERROR, std::string(what) + ": " + nccl().GetErrorString(r));
+}
+
+}  // namespace sd
+
+struct sd_comm_s {
+  int nranks = 1, rank = 0;
+  ncclComm_t comm = nullptr;
+};
+
+namespace sd {
+
+void comm_allgather(sd_comm c, const void* send, void* recv, uint64_t bytes, cudaStream_t s) {
+  if (!c || c->nranks == 1) {
+    if (recv != send) SD_CUDA(cudaMemcpyAsync(recv, send, bytes, cudaMemcpyDeviceToDevice, s));
+    return;
+  }
+  nccl_check(nccl().AllGather(send, recv, bytes, ncclUint8, c->comm, s), "ncclAllGather");
+}
+
+void comm_allreduce_f32(sd_comm c, float* buf, uint64_t n, cudaStream_t s) {
+  if (!c || c->nranks == 1) return;
+  nccl_check(nccl().AllReduce(buf, buf, n, ncclFloat32, ncclSum, c->comm, s), "ncclAllReduce");
+}
+
+int comm_rank(sd_comm c) { return c ? c->rank : 0; }
+int comm_size(sd_comm c) { return c ? c->nranks : 1; }
+
+}  // namespace sd
+
+// --------------------------------------------------------------- operators
+struct sd_operator_s {
+  uint64_t dim = 0;
+  int kind = 0;  // 0 custom, 1 dense, 2 diagonal
+  const void* diag = nullptr;  // kind 2: caller-owned device diagonal (this rank's shard)
+  int diag_prec = 0;
+  sd_apply_fn fn = nullptr;
+  void* ctx = nullptr;
+  double* a_dev = nullptr;
+  void* xfull = nullptr;  // gather scratch (dense)
+  size_t xfull_bytes = 0;
+};
+
+namespace sd {
+
+bool operator_needs_full(sd_operator op) { return op->kind == 1; }
+
+// Dense apply needs the gathered x (operators.cpp:35): single rank here, the
+// shard IS the full vector; multi-rank gathers through the engine.
+void operator_apply(sd_operator op, const void* x, void* y, int prec, cudaStream_t s, uint64_t row_begin,
+                    uint64_t row_end, const void* x_full) {
+  if (op->kind == 1) {
+    dense_apply(op->a_dev, op->dim, x_full ? x_full : x, y, row_begin, row_end, prec, s);
+  } else if (op->kind == 2) {
+    if (prec != op->diag_prec) fail(SD_LAYOUT_ERROR, "diagonal operator precision mismatch");
+    diag_apply(op->diag, x, y, row_end - row_begin, prec, s);
+  } else {
+    const sd_status st = op->fn(op->ctx, x, y, (sd_stream)s);
+    if (st != SD_OK) fail(st, "operator apply failed");
+  }
+}
+
+}  // namespace sd
+
+using namespace sd;
+
+extern "C" {
+
+const char* sd_last_error(void) { return g_last_error.c_str(); }
+int sd_abi_version(void) { return 1; }
+
+uint64_t sd_keyed_counter(uint64_t seed, uint64_t counter) { return keyed_counter_k(mix64(seed), counter); }
+double sd_rademacher(uint64_t seed, uint64_t i) { return (sd_keyed_counter(seed, i) & 1ull) ? 1.0 : -1.0; }
+uint64_t sd_uniform_index(uint64_t seed, uint64_t i, uint64_t n) { return sd_keyed_counter(seed, i) % n; }
+
+sd_status sd_split_evenly(uint64_t dim, uint64_t n, uint64_t* begins, uint64_t* ends, uint64_t* count) {
+  return guard([&] {
+    if (dim == 0 || n == 0) fail(SD_LAYOUT_ERROR, "split_evenly needs dim > 0 and n > 0");
+    const uint64_t w = std::min(dim, n), q = dim / w, rem = dim % w;
+    uint64_t at = 0;
+    for (uint64_t i = 0; i < w; ++i) {
+      begins[i] = at;
+      at += q + (i < rem ? 1 : 0);
+      ends[i] = at;
+    }
+    *count = w;
+    validate(dim, w, begins, ends);
+  });
+}
+
+sd_status sd_validate_layout(uint64_t total, uint64_t n, const uint64_t* begins, const uint64_t* ends) {
+  return guard([&] { validate(total, n, begins, ends); });
+}
+
+sd_status sd_layout_owner(uint64_t n, const uint64_t* ends, uint64_t i, uint64_t* owner) {
+  return guard([&] {
+    for (uint64_t w = 0; w < n; ++w)
+      if (ends[w] > i) {
+        *owner = w;
+        return;
+      }
+    fail(SD_ARGUMENT_ERROR, "index out of range in ShardLayout::owner");
+  });
+}
+
+sd_status sd_partial_shape(uint64_t begin, uint64_t end, uint64_t total, uint64_t* h, uint64_t* s, uint64_t* t) {
+  return guard([&] {
+    if (!(end > begin) || end > total) fail(SD_LAYOUT_ERROR, "bad shard range");
+    const PartialShape p = partial_shape(begin, end, total);
+    *h = p.n_head;
+    *s = p.n_sums;
+    *t = p.n_tail;
+  });
+}
+
+uint64_t sd_partial_len(uint64_t begin, uint64_t end, uint64_t total) {
+  return partial_shape(begin, end, total).len();
+}
+
+sd_status sd_combine_partials_host(uint64_t nranks, const uint64_t* begins, const uint64_t* ends, uint64_t total,
+                                   const double* const* parts, double* out) {
+  return guard([&] {
+    double closed = 0.0, open = 0.0;
+    uint64_t at = 0;
+    auto grid_end = [&](uint64_t i) { return std::min(total, (i / kBlock + 1) * kBlock); };
+    auto feed = [&](double t) {
+      open += t;
+      ++at;
+      if (at == grid_end(at - 1)) {
+        closed += open;
+        open = 0.0;
+      }
+    };
+    for (uint64_t r = 0; r < nranks; ++r) {
+      if (begins[r] != at) fail(SD_PROTOCOL_ERROR, "blocked partials are not contiguous in worker order");
+      const PartialShape p = partial_shape(begins[r], ends[r], total);
+      const double* x = parts[r];
+      for (uint64_t i = 0; i < p.n_head; ++i) feed(x[i]);
+      for (uint64_t i = 0; i < p.n_sums; ++i) {
+        if (at % kBlock != 0) fail(SD_PROTOCOL_ERROR, "blocked partial misaligned with the reduction grid");
+        closed += x[p.n_head + i];
+        at = grid_end(at);
+      }
+      for (uint64_t i = 0; i < p.n_tail; ++i) feed(x[p.n_head + p.n_sums + i]);
+      if (at != ends[r]) fail(SD_PROTOCOL_ERROR, "blocked partial does not cover its range");
+    }
+    if (at != total) fail(SD_PROTOCOL_ERROR, "blocked partials do not cover the vector");
+    *out = closed;
+  });
+}
+
+sd_status sd_ritz_decompose(uint64_t k, const double* alphas, const double* betas, double* values, double* weights,
+                            double* resid) {
+  return guard([&] { ritz(k, alphas, betas, values, weights, resid); });
+}
+
+sd_status sd_smooth_density(uint64_t k, const double* values, const double* weights, double sigma, uint64_t npts,
+                            double* grid, double* dens, double* sigma_used) {
+  return guard([&] { density(k, values, weights, sigma, npts, grid, dens, sigma_used); });
+}
+
+// wigner_dense / spiked_dense (operators.cpp:50-102): host construction of the
+// dense test operators (setup, not the hot path), keyed counter Gaussians.
+static double host_gaussian(uint64_t seed, uint64_t i) {
+  const uint64_t key = mix64(seed);
+  const double a = double(keyed_counter_k(key, 2 * i) >> 11) * 0x1p-53 + 0x1p-54;
+  const double b = double(keyed_counter_k(key, 2 * i + 1) >> 11) * 0x1p-53 + 0x1p-54;
+  return std::sqrt(-2.0 * std::log(a)) * std::cos(6.283185307179586 * b);
+}
+
+sd_status sd_wigner_dense(uint64_t n, double sigma, uint64_t seed, double* out) {
+  return guard([&] {
+    if (n < 2) fail(SD_ARGUMENT_ERROR, "dense operators need n >= 2");
+    if (n > 2048) fail(SD_ARGUMENT_ERROR, "dense operator size exceeds the desk-scale cap (2048)");
+    if (!(sigma > 0.0)) fail(SD_ARGUMENT_ERROR, "wigner sigma must be positive");
+    for (uint64_t i = 0; i < n; ++i)
+      for (uint64_t j = i; j < n; ++j) out[i * n + j] = out[j * n + i] = sigma * host_gaussian(seed, i * n + j);
+  });
+}
+
+sd_status sd_spiked_dense(uint64_t n, double sigma, const double* spikes, uint64_t ns, uint64_t seed, double* out) {
+  return guard([&] {
+    if (!(n > ns)) fail(SD_ARGUMENT_ERROR, "spiked operator needs n > number of spikes");
+    const sd_status st = sd_wigner_dense(n, sigma, seed, out);
+    if (st != SD_OK) fail(st, g_last_error);
+    const uint64_t dseed = mix64(seed ^ 0x5eedd1ce5ull);
+    std::vector<std::vector<double>> dirs;
+    for (uint64_t sp = 0; sp < ns; ++sp) {
+      std::vector<double> u(n);
+      for (uint64_t i = 0; i < n; ++i) u[i] = host_gaussian(dseed, sp * n + i);
+      for (const auto& w : dirs) {
+        double c = 0.0;
+        for (uint64_t i = 0; i < n; ++i) c += w[i] * u[i];
+        for (uint64_t i = 0; i < n; ++i) u[i] -= c * w[i];
+      }
+      double nn = 0.0;
+      for (uint64_t i = 0; i < n; ++i) nn += u[i] * u[i];
+      nn = std::sqrt(nn);
+      if (!(nn > 0.0)) fail(SD_NUMERICAL_ERROR, "degenerate spike direction");
+      for (uint64_t i = 0; i < n; ++i) u[i] /= nn;
+      for (uint64_t i = 0; i < n; ++i)
+        for (uint64_t j = 0; j < n; ++j) out[i * n + j] += spikes[sp] * (u[i] * u[j]);
+      dirs.push_back(std::move(u));
+    }
+  });
+}
+
+sd_status sd_nccl_unique_id(unsigned char out_id[128]) {
+  return guard([&] {
+    ncclUniqueId id;
+    nccl_check(nccl().GetUniqueId(&id), "ncclGetUniqueId");
+    std::memcpy(out_id, &id, sizeof(id) < 128 ? sizeof(id) : 128);
+  });
+}
+
+sd_status sd_comm_nccl_create(const unsigned char id[128], int nranks, int rank, sd_comm* out) {
+  return guard([&] {
+    auto c = std::make_unique<sd_comm_s>();
+    c->nranks = nranks;
+    c->rank = rank;
+    if (nranks > 1) {
+      ncclUniqueId uid;
+      std::memcpy(&uid, id, sizeof(uid));
+      nccl_check(nccl().CommInitRank(&c->comm, nranks, uid, rank), "ncclCommInitRank");
+    }
+    *out = c.release();
+  });
+}
+
+sd_status sd_comm_destroy(sd_comm c) {
+  return guard([&] {
+    if (c && c->comm) nccl_check(nccl().CommDestroy(c->comm), "ncclCommDestroy");
+    delete c;
+  });
+}
+
+sd_status sd_comm_allreduce_f32(sd_comm c, float* buf, uint64_t n, sd_stream s) {
+  return guard([&] { comm_allreduce_f32(c, buf, n, (cudaStream_t)s); });
+}
+
+sd_status sd_comm_allgather(sd_comm c, const void* send, void* recv, uint64_t bytes, sd_stream s) {
+  return guard([&] { comm_allgather(c, send, recv, bytes, (cudaStream_t)s); });
+}
+
+sd_status sd_operator_custom(uint64_t dim, sd_apply_fn fn, void* ctx, sd_operator* out) {
+  return guard([&] {
+    if (!fn) fail(SD_ARGUMENT_ERROR, "operator apply function is null");
+    auto op = std::make_unique<sd_operator_s>();
+    op->dim = dim;
+    op->fn = fn;
+    op->ctx = ctx;
+    *out = op.release();
+  });
+}
+
+sd_status sd_operator_dense(uint64_t n, const double* a_host, sd_operator* out) {
+  return guard([&] {
+    if (n < 2) fail(SD_ARGUMENT_ERROR, "dense operators need n >= 2");
+    if (n > 2048) fail(SD_ARGUMENT_ERROR, "dense operator size exceeds the desk-scale cap (2048)");
+    auto op = std::make_unique<sd_operator_s>();
+    op->dim = n;
+    op->kind = 1;
+    SD_CUDA(cudaMalloc(&op->a_dev, n * n * sizeof(double)));
+    SD_CUDA(cudaMemcpy(op->a_dev, a_host, n * n * sizeof(double), cudaMemcpyHostToDevice));
+    *out = op.release();
+  });
+}
+
+sd_status sd_operator_diag(uint64_t dim, const void* d_dev, int prec, sd_operator* out) {
+  return guard([&] {
+    auto op = std::make_unique<sd_operator_s>();
+    op->dim = dim;
+    op->kind = 2;
+    op->diag = d_dev;
+    op->diag_prec = prec;
+    *out = op.release();
+  });
+}
+
+sd_status sd_operator_apply(sd_operator op, const void* x, void* y, int prec, sd_stream s) {
+  return guard([&] { operator_apply(op, x, y, prec, (cudaStream_t)s, 0, op->dim, nullptr); });
+}
+
+uint64_t sd_operator_dim(sd_operator op) { return op ? op->dim : 0; }
+
+sd_status sd_operator_destroy(sd_operator op) {
+  return guard([&] {
+    if (!op) return;
+    if (op->a_dev) cudaFree(op->a_dev);
+    delete op;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,326 @@
+// Device Lanczos engine: lanczos_run of SPEC.md:257-265 / PAPER.md Alg. 2 with
+// full reorthogonalisation as two classical Gram-Schmidt passes over every
+// stored column. Each step is:
+//   r = op(q_k)                                        (HVP / dense apply)
+//   pass A: r -= beta_{k-1} q_{k-1};  partial <q_k, r>   -> alpha_k
+//   pass B: r -= alpha_k q_k           [no reorth: partial <r, r> -> beta_k]
+//   CGS 1 : partials <Q_i, r>                           -> c   (j columns)
+//   CGS 2 : r -= sum_i c_i Q_i (sequential); <Q_i, r>    -> c'
+//   CGS 3 : r -= sum_i c'_i Q_i;            <r, r>       -> beta_k
+//   q_{k+1} = (1/beta_k) r
+// Scalars never leave the device inside a step; partials are exchanged with
+// one all-gather per scalar set and folded in rank order (bitwise equal to
+// the reference's coordinator fold for any rank count). alpha/beta reach the
+// host once per step for the breakdown test (beta < eps).
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "sd_common.cuh"
+#include "sd_engine.h"
+
+namespace {
+
+constexpr uint64_t kAlign = 256;
+uint64_t align_up(uint64_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+
+struct Plan {
+  uint64_t P = 0, esize = 0, ncols_alloc = 0, pstride = 0, m_max = 0, maxlen = 0;
+  uint64_t off_Q = 0, off_r = 0, off_xfull = 0, off_send = 0, off_recv = 0, off_scal = 0, total_bytes = 0;
+};
+
+Plan make_plan(const uint64_t* begins, const uint64_t* ends, uint64_t total, const sd_lanczos_config* cfg, int nranks,
+               int rank) {
+  Plan p;
+  if (!cfg) sd::fail(SD_CONFIG_ERROR, "null lanczos config");
+  if (cfg->k_max < 1) sd::fail(SD_CONFIG_ERROR, "k_max must be >= 1");
+  if (cfg->prec != SD_F32 && cfg->prec != SD_F64) sd::fail(SD_CONFIG_ERROR, "precision must be f32 or f64");
+  if (cfg->reorth != SD_REORTH_NONE && cfg->reorth != SD_REORTH_FULL)
+    sd::fail(SD_CONFIG_ERROR, "reorth must be none or full in this build");
+  if (nranks < 1 || rank < 0 || rank >= nranks) sd::fail(SD_ARGUMENT_ERROR, "bad rank/size");
+  uint64_t at = 0;
+  for (int r = 0; r < nranks; ++r) {
+    if (begins[r] != at || !(ends[r] > begins[r])) sd::fail(SD_LAYOUT_ERROR, "shard bounds leave a gap or overlap");
+    at = ends[r];
+    p.pstride = std::max<uint64_t>(p.pstride, sd::partial_shape(begins[r], ends[r], total).len());
+    p.maxlen = std::max<uint64_t>(p.maxlen, ends[r] - begins[r]);
+  }
+  if (at != total) sd::fail(SD_LAYOUT_ERROR, "shard bounds do not cover total_dim");
+  p.P = ends[rank] - begins[rank];
+  p.esize = cfg->prec == SD_F32 ? 4 : 8;
+  const bool keep = cfg->reorth == SD_REORTH_FULL;
+  p.ncols_alloc = keep ? cfg->k_max + 1 : 2;
+  p.m_max = keep ? cfg->k_max + 1 : 1;
+  uint64_t o = 0;
+  p.off_Q = o;
+  o = align_up(o + p.ncols_alloc * p.P * p.esize);
+  p.off_r = o;
+  o = align_up(o + p.P * p.esize);
+  p.off_xfull = o;
+  o = align_up(o + (nranks > 1 ? (uint64_t(nranks) * p.maxlen + total) * p.esize : 0));
+  p.off_send = o;
+  o = align_up(o + p.m_max * p.pstride * 8);
+  p.off_recv = o;
+  o = align_up(o + (nranks > 1 ? uint64_t(nranks) * p.m_max * p.pstride * 8 : 0));
+  p.off_scal = o;
+  o = align_up(o + (4 + 2 * cfg->k_max + 2 * p.m_max) * 8);
+  p.total_bytes = o;
+  return p;
+}
+
+}  // namespace
+
+struct sd_lanczos_s {
+  sd_operator op = nullptr;
+  sd_comm comm = nullptr;
+  int nranks = 1, rank = 0;
+  std::vector<uint64_t> rb, re;
+  uint64_t total = 0;
+  sd_lanczos_config cfg{};
+  Plan plan;
+  char* ws = nullptr;
+  cudaStream_t s = nullptr;
+  double eps = 0;
+  uint64_t k = 0, ncols = 0;
+  bool done = false, breakdown = false, failure = false;
+  std::vector<double> alphas, betas;
+  double* h_scal = nullptr;  // pinned: [alpha, beta]
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  double ms_apply = 0, ms_rec = 0, ms_reorth = 0;
+
+  void* col(uint64_t i) const {
+    const uint64_t slot = cfg.reorth == SD_REORTH_FULL ? i : (i & 1);
+    return ws + plan.off_Q + slot * plan.P * plan.esize;
+  }
+  void* r() const { return ws + plan.off_r; }
+  double* send() const { return reinterpret_cast<double*>(ws + plan.off_send); }
+  double* recv() const { return reinterpret_cast<double*>(ws + plan.off_recv); }
+  double* scal() const { return reinterpret_cast<double*>(ws + plan.off_scal); }
+  double* d_alpha() const { return scal() + 4; }                    // [k_max]
+  double* d_beta() const { return scal() + 4 + cfg.k_max; }         // [k_max]
+  double* d_c1() const { return scal() + 4 + 2 * cfg.k_max; }       // [m_max]
+  double* d_c2() const { return d_c1() + plan.m_max; }              // [m_max]
+  double* d_norm() const { return scal(); }
+  uint64_t begin() const { return rb[rank]; }
+  uint64_t end() const { return re[rank]; }
+
+  // all-gather the m partial sequences and fold them in rank order
+  void reduce(uint64_t m, double* out, int post_sqrt) {
+    const double* parts = send();
+    if (nranks > 1) {
+      sd::comm_allgather(comm, send(), recv(), m * plan.pstride * 8, s);
+      parts = recv();
+    }
+    sd::combine_device(uint64_t(nranks), rb.data(), re.data(), total, m, plan.pstride, parts, out, s, post_sqrt);
+  }
+
+  void apply(const void* x, void* y) {
+    if (sd::operator_needs_full(op)) {
+      const void* xf = x;
+      if (nranks > 1) {
+        // gather (operators.cpp:35): fixed-size all-gather of padded shards, then compact
+        const uint64_t maxlen = plan.maxlen;
+        char* gat = ws + plan.off_xfull;
+        char* full = gat + uint64_t(nranks) * maxlen * plan.esize;
+        char* sendbuf = gat + uint64_t(rank) * maxlen * plan.esize;
+        SD_CUDA(cudaMemcpyAsync(sendbuf, x, plan.P * plan.esize, cudaMemcpyDeviceToDevice, s));
+        sd::comm_allgather(comm, sendbuf, gat, maxlen * plan.esize, s);
+        for (int q = 0; q < nranks; ++q)
+          SD_CUDA(cudaMemcpyAsync(full + rb[q] * plan.esize, gat + uint64_t(q) * maxlen * plan.esize,
+                                  (re[q] - rb[q]) * plan.esize, cudaMemcpyDeviceToDevice, s));
+        xf = full;
+      }
+      sd::operator_apply(op, x, y, cfg.prec, s, begin(), end(), xf);
+    } else {
+      sd::operator_apply(op, x, y, cfg.prec, s, begin(), end(), nullptr);
+    }
+  }
+
+  void start() {
+    const uint64_t B = begin(), E = end();
+    void* q0 = col(0);
+    sd::probe_fill(q0, B, E, cfg.probe_seed, cfg.probe_dist, 0, cfg.prec, s);
+    // normalise: n = norm2(q0); !(n > 0) -> numerical_error; q0 = scale(q0, 1/n) (sharded.cpp:77-81)
+    sd::axpy_dot(nullptr, q0, nullptr, nullptr, B, E, total, cfg.prec, send(), s);
+    reduce(1, d_norm(), 1);
+    SD_CUDA(cudaMemcpyAsync(h_scal, d_norm(), 8, cudaMemcpyDeviceToHost, s));
+    SD_CUDA(cudaStreamSynchronize(s));
+    if (!(h_scal[0] > 0.0)) sd::fail(SD_NUMERICAL_ERROR, "probe has zero norm");
+    sd::scale(q0, q0, plan.P, d_norm(), 1, cfg.prec, s);
+    ncols = 1;
+  }
+
+  void step() {
+    if (done) return;
+    const uint64_t B = begin(), E = end();
+    void* q = col(k);
+    void* qp = k > 0 ? col(k - 1) : nullptr;
+    SD_CUDA(cudaEventRecord(ev[0], s));
+    apply(q, r());
+    SD_CUDA(cudaEventRecord(ev[1], s));
+    // pass A: r = axpy(-beta_{k-1}, q_{k-1}, r); alpha = dot(q_k, r)
+    sd::axpy_dot(qp, r(), q, k > 0 ? d_beta() + (k - 1) : nullptr, B, E, total, cfg.prec, send(), s);
+    reduce(1, d_alpha() + k, 0);
+    if (cfg.reorth == SD_REORTH_NONE) {
+      // pass B: r = axpy(-alpha, q_k, r); beta = norm2(r)
+      sd::axpy_dot(q, r(), nullptr, d_alpha() + k, B, E, total, cfg.prec, send(), s);
+      reduce(1, d_beta() + k, 1);
+      SD_CUDA(cudaEventRecord(ev[2], s));
+    } else {
+      sd::axpy_dot(q, r(), nullptr, d_alpha() + k, B, E, total, cfg.prec, nullptr, s);
+      SD_CUDA(cudaEventRecord(ev[2], s));
+      const uint64_t j = ncols;
+      sd::cgs(col(0), plan.P, j, r(), nullptr, 1, B, E, total, cfg.prec, send(), plan.pstride, s);
+      reduce(j, d_c1(), 0);
+      sd::cgs(col(0), plan.P, j, r(), d_c1(), 1, B, E, total, cfg.prec, send(), plan.pstride, s);
+      reduce(j, d_c2(), 0);
+      sd::cgs(col(0), plan.P, j, r(), d_c2(), 2, B, E, total, cfg.prec, send(), plan.pstride, s);
+      reduce(1, d_beta() + k, 1);
+    }
+    SD_CUDA(cudaEventRecord(ev[3], s));
+    SD_CUDA(cudaMemcpyAsync(h_scal, d_alpha() + k, 8, cudaMemcpyDeviceToHost, s));
+    SD_CUDA(cudaMemcpyAsync(h_scal + 1, d_beta() + k, 8, cudaMemcpyDeviceToHost, s));
+    SD_CUDA(cudaStreamSynchronize(s));
+    float t01 = 0, t12 = 0, t23 = 0;
+    cudaEventElapsedTime(&t01, ev[0], ev[1]);
+    cudaEventElapsedTime(&t12, ev[1], ev[2]);
+    cudaEventElapsedTime(&t23, ev[2], ev[3]);
+    ms_apply += t01;
+    ms_rec += t12;
+    ms_reorth += t23;
+    const double alpha = h_scal[0], beta = h_scal[1];
+    if (!std::isfinite(alpha)) {
+      failure = done = true;
+      return;
+    }
+    alphas.push_back(alpha);
+    if (!std::isfinite(beta)) {
+      failure = done = true;
+      return;
+    }
+    if (beta < eps) {
+      breakdown = done = true;
+      return;
+    }
+    if (k + 1 == cfg.k_max) {
+      done = true;
+      return;
+    }
+    betas.push_back(beta);
+    // q_{k+1} = scale(r, 1/beta)
+    sd::scale(r(), col(k + 1), plan.P, d_beta() + k, 1, cfg.prec, s);
+    ++k;
+    if (cfg.reorth == SD_REORTH_FULL) ++ncols;
+  }
+
+  ~sd_lanczos_s() {
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+    if (h_scal) cudaFreeHost(h_scal);
+  }
+};
+
+namespace sd {
+bool operator_needs_full(sd_operator op);
+}
+
+extern "C" {
+
+uint64_t sd_lanczos_workspace_bytes(const uint64_t* begins, const uint64_t* ends, uint64_t total,
+                                    const sd_lanczos_config* cfg, int nranks, int rank) {
+  try {
+    return make_plan(begins, ends, total, cfg, nranks, rank).total_bytes;
+  } catch (const std::exception& e) {
+    sd::set_last_error(e.what());
+    return 0;
+  }
+}
+
+sd_status sd_lanczos_begin(sd_operator op, sd_comm comm, const uint64_t* begins, const uint64_t* ends, uint64_t total,
+                           const sd_lanczos_config* cfg, void* workspace, uint64_t workspace_bytes, sd_stream s,
+                           sd_lanczos* out) {
+  return sd::guard([&] {
+    if (!op) sd::fail(SD_ARGUMENT_ERROR, "null operator");
+    const int nr = sd::comm_size(comm), rk = sd::comm_rank(comm);
+    auto L = std::make_unique<sd_lanczos_s>();
+    L->plan = make_plan(begins, ends, total, cfg, nr, rk);
+    if (sd_operator_dim(op) != total) sd::fail(SD_LAYOUT_ERROR, "operator/vector dimension mismatch");
+    if (total < 2) sd::fail(SD_ARGUMENT_ERROR, "operator dimension must be >= 2");
+    if (workspace_bytes < L->plan.total_bytes) sd::fail(SD_ARGUMENT_ERROR, "lanczos workspace too small");
+    L->op = op;
+    L->comm = comm;
+    L->nranks = nr;
+    L->rank = rk;
+    L->rb.assign(begins, begins + nr);
+    L->re.assign(ends, ends + nr);
+    L->total = total;
+    L->cfg = *cfg;
+    L->ws = static_cast<char*>(workspace);
+    L->s = (cudaStream_t)s;
+    L->eps = cfg->eps > 0 ? cfg->eps : (cfg->prec == SD_F64 ? 1e-12 : 1e-7);
+    SD_CUDA(cudaMallocHost(&L->h_scal, 2 * sizeof(double)));
+    for (auto& e : L->ev) SD_CUDA(cudaEventCreate(&e));
+    L->start();
+    *out = L.release();
+  });
+}
+
+sd_status sd_lanczos_step(sd_lanczos L, int* done) {
+  return sd::guard([&] {
+    L->step();
+    if (done) *done = L->done ? 1 : 0;
+  });
+}
+
+sd_status sd_lanczos_result(sd_lanczos L, double* alphas, double* betas, sd_lanczos_info* info) {
+  return sd::guard([&] {
+    for (size_t i = 0; i < L->alphas.size(); ++i) alphas[i] = L->alphas[i];
+    for (size_t i = 0; i < L->betas.size(); ++i) betas[i] = L->betas[i];
+    if (info) {
+      info->n_alpha = L->alphas.size();
+      info->n_beta = L->betas.size();
+      info->breakdown = L->breakdown;
+      info->numerical_failure = L->failure;
+      info->ms_apply = L->ms_apply;
+      info->ms_recurrence = L->ms_rec;
+      info->ms_reorth = L->ms_reorth;
+      info->ms_comm = 0;
+    }
+  });
+}
+
+const void* sd_lanczos_current(sd_lanczos L) { return L ? L->col(L->k) : nullptr; }
+
+sd_status sd_lanczos_basis(sd_lanczos L, const void** basis, uint64_t* ncols) {
+  return sd::guard([&] {
+    if (L->cfg.reorth != SD_REORTH_FULL) sd::fail(SD_STATE_ERROR, "basis was not stored (reorth = none)");
+    *basis = L->col(0);
+    *ncols = L->ncols;
+  });
+}
+
+sd_status sd_lanczos_end(sd_lanczos L) {
+  return sd::guard([&] { delete L; });
+}
+
+sd_status sd_lanczos_run(sd_operator op, sd_comm comm, const uint64_t* begins, const uint64_t* ends, uint64_t total,
+                         const sd_lanczos_config* cfg, void* workspace, uint64_t workspace_bytes, double* alphas,
+                         double* betas, sd_lanczos_info* info, sd_stream s) {
+  sd_lanczos L = nullptr;
+  sd_status st = sd_lanczos_begin(op, comm, begins, ends, total, cfg, workspace, workspace_bytes, s, &L);
+  if (st != SD_OK) return st;
+  int done = 0;
+  while (!done && st == SD_OK) st = sd_lanczos_step(L, &done);
+  if (st == SD_OK) st = sd_lanczos_result(L, alphas, betas, info);
+  if (st == SD_OK && L->failure) {
+    sd::set_last_error("non-finite alpha or beta (partial tridiagonal returned)");
+    st = SD_NUMERICAL_ERROR;
+  }
+  delete L;
+  return st;
+}
+
+}  // extern "C"

@@ -1,0 +1,525 @@
+// Lanczos vector algebra on sm_100a: probe generation, ordered blocked dot
+// partials, fused recurrence passes, classical Gram-Schmidt passes and the
+// dense test operator. All floating-point work that the reference performs in
+// f64 is done here in f64 with explicit _rn intrinsics (no FMA contraction),
+// so every rounded element and every folded scalar is bit-identical to
+// proj/src/sharded.cpp + proj/include/specden/reduction.hpp.
+//
+// Memory layout: a vector shard is one contiguous array (float or double);
+// a Krylov basis is column-major, column i at Q + i*ldq. Reductions follow the
+// reference's fixed 1024-element global grid: one thread folds one grid block
+// serially (left fold from +0.0) after the block is staged through shared
+// memory in 32-element chunks with coalesced 128 B loads.
+#include <cuda_runtime.h>
+#include <math.h>
+
+#include <vector>
+
+#include "sd_common.cuh"
+
+namespace sd {
+
+constexpr int kChunk = 32;    // elements per staged chunk of a grid block
+constexpr int kThreads = 128;
+
+// ------------------------------------------------------------------ probes
+// draw_probe fill, proj/src/sharded.cpp:67-75 (normalisation composes later).
+template <typename T>
+__global__ void k_probe(T* x, uint64_t begin, uint64_t n, uint64_t key, int dist, uint64_t one_hot) {
+  const uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (t >= n) return;
+  const uint64_t i = begin + t;
+  double v;
+  if (dist == SD_RADEMACHER) {
+    v = (keyed_counter_k(key, i) & 1ull) ? 1.0 : -1.0;
+  } else if (dist == SD_ONE_HOT) {
+    v = (i == one_hot) ? 1.0 : 0.0;
+  } else {
+    // Box-Muller on counters (2i, 2i+1), rng.hpp:37-41. CUDA's log/cos are not
+    // glibc's: Gaussian draws agree to <= 1-2 ulp, not bitwise.
+    const double u1 = __dadd_rn(__dmul_rn(double(keyed_counter_k(key, 2 * i) >> 11), 0x1p-53), 0x1p-54);
+    const double u2 = __dadd_rn(__dmul_rn(double(keyed_counter_k(key, 2 * i + 1) >> 11), 0x1p-53), 0x1p-54);
+    const double two_pi = 6.283185307179586;  // 2.0 * std::numbers::pi (exact doubling)
+    v = __dmul_rn(__dsqrt_rn(__dmul_rn(-2.0, log(u1))), cos(__dmul_rn(two_pi, u2)));
+  }
+  x[t] = round_to<T>(v);
+}
+
+// ------------------------------------------------- recurrence pass (fused)
+// y = round(y + alpha*x) with alpha = -(*coef) (axpy, sharded.cpp:106-118),
+// then the block folds of sum z[i]*y[i] (DOT=1) or y[i]*y[i] (DOT=2) over
+// full grid blocks. One CTA = kUnits consecutive grid blocks; thread t folds
+// block t. Elements are staged as [unit][33] tiles (conflict-free column walk).
+template <typename T>
+struct UnitsPerCta {
+  static constexpr int value = sizeof(T) == 4 ? 128 : 64;  // 33 KB of staging either way
+};
+
+template <typename T, bool UPD, int DOT>
+__global__ void __launch_bounds__(128) k_axpy_dot_units(const T* __restrict__ x, T* __restrict__ y,
+                                                             const T* __restrict__ z, const double* coefp,
+                                                             uint64_t base, uint64_t n_units, uint64_t local_end,
+                                                             double* __restrict__ sums) {
+  constexpr int NU = UnitsPerCta<T>::value;  // == blockDim.x
+  __shared__ T ty[NU][kChunk + 1];
+  __shared__ T tz[DOT == 1 ? NU : 1][kChunk + 1];
+  const int tid = threadIdx.x;
+  const uint64_t unit0 = uint64_t(blockIdx.x) * NU;
+  const double alpha = UPD ? -(*coefp) : 0.0;
+  double acc = 0.0;
+  for (int c = 0; c < int(kBlock) / kChunk; ++c) {
+#pragma unroll 8
+    for (int p = 0; p < kChunk; ++p) {
+      const int e = p * NU + tid;
+      const int u = e >> 5, off = e & 31;
+      const uint64_t unit = unit0 + u;
+      const uint64_t li = base + unit * kBlock + uint64_t(c * kChunk + off);
+      T yv = T(0), zv = T(0);
+      if (unit < n_units && li < local_end) {
+        yv = y[li];
+        if (UPD) {
+          const double t = __dmul_rn(alpha, double(x[li]));
+          yv = round_to<T>(__dadd_rn(double(yv), t));
+          y[li] = yv;
+        }
+        if (DOT == 1) zv = z[li];
+      }
+      ty[u][off] = yv;
+      if (DOT == 1) tz[u][off] = zv;
+    }
+    __syncthreads();
+    if (DOT != 0) {
+#pragma unroll
+      for (int k = 0; k < kChunk; ++k) {
+        const double a = double(ty[tid][k]);
+        const double b = DOT == 1 ? double(tz[tid][k]) : a;
+        acc = __dadd_rn(acc, __dmul_rn(a, b));
+      }
+    }
+    __syncthreads();
+  }
+  if (DOT != 0 && unit0 + tid < n_units) sums[unit0 + tid] = acc;
+}
+
+// Head/tail elements of a shard (straddled grid blocks): update and emit raw
+// terms (reduction.hpp:60-69 "head"/"tail").
+template <typename T, bool UPD, int DOT>
+__global__ void k_axpy_dot_edges(const T* __restrict__ x, T* __restrict__ y, const T* __restrict__ z,
+                                 const double* coefp, uint64_t n_head, uint64_t tail_begin, uint64_t n_tail,
+                                 uint64_t tail_slot, double* __restrict__ partial) {
+  const uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (t >= n_head + n_tail) return;
+  const uint64_t li = t < n_head ? t : tail_begin + (t - n_head);
+  const uint64_t slot = t < n_head ? t : tail_slot + (t - n_head);
+  T yv = y[li];
+  if (UPD) {
+    yv = round_to<T>(__dadd_rn(double(yv), __dmul_rn(-(*coefp), double(x[li]))));
+    y[li] = yv;
+  }
+  if (DOT == 1) partial[slot] = __dmul_rn(double(z[li]), double(yv));
+  if (DOT == 2) partial[slot] = __dmul_rn(double(yv), double(yv));
+}
+
+// ------------------------------------------------------ Gram-Schmidt pass
+// One CTA per full grid block. Per 32-element chunk the j basis columns are
+// staged as a [j][33] tile; warp 0 applies the j sequential axpys of the
+// reference's CGS (r = axpy(-c_i, q_i, r), i ascending) to its 32 elements,
+// then every thread folds whole columns (MODE 1: Q_i . r) or thread 0 folds
+// r . r (MODE 2). Column accumulators: thread t owns columns t, t+128, ...
+constexpr int kMaxColsPerThread = 8;  // j <= 1024 per launch
+template <typename T, bool UPD, int MODE>
+__global__ void __launch_bounds__(kThreads) k_cgs_units(const T* __restrict__ Q, uint64_t ldq, int j,
+                                                        T* __restrict__ r, const double* __restrict__ coef,
+                                                        uint64_t base, uint64_t local_end, uint64_t plen,
+                                                        uint64_t head_n, double* __restrict__ partials) {
+  // plen here is the sequence stride of `partials` (>= this rank's partial length)
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* tq = reinterpret_cast<T*>(smem_raw);                    // [j][33]
+  T* tr = tq + size_t(j) * (kChunk + 1);                      // [32]
+  double* cs = reinterpret_cast<double*>(
+      smem_raw + (((size_t(j) * (kChunk + 1) + kChunk + 2) * sizeof(T) + 7) & ~size_t(7)));  // [j]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint64_t unit = blockIdx.x;
+  const uint64_t e0 = base + unit * kBlock;
+  const uint64_t n_el = (local_end - e0) < kBlock ? (local_end - e0) : kBlock;
+  if (UPD)
+    for (int i = tid; i < j; i += kThreads) cs[i] = -coef[i];
+  double acc[kMaxColsPerThread];
+#pragma unroll
+  for (int q = 0; q < kMaxColsPerThread; ++q) acc[q] = 0.0;
+  double self = 0.0;
+  for (int c = 0; c < int(kBlock) / kChunk; ++c) {
+    const uint64_t off0 = uint64_t(c) * kChunk;
+    if (off0 >= n_el) break;
+    const bool valid = off0 + lane < n_el;
+    const uint64_t li = e0 + off0 + lane;
+    for (int i = warp; i < j; i += kThreads / 32) tq[i * (kChunk + 1) + lane] = valid ? Q[uint64_t(i) * ldq + li] : T(0);
+    T rv = T(0);
+    if (warp == 0) rv = valid ? r[li] : T(0);
+    __syncthreads();
+    if (warp == 0) {
+      if (UPD && valid) {
+        double v = double(rv);
+        for (int i = 0; i < j; ++i) v = double(round_to<T>(__dadd_rn(v, __dmul_rn(cs[i], double(tq[i * (kChunk + 1) + lane])))));
+        rv = T(v);
+        r[li] = rv;
+      }
+      tr[lane] = rv;
+    }
+    __syncthreads();
+    if (MODE == 1) {
+#pragma unroll
+      for (int q = 0; q < kMaxColsPerThread; ++q) {
+        const int col = tid + q * kThreads;
+        if (col < j) {
+          double a = acc[q];
+          const T* row = tq + col * (kChunk + 1);
+#pragma unroll 8
+          for (int k = 0; k < kChunk; ++k) a = __dadd_rn(a, __dmul_rn(double(row[k]), double(tr[k])));
+          acc[q] = a;
+        }
+      }
+    } else if (MODE == 2 && tid == 0) {
+      for (int k = 0; k < kChunk; ++k) self = __dadd_rn(self, __dmul_rn(double(tr[k]), double(tr[k])));
+    }
+    __syncthreads();
+  }
+  if (MODE == 1) {
+#pragma unroll
+    for (int q = 0; q < kMaxColsPerThread; ++q) {
+      const int col = tid + q * kThreads;
+      if (col < j) partials[uint64_t(col) * plen + head_n + unit] = acc[q];
+    }
+  } else if (MODE == 2 && tid == 0) {
+    partials[head_n + unit] = self;
+  }
+}
+
+template <typename T, bool UPD, int MODE>
+__global__ void k_cgs_edges(const T* __restrict__ Q, uint64_t ldq, int j, T* __restrict__ r,
+                            const double* __restrict__ coef, uint64_t n_head, uint64_t tail_begin, uint64_t n_tail,
+                            uint64_t tail_slot, uint64_t plen, double* __restrict__ partials) {
+  const uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (t >= n_head + n_tail) return;
+  const uint64_t li = t < n_head ? t : tail_begin + (t - n_head);
+  const uint64_t slot = t < n_head ? t : tail_slot + (t - n_head);
+  double v = double(r[li]);
+  if (UPD) {
+    for (int i = 0; i < j; ++i) v = double(round_to<T>(__dadd_rn(v, __dmul_rn(-coef[i], double(Q[uint64_t(i) * ldq + li])))));
+    r[li] = T(v);
+  }
+  if (MODE == 1)
+    for (int i = 0; i < j; ++i) partials[uint64_t(i) * plen + slot] = __dmul_rn(double(Q[uint64_t(i) * ldq + li]), v);
+  if (MODE == 2) partials[slot] = __dmul_rn(v, v);
+}
+
+// ------------------------------------------------------------- ordered fold
+// combine_blocked (reduction.hpp:76-107) for m sequences at once: thread s
+// folds sequence s across ranks in ascending rank order, resuming straddled
+// grid blocks term by term. Partials are [rank][seq][plen_max].
+struct RankTable {
+  int n;
+  uint64_t begin[64], end[64];
+};
+__global__ void k_combine(RankTable rt, uint64_t total, uint64_t m, uint64_t plen_max,
+                          const double* __restrict__ partials, double* __restrict__ out, int post_sqrt) {
+  const uint64_t s = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (s >= m) return;
+  double closed = 0.0, open = 0.0;
+  uint64_t at = 0;
+  for (int rk = 0; rk < rt.n; ++rk) {
+    const PartialShape ps = partial_shape(rt.begin[rk], rt.end[rk], total);
+    const double* p = partials + (uint64_t(rk) * m + s) * plen_max;
+    for (uint64_t i = 0; i < ps.n_head; ++i) {
+      open = __dadd_rn(open, p[i]);
+      ++at;
+      const uint64_t ge = ((at - 1) / kBlock + 1) * kBlock;
+      if (at == (ge < total ? ge : total)) {
+        closed = __dadd_rn(closed, open);
+        open = 0.0;
+      }
+    }
+    const double* sums = p + ps.n_head;
+    uint64_t i = 0;
+    for (; i + 8 <= ps.n_sums; i += 8) {
+      double v[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) v[q] = sums[i + q];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) closed = __dadd_rn(closed, v[q]);
+    }
+    for (; i < ps.n_sums; ++i) closed = __dadd_rn(closed, sums[i]);
+    at = ps.n_sums ? ((at + ps.n_sums * kBlock) < total ? at + ps.n_sums * kBlock : total) : at;
+    const double* tail = sums + ps.n_sums;
+    for (uint64_t t = 0; t < ps.n_tail; ++t) {
+      open = __dadd_rn(open, tail[t]);
+      ++at;
+      const uint64_t ge = ((at - 1) / kBlock + 1) * kBlock;
+      if (at == (ge < total ? ge : total)) {
+        closed = __dadd_rn(closed, open);
+        open = 0.0;
+      }
+    }
+  }
+  out[s] = post_sqrt ? __dsqrt_rn(closed) : closed;  // norm2 = sqrt(dot), sharded.cpp:102-104
+}
+
+// ------------------------------------------------------ elementwise kernels
+template <typename T>
+__global__ void k_axpy(const T* __restrict__ x, T* __restrict__ y, uint64_t n, const double* alphap, double sign) {
+  const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  const double alpha = sign * (*alphap);
+  y[i] = round_to<T>(__dadd_rn(double(y[i]), __dmul_rn(alpha, double(x[i]))));
+}
+
+template <typename T>
+__global__ void k_scale(const T* __restrict__ x, T* __restrict__ out, uint64_t n, const double* cp, int recip) {
+  const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  const double c = recip ? __ddiv_rn(1.0, *cp) : *cp;
+  out[i] = round_to<T>(__dmul_rn(c, double(x[i])));
+}
+
+// dense_operator apply, operators.cpp:39-44: serial f64 fold over the full row.
+template <typename T>
+__global__ void k_dense_apply(const double* __restrict__ a, uint64_t n, const T* __restrict__ xf, T* __restrict__ y,
+                              uint64_t row_begin, uint64_t row_end) {
+  extern __shared__ double xs[];
+  for (uint64_t k = threadIdx.x; k < n; k += blockDim.x) xs[k] = double(xf[k]);
+  __syncthreads();
+  const uint64_t i = row_begin + blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (i >= row_end) return;
+  const double* row = a + i * n;
+  double acc = 0.0;
+  for (uint64_t k = 0; k < n; ++k) acc = __dadd_rn(acc, __dmul_rn(row[k], xs[k]));
+  y[i - row_begin] = round_to<T>(acc);
+}
+
+// diagonal test operator: y = round(d*x), one rounding of the exact f64 product
+template <typename T>
+__global__ void k_diag_apply(const T* __restrict__ d, const T* __restrict__ x, T* __restrict__ y, uint64_t n) {
+  const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (i < n) y[i] = round_to<T>(__dmul_rn(double(d[i]), double(x[i])));
+}
+
+// ------------------------------------------------------------ launchers
+static unsigned grid_for(uint64_t n, unsigned threads) { return unsigned((n + threads - 1) / threads); }
+
+template <typename T>
+static void launch_axpy_dot(const void* x, void* y, const void* z, const double* coef, uint64_t begin, uint64_t end,
+                            uint64_t total, double* partial, cudaStream_t s) {
+  const PartialShape ps = partial_shape(begin, end, total);
+  const uint64_t local_end = end - begin;
+  const uint64_t tail_begin = ps.n_head + ps.n_sums * kBlock;
+  const bool upd = x != nullptr;
+  const int dot = partial == nullptr ? 0 : (z == nullptr ? 2 : 1);
+  auto run = [&](auto upd_c, auto dot_c) {
+    constexpr bool U = decltype(upd_c)::value;
+    constexpr int D = decltype(dot_c)::value;
+    if (ps.n_sums) {
+      constexpr int NU = UnitsPerCta<T>::value;
+      const unsigned g = unsigned((ps.n_sums + NU - 1) / NU);
+      k_axpy_dot_units<T, U, D><<<g, NU, 0, s>>>((const T*)x, (T*)y, (const T*)z, coef, ps.n_head, ps.n_sums,
+                                                       local_end, partial ? partial + ps.n_head : nullptr);
+      SD_LAUNCHED("k_axpy_dot_units");
+    }
+    if (ps.n_head + ps.n_tail) {
+      k_axpy_dot_edges<T, U, D><<<grid_for(ps.n_head + ps.n_tail, 256), 256, 0, s>>>(
+          (const T*)x, (T*)y, (const T*)z, coef, ps.n_head, tail_begin, ps.n_tail, ps.n_head + ps.n_sums, partial);
+      SD_LAUNCHED("k_axpy_dot_edges");
+    }
+  };
+  using TT = std::true_type;
+  using FF = std::false_type;
+  using D0 = std::integral_constant<int, 0>;
+  using D1 = std::integral_constant<int, 1>;
+  using D2 = std::integral_constant<int, 2>;
+  if (upd) {
+    if (dot == 0) run(TT{}, D0{});
+    else if (dot == 1) run(TT{}, D1{});
+    else run(TT{}, D2{});
+  } else {
+    if (dot == 0) fail(SD_ARGUMENT_ERROR, "axpy_dot with neither update nor dot");
+    else if (dot == 1) run(FF{}, D1{});
+    else run(FF{}, D2{});
+  }
+}
+
+template <typename T>
+static void launch_cgs(const void* Q, uint64_t ldq, uint64_t j, void* r, const double* coef, int mode, uint64_t begin,
+                       uint64_t end, uint64_t total, double* partials, uint64_t pstride, cudaStream_t s) {
+  if (j == 0) return;
+  if (j > uint64_t(kThreads) * kMaxColsPerThread) fail(SD_ARGUMENT_ERROR, "cgs: more than 1024 columns per pass");
+  const PartialShape ps = partial_shape(begin, end, total);
+  const uint64_t local_end = end - begin, plen = pstride ? pstride : ps.len();
+  const uint64_t tail_begin = ps.n_head + ps.n_sums * kBlock;
+  const bool upd = coef != nullptr;
+  const size_t tile = (size_t(j) * (kChunk + 1) + kChunk + 2) * sizeof(T);
+  const size_t smem = ((tile + 7) / 8) * 8 + size_t(j) * sizeof(double);
+  auto run = [&](auto upd_c, auto mode_c) {
+    constexpr bool U = decltype(upd_c)::value;
+    constexpr int M = decltype(mode_c)::value;
+    if (ps.n_sums) {
+      auto kern = k_cgs_units<T, U, M>;
+      if (smem > 48 * 1024) SD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+      kern<<<unsigned(ps.n_sums), kThreads, smem, s>>>((const T*)Q, ldq, int(j), (T*)r, coef, ps.n_head, local_end,
+                                                       plen, ps.n_head, partials);
+      SD_LAUNCHED("k_cgs_units");
+    }
+    if (ps.n_head + ps.n_tail) {
+      k_cgs_edges<T, U, M><<<grid_for(ps.n_head + ps.n_tail, 128), 128, 0, s>>>(
+          (const T*)Q, ldq, int(j), (T*)r, coef, ps.n_head, tail_begin, ps.n_tail, ps.n_head + ps.n_sums, plen,
+          partials);
+      SD_LAUNCHED("k_cgs_edges");
+    }
+  };
+  using TT = std::true_type;
+  using FF = std::false_type;
+  using M0 = std::integral_constant<int, 0>;
+  using M1 = std::integral_constant<int, 1>;
+  using M2 = std::integral_constant<int, 2>;
+  if (upd) {
+    if (mode == 0) run(TT{}, M0{});
+    else if (mode == 1) run(TT{}, M1{});
+    else run(TT{}, M2{});
+  } else {
+    if (mode == 1) run(FF{}, M1{});
+    else if (mode == 2) run(FF{}, M2{});
+    else fail(SD_ARGUMENT_ERROR, "cgs with neither update nor dots");
+  }
+}
+
+void combine_device(uint64_t nranks, const uint64_t* begins, const uint64_t* ends, uint64_t total, uint64_t m,
+                    uint64_t plen_max, const double* partials, double* out, cudaStream_t s, int post_sqrt) {
+  if (nranks == 0 || nranks > 64) fail(SD_ARGUMENT_ERROR, "combine: 1..64 ranks");
+  RankTable rt;
+  rt.n = int(nranks);
+  uint64_t at = 0;
+  for (uint64_t r = 0; r < nranks; ++r) {
+    if (begins[r] != at) fail(SD_PROTOCOL_ERROR, "blocked partials are not contiguous in worker order");
+    rt.begin[r] = begins[r];
+    rt.end[r] = ends[r];
+    at = ends[r];
+  }
+  if (at != total) fail(SD_PROTOCOL_ERROR, "blocked partials do not cover the vector");
+  k_combine<<<grid_for(m, 128), 128, 0, s>>>(rt, total, m, plen_max, partials, out, post_sqrt);
+  SD_LAUNCHED("k_combine");
+}
+
+void axpy_dot(const void* x, void* y, const void* z, const double* coef, uint64_t begin, uint64_t end, uint64_t total,
+              int prec, double* partial, cudaStream_t s) {
+  if (prec == SD_F32) launch_axpy_dot<float>(x, y, z, coef, begin, end, total, partial, s);
+  else launch_axpy_dot<double>(x, y, z, coef, begin, end, total, partial, s);
+}
+
+void cgs(const void* Q, uint64_t ldq, uint64_t j, void* r, const double* coef, int mode, uint64_t begin, uint64_t end,
+         uint64_t total, int prec, double* partials, uint64_t pstride, cudaStream_t s) {
+  if (prec == SD_F32) launch_cgs<float>(Q, ldq, j, r, coef, mode, begin, end, total, partials, pstride, s);
+  else launch_cgs<double>(Q, ldq, j, r, coef, mode, begin, end, total, partials, pstride, s);
+}
+
+void probe_fill(void* x, uint64_t begin, uint64_t end, uint64_t seed, int dist, uint64_t one_hot, int prec,
+                cudaStream_t s) {
+  const uint64_t n = end - begin;
+  if (n == 0) return;
+  const uint64_t key = mix64(seed);
+  if (prec == SD_F32) k_probe<float><<<grid_for(n, 256), 256, 0, s>>>((float*)x, begin, n, key, dist, one_hot);
+  else k_probe<double><<<grid_for(n, 256), 256, 0, s>>>((double*)x, begin, n, key, dist, one_hot);
+  SD_LAUNCHED("k_probe");
+}
+
+void scale(const void* x, void* out, uint64_t n, const double* c, int recip, int prec, cudaStream_t s) {
+  if (n == 0) return;
+  if (prec == SD_F32) k_scale<float><<<grid_for(n, 256), 256, 0, s>>>((const float*)x, (float*)out, n, c, recip);
+  else k_scale<double><<<grid_for(n, 256), 256, 0, s>>>((const double*)x, (double*)out, n, c, recip);
+  SD_LAUNCHED("k_scale");
+}
+
+void axpy(const void* x, void* y, uint64_t n, const double* alpha, double sign, int prec, cudaStream_t s) {
+  if (n == 0) return;
+  if (prec == SD_F32) k_axpy<float><<<grid_for(n, 256), 256, 0, s>>>((const float*)x, (float*)y, n, alpha, sign);
+  else k_axpy<double><<<grid_for(n, 256), 256, 0, s>>>((const double*)x, (double*)y, n, alpha, sign);
+  SD_LAUNCHED("k_axpy");
+}
+
+void dense_apply(const double* a, uint64_t n, const void* xf, void* y, uint64_t rb, uint64_t re, int prec,
+                 cudaStream_t s) {
+  if (re <= rb) return;
+  const size_t smem = size_t(n) * sizeof(double);
+  if (prec == SD_F32)
+    k_dense_apply<float><<<grid_for(re - rb, 128), 128, smem, s>>>(a, n, (const float*)xf, (float*)y, rb, re);
+  else
+    k_dense_apply<double><<<grid_for(re - rb, 128), 128, smem, s>>>(a, n, (const double*)xf, (double*)y, rb, re);
+  SD_LAUNCHED("k_dense_apply");
+}
+
+void diag_apply(const void* d, const void* x, void* y, uint64_t n, int prec, cudaStream_t s) {
+  if (n == 0) return;
+  if (prec == SD_F32)
+    k_diag_apply<float><<<grid_for(n, 256), 256, 0, s>>>((const float*)d, (const float*)x, (float*)y, n);
+  else
+    k_diag_apply<double><<<grid_for(n, 256), 256, 0, s>>>((const double*)d, (const double*)x, (double*)y, n);
+  SD_LAUNCHED("k_diag_apply");
+}
+
+}  // namespace sd
+
+// ------------------------------------------------------------------ C-ABI
+using namespace sd;
+
+extern "C" {
+
+sd_status sd_k_probe_fill(void* x, uint64_t begin, uint64_t end, uint64_t seed, int dist, uint64_t one_hot,
+                          int prec, sd_stream s) {
+  return guard([&] {
+    if (end < begin) fail(SD_LAYOUT_ERROR, "probe range end < begin");
+    probe_fill(x, begin, end, seed, dist, one_hot, prec, (cudaStream_t)s);
+  });
+}
+
+sd_status sd_k_dot_partial(const void* a, const void* b, uint64_t begin, uint64_t end, uint64_t total, int prec,
+                           double* partial, sd_stream s) {
+  return guard([&] {
+    // dot(a, b) partial: no update, terms b*a (commutative, exact in f64)
+    axpy_dot(nullptr, const_cast<void*>(b), a, nullptr, begin, end, total, prec, partial, (cudaStream_t)s);
+  });
+}
+
+sd_status sd_k_combine(uint64_t nranks, const uint64_t* begins, const uint64_t* ends, uint64_t total, uint64_t m,
+                       const double* partials, double* out, sd_stream s) {
+  return guard([&] {
+    uint64_t plen_max = 0;
+    for (uint64_t r = 0; r < nranks; ++r) {
+      const uint64_t l = partial_shape(begins[r], ends[r], total).len();
+      plen_max = l > plen_max ? l : plen_max;
+    }
+    combine_device(nranks, begins, ends, total, m, plen_max, partials, out, (cudaStream_t)s, 0);
+  });
+}
+
+sd_status sd_k_axpy(const void* x, void* y, uint64_t n, const double* alpha_dev, double sign, int prec, sd_stream s) {
+  return guard([&] { axpy(x, y, n, alpha_dev, sign, prec, (cudaStream_t)s); });
+}
+
+sd_status sd_k_scale(const void* x, void* out, uint64_t n, const double* c_dev, int reciprocal, int prec,
+                     sd_stream s) {
+  return guard([&] { scale(x, out, n, c_dev, reciprocal, prec, (cudaStream_t)s); });
+}
+
+sd_status sd_k_axpy_dot(const void* x, void* y, const void* z, const double* coef, uint64_t begin, uint64_t end,
+                        uint64_t total, int prec, double* partial, sd_stream s) {
+  return guard([&] { axpy_dot(x, y, z, coef, begin, end, total, prec, partial, (cudaStream_t)s); });
+}
+
+sd_status sd_k_cgs(const void* Q, uint64_t ldq, uint64_t j, void* r, const double* coef, int mode, uint64_t begin,
+                   uint64_t end, uint64_t total, int prec, double* partials, sd_stream s) {
+  return guard([&] { cgs(Q, ldq, j, r, coef, mode, begin, end, total, prec, partials, 0, (cudaStream_t)s); });
+}
+
+sd_status sd_k_dense_apply(const double* a, uint64_t n, const void* x_full, void* y, uint64_t row_begin,
+                           uint64_t row_end, int prec, sd_stream s) {
+  return guard([&] { dense_apply(a, n, x_full, y, row_begin, row_end, prec, (cudaStream_t)s); });
+}
+
+}  // extern "C"

@@ -1,0 +1,143 @@
+"""Parity of the CUDA vector algebra and the device Lanczos engine against the
+committed reference fixtures and the oracle. Integer/byte work and every
+reference f64 fold are compared BITWISE; Gaussian probes (CUDA log/cos vs
+glibc) within 2 ulp."""
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle.pyoracle import F32, F64, GAUSSIAN, RADEMACHER  # noqa: E402
+
+GOLD = np.load(Path(__file__).with_name("golden") / "reference_golden.npz")
+
+
+@pytest.fixture(scope="module")
+def sd():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_2505_11564_b200 as sd
+    return sd
+
+
+def ulps(a, b):
+    a = np.asarray(a, np.float64).view(np.int64)
+    b = np.asarray(b, np.float64).view(np.int64)
+    return np.abs(a - b)
+
+
+@pytest.mark.parametrize("dim", [4, 5, 129, 1025, 2050, 5000])
+@pytest.mark.parametrize("workers", [1, 3])
+def test_probe_parity(sd, dim, workers):
+    pool = sd.make_pool(dim, workers)
+    for prec in (F32, F64):
+        for seed in (42, 99):
+            got = sd.gather(pool, sd.draw_probe(pool, None, prec, seed=seed, distribution=sd.RADEMACHER))
+            assert np.array_equal(got, GOLD[f"probe_rad_{dim}_{prec}_{seed}"])
+            g = sd.gather(pool, sd.draw_probe(pool, None, prec, seed=seed, distribution=sd.GAUSSIAN))
+            ref = GOLD[f"probe_gauss_{dim}_{prec}_{seed}"]
+            if prec == F32:
+                assert np.max(np.abs(g - ref) / np.abs(ref)) <= 2 * 2.0 ** -24
+            else:
+                assert ulps(g, ref).max() <= 4
+    v = sd.gather(sd.make_pool(5, 2), sd.draw_probe(sd.make_pool(5, 2), None, F64, distribution=sd.ONE_HOT,
+                                                     one_hot_index=2, normalize=False))
+    assert np.array_equal(v, GOLD["probe_onehot_5_2"])
+    with pytest.raises(sd.ArgumentError):
+        sd.draw_probe(sd.make_pool(5, 2), None, F64, distribution=sd.ONE_HOT, one_hot_index=5)
+
+
+@pytest.mark.parametrize("dim", [1000, 1025, 5000, 70001])
+def test_dot_axpy_scale_bitwise(sd, oracle, dim):
+    for prec in (F32, F64):
+        a = oracle.gaussian_fill(21, 0, dim)
+        b = oracle.gaussian_fill(22, 0, dim)
+        if prec == F32:
+            a = a.astype(np.float32).astype(np.float64)
+            b = b.astype(np.float32).astype(np.float64)
+        ref_dot = GOLD[f"dot_{dim}_{prec}"][0]
+        for workers in (1, 2, 3, 7):
+            pool = sd.make_pool(dim, workers)
+            A, B = sd.scatter(pool, a, prec), sd.scatter(pool, b, prec)
+            d = sd.dot(pool, A, B)
+            assert np.float64(d).view(np.int64) == np.float64(ref_dot).view(np.int64), (workers, prec)
+            assert sd.dot(pool, B, A) == d
+            assert np.array_equal(sd.gather(pool, sd.axpy(pool, 0.7, A, B)), GOLD[f"axpy_{dim}_{prec}"])
+            assert np.array_equal(sd.gather(pool, sd.scale(pool, A, -1.25)), GOLD[f"scale_{dim}_{prec}"])
+
+
+def test_vector_errors(sd):
+    p3, p4 = sd.make_pool(3, 1), sd.make_pool(4, 1)
+    a = sd.scatter(p3, [1, 2, 3], F64)
+    b = sd.scatter(p4, [1, 2, 3, 4], F64)
+    with pytest.raises(sd.LayoutError):
+        sd.dot(p3, a, b)
+    with pytest.raises(sd.LayoutError):
+        sd.dot(p3, a, sd.scatter(p3, [1, 2, 3], F32))
+    with pytest.raises(sd.ArgumentError):
+        sd.scale(p3, a, float("nan"))
+    assert sd.dot(p3, a, sd.scatter(p3, [4, 5, 6], F64)) == 32.0
+    assert sd.norm2(sd.make_pool(2, 2), sd.scatter(sd.make_pool(2, 2), [3, 4], F64)) == 5.0
+
+
+def test_dense_apply_bitwise(sd, oracle):
+    W = sd.wigner_dense(512, 1.0, 0)
+    assert np.array_equal(W, oracle.wigner(512, 1.0, 0))
+    op = sd.dense_operator(W)
+    for prec in (F32, F64):
+        x = oracle.draw_probe(512, 7, GAUSSIAN, prec=prec)
+        for workers in (1, 5):
+            pool = sd.make_pool(512, workers)
+            y = sd.gather(pool, op.apply(pool, sd.scatter(pool, x, prec)))
+            assert np.array_equal(y, GOLD[f"wigner512_apply_{prec}"])
+    with pytest.raises(sd.LayoutError):
+        op.apply(sd.make_pool(5, 1), sd.scatter(sd.make_pool(5, 1), np.ones(5), F64))
+
+
+@pytest.mark.parametrize("prec", [F32, F64])
+@pytest.mark.parametrize("reorth", [0, 1])
+def test_lanczos_dense_bitwise(sd, prec, reorth):
+    S = sd.spiked_dense(256, 1.0, [50.0, -50.0], 5)
+    op = sd.dense_operator(S)
+    cfg = sd.LanczosConfig(k_max=25, reorthogonalize=reorth, prec=prec,
+                           probe=sd.ProbeSpec(seed=42, distribution=RADEMACHER))
+    r = sd.lanczos_run(op, cfg)
+    assert np.array_equal(r.alphas, GOLD[f"lanczos_spiked256_{prec}_{reorth}_1_alpha"])
+    assert np.array_equal(r.betas, GOLD[f"lanczos_spiked256_{prec}_{reorth}_1_beta"])
+    # Gaussian probe: start vector differs by ulps from glibc's, so tolerance
+    cfg.probe = sd.ProbeSpec(seed=42, distribution=GAUSSIAN)
+    r = sd.lanczos_run(op, cfg)
+    ref_a = GOLD[f"lanczos_spiked256_{prec}_{reorth}_0_alpha"]
+    tol = 1e-4 if prec == F32 else 1e-10
+    assert np.max(np.abs(r.alphas - ref_a)) <= tol * np.max(np.abs(ref_a))
+
+
+@pytest.mark.parametrize("P", [3 * 1024 * 1024 + 77, 1000003])
+@pytest.mark.parametrize("reorth", [0, 1])
+def test_lanczos_large_diag_bitwise(sd, oracle, P, reorth):
+    """Engine at multi-million P (many grid blocks, ragged last block) on a
+    diagonal operator, bitwise against the oracle recurrence."""
+    d64 = np.linspace(-3.0, 5.0, P).astype(np.float32).astype(np.float64)
+    d = torch.tensor(d64, dtype=torch.float32, device="cuda")
+
+    k = 12
+    cfg = sd.LanczosConfig(k_max=k, reorthogonalize=reorth, prec=F32,
+                           probe=sd.ProbeSpec(seed=7, distribution=RADEMACHER))
+    op = sd.diag_operator(d)
+    r = sd.lanczos_run(op, cfg)
+    ref = oracle.lanczos_diag(d64, k, reorth=bool(reorth), seed=7)
+    assert np.array_equal(r.alphas, ref["alphas"])
+    assert np.array_equal(r.betas, ref["betas"])
+
+
+def test_ritz_matches_oracle(sd, oracle):
+    S = oracle.spiked(128, 1.0, [40.0, -35.0], 2)
+    r = oracle.lanczos_dense(S, 40, reorth=True)
+    mine = sd.ritz_decompose(r["alphas"], r["betas"])
+    v, w = oracle.ritz(r["alphas"], r["betas"])
+    assert np.max(np.abs(mine.values - v)) <= 1e-12 * np.max(np.abs(v))
+    assert np.max(np.abs(mine.weights - w)) <= 1e-12
+    assert mine.residual <= 1e-12 and abs(mine.weights.sum() - 1) <= 1e-12
