@@ -137,6 +137,34 @@ sd_status sd_comm_allreduce_f32(sd_comm c, float* buf, uint64_t n, sd_stream s);
 /* All-gather of `bytes` per rank (ordered scalar partial exchange). */
 sd_status sd_comm_allgather(sd_comm c, const void* send, void* recv, uint64_t bytes, sd_stream s);
 
+/* ------------------------------------------------------------- GEMM
+ * C[z] = alpha * op(A[z]) . op(B[z]) + beta * C[z] on tcgen05 tensor cores,
+ * fp32 in/out. 3xTF32 when a_small and b_small are given (x_small =
+ * x - trunc_tf32(x), see sd_split_tf32), else 1xTF32. a_mn = 0: A row-major
+ * m x k, 1: row-major k x m; b_mn = 0: B row-major n x k, 1: row-major k x n.
+ * Batch z = z1 + Z1*z2 with element strides per operand. Leading dimensions
+ * and strides must be multiples of 4 elements (16 B, TMA). */
+typedef struct {
+  int m, n, k;
+  const float* a;
+  const float* a_small;
+  long long lda;
+  int a_mn;
+  const float* b;
+  const float* b_small;
+  long long ldb;
+  int b_mn;
+  float* c;
+  long long ldc;
+  float alpha, beta;
+  int z1, z2;
+  long long sa1, sa2, sb1, sb2, sc1, sc2;
+} sd_gemm_desc;
+sd_status sd_gemm_tf32(const sd_gemm_desc* d, sd_stream s);
+/* small[i] = x[i] - hi(x[i]); mode 0: hi = trunc_tf32 (what the MMA reads),
+ * mode 1: hi = round-to-nearest-away tf32. */
+sd_status sd_split_tf32(const float* x, float* small, uint64_t n, int mode, sd_stream s);
+
 /* ------------------------------------------------------------ operators
  * OperatorHandle (operators.hpp:15-21): apply(x, y) on this rank's shard.
  * x_full is the gathered logical vector when the operator needs it. */

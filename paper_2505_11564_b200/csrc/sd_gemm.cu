@@ -1,0 +1,471 @@
+// fp32-faithful GEMM on the 5th-generation tensor cores (sm_100a).
+//
+//   C[z] = alpha * op(A[z]) . op(B[z]) + beta * C[z]      (fp32 in, fp32 out)
+//
+// 3xTF32: every operand x is consumed as its raw fp32 bits (the tensor core
+// reads the top 19 bits, i.e. trunc_tf32(x)) plus a precomputed residual
+// x_s = x - trunc_tf32(x); the product is accumulated in TMEM as
+//   A.B ~= A_b.B_b + A_b.B_s + A_s.B_b        (3 tcgen05.mma kind::tf32)
+// which carries ~21-22 significant bits per product (fp32-faithful).
+//
+// Structure (one 128x128 output tile per CTA, 6 warps):
+//   warp 0   : TMA producer (cp.async.bulk.tensor, 128B swizzle) into a
+//              3-stage smem ring guarded by full/empty mbarriers;
+//   warp 1   : TMEM allocator + single-thread tcgen05.mma issuer, releasing
+//              ring slots with tcgen05.commit;
+//   warps 2-5: epilogue, tcgen05.ld 32x32b from TMEM -> registers -> global.
+// Operand majors: A is K-major (row-major M x K) or MN-major (row-major K x M);
+// B is K-major (row-major N x K) or MN-major (row-major K x N). A batch index
+// z decomposes as (z1 = z % Z1, z2 = z / Z1) with independent strides, which
+// covers per-head attention slices of a packed QKV activation.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <mutex>
+
+#include "sd_common.cuh"
+#include "sd_gemm.h"
+
+namespace sd {
+
+namespace {
+
+constexpr int BM = 128, BN = 128, BK = 32, STAGES = 3;
+constexpr int TILE_BYTES = BM * BK * 4;  // 16 KB per operand tile (BN == BM)
+constexpr int NUM_THREADS = 192;
+constexpr uint32_t TMEM_COLS = 2 * BN;  // two accumulation buffers
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t"
+      "}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_4d(const CUtensorMap* map, uint64_t* bar, void* dst, int c0, int c1, int c2,
+                                            int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], [%2];" ::
+          "r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+
+// UMMA shared-memory descriptor (tcgen05 "matrix descriptor"). layout 2 =
+// SWIZZLE_128B (K-major tiles), 1 = SWIZZLE_128B_BASE32B (MN-major tf32 tiles,
+// the only MN-major smem layout the tf32 MMA accepts).
+__device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
+  uint64_t d = 0;
+  d |= uint64_t((saddr >> 4) & 0x3FFF);
+  d |= uint64_t((lbo >> 4) & 0x3FFF) << 16;
+  d |= uint64_t((sbo >> 4) & 0x3FFF) << 32;
+  d |= uint64_t(1) << 46;  // descriptor version (sm_100)
+  d |= uint64_t(layout) << 61;
+  return d;
+}
+
+// Instruction descriptor: kind::tf32, fp32 accumulate, M=128, N=BN.
+__host__ __device__ constexpr uint32_t make_idesc(bool a_mn, bool b_mn) {
+  return (1u << 4)                 // D format F32
+         | (2u << 7)               // A format TF32
+         | (2u << 10)              // B format TF32
+         | (uint32_t(a_mn) << 15)  // A major
+         | (uint32_t(b_mn) << 16)  // B major
+         | (uint32_t(BN >> 3) << 17) | (uint32_t(BM >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t"
+      "}" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+struct EpiParams {
+  float* C;
+  long long ldc, sc1, sc2;
+  int M, N, Z1;
+  float alpha, beta;
+  float* dbg;  // debug: receives smem stage 0 after the accumulator is complete
+};
+
+// Descriptor of k-step `ks` (8 tf32) of an operand tile. K-major tiles are 128
+// rows x 128 B, 128B-swizzled in 8-row (1024 B) atoms: advance 32 B per k-step,
+// SBO = 1024 B. MN-major tiles are four 32-element chunks of [32 k-rows x 128 B]
+// swizzled in 4-row (512 B) atoms of 32 B granules: advance 8 rows = 1024 B per
+// k-step, LBO = 4096 B between MN chunks, SBO = 512 B between 4-row groups.
+template <bool MN>
+__device__ __forceinline__ uint64_t tile_desc(uint32_t base, int ks) {
+  if (MN) return make_desc(base + ks * 1024, 4096, 512, 1);
+  return make_desc(base + ks * 32, 16, 1024, 2);
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* v) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]),
+        "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+        "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+}
+
+// The tensor core's fp32 accumulation is not round-to-nearest (its error grows
+// ~linearly with the number of accumulated MMAs). To stay fp32-faithful at
+// K = 8192 the K loop is cut into chunks of KC k-blocks: each chunk
+// accumulates in one of two TMEM buffers, and the epilogue warps drain every
+// finished chunk into round-to-nearest fp32 registers while the MMA warp
+// fills the other buffer.
+constexpr int KC = 4;  // k-blocks (4 x 32 = 128 of K) per TMEM chunk
+
+template <bool A_MN, bool B_MN, bool THREE>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    k_gemm_tf32(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mAs,
+                const __grid_constant__ CUtensorMap mB, const __grid_constant__ CUtensorMap mBs, int K, EpiParams ep) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  // 1024-byte aligned ring: per stage [A | As | B | Bs]
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  constexpr int NT = THREE ? 4 : 2;
+  constexpr int STAGE_BYTES = NT * TILE_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;  // [2]
+  uint64_t* tempty = tfull + 2;      // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n0 = blockIdx.x * BN, m0 = blockIdx.y * BM;
+  const int z = blockIdx.z, z1 = z % ep.Z1, z2 = z / ep.Z1;
+  const int num_kb = (K + BK - 1) / BK;
+  const int num_chunks = (num_kb + KC - 1) / KC;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&mA) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&mB) : "memory");
+      for (int kb = 0; kb < num_kb; ++kb) {
+        const int s = kb % STAGES;
+        const uint32_t ph = (kb / STAGES) & 1;
+        mbar_wait(&empty[s], ph ^ 1);
+        unsigned char* st = smem + s * STAGE_BYTES;
+        mbar_expect_tx(&full[s], STAGE_BYTES);
+        const int k0 = kb * BK;
+        if (A_MN) {
+          for (int c = 0; c < 4; ++c) {
+            tma_load_4d(&mA, &full[s], st + c * 4096, m0 + 32 * c, k0, z1, z2);
+            if (THREE) tma_load_4d(&mAs, &full[s], st + TILE_BYTES + c * 4096, m0 + 32 * c, k0, z1, z2);
+          }
+        } else {
+          tma_load_4d(&mA, &full[s], st, k0, m0, z1, z2);
+          if (THREE) tma_load_4d(&mAs, &full[s], st + TILE_BYTES, k0, m0, z1, z2);
+        }
+        unsigned char* sb = st + (THREE ? 2 : 1) * TILE_BYTES;
+        if (B_MN) {
+          for (int c = 0; c < 4; ++c) {
+            tma_load_4d(&mB, &full[s], sb + c * 4096, n0 + 32 * c, k0, z1, z2);
+            if (THREE) tma_load_4d(&mBs, &full[s], sb + TILE_BYTES + c * 4096, n0 + 32 * c, k0, z1, z2);
+          }
+        } else {
+          tma_load_4d(&mB, &full[s], sb, k0, n0, z1, z2);
+          if (THREE) tma_load_4d(&mBs, &full[s], sb + TILE_BYTES, k0, n0, z1, z2);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc = make_idesc(A_MN, B_MN);
+    for (int kb = 0; kb < num_kb; ++kb) {
+      const int s = kb % STAGES;
+      const uint32_t ph = (kb / STAGES) & 1;
+      const int chunk = kb / KC, buf = chunk & 1;
+      const bool first = (kb % KC) == 0;
+      const bool last = (kb % KC) == KC - 1 || kb == num_kb - 1;
+      if (first && chunk >= 2) mbar_wait(&tempty[buf], ((chunk >> 1) - 1) & 1);
+      mbar_wait(&full[s], ph);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      if (lane == 0) {
+        const uint32_t d = tmem + uint32_t(buf * BN);
+        const uint32_t st = smem_u32(smem + s * STAGE_BYTES);
+        const uint32_t a = st, as = st + TILE_BYTES;
+        const uint32_t b = st + (THREE ? 2 : 1) * TILE_BYTES, bs = b + TILE_BYTES;
+#pragma unroll
+        for (int ks = 0; ks < BK / 8; ++ks) {
+          const uint32_t acc0 = (first && ks == 0) ? 0u : 1u;
+          if (THREE) {
+            mma_tf32(d, tile_desc<A_MN>(as, ks), tile_desc<B_MN>(b, ks), idesc, acc0);
+            mma_tf32(d, tile_desc<A_MN>(a, ks), tile_desc<B_MN>(bs, ks), idesc, 1u);
+            mma_tf32(d, tile_desc<A_MN>(a, ks), tile_desc<B_MN>(b, ks), idesc, 1u);
+          } else {
+            mma_tf32(d, tile_desc<A_MN>(a, ks), tile_desc<B_MN>(b, ks), idesc, acc0);
+          }
+        }
+        mma_commit(&empty[s]);
+        if (last) mma_commit(&tfull[buf]);
+      }
+      __syncwarp();
+    }
+  } else {
+    // epilogue: warp w drains TMEM lanes 32*(w%4) .. +31 (its sub-partition);
+    // thread = one output row, BN fp32 accumulators in registers.
+    const int sub = warp & 3;
+    const int row = m0 + sub * 32 + lane;
+    float acc[BN];
+#pragma unroll
+    for (int j = 0; j < BN; ++j) acc[j] = 0.0f;
+    for (int c = 0; c < num_chunks; ++c) {
+      const int buf = c & 1;
+      mbar_wait(&tfull[buf], (c >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        uint32_t v[32];
+        tmem_ld32(tmem + (uint32_t(sub * 32) << 16) + uint32_t(buf * BN + c0), v);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int j = 0; j < 32; ++j) acc[c0 + j] += __uint_as_float(v[j]);
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[buf]);
+    }
+    if (ep.dbg) {
+      const float* sm = reinterpret_cast<const float*>(smem);
+      for (int i = threadIdx.x - 64; i < STAGE_BYTES / 4; i += 128) ep.dbg[i] = sm[i];
+    }
+    if (row < ep.M) {
+      float* crow = ep.C + z1 * ep.sc1 + z2 * ep.sc2 + (long long)row * ep.ldc + n0;
+      const int nvalid = ep.N - n0;
+      const bool vec = nvalid >= BN && ((reinterpret_cast<uintptr_t>(crow) & 15) == 0);
+      if (vec) {
+#pragma unroll
+        for (int j = 0; j < BN; j += 4) {
+          float4 o = make_float4(ep.alpha * acc[j], ep.alpha * acc[j + 1], ep.alpha * acc[j + 2], ep.alpha * acc[j + 3]);
+          if (ep.beta != 0.0f) {
+            const float4 old = *reinterpret_cast<const float4*>(crow + j);
+            o.x += ep.beta * old.x;
+            o.y += ep.beta * old.y;
+            o.z += ep.beta * old.z;
+            o.w += ep.beta * old.w;
+          }
+          *reinterpret_cast<float4*>(crow + j) = o;
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < BN; ++j) {
+          if (j < nvalid) {
+            float r = ep.alpha * acc[j];
+            if (ep.beta != 0.0f) r += ep.beta * crow[j];
+            crow[j] = r;
+          }
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+  }
+}
+
+// residual x - trunc_tf32(x) (the tensor core reads trunc_tf32 of the raw bits)
+__global__ void k_split_tf32(const float* __restrict__ x, float* __restrict__ s, long long n, int mode) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const float v = x[i];
+  float hi;
+  if (mode == 0) {
+    hi = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+  } else {
+    uint32_t t;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(t) : "f"(v));
+    hi = __uint_as_float(t);
+  }
+  s[i] = v - hi;
+}
+
+// ------------------------------------------------------------- tensor maps
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encoder() {
+  static EncodeFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<EncodeFn>(p);
+  }();
+  if (!fn) fail(SD_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
+  return fn;
+}
+
+// 4-D map over a row-major operand: inner extent `inner` (contiguous),
+// `outer` rows of stride ld, then two batch dims.
+void make_map(CUtensorMap* m, const float* base, long long inner, long long outer, long long ld, int Z1,
+              long long s1, int Z2, long long s2, int box_inner, int box_outer, bool mn_major) {
+  if ((reinterpret_cast<uintptr_t>(base) & 15) != 0) fail(SD_ARGUMENT_ERROR, "gemm operand not 16-byte aligned");
+  if ((ld * 4) % 16 != 0 || (Z1 > 1 && (s1 * 4) % 16) || (Z2 > 1 && (s2 * 4) % 16))
+    fail(SD_ARGUMENT_ERROR, "gemm operand strides must be multiples of 16 bytes");
+  cuuint64_t dims[4] = {cuuint64_t(inner), cuuint64_t(outer), cuuint64_t(Z1), cuuint64_t(Z2)};
+  const long long whole = ((ld * outer * 4 + 15) / 16) * 16;  // stride of a size-1 batch dim
+  cuuint64_t strides[3] = {cuuint64_t(ld * 4), cuuint64_t(Z1 > 1 ? s1 * 4 : whole), cuuint64_t(Z2 > 1 ? s2 * 4 : whole)};
+  cuuint32_t box[4] = {cuuint32_t(box_inner), cuuint32_t(box_outer), 1, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  const CUresult r = encoder()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(base), dims, strides, box, es,
+                               CU_TENSOR_MAP_INTERLEAVE_NONE,
+                               mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(SD_CUDA_ERROR, "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+}
+
+template <bool A_MN, bool B_MN, bool THREE>
+void launch(const GemmArgs& g, cudaStream_t s) {
+  CUtensorMap mA, mAs, mB, mBs;
+  // A logical M x K. K-major: rows = M (ld = lda), inner = K. MN-major: rows = K, inner = M.
+  if (A_MN) {
+    make_map(&mA, g.A, g.M, g.K, g.lda, g.Z1, g.sa1, g.Z2, g.sa2, 32, BK, true);
+    make_map(&mAs, THREE ? g.As : g.A, g.M, g.K, g.lda, g.Z1, g.sa1, g.Z2, g.sa2, 32, BK, true);
+  } else {
+    make_map(&mA, g.A, g.K, g.M, g.lda, g.Z1, g.sa1, g.Z2, g.sa2, BK, BM, false);
+    make_map(&mAs, THREE ? g.As : g.A, g.K, g.M, g.lda, g.Z1, g.sa1, g.Z2, g.sa2, BK, BM, false);
+  }
+  if (B_MN) {
+    make_map(&mB, g.B, g.N, g.K, g.ldb, g.Z1, g.sb1, g.Z2, g.sb2, 32, BK, true);
+    make_map(&mBs, THREE ? g.Bs : g.B, g.N, g.K, g.ldb, g.Z1, g.sb1, g.Z2, g.sb2, 32, BK, true);
+  } else {
+    make_map(&mB, g.B, g.K, g.N, g.ldb, g.Z1, g.sb1, g.Z2, g.sb2, BK, BN, false);
+    make_map(&mBs, THREE ? g.Bs : g.B, g.K, g.N, g.ldb, g.Z1, g.sb1, g.Z2, g.sb2, BK, BN, false);
+  }
+  EpiParams ep{g.C, g.ldc, g.sc1, g.sc2, g.M, g.N, g.Z1, g.alpha, g.beta, g.dbg};
+  constexpr int NT = THREE ? 4 : 2;
+  const size_t smem = 1024 + STAGES * NT * TILE_BYTES + 256;
+  auto kern = k_gemm_tf32<A_MN, B_MN, THREE>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    SD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    attr_set = true;
+  }
+  dim3 grid((g.N + BN - 1) / BN, (g.M + BM - 1) / BM, g.Z1 * g.Z2);
+  kern<<<grid, NUM_THREADS, smem, s>>>(mA, mAs, mB, mBs, g.K, ep);
+  SD_LAUNCHED("k_gemm_tf32");
+}
+
+}  // namespace
+
+void gemm(const GemmArgs& g, cudaStream_t s) {
+  if (g.M <= 0 || g.N <= 0 || g.K <= 0) return;
+  const bool three = g.As != nullptr && g.Bs != nullptr;
+#define SD_GEMM_CASE(AM, BMJ, TH) \
+  if (g.a_mn == AM && g.b_mn == BMJ && three == TH) return launch<AM, BMJ, TH>(g, s);
+  SD_GEMM_CASE(false, false, true)
+  SD_GEMM_CASE(false, true, true)
+  SD_GEMM_CASE(true, false, true)
+  SD_GEMM_CASE(true, true, true)
+  SD_GEMM_CASE(false, false, false)
+  SD_GEMM_CASE(false, true, false)
+  SD_GEMM_CASE(true, false, false)
+  SD_GEMM_CASE(true, true, false)
+#undef SD_GEMM_CASE
+}
+
+void split_tf32(const float* x, float* small, long long n, int mode, cudaStream_t s) {
+  if (n <= 0) return;
+  k_split_tf32<<<unsigned((n + 255) / 256), 256, 0, s>>>(x, small, n, mode);
+  SD_LAUNCHED("k_split_tf32");
+}
+
+}  // namespace sd
+
+extern "C" {
+
+float* sd_gemm_debug_buffer = nullptr;  // test hook: set from tests to capture smem stage 0
+
+sd_status sd_gemm_tf32(const sd_gemm_desc* d, sd_stream s) {
+  return sd::guard([&] {
+    sd::GemmArgs g;
+    g.M = d->m;
+    g.N = d->n;
+    g.K = d->k;
+    g.A = d->a;
+    g.As = d->a_small;
+    g.lda = d->lda;
+    g.a_mn = d->a_mn != 0;
+    g.B = d->b;
+    g.Bs = d->b_small;
+    g.ldb = d->ldb;
+    g.b_mn = d->b_mn != 0;
+    g.C = d->c;
+    g.ldc = d->ldc;
+    g.alpha = d->alpha;
+    g.beta = d->beta;
+    g.Z1 = d->z1 > 0 ? d->z1 : 1;
+    g.Z2 = d->z2 > 0 ? d->z2 : 1;
+    g.sa1 = d->sa1;
+    g.sa2 = d->sa2;
+    g.sb1 = d->sb1;
+    g.sb2 = d->sb2;
+    g.sc1 = d->sc1;
+    g.sc2 = d->sc2;
+    g.dbg = sd_gemm_debug_buffer;
+    sd::gemm(g, (cudaStream_t)s);
+  });
+}
+
+sd_status sd_split_tf32(const float* x, float* small, uint64_t n, int mode, sd_stream s) {
+  return sd::guard([&] { sd::split_tf32(x, small, (long long)n, mode, (cudaStream_t)s); });
+}
+
+}  // extern "C"

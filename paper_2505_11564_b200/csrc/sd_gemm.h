@@ -1,0 +1,25 @@
+// Internal GEMM interface (see sd_gemm.cu).
+#pragma once
+#include <cuda_runtime.h>
+
+namespace sd {
+struct GemmArgs {
+  int M = 0, N = 0, K = 0;
+  const float* A = nullptr;   // raw fp32 operand
+  const float* As = nullptr;  // residual (3xTF32); nullptr -> 1xTF32
+  long long lda = 0;
+  bool a_mn = false;          // false: A row-major M x K; true: row-major K x M
+  const float* B = nullptr;
+  const float* Bs = nullptr;
+  long long ldb = 0;
+  bool b_mn = false;          // false: B row-major N x K; true: row-major K x N
+  float* C = nullptr;
+  long long ldc = 0;
+  float alpha = 1.0f, beta = 0.0f;
+  int Z1 = 1, Z2 = 1;         // batch z = z1 + Z1 * z2
+  float* dbg = nullptr;
+  long long sa1 = 0, sa2 = 0, sb1 = 0, sb2 = 0, sc1 = 0, sc2 = 0;  // element strides
+};
+void gemm(const GemmArgs& g, cudaStream_t s);
+void split_tf32(const float* x, float* small, long long n, int mode, cudaStream_t s);
+}  // namespace sd
