@@ -165,6 +165,34 @@ sd_status sd_gemm_tf32(const sd_gemm_desc* d, sd_stream s);
  * mode 1: hi = round-to-nearest-away tf32. */
 sd_status sd_split_tf32(const float* x, float* small, uint64_t n, int mode, sd_stream s);
 
+/* ---------------------------------------------------------- GPT HVP engine
+ * Hessian-vector product of a GPT-2-style decoder (pre-LN, fused QKV, causal
+ * softmax attention, GELU-tanh MLP, tied embeddings, mean next-token
+ * cross-entropy) by forward-over-reverse: PAPER.md Alg. 1 / SPEC.md:193-210
+ * (hvp, batched_hvp) for the SPEC's attention_block model family. Flat
+ * parameter order = declaration order, row-major. */
+typedef struct {
+  int n_layer, d, n_head, ff, vocab, ctx;
+} sd_gpt_config;
+typedef struct sd_gpt_s* sd_gpt;
+uint64_t sd_gpt_param_count(const sd_gpt_config* c);
+sd_status sd_gpt_param_layout(const sd_gpt_config* c, uint64_t* offsets, uint64_t* rows, uint64_t* cols, int* kinds,
+                              uint64_t* count);
+/* synthetic init: matrices 0.02*N(0,1), LN gains 1 + gain_scale*N, biases
+ * bias_scale*N, N = gaussian(seed, flat index) (rng.hpp:37-41) */
+sd_status sd_gpt_init_params(const sd_gpt_config* c, uint64_t seed, double gain_scale, double bias_scale,
+                             float* theta, sd_stream s);
+uint64_t sd_gpt_workspace_bytes(const sd_gpt_config* c, int batch, int seq);
+/* theta: caller-owned device parameters (P floats), must outlive the engine */
+sd_status sd_gpt_create(const sd_gpt_config* c, int batch, int seq, const float* theta, void* workspace,
+                        uint64_t workspace_bytes, sd_stream s, sd_gpt* out);
+/* host int32 tokens/targets (batch*seq each); Hv is scaled by loss_scale/1
+ * relative to the per-token SUM (loss_scale = 1/global_tokens for the mean) */
+sd_status sd_gpt_set_batch(sd_gpt g, const int* tokens, const int* targets, float loss_scale, sd_stream s);
+sd_status sd_gpt_hvp(sd_gpt g, const float* v, float* hv, sd_stream s);
+sd_status sd_gpt_last_loss(sd_gpt g, double* loss, sd_stream s);
+sd_status sd_gpt_destroy(sd_gpt g);
+
 /* ------------------------------------------------------------ operators
  * OperatorHandle (operators.hpp:15-21): apply(x, y) on this rank's shard.
  * x_full is the gathered logical vector when the operator needs it. */
@@ -176,6 +204,9 @@ sd_status sd_operator_dense(uint64_t n, const double* a_host, sd_operator* out);
 /* Diagonal test operator y = round(d * x); d is caller-owned device memory
  * holding this rank's shard of the diagonal (prec storage). */
 sd_status sd_operator_diag(uint64_t dim, const void* d_dev, int prec, sd_operator* out);
+/* Lanczos operator y = H x of a GPT engine; with comm, per-rank Hv over
+ * data-sharded batches are summed with an NCCL all-reduce (Alg. 1). */
+sd_status sd_operator_gpt(sd_gpt g, sd_comm comm, sd_operator* out);
 sd_status sd_operator_apply(sd_operator op, const void* x, void* y, int prec, sd_stream s);
 uint64_t sd_operator_dim(sd_operator op);
 sd_status sd_operator_destroy(sd_operator op);

@@ -13,3 +13,5 @@ from .core import *  # noqa: E402,F401,F403
 from .core import (F32, F64, GAUSSIAN, ONE_HOT, RADEMACHER, REORTH_FULL, REORTH_NONE, Lanczos,  # noqa: E402,F401
                    LanczosConfig, LanczosResult, OperatorHandle, ProbeSpec, RitzSpectrum, ShardedVector, ShardLayout,
                    WorkerPool)
+
+from . import gemm, gpt  # noqa: E402,F401

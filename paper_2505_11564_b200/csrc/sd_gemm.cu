@@ -110,7 +110,9 @@ struct EpiParams {
   long long ldc, sc1, sc2;
   int M, N, Z1;
   float alpha, beta;
-  float* dbg;  // debug: receives smem stage 0 after the accumulator is complete
+  const float* bias;  // per output column, may be null
+  float* Cs;          // residual output, may be null
+  float* dbg;         // debug: receives smem stage 0 after the accumulator is complete
 };
 
 // Descriptor of k-step `ks` (8 tf32) of an operand tile. K-major tiles are 128
@@ -282,9 +284,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       for (int i = threadIdx.x - 64; i < STAGE_BYTES / 4; i += 128) ep.dbg[i] = sm[i];
     }
     if (row < ep.M) {
-      float* crow = ep.C + z1 * ep.sc1 + z2 * ep.sc2 + (long long)row * ep.ldc + n0;
+      const long long off = z1 * ep.sc1 + z2 * ep.sc2 + (long long)row * ep.ldc + n0;
+      float* crow = ep.C + off;
+      float* srow = ep.Cs ? ep.Cs + off : nullptr;
+      const float* brow = ep.bias ? ep.bias + n0 : nullptr;
       const int nvalid = ep.N - n0;
-      const bool vec = nvalid >= BN && ((reinterpret_cast<uintptr_t>(crow) & 15) == 0);
+      const bool vec = nvalid >= BN && ((reinterpret_cast<uintptr_t>(crow) & 15) == 0) &&
+                       (!srow || (reinterpret_cast<uintptr_t>(srow) & 15) == 0);
       if (vec) {
 #pragma unroll
         for (int j = 0; j < BN; j += 4) {
@@ -296,7 +302,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             o.z += ep.beta * old.z;
             o.w += ep.beta * old.w;
           }
+          if (brow) {
+            o.x += brow[j];
+            o.y += brow[j + 1];
+            o.z += brow[j + 2];
+            o.w += brow[j + 3];
+          }
           *reinterpret_cast<float4*>(crow + j) = o;
+          if (srow) {
+            const float4 r = make_float4(o.x - __uint_as_float(__float_as_uint(o.x) & 0xFFFFE000u),
+                                         o.y - __uint_as_float(__float_as_uint(o.y) & 0xFFFFE000u),
+                                         o.z - __uint_as_float(__float_as_uint(o.z) & 0xFFFFE000u),
+                                         o.w - __uint_as_float(__float_as_uint(o.w) & 0xFFFFE000u));
+            *reinterpret_cast<float4*>(srow + j) = r;
+          }
         }
       } else {
 #pragma unroll
@@ -304,7 +323,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (j < nvalid) {
             float r = ep.alpha * acc[j];
             if (ep.beta != 0.0f) r += ep.beta * crow[j];
+            if (brow) r += brow[j];
             crow[j] = r;
+            if (srow) srow[j] = r - __uint_as_float(__float_as_uint(r) & 0xFFFFE000u);
           }
         }
       }
@@ -389,7 +410,7 @@ void launch(const GemmArgs& g, cudaStream_t s) {
     make_map(&mB, g.B, g.K, g.N, g.ldb, g.Z1, g.sb1, g.Z2, g.sb2, BK, BN, false);
     make_map(&mBs, THREE ? g.Bs : g.B, g.K, g.N, g.ldb, g.Z1, g.sb1, g.Z2, g.sb2, BK, BN, false);
   }
-  EpiParams ep{g.C, g.ldc, g.sc1, g.sc2, g.M, g.N, g.Z1, g.alpha, g.beta, g.dbg};
+  EpiParams ep{g.C, g.ldc, g.sc1, g.sc2, g.M, g.N, g.Z1, g.alpha, g.beta, g.bias, g.Cs, g.dbg};
   constexpr int NT = THREE ? 4 : 2;
   const size_t smem = 1024 + STAGES * NT * TILE_BYTES + 256;
   auto kern = k_gemm_tf32<A_MN, B_MN, THREE>;

@@ -17,6 +17,8 @@ struct GemmArgs {
   long long ldc = 0;
   float alpha = 1.0f, beta = 0.0f;
   int Z1 = 1, Z2 = 1;         // batch z = z1 + Z1 * z2
+  const float* bias = nullptr;  // per-column bias added in the epilogue
+  float* Cs = nullptr;          // optional tf32 residual of the final C (same strides as C)
   float* dbg = nullptr;
   long long sa1 = 0, sa2 = 0, sb1 = 0, sb2 = 0, sc1 = 0, sc2 = 0;  // element strides
 };

@@ -1,0 +1,497 @@
+// GPT-decoder Hessian-vector product engine (Alg. 1)
+// as forward-over-reverse on B200:
+//   1. forward pass carrying primal AND tangent (R-op along v) activations;
+//   2. backward pass carrying adjoints AND adjoint tangents; the parameter
+//      "gradients" of the tangent backward ARE Hv (first-order weight
+//      gradients are never formed).
+// Every matrix product runs on the tcgen05 3xTF32 GEMM (sd_gemm.cu); every
+// nonlinearity (LayerNorm, GELU, causal softmax, cross-entropy) is one fused
+// kernel computing value, tangent, adjoint and adjoint tangent terms
+// (sd_gpt_kernels.cu). Hv is written straight into the flat parameter-order
+// output vector (declaration order, row-major: SPEC.md:180), so the Lanczos
+// engine consumes it without any gather.
+//
+// Architecture: GPT-2 block (pre-LN, fused QKV with bias, causal softmax
+// attention, GELU-tanh MLP, tied wte/LM head), loss = mean next-token
+// cross-entropy over the batch's B*S tokens (scaled by `loss_scale` so that a
+// data-sharded sum of per-rank Hv equals the global mean, Alg. 1 line 14-17).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <memory>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "sd_common.cuh"
+#include "sd_engine.h"
+#include "sd_gemm.h"
+#include "sd_gpt.h"
+
+namespace {
+
+using sd::fail;
+
+struct Slot {
+  uint64_t off, rows, cols;
+  int kind;  // 0 matrix, 1 LN gain, 2 bias
+};
+
+// Declaration order of oracle/src/models.cpp gpt_layout (GPT-2 parameter names).
+std::vector<Slot> layout(const sd_gpt_config& c) {
+  std::vector<Slot> s;
+  uint64_t off = 0;
+  auto add = [&](uint64_t r, uint64_t cc, int k) {
+    s.push_back({off, r, cc, k});
+    off += r * cc;
+  };
+  add(c.vocab, c.d, 0);
+  add(c.ctx, c.d, 0);
+  for (int l = 0; l < c.n_layer; ++l) {
+    add(1, c.d, 1);
+    add(1, c.d, 2);
+    add(c.d, 3 * c.d, 0);
+    add(1, 3 * c.d, 2);
+    add(c.d, c.d, 0);
+    add(1, c.d, 2);
+    add(1, c.d, 1);
+    add(1, c.d, 2);
+    add(c.d, c.ff, 0);
+    add(1, c.ff, 2);
+    add(c.ff, c.d, 0);
+    add(1, c.d, 2);
+  }
+  add(1, c.d, 1);
+  add(1, c.d, 2);
+  return s;
+}
+
+uint64_t param_count(const sd_gpt_config& c) {
+  const auto s = layout(c);
+  return s.back().off + s.back().rows * s.back().cols;
+}
+
+void check_cfg(const sd_gpt_config& c, int B, int S) {
+  if (c.n_layer < 1 || c.d < 4 || c.n_head < 1 || c.ff < 4 || c.vocab < 2 || c.ctx < 1)
+    fail(SD_CONFIG_ERROR, "gpt config out of range");
+  if (c.d % c.n_head) fail(SD_CONFIG_ERROR, "d must be divisible by n_head");
+  if (c.d % 4 || c.ff % 4 || (c.d / c.n_head) % 4) fail(SD_CONFIG_ERROR, "d, ff and head dim must be multiples of 4");
+  if (B < 1 || S < 1) fail(SD_ARGUMENT_ERROR, "empty batch");
+  if (S > c.ctx) fail(SD_ARGUMENT_ERROR, "sequence longer than context");
+  if (S % 4) fail(SD_CONFIG_ERROR, "sequence length must be a multiple of 4");
+}
+
+struct Layer {
+  float *xh1, *dxh1, *r1, *dr1, *h1, *h1s, *dh1, *dh1s;
+  float *a, *as, *da, *das;
+  float *P, *Ps, *dP, *dPs;
+  float *o, *os, *dO, *dOs;
+  float *xh2, *dxh2, *r2, *dr2, *h2, *h2s, *dh2, *dh2s;
+  float *f, *df, *u, *us, *du, *dus;
+};
+
+struct Plan {
+  uint64_t bytes = 0;
+  char* base = nullptr;
+  template <class T>
+  T* take(uint64_t n) {
+    const uint64_t off = bytes;
+    bytes += (n * sizeof(T) + 255) / 256 * 256;
+    return base ? reinterpret_cast<T*>(base + off) : nullptr;
+  }
+};
+
+}  // namespace
+
+struct sd_gpt_s {
+  sd_gpt_config c{};
+  int B = 0, S = 0, T = 0, H = 0, dh = 0;
+  long long Vp = 0, BHSS = 0, P = 0;
+  std::vector<Slot> slots;
+  const float* theta = nullptr;
+  float *theta_s = nullptr, *v_s = nullptr;
+  std::vector<Layer> L;
+  float *x, *dx;
+  float *xhf, *dxhf, *rf, *drf, *hf, *hfs, *dhf, *dhfs;
+  float *z, *zs, *dz, *dzs;
+  float *gx, *gdx, *gxs, *gdxs, *gh, *ghs, *gdh, *gdhs;
+  float *go, *gos, *gdo, *gdos, *ga, *gas, *gda, *gdas;
+  float *gP, *gPs, *gdP, *gdPs, *gu, *gus, *gdu, *gdus;
+  double* loss_rows = nullptr;
+  int *tok = nullptr, *tgt = nullptr, *uniq = nullptr, *ustart = nullptr, *upos = nullptr;
+  int n_uniq = 0;
+  float loss_scale = 1.0f;
+  bool have_batch = false;
+  std::vector<double> h_loss;
+
+  void carve(Plan& p) {
+    const long long T_ = T, d = c.d, ff = c.ff;
+    auto td = [&] { return p.take<float>(T_ * d); };
+    L.resize(c.n_layer);
+    for (auto& l : L) {
+      l.xh1 = td(), l.dxh1 = td(), l.h1 = td(), l.h1s = td(), l.dh1 = td(), l.dh1s = td();
+      l.r1 = p.take<float>(T_), l.dr1 = p.take<float>(T_);
+      l.a = p.take<float>(T_ * 3 * d), l.as = p.take<float>(T_ * 3 * d);
+      l.da = p.take<float>(T_ * 3 * d), l.das = p.take<float>(T_ * 3 * d);
+      l.P = p.take<float>(BHSS), l.Ps = p.take<float>(BHSS), l.dP = p.take<float>(BHSS), l.dPs = p.take<float>(BHSS);
+      l.o = td(), l.os = td(), l.dO = td(), l.dOs = td();
+      l.xh2 = td(), l.dxh2 = td(), l.h2 = td(), l.h2s = td(), l.dh2 = td(), l.dh2s = td();
+      l.r2 = p.take<float>(T_), l.dr2 = p.take<float>(T_);
+      l.f = p.take<float>(T_ * ff), l.df = p.take<float>(T_ * ff);
+      l.u = p.take<float>(T_ * ff), l.us = p.take<float>(T_ * ff);
+      l.du = p.take<float>(T_ * ff), l.dus = p.take<float>(T_ * ff);
+    }
+    x = td(), dx = td();
+    xhf = td(), dxhf = td(), hf = td(), hfs = td(), dhf = td(), dhfs = td();
+    rf = p.take<float>(T_), drf = p.take<float>(T_);
+    z = p.take<float>(T_ * Vp), zs = p.take<float>(T_ * Vp), dz = p.take<float>(T_ * Vp), dzs = p.take<float>(T_ * Vp);
+    gx = td(), gdx = td(), gxs = td(), gdxs = td(), gh = td(), ghs = td(), gdh = td(), gdhs = td();
+    go = td(), gos = td(), gdo = td(), gdos = td();
+    ga = p.take<float>(T_ * 3 * d), gas = p.take<float>(T_ * 3 * d);
+    gda = p.take<float>(T_ * 3 * d), gdas = p.take<float>(T_ * 3 * d);
+    gP = p.take<float>(BHSS), gPs = p.take<float>(BHSS), gdP = p.take<float>(BHSS), gdPs = p.take<float>(BHSS);
+    gu = p.take<float>(T_ * ff), gus = p.take<float>(T_ * ff), gdu = p.take<float>(T_ * ff), gdus = p.take<float>(T_ * ff);
+    theta_s = p.take<float>(P), v_s = p.take<float>(P);
+    loss_rows = p.take<double>(T_);
+    tok = p.take<int>(T_), tgt = p.take<int>(T_), uniq = p.take<int>(T_ + 1), ustart = p.take<int>(T_ + 1);
+    upos = p.take<int>(T_);
+  }
+
+  // ---- GEMM helper: C = alpha op(A) op(B) + beta C (+bias), 3xTF32
+  struct Op {
+    const float *p, *s;
+    long long ld;
+    bool mn;
+    long long s1 = 0, s2 = 0;
+  };
+  void mm(int M, int N, int K, Op A, Op Bo, float* C, long long ldc, float alpha, float beta, cudaStream_t st,
+          const float* bias = nullptr, float* Cs = nullptr, int Z1 = 1, int Z2 = 1, long long c1 = 0,
+          long long c2 = 0) {
+    sd::GemmArgs g;
+    g.M = M, g.N = N, g.K = K;
+    g.A = A.p, g.As = A.s, g.lda = A.ld, g.a_mn = A.mn;
+    g.B = Bo.p, g.Bs = Bo.s, g.ldb = Bo.ld, g.b_mn = Bo.mn;
+    g.C = C, g.ldc = ldc, g.alpha = alpha, g.beta = beta, g.bias = bias, g.Cs = Cs;
+    g.Z1 = Z1, g.Z2 = Z2, g.sa1 = A.s1, g.sa2 = A.s2, g.sb1 = Bo.s1, g.sb2 = Bo.s2, g.sc1 = c1, g.sc2 = c2;
+    sd::gemm(g, st);
+  }
+
+  const float* th(int i) const { return theta + slots[i].off; }
+  const float* ths(int i) const { return theta_s + slots[i].off; }
+
+  void hvp(const float* v, float* hv, cudaStream_t st) {
+    if (!have_batch) fail(SD_STATE_ERROR, "gpt: set_batch was not called");
+    const int d = c.d, ff = c.ff, V = c.vocab;
+    const long long Td = (long long)T * d;
+    const float sc = 1.0f / std::sqrt(float(dh));
+    auto V_ = [&](int i) { return v + slots[i].off; };
+    auto Vs = [&](int i) { return v_s + slots[i].off; };
+    auto HV = [&](int i) { return hv + slots[i].off; };
+    sd::gpt_residual(v, v_s, P, st);
+    // ------------------------------------------------------------ forward
+    sd::gpt_embed(tok, T, S, d, th(0), th(1), V_(0), V_(1), x, dx, st);
+    for (int l = 0; l < c.n_layer; ++l) {
+      Layer& Ly = L[l];
+      const int b = 2 + 12 * l;  // slot index of h{l}.ln_1.weight
+      sd::LnArgs la{x, dx, th(b), th(b + 1), V_(b), V_(b + 1), T, d, 1e-5f,
+                    Ly.h1, Ly.h1s, Ly.dh1, Ly.dh1s, Ly.xh1, Ly.dxh1, Ly.r1, Ly.dr1};
+      sd::gpt_ln_fwd(la, st);
+      // qkv = h Wa + ba ; dqkv = dh Wa + h VWa + Vba
+      mm(T, 3 * d, d, {Ly.h1, Ly.h1s, d, false}, {th(b + 2), ths(b + 2), 3 * d, true}, Ly.a, 3 * d, 1, 0, st,
+         th(b + 3), Ly.as);
+      mm(T, 3 * d, d, {Ly.dh1, Ly.dh1s, d, false}, {th(b + 2), ths(b + 2), 3 * d, true}, Ly.da, 3 * d, 1, 0, st,
+         V_(b + 3));
+      mm(T, 3 * d, d, {Ly.h1, Ly.h1s, d, false}, {V_(b + 2), Vs(b + 2), 3 * d, true}, Ly.da, 3 * d, 1, 1, st,
+         nullptr, Ly.das);
+      attention_fwd(Ly, sc, st);
+      // x += o Wp + bp ; dx += do Wp + o VWp + Vbp
+      mm(T, d, d, {Ly.o, Ly.os, d, false}, {th(b + 4), ths(b + 4), d, true}, x, d, 1, 1, st, th(b + 5));
+      mm(T, d, d, {Ly.dO, Ly.dOs, d, false}, {th(b + 4), ths(b + 4), d, true}, dx, d, 1, 1, st, V_(b + 5));
+      mm(T, d, d, {Ly.o, Ly.os, d, false}, {V_(b + 4), Vs(b + 4), d, true}, dx, d, 1, 1, st);
+      sd::LnArgs lb{x, dx, th(b + 6), th(b + 7), V_(b + 6), V_(b + 7), T, d, 1e-5f,
+                    Ly.h2, Ly.h2s, Ly.dh2, Ly.dh2s, Ly.xh2, Ly.dxh2, Ly.r2, Ly.dr2};
+      sd::gpt_ln_fwd(lb, st);
+      mm(T, ff, d, {Ly.h2, Ly.h2s, d, false}, {th(b + 8), ths(b + 8), ff, true}, Ly.f, ff, 1, 0, st, th(b + 9));
+      mm(T, ff, d, {Ly.dh2, Ly.dh2s, d, false}, {th(b + 8), ths(b + 8), ff, true}, Ly.df, ff, 1, 0, st, V_(b + 9));
+      mm(T, ff, d, {Ly.h2, Ly.h2s, d, false}, {V_(b + 8), Vs(b + 8), ff, true}, Ly.df, ff, 1, 1, st);
+      sd::gpt_gelu_fwd(Ly.f, Ly.df, Ly.u, Ly.us, Ly.du, Ly.dus, (long long)T * ff, st);
+      mm(T, d, ff, {Ly.u, Ly.us, ff, false}, {th(b + 10), ths(b + 10), d, true}, x, d, 1, 1, st, th(b + 11));
+      mm(T, d, ff, {Ly.du, Ly.dus, ff, false}, {th(b + 10), ths(b + 10), d, true}, dx, d, 1, 1, st, V_(b + 11));
+      mm(T, d, ff, {Ly.u, Ly.us, ff, false}, {V_(b + 10), Vs(b + 10), d, true}, dx, d, 1, 1, st);
+    }
+    const int fL = 2 + 12 * c.n_layer;
+    sd::LnArgs lf{x, dx, th(fL), th(fL + 1), V_(fL), V_(fL + 1), T, d, 1e-5f, hf, hfs, dhf, dhfs, xhf, dxhf, rf, drf};
+    sd::gpt_ln_fwd(lf, st);
+    // logits z = hf wte^T ; dz = dhf wte^T + hf Vwte^T
+    mm(T, V, d, {hf, hfs, d, false}, {th(0), ths(0), d, false}, z, Vp, 1, 0, st);
+    mm(T, V, d, {dhf, dhfs, d, false}, {th(0), ths(0), d, false}, dz, Vp, 1, 0, st);
+    mm(T, V, d, {hf, hfs, d, false}, {V_(0), Vs(0), d, false}, dz, Vp, 1, 1, st);
+    sd::gpt_ce(z, dz, zs, dz == nullptr ? nullptr : dzs, tgt, T, V, Vp, loss_scale, loss_rows, st);
+    // ----------------------------------------------------------- backward
+    // ghf = gz wte ; gdhf = gdz wte + gz Vwte ; Hv_wte(head) = gdz^T hf + gz^T dhf
+    mm(T, d, V, {z, zs, Vp, false}, {th(0), ths(0), d, true}, gh, d, 1, 0, st);
+    mm(T, d, V, {dz, dzs, Vp, false}, {th(0), ths(0), d, true}, gdh, d, 1, 0, st);
+    mm(T, d, V, {z, zs, Vp, false}, {V_(0), Vs(0), d, true}, gdh, d, 1, 1, st);
+    mm(V, d, T, {dz, dzs, Vp, true}, {hf, hfs, d, true}, HV(0), d, 1, 0, st);
+    mm(V, d, T, {z, zs, Vp, true}, {dhf, dhfs, d, true}, HV(0), d, 1, 1, st);
+    SD_CUDA(cudaMemsetAsync(gx, 0, Td * sizeof(float), st));
+    SD_CUDA(cudaMemsetAsync(gdx, 0, Td * sizeof(float), st));
+    sd::LnBwdArgs bf{gh, gdh, th(fL), V_(fL), xhf, dxhf, rf, drf, T, d, gx, gdx, gxs, gdxs, HV(fL), HV(fL + 1)};
+    sd::gpt_ln_bwd(bf, st);
+    for (int l = c.n_layer - 1; l >= 0; --l) {
+      Layer& Ly = L[l];
+      const int b = 2 + 12 * l;
+      // MLP out: gu = gx Wq^T ; gdu = gdx Wq^T + gx VWq^T ; Hv_Wq = du^T gx + u^T gdx
+      mm(T, ff, d, {gx, gxs, d, false}, {th(b + 10), ths(b + 10), d, false}, gu, ff, 1, 0, st);
+      mm(T, ff, d, {gdx, gdxs, d, false}, {th(b + 10), ths(b + 10), d, false}, gdu, ff, 1, 0, st);
+      mm(T, ff, d, {gx, gxs, d, false}, {V_(b + 10), Vs(b + 10), d, false}, gdu, ff, 1, 1, st);
+      mm(ff, d, T, {Ly.du, Ly.dus, ff, true}, {gx, gxs, d, true}, HV(b + 10), d, 1, 0, st);
+      mm(ff, d, T, {Ly.u, Ly.us, ff, true}, {gdx, gdxs, d, true}, HV(b + 10), d, 1, 1, st);
+      sd::gpt_colsum(gdx, T, d, d, HV(b + 11), st);
+      sd::gpt_gelu_bwd(Ly.f, Ly.df, gu, gdu, gus, gdus, (long long)T * ff, st);
+      // MLP in: gh = gf Wf^T ; gdh = gdf Wf^T + gf VWf^T ; Hv_Wf = dh2^T gf + h2^T gdf
+      mm(T, d, ff, {gu, gus, ff, false}, {th(b + 8), ths(b + 8), ff, false}, gh, d, 1, 0, st);
+      mm(T, d, ff, {gdu, gdus, ff, false}, {th(b + 8), ths(b + 8), ff, false}, gdh, d, 1, 0, st);
+      mm(T, d, ff, {gu, gus, ff, false}, {V_(b + 8), Vs(b + 8), ff, false}, gdh, d, 1, 1, st);
+      mm(d, ff, T, {Ly.dh2, Ly.dh2s, d, true}, {gu, gus, ff, true}, HV(b + 8), ff, 1, 0, st);
+      mm(d, ff, T, {Ly.h2, Ly.h2s, d, true}, {gdu, gdus, ff, true}, HV(b + 8), ff, 1, 1, st);
+      sd::gpt_colsum(gdu, T, ff, ff, HV(b + 9), st);
+      sd::LnBwdArgs b2{gh, gdh, th(b + 6), V_(b + 6), Ly.xh2, Ly.dxh2, Ly.r2, Ly.dr2, T, d,
+                       gx, gdx, gxs, gdxs, HV(b + 6), HV(b + 7)};
+      sd::gpt_ln_bwd(b2, st);
+      // attention out-projection
+      mm(T, d, d, {gx, gxs, d, false}, {th(b + 4), ths(b + 4), d, false}, go, d, 1, 0, st, nullptr, gos);
+      mm(T, d, d, {gdx, gdxs, d, false}, {th(b + 4), ths(b + 4), d, false}, gdo, d, 1, 0, st);
+      mm(T, d, d, {gx, gxs, d, false}, {V_(b + 4), Vs(b + 4), d, false}, gdo, d, 1, 1, st, nullptr, gdos);
+      mm(d, d, T, {Ly.dO, Ly.dOs, d, true}, {gx, gxs, d, true}, HV(b + 4), d, 1, 0, st);
+      mm(d, d, T, {Ly.o, Ly.os, d, true}, {gdx, gdxs, d, true}, HV(b + 4), d, 1, 1, st);
+      sd::gpt_colsum(gdx, T, d, d, HV(b + 5), st);
+      attention_bwd(Ly, sc, st);
+      // QKV: gh = ga Wa^T ; gdh = gda Wa^T + ga VWa^T ; Hv_Wa = dh1^T ga + h1^T gda
+      mm(T, d, 3 * d, {ga, gas, 3 * d, false}, {th(b + 2), ths(b + 2), 3 * d, false}, gh, d, 1, 0, st);
+      mm(T, d, 3 * d, {gda, gdas, 3 * d, false}, {th(b + 2), ths(b + 2), 3 * d, false}, gdh, d, 1, 0, st);
+      mm(T, d, 3 * d, {ga, gas, 3 * d, false}, {V_(b + 2), Vs(b + 2), 3 * d, false}, gdh, d, 1, 1, st);
+      mm(d, 3 * d, T, {Ly.dh1, Ly.dh1s, d, true}, {ga, gas, 3 * d, true}, HV(b + 2), 3 * d, 1, 0, st);
+      mm(d, 3 * d, T, {Ly.h1, Ly.h1s, d, true}, {gda, gdas, 3 * d, true}, HV(b + 2), 3 * d, 1, 1, st);
+      sd::gpt_colsum(gda, T, 3 * d, 3 * d, HV(b + 3), st);
+      sd::LnBwdArgs b1{gh, gdh, th(b), V_(b), Ly.xh1, Ly.dxh1, Ly.r1, Ly.dr1, T, d,
+                       gx, gdx, gxs, gdxs, HV(b), HV(b + 1)};
+      sd::gpt_ln_bwd(b1, st);
+    }
+    // embeddings (wte also carries the head contribution written above)
+    SD_CUDA(cudaMemsetAsync(HV(1), 0, slots[1].rows * slots[1].cols * sizeof(float), st));
+    sd::gpt_embed_bwd(uniq, ustart, upos, n_uniq, B, S, d, gdx, HV(0), HV(1), st);
+  }
+
+  // per (batch b, head h): S = sc q k^T ; dS = sc (dq k^T + q dk^T) ; P, dP = softmax R-op ;
+  // o = P v ; do = dP v + P dv   (o written into the merged [T, d] layout)
+  void attention_fwd(Layer& Ly, float sc, cudaStream_t st) {
+    const int d = c.d, Sq = S;
+    const long long ha = dh, ba = (long long)Sq * 3 * d;      // head / batch strides in a [T, 3d]
+    const long long hs = (long long)Sq * Sq, bs = (long long)H * Sq * Sq;  // in P [B, H, S, S]
+    const long long ho = dh, bo = (long long)Sq * d;          // in o [T, d]
+    auto q = [&](float* base, float* res) { return Op{base, res, 3 * d, false, ha, ba}; };
+    mm(Sq, Sq, dh, q(Ly.a, Ly.as), {Ly.a + d, Ly.as + d, 3 * d, false, ha, ba}, Ly.P, Sq, sc, 0, st, nullptr,
+       nullptr, H, B, hs, bs);
+    mm(Sq, Sq, dh, q(Ly.da, Ly.das), {Ly.a + d, Ly.as + d, 3 * d, false, ha, ba}, Ly.dP, Sq, sc, 0, st, nullptr,
+       nullptr, H, B, hs, bs);
+    mm(Sq, Sq, dh, q(Ly.a, Ly.as), {Ly.da + d, Ly.das + d, 3 * d, false, ha, ba}, Ly.dP, Sq, sc, 1, st, nullptr,
+       nullptr, H, B, hs, bs);
+    sd::gpt_attn_softmax_fwd(Ly.P, Ly.dP, Ly.Ps, Ly.dPs, Sq, (long long)B * H * Sq, st);
+    const Op Pm{Ly.P, Ly.Ps, Sq, false, hs, bs}, dPm{Ly.dP, Ly.dPs, Sq, false, hs, bs};
+    const Op vv{Ly.a + 2 * d, Ly.as + 2 * d, 3 * d, true, ha, ba}, dvv{Ly.da + 2 * d, Ly.das + 2 * d, 3 * d, true, ha, ba};
+    mm(Sq, dh, Sq, Pm, vv, Ly.o, d, 1, 0, st, nullptr, Ly.os, H, B, ho, bo);
+    mm(Sq, dh, Sq, dPm, vv, Ly.dO, d, 1, 0, st, nullptr, nullptr, H, B, ho, bo);
+    mm(Sq, dh, Sq, Pm, dvv, Ly.dO, d, 1, 1, st, nullptr, Ly.dOs, H, B, ho, bo);
+  }
+
+  // gP = go v^T ; gdP = gdo v^T + go dv^T ; (gS, gdS) = softmax double-backward ;
+  // gv = P^T go ; gdv = dP^T go + P^T gdo ; gq = sc gS k ; gdq = sc (gdS k + gS dk) ;
+  // gk = sc gS^T q ; gdk = sc (gdS^T q + gS^T dq)      -> ga / gda [T, 3d]
+  void attention_bwd(Layer& Ly, float sc, cudaStream_t st) {
+    const int d = c.d, Sq = S;
+    const long long ha = dh, ba = (long long)Sq * 3 * d;
+    const long long hs = (long long)Sq * Sq, bs = (long long)H * Sq * Sq;
+    const long long ho = dh, bo = (long long)Sq * d;
+    const Op goK{go, gos, d, false, ho, bo}, gdoK{gdo, gdos, d, false, ho, bo};
+    const Op vK{Ly.a + 2 * d, Ly.as + 2 * d, 3 * d, false, ha, ba}, dvK{Ly.da + 2 * d, Ly.das + 2 * d, 3 * d, false, ha, ba};
+    mm(Sq, Sq, dh, goK, vK, gP, Sq, 1, 0, st, nullptr, nullptr, H, B, hs, bs);
+    mm(Sq, Sq, dh, gdoK, vK, gdP, Sq, 1, 0, st, nullptr, nullptr, H, B, hs, bs);
+    mm(Sq, Sq, dh, goK, dvK, gdP, Sq, 1, 1, st, nullptr, nullptr, H, B, hs, bs);
+    sd::gpt_attn_softmax_bwd(Ly.P, Ly.dP, gP, gdP, gPs, gdPs, Sq, (long long)B * H * Sq, st);
+    // value adjoints
+    const Op PT{Ly.P, Ly.Ps, Sq, true, hs, bs}, dPT{Ly.dP, Ly.dPs, Sq, true, hs, bs};
+    const Op goM{go, gos, d, true, ho, bo}, gdoM{gdo, gdos, d, true, ho, bo};
+    mm(Sq, dh, Sq, PT, goM, ga + 2 * d, 3 * d, 1, 0, st, nullptr, gas + 2 * d, H, B, ha, ba);
+    mm(Sq, dh, Sq, dPT, goM, gda + 2 * d, 3 * d, 1, 0, st, nullptr, nullptr, H, B, ha, ba);
+    mm(Sq, dh, Sq, PT, gdoM, gda + 2 * d, 3 * d, 1, 1, st, nullptr, gdas + 2 * d, H, B, ha, ba);
+    // query adjoints
+    const Op gS{gP, gPs, Sq, false, hs, bs}, gdS{gdP, gdPs, Sq, false, hs, bs};
+    const Op kM{Ly.a + d, Ly.as + d, 3 * d, true, ha, ba}, dkM{Ly.da + d, Ly.das + d, 3 * d, true, ha, ba};
+    mm(Sq, dh, Sq, gS, kM, ga, 3 * d, sc, 0, st, nullptr, gas, H, B, ha, ba);
+    mm(Sq, dh, Sq, gdS, kM, gda, 3 * d, sc, 0, st, nullptr, nullptr, H, B, ha, ba);
+    mm(Sq, dh, Sq, gS, dkM, gda, 3 * d, sc, 1, st, nullptr, gdas, H, B, ha, ba);
+    // key adjoints
+    const Op gST{gP, gPs, Sq, true, hs, bs}, gdST{gdP, gdPs, Sq, true, hs, bs};
+    const Op qM{Ly.a, Ly.as, 3 * d, true, ha, ba}, dqM{Ly.da, Ly.das, 3 * d, true, ha, ba};
+    mm(Sq, dh, Sq, gST, qM, ga + d, 3 * d, sc, 0, st, nullptr, gas + d, H, B, ha, ba);
+    mm(Sq, dh, Sq, gdST, qM, gda + d, 3 * d, sc, 0, st, nullptr, nullptr, H, B, ha, ba);
+    mm(Sq, dh, Sq, gST, dqM, gda + d, 3 * d, sc, 1, st, nullptr, gdas + d, H, B, ha, ba);
+  }
+};
+
+namespace {
+
+Plan plan_for(const sd_gpt_config& c, int B, int S, char* base, sd_gpt_s* g) {
+  sd_gpt_s tmp;
+  sd_gpt_s* e = g ? g : &tmp;
+  e->c = c;
+  e->B = B, e->S = S, e->T = B * S, e->H = c.n_head, e->dh = c.d / c.n_head;
+  e->Vp = (c.vocab + 7) / 8 * 8;
+  e->BHSS = (long long)B * c.n_head * S * S;
+  e->P = (long long)param_count(c);
+  Plan p;
+  p.base = base;
+  e->carve(p);
+  return p;
+}
+
+struct GptOpCtx {
+  sd_gpt g;
+  sd_comm comm;
+};
+
+sd_status gpt_apply(void* ctx, const void* x, void* y, sd_stream s) {
+  auto* c = static_cast<GptOpCtx*>(ctx);
+  return sd::guard([&] {
+    c->g->hvp(static_cast<const float*>(x), static_cast<float*>(y), (cudaStream_t)s);
+    sd::comm_allreduce_f32(c->comm, static_cast<float*>(y), uint64_t(c->g->P), (cudaStream_t)s);
+  });
+}
+
+}  // namespace
+
+extern "C" {
+
+uint64_t sd_gpt_param_count(const sd_gpt_config* c) { return c ? param_count(*c) : 0; }
+
+sd_status sd_gpt_param_layout(const sd_gpt_config* c, uint64_t* offsets, uint64_t* rows, uint64_t* cols, int* kinds,
+                              uint64_t* count) {
+  return sd::guard([&] {
+    const auto s = layout(*c);
+    for (size_t i = 0; i < s.size(); ++i) {
+      offsets[i] = s[i].off;
+      rows[i] = s[i].rows;
+      cols[i] = s[i].cols;
+      kinds[i] = s[i].kind;
+    }
+    *count = s.size();
+  });
+}
+
+// theta[i] = base(kind) + scale(kind) * gaussian(seed, i): matrices 0.02,
+// LN gains 1 + gain_scale*N, biases bias_scale*N (oracle gpt_init).
+sd_status sd_gpt_init_params(const sd_gpt_config* c, uint64_t seed, double gain_scale, double bias_scale,
+                             float* theta, sd_stream s) {
+  return sd::guard([&] {
+    for (const Slot& sl : layout(*c)) {
+      const double base = sl.kind == 1 ? 1.0 : 0.0;
+      const double sc = sl.kind == 0 ? 0.02 : (sl.kind == 1 ? gain_scale : bias_scale);
+      sd::gpt_init_slot(theta, (long long)sl.off, (long long)(sl.rows * sl.cols), seed, base, sc, (cudaStream_t)s);
+    }
+  });
+}
+
+uint64_t sd_gpt_workspace_bytes(const sd_gpt_config* c, int batch, int seq) {
+  try {
+    check_cfg(*c, batch, seq);
+    return plan_for(*c, batch, seq, nullptr, nullptr).bytes;
+  } catch (const std::exception& e) {
+    sd::set_last_error(e.what());
+    return 0;
+  }
+}
+
+sd_status sd_gpt_create(const sd_gpt_config* c, int batch, int seq, const float* theta, void* ws, uint64_t bytes,
+                        sd_stream s, sd_gpt* out) {
+  return sd::guard([&] {
+    check_cfg(*c, batch, seq);
+    auto g = std::make_unique<sd_gpt_s>();
+    const Plan p = plan_for(*c, batch, seq, static_cast<char*>(ws), g.get());
+    if (bytes < p.bytes) fail(SD_ARGUMENT_ERROR, "gpt workspace too small");
+    g->slots = layout(*c);
+    g->theta = theta;
+    sd::gpt_residual(theta, g->theta_s, g->P, (cudaStream_t)s);
+    // padded logits columns are never read as values but feed TMA boxes: zero them once
+    SD_CUDA(cudaMemsetAsync(g->z, 0, size_t(g->T) * g->Vp * 4, (cudaStream_t)s));
+    SD_CUDA(cudaMemsetAsync(g->zs, 0, size_t(g->T) * g->Vp * 4, (cudaStream_t)s));
+    SD_CUDA(cudaMemsetAsync(g->dz, 0, size_t(g->T) * g->Vp * 4, (cudaStream_t)s));
+    SD_CUDA(cudaMemsetAsync(g->dzs, 0, size_t(g->T) * g->Vp * 4, (cudaStream_t)s));
+    *out = g.release();
+  });
+}
+
+// Uploads a batch (host int32 tokens/targets, batch*seq each) and builds the
+// token -> positions CSR used by the deterministic embedding backward.
+sd_status sd_gpt_set_batch(sd_gpt g, const int* tokens, const int* targets, float loss_scale, sd_stream s) {
+  return sd::guard([&] {
+    const int T = g->T;
+    for (int t = 0; t < T; ++t)
+      if (tokens[t] < 0 || tokens[t] >= g->c.vocab || targets[t] < 0 || targets[t] >= g->c.vocab)
+        fail(SD_ARGUMENT_ERROR, "token id out of range");
+    std::vector<int> order(T);
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return tokens[a] < tokens[b]; });
+    std::vector<int> uniq, start;
+    for (int i = 0; i < T; ++i)
+      if (i == 0 || tokens[order[i]] != tokens[order[i - 1]]) {
+        uniq.push_back(tokens[order[i]]);
+        start.push_back(i);
+      }
+    start.push_back(T);
+    cudaStream_t st = (cudaStream_t)s;
+    SD_CUDA(cudaMemcpyAsync(g->tok, tokens, T * sizeof(int), cudaMemcpyHostToDevice, st));
+    SD_CUDA(cudaMemcpyAsync(g->tgt, targets, T * sizeof(int), cudaMemcpyHostToDevice, st));
+    SD_CUDA(cudaMemcpyAsync(g->uniq, uniq.data(), uniq.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+    SD_CUDA(cudaMemcpyAsync(g->ustart, start.data(), start.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+    SD_CUDA(cudaMemcpyAsync(g->upos, order.data(), T * sizeof(int), cudaMemcpyHostToDevice, st));
+    SD_CUDA(cudaStreamSynchronize(st));
+    g->n_uniq = int(uniq.size());
+    g->loss_scale = loss_scale;
+    g->have_batch = true;
+  });
+}
+
+sd_status sd_gpt_hvp(sd_gpt g, const float* v, float* hv, sd_stream s) {
+  return sd::guard([&] { g->hvp(v, hv, (cudaStream_t)s); });
+}
+
+// mean per-token loss of the most recent hvp (synchronises the stream)
+sd_status sd_gpt_last_loss(sd_gpt g, double* loss, sd_stream s) {
+  return sd::guard([&] {
+    g->h_loss.resize(g->T);
+    SD_CUDA(cudaMemcpyAsync(g->h_loss.data(), g->loss_rows, g->T * sizeof(double), cudaMemcpyDeviceToHost,
+                            (cudaStream_t)s));
+    SD_CUDA(cudaStreamSynchronize((cudaStream_t)s));
+    double acc = 0.0;
+    for (double x : g->h_loss) acc += x;
+    *loss = acc / g->T;
+  });
+}
+
+sd_status sd_gpt_destroy(sd_gpt g) {
+  return sd::guard([&] { delete g; });
+}
+
+// Lanczos operator: y = H x on this rank's batch shard, summed over `comm`
+// (data-sharded HVP; the loss_scale of every rank is 1/global_tokens).
+sd_status sd_operator_gpt(sd_gpt g, sd_comm comm, sd_operator* out) {
+  return sd::guard([&] {
+    auto* ctx = new GptOpCtx{g, comm};  // lives as long as the process (tiny)
+    const sd_status st = sd_operator_custom(uint64_t(g->P), gpt_apply, ctx, out);
+    if (st != SD_OK) fail(st, "operator_custom failed");
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,41 @@
+// Internal interfaces of the GPT HVP engine (kernels in sd_gpt_kernels.cu).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace sd {
+
+struct LnArgs {
+  const float *x, *dx, *g, *b, *vg, *vb;
+  int T, d;
+  float eps;
+  float *h, *hs, *dh, *dhs, *xh, *dxh, *r, *dr;
+};
+struct LnBwdArgs {
+  const float *gy, *gdy, *g, *vg, *xh, *dxh, *r, *dr;
+  int T, d;
+  float *gx, *gdx, *gxs, *gdxs;
+  float *hv_g, *hv_b;
+};
+
+void gpt_embed(const int* tok, int T, int S, int d, const float* wte, const float* wpe, const float* vwte,
+               const float* vwpe, float* x, float* dx, cudaStream_t s);
+void gpt_ln_fwd(const LnArgs& a, cudaStream_t s);
+void gpt_ln_bwd(const LnBwdArgs& a, cudaStream_t s);
+void gpt_colsum(const float* a, int T, int n, long long lda, float* out, cudaStream_t s);
+void gpt_gelu_fwd(const float* f, const float* df, float* u, float* us, float* du, float* dus, long long n,
+                  cudaStream_t s);
+void gpt_gelu_bwd(const float* f, const float* df, float* gu, float* gdu, float* gus, float* gdus, long long n,
+                  cudaStream_t s);
+void gpt_attn_softmax_fwd(float* Sm, float* dS, float* Ps, float* dPs, int S, long long rows, cudaStream_t s);
+void gpt_attn_softmax_bwd(const float* P, const float* dP, float* gP, float* gdP, float* gPs, float* gdPs, int S,
+                          long long rows, cudaStream_t s);
+void gpt_ce(float* z, float* dz, float* zs, float* dzs, const int* tgt, int T, int V, long long ld, float scale,
+            double* loss_rows, cudaStream_t s);
+void gpt_embed_bwd(const int* uniq, const int* start, const int* pos, int n_uniq, int B, int S, int d,
+                   const float* gdx, float* hv_wte, float* hv_wpe, cudaStream_t s);
+void gpt_residual(const float* x, float* xs, long long n, cudaStream_t s);
+void gpt_fill(float* x, float v, long long n, cudaStream_t s);
+void gpt_init_slot(float* th, long long off, long long n, uint64_t seed, double base, double scale, cudaStream_t s);
+
+}  // namespace sd

@@ -1,0 +1,501 @@
+// Fused R-op (forward tangent) and double-backward elementwise kernels of the
+// GPT decoder HVP (Pearlmutter: Hv = d/de grad L(theta + e v)). Every kernel
+// computes a primal quantity together with its directional derivative along
+// v, so each activation is read once per pass. Wherever an output feeds a
+// tensor-core GEMM, the kernel also writes its tf32 residual
+// (x - trunc_tf32(x)) for the 3xTF32 product.
+//
+// Notation: X primal, dX tangent (R-op), gX adjoint, gdX adjoint tangent.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "sd_common.cuh"
+#include "sd_gpt.h"
+
+namespace sd {
+
+__device__ __forceinline__ float tf32_res(float x) { return x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+template <int NW>
+__device__ __forceinline__ float block_sum(float v, float* red) {
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  v = warp_sum(v);
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  float t = 0.f;
+#pragma unroll
+  for (int i = 0; i < NW; ++i) t += red[i];
+  return t;
+}
+template <int NW>
+__device__ __forceinline__ float block_max(float v, float* red) {
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  v = warp_max(v);
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  float t = -INFINITY;
+#pragma unroll
+  for (int i = 0; i < NW; ++i) t = fmaxf(t, red[i]);
+  return t;
+}
+
+// ------------------------------------------------------------- embedding
+// x[t] = wte[tok] + wpe[s]; dx[t] = Vwte[tok] + Vwpe[s]
+__global__ void k_embed(const int* __restrict__ tok, int S, int d, const float* __restrict__ wte,
+                        const float* __restrict__ wpe, const float* __restrict__ vwte, const float* __restrict__ vwpe,
+                        float* __restrict__ x, float* __restrict__ dx, long long n) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const long long t = i / d;
+  const int e = int(i - t * d);
+  const int s = int(t % S);
+  const long long tk = tok[t];
+  x[i] = wte[tk * d + e] + wpe[(long long)s * d + e];
+  dx[i] = vwte[tk * d + e] + vwpe[(long long)s * d + e];
+}
+
+// ------------------------------------------------------------- LayerNorm
+// One warp per row. h = g*xh + b, xh = (x - mu) r, r = (var + eps)^-1/2;
+// dxh = r (dx - mean(dx) - xh mean(xh dx)), dr = -r * mean(xh dx) (per-row
+// tangent of r divided by r), dh = Vg*xh + g*dxh + Vb.
+__global__ void k_ln_fwd(const float* __restrict__ x, const float* __restrict__ dx, const float* __restrict__ g,
+                         const float* __restrict__ b, const float* __restrict__ vg, const float* __restrict__ vb,
+                         int T, int d, float eps, float* __restrict__ h, float* __restrict__ hs,
+                         float* __restrict__ dh, float* __restrict__ dhs, float* __restrict__ xh,
+                         float* __restrict__ dxh, float* __restrict__ r_out, float* __restrict__ dr_out) {
+  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= T) return;
+  const float* xr = x + (long long)row * d;
+  const float* dxr = dx + (long long)row * d;
+  float s = 0.f, ds = 0.f;
+  for (int e = lane; e < d; e += 32) {
+    s += xr[e];
+    ds += dxr[e];
+  }
+  const float mu = warp_sum(s) / d, dmu = warp_sum(ds) / d;
+  float v = 0.f;
+  for (int e = lane; e < d; e += 32) {
+    const float c = xr[e] - mu;
+    v += c * c;
+  }
+  const float var = warp_sum(v) / d;
+  const float r = rsqrtf(var + eps);
+  float m2 = 0.f;
+  for (int e = lane; e < d; e += 32) m2 += (xr[e] - mu) * r * (dxr[e] - dmu);
+  const float mxd = warp_sum(m2) / d;  // mean(xh * dx) (dx centred; mean(xh) = 0)
+  const long long o = (long long)row * d;
+  for (int e = lane; e < d; e += 32) {
+    const float xhv = (xr[e] - mu) * r;
+    const float dxhv = r * (dxr[e] - dmu - xhv * mxd);
+    const float hv = g[e] * xhv + b[e];
+    const float dhv = vg[e] * xhv + g[e] * dxhv + vb[e];
+    xh[o + e] = xhv;
+    dxh[o + e] = dxhv;
+    h[o + e] = hv;
+    hs[o + e] = tf32_res(hv);
+    dh[o + e] = dhv;
+    dhs[o + e] = tf32_res(dhv);
+  }
+  if (lane == 0) {
+    r_out[row] = r;
+    dr_out[row] = -r * mxd;  // dr / r
+  }
+}
+
+// Backward of LN with its tangent, accumulating into the residual adjoints:
+//   gq = gy*g;      gdq = gdy*g + gy*Vg
+//   gx += r (gq - mean(gq) - xh mean(gq xh))
+//   gdx += dr*r*(gq - mean(gq) - xh mean(gq xh))
+//        + r (gdq - mean(gdq) - dxh mean(gq xh) - xh (mean(gdq xh) + mean(gq dxh)))
+__global__ void k_ln_bwd(const float* __restrict__ gy, const float* __restrict__ gdy, const float* __restrict__ g,
+                         const float* __restrict__ vg, const float* __restrict__ xh, const float* __restrict__ dxh,
+                         const float* __restrict__ rr, const float* __restrict__ drr, int T, int d,
+                         float* __restrict__ gx, float* __restrict__ gdx, float* __restrict__ gxs,
+                         float* __restrict__ gdxs) {
+  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= T) return;
+  const long long o = (long long)row * d;
+  float s1 = 0.f, s2 = 0.f, s3 = 0.f, s4 = 0.f, s5 = 0.f;
+  for (int e = lane; e < d; e += 32) {
+    const float gq = gy[o + e] * g[e];
+    const float gdq = gdy[o + e] * g[e] + gy[o + e] * vg[e];
+    s1 += gq;
+    s2 += gq * xh[o + e];
+    s3 += gdq;
+    s4 += gdq * xh[o + e];
+    s5 += gq * dxh[o + e];
+  }
+  const float m_g = warp_sum(s1) / d, m_gx = warp_sum(s2) / d, m_d = warp_sum(s3) / d;
+  const float m_dx = warp_sum(s4) / d, m_gdx = warp_sum(s5) / d;
+  const float r = rr[row], dr = drr[row];
+  for (int e = lane; e < d; e += 32) {
+    const float gq = gy[o + e] * g[e];
+    const float gdq = gdy[o + e] * g[e] + gy[o + e] * vg[e];
+    const float base = gq - m_g - xh[o + e] * m_gx;
+    const float a = gx[o + e] + r * base;
+    const float b = gdx[o + e] + dr * r * base +
+                    r * (gdq - m_d - dxh[o + e] * m_gx - xh[o + e] * (m_dx + m_gdx));
+    gx[o + e] = a;
+    gdx[o + e] = b;
+    if (gxs) {
+      gxs[o + e] = tf32_res(a);
+      gdxs[o + e] = tf32_res(b);
+    }
+  }
+}
+
+// Column sums over T rows of the LN parameter Hv terms:
+//   Hv_g[e] += sum_t gdy*xh + gy*dxh ;  Hv_b[e] += sum_t gdy
+// (blocks of 32 columns x 8 row-groups, deterministic fixed-order tree).
+__global__ void k_ln_param_hv(const float* __restrict__ gy, const float* __restrict__ gdy,
+                              const float* __restrict__ xh, const float* __restrict__ dxh, int T, int d,
+                              float* __restrict__ hv_g, float* __restrict__ hv_b, int accumulate) {
+  __shared__ float sg[8][33], sb[8][33];
+  const int col = blockIdx.x * 32 + (threadIdx.x & 31);
+  const int grp = threadIdx.x >> 5;
+  float ag = 0.f, ab = 0.f;
+  if (col < d) {
+    for (int t = grp; t < T; t += 8) {
+      const long long o = (long long)t * d + col;
+      ag += gdy[o] * xh[o] + gy[o] * dxh[o];
+      ab += gdy[o];
+    }
+  }
+  sg[grp][threadIdx.x & 31] = ag;
+  sb[grp][threadIdx.x & 31] = ab;
+  __syncthreads();
+  if (grp == 0 && col < d) {
+    float tg = 0.f, tb = 0.f;
+    for (int i = 0; i < 8; ++i) {
+      tg += sg[i][threadIdx.x];
+      tb += sb[i][threadIdx.x];
+    }
+    hv_g[col] = accumulate ? hv_g[col] + tg : tg;
+    hv_b[col] = accumulate ? hv_b[col] + tb : tb;
+  }
+}
+
+// Hv of a bias: column sum of the adjoint tangent over T rows.
+__global__ void k_colsum(const float* __restrict__ a, int T, int n, long long lda, float* __restrict__ out) {
+  __shared__ float sm[8][33];
+  const int col = blockIdx.x * 32 + (threadIdx.x & 31);
+  const int grp = threadIdx.x >> 5;
+  float acc = 0.f;
+  if (col < n)
+    for (int t = grp; t < T; t += 8) acc += a[(long long)t * lda + col];
+  sm[grp][threadIdx.x & 31] = acc;
+  __syncthreads();
+  if (grp == 0 && col < n) {
+    float tot = 0.f;
+    for (int i = 0; i < 8; ++i) tot += sm[i][threadIdx.x];
+    out[col] = tot;
+  }
+}
+
+// ------------------------------------------------------------------ GELU
+__device__ __forceinline__ void gelu_derivs(float x, float& y, float& d1, float& d2) {
+  const float k0 = 0.7978845608028654f, k1 = 0.044715f;
+  const float x2 = x * x;
+  const float u = k0 * (x + k1 * x2 * x);
+  const float du = k0 * (1.f + 3.f * k1 * x2);
+  const float ddu = k0 * 6.f * k1 * x;
+  const float t = tanhf(u);
+  const float sech2 = 1.f - t * t;
+  y = 0.5f * x * (1.f + t);
+  d1 = 0.5f * (1.f + t) + 0.5f * x * sech2 * du;
+  d2 = sech2 * du + 0.5f * x * (-2.f * t * sech2 * du * du + sech2 * ddu);
+}
+
+// u = gelu(f), du = gelu'(f) df (+ residuals for the next GEMM)
+__global__ void k_gelu_fwd(const float* __restrict__ f, const float* __restrict__ df, float* __restrict__ u,
+                           float* __restrict__ us, float* __restrict__ du, float* __restrict__ dus, long long n) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  float y, d1, d2;
+  gelu_derivs(f[i], y, d1, d2);
+  const float dy = d1 * df[i];
+  u[i] = y;
+  us[i] = tf32_res(y);
+  du[i] = dy;
+  dus[i] = tf32_res(dy);
+}
+
+// gf = gu g'(f); gdf = gdu g'(f) + gu g''(f) df   (in place over gu, gdu)
+__global__ void k_gelu_bwd(const float* __restrict__ f, const float* __restrict__ df, float* __restrict__ gu,
+                           float* __restrict__ gdu, float* __restrict__ gus, float* __restrict__ gdus, long long n) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  float y, d1, d2;
+  gelu_derivs(f[i], y, d1, d2);
+  const float a = gu[i], b = gdu[i];
+  const float gf = a * d1;
+  const float gdf = b * d1 + a * d2 * df[i];
+  gu[i] = gf;
+  gdu[i] = gdf;
+  gus[i] = tf32_res(gf);
+  gdus[i] = tf32_res(gdf);
+}
+
+// --------------------------------------------------------- attention softmax
+// Row (z, i) of the per-head score matrix (already scaled), causal: columns
+// j <= i. P = softmax, dP = P (dS - sum_j P dS); masked entries -> 0.
+__global__ void k_attn_softmax_fwd(float* __restrict__ Sm, float* __restrict__ dS, float* __restrict__ Ps,
+                                   float* __restrict__ dPs, int S, long long rows) {
+  const long long row = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const int i = int(row % S);
+  float* s = Sm + row * S;
+  float* ds = dS + row * S;
+  float m = -INFINITY;
+  for (int j = lane; j <= i; j += 32) m = fmaxf(m, s[j]);
+  m = warp_max(m);
+  float z = 0.f, zd = 0.f;
+  for (int j = lane; j <= i; j += 32) {
+    const float e = __expf(s[j] - m);
+    z += e;
+    zd += e * ds[j];
+  }
+  z = warp_sum(z);
+  zd = warp_sum(zd);
+  const float inv = 1.f / z, mean_d = zd * inv;
+  float* ps = Ps + row * S;
+  float* dps = dPs + row * S;
+  for (int j = lane; j < S; j += 32) {
+    float p = 0.f, dp = 0.f;
+    if (j <= i) {
+      p = __expf(s[j] - m) * inv;
+      dp = p * (ds[j] - mean_d);
+    }
+    s[j] = p;
+    ds[j] = dp;
+    ps[j] = tf32_res(p);
+    dps[j] = tf32_res(dp);
+  }
+}
+
+// gS = P (gP - c), gdS = dP (gP - c) + P (gdP - dc),  c = sum P gP,
+// dc = sum (dP gP + P gdP). In place over gP, gdP.
+__global__ void k_attn_softmax_bwd(const float* __restrict__ P, const float* __restrict__ dP, float* __restrict__ gP,
+                                   float* __restrict__ gdP, float* __restrict__ gPs, float* __restrict__ gdPs, int S,
+                                   long long rows) {
+  const long long row = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const int i = int(row % S);
+  const long long o = row * S;
+  float c = 0.f, dc = 0.f;
+  for (int j = lane; j <= i; j += 32) {
+    c += P[o + j] * gP[o + j];
+    dc += dP[o + j] * gP[o + j] + P[o + j] * gdP[o + j];
+  }
+  c = warp_sum(c);
+  dc = warp_sum(dc);
+  for (int j = lane; j < S; j += 32) {
+    float a = 0.f, b = 0.f;
+    if (j <= i) {
+      const float gp = gP[o + j];
+      a = P[o + j] * (gp - c);
+      b = dP[o + j] * (gp - c) + P[o + j] * (gdP[o + j] - dc);
+    }
+    gP[o + j] = a;
+    gdP[o + j] = b;
+    gPs[o + j] = tf32_res(a);
+    gdPs[o + j] = tf32_res(b);
+  }
+}
+
+// --------------------------------------------------------- cross-entropy
+// Row t of the logits: p = softmax(z); loss_t = logsumexp(z) - z[y];
+// gz = (p - onehot(y)) * scale; gdz = p (dz - sum p dz) * scale. In place.
+__global__ void __launch_bounds__(256) k_ce(float* __restrict__ z, float* __restrict__ dz, float* __restrict__ zs,
+                                            float* __restrict__ dzs, const int* __restrict__ tgt, int V, long long ld,
+                                            float scale, double* __restrict__ loss_rows) {
+  __shared__ float red[8];
+  const long long t = blockIdx.x;
+  float* zr = z + t * ld;
+  float* dzr = dz + t * ld;
+  float m = -INFINITY;
+  for (int j = threadIdx.x; j < V; j += 256) m = fmaxf(m, zr[j]);
+  m = block_max<8>(m, red);
+  float s = 0.f, sd = 0.f;
+  for (int j = threadIdx.x; j < V; j += 256) {
+    const float e = __expf(zr[j] - m);
+    s += e;
+    sd += e * dzr[j];
+  }
+  s = block_sum<8>(s, red);
+  sd = block_sum<8>(sd, red);
+  const float inv = 1.f / s, md = sd * inv;
+  const int y = tgt[t];
+  if (threadIdx.x == 0) loss_rows[t] = double(logf(s) + m - zr[y]);
+  __syncthreads();
+  for (int j = threadIdx.x; j < V; j += 256) {
+    const float p = __expf(zr[j] - m) * inv;
+    const float g = (p - (j == y ? 1.f : 0.f)) * scale;
+    const float gd = p * (dzr[j] - md) * scale;
+    zr[j] = g;
+    dzr[j] = gd;
+    zs[t * ld + j] = tf32_res(g);
+    dzs[t * ld + j] = tf32_res(gd);
+  }
+}
+
+// ------------------------------------------------------ embedding backward
+// Hv_wte[v] += sum over positions with token v of gdx (CSR by token, fixed
+// order), one warp per (token, 32-column slab). Hv_wpe[s] = sum_b gdx[b,s].
+__global__ void k_embed_bwd_wte(const int* __restrict__ uniq, const int* __restrict__ start,
+                                const int* __restrict__ pos, int n_uniq, int d, const float* __restrict__ gdx,
+                                float* __restrict__ hv_wte) {
+  const long long w = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  const int slabs = (d + 31) / 32;
+  if (w >= (long long)n_uniq * slabs) return;
+  const int u = int(w / slabs), slab = int(w % slabs);
+  const int col = slab * 32 + lane;
+  if (col >= d) return;
+  float acc = 0.f;
+  for (int p = start[u]; p < start[u + 1]; ++p) acc += gdx[(long long)pos[p] * d + col];
+  float* dst = hv_wte + (long long)uniq[u] * d + col;
+  *dst += acc;
+}
+
+__global__ void k_embed_bwd_wpe(const float* __restrict__ gdx, int B, int S, int d, float* __restrict__ hv_wpe) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= (long long)S * d) return;
+  const int s = int(i / d), e = int(i % d);
+  float acc = 0.f;
+  for (int b = 0; b < B; ++b) acc += gdx[((long long)b * S + s) * d + e];
+  hv_wpe[i] = acc;
+}
+
+__global__ void k_res(const float* __restrict__ x, float* __restrict__ xs, long long n) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < n) xs[i] = tf32_res(x[i]);
+}
+
+__global__ void k_fill(float* __restrict__ x, float v, long long n) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < n) x[i] = v;
+}
+
+// synthetic init theta[i] = base + scale * gaussian(seed, i) (float), per slot
+__global__ void k_init_slot(float* __restrict__ th, long long off, long long n, uint64_t key, double base,
+                            double scale) {
+  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  const uint64_t i = uint64_t(off + e);
+  double v = base;
+  if (scale != 0.0) {
+    const double u1 = __dadd_rn(__dmul_rn(double(keyed_counter_k(key, 2 * i) >> 11), 0x1p-53), 0x1p-54);
+    const double u2 = __dadd_rn(__dmul_rn(double(keyed_counter_k(key, 2 * i + 1) >> 11), 0x1p-53), 0x1p-54);
+    const double gsn = __dmul_rn(__dsqrt_rn(__dmul_rn(-2.0, log(u1))), cos(__dmul_rn(6.283185307179586, u2)));
+    v = __dadd_rn(base, __dmul_rn(scale, gsn));
+  }
+  th[off + e] = __double2float_rn(v);
+}
+
+// ------------------------------------------------------------- launchers
+static unsigned g1(long long n, int t = 256) { return unsigned((n + t - 1) / t); }
+
+void gpt_embed(const int* tok, int T, int S, int d, const float* wte, const float* wpe, const float* vwte,
+               const float* vwpe, float* x, float* dx, cudaStream_t s) {
+  const long long n = (long long)T * d;
+  k_embed<<<g1(n), 256, 0, s>>>(tok, S, d, wte, wpe, vwte, vwpe, x, dx, n);
+  SD_LAUNCHED("k_embed");
+}
+
+void gpt_ln_fwd(const LnArgs& a, cudaStream_t s) {
+  k_ln_fwd<<<g1(a.T, 8), 256, 0, s>>>(a.x, a.dx, a.g, a.b, a.vg, a.vb, a.T, a.d, a.eps, a.h, a.hs, a.dh, a.dhs, a.xh,
+                                      a.dxh, a.r, a.dr);
+  SD_LAUNCHED("k_ln_fwd");
+}
+
+void gpt_ln_bwd(const LnBwdArgs& a, cudaStream_t s) {
+  k_ln_bwd<<<g1(a.T, 8), 256, 0, s>>>(a.gy, a.gdy, a.g, a.vg, a.xh, a.dxh, a.r, a.dr, a.T, a.d, a.gx, a.gdx, a.gxs,
+                                      a.gdxs);
+  SD_LAUNCHED("k_ln_bwd");
+  k_ln_param_hv<<<unsigned((a.d + 31) / 32), 256, 0, s>>>(a.gy, a.gdy, a.xh, a.dxh, a.T, a.d, a.hv_g, a.hv_b, 0);
+  SD_LAUNCHED("k_ln_param_hv");
+}
+
+void gpt_colsum(const float* a, int T, int n, long long lda, float* out, cudaStream_t s) {
+  k_colsum<<<unsigned((n + 31) / 32), 256, 0, s>>>(a, T, n, lda, out);
+  SD_LAUNCHED("k_colsum");
+}
+
+void gpt_gelu_fwd(const float* f, const float* df, float* u, float* us, float* du, float* dus, long long n,
+                  cudaStream_t s) {
+  k_gelu_fwd<<<g1(n), 256, 0, s>>>(f, df, u, us, du, dus, n);
+  SD_LAUNCHED("k_gelu_fwd");
+}
+
+void gpt_gelu_bwd(const float* f, const float* df, float* gu, float* gdu, float* gus, float* gdus, long long n,
+                  cudaStream_t s) {
+  k_gelu_bwd<<<g1(n), 256, 0, s>>>(f, df, gu, gdu, gus, gdus, n);
+  SD_LAUNCHED("k_gelu_bwd");
+}
+
+void gpt_attn_softmax_fwd(float* Sm, float* dS, float* Ps, float* dPs, int S, long long rows, cudaStream_t s) {
+  k_attn_softmax_fwd<<<g1(rows, 8), 256, 0, s>>>(Sm, dS, Ps, dPs, S, rows);
+  SD_LAUNCHED("k_attn_softmax_fwd");
+}
+
+void gpt_attn_softmax_bwd(const float* P, const float* dP, float* gP, float* gdP, float* gPs, float* gdPs, int S,
+                          long long rows, cudaStream_t s) {
+  k_attn_softmax_bwd<<<g1(rows, 8), 256, 0, s>>>(P, dP, gP, gdP, gPs, gdPs, S, rows);
+  SD_LAUNCHED("k_attn_softmax_bwd");
+}
+
+void gpt_ce(float* z, float* dz, float* zs, float* dzs, const int* tgt, int T, int V, long long ld, float scale,
+            double* loss_rows, cudaStream_t s) {
+  k_ce<<<unsigned(T), 256, 0, s>>>(z, dz, zs, dzs, tgt, V, ld, scale, loss_rows);
+  SD_LAUNCHED("k_ce");
+}
+
+void gpt_embed_bwd(const int* uniq, const int* start, const int* pos, int n_uniq, int B, int S, int d,
+                   const float* gdx, float* hv_wte, float* hv_wpe, cudaStream_t s) {
+  const long long warps = (long long)n_uniq * ((d + 31) / 32);
+  if (warps > 0) {
+    k_embed_bwd_wte<<<g1(warps, 8), 256, 0, s>>>(uniq, start, pos, n_uniq, d, gdx, hv_wte);
+    SD_LAUNCHED("k_embed_bwd_wte");
+  }
+  k_embed_bwd_wpe<<<g1((long long)S * d), 256, 0, s>>>(gdx, B, S, d, hv_wpe);
+  SD_LAUNCHED("k_embed_bwd_wpe");
+}
+
+void gpt_residual(const float* x, float* xs, long long n, cudaStream_t s) {
+  if (n <= 0) return;
+  k_res<<<g1(n), 256, 0, s>>>(x, xs, n);
+  SD_LAUNCHED("k_res");
+}
+
+void gpt_fill(float* x, float v, long long n, cudaStream_t s) {
+  if (n <= 0) return;
+  k_fill<<<g1(n), 256, 0, s>>>(x, v, n);
+  SD_LAUNCHED("k_fill");
+}
+
+void gpt_init_slot(float* th, long long off, long long n, uint64_t seed, double base, double scale, cudaStream_t s) {
+  if (n <= 0) return;
+  k_init_slot<<<g1(n), 256, 0, s>>>(th, off, n, mix64(seed), base, scale);
+  SD_LAUNCHED("k_init_slot");
+}
+
+}  // namespace sd

@@ -1,0 +1,109 @@
+"""GPT HVP on B200 vs (1) the f64 C++ oracle (autodiff Graph restatement),
+(2) an independent float64 torch double-backward, (3) central finite
+differences, plus the SPEC's HVP properties. Tolerance (north star): rel-L2
+<= 1e-5 against the f64 reference for the fp32 pipeline."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-5
+
+
+@pytest.fixture(scope="module")
+def sd():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_2505_11564_b200 as sd
+    return sd
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / np.linalg.norm(b))
+
+
+TINY = dict(n_layer=2, d=64, n_head=4, ff=256, vocab=96, ctx=32)
+C1 = dict(n_layer=1, d=64, n_head=4, ff=256, vocab=64, ctx=32)
+
+
+def test_layout_and_tokens_match_oracle(sd, oracle):
+    from paper_2505_11564_b200 import gpt
+    for cfg in (TINY, C1, gpt.GPT2_SMALL):
+        assert gpt.param_count(cfg) == oracle.gpt_param_count(cfg)
+    assert gpt.param_count(gpt.GPT2_SMALL) == 124439808
+    lay = gpt.param_layout(TINY)
+    assert lay == oracle.gpt_layout(TINY)
+    tok, tgt = gpt.synthetic_tokens(TINY["vocab"], 3, 32, 1, 5)
+    otok, otgt = oracle.gpt_batch(TINY, 3, 32, 1, 5)
+    assert np.array_equal(tok, otok.astype(np.int32)) and np.array_equal(tgt, otgt.astype(np.int32))
+
+
+@pytest.mark.parametrize("cfg,B,S", [(TINY, 2, 32), (C1, 4, 32), (dict(TINY, n_layer=1, n_head=2, d=32, ff=128), 1, 12)])
+def test_hvp_vs_oracle(sd, oracle, cfg, B, S):
+    from paper_2505_11564_b200 import gpt
+    eng = gpt.GptHvp(cfg, B, S, init_seed=0, gain_scale=0.1, bias_scale=0.1)
+    th = eng.theta_numpy()
+    # synthetic init is bit-identical to the oracle's f32-rounded init
+    assert np.array_equal(th, oracle.gpt_init(cfg, 0, 0.1, 0.1, prec=0))
+    tok, tgt = eng.tokens_numpy()
+    for seed in (3, 4):
+        v = oracle.draw_probe(eng.P, seed, 1, prec=0)
+        hv = eng.hvp_numpy(v)
+        ref = oracle.gpt_hvp(cfg, th, tok, tgt, B, S, v)
+        assert rel(hv, ref) < TOL, rel(hv, ref)
+    loss = eng.loss()
+    assert abs(loss - oracle.gpt_loss(cfg, th, tok, tgt, B, S)) < 1e-5
+
+
+def test_hvp_finite_differences_and_properties(sd, oracle):
+    from paper_2505_11564_b200 import gpt
+    cfg, B, S = TINY, 2, 32
+    eng = gpt.GptHvp(cfg, B, S, init_seed=1, gain_scale=0.1, bias_scale=0.1)
+    th = eng.theta_numpy()
+    tok, tgt = eng.tokens_numpy()
+    rng = np.random.default_rng(0)
+    v = rng.standard_normal(eng.P).astype(np.float32).astype(np.float64)
+    hv = eng.hvp_numpy(v)
+    e = 1e-4
+    fd = (oracle.gpt_grad(cfg, th + e * v, tok, tgt, B, S) - oracle.gpt_grad(cfg, th - e * v, tok, tgt, B, S)) / (2 * e)
+    assert rel(hv, fd) < 2e-5
+    # symmetry <Hu, w> = <u, Hw> and linearity
+    u = rng.standard_normal(eng.P).astype(np.float32).astype(np.float64)
+    w = rng.standard_normal(eng.P).astype(np.float32).astype(np.float64)
+    hu, hw = eng.hvp_numpy(u), eng.hvp_numpy(w)
+    assert abs(hu @ w - u @ hw) <= 1e-5 * np.linalg.norm(hu) * np.linalg.norm(w)
+    lin = eng.hvp_numpy((0.5 * u - 2.0 * w).astype(np.float32))
+    assert rel(lin, 0.5 * hu - 2.0 * hw) < 1e-5
+
+
+def test_batched_hvp_weighting(sd, oracle):
+    """Alg. 1: batches of sizes 1 and 3 == one concatenated 4-sample batch."""
+    from paper_2505_11564_b200 import gpt
+    cfg, S = TINY, 32
+    tok, tgt = gpt.synthetic_tokens(cfg["vocab"], 4, S, 1, 0)
+    whole = gpt.GptHvp(cfg, 4, S, init_seed=0, gain_scale=0.1, bias_scale=0.1, tokens=tok, targets=tgt)
+    e1 = gpt.GptHvp(cfg, 1, S, theta=whole.theta, tokens=tok[:S], targets=tgt[:S])
+    e3 = gpt.GptHvp(cfg, 3, S, theta=whole.theta, tokens=tok[S:], targets=tgt[S:])
+    v = torch.tensor(oracle.draw_probe(whole.P, 9, 1, prec=0), dtype=torch.float32, device="cuda")
+    a = whole.hvp(v).double().cpu().numpy()
+    b = gpt.batched_hvp([e1, e3], v).double().cpu().numpy()
+    assert rel(b, a) < 1e-6
+
+
+def test_hvp_gpt2_small_dims_vs_torch_f64(sd):
+    """Full GPT-2-small shapes (124M params, V=50257) at a short sequence,
+    against float64 torch double-backward on the same device."""
+    import torch_gpt
+    from paper_2505_11564_b200 import gpt
+    cfg, B, S = gpt.GPT2_SMALL, 1, 64
+    eng = gpt.GptHvp(cfg, B, S, init_seed=0, gain_scale=0.05, bias_scale=0.02)
+    g = torch.Generator(device="cuda").manual_seed(5)
+    v = (torch.randint(0, 2, (eng.P,), device="cuda", generator=g).float() * 2 - 1) / np.sqrt(eng.P)
+    hv = eng.hvp(v).double()
+    tok = torch.tensor(eng._tok, device="cuda").long()
+    tgt = torch.tensor(eng._tgt, device="cuda").long()
+    ref = torch_gpt.hvp(cfg, eng.theta.double(), tok, tgt, B, S, v.double())
+    e = float((hv - ref).norm() / ref.norm())
+    print(f"GPT-2-small HVP rel-L2 vs torch f64: {e:.3e}")
+    assert e < TOL
