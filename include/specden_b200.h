@@ -48,6 +48,8 @@ enum { SD_REORTH_NONE = 0, SD_REORTH_FULL = 1, SD_REORTH_SELECTIVE = 2 };
 
 const char* sd_last_error(void);
 int sd_abi_version(void);
+/* number of CUDA kernels this library has launched in this process */
+uint64_t sd_launch_count(void);
 
 /* ---------------------------------------------------------------- RNG (host)
  * Replaces mix64/keyed_counter/uniform01/gaussian/rademacher/uniform_index,
@@ -164,6 +166,10 @@ sd_status sd_gemm_tf32(const sd_gemm_desc* d, sd_stream s);
 /* small[i] = x[i] - hi(x[i]); mode 0: hi = trunc_tf32 (what the MMA reads),
  * mode 1: hi = round-to-nearest-away tf32. */
 sd_status sd_split_tf32(const float* x, float* small, uint64_t n, int mode, sd_stream s);
+/* CUDA-event timing of every GEMM launch between begin and end (end syncs):
+ * summed kernel ms, algorithmic flops (2*m*n*k*batch), launch count. */
+sd_status sd_gemm_profile_begin(void);
+sd_status sd_gemm_profile_end(double* ms, double* flops, uint64_t* launches);
 
 /* ---------------------------------------------------------- GPT HVP engine
  * Hessian-vector product of a GPT-2-style decoder (pre-LN, fused QKV, causal

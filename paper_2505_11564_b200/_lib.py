@@ -75,6 +75,9 @@ APPLY_FN = C.CFUNCTYPE(i32, vp, vp, vp, vp)
 _SIGS = {
     "sd_last_error": (C.c_char_p, []),
     "sd_abi_version": (i32, []),
+    "sd_launch_count": (u64, []),
+    "sd_gemm_profile_begin": (i32, []),
+    "sd_gemm_profile_end": (i32, [dp, dp, u64p]),
     "sd_keyed_counter": (u64, [u64, u64]),
     "sd_rademacher": (C.c_double, [u64, u64]),
     "sd_uniform_index": (u64, [u64, u64, u64]),

@@ -392,7 +392,7 @@ class Lanczos:
     """Step-level handle on the device engine (sd_lanczos_begin/step/end)."""
 
     def __init__(self, op: OperatorHandle, cfg: LanczosConfig, layout: ShardLayout | None = None, comm=None,
-                 device=None):
+                 device=None, workspace: torch.Tensor | None = None):
         self.cfg = cfg
         self.total = op.dim
         self.layout = layout or ShardLayout(op.dim, ((0, op.dim),))
@@ -405,7 +405,10 @@ class Lanczos:
         if nbytes == 0:
             check(1)
         dev = device or torch.device("cuda", torch.cuda.current_device())
-        self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+        if workspace is not None and workspace.numel() >= nbytes:
+            self.workspace = workspace
+        else:
+            self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=dev)
         self.op = op
         self.h = C.c_void_p()
         check(lib().sd_lanczos_begin(op.handle, comm.handle if comm is not None else None, self._b, self._e, op.dim,
@@ -522,3 +525,30 @@ def average_spectra(runs) -> RitzSpectrum:
     w = np.concatenate([r.weights for r in runs]) / len(runs)
     o = np.argsort(v, kind="stable")
     return RitzSpectrum(v[o], w[o] / w.sum())
+
+
+# ------------------------------------------------------------- communication
+class Comm:
+    """An NCCL communicator owned by the C++ engine (one process per GPU).
+    torch.distributed is only the bootstrap: it carries the ncclUniqueId."""
+
+    def __init__(self, handle, rank: int, nranks: int):
+        self.handle, self.rank, self.nranks = handle, rank, nranks
+
+    def close(self):
+        if self.handle:
+            lib().sd_comm_destroy(self.handle)
+            self.handle = None
+
+
+def nccl_comm() -> Comm:
+    import torch.distributed as dist
+    rank, n = dist.get_rank(), dist.get_world_size()
+    uid = C.create_string_buffer(128)
+    if rank == 0:
+        check(lib().sd_nccl_unique_id(uid))
+    obj = [bytes(uid.raw) if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    h = C.c_void_p()
+    check(lib().sd_comm_nccl_create(C.create_string_buffer(obj[0], 128), n, rank, C.byref(h)))
+    return Comm(h, rank, n)

@@ -22,7 +22,10 @@ inline void cuda_check(cudaError_t e, const char* what) {
   if (e != cudaSuccess) fail(SD_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
 }
 #define SD_CUDA(call) ::sd::cuda_check((call), #call)
-#define SD_LAUNCHED(name) ::sd::cuda_check(cudaGetLastError(), name)
+// every kernel launch of the library passes through here: it is checked and
+// counted (sd_launch_count, reported as gpu_launches by bench.py)
+void count_launch();
+#define SD_LAUNCHED(name) (::sd::count_launch(), ::sd::cuda_check(cudaGetLastError(), name))
 
 void set_last_error(const std::string& m);
 

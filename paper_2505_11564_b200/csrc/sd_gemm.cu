@@ -23,6 +23,7 @@
 
 #include <cstring>
 #include <mutex>
+#include <vector>
 
 #include "sd_common.cuh"
 #include "sd_gemm.h"
@@ -392,6 +393,37 @@ void make_map(CUtensorMap* m, const float* base, long long inner, long long oute
   if (r != CUDA_SUCCESS) fail(SD_CUDA_ERROR, "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
 }
 
+// Optional per-launch CUDA-event timing of every GEMM (bench.py roofline):
+// events are recorded on the launching stream around each kernel.
+struct Prof {
+  bool on = false;
+  std::vector<cudaEvent_t> ev;
+  std::vector<double> flops;
+  size_t used = 0;
+  double pending_flops = 0;
+};
+Prof& prof() {
+  static Prof p;
+  return p;
+}
+void prof_begin(cudaStream_t s) {
+  Prof& p = prof();
+  if (!p.on) return;
+  if (p.used + 2 > p.ev.size()) {
+    const size_t n = p.ev.size();
+    p.ev.resize(n + 4096);
+    for (size_t i = n; i < p.ev.size(); ++i) SD_CUDA(cudaEventCreate(&p.ev[i]));
+  }
+  SD_CUDA(cudaEventRecord(p.ev[p.used], s));
+}
+void prof_end(cudaStream_t s, double flops) {
+  Prof& p = prof();
+  if (!p.on) return;
+  SD_CUDA(cudaEventRecord(p.ev[p.used + 1], s));
+  p.flops.push_back(flops);
+  p.used += 2;
+}
+
 template <bool A_MN, bool B_MN, bool THREE>
 void launch(const GemmArgs& g, cudaStream_t s) {
   CUtensorMap mA, mAs, mB, mBs;
@@ -420,7 +452,9 @@ void launch(const GemmArgs& g, cudaStream_t s) {
     attr_set = true;
   }
   dim3 grid((g.N + BN - 1) / BN, (g.M + BM - 1) / BM, g.Z1 * g.Z2);
+  prof_begin(s);
   kern<<<grid, NUM_THREADS, smem, s>>>(mA, mAs, mB, mBs, g.K, ep);
+  prof_end(s, 2.0 * double(g.M) * g.N * g.K * g.Z1 * g.Z2);
   SD_LAUNCHED("k_gemm_tf32");
 }
 
@@ -482,6 +516,35 @@ sd_status sd_gemm_tf32(const sd_gemm_desc* d, sd_stream s) {
     g.sc2 = d->sc2;
     g.dbg = sd_gemm_debug_buffer;
     sd::gemm(g, (cudaStream_t)s);
+  });
+}
+
+// GEMM profiling window: begin() clears; end() synchronises and returns the
+// summed kernel time (ms), algorithmic flops (2MNK per launch) and launches.
+sd_status sd_gemm_profile_begin(void) {
+  return sd::guard([] {
+    auto& p = sd::prof();
+    p.on = true;
+    p.used = 0;
+    p.flops.clear();
+  });
+}
+
+sd_status sd_gemm_profile_end(double* ms, double* flops, uint64_t* launches) {
+  return sd::guard([&] {
+    auto& p = sd::prof();
+    p.on = false;
+    double t = 0, f = 0;
+    for (size_t i = 0; i + 1 < p.used; i += 2) {
+      SD_CUDA(cudaEventSynchronize(p.ev[i + 1]));
+      float x = 0;
+      SD_CUDA(cudaEventElapsedTime(&x, p.ev[i], p.ev[i + 1]));
+      t += x;
+    }
+    for (double x : p.flops) f += x;
+    *ms = t;
+    *flops = f;
+    *launches = p.flops.size();
   });
 }
 

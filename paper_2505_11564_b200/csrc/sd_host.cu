@@ -7,6 +7,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstring>
 #include <memory>
@@ -20,6 +21,8 @@ namespace sd {
 
 static thread_local std::string g_last_error;
 void set_last_error(const std::string& m) { g_last_error = m; }
+static std::atomic<uint64_t> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 // ------------------------------------------------------------------ layout
 static void validate(uint64_t total, uint64_t n, const uint64_t* b, const uint64_t* e) {
@@ -246,6 +249,7 @@ using namespace sd;
 extern "C" {
 
 const char* sd_last_error(void) { return g_last_error.c_str(); }
+uint64_t sd_launch_count(void) { return g_launches.load(); }
 int sd_abi_version(void) { return 1; }
 
 uint64_t sd_keyed_counter(uint64_t seed, uint64_t counter) { return keyed_counter_k(mix64(seed), counter); }
