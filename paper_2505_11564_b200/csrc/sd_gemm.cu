@@ -21,6 +21,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -114,6 +115,8 @@ struct EpiParams {
   const float* bias;  // per output column, may be null
   float* Cs;          // residual output, may be null
   float* dbg;         // debug: receives smem stage 0 after the accumulator is complete
+  int zcount, kb_per;  // batch count; k-blocks per split
+  float* ws;           // split-K: raw partial tiles [split][z][M][N] (else null)
 };
 
 // Descriptor of k-step `ks` (8 tf32) of an operand tile. K-major tiles are 128
@@ -167,8 +170,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n0 = blockIdx.x * BN, m0 = blockIdx.y * BM;
-  const int z = blockIdx.z, z1 = z % ep.Z1, z2 = z / ep.Z1;
-  const int num_kb = (K + BK - 1) / BK;
+  // blockIdx.z = batch + zcount * split (split-K: each split owns kb_per k-blocks)
+  const int z = blockIdx.z % ep.zcount, split = blockIdx.z / ep.zcount;
+  const int z1 = z % ep.Z1, z2 = z / ep.Z1;
+  const int kb0 = split * ep.kb_per;
+  const int num_kb = min(ep.kb_per, (K + BK - 1) / BK - kb0);
   const int num_chunks = (num_kb + KC - 1) / KC;
 
   if (threadIdx.x == 0) {
@@ -202,7 +208,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         mbar_wait(&empty[s], ph ^ 1);
         unsigned char* st = smem + s * STAGE_BYTES;
         mbar_expect_tx(&full[s], STAGE_BYTES);
-        const int k0 = kb * BK;
+        const int k0 = (kb0 + kb) * BK;
         if (A_MN) {
           for (int c = 0; c < 4; ++c) {
             tma_load_4d(&mA, &full[s], st + c * 4096, m0 + 32 * c, k0, z1, z2);
@@ -284,7 +290,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const float* sm = reinterpret_cast<const float*>(smem);
       for (int i = threadIdx.x - 64; i < STAGE_BYTES / 4; i += 128) ep.dbg[i] = sm[i];
     }
-    if (row < ep.M) {
+    if (ep.ws && row < ep.M) {
+      // split-K partial: raw accumulator, dense [M][N] per (split, z)
+      float* prow = ep.ws + ((long long)split * ep.zcount + z) * ((long long)ep.M * ep.N) + (long long)row * ep.N + n0;
+      const int nvalid = ep.N - n0;
+#pragma unroll
+      for (int j = 0; j < BN; ++j)
+        if (j < nvalid) prow[j] = acc[j];
+    } else if (row < ep.M) {
       const long long off = z1 * ep.sc1 + z2 * ep.sc2 + (long long)row * ep.ldc + n0;
       float* crow = ep.C + off;
       float* srow = ep.Cs ? ep.Cs + off : nullptr;
@@ -393,6 +406,41 @@ void make_map(CUtensorMap* m, const float* base, long long inner, long long oute
   if (r != CUDA_SUCCESS) fail(SD_CUDA_ERROR, "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
 }
 
+constexpr int kNumSMs = 148;
+
+// C = alpha * sum_split partial[split] + beta * C + bias (fixed split order)
+__global__ void k_splitk_reduce(const float* __restrict__ ws, int splits, int zc, int Z1, int M, int N,
+                                float* __restrict__ C, long long ldc, long long sc1, long long sc2, float alpha,
+                                float beta, const float* __restrict__ bias, float* __restrict__ Cs) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long mn = (long long)M * N;
+  if (i >= (long long)zc * mn) return;
+  const int z = int(i / mn);
+  const long long rc = i - z * mn;
+  const int row = int(rc / N), col = int(rc % N);
+  float acc = 0.f;
+  for (int sp = 0; sp < splits; ++sp) acc += ws[((long long)sp * zc + z) * mn + rc];
+  float* c = C + (z % Z1) * sc1 + (z / Z1) * sc2 + (long long)row * ldc + col;
+  float r = alpha * acc;
+  if (beta != 0.0f) r += beta * *c;
+  if (bias) r += bias[col];
+  *c = r;
+  if (Cs) Cs[c - C] = r - __uint_as_float(__float_as_uint(r) & 0xFFFFE000u);
+}
+
+// Split-K scratch: one lazily grown device buffer. GEMMs of this library are
+// issued on one stream in program order, so consecutive calls never overlap.
+float* splitk_workspace(size_t floats) {
+  static float* buf = nullptr;
+  static size_t cap = 0;
+  if (floats > cap) {
+    if (buf) SD_CUDA(cudaFree(buf));
+    SD_CUDA(cudaMalloc(&buf, floats * sizeof(float)));
+    cap = floats;
+  }
+  return buf;
+}
+
 // Optional per-launch CUDA-event timing of every GEMM (bench.py roofline):
 // events are recorded on the launching stream around each kernel.
 struct Prof {
@@ -442,7 +490,19 @@ void launch(const GemmArgs& g, cudaStream_t s) {
     make_map(&mB, g.B, g.K, g.N, g.ldb, g.Z1, g.sb1, g.Z2, g.sb2, BK, BN, false);
     make_map(&mBs, THREE ? g.Bs : g.B, g.K, g.N, g.ldb, g.Z1, g.sb1, g.Z2, g.sb2, BK, BN, false);
   }
-  EpiParams ep{g.C, g.ldc, g.sc1, g.sc2, g.M, g.N, g.Z1, g.alpha, g.beta, g.bias, g.Cs, g.dbg};
+  const int zc = g.Z1 * g.Z2;
+  const int tiles = ((g.N + BN - 1) / BN) * ((g.M + BM - 1) / BM) * zc;
+  const int total_kb = (g.K + BK - 1) / BK;
+  // split-K when the output grid cannot fill the 148 SMs and K is long (the
+  // Hv weight products reduce over all T tokens): partial tiles go to a
+  // workspace and are summed in a fixed order by k_splitk_reduce.
+  int splits = 1;
+  if (tiles < kNumSMs && total_kb >= 32) splits = std::min(std::min(total_kb / 16, 16), (2 * kNumSMs + tiles - 1) / tiles);
+  const int kb_per = (total_kb + splits - 1) / splits;
+  splits = (total_kb + kb_per - 1) / kb_per;
+  float* ws = nullptr;
+  if (splits > 1) ws = splitk_workspace(size_t(splits) * zc * size_t(g.M) * g.N);
+  EpiParams ep{g.C, g.ldc, g.sc1, g.sc2, g.M, g.N, g.Z1, g.alpha, g.beta, g.bias, g.Cs, g.dbg, zc, kb_per, ws};
   constexpr int NT = THREE ? 4 : 2;
   const size_t smem = 1024 + STAGES * NT * TILE_BYTES + 256;
   auto kern = k_gemm_tf32<A_MN, B_MN, THREE>;
@@ -451,11 +511,17 @@ void launch(const GemmArgs& g, cudaStream_t s) {
     SD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     attr_set = true;
   }
-  dim3 grid((g.N + BN - 1) / BN, (g.M + BM - 1) / BM, g.Z1 * g.Z2);
+  dim3 grid((g.N + BN - 1) / BN, (g.M + BM - 1) / BM, zc * splits);
   prof_begin(s);
   kern<<<grid, NUM_THREADS, smem, s>>>(mA, mAs, mB, mBs, g.K, ep);
-  prof_end(s, 2.0 * double(g.M) * g.N * g.K * g.Z1 * g.Z2);
   SD_LAUNCHED("k_gemm_tf32");
+  if (splits > 1) {
+    const long long n = (long long)zc * g.M * g.N;
+    k_splitk_reduce<<<unsigned((n + 255) / 256), 256, 0, s>>>(ws, splits, zc, g.Z1, g.M, g.N, g.C, g.ldc, g.sc1, g.sc2,
+                                                              g.alpha, g.beta, g.bias, g.Cs);
+    SD_LAUNCHED("k_splitk_reduce");
+  }
+  prof_end(s, 2.0 * double(g.M) * g.N * g.K * g.Z1 * g.Z2);
 }
 
 }  // namespace

@@ -119,6 +119,7 @@ struct sd_gpt_s {
   float *go, *gos, *gdo, *gdos, *ga, *gas, *gda, *gdas;
   float *gP, *gPs, *gdP, *gdPs, *gu, *gus, *gdu, *gdus;
   double* loss_rows = nullptr;
+  float* red = nullptr;  // column-reduction scratch
   int *tok = nullptr, *tgt = nullptr, *uniq = nullptr, *ustart = nullptr, *upos = nullptr;
   int n_uniq = 0;
   float loss_scale = 1.0f;
@@ -154,6 +155,7 @@ struct sd_gpt_s {
     gu = p.take<float>(T_ * ff), gus = p.take<float>(T_ * ff), gdu = p.take<float>(T_ * ff), gdus = p.take<float>(T_ * ff);
     theta_s = p.take<float>(P), v_s = p.take<float>(P);
     loss_rows = p.take<double>(T_);
+    red = p.take<float>(2LL * 64 * std::max(3 * d, ff));
     tok = p.take<int>(T_), tgt = p.take<int>(T_), uniq = p.take<int>(T_ + 1), ustart = p.take<int>(T_ + 1);
     upos = p.take<int>(T_);
   }
@@ -237,7 +239,7 @@ struct sd_gpt_s {
     mm(V, d, T, {z, zs, Vp, true}, {dhf, dhfs, d, true}, HV(0), d, 1, 1, st);
     SD_CUDA(cudaMemsetAsync(gx, 0, Td * sizeof(float), st));
     SD_CUDA(cudaMemsetAsync(gdx, 0, Td * sizeof(float), st));
-    sd::LnBwdArgs bf{gh, gdh, th(fL), V_(fL), xhf, dxhf, rf, drf, T, d, gx, gdx, gxs, gdxs, HV(fL), HV(fL + 1)};
+    sd::LnBwdArgs bf{gh, gdh, th(fL), V_(fL), xhf, dxhf, rf, drf, T, d, gx, gdx, gxs, gdxs, HV(fL), HV(fL + 1), red};
     sd::gpt_ln_bwd(bf, st);
     for (int l = c.n_layer - 1; l >= 0; --l) {
       Layer& Ly = L[l];
@@ -248,7 +250,7 @@ struct sd_gpt_s {
       mm(T, ff, d, {gx, gxs, d, false}, {V_(b + 10), Vs(b + 10), d, false}, gdu, ff, 1, 1, st);
       mm(ff, d, T, {Ly.du, Ly.dus, ff, true}, {gx, gxs, d, true}, HV(b + 10), d, 1, 0, st);
       mm(ff, d, T, {Ly.u, Ly.us, ff, true}, {gdx, gdxs, d, true}, HV(b + 10), d, 1, 1, st);
-      sd::gpt_colsum(gdx, T, d, d, HV(b + 11), st);
+      sd::gpt_colsum(gdx, T, d, d, HV(b + 11), red, st);
       sd::gpt_gelu_bwd(Ly.f, Ly.df, gu, gdu, gus, gdus, (long long)T * ff, st);
       // MLP in: gh = gf Wf^T ; gdh = gdf Wf^T + gf VWf^T ; Hv_Wf = dh2^T gf + h2^T gdf
       mm(T, d, ff, {gu, gus, ff, false}, {th(b + 8), ths(b + 8), ff, false}, gh, d, 1, 0, st);
@@ -256,9 +258,9 @@ struct sd_gpt_s {
       mm(T, d, ff, {gu, gus, ff, false}, {V_(b + 8), Vs(b + 8), ff, false}, gdh, d, 1, 1, st);
       mm(d, ff, T, {Ly.dh2, Ly.dh2s, d, true}, {gu, gus, ff, true}, HV(b + 8), ff, 1, 0, st);
       mm(d, ff, T, {Ly.h2, Ly.h2s, d, true}, {gdu, gdus, ff, true}, HV(b + 8), ff, 1, 1, st);
-      sd::gpt_colsum(gdu, T, ff, ff, HV(b + 9), st);
+      sd::gpt_colsum(gdu, T, ff, ff, HV(b + 9), red, st);
       sd::LnBwdArgs b2{gh, gdh, th(b + 6), V_(b + 6), Ly.xh2, Ly.dxh2, Ly.r2, Ly.dr2, T, d,
-                       gx, gdx, gxs, gdxs, HV(b + 6), HV(b + 7)};
+                       gx, gdx, gxs, gdxs, HV(b + 6), HV(b + 7), red};
       sd::gpt_ln_bwd(b2, st);
       // attention out-projection
       mm(T, d, d, {gx, gxs, d, false}, {th(b + 4), ths(b + 4), d, false}, go, d, 1, 0, st, nullptr, gos);
@@ -266,7 +268,7 @@ struct sd_gpt_s {
       mm(T, d, d, {gx, gxs, d, false}, {V_(b + 4), Vs(b + 4), d, false}, gdo, d, 1, 1, st, nullptr, gdos);
       mm(d, d, T, {Ly.dO, Ly.dOs, d, true}, {gx, gxs, d, true}, HV(b + 4), d, 1, 0, st);
       mm(d, d, T, {Ly.o, Ly.os, d, true}, {gdx, gdxs, d, true}, HV(b + 4), d, 1, 1, st);
-      sd::gpt_colsum(gdx, T, d, d, HV(b + 5), st);
+      sd::gpt_colsum(gdx, T, d, d, HV(b + 5), red, st);
       attention_bwd(Ly, sc, st);
       // QKV: gh = ga Wa^T ; gdh = gda Wa^T + ga VWa^T ; Hv_Wa = dh1^T ga + h1^T gda
       mm(T, d, 3 * d, {ga, gas, 3 * d, false}, {th(b + 2), ths(b + 2), 3 * d, false}, gh, d, 1, 0, st);
@@ -274,9 +276,9 @@ struct sd_gpt_s {
       mm(T, d, 3 * d, {ga, gas, 3 * d, false}, {V_(b + 2), Vs(b + 2), 3 * d, false}, gdh, d, 1, 1, st);
       mm(d, 3 * d, T, {Ly.dh1, Ly.dh1s, d, true}, {ga, gas, 3 * d, true}, HV(b + 2), 3 * d, 1, 0, st);
       mm(d, 3 * d, T, {Ly.h1, Ly.h1s, d, true}, {gda, gdas, 3 * d, true}, HV(b + 2), 3 * d, 1, 1, st);
-      sd::gpt_colsum(gda, T, 3 * d, 3 * d, HV(b + 3), st);
+      sd::gpt_colsum(gda, T, 3 * d, 3 * d, HV(b + 3), red, st);
       sd::LnBwdArgs b1{gh, gdh, th(b), V_(b), Ly.xh1, Ly.dxh1, Ly.r1, Ly.dr1, T, d,
-                       gx, gdx, gxs, gdxs, HV(b), HV(b + 1)};
+                       gx, gdx, gxs, gdxs, HV(b), HV(b + 1), red};
       sd::gpt_ln_bwd(b1, st);
     }
     // embeddings (wte also carries the head contribution written above)

@@ -16,13 +16,14 @@ struct LnBwdArgs {
   int T, d;
   float *gx, *gdx, *gxs, *gdxs;
   float *hv_g, *hv_b;
+  float* scratch;  // >= 2 * 64 * d floats
 };
 
 void gpt_embed(const int* tok, int T, int S, int d, const float* wte, const float* wpe, const float* vwte,
                const float* vwpe, float* x, float* dx, cudaStream_t s);
 void gpt_ln_fwd(const LnArgs& a, cudaStream_t s);
 void gpt_ln_bwd(const LnBwdArgs& a, cudaStream_t s);
-void gpt_colsum(const float* a, int T, int n, long long lda, float* out, cudaStream_t s);
+void gpt_colsum(const float* a, int T, int n, long long lda, float* out, float* scratch, cudaStream_t s);
 void gpt_gelu_fwd(const float* f, const float* df, float* u, float* us, float* du, float* dus, long long n,
                   cudaStream_t s);
 void gpt_gelu_bwd(const float* f, const float* df, float* gu, float* gdu, float* gus, float* gdus, long long n,

@@ -10,6 +10,8 @@
 #include <math.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "sd_common.cuh"
 #include "sd_gpt.h"
 
@@ -160,51 +162,56 @@ __global__ void k_ln_bwd(const float* __restrict__ gy, const float* __restrict__
   }
 }
 
-// Column sums over T rows of the LN parameter Hv terms:
-//   Hv_g[e] += sum_t gdy*xh + gy*dxh ;  Hv_b[e] += sum_t gdy
-// (blocks of 32 columns x 8 row-groups, deterministic fixed-order tree).
-__global__ void k_ln_param_hv(const float* __restrict__ gy, const float* __restrict__ gdy,
-                              const float* __restrict__ xh, const float* __restrict__ dxh, int T, int d,
-                              float* __restrict__ hv_g, float* __restrict__ hv_b, int accumulate) {
-  __shared__ float sg[8][33], sb[8][33];
+// Column reductions over the T token rows (bias and LN-parameter Hv), two
+// deterministic stages: stage 1 = CTA (32 columns x row group) folds its rows
+// with 8 row-lanes per column and a fixed shared-memory tree; stage 2 sums the
+// row-group partials in ascending order.
+constexpr int kRowGroups = 64;
+
+// mode 0: sum a ; mode 1: sum (gdy*xh + gy*dxh) and sum gdy (two outputs)
+template <int MODE>
+__global__ void k_colred1(const float* __restrict__ a, const float* __restrict__ b, const float* __restrict__ c,
+                          const float* __restrict__ e, int T, int n, long long lda, float* __restrict__ part) {
+  __shared__ float s0[8][33], s1[8][33];
   const int col = blockIdx.x * 32 + (threadIdx.x & 31);
-  const int grp = threadIdx.x >> 5;
-  float ag = 0.f, ab = 0.f;
-  if (col < d) {
-    for (int t = grp; t < T; t += 8) {
-      const long long o = (long long)t * d + col;
-      ag += gdy[o] * xh[o] + gy[o] * dxh[o];
-      ab += gdy[o];
+  const int rl = threadIdx.x >> 5;
+  const int rows = (T + gridDim.y - 1) / gridDim.y;
+  const int r0 = blockIdx.y * rows, r1 = min(T, r0 + rows);
+  float x0 = 0.f, x1 = 0.f;
+  if (col < n)
+    for (int t = r0 + rl; t < r1; t += 8) {
+      const long long o = (long long)t * lda + col;
+      if (MODE == 0) {
+        x0 += a[o];
+      } else {  // a = gy, b = gdy, c = xh, e = dxh
+        x0 += b[o] * c[o] + a[o] * e[o];
+        x1 += b[o];
+      }
     }
-  }
-  sg[grp][threadIdx.x & 31] = ag;
-  sb[grp][threadIdx.x & 31] = ab;
+  s0[rl][threadIdx.x & 31] = x0;
+  s1[rl][threadIdx.x & 31] = x1;
   __syncthreads();
-  if (grp == 0 && col < d) {
-    float tg = 0.f, tb = 0.f;
+  if (rl == 0 && col < n) {
+    float t0 = 0.f, t1 = 0.f;
     for (int i = 0; i < 8; ++i) {
-      tg += sg[i][threadIdx.x];
-      tb += sb[i][threadIdx.x];
+      t0 += s0[i][threadIdx.x];
+      t1 += s1[i][threadIdx.x];
     }
-    hv_g[col] = accumulate ? hv_g[col] + tg : tg;
-    hv_b[col] = accumulate ? hv_b[col] + tb : tb;
+    part[(long long)blockIdx.y * n + col] = t0;
+    if (MODE == 1) part[(long long)(gridDim.y + blockIdx.y) * n + col] = t1;
   }
 }
 
-// Hv of a bias: column sum of the adjoint tangent over T rows.
-__global__ void k_colsum(const float* __restrict__ a, int T, int n, long long lda, float* __restrict__ out) {
-  __shared__ float sm[8][33];
-  const int col = blockIdx.x * 32 + (threadIdx.x & 31);
-  const int grp = threadIdx.x >> 5;
-  float acc = 0.f;
-  if (col < n)
-    for (int t = grp; t < T; t += 8) acc += a[(long long)t * lda + col];
-  sm[grp][threadIdx.x & 31] = acc;
-  __syncthreads();
-  if (grp == 0 && col < n) {
-    float tot = 0.f;
-    for (int i = 0; i < 8; ++i) tot += sm[i][threadIdx.x];
-    out[col] = tot;
+__global__ void k_colred2(const float* __restrict__ part, int groups, int n, float* __restrict__ out0,
+                          float* __restrict__ out1) {
+  const int col = blockIdx.x * blockDim.x + threadIdx.x;
+  if (col >= n) return;
+  float t0 = 0.f, t1 = 0.f;
+  for (int g = 0; g < groups; ++g) t0 += part[(long long)g * n + col];
+  out0[col] = t0;
+  if (out1) {
+    for (int g = 0; g < groups; ++g) t1 += part[(long long)(groups + g) * n + col];
+    out1[col] = t1;
   }
 }
 
@@ -431,13 +438,21 @@ void gpt_ln_bwd(const LnBwdArgs& a, cudaStream_t s) {
   k_ln_bwd<<<g1(a.T, 8), 256, 0, s>>>(a.gy, a.gdy, a.g, a.vg, a.xh, a.dxh, a.r, a.dr, a.T, a.d, a.gx, a.gdx, a.gxs,
                                       a.gdxs);
   SD_LAUNCHED("k_ln_bwd");
-  k_ln_param_hv<<<unsigned((a.d + 31) / 32), 256, 0, s>>>(a.gy, a.gdy, a.xh, a.dxh, a.T, a.d, a.hv_g, a.hv_b, 0);
-  SD_LAUNCHED("k_ln_param_hv");
+  const int groups = std::min(kRowGroups, std::max(1, a.T / 64));
+  k_colred1<1><<<dim3(unsigned((a.d + 31) / 32), unsigned(groups)), 256, 0, s>>>(a.gy, a.gdy, a.xh, a.dxh, a.T, a.d,
+                                                                                 a.d, a.scratch);
+  SD_LAUNCHED("k_colred1");
+  k_colred2<<<unsigned((a.d + 255) / 256), 256, 0, s>>>(a.scratch, groups, a.d, a.hv_g, a.hv_b);
+  SD_LAUNCHED("k_colred2");
 }
 
-void gpt_colsum(const float* a, int T, int n, long long lda, float* out, cudaStream_t s) {
-  k_colsum<<<unsigned((n + 31) / 32), 256, 0, s>>>(a, T, n, lda, out);
-  SD_LAUNCHED("k_colsum");
+void gpt_colsum(const float* a, int T, int n, long long lda, float* out, float* scratch, cudaStream_t s) {
+  const int groups = std::min(kRowGroups, std::max(1, T / 64));
+  k_colred1<0><<<dim3(unsigned((n + 31) / 32), unsigned(groups)), 256, 0, s>>>(a, nullptr, nullptr, nullptr, T, n, lda,
+                                                                              scratch);
+  SD_LAUNCHED("k_colred1");
+  k_colred2<<<unsigned((n + 255) / 256), 256, 0, s>>>(scratch, groups, n, out, nullptr);
+  SD_LAUNCHED("k_colred2");
 }
 
 void gpt_gelu_fwd(const float* f, const float* df, float* u, float* us, float* du, float* dus, long long n,

@@ -121,76 +121,112 @@ __global__ void k_axpy_dot_edges(const T* __restrict__ x, T* __restrict__ y, con
 }
 
 // ------------------------------------------------------ Gram-Schmidt pass
-// One CTA per full grid block. Per 32-element chunk the j basis columns are
-// staged as a [j][33] tile; warp 0 applies the j sequential axpys of the
-// reference's CGS (r = axpy(-c_i, q_i, r), i ascending) to its 32 elements,
-// then every thread folds whole columns (MODE 1: Q_i . r) or thread 0 folds
-// r . r (MODE 2). Column accumulators: thread t owns columns t, t+128, ...
-constexpr int kMaxColsPerThread = 8;  // j <= 1024 per launch
+// One WARP per full grid block (1024 elements), walked in 32-element chunks.
+//  update (UPD): lane = element; the j basis entries of the chunk arrive as j
+//    coalesced 128 B loads and are applied in the reference's order
+//    r = axpy(-c_0, q_0, r), ..., axpy(-c_{j-1}, q_{j-1}, r) (per-element f64
+//    product and sum, rounded to the storage precision after every axpy);
+//  fold (MODE 1): lane = column; each lane loads its column's 32 chunk
+//    elements as 128 B vectors and continues its serial f64 block fold of
+//    Q_i . r against the chunk's updated r (broadcast through shared memory);
+//  fold (MODE 2): lane 0 continues the serial fold of r . r.
+// Column accumulators live in registers: lane owns columns lane + 32 q.
+constexpr int kWarpsPerCta = 8;
+constexpr int kMaxColGroups = 8;  // j <= 256 per launch
+
+template <typename T, int N>
+struct VecLoad;
+template <>
+struct VecLoad<float, 32> {
+  __device__ static void load(const float* p, float* out) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(p) + i);
+      out[4 * i] = v.x, out[4 * i + 1] = v.y, out[4 * i + 2] = v.z, out[4 * i + 3] = v.w;
+    }
+  }
+};
+template <>
+struct VecLoad<double, 32> {
+  __device__ static void load(const double* p, double* out) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const double2 v = __ldg(reinterpret_cast<const double2*>(p) + i);
+      out[2 * i] = v.x, out[2 * i + 1] = v.y;
+    }
+  }
+};
+
 template <typename T, bool UPD, int MODE>
-__global__ void __launch_bounds__(kThreads) k_cgs_units(const T* __restrict__ Q, uint64_t ldq, int j,
-                                                        T* __restrict__ r, const double* __restrict__ coef,
-                                                        uint64_t base, uint64_t local_end, uint64_t plen,
-                                                        uint64_t head_n, double* __restrict__ partials) {
-  // plen here is the sequence stride of `partials` (>= this rank's partial length)
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  T* tq = reinterpret_cast<T*>(smem_raw);                    // [j][33]
-  T* tr = tq + size_t(j) * (kChunk + 1);                      // [32]
-  double* cs = reinterpret_cast<double*>(
-      smem_raw + (((size_t(j) * (kChunk + 1) + kChunk + 2) * sizeof(T) + 7) & ~size_t(7)));  // [j]
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint64_t unit = blockIdx.x;
+__global__ void __launch_bounds__(32 * kWarpsPerCta) k_cgs_units(const T* __restrict__ Q, uint64_t ldq, int j,
+                                                                T* __restrict__ r, const double* __restrict__ coef,
+                                                                uint64_t base, uint64_t n_units, uint64_t local_end,
+                                                                uint64_t pstride, uint64_t head_n,
+                                                                double* __restrict__ partials) {
+  extern __shared__ double cs[];  // -coef[0..j)
+  __shared__ T rbuf[kWarpsPerCta][kChunk];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (UPD)
+    for (int i = threadIdx.x; i < j; i += blockDim.x) cs[i] = -coef[i];
+  __syncthreads();
+  const uint64_t unit = uint64_t(blockIdx.x) * kWarpsPerCta + warp;
+  if (unit >= n_units) return;
   const uint64_t e0 = base + unit * kBlock;
   const uint64_t n_el = (local_end - e0) < kBlock ? (local_end - e0) : kBlock;
-  if (UPD)
-    for (int i = tid; i < j; i += kThreads) cs[i] = -coef[i];
-  double acc[kMaxColsPerThread];
+  const bool vec_ok = ((reinterpret_cast<uintptr_t>(Q + e0) | (ldq * sizeof(T))) & 15) == 0;
+  double acc[kMaxColGroups];
 #pragma unroll
-  for (int q = 0; q < kMaxColsPerThread; ++q) acc[q] = 0.0;
+  for (int q = 0; q < kMaxColGroups; ++q) acc[q] = 0.0;
   double self = 0.0;
-  for (int c = 0; c < int(kBlock) / kChunk; ++c) {
-    const uint64_t off0 = uint64_t(c) * kChunk;
-    if (off0 >= n_el) break;
-    const bool valid = off0 + lane < n_el;
-    const uint64_t li = e0 + off0 + lane;
-    for (int i = warp; i < j; i += kThreads / 32) tq[i * (kChunk + 1) + lane] = valid ? Q[uint64_t(i) * ldq + li] : T(0);
-    T rv = T(0);
-    if (warp == 0) rv = valid ? r[li] : T(0);
-    __syncthreads();
-    if (warp == 0) {
-      if (UPD && valid) {
-        double v = double(rv);
-        for (int i = 0; i < j; ++i) v = double(round_to<T>(__dadd_rn(v, __dmul_rn(cs[i], double(tq[i * (kChunk + 1) + lane])))));
-        rv = T(v);
-        r[li] = rv;
-      }
-      tr[lane] = rv;
+  for (uint64_t off = 0; off < n_el; off += kChunk) {
+    const int cnt = int((n_el - off) < uint64_t(kChunk) ? (n_el - off) : kChunk);
+    const bool valid = lane < cnt;
+    const uint64_t li = e0 + off + lane;
+    T rv = valid ? r[li] : T(0);
+    if (UPD && valid) {
+      double v = double(rv);
+      const T* qp = Q + li;
+#pragma unroll 8
+      for (int i = 0; i < j; ++i) v = double(round_to<T>(__dadd_rn(v, __dmul_rn(cs[i], double(qp[uint64_t(i) * ldq])))));
+      rv = T(v);
+      r[li] = rv;
     }
-    __syncthreads();
+    if (MODE != 0) {
+      rbuf[warp][lane] = rv;
+      __syncwarp();
+    }
     if (MODE == 1) {
 #pragma unroll
-      for (int q = 0; q < kMaxColsPerThread; ++q) {
-        const int col = tid + q * kThreads;
-        if (col < j) {
+      for (int q = 0; q < kMaxColGroups; ++q) {
+        const int col = lane + 32 * q;
+        if (q * 32 < j && col < j) {
+          const T* cp = Q + uint64_t(col) * ldq + e0 + off;
           double a = acc[q];
-          const T* row = tq + col * (kChunk + 1);
-#pragma unroll 8
-          for (int k = 0; k < kChunk; ++k) a = __dadd_rn(a, __dmul_rn(double(row[k]), double(tr[k])));
+          if (vec_ok && cnt == kChunk) {
+            T x[kChunk];
+            VecLoad<T, kChunk>::load(cp, x);
+#pragma unroll
+            for (int k = 0; k < kChunk; ++k) a = __dadd_rn(a, __dmul_rn(double(x[k]), double(rbuf[warp][k])));
+          } else {
+            for (int k = 0; k < cnt; ++k) a = __dadd_rn(a, __dmul_rn(double(cp[k]), double(rbuf[warp][k])));
+          }
           acc[q] = a;
         }
       }
-    } else if (MODE == 2 && tid == 0) {
-      for (int k = 0; k < kChunk; ++k) self = __dadd_rn(self, __dmul_rn(double(tr[k]), double(tr[k])));
+      __syncwarp();
+    } else if (MODE == 2) {
+      if (lane == 0)
+        for (int k = 0; k < cnt; ++k) self = __dadd_rn(self, __dmul_rn(double(rbuf[warp][k]), double(rbuf[warp][k])));
+      __syncwarp();
     }
-    __syncthreads();
   }
   if (MODE == 1) {
 #pragma unroll
-    for (int q = 0; q < kMaxColsPerThread; ++q) {
-      const int col = tid + q * kThreads;
-      if (col < j) partials[uint64_t(col) * plen + head_n + unit] = acc[q];
+    for (int q = 0; q < kMaxColGroups; ++q) {
+      const int col = lane + 32 * q;
+      if (col < j) partials[uint64_t(col) * pstride + head_n + unit] = acc[q];
     }
-  } else if (MODE == 2 && tid == 0) {
+  } else if (MODE == 2 && lane == 0) {
     partials[head_n + unit] = self;
   }
 }
@@ -221,47 +257,63 @@ struct RankTable {
   int n;
   uint64_t begin[64], end[64];
 };
-__global__ void k_combine(RankTable rt, uint64_t total, uint64_t m, uint64_t plen_max,
-                          const double* __restrict__ partials, double* __restrict__ out, int post_sqrt) {
-  const uint64_t s = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
-  if (s >= m) return;
+constexpr int kCombChunk = 2048;
+__global__ void __launch_bounds__(256) k_combine(RankTable rt, uint64_t total, uint64_t m, uint64_t plen_max,
+                                                 const double* __restrict__ partials, double* __restrict__ out,
+                                                 int post_sqrt) {
+  // One CTA per sequence: warps 1..7 stream the block sums into a shared
+  // double buffer while thread 0 runs the (inherently serial) left fold.
+  __shared__ double buf[2][kCombChunk];
+  const uint64_t s = blockIdx.x;
   double closed = 0.0, open = 0.0;
   uint64_t at = 0;
+  auto feed = [&](double t) {
+    open = __dadd_rn(open, t);
+    ++at;
+    const uint64_t ge = ((at - 1) / kBlock + 1) * kBlock;
+    if (at == (ge < total ? ge : total)) {
+      closed = __dadd_rn(closed, open);
+      open = 0.0;
+    }
+  };
   for (int rk = 0; rk < rt.n; ++rk) {
     const PartialShape ps = partial_shape(rt.begin[rk], rt.end[rk], total);
     const double* p = partials + (uint64_t(rk) * m + s) * plen_max;
-    for (uint64_t i = 0; i < ps.n_head; ++i) {
-      open = __dadd_rn(open, p[i]);
-      ++at;
-      const uint64_t ge = ((at - 1) / kBlock + 1) * kBlock;
-      if (at == (ge < total ? ge : total)) {
-        closed = __dadd_rn(closed, open);
-        open = 0.0;
-      }
-    }
+    if (threadIdx.x == 0)
+      for (uint64_t i = 0; i < ps.n_head; ++i) feed(p[i]);
     const double* sums = p + ps.n_head;
-    uint64_t i = 0;
-    for (; i + 8 <= ps.n_sums; i += 8) {
-      double v[8];
+    const uint64_t nch = (ps.n_sums + kCombChunk - 1) / kCombChunk;
+    // prologue: chunk 0
+    for (uint64_t i = threadIdx.x; i < kCombChunk && i < ps.n_sums; i += blockDim.x) buf[0][i] = sums[i];
+    __syncthreads();
+    for (uint64_t c = 0; c < nch; ++c) {
+      const uint64_t c0 = c * kCombChunk;
+      const int len = int((ps.n_sums - c0) < uint64_t(kCombChunk) ? (ps.n_sums - c0) : kCombChunk);
+      if (threadIdx.x == 0) {
+        const double* b = buf[c & 1];
+        int i = 0;
+        for (; i + 8 <= len; i += 8) {
+          double v[8];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) v[q] = sums[i + q];
+          for (int q = 0; q < 8; ++q) v[q] = b[i + q];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) closed = __dadd_rn(closed, v[q]);
-    }
-    for (; i < ps.n_sums; ++i) closed = __dadd_rn(closed, sums[i]);
-    at = ps.n_sums ? ((at + ps.n_sums * kBlock) < total ? at + ps.n_sums * kBlock : total) : at;
-    const double* tail = sums + ps.n_sums;
-    for (uint64_t t = 0; t < ps.n_tail; ++t) {
-      open = __dadd_rn(open, tail[t]);
-      ++at;
-      const uint64_t ge = ((at - 1) / kBlock + 1) * kBlock;
-      if (at == (ge < total ? ge : total)) {
-        closed = __dadd_rn(closed, open);
-        open = 0.0;
+          for (int q = 0; q < 8; ++q) closed = __dadd_rn(closed, v[q]);
+        }
+        for (; i < len; ++i) closed = __dadd_rn(closed, b[i]);
+      } else if (threadIdx.x >= 32 && c + 1 < nch) {
+        const uint64_t n0 = c0 + kCombChunk;
+        for (uint64_t i = threadIdx.x - 32; i < kCombChunk && n0 + i < ps.n_sums; i += blockDim.x - 32)
+          buf[(c + 1) & 1][i] = sums[n0 + i];
       }
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      at = ps.n_sums ? ((at + ps.n_sums * kBlock) < total ? at + ps.n_sums * kBlock : total) : at;
+      const double* tail = sums + ps.n_sums;
+      for (uint64_t t = 0; t < ps.n_tail; ++t) feed(tail[t]);
     }
   }
-  out[s] = post_sqrt ? __dsqrt_rn(closed) : closed;  // norm2 = sqrt(dot), sharded.cpp:102-104
+  if (threadIdx.x == 0) out[s] = post_sqrt ? __dsqrt_rn(closed) : closed;  // norm2 = sqrt(dot), sharded.cpp:102-104
 }
 
 // ------------------------------------------------------ elementwise kernels
@@ -350,21 +402,20 @@ template <typename T>
 static void launch_cgs(const void* Q, uint64_t ldq, uint64_t j, void* r, const double* coef, int mode, uint64_t begin,
                        uint64_t end, uint64_t total, double* partials, uint64_t pstride, cudaStream_t s) {
   if (j == 0) return;
-  if (j > uint64_t(kThreads) * kMaxColsPerThread) fail(SD_ARGUMENT_ERROR, "cgs: more than 1024 columns per pass");
   const PartialShape ps = partial_shape(begin, end, total);
   const uint64_t local_end = end - begin, plen = pstride ? pstride : ps.len();
   const uint64_t tail_begin = ps.n_head + ps.n_sums * kBlock;
   const bool upd = coef != nullptr;
-  const size_t tile = (size_t(j) * (kChunk + 1) + kChunk + 2) * sizeof(T);
-  const size_t smem = ((tile + 7) / 8) * 8 + size_t(j) * sizeof(double);
+  if (j > uint64_t(32) * kMaxColGroups) fail(SD_ARGUMENT_ERROR, "cgs: more than 256 columns per pass");
+  const size_t smem = size_t(j) * sizeof(double);
   auto run = [&](auto upd_c, auto mode_c) {
     constexpr bool U = decltype(upd_c)::value;
     constexpr int M = decltype(mode_c)::value;
     if (ps.n_sums) {
       auto kern = k_cgs_units<T, U, M>;
-      if (smem > 48 * 1024) SD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-      kern<<<unsigned(ps.n_sums), kThreads, smem, s>>>((const T*)Q, ldq, int(j), (T*)r, coef, ps.n_head, local_end,
-                                                       plen, ps.n_head, partials);
+      const unsigned g = unsigned((ps.n_sums + kWarpsPerCta - 1) / kWarpsPerCta);
+      kern<<<g, 32 * kWarpsPerCta, smem, s>>>((const T*)Q, ldq, int(j), (T*)r, coef, ps.n_head, ps.n_sums, local_end,
+                                              plen, ps.n_head, partials);
       SD_LAUNCHED("k_cgs_units");
     }
     if (ps.n_head + ps.n_tail) {
@@ -403,7 +454,7 @@ void combine_device(uint64_t nranks, const uint64_t* begins, const uint64_t* end
     at = ends[r];
   }
   if (at != total) fail(SD_PROTOCOL_ERROR, "blocked partials do not cover the vector");
-  k_combine<<<grid_for(m, 128), 128, 0, s>>>(rt, total, m, plen_max, partials, out, post_sqrt);
+  k_combine<<<unsigned(m), 256, 0, s>>>(rt, total, m, plen_max, partials, out, post_sqrt);
   SD_LAUNCHED("k_combine");
 }
 

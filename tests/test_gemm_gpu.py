@@ -57,3 +57,25 @@ def test_tf32_truncation_split_mode(G):
     e_rna = rel(G.matmul(A, B, True, mode=1), ref)
     print(f"3xTF32 rel err: trunc-split {e_trunc:.3e}  rna-split {e_rna:.3e}")
     assert min(e_trunc, e_rna) < 2e-6
+
+
+@pytest.mark.parametrize("a_t,b_t", [(True, True), (False, False)])
+def test_gemm_split_k(G, a_t, b_t):
+    """Few output tiles + long K (the Hv weight products over T tokens) take
+    the deterministic split-K path; alpha/beta/bias/residual still apply."""
+    M, N, K = 256, 384, 8192
+    A = torch.randn(*((K, M) if a_t else (M, K)), device="cuda")
+    B = torch.randn(*((N, K) if b_t else (K, N)), device="cuda")
+    bias = torch.randn(N, device="cuda")
+    C = torch.randn(M, N, device="cuda")
+    C0 = C.clone()
+    Cs = torch.empty_like(C)
+    G.gemm(M, N, K, A, A.shape[1], a_t, B, B.shape[1], not b_t, C, N, alpha=0.5, beta=2.0,
+           a_small=G.split(A), b_small=G.split(B))
+    ref = 0.5 * ((A.double().t() if a_t else A.double()) @ (B.double().t() if b_t else B.double())) + 2.0 * C0.double()
+    assert rel(C, ref) < 2e-6
+    first = C.clone()
+    C.copy_(C0)
+    G.gemm(M, N, K, A, A.shape[1], a_t, B, B.shape[1], not b_t, C, N, alpha=0.5, beta=2.0,
+           a_small=G.split(A), b_small=G.split(B))
+    assert torch.equal(C, first)  # deterministic split order
