@@ -117,6 +117,7 @@ struct EpiParams {
   float* dbg;         // debug: receives smem stage 0 after the accumulator is complete
   int zcount, kb_per;  // batch count; k-blocks per split
   float* ws;           // split-K: raw partial tiles [split][z][M][N] (else null)
+  int causal;          // 0 none, 1 lower output, 2 lower-triangular A, 3 upper-triangular A
 };
 
 // Descriptor of k-step `ks` (8 tf32) of an operand tile. K-major tiles are 128
@@ -173,8 +174,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   // blockIdx.z = batch + zcount * split (split-K: each split owns kb_per k-blocks)
   const int z = blockIdx.z % ep.zcount, split = blockIdx.z / ep.zcount;
   const int z1 = z % ep.Z1, z2 = z / ep.Z1;
-  const int kb0 = split * ep.kb_per;
-  const int num_kb = min(ep.kb_per, (K + BK - 1) / BK - kb0);
+  // Causal attention structure (square S x S per head, tile-aligned):
+  //  1: C[i][j] is only needed for j <= i -> tiles strictly above the diagonal exit;
+  //  2: A[i][k] is zero for k > i  -> K range [0, m0 + BM);
+  //  3: A[i][k] is zero for k < i  -> K range [m0, K).
+  if (ep.causal == 1 && n0 > m0 + BM - 1) return;
+  int kb0 = split * ep.kb_per;
+  int num_kb = min(ep.kb_per, (K + BK - 1) / BK - kb0);
+  if (ep.causal == 2) num_kb = min(num_kb, (m0 + BM + BK - 1) / BK - kb0);
+  if (ep.causal == 3) {
+    const int lo = m0 / BK;
+    num_kb -= max(0, lo - kb0);
+    kb0 = max(kb0, lo);
+  }
   const int num_chunks = (num_kb + KC - 1) / KC;
 
   if (threadIdx.x == 0) {
@@ -497,12 +509,12 @@ void launch(const GemmArgs& g, cudaStream_t s) {
   // Hv weight products reduce over all T tokens): partial tiles go to a
   // workspace and are summed in a fixed order by k_splitk_reduce.
   int splits = 1;
-  if (tiles < kNumSMs && total_kb >= 32) splits = std::min(std::min(total_kb / 16, 16), (2 * kNumSMs + tiles - 1) / tiles);
+  if (g.causal == 0 && tiles < kNumSMs && total_kb >= 32) splits = std::min(std::min(total_kb / 16, 16), (2 * kNumSMs + tiles - 1) / tiles);
   const int kb_per = (total_kb + splits - 1) / splits;
   splits = (total_kb + kb_per - 1) / kb_per;
   float* ws = nullptr;
   if (splits > 1) ws = splitk_workspace(size_t(splits) * zc * size_t(g.M) * g.N);
-  EpiParams ep{g.C, g.ldc, g.sc1, g.sc2, g.M, g.N, g.Z1, g.alpha, g.beta, g.bias, g.Cs, g.dbg, zc, kb_per, ws};
+  EpiParams ep{g.C, g.ldc, g.sc1, g.sc2, g.M, g.N, g.Z1, g.alpha, g.beta, g.bias, g.Cs, g.dbg, zc, kb_per, ws, g.causal};
   constexpr int NT = THREE ? 4 : 2;
   const size_t smem = 1024 + STAGES * NT * TILE_BYTES + 256;
   auto kern = k_gemm_tf32<A_MN, B_MN, THREE>;

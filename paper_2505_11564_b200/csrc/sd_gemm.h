@@ -20,6 +20,7 @@ struct GemmArgs {
   const float* bias = nullptr;  // per-column bias added in the epilogue
   float* Cs = nullptr;          // optional tf32 residual of the final C (same strides as C)
   float* dbg = nullptr;
+  int causal = 0;  // causal attention structure, see k_gemm_tf32
   long long sa1 = 0, sa2 = 0, sb1 = 0, sb2 = 0, sc1 = 0, sc2 = 0;  // element strides
 };
 void gemm(const GemmArgs& g, cudaStream_t s);

@@ -176,8 +176,10 @@ struct sd_gpt_s {
     g.B = Bo.p, g.Bs = Bo.s, g.ldb = Bo.ld, g.b_mn = Bo.mn;
     g.C = C, g.ldc = ldc, g.alpha = alpha, g.beta = beta, g.bias = bias, g.Cs = Cs;
     g.Z1 = Z1, g.Z2 = Z2, g.sa1 = A.s1, g.sa2 = A.s2, g.sb1 = Bo.s1, g.sb2 = Bo.s2, g.sc1 = c1, g.sc2 = c2;
+    g.causal = cmode;
     sd::gemm(g, st);
   }
+  int cmode = 0;  // causal tile/K skipping for the per-head S x S products (sd_gemm.cu)
 
   const float* th(int i) const { return theta + slots[i].off; }
   const float* ths(int i) const { return theta_s + slots[i].off; }
@@ -294,6 +296,7 @@ struct sd_gpt_s {
     const long long hs = (long long)Sq * Sq, bs = (long long)H * Sq * Sq;  // in P [B, H, S, S]
     const long long ho = dh, bo = (long long)Sq * d;          // in o [T, d]
     auto q = [&](float* base, float* res) { return Op{base, res, 3 * d, false, ha, ba}; };
+    cmode = 1;  // scores: only j <= i tiles
     mm(Sq, Sq, dh, q(Ly.a, Ly.as), {Ly.a + d, Ly.as + d, 3 * d, false, ha, ba}, Ly.P, Sq, sc, 0, st, nullptr,
        nullptr, H, B, hs, bs);
     mm(Sq, Sq, dh, q(Ly.da, Ly.das), {Ly.a + d, Ly.as + d, 3 * d, false, ha, ba}, Ly.dP, Sq, sc, 0, st, nullptr,
@@ -303,9 +306,11 @@ struct sd_gpt_s {
     sd::gpt_attn_softmax_fwd(Ly.P, Ly.dP, Ly.Ps, Ly.dPs, Sq, (long long)B * H * Sq, st);
     const Op Pm{Ly.P, Ly.Ps, Sq, false, hs, bs}, dPm{Ly.dP, Ly.dPs, Sq, false, hs, bs};
     const Op vv{Ly.a + 2 * d, Ly.as + 2 * d, 3 * d, true, ha, ba}, dvv{Ly.da + 2 * d, Ly.das + 2 * d, 3 * d, true, ha, ba};
+    cmode = 2;  // P, dP lower-triangular: keys k <= query i
     mm(Sq, dh, Sq, Pm, vv, Ly.o, d, 1, 0, st, nullptr, Ly.os, H, B, ho, bo);
     mm(Sq, dh, Sq, dPm, vv, Ly.dO, d, 1, 0, st, nullptr, nullptr, H, B, ho, bo);
     mm(Sq, dh, Sq, Pm, dvv, Ly.dO, d, 1, 1, st, nullptr, Ly.dOs, H, B, ho, bo);
+    cmode = 0;
   }
 
   // gP = go v^T ; gdP = gdo v^T + go dv^T ; (gS, gdS) = softmax double-backward ;
@@ -318,6 +323,7 @@ struct sd_gpt_s {
     const long long ho = dh, bo = (long long)Sq * d;
     const Op goK{go, gos, d, false, ho, bo}, gdoK{gdo, gdos, d, false, ho, bo};
     const Op vK{Ly.a + 2 * d, Ly.as + 2 * d, 3 * d, false, ha, ba}, dvK{Ly.da + 2 * d, Ly.das + 2 * d, 3 * d, false, ha, ba};
+    cmode = 1;
     mm(Sq, Sq, dh, goK, vK, gP, Sq, 1, 0, st, nullptr, nullptr, H, B, hs, bs);
     mm(Sq, Sq, dh, gdoK, vK, gdP, Sq, 1, 0, st, nullptr, nullptr, H, B, hs, bs);
     mm(Sq, Sq, dh, goK, dvK, gdP, Sq, 1, 1, st, nullptr, nullptr, H, B, hs, bs);
@@ -325,21 +331,25 @@ struct sd_gpt_s {
     // value adjoints
     const Op PT{Ly.P, Ly.Ps, Sq, true, hs, bs}, dPT{Ly.dP, Ly.dPs, Sq, true, hs, bs};
     const Op goM{go, gos, d, true, ho, bo}, gdoM{gdo, gdos, d, true, ho, bo};
+    cmode = 3;  // P^T upper-triangular: queries i >= key j
     mm(Sq, dh, Sq, PT, goM, ga + 2 * d, 3 * d, 1, 0, st, nullptr, gas + 2 * d, H, B, ha, ba);
     mm(Sq, dh, Sq, dPT, goM, gda + 2 * d, 3 * d, 1, 0, st, nullptr, nullptr, H, B, ha, ba);
     mm(Sq, dh, Sq, PT, gdoM, gda + 2 * d, 3 * d, 1, 1, st, nullptr, gdas + 2 * d, H, B, ha, ba);
     // query adjoints
     const Op gS{gP, gPs, Sq, false, hs, bs}, gdS{gdP, gdPs, Sq, false, hs, bs};
     const Op kM{Ly.a + d, Ly.as + d, 3 * d, true, ha, ba}, dkM{Ly.da + d, Ly.das + d, 3 * d, true, ha, ba};
+    cmode = 2;
     mm(Sq, dh, Sq, gS, kM, ga, 3 * d, sc, 0, st, nullptr, gas, H, B, ha, ba);
     mm(Sq, dh, Sq, gdS, kM, gda, 3 * d, sc, 0, st, nullptr, nullptr, H, B, ha, ba);
     mm(Sq, dh, Sq, gS, dkM, gda, 3 * d, sc, 1, st, nullptr, gdas, H, B, ha, ba);
     // key adjoints
     const Op gST{gP, gPs, Sq, true, hs, bs}, gdST{gdP, gdPs, Sq, true, hs, bs};
     const Op qM{Ly.a, Ly.as, 3 * d, true, ha, ba}, dqM{Ly.da, Ly.das, 3 * d, true, ha, ba};
+    cmode = 3;
     mm(Sq, dh, Sq, gST, qM, ga + d, 3 * d, sc, 0, st, nullptr, gas + d, H, B, ha, ba);
     mm(Sq, dh, Sq, gdST, qM, gda + d, 3 * d, sc, 0, st, nullptr, nullptr, H, B, ha, ba);
     mm(Sq, dh, Sq, gST, dqM, gda + d, 3 * d, sc, 1, st, nullptr, gdas + d, H, B, ha, ba);
+    cmode = 0;
   }
 };
 
