@@ -1,6 +1,6 @@
 // fp32-faithful GEMM on the 5th-generation tensor cores (sm_100a).
 //
-//   C[z] = alpha * op(A[z]) . op(B[z]) + beta * C[z]      (fp32 in, fp32 out)
+//   C[z] = alpha * op(A[z]) . op(B[z]) + beta * C[z] (+ bias)   (fp32 in/out)
 //
 // 3xTF32: every operand x is consumed as its raw fp32 bits (the tensor core
 // reads the top 19 bits, i.e. trunc_tf32(x)) plus a precomputed residual
@@ -8,12 +8,14 @@
 //   A.B ~= A_b.B_b + A_b.B_s + A_s.B_b        (3 tcgen05.mma kind::tf32)
 // which carries ~21-22 significant bits per product (fp32-faithful).
 //
-// Structure (one 128x128 output tile per CTA, 6 warps):
-//   warp 0   : TMA producer (cp.async.bulk.tensor, 128B swizzle) into a
-//              3-stage smem ring guarded by full/empty mbarriers;
-//   warp 1   : TMEM allocator + single-thread tcgen05.mma issuer, releasing
-//              ring slots with tcgen05.commit;
-//   warps 2-5: epilogue, tcgen05.ld 32x32b from TMEM -> registers -> global.
+// Persistent warp-specialised kernel, one CTA per SM, 128 x 128 output tiles
+// walked in a static round-robin schedule:
+//   warp 0   : TMA producer (cp.async.bulk.tensor) into a STAGES-deep smem
+//              ring (full/empty mbarriers), running ahead across tiles;
+//   warp 1   : TMEM allocator + single-thread tcgen05.mma issuer;
+//   warps 2-5: epilogue: drain TMEM chunks (tcgen05.ld 32x32b) into
+//              round-to-nearest fp32 registers, then alpha/beta/bias,
+//              residual and store — overlapped with the next tile's MMAs.
 // Operand majors: A is K-major (row-major M x K) or MN-major (row-major K x M);
 // B is K-major (row-major N x K) or MN-major (row-major K x N). A batch index
 // z decomposes as (z1 = z % Z1, z2 = z / Z1) with independent strides, which
@@ -22,7 +24,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstring>
+#include <string>
 #include <mutex>
 #include <vector>
 
@@ -33,10 +37,13 @@ namespace sd {
 
 namespace {
 
-constexpr int BM = 128, BN = 128, BK = 32, STAGES = 3;
-constexpr int TILE_BYTES = BM * BK * 4;  // 16 KB per operand tile (BN == BM)
+// BK = 16 fp32 (64 B) per stage keeps a 6-deep ring of 4 operand tiles in
+// 192 KB of shared memory: enough bytes in flight to cover TMA latency.
+constexpr int BM = 128, BN = 128, BK = 16, STAGES = 6;
+constexpr int TILE_BYTES = BM * BK * 4;  // 8 KB per operand tile (BN == BM)
 constexpr int NUM_THREADS = 192;
 constexpr uint32_t TMEM_COLS = 2 * BN;  // two accumulation buffers
+constexpr int kNumSMs = 148;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -59,6 +66,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 
 __device__ __forceinline__ void tma_load_4d(const CUtensorMap* map, uint64_t* bar, void* dst, int c0, int c1, int c2,
                                             int c3) {
@@ -69,9 +79,9 @@ __device__ __forceinline__ void tma_load_4d(const CUtensorMap* map, uint64_t* ba
       : "memory");
 }
 
-// UMMA shared-memory descriptor (tcgen05 "matrix descriptor"). layout 2 =
-// SWIZZLE_128B (K-major tiles), 1 = SWIZZLE_128B_BASE32B (MN-major tf32 tiles,
-// the only MN-major smem layout the tf32 MMA accepts).
+// UMMA shared-memory matrix descriptor. Layout codes: 4 = SWIZZLE_64B (K-major
+// tiles), 1 = SWIZZLE_128B_BASE32B (MN-major tf32 tiles: the only MN-major
+// smem layout the tf32 MMA accepts).
 __device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
   uint64_t d = 0;
   d |= uint64_t((saddr >> 4) & 0x3FFF);
@@ -107,34 +117,6 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
                : "memory");
 }
 
-struct EpiParams {
-  float* C;
-  long long ldc, sc1, sc2;
-  int M, N, Z1;
-  float alpha, beta;
-  const float* bias;  // per output column, may be null
-  float* Cs;          // residual output, may be null
-  float* dbg;         // debug: receives smem stage 0 after the accumulator is complete
-  int zcount, kb_per;  // batch count; k-blocks per split
-  float* ws;           // split-K: raw partial tiles [split][z][M][N] (else null)
-  int causal;          // 0 none, 1 lower output, 2 lower-triangular A, 3 upper-triangular A
-};
-
-// Descriptor of k-step `ks` (8 tf32) of an operand tile. K-major tiles are 128
-// rows x 128 B, 128B-swizzled in 8-row (1024 B) atoms: advance 32 B per k-step,
-// SBO = 1024 B. MN-major tiles are four 32-element chunks of [32 k-rows x 128 B]
-// swizzled in 4-row (512 B) atoms of 32 B granules: advance 8 rows = 1024 B per
-// k-step, LBO = 4096 B between MN chunks, SBO = 512 B between 4-row groups.
-template <bool MN>
-__device__ __forceinline__ uint64_t tile_desc(uint32_t base, int ks) {
-  if (MN) return make_desc(base + ks * 1024, 4096, 512, 1);
-  return make_desc(base + ks * 32, 16, 1024, 2);
-}
-
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* v) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
@@ -146,13 +128,69 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* v) {
       : "r"(taddr));
 }
 
+struct EpiParams {
+  float* C;
+  long long ldc, sc1, sc2;
+  int M, N, Z1;
+  float alpha, beta;
+  const float* bias;  // per output column, may be null
+  float* Cs;          // residual output, may be null
+  float* dbg;         // debug hook (unused by the persistent kernel)
+  int zcount, kb_per;  // batch count; k-blocks per split
+  float* ws;           // split-K: raw partial tiles [split][z][M][N] (else null)
+  int causal;          // 0 none, 1 lower output, 2 lower-triangular A, 3 upper-triangular A
+  int n_tiles_n, n_tiles_m, n_tiles;  // tile grid (n fastest), n_tiles over all (split, z)
+};
+
+// Descriptor of k-step `ks` (8 tf32 = 32 B of K) of an operand tile.
+// K-major: 128 rows x 64 B, SWIZZLE_64B in 8-row (512 B) atoms: advance 32 B
+// per k-step, SBO = 512 B. MN-major: four 32-element chunks of [16 k-rows x
+// 128 B] swizzled in 4-row (512 B) atoms of 32 B granules: advance 8 rows =
+// 1024 B per k-step, LBO = 2048 B between MN chunks, SBO = 512 B.
+template <bool MN>
+__device__ __forceinline__ uint64_t tile_desc(uint32_t base, int ks) {
+  if (MN) return make_desc(base + ks * 1024, 2048, 512, 1);
+  return make_desc(base + ks * 32, 16, 512, 4);
+}
+
 // The tensor core's fp32 accumulation is not round-to-nearest (its error grows
 // ~linearly with the number of accumulated MMAs). To stay fp32-faithful at
 // K = 8192 the K loop is cut into chunks of KC k-blocks: each chunk
 // accumulates in one of two TMEM buffers, and the epilogue warps drain every
 // finished chunk into round-to-nearest fp32 registers while the MMA warp
-// fills the other buffer.
-constexpr int KC = 4;  // k-blocks (4 x 32 = 128 of K) per TMEM chunk
+// fills the other buffer (chunks continue across the tiles of a CTA).
+constexpr int KC = 8;  // k-blocks (8 x 16 = 128 of K) per TMEM chunk
+
+struct TileInfo {
+  int n0, m0, z, split, kb0, num_kb;
+  bool skip;
+};
+
+__device__ __forceinline__ TileInfo tile_info(const EpiParams& ep, int t, int K) {
+  TileInfo ti;
+  const int nt = t % ep.n_tiles_n;
+  const int mt = (t / ep.n_tiles_n) % ep.n_tiles_m;
+  const int zz = t / (ep.n_tiles_n * ep.n_tiles_m);
+  ti.n0 = nt * BN;
+  ti.m0 = mt * BM;
+  ti.z = zz % ep.zcount;
+  ti.split = zz / ep.zcount;
+  ti.kb0 = ti.split * ep.kb_per;
+  ti.num_kb = min(ep.kb_per, (K + BK - 1) / BK - ti.kb0);
+  // Causal attention structure (square S x S per head, tile-aligned):
+  //  1: C[i][j] is only needed for j <= i -> tiles strictly above the diagonal skip;
+  //  2: A[i][k] is zero for k > i  -> K range [0, m0 + BM);
+  //  3: A[i][k] is zero for k < i  -> K range [m0, K).
+  ti.skip = (ep.causal == 1 && ti.n0 > ti.m0 + BM - 1);
+  if (ep.causal == 2) ti.num_kb = min(ti.num_kb, (ti.m0 + BM + BK - 1) / BK - ti.kb0);
+  if (ep.causal == 3) {
+    const int lo = ti.m0 / BK;
+    ti.num_kb -= max(0, lo - ti.kb0);
+    ti.kb0 = max(ti.kb0, lo);
+  }
+  if (ti.num_kb <= 0) ti.skip = true;
+  return ti;
+}
 
 template <bool A_MN, bool B_MN, bool THREE>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
@@ -170,24 +208,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n0 = blockIdx.x * BN, m0 = blockIdx.y * BM;
-  // blockIdx.z = batch + zcount * split (split-K: each split owns kb_per k-blocks)
-  const int z = blockIdx.z % ep.zcount, split = blockIdx.z / ep.zcount;
-  const int z1 = z % ep.Z1, z2 = z / ep.Z1;
-  // Causal attention structure (square S x S per head, tile-aligned):
-  //  1: C[i][j] is only needed for j <= i -> tiles strictly above the diagonal exit;
-  //  2: A[i][k] is zero for k > i  -> K range [0, m0 + BM);
-  //  3: A[i][k] is zero for k < i  -> K range [m0, K).
-  if (ep.causal == 1 && n0 > m0 + BM - 1) return;
-  int kb0 = split * ep.kb_per;
-  int num_kb = min(ep.kb_per, (K + BK - 1) / BK - kb0);
-  if (ep.causal == 2) num_kb = min(num_kb, (m0 + BM + BK - 1) / BK - kb0);
-  if (ep.causal == 3) {
-    const int lo = m0 / BK;
-    num_kb -= max(0, lo - kb0);
-    kb0 = max(kb0, lo);
-  }
-  const int num_chunks = (num_kb + KC - 1) / KC;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -214,107 +234,125 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(&mA) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(&mB) : "memory");
-      for (int kb = 0; kb < num_kb; ++kb) {
-        const int s = kb % STAGES;
-        const uint32_t ph = (kb / STAGES) & 1;
-        mbar_wait(&empty[s], ph ^ 1);
-        unsigned char* st = smem + s * STAGE_BYTES;
-        mbar_expect_tx(&full[s], STAGE_BYTES);
-        const int k0 = (kb0 + kb) * BK;
-        if (A_MN) {
-          for (int c = 0; c < 4; ++c) {
-            tma_load_4d(&mA, &full[s], st + c * 4096, m0 + 32 * c, k0, z1, z2);
-            if (THREE) tma_load_4d(&mAs, &full[s], st + TILE_BYTES + c * 4096, m0 + 32 * c, k0, z1, z2);
+      uint32_t g = 0;  // global k-block counter (ring position)
+      for (int t = blockIdx.x; t < ep.n_tiles; t += gridDim.x) {
+        const TileInfo ti = tile_info(ep, t, K);
+        if (ti.skip) continue;
+        const int z1 = ti.z % ep.Z1, z2 = ti.z / ep.Z1;
+        for (int kb = 0; kb < ti.num_kb; ++kb, ++g) {
+          const int s = g % STAGES;
+          const uint32_t ph = (g / STAGES) & 1;
+          mbar_wait(&empty[s], ph ^ 1);
+          unsigned char* st = smem + s * STAGE_BYTES;
+          mbar_expect_tx(&full[s], STAGE_BYTES);
+          const int k0 = (ti.kb0 + kb) * BK;
+          if (A_MN) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              tma_load_4d(&mA, &full[s], st + c * 2048, ti.m0 + 32 * c, k0, z1, z2);
+              if (THREE) tma_load_4d(&mAs, &full[s], st + TILE_BYTES + c * 2048, ti.m0 + 32 * c, k0, z1, z2);
+            }
+          } else {
+            tma_load_4d(&mA, &full[s], st, k0, ti.m0, z1, z2);
+            if (THREE) tma_load_4d(&mAs, &full[s], st + TILE_BYTES, k0, ti.m0, z1, z2);
           }
-        } else {
-          tma_load_4d(&mA, &full[s], st, k0, m0, z1, z2);
-          if (THREE) tma_load_4d(&mAs, &full[s], st + TILE_BYTES, k0, m0, z1, z2);
-        }
-        unsigned char* sb = st + (THREE ? 2 : 1) * TILE_BYTES;
-        if (B_MN) {
-          for (int c = 0; c < 4; ++c) {
-            tma_load_4d(&mB, &full[s], sb + c * 4096, n0 + 32 * c, k0, z1, z2);
-            if (THREE) tma_load_4d(&mBs, &full[s], sb + TILE_BYTES + c * 4096, n0 + 32 * c, k0, z1, z2);
+          unsigned char* sb = st + (THREE ? 2 : 1) * TILE_BYTES;
+          if (B_MN) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              tma_load_4d(&mB, &full[s], sb + c * 2048, ti.n0 + 32 * c, k0, z1, z2);
+              if (THREE) tma_load_4d(&mBs, &full[s], sb + TILE_BYTES + c * 2048, ti.n0 + 32 * c, k0, z1, z2);
+            }
+          } else {
+            tma_load_4d(&mB, &full[s], sb, k0, ti.n0, z1, z2);
+            if (THREE) tma_load_4d(&mBs, &full[s], sb + TILE_BYTES, k0, ti.n0, z1, z2);
           }
-        } else {
-          tma_load_4d(&mB, &full[s], sb, k0, n0, z1, z2);
-          if (THREE) tma_load_4d(&mBs, &full[s], sb + TILE_BYTES, k0, n0, z1, z2);
         }
       }
     }
   } else if (warp == 1) {
     constexpr uint32_t idesc = make_idesc(A_MN, B_MN);
-    for (int kb = 0; kb < num_kb; ++kb) {
-      const int s = kb % STAGES;
-      const uint32_t ph = (kb / STAGES) & 1;
-      const int chunk = kb / KC, buf = chunk & 1;
-      const bool first = (kb % KC) == 0;
-      const bool last = (kb % KC) == KC - 1 || kb == num_kb - 1;
-      if (first && chunk >= 2) mbar_wait(&tempty[buf], ((chunk >> 1) - 1) & 1);
-      mbar_wait(&full[s], ph);
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      if (lane == 0) {
-        const uint32_t d = tmem + uint32_t(buf * BN);
-        const uint32_t st = smem_u32(smem + s * STAGE_BYTES);
-        const uint32_t a = st, as = st + TILE_BYTES;
-        const uint32_t b = st + (THREE ? 2 : 1) * TILE_BYTES, bs = b + TILE_BYTES;
+    uint32_t g = 0, chunk = 0;
+    for (int t = blockIdx.x; t < ep.n_tiles; t += gridDim.x) {
+      const TileInfo ti = tile_info(ep, t, K);
+      if (ti.skip) continue;
+      for (int kb = 0; kb < ti.num_kb; ++kb, ++g) {
+        const int s = g % STAGES;
+        const uint32_t ph = (g / STAGES) & 1;
+        const bool first = (kb % KC) == 0;
+        const bool last = (kb % KC) == KC - 1 || kb == ti.num_kb - 1;
+        const uint32_t buf = chunk & 1;
+        if (first && chunk >= 2) mbar_wait(&tempty[buf], ((chunk >> 1) - 1) & 1);
+        mbar_wait(&full[s], ph);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        if (lane == 0) {
+          const uint32_t d = tmem + buf * BN;
+          const uint32_t st = smem_u32(smem + s * STAGE_BYTES);
+          const uint32_t a = st, as = st + TILE_BYTES;
+          const uint32_t b = st + (THREE ? 2 : 1) * TILE_BYTES, bs = b + TILE_BYTES;
 #pragma unroll
-        for (int ks = 0; ks < BK / 8; ++ks) {
-          const uint32_t acc0 = (first && ks == 0) ? 0u : 1u;
-          if (THREE) {
-            mma_tf32(d, tile_desc<A_MN>(as, ks), tile_desc<B_MN>(b, ks), idesc, acc0);
-            mma_tf32(d, tile_desc<A_MN>(a, ks), tile_desc<B_MN>(bs, ks), idesc, 1u);
-            mma_tf32(d, tile_desc<A_MN>(a, ks), tile_desc<B_MN>(b, ks), idesc, 1u);
-          } else {
-            mma_tf32(d, tile_desc<A_MN>(a, ks), tile_desc<B_MN>(b, ks), idesc, acc0);
+          for (int ks = 0; ks < BK / 8; ++ks) {
+            const uint32_t acc0 = (first && ks == 0) ? 0u : 1u;
+            if (THREE) {
+              mma_tf32(d, tile_desc<A_MN>(as, ks), tile_desc<B_MN>(b, ks), idesc, acc0);
+              mma_tf32(d, tile_desc<A_MN>(a, ks), tile_desc<B_MN>(bs, ks), idesc, 1u);
+              mma_tf32(d, tile_desc<A_MN>(a, ks), tile_desc<B_MN>(b, ks), idesc, 1u);
+            } else {
+              mma_tf32(d, tile_desc<A_MN>(a, ks), tile_desc<B_MN>(b, ks), idesc, acc0);
+            }
           }
+          mma_commit(&empty[s]);
+          if (last) mma_commit(&tfull[buf]);
         }
-        mma_commit(&empty[s]);
-        if (last) mma_commit(&tfull[buf]);
+        __syncwarp();
+        if (last) ++chunk;
       }
-      __syncwarp();
     }
   } else {
     // epilogue: warp w drains TMEM lanes 32*(w%4) .. +31 (its sub-partition);
     // thread = one output row, BN fp32 accumulators in registers.
     const int sub = warp & 3;
-    const int row = m0 + sub * 32 + lane;
-    float acc[BN];
+    uint32_t chunk = 0;
+    for (int t = blockIdx.x; t < ep.n_tiles; t += gridDim.x) {
+      const TileInfo ti = tile_info(ep, t, K);
+      if (ti.skip) continue;
+      const int row = ti.m0 + sub * 32 + lane;
+      float acc[BN];
 #pragma unroll
-    for (int j = 0; j < BN; ++j) acc[j] = 0.0f;
-    for (int c = 0; c < num_chunks; ++c) {
-      const int buf = c & 1;
-      mbar_wait(&tfull[buf], (c >> 1) & 1);
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      for (int j = 0; j < BN; ++j) acc[j] = 0.0f;
+      const int nchunks = (ti.num_kb + KC - 1) / KC;
+      for (int c = 0; c < nchunks; ++c, ++chunk) {
+        const uint32_t buf = chunk & 1;
+        mbar_wait(&tfull[buf], (chunk >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
-      for (int c0 = 0; c0 < BN; c0 += 32) {
-        uint32_t v[32];
-        tmem_ld32(tmem + (uint32_t(sub * 32) << 16) + uint32_t(buf * BN + c0), v);
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+          uint32_t v[32];
+          tmem_ld32(tmem + (uint32_t(sub * 32) << 16) + buf * BN + uint32_t(c0), v);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-        for (int j = 0; j < 32; ++j) acc[c0 + j] += __uint_as_float(v[j]);
+          for (int j = 0; j < 32; ++j) acc[c0 + j] += __uint_as_float(v[j]);
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[buf]);
       }
-      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[buf]);
-    }
-    if (ep.dbg) {
-      const float* sm = reinterpret_cast<const float*>(smem);
-      for (int i = threadIdx.x - 64; i < STAGE_BYTES / 4; i += 128) ep.dbg[i] = sm[i];
-    }
-    if (ep.ws && row < ep.M) {
-      // split-K partial: raw accumulator, dense [M][N] per (split, z)
-      float* prow = ep.ws + ((long long)split * ep.zcount + z) * ((long long)ep.M * ep.N) + (long long)row * ep.N + n0;
-      const int nvalid = ep.N - n0;
+      if (row >= ep.M) continue;
+      const int z1 = ti.z % ep.Z1, z2 = ti.z / ep.Z1;
+      const int nvalid = ep.N - ti.n0;
+      if (ep.ws) {
+        // split-K partial: raw accumulator, dense [M][N] per (split, z)
+        float* prow = ep.ws + ((long long)ti.split * ep.zcount + ti.z) * ((long long)ep.M * ep.N) +
+                      (long long)row * ep.N + ti.n0;
 #pragma unroll
-      for (int j = 0; j < BN; ++j)
-        if (j < nvalid) prow[j] = acc[j];
-    } else if (row < ep.M) {
-      const long long off = z1 * ep.sc1 + z2 * ep.sc2 + (long long)row * ep.ldc + n0;
+        for (int j = 0; j < BN; ++j)
+          if (j < nvalid) prow[j] = acc[j];
+        continue;
+      }
+      const long long off = z1 * ep.sc1 + z2 * ep.sc2 + (long long)row * ep.ldc + ti.n0;
       float* crow = ep.C + off;
       float* srow = ep.Cs ? ep.Cs + off : nullptr;
-      const float* brow = ep.bias ? ep.bias + n0 : nullptr;
-      const int nvalid = ep.N - n0;
+      const float* brow = ep.bias ? ep.bias + ti.n0 : nullptr;
       const bool vec = nvalid >= BN && ((reinterpret_cast<uintptr_t>(crow) & 15) == 0) &&
                        (!srow || (reinterpret_cast<uintptr_t>(srow) & 15) == 0);
       if (vec) {
@@ -413,12 +451,10 @@ void make_map(CUtensorMap* m, const float* base, long long inner, long long oute
   cuuint32_t es[4] = {1, 1, 1, 1};
   const CUresult r = encoder()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(base), dims, strides, box, es,
                                CU_TENSOR_MAP_INTERLEAVE_NONE,
-                               mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                               mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_64B,
                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) fail(SD_CUDA_ERROR, "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
 }
-
-constexpr int kNumSMs = 148;
 
 // C = alpha * sum_split partial[split] + beta * C + bias (fixed split order)
 __global__ void k_splitk_reduce(const float* __restrict__ ws, int splits, int zc, int Z1, int M, int N,
@@ -459,8 +495,9 @@ struct Prof {
   bool on = false;
   std::vector<cudaEvent_t> ev;
   std::vector<double> flops;
+  std::vector<std::string> tags;  // "M,N,K,batch,a_mn,b_mn,causal,splits" per launch
   size_t used = 0;
-  double pending_flops = 0;
+  std::string next_tag;
 };
 Prof& prof() {
   static Prof p;
@@ -481,6 +518,7 @@ void prof_end(cudaStream_t s, double flops) {
   if (!p.on) return;
   SD_CUDA(cudaEventRecord(p.ev[p.used + 1], s));
   p.flops.push_back(flops);
+  p.tags.push_back(p.next_tag);
   p.used += 2;
 }
 
@@ -503,18 +541,21 @@ void launch(const GemmArgs& g, cudaStream_t s) {
     make_map(&mBs, THREE ? g.Bs : g.B, g.K, g.N, g.ldb, g.Z1, g.sb1, g.Z2, g.sb2, BK, BN, false);
   }
   const int zc = g.Z1 * g.Z2;
-  const int tiles = ((g.N + BN - 1) / BN) * ((g.M + BM - 1) / BM) * zc;
+  const int tn = (g.N + BN - 1) / BN, tm = (g.M + BM - 1) / BM;
+  const int tiles = tn * tm * zc;
   const int total_kb = (g.K + BK - 1) / BK;
   // split-K when the output grid cannot fill the 148 SMs and K is long (the
   // Hv weight products reduce over all T tokens): partial tiles go to a
   // workspace and are summed in a fixed order by k_splitk_reduce.
   int splits = 1;
-  if (g.causal == 0 && tiles < kNumSMs && total_kb >= 32) splits = std::min(std::min(total_kb / 16, 16), (2 * kNumSMs + tiles - 1) / tiles);
+  if (g.causal == 0 && 2 * tiles <= kNumSMs && total_kb >= 64)
+    splits = std::min(std::min(total_kb / 32, 16), (2 * kNumSMs + tiles - 1) / tiles);
   const int kb_per = (total_kb + splits - 1) / splits;
   splits = (total_kb + kb_per - 1) / kb_per;
   float* ws = nullptr;
   if (splits > 1) ws = splitk_workspace(size_t(splits) * zc * size_t(g.M) * g.N);
-  EpiParams ep{g.C, g.ldc, g.sc1, g.sc2, g.M, g.N, g.Z1, g.alpha, g.beta, g.bias, g.Cs, g.dbg, zc, kb_per, ws, g.causal};
+  EpiParams ep{g.C, g.ldc, g.sc1, g.sc2, g.M, g.N, g.Z1, g.alpha, g.beta, g.bias, g.Cs, g.dbg, zc, kb_per, ws,
+               g.causal, tn, tm, tiles * splits};
   constexpr int NT = THREE ? 4 : 2;
   const size_t smem = 1024 + STAGES * NT * TILE_BYTES + 256;
   auto kern = k_gemm_tf32<A_MN, B_MN, THREE>;
@@ -523,7 +564,11 @@ void launch(const GemmArgs& g, cudaStream_t s) {
     SD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     attr_set = true;
   }
-  dim3 grid((g.N + BN - 1) / BN, (g.M + BM - 1) / BM, zc * splits);
+  const int grid = std::min(ep.n_tiles, kNumSMs);
+  if (prof().on)
+    prof().next_tag = std::to_string(g.M) + "," + std::to_string(g.N) + "," + std::to_string(g.K) + "," +
+                      std::to_string(zc) + "," + std::to_string(int(A_MN)) + "," + std::to_string(int(B_MN)) + "," +
+                      std::to_string(g.causal) + "," + std::to_string(splits);
   prof_begin(s);
   kern<<<grid, NUM_THREADS, smem, s>>>(mA, mAs, mB, mBs, g.K, ep);
   SD_LAUNCHED("k_gemm_tf32");
@@ -564,8 +609,6 @@ void split_tf32(const float* x, float* small, long long n, int mode, cudaStream_
 
 extern "C" {
 
-float* sd_gemm_debug_buffer = nullptr;  // test hook: set from tests to capture smem stage 0
-
 sd_status sd_gemm_tf32(const sd_gemm_desc* d, sd_stream s) {
   return sd::guard([&] {
     sd::GemmArgs g;
@@ -592,7 +635,6 @@ sd_status sd_gemm_tf32(const sd_gemm_desc* d, sd_stream s) {
     g.sb2 = d->sb2;
     g.sc1 = d->sc1;
     g.sc2 = d->sc2;
-    g.dbg = sd_gemm_debug_buffer;
     sd::gemm(g, (cudaStream_t)s);
   });
 }
@@ -605,6 +647,7 @@ sd_status sd_gemm_profile_begin(void) {
     p.on = true;
     p.used = 0;
     p.flops.clear();
+    p.tags.clear();
   });
 }
 
@@ -623,6 +666,23 @@ sd_status sd_gemm_profile_end(double* ms, double* flops, uint64_t* launches) {
     *ms = t;
     *flops = f;
     *launches = p.flops.size();
+  });
+}
+
+// Per-launch record of the last profiling window as CSV lines
+// "M,N,K,batch,a_mn,b_mn,causal,splits,ms,flops" (call after profile_end).
+sd_status sd_gemm_profile_dump(const char* path) {
+  return sd::guard([&] {
+    auto& p = sd::prof();
+    FILE* f = std::fopen(path, "w");
+    if (!f) sd::fail(SD_ARGUMENT_ERROR, "cannot open profile dump path");
+    std::fprintf(f, "M,N,K,batch,a_mn,b_mn,causal,splits,ms,flops\n");
+    for (size_t i = 0; i + 1 < p.used; i += 2) {
+      float x = 0;
+      SD_CUDA(cudaEventElapsedTime(&x, p.ev[i], p.ev[i + 1]));
+      std::fprintf(f, "%s,%.6f,%.0f\n", p.tags[i / 2].c_str(), x, p.flops[i / 2]);
+    }
+    std::fclose(f);
   });
 }
 
