@@ -41,7 +41,7 @@ namespace {
 // 192 KB of shared memory: enough bytes in flight to cover TMA latency.
 constexpr int BM = 128, BN = 128, BK = 16, STAGES = 6;
 constexpr int TILE_BYTES = BM * BK * 4;  // 8 KB per operand tile (BN == BM)
-constexpr int NUM_THREADS = 192;
+constexpr int NUM_THREADS = 320;  // producer, MMA, 8 epilogue warps
 constexpr uint32_t TMEM_COLS = 2 * BN;  // two accumulation buffers
 constexpr int kNumSMs = 148;
 
@@ -160,6 +160,7 @@ __device__ __forceinline__ uint64_t tile_desc(uint32_t base, int ks) {
 // finished chunk into round-to-nearest fp32 registers while the MMA warp
 // fills the other buffer (chunks continue across the tiles of a CTA).
 constexpr int KC = 8;  // k-blocks (8 x 16 = 128 of K) per TMEM chunk
+constexpr int EC = 64;  // accumulator columns per epilogue thread (8 epilogue warps)
 
 struct TileInfo {
   int n0, m0, z, split, kb0, num_kb;
@@ -216,7 +217,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], 4);
+      mbar_init(&tempty[b], 8);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -309,26 +310,28 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
     }
   } else {
-    // epilogue: warp w drains TMEM lanes 32*(w%4) .. +31 (its sub-partition);
-    // thread = one output row, BN fp32 accumulators in registers.
+    // epilogue: 8 warps; warp w drains TMEM lanes 32*(w%4) .. +31 (its
+    // sub-partition) and the column half (w-2)/4 of the tile: thread = one
+    // output row, EC = 64 fp32 accumulators in registers.
     const int sub = warp & 3;
+    const int cb = ((warp - 2) >> 2) * EC;
     uint32_t chunk = 0;
     for (int t = blockIdx.x; t < ep.n_tiles; t += gridDim.x) {
       const TileInfo ti = tile_info(ep, t, K);
       if (ti.skip) continue;
       const int row = ti.m0 + sub * 32 + lane;
-      float acc[BN];
+      float acc[EC];
 #pragma unroll
-      for (int j = 0; j < BN; ++j) acc[j] = 0.0f;
+      for (int j = 0; j < EC; ++j) acc[j] = 0.0f;
       const int nchunks = (ti.num_kb + KC - 1) / KC;
       for (int c = 0; c < nchunks; ++c, ++chunk) {
         const uint32_t buf = chunk & 1;
         mbar_wait(&tfull[buf], (chunk >> 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
-        for (int c0 = 0; c0 < BN; c0 += 32) {
+        for (int c0 = 0; c0 < EC; c0 += 32) {
           uint32_t v[32];
-          tmem_ld32(tmem + (uint32_t(sub * 32) << 16) + buf * BN + uint32_t(c0), v);
+          tmem_ld32(tmem + (uint32_t(sub * 32) << 16) + buf * BN + uint32_t(cb + c0), v);
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
           for (int j = 0; j < 32; ++j) acc[c0 + j] += __uint_as_float(v[j]);
@@ -339,25 +342,27 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
       if (row >= ep.M) continue;
       const int z1 = ti.z % ep.Z1, z2 = ti.z / ep.Z1;
-      const int nvalid = ep.N - ti.n0;
+      const int n0 = ti.n0 + cb;
+      const int nvalid = ep.N - n0;
+      if (nvalid <= 0) continue;
       if (ep.ws) {
         // split-K partial: raw accumulator, dense [M][N] per (split, z)
         float* prow = ep.ws + ((long long)ti.split * ep.zcount + ti.z) * ((long long)ep.M * ep.N) +
-                      (long long)row * ep.N + ti.n0;
+                      (long long)row * ep.N + n0;
 #pragma unroll
-        for (int j = 0; j < BN; ++j)
+        for (int j = 0; j < EC; ++j)
           if (j < nvalid) prow[j] = acc[j];
         continue;
       }
-      const long long off = z1 * ep.sc1 + z2 * ep.sc2 + (long long)row * ep.ldc + ti.n0;
+      const long long off = z1 * ep.sc1 + z2 * ep.sc2 + (long long)row * ep.ldc + n0;
       float* crow = ep.C + off;
       float* srow = ep.Cs ? ep.Cs + off : nullptr;
-      const float* brow = ep.bias ? ep.bias + ti.n0 : nullptr;
-      const bool vec = nvalid >= BN && ((reinterpret_cast<uintptr_t>(crow) & 15) == 0) &&
+      const float* brow = ep.bias ? ep.bias + n0 : nullptr;
+      const bool vec = nvalid >= EC && ((reinterpret_cast<uintptr_t>(crow) & 15) == 0) &&
                        (!srow || (reinterpret_cast<uintptr_t>(srow) & 15) == 0);
       if (vec) {
 #pragma unroll
-        for (int j = 0; j < BN; j += 4) {
+        for (int j = 0; j < EC; j += 4) {
           float4 o = make_float4(ep.alpha * acc[j], ep.alpha * acc[j + 1], ep.alpha * acc[j + 2], ep.alpha * acc[j + 3]);
           if (ep.beta != 0.0f) {
             const float4 old = *reinterpret_cast<const float4*>(crow + j);
@@ -383,7 +388,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
       } else {
 #pragma unroll
-        for (int j = 0; j < BN; ++j) {
+        for (int j = 0; j < EC; ++j) {
           if (j < nvalid) {
             float r = ep.alpha * acc[j];
             if (ep.beta != 0.0f) r += ep.beta * crow[j];
