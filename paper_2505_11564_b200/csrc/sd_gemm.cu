@@ -39,11 +39,21 @@ namespace {
 
 // BK = 16 fp32 (64 B) per stage keeps a 6-deep ring of 4 operand tiles in
 // 192 KB of shared memory: enough bytes in flight to cover TMA latency.
-constexpr int BM = 128, BN = 128, BK = 16, STAGES = 6;
-constexpr int TILE_BYTES = BM * BK * 4;  // 8 KB per operand tile (BN == BM)
+constexpr int BM = 128, BK = 16;
 constexpr int NUM_THREADS = 320;  // producer, MMA, 8 epilogue warps
-constexpr uint32_t TMEM_COLS = 2 * BN;  // two accumulation buffers
 constexpr int kNumSMs = 148;
+
+// Tile-width dependent constants: BN = 128 for general products, BN = 64 for
+// the per-head attention products whose N is the head dimension (64).
+template <int BN_>
+struct Cfg {
+  static constexpr int BN = BN_;
+  static constexpr int A_BYTES = BM * BK * 4;         // 8 KB per A tile
+  static constexpr int B_BYTES = BN_ * BK * 4;        // 8 / 4 KB per B tile
+  static constexpr int STAGES = BN_ == 128 ? 6 : 8;   // <= 192 KB ring
+  static constexpr uint32_t TMEM_COLS = 2 * BN_;      // two accumulation buffers
+  static constexpr int EC = BN_ / 2;                  // accumulator columns per epilogue thread
+};
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -92,14 +102,14 @@ __device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint
   return d;
 }
 
-// Instruction descriptor: kind::tf32, fp32 accumulate, M=128, N=BN.
-__host__ __device__ constexpr uint32_t make_idesc(bool a_mn, bool b_mn) {
+// Instruction descriptor: kind::tf32, fp32 accumulate, M=128, N=bn.
+__host__ __device__ constexpr uint32_t make_idesc(bool a_mn, bool b_mn, int bn) {
   return (1u << 4)                 // D format F32
          | (2u << 7)               // A format TF32
          | (2u << 10)              // B format TF32
          | (uint32_t(a_mn) << 15)  // A major
          | (uint32_t(b_mn) << 16)  // B major
-         | (uint32_t(BN >> 3) << 17) | (uint32_t(BM >> 4) << 24);
+         | (uint32_t(bn >> 3) << 17) | (uint32_t(BM >> 4) << 24);
 }
 
 __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
@@ -160,13 +170,13 @@ __device__ __forceinline__ uint64_t tile_desc(uint32_t base, int ks) {
 // finished chunk into round-to-nearest fp32 registers while the MMA warp
 // fills the other buffer (chunks continue across the tiles of a CTA).
 constexpr int KC = 8;  // k-blocks (8 x 16 = 128 of K) per TMEM chunk
-constexpr int EC = 64;  // accumulator columns per epilogue thread (8 epilogue warps)
 
 struct TileInfo {
   int n0, m0, z, split, kb0, num_kb;
   bool skip;
 };
 
+template <int BN>
 __device__ __forceinline__ TileInfo tile_info(const EpiParams& ep, int t, int K) {
   TileInfo ti;
   const int nt = t % ep.n_tiles_n;
@@ -193,15 +203,18 @@ __device__ __forceinline__ TileInfo tile_info(const EpiParams& ep, int t, int K)
   return ti;
 }
 
-template <bool A_MN, bool B_MN, bool THREE>
+template <bool A_MN, bool B_MN, bool THREE, int BN_>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     k_gemm_tf32(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mAs,
                 const __grid_constant__ CUtensorMap mB, const __grid_constant__ CUtensorMap mBs, int K, EpiParams ep) {
+  using Cf = Cfg<BN_>;
+  constexpr int BN = Cf::BN, STAGES = Cf::STAGES, EC = Cf::EC;
+  constexpr int A_BYTES = Cf::A_BYTES, B_BYTES = Cf::B_BYTES;
+  constexpr uint32_t TMEM_COLS = Cf::TMEM_COLS;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // 1024-byte aligned ring: per stage [A | As | B | Bs]
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  constexpr int NT = THREE ? 4 : 2;
-  constexpr int STAGE_BYTES = NT * TILE_BYTES;
+  constexpr int STAGE_BYTES = (THREE ? 2 : 1) * (A_BYTES + B_BYTES);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;  // [2]
@@ -237,7 +250,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       asm volatile("prefetch.tensormap [%0];" ::"l"(&mB) : "memory");
       uint32_t g = 0;  // global k-block counter (ring position)
       for (int t = blockIdx.x; t < ep.n_tiles; t += gridDim.x) {
-        const TileInfo ti = tile_info(ep, t, K);
+        const TileInfo ti = tile_info<BN>(ep, t, K);
         if (ti.skip) continue;
         const int z1 = ti.z % ep.Z1, z2 = ti.z / ep.Z1;
         for (int kb = 0; kb < ti.num_kb; ++kb, ++g) {
@@ -249,33 +262,33 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const int k0 = (ti.kb0 + kb) * BK;
           if (A_MN) {
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
+            for (int c = 0; c < BM / 32; ++c) {
               tma_load_4d(&mA, &full[s], st + c * 2048, ti.m0 + 32 * c, k0, z1, z2);
-              if (THREE) tma_load_4d(&mAs, &full[s], st + TILE_BYTES + c * 2048, ti.m0 + 32 * c, k0, z1, z2);
+              if (THREE) tma_load_4d(&mAs, &full[s], st + A_BYTES + c * 2048, ti.m0 + 32 * c, k0, z1, z2);
             }
           } else {
             tma_load_4d(&mA, &full[s], st, k0, ti.m0, z1, z2);
-            if (THREE) tma_load_4d(&mAs, &full[s], st + TILE_BYTES, k0, ti.m0, z1, z2);
+            if (THREE) tma_load_4d(&mAs, &full[s], st + A_BYTES, k0, ti.m0, z1, z2);
           }
-          unsigned char* sb = st + (THREE ? 2 : 1) * TILE_BYTES;
+          unsigned char* sb = st + (THREE ? 2 : 1) * A_BYTES;
           if (B_MN) {
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
+            for (int c = 0; c < BN / 32; ++c) {
               tma_load_4d(&mB, &full[s], sb + c * 2048, ti.n0 + 32 * c, k0, z1, z2);
-              if (THREE) tma_load_4d(&mBs, &full[s], sb + TILE_BYTES + c * 2048, ti.n0 + 32 * c, k0, z1, z2);
+              if (THREE) tma_load_4d(&mBs, &full[s], sb + B_BYTES + c * 2048, ti.n0 + 32 * c, k0, z1, z2);
             }
           } else {
             tma_load_4d(&mB, &full[s], sb, k0, ti.n0, z1, z2);
-            if (THREE) tma_load_4d(&mBs, &full[s], sb + TILE_BYTES, k0, ti.n0, z1, z2);
+            if (THREE) tma_load_4d(&mBs, &full[s], sb + B_BYTES, k0, ti.n0, z1, z2);
           }
         }
       }
     }
   } else if (warp == 1) {
-    constexpr uint32_t idesc = make_idesc(A_MN, B_MN);
+    constexpr uint32_t idesc = make_idesc(A_MN, B_MN, BN);
     uint32_t g = 0, chunk = 0;
     for (int t = blockIdx.x; t < ep.n_tiles; t += gridDim.x) {
-      const TileInfo ti = tile_info(ep, t, K);
+      const TileInfo ti = tile_info<BN>(ep, t, K);
       if (ti.skip) continue;
       for (int kb = 0; kb < ti.num_kb; ++kb, ++g) {
         const int s = g % STAGES;
@@ -289,8 +302,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (lane == 0) {
           const uint32_t d = tmem + buf * BN;
           const uint32_t st = smem_u32(smem + s * STAGE_BYTES);
-          const uint32_t a = st, as = st + TILE_BYTES;
-          const uint32_t b = st + (THREE ? 2 : 1) * TILE_BYTES, bs = b + TILE_BYTES;
+          const uint32_t a = st, as = st + A_BYTES;
+          const uint32_t b = st + (THREE ? 2 : 1) * A_BYTES, bs = b + B_BYTES;
 #pragma unroll
           for (int ks = 0; ks < BK / 8; ++ks) {
             const uint32_t acc0 = (first && ks == 0) ? 0u : 1u;
@@ -312,12 +325,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   } else {
     // epilogue: 8 warps; warp w drains TMEM lanes 32*(w%4) .. +31 (its
     // sub-partition) and the column half (w-2)/4 of the tile: thread = one
-    // output row, EC = 64 fp32 accumulators in registers.
+    // output row, EC = BN/2 fp32 accumulators in registers.
     const int sub = warp & 3;
     const int cb = ((warp - 2) >> 2) * EC;
     uint32_t chunk = 0;
     for (int t = blockIdx.x; t < ep.n_tiles; t += gridDim.x) {
-      const TileInfo ti = tile_info(ep, t, K);
+      const TileInfo ti = tile_info<BN>(ep, t, K);
       if (ti.skip) continue;
       const int row = ti.m0 + sub * 32 + lane;
       float acc[EC];
@@ -527,8 +540,9 @@ void prof_end(cudaStream_t s, double flops) {
   p.used += 2;
 }
 
-template <bool A_MN, bool B_MN, bool THREE>
+template <bool A_MN, bool B_MN, bool THREE, int BN>
 void launch(const GemmArgs& g, cudaStream_t s) {
+  using Cf = Cfg<BN>;
   CUtensorMap mA, mAs, mB, mBs;
   // A logical M x K. K-major: rows = M (ld = lda), inner = K. MN-major: rows = K, inner = M.
   if (A_MN) {
@@ -561,9 +575,8 @@ void launch(const GemmArgs& g, cudaStream_t s) {
   if (splits > 1) ws = splitk_workspace(size_t(splits) * zc * size_t(g.M) * g.N);
   EpiParams ep{g.C, g.ldc, g.sc1, g.sc2, g.M, g.N, g.Z1, g.alpha, g.beta, g.bias, g.Cs, g.dbg, zc, kb_per, ws,
                g.causal, tn, tm, tiles * splits};
-  constexpr int NT = THREE ? 4 : 2;
-  const size_t smem = 1024 + STAGES * NT * TILE_BYTES + 256;
-  auto kern = k_gemm_tf32<A_MN, B_MN, THREE>;
+  const size_t smem = 1024 + size_t(Cf::STAGES) * (THREE ? 2 : 1) * (Cf::A_BYTES + Cf::B_BYTES) + 256;
+  auto kern = k_gemm_tf32<A_MN, B_MN, THREE, BN>;
   static bool attr_set = false;
   if (!attr_set) {
     SD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
@@ -591,8 +604,12 @@ void launch(const GemmArgs& g, cudaStream_t s) {
 void gemm(const GemmArgs& g, cudaStream_t s) {
   if (g.M <= 0 || g.N <= 0 || g.K <= 0) return;
   const bool three = g.As != nullptr && g.Bs != nullptr;
-#define SD_GEMM_CASE(AM, BMJ, TH) \
-  if (g.a_mn == AM && g.b_mn == BMJ && three == TH) return launch<AM, BMJ, TH>(g, s);
+  const bool narrow = g.N <= 64;  // head-dimension outputs: 64-wide tiles
+#define SD_GEMM_CASE(AM, BMJ, TH)                                  \
+  if (g.a_mn == AM && g.b_mn == BMJ && three == TH) {              \
+    if (narrow) return launch<AM, BMJ, TH, 64>(g, s);              \
+    return launch<AM, BMJ, TH, 128>(g, s);                         \
+  }
   SD_GEMM_CASE(false, false, true)
   SD_GEMM_CASE(false, true, true)
   SD_GEMM_CASE(true, false, true)

@@ -19,7 +19,7 @@ def rel(a, b):
 
 @pytest.mark.parametrize("a_t", [False, True])
 @pytest.mark.parametrize("b_t", [False, True])
-@pytest.mark.parametrize("shape", [(128, 128, 32), (256, 384, 768), (200, 300, 100), (1000, 520, 264)])
+@pytest.mark.parametrize("shape", [(128, 128, 32), (256, 384, 768), (200, 300, 100), (1000, 520, 264), (256, 64, 1024), (300, 40, 200)])
 def test_gemm_majors(G, a_t, b_t, shape):
     M, N, K = shape
     g = torch.Generator(device="cuda").manual_seed(M * 7 + N + K)
