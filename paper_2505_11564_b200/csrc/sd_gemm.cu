@@ -25,6 +25,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <mutex>
@@ -50,7 +51,7 @@ struct Cfg {
   static constexpr int BN = BN_;
   static constexpr int A_BYTES = BM * BK * 4;         // 8 KB per A tile
   static constexpr int B_BYTES = BN_ * BK * 4;        // 8 / 4 KB per B tile
-  static constexpr int STAGES = BN_ == 128 ? 6 : 8;   // <= 192 KB ring
+  static constexpr int STAGES = BN_ == 256 ? 4 : (BN_ == 128 ? 6 : 8);  // <= 192 KB ring
   static constexpr uint32_t TMEM_COLS = 2 * BN_;      // two accumulation buffers
   static constexpr int EC = BN_ / 2;                  // accumulator columns per epilogue thread
 };
@@ -566,9 +567,19 @@ void launch(const GemmArgs& g, cudaStream_t s) {
   // split-K when the output grid cannot fill the 148 SMs and K is long (the
   // Hv weight products reduce over all T tokens): partial tiles go to a
   // workspace and are summed in a fixed order by k_splitk_reduce.
+  // Choose the split count minimising waves-per-unit-of-work
+  // ceil(tiles*s/148)/s (each split keeps >= 16 k-blocks), smallest s on ties.
   int splits = 1;
-  if (g.causal == 0 && 2 * tiles <= kNumSMs && total_kb >= 64)
-    splits = std::min(std::min(total_kb / 32, 16), (2 * kNumSMs + tiles - 1) / tiles);
+  if (g.causal == 0 && tiles < kNumSMs && total_kb >= 32) {
+    double best = 1.0;
+    for (int s2 = 2; s2 <= 16 && total_kb / s2 >= 16; ++s2) {
+      const double cost = double((tiles * s2 + kNumSMs - 1) / kNumSMs) / s2 + 0.04 * s2;  // + reduce traffic
+      if (cost < best - 1e-9) {
+        best = cost;
+        splits = s2;
+      }
+    }
+  }
   const int kb_per = (total_kb + splits - 1) / splits;
   splits = (total_kb + kb_per - 1) / kb_per;
   float* ws = nullptr;
@@ -599,15 +610,29 @@ void launch(const GemmArgs& g, cudaStream_t s) {
   prof_end(s, 2.0 * double(g.M) * g.N * g.K * g.Z1 * g.Z2);
 }
 
+bool sd_gemm_wide_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("SD_GEMM_WIDE");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 }  // namespace
 
 void gemm(const GemmArgs& g, cudaStream_t s) {
   if (g.M <= 0 || g.N <= 0 || g.K <= 0) return;
   const bool three = g.As != nullptr && g.Bs != nullptr;
   const bool narrow = g.N <= 64;  // head-dimension outputs: 64-wide tiles
+  // 256-wide tiles halve the shared-memory operand traffic per MMA flop (the
+  // tf32 SS-MMA at N=128 is shared-memory-bandwidth bound) when there are
+  // enough output tiles to fill the machine.
+  const long long t256 = (long long)((g.N + 255) / 256) * ((g.M + BM - 1) / BM) * g.Z1 * g.Z2;
+  const bool wide = g.N >= 256 && t256 >= 2 * kNumSMs && g.causal == 0 && sd_gemm_wide_enabled();
 #define SD_GEMM_CASE(AM, BMJ, TH)                                  \
   if (g.a_mn == AM && g.b_mn == BMJ && three == TH) {              \
     if (narrow) return launch<AM, BMJ, TH, 64>(g, s);              \
+    if (wide) return launch<AM, BMJ, TH, 256>(g, s);               \
     return launch<AM, BMJ, TH, 128>(g, s);                         \
   }
   SD_GEMM_CASE(false, false, true)

@@ -79,3 +79,13 @@ def test_gemm_split_k(G, a_t, b_t):
     G.gemm(M, N, K, A, A.shape[1], a_t, B, B.shape[1], not b_t, C, N, alpha=0.5, beta=2.0,
            a_small=G.split(A), b_small=G.split(B))
     assert torch.equal(C, first)  # deterministic split order
+
+
+def test_gemm_wide_tiles(G):
+    """Shapes that select the 256-wide tile path (enough output tiles)."""
+    for (M, N, K, a_t, b_t) in [(4096, 2304, 256, False, False), (4096, 1024, 512, False, True),
+                                (2560, 2048, 300, True, False)]:
+        A = torch.randn(*((K, M) if a_t else (M, K)), device="cuda")
+        B = torch.randn(*((N, K) if b_t else (K, N)), device="cuda")
+        ref = (A.double().t() if a_t else A.double()) @ (B.double().t() if b_t else B.double())
+        assert rel(G.matmul(A, B, True, a_t, b_t), ref) < 2e-6
