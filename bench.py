@@ -7,7 +7,8 @@ the three-term recurrence plus full reorthogonalisation (2x classical
 Gram-Schmidt over every stored column). Workload = BASELINE configs[1]:
 GPT-2-small shape (124,439,808 params) random init, synthetic tokens, batch
 8 x 1024, 10 probes x 100 Lanczos steps, full reorth, fp32 (3xTF32 GEMMs).
-Timed: steps W .. W+K-1 of the probe chain (probes restart every k_max steps).
+Timed: K steps of the probe chain centred on column k_max/2 (probes restart
+every k_max steps), after W warm-up steps.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
@@ -152,7 +153,7 @@ def run_reference(args):
         return
     from paper_2505_11564_b200.gpt import GPT2_SMALL
     cfg = GPT2_SMALL
-    k_mid = args.warmup + args.steps // 2
+    k_mid = args.k_max // 2  # same mean reorth width as the GPU arm's timed window
     # each reference "step" is one bounded CPU sample (~1 min on 8 cores); at
     # most two are run so the arm ends within a few minutes
     n = max(1, min(args.steps, 2))
@@ -218,7 +219,11 @@ def run_ours(args):
         state["L"].step()
 
     new_chain()
-    for _ in range(args.warmup):
+    # untimed: W warm-up steps, then advance the chain so the timed window is
+    # centred on k_max/2 -- its mean reorthogonalisation width equals that of
+    # a whole k_max chain (full reorth cost grows linearly with the column)
+    advance = max(0, args.k_max // 2 - args.steps // 2 - args.warmup) if args.steps < args.k_max else 0
+    for _ in range(args.warmup + advance):
         step()
     torch.cuda.synchronize()
     if world > 1:
@@ -294,7 +299,8 @@ def run_ours(args):
         "config": {"workload": "BASELINE configs[1]: GPT-2-small shape 124M, batch 8x1024 tokens, "
                                "Rademacher probes, k_max=100, full reorth",
                    "model": "gpt2-small", "params": P, "global_batch": B, "seq_len": S, "k_max": args.k_max,
-                   "reorth_columns_timed": [j_first, j_last], "parallelism": f"dp{world} (HVP all-reduce)",
+                   "reorth_columns_timed": [j_first, j_last], "untimed_advance_steps": advance,
+                   "parallelism": f"dp{world} (HVP all-reduce)",
                    "l2": "inputs larger than L2 (0.5 GB Lanczos vectors, 45 GB activations)"},
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": tc_peak, "unit": "TFLOP/s",
                      "frac": achieved / tc_peak if tc_peak else None, "traffic": traffic,

@@ -19,7 +19,6 @@
 
 namespace sd {
 
-constexpr int kChunk = 32;    // elements per staged chunk of a grid block
 constexpr int kThreads = 128;
 
 // ------------------------------------------------------------------ probes
@@ -50,55 +49,78 @@ __global__ void k_probe(T* x, uint64_t begin, uint64_t n, uint64_t key, int dist
 // then the block folds of sum z[i]*y[i] (DOT=1) or y[i]*y[i] (DOT=2) over
 // full grid blocks. One CTA = kUnits consecutive grid blocks; thread t folds
 // block t. Elements are staged as [unit][33] tiles (conflict-free column walk).
+// 16-byte vector view of T (float4 / double2) for streaming loads.
 template <typename T>
-struct UnitsPerCta {
-  static constexpr int value = sizeof(T) == 4 ? 128 : 64;  // 33 KB of staging either way
+struct V16;
+template <>
+struct V16<float> {
+  using type = float4;
+  static constexpr int W = 4;
 };
+template <>
+struct V16<double> {
+  using type = double2;
+  static constexpr int W = 2;
+};
+template <typename T>
+union VU {
+  typename V16<T>::type v;
+  T a[V16<T>::W];
+};
+__device__ __forceinline__ bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
+// One THREAD per full grid block: it streams its 1024 elements with 16 B
+// loads (several in flight, unroll 4), applies the update element by element
+// and continues the block's serial f64 fold in element order.
 template <typename T, bool UPD, int DOT>
 __global__ void __launch_bounds__(128) k_axpy_dot_units(const T* __restrict__ x, T* __restrict__ y,
-                                                             const T* __restrict__ z, const double* coefp,
-                                                             uint64_t base, uint64_t n_units, uint64_t local_end,
-                                                             double* __restrict__ sums) {
-  constexpr int NU = UnitsPerCta<T>::value;  // == blockDim.x
-  __shared__ T ty[NU][kChunk + 1];
-  __shared__ T tz[DOT == 1 ? NU : 1][kChunk + 1];
-  const int tid = threadIdx.x;
-  const uint64_t unit0 = uint64_t(blockIdx.x) * NU;
+                                                        const T* __restrict__ z, const double* coefp, uint64_t base,
+                                                        uint64_t n_units, uint64_t local_end,
+                                                        double* __restrict__ sums) {
+  constexpr int W = V16<T>::W;
+  using V = typename V16<T>::type;
+  const uint64_t unit = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (unit >= n_units) return;
+  const uint64_t e0 = base + unit * kBlock;
+  const uint64_t n = (local_end - e0) < kBlock ? (local_end - e0) : kBlock;
   const double alpha = UPD ? -(*coefp) : 0.0;
   double acc = 0.0;
-  for (int c = 0; c < int(kBlock) / kChunk; ++c) {
-#pragma unroll 8
-    for (int p = 0; p < kChunk; ++p) {
-      const int e = p * NU + tid;
-      const int u = e >> 5, off = e & 31;
-      const uint64_t unit = unit0 + u;
-      const uint64_t li = base + unit * kBlock + uint64_t(c * kChunk + off);
-      T yv = T(0), zv = T(0);
-      if (unit < n_units && li < local_end) {
-        yv = y[li];
-        if (UPD) {
-          const double t = __dmul_rn(alpha, double(x[li]));
-          yv = round_to<T>(__dadd_rn(double(yv), t));
-          y[li] = yv;
-        }
-        if (DOT == 1) zv = z[li];
-      }
-      ty[u][off] = yv;
-      if (DOT == 1) tz[u][off] = zv;
-    }
-    __syncthreads();
-    if (DOT != 0) {
+  T* yp = y + e0;
+  const bool vec = n == kBlock && al16(yp) && (!UPD || al16(x + e0)) && (DOT != 1 || al16(z + e0));
+  if (vec) {
+#pragma unroll 4
+    for (int i = 0; i < int(kBlock) / W; ++i) {
+      VU<T> yv, xv, zv;
+      yv.v = reinterpret_cast<const V*>(yp)[i];
+      if (UPD) xv.v = __ldg(reinterpret_cast<const V*>(x + e0) + i);
+      if (DOT == 1) zv.v = __ldg(reinterpret_cast<const V*>(z + e0) + i);
+      if (UPD) {
 #pragma unroll
-      for (int k = 0; k < kChunk; ++k) {
-        const double a = double(ty[tid][k]);
-        const double b = DOT == 1 ? double(tz[tid][k]) : a;
-        acc = __dadd_rn(acc, __dmul_rn(a, b));
+        for (int k = 0; k < W; ++k) yv.a[k] = round_to<T>(__dadd_rn(double(yv.a[k]), __dmul_rn(alpha, double(xv.a[k]))));
+        reinterpret_cast<V*>(yp)[i] = yv.v;
+      }
+      if (DOT != 0) {
+#pragma unroll
+        for (int k = 0; k < W; ++k) {
+          const double a = double(yv.a[k]);
+          acc = __dadd_rn(acc, __dmul_rn(DOT == 1 ? double(zv.a[k]) : a, a));
+        }
       }
     }
-    __syncthreads();
+  } else {
+    for (uint64_t i = 0; i < n; ++i) {
+      T yv = yp[i];
+      if (UPD) {
+        yv = round_to<T>(__dadd_rn(double(yv), __dmul_rn(alpha, double(x[e0 + i]))));
+        yp[i] = yv;
+      }
+      if (DOT != 0) {
+        const double a = double(yv);
+        acc = __dadd_rn(acc, __dmul_rn(DOT == 1 ? double(z[e0 + i]) : a, a));
+      }
+    }
   }
-  if (DOT != 0 && unit0 + tid < n_units) sums[unit0 + tid] = acc;
+  if (DOT != 0) sums[unit] = acc;
 }
 
 // Head/tail elements of a shard (straddled grid blocks): update and emit raw
@@ -121,114 +143,129 @@ __global__ void k_axpy_dot_edges(const T* __restrict__ x, T* __restrict__ y, con
 }
 
 // ------------------------------------------------------ Gram-Schmidt pass
-// One WARP per full grid block (1024 elements), walked in 32-element chunks.
-//  update (UPD): lane = element; the j basis entries of the chunk arrive as j
-//    coalesced 128 B loads and are applied in the reference's order
-//    r = axpy(-c_0, q_0, r), ..., axpy(-c_{j-1}, q_{j-1}, r) (per-element f64
-//    product and sum, rounded to the storage precision after every axpy);
-//  fold (MODE 1): lane = column; each lane loads its column's 32 chunk
-//    elements as 128 B vectors and continues its serial f64 block fold of
-//    Q_i . r against the chunk's updated r (broadcast through shared memory);
-//  fold (MODE 2): lane 0 continues the serial fold of r . r.
-// Column accumulators live in registers: lane owns columns lane + 32 q.
-constexpr int kWarpsPerCta = 8;
-constexpr int kMaxColGroups = 8;  // j <= 256 per launch
+// Reorthogonalisation runs as two kernels per pass: an element-parallel
+// update (k_cgs_update) and a block-fold for the next pass's dots
+// (k_cgs_dots_pairs for few columns, warp-staged k_cgs_dots for many).
 
-template <typename T, int N>
-struct VecLoad;
-template <>
-struct VecLoad<float, 32> {
-  __device__ static void load(const float* p, float* out) {
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const float4 v = __ldg(reinterpret_cast<const float4*>(p) + i);
-      out[4 * i] = v.x, out[4 * i + 1] = v.y, out[4 * i + 2] = v.z, out[4 * i + 3] = v.w;
-    }
-  }
-};
-template <>
-struct VecLoad<double, 32> {
-  __device__ static void load(const double* p, double* out) {
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const double2 v = __ldg(reinterpret_cast<const double2*>(p) + i);
-      out[2 * i] = v.x, out[2 * i + 1] = v.y;
-    }
-  }
-};
-
-template <typename T, bool UPD, int MODE>
-__global__ void __launch_bounds__(32 * kWarpsPerCta) k_cgs_units(const T* __restrict__ Q, uint64_t ldq, int j,
-                                                                T* __restrict__ r, const double* __restrict__ coef,
-                                                                uint64_t base, uint64_t n_units, uint64_t local_end,
-                                                                uint64_t pstride, uint64_t head_n,
-                                                                double* __restrict__ partials) {
+// CGS update, element-parallel: every element applies the reference's j
+// sequential axpys r = axpy(-c_i, q_i, r) (f64 product and sum, rounded to
+// the storage type after each); 16 B vector loads of the j columns, several
+// in flight per thread.
+template <typename T>
+__global__ void __launch_bounds__(256) k_cgs_update(const T* __restrict__ Q, uint64_t ldq, int j, T* __restrict__ r,
+                                                    const double* __restrict__ coef, uint64_t n) {
   extern __shared__ double cs[];  // -coef[0..j)
-  __shared__ T rbuf[kWarpsPerCta][kChunk];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (UPD)
-    for (int i = threadIdx.x; i < j; i += blockDim.x) cs[i] = -coef[i];
+  for (int i = threadIdx.x; i < j; i += blockDim.x) cs[i] = -coef[i];
   __syncthreads();
-  const uint64_t unit = uint64_t(blockIdx.x) * kWarpsPerCta + warp;
-  if (unit >= n_units) return;
-  const uint64_t e0 = base + unit * kBlock;
-  const uint64_t n_el = (local_end - e0) < kBlock ? (local_end - e0) : kBlock;
-  const bool vec_ok = ((reinterpret_cast<uintptr_t>(Q + e0) | (ldq * sizeof(T))) & 15) == 0;
-  double acc[kMaxColGroups];
+  constexpr int W = V16<T>::W;
+  using V = typename V16<T>::type;
+  const uint64_t e = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) * W;
+  if (e >= n) return;
+  if (e + W <= n && al16(r + e) && al16(Q + e) && ((ldq * sizeof(T)) & 15) == 0) {
+    VU<T> rv;
+    rv.v = *reinterpret_cast<const V*>(r + e);
+    double v[W];
 #pragma unroll
-  for (int q = 0; q < kMaxColGroups; ++q) acc[q] = 0.0;
-  double self = 0.0;
-  for (uint64_t off = 0; off < n_el; off += kChunk) {
-    const int cnt = int((n_el - off) < uint64_t(kChunk) ? (n_el - off) : kChunk);
-    const bool valid = lane < cnt;
-    const uint64_t li = e0 + off + lane;
-    T rv = valid ? r[li] : T(0);
-    if (UPD && valid) {
-      double v = double(rv);
-      const T* qp = Q + li;
-#pragma unroll 8
-      for (int i = 0; i < j; ++i) v = double(round_to<T>(__dadd_rn(v, __dmul_rn(cs[i], double(qp[uint64_t(i) * ldq])))));
-      rv = T(v);
-      r[li] = rv;
+    for (int k = 0; k < W; ++k) v[k] = double(rv.a[k]);
+#pragma unroll 4
+    for (int i = 0; i < j; ++i) {
+      VU<T> q;
+      q.v = __ldg(reinterpret_cast<const V*>(Q + uint64_t(i) * ldq + e));
+#pragma unroll
+      for (int k = 0; k < W; ++k) v[k] = double(round_to<T>(__dadd_rn(v[k], __dmul_rn(cs[i], double(q.a[k])))));
     }
-    if (MODE != 0) {
-      rbuf[warp][lane] = rv;
-      __syncwarp();
+#pragma unroll
+    for (int k = 0; k < W; ++k) rv.a[k] = T(v[k]);
+    *reinterpret_cast<V*>(r + e) = rv.v;
+  } else {
+    for (uint64_t m = e; m < n && m < e + W; ++m) {
+      double v = double(r[m]);
+      for (int i = 0; i < j; ++i) v = double(round_to<T>(__dadd_rn(v, __dmul_rn(cs[i], double(Q[uint64_t(i) * ldq + m])))));
+      r[m] = T(v);
     }
-    if (MODE == 1) {
+  }
+}
+
+// CGS dots for few columns (j < 24): one THREAD per (column, block) pair
+// streams the column's 1024 block elements with 16 B loads and runs the
+// serial f64 fold against r, staged once per block in shared memory.
+template <typename T, int NB>
+__global__ void __launch_bounds__(256) k_cgs_dots_pairs(const T* __restrict__ Q, uint64_t ldq, int j,
+                                                        const T* __restrict__ r, uint64_t base, uint64_t n_units,
+                                                        uint64_t local_end, uint64_t pstride, uint64_t head_n,
+                                                        double* __restrict__ partials) {
+  constexpr int W = V16<T>::W;
+  using V = typename V16<T>::type;
+  __shared__ __align__(16) T rs[NB][kBlock];
+  const uint64_t u0 = uint64_t(blockIdx.x) * NB;
+  for (int idx = threadIdx.x; idx < NB * int(kBlock); idx += blockDim.x) {
+    const int b = idx / int(kBlock), o = idx % int(kBlock);
+    const uint64_t e = base + (u0 + b) * kBlock + o;
+    rs[b][o] = (u0 + b < n_units && e < local_end) ? r[e] : T(0);
+  }
+  __syncthreads();
+  for (int p = threadIdx.x; p < NB * j; p += blockDim.x) {
+    const int col = p % j, b = p / j;
+    const uint64_t unit = u0 + b;
+    if (unit >= n_units) continue;
+    const uint64_t e0 = base + unit * kBlock;
+    const uint64_t n = (local_end - e0) < kBlock ? (local_end - e0) : kBlock;
+    const T* qp = Q + uint64_t(col) * ldq + e0;
+    const T* rb = rs[b];
+    double acc = 0.0;
+    if (n == kBlock && al16(qp)) {
+#pragma unroll 4
+      for (int i = 0; i < int(kBlock) / W; ++i) {
+        VU<T> q;
+        q.v = __ldg(reinterpret_cast<const V*>(qp) + i);
 #pragma unroll
-      for (int q = 0; q < kMaxColGroups; ++q) {
-        const int col = lane + 32 * q;
-        if (q * 32 < j && col < j) {
-          const T* cp = Q + uint64_t(col) * ldq + e0 + off;
-          double a = acc[q];
-          if (vec_ok && cnt == kChunk) {
-            T x[kChunk];
-            VecLoad<T, kChunk>::load(cp, x);
-#pragma unroll
-            for (int k = 0; k < kChunk; ++k) a = __dadd_rn(a, __dmul_rn(double(x[k]), double(rbuf[warp][k])));
-          } else {
-            for (int k = 0; k < cnt; ++k) a = __dadd_rn(a, __dmul_rn(double(cp[k]), double(rbuf[warp][k])));
-          }
-          acc[q] = a;
-        }
+        for (int k = 0; k < W; ++k) acc = __dadd_rn(acc, __dmul_rn(double(q.a[k]), double(rb[i * W + k])));
       }
-      __syncwarp();
-    } else if (MODE == 2) {
-      if (lane == 0)
-        for (int k = 0; k < cnt; ++k) self = __dadd_rn(self, __dmul_rn(double(rbuf[warp][k]), double(rbuf[warp][k])));
-      __syncwarp();
+    } else {
+      for (uint64_t i = 0; i < n; ++i) acc = __dadd_rn(acc, __dmul_rn(double(qp[i]), double(rb[i])));
     }
+    partials[uint64_t(col) * pstride + head_n + unit] = acc;
   }
-  if (MODE == 1) {
-#pragma unroll
-    for (int q = 0; q < kMaxColGroups; ++q) {
-      const int col = lane + 32 * q;
-      if (col < j) partials[uint64_t(col) * pstride + head_n + unit] = acc[q];
+}
+
+// CGS dots over full grid blocks. One WARP per (block, group of 32 columns):
+// per 32-element chunk the warp loads each column's chunk as one coalesced
+// 128 B row into a per-warp [32][33] shared tile (no CTA barrier), then lane c
+// continues the serial f64 fold of column c against the chunk of r.
+template <typename T>
+__global__ void __launch_bounds__(256) k_cgs_dots(const T* __restrict__ Q, uint64_t ldq, int j,
+                                                  const T* __restrict__ r, uint64_t base, uint64_t n_units,
+                                                  uint64_t local_end, uint64_t pstride, uint64_t head_n,
+                                                  double* __restrict__ partials) {
+  constexpr int WPC = sizeof(T) == 4 ? 8 : 4;  // warps per CTA (== blockDim.x / 32)
+  __shared__ T tile[WPC][32][33];
+  __shared__ T rbuf[WPC][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int groups = (j + 31) / 32;
+  const uint64_t gw = uint64_t(blockIdx.x) * WPC + warp;
+  const uint64_t unit = gw / groups;
+  if (unit >= n_units) return;
+  const int c0 = int(gw % groups) * 32;
+  const int ncol = (j - c0) < 32 ? (j - c0) : 32;
+  const uint64_t e0 = base + unit * kBlock;
+  const uint64_t n = (local_end - e0) < kBlock ? (local_end - e0) : kBlock;
+  const T* qb = Q + uint64_t(c0) * ldq + e0;
+  T(*tl)[33] = tile[warp];
+  double acc = 0.0;
+  for (uint64_t off = 0; off < n; off += 32) {
+    const int cnt = int((n - off) < 32 ? (n - off) : 32);
+    const bool valid = lane < cnt;
+    rbuf[warp][lane] = valid ? r[e0 + off + lane] : T(0);
+#pragma unroll 8
+    for (int c = 0; c < ncol; ++c) tl[c][lane] = valid ? __ldg(qb + uint64_t(c) * ldq + off + lane) : T(0);
+    __syncwarp();
+    if (lane < ncol) {
+#pragma unroll 8
+      for (int k = 0; k < cnt; ++k) acc = __dadd_rn(acc, __dmul_rn(double(tl[lane][k]), double(rbuf[warp][k])));
     }
-  } else if (MODE == 2 && lane == 0) {
-    partials[head_n + unit] = self;
+    __syncwarp();
   }
+  if (lane < ncol) partials[uint64_t(c0 + lane) * pstride + head_n + unit] = acc;
 }
 
 template <typename T, bool UPD, int MODE>
@@ -370,9 +407,8 @@ static void launch_axpy_dot(const void* x, void* y, const void* z, const double*
     constexpr bool U = decltype(upd_c)::value;
     constexpr int D = decltype(dot_c)::value;
     if (ps.n_sums) {
-      constexpr int NU = UnitsPerCta<T>::value;
-      const unsigned g = unsigned((ps.n_sums + NU - 1) / NU);
-      k_axpy_dot_units<T, U, D><<<g, NU, 0, s>>>((const T*)x, (T*)y, (const T*)z, coef, ps.n_head, ps.n_sums,
+      const unsigned g = unsigned((ps.n_sums + 127) / 128);
+      k_axpy_dot_units<T, U, D><<<g, 128, 0, s>>>((const T*)x, (T*)y, (const T*)z, coef, ps.n_head, ps.n_sums,
                                                        local_end, partial ? partial + ps.n_head : nullptr);
       SD_LAUNCHED("k_axpy_dot_units");
     }
@@ -406,38 +442,38 @@ static void launch_cgs(const void* Q, uint64_t ldq, uint64_t j, void* r, const d
   const uint64_t local_end = end - begin, plen = pstride ? pstride : ps.len();
   const uint64_t tail_begin = ps.n_head + ps.n_sums * kBlock;
   const bool upd = coef != nullptr;
-  if (j > uint64_t(32) * kMaxColGroups) fail(SD_ARGUMENT_ERROR, "cgs: more than 256 columns per pass");
-  const size_t smem = size_t(j) * sizeof(double);
-  auto run = [&](auto upd_c, auto mode_c) {
-    constexpr bool U = decltype(upd_c)::value;
-    constexpr int M = decltype(mode_c)::value;
+  if (!upd && mode == 0) fail(SD_ARGUMENT_ERROR, "cgs with neither update nor dots");
+  // (1) the j sequential axpys, element-parallel and streaming
+  if (upd) {
+    constexpr int W = V16<T>::W;
+    const uint64_t threads = (local_end + W - 1) / W;
+    k_cgs_update<T><<<unsigned((threads + 255) / 256), 256, size_t(j) * sizeof(double), s>>>(
+        (const T*)Q, ldq, int(j), (T*)r, coef, local_end);
+    SD_LAUNCHED("k_cgs_update");
+  }
+  // (2) the dots against the updated r
+  if (mode == 1) {
     if (ps.n_sums) {
-      auto kern = k_cgs_units<T, U, M>;
-      const unsigned g = unsigned((ps.n_sums + kWarpsPerCta - 1) / kWarpsPerCta);
-      kern<<<g, 32 * kWarpsPerCta, smem, s>>>((const T*)Q, ldq, int(j), (T*)r, coef, ps.n_head, ps.n_sums, local_end,
-                                              plen, ps.n_head, partials);
-      SD_LAUNCHED("k_cgs_units");
+      if (j < 24) {
+        constexpr int NB = sizeof(T) == 4 ? 8 : 4;  // 32 KB of staged r
+        k_cgs_dots_pairs<T, NB><<<unsigned((ps.n_sums + NB - 1) / NB), 256, 0, s>>>(
+            (const T*)Q, ldq, int(j), (const T*)r, ps.n_head, ps.n_sums, local_end, plen, ps.n_head, partials);
+      } else {
+        const uint64_t warps = ps.n_sums * ((j + 31) / 32);
+        constexpr unsigned WPC = sizeof(T) == 4 ? 8 : 4;
+        k_cgs_dots<T><<<unsigned((warps + WPC - 1) / WPC), 32 * WPC, 0, s>>>(
+            (const T*)Q, ldq, int(j), (const T*)r, ps.n_head, ps.n_sums, local_end, plen, ps.n_head, partials);
+      }
+      SD_LAUNCHED("k_cgs_dots");
     }
     if (ps.n_head + ps.n_tail) {
-      k_cgs_edges<T, U, M><<<grid_for(ps.n_head + ps.n_tail, 128), 128, 0, s>>>(
-          (const T*)Q, ldq, int(j), (T*)r, coef, ps.n_head, tail_begin, ps.n_tail, ps.n_head + ps.n_sums, plen,
+      k_cgs_edges<T, false, 1><<<grid_for(ps.n_head + ps.n_tail, 128), 128, 0, s>>>(
+          (const T*)Q, ldq, int(j), (T*)r, nullptr, ps.n_head, tail_begin, ps.n_tail, ps.n_head + ps.n_sums, plen,
           partials);
       SD_LAUNCHED("k_cgs_edges");
     }
-  };
-  using TT = std::true_type;
-  using FF = std::false_type;
-  using M0 = std::integral_constant<int, 0>;
-  using M1 = std::integral_constant<int, 1>;
-  using M2 = std::integral_constant<int, 2>;
-  if (upd) {
-    if (mode == 0) run(TT{}, M0{});
-    else if (mode == 1) run(TT{}, M1{});
-    else run(TT{}, M2{});
-  } else {
-    if (mode == 1) run(FF{}, M1{});
-    else if (mode == 2) run(FF{}, M2{});
-    else fail(SD_ARGUMENT_ERROR, "cgs with neither update nor dots");
+  } else if (mode == 2) {
+    launch_axpy_dot<T>(nullptr, r, nullptr, nullptr, begin, end, total, partials, s);
   }
 }
 
