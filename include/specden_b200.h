@@ -163,6 +163,11 @@ typedef struct {
   long long sa1, sa2, sb1, sb2, sc1, sc2;
 } sd_gemm_desc;
 sd_status sd_gemm_tf32(const sd_gemm_desc* d, sd_stream s);
+/* Dual source: C = alpha (op(A1) op(B1) + op(A2) op(B2)) + beta C in one
+ * accumulation (the tangent products of the HVP). d1 carries the shape, C,
+ * alpha/beta and the first pair; d2 only its a/b operands, lds and strides
+ * (m, n, k, majors and precision must match d1). */
+sd_status sd_gemm_tf32_dual(const sd_gemm_desc* d1, const sd_gemm_desc* d2, sd_stream s);
 /* small[i] = x[i] - hi(x[i]); mode 0: hi = trunc_tf32 (what the MMA reads),
  * mode 1: hi = round-to-nearest-away tf32. */
 sd_status sd_split_tf32(const float* x, float* small, uint64_t n, int mode, sd_stream s);

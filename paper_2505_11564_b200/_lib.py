@@ -7,10 +7,11 @@ There is no fallback: if the CUDA library is missing the import fails loudly.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
-LIB_PATH = PKG / "libspecden_b200.so"
+LIB_PATH = Path(os.environ["SD_LIB_OVERRIDE"]) if os.environ.get("SD_LIB_OVERRIDE") else PKG / "libspecden_b200.so"
 
 
 class SpecdenError(RuntimeError):

@@ -22,6 +22,10 @@ struct GemmArgs {
   float* dbg = nullptr;
   int causal = 0;  // causal attention structure, see k_gemm_tf32
   long long sa1 = 0, sa2 = 0, sb1 = 0, sb2 = 0, sc1 = 0, sc2 = 0;  // element strides
+  // optional second product accumulated into the same tile (dual source):
+  //   C = alpha (op(A) op(B) + op(A2) op(B2)) + beta C ; same M, N, K, majors
+  const float *A2 = nullptr, *A2s = nullptr, *B2 = nullptr, *B2s = nullptr;
+  long long lda2 = 0, ldb2 = 0, sa1_2 = 0, sa2_2 = 0, sb1_2 = 0, sb2_2 = 0;
 };
 void gemm(const GemmArgs& g, cudaStream_t s);
 void split_tf32(const float* x, float* small, long long n, int mode, cudaStream_t s);

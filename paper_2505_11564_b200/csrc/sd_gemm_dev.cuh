@@ -1,0 +1,297 @@
+// Device helpers shared by the 1-CTA and CTA-pair tcgen05 GEMM kernels
+// (sd_gemm.cu, sd_gemm_pair.cu): mbarriers, TMA, UMMA descriptors, TMEM
+// loads, epilogue parameters and the persistent tile walk.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <string>
+
+#include "sd_common.cuh"
+#include "sd_gemm.h"
+
+namespace sd {
+namespace gk {
+
+
+// BK = 16 fp32 (64 B) per stage keeps a 6-deep ring of 4 operand tiles in
+// 192 KB of shared memory: enough bytes in flight to cover TMA latency.
+constexpr int BM = 128, BK = 16;
+constexpr int NUM_THREADS = 320;  // producer, MMA, 8 epilogue warps
+constexpr int kNumSMs = 148;
+
+// Tile-width dependent constants: BN = 128 for general products, BN = 64 for
+// the per-head attention products whose N is the head dimension (64).
+template <int BN_>
+struct Cfg {
+  static constexpr int BN = BN_;
+  static constexpr int A_BYTES = BM * BK * 4;         // 8 KB per A tile
+  static constexpr int B_BYTES = BN_ * BK * 4;        // 8 / 4 KB per B tile
+  static constexpr int STAGES = BN_ == 256 ? 4 : (BN_ == 128 ? 6 : 8);  // <= 192 KB ring
+  static constexpr uint32_t TMEM_COLS = 2 * BN_;      // two accumulation buffers
+  static constexpr int EC = BN_ / 2;                  // accumulator columns per epilogue thread
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t"
+      "}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void tma_load_4d(const CUtensorMap* map, uint64_t* bar, void* dst, int c0, int c1, int c2,
+                                            int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], [%2];" ::
+          "r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+
+// UMMA shared-memory matrix descriptor. Layout codes: 4 = SWIZZLE_64B (K-major
+// tiles), 1 = SWIZZLE_128B_BASE32B (MN-major tf32 tiles: the only MN-major
+// smem layout the tf32 MMA accepts).
+__device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
+  uint64_t d = 0;
+  d |= uint64_t((saddr >> 4) & 0x3FFF);
+  d |= uint64_t((lbo >> 4) & 0x3FFF) << 16;
+  d |= uint64_t((sbo >> 4) & 0x3FFF) << 32;
+  d |= uint64_t(1) << 46;  // descriptor version (sm_100)
+  d |= uint64_t(layout) << 61;
+  return d;
+}
+
+// Instruction descriptor: kind::tf32, fp32 accumulate, M=128, N=bn.
+__host__ __device__ constexpr uint32_t make_idesc(bool a_mn, bool b_mn, int bn, int m = BM) {
+  return (1u << 4)                 // D format F32
+         | (2u << 7)               // A format TF32
+         | (2u << 10)              // B format TF32
+         | (uint32_t(a_mn) << 15)  // A major
+         | (uint32_t(b_mn) << 16)  // B major
+         | (uint32_t(bn >> 3) << 17) | (uint32_t(m >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t"
+      "}" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* v) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]),
+        "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+        "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+}
+
+struct EpiParams {
+  float* C;
+  long long ldc, sc1, sc2;
+  int M, N, Z1;
+  float alpha, beta;
+  const float* bias;  // per output column, may be null
+  float* Cs;          // residual output, may be null
+  float* dbg;         // debug hook (unused by the persistent kernel)
+  int zcount, kb_per;  // batch count; k-blocks per split
+  float* ws;           // split-K: raw partial tiles [split][z][M][N] (else null)
+  int causal;          // 0 none, 1 lower output, 2 lower-triangular A, 3 upper-triangular A
+  int n_tiles_n, n_tiles_m, n_tiles;  // tile grid (n fastest), n_tiles over all (split, z)
+  int nsrc;                           // 1, or 2 for a dual-source product
+};
+
+// Descriptor of k-step `ks` (8 tf32 = 32 B of K) of an operand tile.
+// K-major: 128 rows x 64 B, SWIZZLE_64B in 8-row (512 B) atoms: advance 32 B
+// per k-step, SBO = 512 B. MN-major: four 32-element chunks of [16 k-rows x
+// 128 B] swizzled in 4-row (512 B) atoms of 32 B granules: advance 8 rows =
+// 1024 B per k-step, LBO = 2048 B between MN chunks, SBO = 512 B.
+template <bool MN>
+__device__ __forceinline__ uint64_t tile_desc(uint32_t base, int ks) {
+  if (MN) return make_desc(base + ks * 1024, 2048, 512, 1);
+  return make_desc(base + ks * 32, 16, 512, 4);
+}
+
+// The tensor core's fp32 accumulation is not round-to-nearest (its error grows
+// ~linearly with the number of accumulated MMAs). To stay fp32-faithful at
+// K = 8192 the K loop is cut into chunks of KC k-blocks: each chunk
+// accumulates in one of two TMEM buffers, and the epilogue warps drain every
+// finished chunk into round-to-nearest fp32 registers while the MMA warp
+// fills the other buffer (chunks continue across the tiles of a CTA).
+constexpr int KC = 8;  // k-blocks (8 x 16 = 128 of K) per TMEM chunk
+
+struct TileInfo {
+  int n0, m0, z, split, kb0, num_kb;
+  bool skip;
+};
+
+template <int BN, bool CAUSAL>
+__device__ __forceinline__ TileInfo tile_info(const EpiParams& ep, int t, int K) {
+  TileInfo ti;
+  int nt, mt, zz;
+  if (CAUSAL && ep.causal == 1 && BN == BM) {
+    // only the tm (tm + 1) / 2 lower-triangle tiles of each square head are
+    // enumerated: every CTA of the round-robin gets equal work
+    const int per = ep.n_tiles_m * (ep.n_tiles_m + 1) / 2;
+    const int q = t % per;
+    zz = t / per;
+    int m = int((sqrtf(8.0f * q + 1.0f) - 1.0f) * 0.5f);
+    while ((m + 1) * (m + 2) / 2 <= q) ++m;
+    while (m * (m + 1) / 2 > q) --m;
+    mt = m;
+    nt = q - m * (m + 1) / 2;
+  } else if (CAUSAL && (ep.causal == 2 || ep.causal == 3)) {
+    // K range grows (2) / shrinks (3) with the row tile: walk the row tiles
+    // from the longest to the shortest, so that each round-robin wave holds
+    // tiles of (nearly) equal cost
+    const int per = ep.n_tiles / ep.n_tiles_m;  // n tiles x (split, z)
+    const int mi = t / per, rem = t % per;
+    mt = ep.causal == 2 ? ep.n_tiles_m - 1 - mi : mi;
+    nt = rem % ep.n_tiles_n;
+    zz = rem / ep.n_tiles_n;
+  } else {
+    nt = t % ep.n_tiles_n;
+    mt = (t / ep.n_tiles_n) % ep.n_tiles_m;
+    zz = t / (ep.n_tiles_n * ep.n_tiles_m);
+  }
+  ti.n0 = nt * BN;
+  ti.m0 = mt * BM;
+  ti.z = zz % ep.zcount;
+  ti.split = zz / ep.zcount;
+  ti.kb0 = ti.split * ep.kb_per;
+  ti.num_kb = min(ep.kb_per, (K + BK - 1) / BK - ti.kb0);
+  // Causal attention structure (square S x S per head, tile-aligned):
+  //  1: C[i][j] is only needed for j <= i -> tiles strictly above the diagonal skip;
+  //  2: A[i][k] is zero for k > i  -> K range [0, m0 + BM);
+  //  3: A[i][k] is zero for k < i  -> K range [m0, K).
+  ti.skip = false;
+  if (CAUSAL) {
+    ti.skip = (ep.causal == 1 && ti.n0 > ti.m0 + BM - 1);
+    if (ep.causal == 2) ti.num_kb = min(ti.num_kb, (ti.m0 + BM + BK - 1) / BK - ti.kb0);
+    if (ep.causal == 3) {
+      const int lo = ti.m0 / BK;
+      ti.num_kb -= max(0, lo - ti.kb0);
+      ti.kb0 = max(ti.kb0, lo);
+    }
+  }
+  if (ti.num_kb <= 0) ti.skip = true;
+  return ti;
+}
+
+
+// Epilogue of one output row segment [n0, n0 + EC) held by one thread:
+// C = alpha acc + beta C + bias (and the tf32 residual Cs of the result), or
+// the raw split-K partial.
+template <int EC>
+__device__ __forceinline__ void store_row(const EpiParams& ep, const TileInfo& ti, int row, int n0,
+                                          const float (&acc)[EC]) {
+  if (row >= ep.M) return;
+  const int z1 = ti.z % ep.Z1, z2 = ti.z / ep.Z1;
+  const int nvalid = ep.N - n0;
+  if (nvalid <= 0) return;
+  if (ep.ws) {
+    // split-K partial: raw accumulator, dense [M][N] per (split, z)
+    float* prow = ep.ws + ((long long)ti.split * ep.zcount + ti.z) * ((long long)ep.M * ep.N) +
+                  (long long)row * ep.N + n0;
+    if (nvalid >= EC && (ep.N & 3) == 0) {
+#pragma unroll
+      for (int j = 0; j < EC; j += 4)
+        *reinterpret_cast<float4*>(prow + j) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < EC; ++j)
+        if (j < nvalid) prow[j] = acc[j];
+    }
+    return;
+  }
+  const long long off = z1 * ep.sc1 + z2 * ep.sc2 + (long long)row * ep.ldc + n0;
+  float* crow = ep.C + off;
+  float* srow = ep.Cs ? ep.Cs + off : nullptr;
+  const float* brow = ep.bias ? ep.bias + n0 : nullptr;
+  const bool vec = nvalid >= EC && ((reinterpret_cast<uintptr_t>(crow) & 15) == 0) &&
+                   (!srow || (reinterpret_cast<uintptr_t>(srow) & 15) == 0);
+  if (vec) {
+#pragma unroll
+    for (int j = 0; j < EC; j += 4) {
+      float4 o = make_float4(ep.alpha * acc[j], ep.alpha * acc[j + 1], ep.alpha * acc[j + 2], ep.alpha * acc[j + 3]);
+      if (ep.beta != 0.0f) {
+        const float4 old = *reinterpret_cast<const float4*>(crow + j);
+        o.x += ep.beta * old.x;
+        o.y += ep.beta * old.y;
+        o.z += ep.beta * old.z;
+        o.w += ep.beta * old.w;
+      }
+      if (brow) {
+        o.x += brow[j];
+        o.y += brow[j + 1];
+        o.z += brow[j + 2];
+        o.w += brow[j + 3];
+      }
+      *reinterpret_cast<float4*>(crow + j) = o;
+      if (srow) {
+        const float4 r = make_float4(o.x - __uint_as_float(__float_as_uint(o.x) & 0xFFFFE000u),
+                                     o.y - __uint_as_float(__float_as_uint(o.y) & 0xFFFFE000u),
+                                     o.z - __uint_as_float(__float_as_uint(o.z) & 0xFFFFE000u),
+                                     o.w - __uint_as_float(__float_as_uint(o.w) & 0xFFFFE000u));
+        *reinterpret_cast<float4*>(srow + j) = r;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < EC; ++j) {
+      if (j < nvalid) {
+        float r = ep.alpha * acc[j];
+        if (ep.beta != 0.0f) r += ep.beta * crow[j];
+        if (brow) r += brow[j];
+        crow[j] = r;
+        if (srow) srow[j] = r - __uint_as_float(__float_as_uint(r) & 0xFFFFE000u);
+      }
+    }
+  }
+}
+
+// ---- host helpers (sd_gemm.cu)
+void make_map(CUtensorMap* m, const float* base, long long inner, long long outer, long long ld, int Z1,
+              long long s1, int Z2, long long s2, int box_inner, int box_outer, bool mn_major);
+float* splitk_workspace(size_t floats);
+int choose_splits(int tiles, int units, int total_kb, int nsrc, double t_kb, double out_bytes);
+void operand_maps(const GemmArgs& g, bool a_mn, bool b_mn, bool three, int box_n, CUtensorMap* m);
+bool prof_on();
+void prof_tag(const std::string& tag);
+void prof_begin(cudaStream_t s);
+void prof_end(cudaStream_t s, double flops);
+void launch_splitk_reduce(const float* ws, int splits, int zc, const GemmArgs& g, cudaStream_t s);
+// CTA-pair (cta_group::2) 256 x 256 tiles (sd_gemm_pair.cu)
+void gemm_pair(const GemmArgs& g, cudaStream_t s);
+
+}  // namespace gk
+}  // namespace sd

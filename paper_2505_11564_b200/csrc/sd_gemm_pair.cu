@@ -1,0 +1,348 @@
+// CTA-pair variant of the fp32-faithful tcgen05 GEMM (sm_100a).
+//
+// Two CTAs of a cluster (two SMs of one TPC) compute one 256 x 256 output
+// tile with tcgen05.mma.cta_group::2 (M = 256): CTA r stages rows
+// [m0 + 128 r, +128) of A and columns [n0 + 128 r, +128) of B, and holds rows
+// [m0 + 128 r, +128) x all 256 columns of the accumulator in its TMEM. Each
+// SM therefore moves half the operand bytes per flop of the single-CTA
+// 128 x 256 tile: the 3xTF32 products (raw + residual operands, 2x the bytes
+// of a plain GEMM) are otherwise bound by L2 -> SM bandwidth.
+//
+// Roles per CTA: warp 0 TMA producer (both CTAs; bytes land on the leader's
+// full barrier), warp 1 TMEM allocator + (leader only) MMA issuer, warps
+// 2..17 epilogue (16 warps: lane quadrant warp % 4, 64 columns each).
+// Same 3xTF32 scheme, chunked round-to-nearest drain (KC), dual-source and
+// split-K support as the single-CTA kernel in sd_gemm.cu.
+#include <algorithm>
+#include <string>
+
+#include "sd_gemm_dev.cuh"
+
+namespace sd {
+namespace gk {
+namespace {
+
+constexpr int kPairN = 256;                           // pair tile N (each CTA stages 128 columns of B)
+constexpr int kPairM = 256;                           // pair tile M (each CTA stages 128 rows of A)
+constexpr int kEpiWarps = 16;
+constexpr int kPairThreads = 64 + 32 * kEpiWarps;     // producer, MMA, epilogue
+constexpr int kHalfB = kPairN / 2;
+constexpr int PA_BYTES = BM * BK * 4;                 // 8 KB
+constexpr int PB_BYTES = kHalfB * BK * 4;             // 8 KB
+constexpr int kPairStages = 6;
+constexpr uint32_t kPairTmemCols = 2 * kPairN;        // two accumulation buffers
+constexpr int kPairEC = kPairN / (kEpiWarps / 4);     // 64 accumulator columns per epilogue thread
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+// shared::cluster address of the same variable in the leader CTA (rank 0)
+__device__ __forceinline__ uint32_t leader_addr(const void* p) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(r) : "r"(smem_u32(p)));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tma_load_4d_pair(const CUtensorMap* map, uint32_t bar, void* dst, int c0, int c1,
+                                                 int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, "
+      "%5, %6}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+__device__ __forceinline__ void mma_tf32_pair(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
+                                              uint32_t acc) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t"
+      "}" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+// arrive on the barrier at this offset in BOTH CTAs of the pair once the
+// leader's previously issued MMAs complete
+__device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t bar) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t* v) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
+
+__device__ __forceinline__ TileInfo pair_tile(const EpiParams& ep, int t, int K) {
+  TileInfo ti;
+  const int nt = t % ep.n_tiles_n;
+  const int mt = (t / ep.n_tiles_n) % ep.n_tiles_m;
+  const int zz = t / (ep.n_tiles_n * ep.n_tiles_m);
+  ti.n0 = nt * kPairN;
+  ti.m0 = mt * kPairM;
+  ti.z = zz % ep.zcount;
+  ti.split = zz / ep.zcount;
+  ti.kb0 = ti.split * ep.kb_per;
+  ti.num_kb = min(ep.kb_per, (K + BK - 1) / BK - ti.kb0);
+  ti.skip = ti.num_kb <= 0;
+  return ti;
+}
+
+template <bool A_MN, bool B_MN, bool THREE>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
+    k_gemm_pair(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mAs,
+                const __grid_constant__ CUtensorMap mB, const __grid_constant__ CUtensorMap mBs,
+                const __grid_constant__ CUtensorMap mA2, const __grid_constant__ CUtensorMap mAs2,
+                const __grid_constant__ CUtensorMap mB2, const __grid_constant__ CUtensorMap mBs2, int K, EpiParams ep) {
+  constexpr int STAGES = kPairStages, EC = kPairEC;
+  constexpr int STAGE_BYTES = (THREE ? 2 : 1) * (PA_BYTES + PB_BYTES);
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;  // [2]
+  uint64_t* tempty = tfull + 2;      // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 2 * kEpiWarps);  // every epilogue warp of both CTAs
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(kPairTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cluster_sync();  // both CTAs' barriers initialised and TMEM allocated
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint32_t full_leader = leader_addr(full);
+      uint32_t g = 0;
+      for (int t = cid; t < ep.n_tiles; t += ncl) {
+        const TileInfo ti = pair_tile(ep, t, K);
+        if (ti.skip) continue;
+        const int z1 = ti.z % ep.Z1, z2 = ti.z / ep.Z1;
+        const int m_own = ti.m0 + int(rank) * BM, n_own = ti.n0 + int(rank) * kHalfB;
+        for (int kk = 0; kk < ep.nsrc * ti.num_kb; ++kk, ++g) {
+          const int s = g % STAGES;
+          const uint32_t ph = (g / STAGES) & 1;
+          mbar_wait(&empty[s], ph ^ 1);
+          unsigned char* st = smem + s * STAGE_BYTES;
+          // the leader's barrier counts the bytes of both CTAs
+          if (rank == 0) mbar_expect_tx(&full[s], 2 * STAGE_BYTES);
+          const uint32_t bar = full_leader + 8u * s;
+          const bool src2 = kk >= ti.num_kb;
+          const int kb = src2 ? kk - ti.num_kb : kk;
+          const CUtensorMap* pA = src2 ? &mA2 : &mA;
+          const CUtensorMap* pAs = src2 ? &mAs2 : &mAs;
+          const CUtensorMap* pB = src2 ? &mB2 : &mB;
+          const CUtensorMap* pBs = src2 ? &mBs2 : &mBs;
+          const int k0 = (ti.kb0 + kb) * BK;
+          if (A_MN) {
+#pragma unroll
+            for (int c = 0; c < BM / 32; ++c) {
+              tma_load_4d_pair(pA, bar, st + c * 2048, m_own + 32 * c, k0, z1, z2);
+              if (THREE) tma_load_4d_pair(pAs, bar, st + PA_BYTES + c * 2048, m_own + 32 * c, k0, z1, z2);
+            }
+          } else {
+            tma_load_4d_pair(pA, bar, st, k0, m_own, z1, z2);
+            if (THREE) tma_load_4d_pair(pAs, bar, st + PA_BYTES, k0, m_own, z1, z2);
+          }
+          unsigned char* sb = st + (THREE ? 2 : 1) * PA_BYTES;
+          if (B_MN) {
+#pragma unroll
+            for (int c = 0; c < kHalfB / 32; ++c) {
+              tma_load_4d_pair(pB, bar, sb + c * 2048, n_own + 32 * c, k0, z1, z2);
+              if (THREE) tma_load_4d_pair(pBs, bar, sb + PB_BYTES + c * 2048, n_own + 32 * c, k0, z1, z2);
+            }
+          } else {
+            tma_load_4d_pair(pB, bar, sb, k0, n_own, z1, z2);
+            if (THREE) tma_load_4d_pair(pBs, bar, sb + PB_BYTES, k0, n_own, z1, z2);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (rank == 0) {
+      constexpr uint32_t idesc = make_idesc(A_MN, B_MN, kPairN, kPairM);
+      uint32_t g = 0, chunk = 0;
+      for (int t = cid; t < ep.n_tiles; t += ncl) {
+        const TileInfo ti = pair_tile(ep, t, K);
+        if (ti.skip) continue;
+        const int nkb = ep.nsrc * ti.num_kb;
+        for (int kb = 0; kb < nkb; ++kb, ++g) {
+          const int s = g % STAGES;
+          const uint32_t ph = (g / STAGES) & 1;
+          const bool first = (kb % KC) == 0;
+          const bool last = (kb % KC) == KC - 1 || kb == nkb - 1;
+          const uint32_t buf = chunk & 1;
+          if (first && chunk >= 2) mbar_wait(&tempty[buf], ((chunk >> 1) - 1) & 1);
+          mbar_wait(&full[s], ph);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          if (lane == 0) {
+            const uint32_t d = tmem + buf * kPairN;
+            const uint32_t st = smem_u32(smem + s * STAGE_BYTES);
+            const uint32_t a = st, as = st + PA_BYTES;
+            const uint32_t b = st + (THREE ? 2 : 1) * PA_BYTES, bs = b + PB_BYTES;
+#pragma unroll
+            for (int ks = 0; ks < BK / 8; ++ks) {
+              const uint32_t acc0 = (first && ks == 0) ? 0u : 1u;
+              if (THREE) {
+                mma_tf32_pair(d, tile_desc<A_MN>(as, ks), tile_desc<B_MN>(b, ks), idesc, acc0);
+                mma_tf32_pair(d, tile_desc<A_MN>(a, ks), tile_desc<B_MN>(bs, ks), idesc, 1u);
+                mma_tf32_pair(d, tile_desc<A_MN>(a, ks), tile_desc<B_MN>(b, ks), idesc, 1u);
+              } else {
+                mma_tf32_pair(d, tile_desc<A_MN>(a, ks), tile_desc<B_MN>(b, ks), idesc, acc0);
+              }
+            }
+            mma_commit_pair(&empty[s]);
+            if (last) mma_commit_pair(&tfull[buf]);
+          }
+          __syncwarp();
+          if (last) ++chunk;
+        }
+      }
+    }
+  } else {
+    // epilogue: warp w drains TMEM lanes 32 (w % 4) .. +31 and the column
+    // group (w - 2) / 4 (EC = 64 columns) of this CTA's 128 accumulator rows
+    const int sub = warp & 3;
+    const int cb = ((warp - 2) >> 2) * EC;
+    const uint32_t tempty_leader = leader_addr(tempty);
+    uint32_t chunk = 0;
+    for (int t = cid; t < ep.n_tiles; t += ncl) {
+      const TileInfo ti = pair_tile(ep, t, K);
+      if (ti.skip) continue;
+      const int row = ti.m0 + int(rank) * BM + sub * 32 + lane;
+      float acc[EC];
+#pragma unroll
+      for (int j = 0; j < EC; ++j) acc[j] = 0.0f;
+      const int nchunks = (ep.nsrc * ti.num_kb + KC - 1) / KC;
+      for (int c = 0; c < nchunks; ++c, ++chunk) {
+        const uint32_t buf = chunk & 1;
+        mbar_wait(&tfull[buf], (chunk >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+        for (int c0 = 0; c0 < EC; c0 += 16) {
+          uint32_t v[16];
+          tmem_ld16(tmem + (uint32_t(sub * 32) << 16) + buf * kPairN + uint32_t(cb + c0), v);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+          for (int j = 0; j < 16; ++j) acc[c0 + j] += __uint_as_float(v[j]);
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive_remote(tempty_leader + 8u * buf);
+      }
+      store_row<EC>(ep, ti, row, ti.n0 + cb, acc);
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cluster_sync();  // no CTA leaves while its peer may still touch its smem / barriers
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kPairTmemCols));
+  }
+}
+
+int max_clusters(const void* kern, size_t smem) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(2 * kNumSMs);
+  cfg.blockDim = dim3(kPairThreads);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  SD_CUDA(cudaOccupancyMaxActiveClusters(&n, kern, &cfg));
+  return n;
+}
+
+template <bool A_MN, bool B_MN, bool THREE>
+void launch_pair_t(const GemmArgs& g, cudaStream_t s) {
+  CUtensorMap maps[8];
+  operand_maps(g, A_MN, B_MN, THREE, kHalfB, maps);
+  const bool dual = g.A2 != nullptr;
+  const int zc = g.Z1 * g.Z2;
+  const int tn = (g.N + kPairN - 1) / kPairN, tm = (g.M + kPairM - 1) / kPairM;
+  const int tiles = tn * tm * zc;
+  const size_t smem = 1024 + size_t(kPairStages) * (THREE ? 2 : 1) * (PA_BYTES + PB_BYTES) + 256;
+  auto kern = k_gemm_pair<A_MN, B_MN, THREE>;
+  static int clusters = 0;
+  if (!clusters) {
+    SD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    clusters = std::max(1, max_clusters(reinterpret_cast<const void*>(kern), smem));
+  }
+  // split-K as in the single-CTA launcher, over the cluster (pair) slots
+  const int total_kb = (g.K + BK - 1) / BK;
+  const double t_kb = 2.0 * kPairM * kPairN * BK / (2.0e14 / clusters) / (THREE ? 1.0 : 3.0);
+  int splits = choose_splits(tiles, clusters, total_kb, dual ? 2 : 1, t_kb, 4.0 * zc * g.M * g.N);
+  const int kb_per = (total_kb + splits - 1) / splits;
+  splits = (total_kb + kb_per - 1) / kb_per;
+  float* ws = nullptr;
+  if (splits > 1) ws = splitk_workspace(size_t(splits) * zc * size_t(g.M) * g.N);
+  EpiParams ep{g.C, g.ldc, g.sc1, g.sc2, g.M, g.N, g.Z1, g.alpha, g.beta, g.bias, g.Cs, g.dbg, zc, kb_per, ws,
+               0, tn, tm, tiles * splits, dual ? 2 : 1};
+  const int grid = 2 * std::min(ep.n_tiles, clusters);
+  if (prof_on())
+    prof_tag(std::to_string(g.M) + "," + std::to_string(g.N) + "," + std::to_string(g.K) + "," + std::to_string(zc) +
+             "," + std::to_string(int(A_MN)) + "," + std::to_string(int(B_MN)) + ",pair," + std::to_string(splits) +
+             (dual ? ",2" : ",1"));
+  prof_begin(s);
+  kern<<<grid, kPairThreads, smem, s>>>(maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], maps[6], maps[7], g.K,
+                                        ep);
+  SD_LAUNCHED("k_gemm_pair");
+  if (splits > 1) launch_splitk_reduce(ws, splits, zc, g, s);
+  prof_end(s, (dual ? 4.0 : 2.0) * double(g.M) * g.N * g.K * g.Z1 * g.Z2);
+}
+
+}  // namespace
+
+void gemm_pair(const GemmArgs& g, cudaStream_t s) {
+  const bool three = g.As != nullptr && g.Bs != nullptr;
+#define SD_PAIR_CASE(AM, BMJ, TH) \
+  if (g.a_mn == AM && g.b_mn == BMJ && three == TH) return launch_pair_t<AM, BMJ, TH>(g, s);
+  SD_PAIR_CASE(false, false, true)
+  SD_PAIR_CASE(false, true, true)
+  SD_PAIR_CASE(true, false, true)
+  SD_PAIR_CASE(true, true, true)
+  SD_PAIR_CASE(false, false, false)
+  SD_PAIR_CASE(false, true, false)
+  SD_PAIR_CASE(true, false, false)
+  SD_PAIR_CASE(true, true, false)
+#undef SD_PAIR_CASE
+}
+
+}  // namespace gk
+}  // namespace sd

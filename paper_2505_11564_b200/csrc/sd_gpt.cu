@@ -179,6 +179,23 @@ struct sd_gpt_s {
     g.causal = cmode;
     sd::gemm(g, st);
   }
+  // dual source: C = alpha (op(A) op(B) + op(A2) op(B2)) + beta C (+bias), one
+  // launch and one accumulation (the tangent products of Pearlmutter's R-op)
+  void mm2(int M, int N, int K, Op A, Op Bo, Op A2, Op B2, float* C, long long ldc, float alpha, float beta,
+           cudaStream_t st, const float* bias = nullptr, float* Cs = nullptr, int Z1 = 1, int Z2 = 1,
+           long long c1 = 0, long long c2 = 0) {
+    sd::GemmArgs g;
+    g.M = M, g.N = N, g.K = K;
+    g.A = A.p, g.As = A.s, g.lda = A.ld, g.a_mn = A.mn;
+    g.B = Bo.p, g.Bs = Bo.s, g.ldb = Bo.ld, g.b_mn = Bo.mn;
+    if (A2.mn != A.mn || B2.mn != Bo.mn) fail(SD_ARGUMENT_ERROR, "gpt: dual product majors differ");
+    g.A2 = A2.p, g.A2s = A2.s, g.lda2 = A2.ld, g.B2 = B2.p, g.B2s = B2.s, g.ldb2 = B2.ld;
+    g.sa1_2 = A2.s1, g.sa2_2 = A2.s2, g.sb1_2 = B2.s1, g.sb2_2 = B2.s2;
+    g.C = C, g.ldc = ldc, g.alpha = alpha, g.beta = beta, g.bias = bias, g.Cs = Cs;
+    g.Z1 = Z1, g.Z2 = Z2, g.sa1 = A.s1, g.sa2 = A.s2, g.sb1 = Bo.s1, g.sb2 = Bo.s2, g.sc1 = c1, g.sc2 = c2;
+    g.causal = cmode;
+    sd::gemm(g, st);
+  }
   int cmode = 0;  // causal tile/K skipping for the per-head S x S products (sd_gemm.cu)
 
   const float* th(int i) const { return theta + slots[i].off; }
@@ -204,41 +221,38 @@ struct sd_gpt_s {
       // qkv = h Wa + ba ; dqkv = dh Wa + h VWa + Vba
       mm(T, 3 * d, d, {Ly.h1, Ly.h1s, d, false}, {th(b + 2), ths(b + 2), 3 * d, true}, Ly.a, 3 * d, 1, 0, st,
          th(b + 3), Ly.as);
-      mm(T, 3 * d, d, {Ly.dh1, Ly.dh1s, d, false}, {th(b + 2), ths(b + 2), 3 * d, true}, Ly.da, 3 * d, 1, 0, st,
-         V_(b + 3));
-      mm(T, 3 * d, d, {Ly.h1, Ly.h1s, d, false}, {V_(b + 2), Vs(b + 2), 3 * d, true}, Ly.da, 3 * d, 1, 1, st,
-         nullptr, Ly.das);
+      mm2(T, 3 * d, d, {Ly.dh1, Ly.dh1s, d, false}, {th(b + 2), ths(b + 2), 3 * d, true}, {Ly.h1, Ly.h1s, d, false},
+          {V_(b + 2), Vs(b + 2), 3 * d, true}, Ly.da, 3 * d, 1, 0, st, V_(b + 3), Ly.das);
       attention_fwd(Ly, sc, st);
       // x += o Wp + bp ; dx += do Wp + o VWp + Vbp
       mm(T, d, d, {Ly.o, Ly.os, d, false}, {th(b + 4), ths(b + 4), d, true}, x, d, 1, 1, st, th(b + 5));
-      mm(T, d, d, {Ly.dO, Ly.dOs, d, false}, {th(b + 4), ths(b + 4), d, true}, dx, d, 1, 1, st, V_(b + 5));
-      mm(T, d, d, {Ly.o, Ly.os, d, false}, {V_(b + 4), Vs(b + 4), d, true}, dx, d, 1, 1, st);
+      mm2(T, d, d, {Ly.dO, Ly.dOs, d, false}, {th(b + 4), ths(b + 4), d, true}, {Ly.o, Ly.os, d, false},
+          {V_(b + 4), Vs(b + 4), d, true}, dx, d, 1, 1, st, V_(b + 5));
       sd::LnArgs lb{x, dx, th(b + 6), th(b + 7), V_(b + 6), V_(b + 7), T, d, 1e-5f,
                     Ly.h2, Ly.h2s, Ly.dh2, Ly.dh2s, Ly.xh2, Ly.dxh2, Ly.r2, Ly.dr2};
       sd::gpt_ln_fwd(lb, st);
       mm(T, ff, d, {Ly.h2, Ly.h2s, d, false}, {th(b + 8), ths(b + 8), ff, true}, Ly.f, ff, 1, 0, st, th(b + 9));
-      mm(T, ff, d, {Ly.dh2, Ly.dh2s, d, false}, {th(b + 8), ths(b + 8), ff, true}, Ly.df, ff, 1, 0, st, V_(b + 9));
-      mm(T, ff, d, {Ly.h2, Ly.h2s, d, false}, {V_(b + 8), Vs(b + 8), ff, true}, Ly.df, ff, 1, 1, st);
+      mm2(T, ff, d, {Ly.dh2, Ly.dh2s, d, false}, {th(b + 8), ths(b + 8), ff, true}, {Ly.h2, Ly.h2s, d, false},
+          {V_(b + 8), Vs(b + 8), ff, true}, Ly.df, ff, 1, 0, st, V_(b + 9));
       sd::gpt_gelu_fwd(Ly.f, Ly.df, Ly.u, Ly.us, Ly.du, Ly.dus, (long long)T * ff, st);
       mm(T, d, ff, {Ly.u, Ly.us, ff, false}, {th(b + 10), ths(b + 10), d, true}, x, d, 1, 1, st, th(b + 11));
-      mm(T, d, ff, {Ly.du, Ly.dus, ff, false}, {th(b + 10), ths(b + 10), d, true}, dx, d, 1, 1, st, V_(b + 11));
-      mm(T, d, ff, {Ly.u, Ly.us, ff, false}, {V_(b + 10), Vs(b + 10), d, true}, dx, d, 1, 1, st);
+      mm2(T, d, ff, {Ly.du, Ly.dus, ff, false}, {th(b + 10), ths(b + 10), d, true}, {Ly.u, Ly.us, ff, false},
+          {V_(b + 10), Vs(b + 10), d, true}, dx, d, 1, 1, st, V_(b + 11));
     }
     const int fL = 2 + 12 * c.n_layer;
     sd::LnArgs lf{x, dx, th(fL), th(fL + 1), V_(fL), V_(fL + 1), T, d, 1e-5f, hf, hfs, dhf, dhfs, xhf, dxhf, rf, drf};
     sd::gpt_ln_fwd(lf, st);
     // logits z = hf wte^T ; dz = dhf wte^T + hf Vwte^T
     mm(T, V, d, {hf, hfs, d, false}, {th(0), ths(0), d, false}, z, Vp, 1, 0, st);
-    mm(T, V, d, {dhf, dhfs, d, false}, {th(0), ths(0), d, false}, dz, Vp, 1, 0, st);
-    mm(T, V, d, {hf, hfs, d, false}, {V_(0), Vs(0), d, false}, dz, Vp, 1, 1, st);
+    mm2(T, V, d, {dhf, dhfs, d, false}, {th(0), ths(0), d, false}, {hf, hfs, d, false}, {V_(0), Vs(0), d, false}, dz,
+        Vp, 1, 0, st);
     sd::gpt_ce(z, dz, zs, dz == nullptr ? nullptr : dzs, tgt, T, V, Vp, loss_scale, loss_rows, st);
     // ----------------------------------------------------------- backward
     // ghf = gz wte ; gdhf = gdz wte + gz Vwte ; Hv_wte(head) = gdz^T hf + gz^T dhf
     mm(T, d, V, {z, zs, Vp, false}, {th(0), ths(0), d, true}, gh, d, 1, 0, st);
-    mm(T, d, V, {dz, dzs, Vp, false}, {th(0), ths(0), d, true}, gdh, d, 1, 0, st);
-    mm(T, d, V, {z, zs, Vp, false}, {V_(0), Vs(0), d, true}, gdh, d, 1, 1, st);
-    mm(V, d, T, {dz, dzs, Vp, true}, {hf, hfs, d, true}, HV(0), d, 1, 0, st);
-    mm(V, d, T, {z, zs, Vp, true}, {dhf, dhfs, d, true}, HV(0), d, 1, 1, st);
+    mm2(T, d, V, {dz, dzs, Vp, false}, {th(0), ths(0), d, true}, {z, zs, Vp, false}, {V_(0), Vs(0), d, true}, gdh, d,
+        1, 0, st);
+    mm2(V, d, T, {dz, dzs, Vp, true}, {hf, hfs, d, true}, {z, zs, Vp, true}, {dhf, dhfs, d, true}, HV(0), d, 1, 0, st);
     SD_CUDA(cudaMemsetAsync(gx, 0, Td * sizeof(float), st));
     SD_CUDA(cudaMemsetAsync(gdx, 0, Td * sizeof(float), st));
     sd::LnBwdArgs bf{gh, gdh, th(fL), V_(fL), xhf, dxhf, rf, drf, T, d, gx, gdx, gxs, gdxs, HV(fL), HV(fL + 1), red};
@@ -248,36 +262,36 @@ struct sd_gpt_s {
       const int b = 2 + 12 * l;
       // MLP out: gu = gx Wq^T ; gdu = gdx Wq^T + gx VWq^T ; Hv_Wq = du^T gx + u^T gdx
       mm(T, ff, d, {gx, gxs, d, false}, {th(b + 10), ths(b + 10), d, false}, gu, ff, 1, 0, st);
-      mm(T, ff, d, {gdx, gdxs, d, false}, {th(b + 10), ths(b + 10), d, false}, gdu, ff, 1, 0, st);
-      mm(T, ff, d, {gx, gxs, d, false}, {V_(b + 10), Vs(b + 10), d, false}, gdu, ff, 1, 1, st);
-      mm(ff, d, T, {Ly.du, Ly.dus, ff, true}, {gx, gxs, d, true}, HV(b + 10), d, 1, 0, st);
-      mm(ff, d, T, {Ly.u, Ly.us, ff, true}, {gdx, gdxs, d, true}, HV(b + 10), d, 1, 1, st);
+      mm2(T, ff, d, {gdx, gdxs, d, false}, {th(b + 10), ths(b + 10), d, false}, {gx, gxs, d, false},
+          {V_(b + 10), Vs(b + 10), d, false}, gdu, ff, 1, 0, st);
+      mm2(ff, d, T, {Ly.du, Ly.dus, ff, true}, {gx, gxs, d, true}, {Ly.u, Ly.us, ff, true}, {gdx, gdxs, d, true},
+          HV(b + 10), d, 1, 0, st);
       sd::gpt_colsum(gdx, T, d, d, HV(b + 11), red, st);
       sd::gpt_gelu_bwd(Ly.f, Ly.df, gu, gdu, gus, gdus, (long long)T * ff, st);
       // MLP in: gh = gf Wf^T ; gdh = gdf Wf^T + gf VWf^T ; Hv_Wf = dh2^T gf + h2^T gdf
       mm(T, d, ff, {gu, gus, ff, false}, {th(b + 8), ths(b + 8), ff, false}, gh, d, 1, 0, st);
-      mm(T, d, ff, {gdu, gdus, ff, false}, {th(b + 8), ths(b + 8), ff, false}, gdh, d, 1, 0, st);
-      mm(T, d, ff, {gu, gus, ff, false}, {V_(b + 8), Vs(b + 8), ff, false}, gdh, d, 1, 1, st);
-      mm(d, ff, T, {Ly.dh2, Ly.dh2s, d, true}, {gu, gus, ff, true}, HV(b + 8), ff, 1, 0, st);
-      mm(d, ff, T, {Ly.h2, Ly.h2s, d, true}, {gdu, gdus, ff, true}, HV(b + 8), ff, 1, 1, st);
+      mm2(T, d, ff, {gdu, gdus, ff, false}, {th(b + 8), ths(b + 8), ff, false}, {gu, gus, ff, false},
+          {V_(b + 8), Vs(b + 8), ff, false}, gdh, d, 1, 0, st);
+      mm2(d, ff, T, {Ly.dh2, Ly.dh2s, d, true}, {gu, gus, ff, true}, {Ly.h2, Ly.h2s, d, true}, {gdu, gdus, ff, true},
+          HV(b + 8), ff, 1, 0, st);
       sd::gpt_colsum(gdu, T, ff, ff, HV(b + 9), red, st);
       sd::LnBwdArgs b2{gh, gdh, th(b + 6), V_(b + 6), Ly.xh2, Ly.dxh2, Ly.r2, Ly.dr2, T, d,
                        gx, gdx, gxs, gdxs, HV(b + 6), HV(b + 7), red};
       sd::gpt_ln_bwd(b2, st);
       // attention out-projection
       mm(T, d, d, {gx, gxs, d, false}, {th(b + 4), ths(b + 4), d, false}, go, d, 1, 0, st, nullptr, gos);
-      mm(T, d, d, {gdx, gdxs, d, false}, {th(b + 4), ths(b + 4), d, false}, gdo, d, 1, 0, st);
-      mm(T, d, d, {gx, gxs, d, false}, {V_(b + 4), Vs(b + 4), d, false}, gdo, d, 1, 1, st, nullptr, gdos);
-      mm(d, d, T, {Ly.dO, Ly.dOs, d, true}, {gx, gxs, d, true}, HV(b + 4), d, 1, 0, st);
-      mm(d, d, T, {Ly.o, Ly.os, d, true}, {gdx, gdxs, d, true}, HV(b + 4), d, 1, 1, st);
+      mm2(T, d, d, {gdx, gdxs, d, false}, {th(b + 4), ths(b + 4), d, false}, {gx, gxs, d, false},
+          {V_(b + 4), Vs(b + 4), d, false}, gdo, d, 1, 0, st, nullptr, gdos);
+      mm2(d, d, T, {Ly.dO, Ly.dOs, d, true}, {gx, gxs, d, true}, {Ly.o, Ly.os, d, true}, {gdx, gdxs, d, true},
+          HV(b + 4), d, 1, 0, st);
       sd::gpt_colsum(gdx, T, d, d, HV(b + 5), red, st);
       attention_bwd(Ly, sc, st);
       // QKV: gh = ga Wa^T ; gdh = gda Wa^T + ga VWa^T ; Hv_Wa = dh1^T ga + h1^T gda
       mm(T, d, 3 * d, {ga, gas, 3 * d, false}, {th(b + 2), ths(b + 2), 3 * d, false}, gh, d, 1, 0, st);
-      mm(T, d, 3 * d, {gda, gdas, 3 * d, false}, {th(b + 2), ths(b + 2), 3 * d, false}, gdh, d, 1, 0, st);
-      mm(T, d, 3 * d, {ga, gas, 3 * d, false}, {V_(b + 2), Vs(b + 2), 3 * d, false}, gdh, d, 1, 1, st);
-      mm(d, 3 * d, T, {Ly.dh1, Ly.dh1s, d, true}, {ga, gas, 3 * d, true}, HV(b + 2), 3 * d, 1, 0, st);
-      mm(d, 3 * d, T, {Ly.h1, Ly.h1s, d, true}, {gda, gdas, 3 * d, true}, HV(b + 2), 3 * d, 1, 1, st);
+      mm2(T, d, 3 * d, {gda, gdas, 3 * d, false}, {th(b + 2), ths(b + 2), 3 * d, false}, {ga, gas, 3 * d, false},
+          {V_(b + 2), Vs(b + 2), 3 * d, false}, gdh, d, 1, 0, st);
+      mm2(d, 3 * d, T, {Ly.dh1, Ly.dh1s, d, true}, {ga, gas, 3 * d, true}, {Ly.h1, Ly.h1s, d, true},
+          {gda, gdas, 3 * d, true}, HV(b + 2), 3 * d, 1, 0, st);
       sd::gpt_colsum(gda, T, 3 * d, 3 * d, HV(b + 3), red, st);
       sd::LnBwdArgs b1{gh, gdh, th(b), V_(b), Ly.xh1, Ly.dxh1, Ly.r1, Ly.dr1, T, d,
                        gx, gdx, gxs, gdxs, HV(b), HV(b + 1), red};
@@ -299,17 +313,14 @@ struct sd_gpt_s {
     cmode = 1;  // scores: only j <= i tiles
     mm(Sq, Sq, dh, q(Ly.a, Ly.as), {Ly.a + d, Ly.as + d, 3 * d, false, ha, ba}, Ly.P, Sq, sc, 0, st, nullptr,
        nullptr, H, B, hs, bs);
-    mm(Sq, Sq, dh, q(Ly.da, Ly.das), {Ly.a + d, Ly.as + d, 3 * d, false, ha, ba}, Ly.dP, Sq, sc, 0, st, nullptr,
-       nullptr, H, B, hs, bs);
-    mm(Sq, Sq, dh, q(Ly.a, Ly.as), {Ly.da + d, Ly.das + d, 3 * d, false, ha, ba}, Ly.dP, Sq, sc, 1, st, nullptr,
-       nullptr, H, B, hs, bs);
+    mm2(Sq, Sq, dh, q(Ly.da, Ly.das), {Ly.a + d, Ly.as + d, 3 * d, false, ha, ba}, q(Ly.a, Ly.as),
+        {Ly.da + d, Ly.das + d, 3 * d, false, ha, ba}, Ly.dP, Sq, sc, 0, st, nullptr, nullptr, H, B, hs, bs);
     sd::gpt_attn_softmax_fwd(Ly.P, Ly.dP, Ly.Ps, Ly.dPs, Sq, (long long)B * H * Sq, st);
     const Op Pm{Ly.P, Ly.Ps, Sq, false, hs, bs}, dPm{Ly.dP, Ly.dPs, Sq, false, hs, bs};
     const Op vv{Ly.a + 2 * d, Ly.as + 2 * d, 3 * d, true, ha, ba}, dvv{Ly.da + 2 * d, Ly.das + 2 * d, 3 * d, true, ha, ba};
     cmode = 2;  // P, dP lower-triangular: keys k <= query i
     mm(Sq, dh, Sq, Pm, vv, Ly.o, d, 1, 0, st, nullptr, Ly.os, H, B, ho, bo);
-    mm(Sq, dh, Sq, dPm, vv, Ly.dO, d, 1, 0, st, nullptr, nullptr, H, B, ho, bo);
-    mm(Sq, dh, Sq, Pm, dvv, Ly.dO, d, 1, 1, st, nullptr, Ly.dOs, H, B, ho, bo);
+    mm2(Sq, dh, Sq, dPm, vv, Pm, dvv, Ly.dO, d, 1, 0, st, nullptr, Ly.dOs, H, B, ho, bo);
     cmode = 0;
   }
 
@@ -325,30 +336,26 @@ struct sd_gpt_s {
     const Op vK{Ly.a + 2 * d, Ly.as + 2 * d, 3 * d, false, ha, ba}, dvK{Ly.da + 2 * d, Ly.das + 2 * d, 3 * d, false, ha, ba};
     cmode = 1;
     mm(Sq, Sq, dh, goK, vK, gP, Sq, 1, 0, st, nullptr, nullptr, H, B, hs, bs);
-    mm(Sq, Sq, dh, gdoK, vK, gdP, Sq, 1, 0, st, nullptr, nullptr, H, B, hs, bs);
-    mm(Sq, Sq, dh, goK, dvK, gdP, Sq, 1, 1, st, nullptr, nullptr, H, B, hs, bs);
+    mm2(Sq, Sq, dh, gdoK, vK, goK, dvK, gdP, Sq, 1, 0, st, nullptr, nullptr, H, B, hs, bs);
     sd::gpt_attn_softmax_bwd(Ly.P, Ly.dP, gP, gdP, gPs, gdPs, Sq, (long long)B * H * Sq, st);
     // value adjoints
     const Op PT{Ly.P, Ly.Ps, Sq, true, hs, bs}, dPT{Ly.dP, Ly.dPs, Sq, true, hs, bs};
     const Op goM{go, gos, d, true, ho, bo}, gdoM{gdo, gdos, d, true, ho, bo};
     cmode = 3;  // P^T upper-triangular: queries i >= key j
     mm(Sq, dh, Sq, PT, goM, ga + 2 * d, 3 * d, 1, 0, st, nullptr, gas + 2 * d, H, B, ha, ba);
-    mm(Sq, dh, Sq, dPT, goM, gda + 2 * d, 3 * d, 1, 0, st, nullptr, nullptr, H, B, ha, ba);
-    mm(Sq, dh, Sq, PT, gdoM, gda + 2 * d, 3 * d, 1, 1, st, nullptr, gdas + 2 * d, H, B, ha, ba);
+    mm2(Sq, dh, Sq, dPT, goM, PT, gdoM, gda + 2 * d, 3 * d, 1, 0, st, nullptr, gdas + 2 * d, H, B, ha, ba);
     // query adjoints
     const Op gS{gP, gPs, Sq, false, hs, bs}, gdS{gdP, gdPs, Sq, false, hs, bs};
     const Op kM{Ly.a + d, Ly.as + d, 3 * d, true, ha, ba}, dkM{Ly.da + d, Ly.das + d, 3 * d, true, ha, ba};
     cmode = 2;
     mm(Sq, dh, Sq, gS, kM, ga, 3 * d, sc, 0, st, nullptr, gas, H, B, ha, ba);
-    mm(Sq, dh, Sq, gdS, kM, gda, 3 * d, sc, 0, st, nullptr, nullptr, H, B, ha, ba);
-    mm(Sq, dh, Sq, gS, dkM, gda, 3 * d, sc, 1, st, nullptr, gdas, H, B, ha, ba);
+    mm2(Sq, dh, Sq, gdS, kM, gS, dkM, gda, 3 * d, sc, 0, st, nullptr, gdas, H, B, ha, ba);
     // key adjoints
     const Op gST{gP, gPs, Sq, true, hs, bs}, gdST{gdP, gdPs, Sq, true, hs, bs};
     const Op qM{Ly.a, Ly.as, 3 * d, true, ha, ba}, dqM{Ly.da, Ly.das, 3 * d, true, ha, ba};
     cmode = 3;
     mm(Sq, dh, Sq, gST, qM, ga + d, 3 * d, sc, 0, st, nullptr, gas + d, H, B, ha, ba);
-    mm(Sq, dh, Sq, gdST, qM, gda + d, 3 * d, sc, 0, st, nullptr, nullptr, H, B, ha, ba);
-    mm(Sq, dh, Sq, gST, dqM, gda + d, 3 * d, sc, 1, st, nullptr, gdas + d, H, B, ha, ba);
+    mm2(Sq, dh, Sq, gdST, qM, gST, dqM, gda + d, 3 * d, sc, 0, st, nullptr, gdas + d, H, B, ha, ba);
     cmode = 0;
   }
 };

@@ -22,7 +22,7 @@ import csv
 rows = list(csv.DictReader(open("gpurun_out/gemm_prof.csv")))
 agg = collections.defaultdict(lambda: [0, 0.0, 0.0])
 for r in rows:
-    k = (r["M"], r["N"], r["K"], r["batch"], r["a_mn"], r["b_mn"], r["causal"], r["splits"])
+    k = (r["M"], r["N"], r["K"], r["batch"], r["a_mn"], r["b_mn"], r["causal"], r["splits"], r["nsrc"])
     agg[k][0] += 1; agg[k][1] += float(r["ms"]); agg[k][2] += float(r["flops"])
 for k, (c, t, f) in sorted(agg.items(), key=lambda x: -x[1][1]):
-    print(f"{t:8.3f} ms {c:4d}x  {f / t / 1e9:7.1f} TF/s  M,N,K,batch,amn,bmn,causal,splits={','.join(k)}")
+    print(f"{t:8.3f} ms {c:4d}x  {f / t / 1e9:7.1f} TF/s  M,N,K,batch,amn,bmn,causal,splits,nsrc={','.join(k)}")

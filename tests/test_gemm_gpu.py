@@ -89,3 +89,24 @@ def test_gemm_wide_tiles(G):
         B = torch.randn(*((N, K) if b_t else (K, N)), device="cuda")
         ref = (A.double().t() if a_t else A.double()) @ (B.double().t() if b_t else B.double())
         assert rel(G.matmul(A, B, True, a_t, b_t), ref) < 2e-6
+
+
+@pytest.mark.parametrize("a_t", [False, True])
+@pytest.mark.parametrize("b_t", [False, True])
+@pytest.mark.parametrize("shape", [(256, 384, 768), (200, 300, 100), (1024, 64, 1024), (768, 768, 8192)])
+def test_gemm_dual_source(G, a_t, b_t, shape):
+    # C = alpha (A1 B1 + A2 B2) + beta C in one launch (the HVP tangent products)
+    M, N, K = shape
+    g = torch.Generator(device="cuda").manual_seed(M + 3 * N + K)
+    mk = lambda r, c: torch.randn(r, c, device="cuda", generator=g)  # noqa: E731
+    A1, A2 = [mk(*((K, M) if a_t else (M, K))) for _ in range(2)]
+    B1, B2 = [mk(*((N, K) if b_t else (K, N))) for _ in range(2)]
+    C0 = mk(M, N)
+    op = lambda X, t: X.double().t() if t else X.double()  # noqa: E731
+    alpha, beta = 0.75, 1.0
+    ref = alpha * (op(A1, a_t) @ op(B1, b_t) + op(A2, a_t) @ op(B2, b_t)) + beta * C0.double()
+    C = C0.clone()
+    G.gemm_dual(M, N, K, A1, A1.shape[1], a_t, B1, B1.shape[1], not b_t, A2, A2.shape[1], B2, B2.shape[1], C, N,
+                alpha=alpha, beta=beta, a_small=G.split(A1), b_small=G.split(B1), a2_small=G.split(A2),
+                b2_small=G.split(B2))
+    assert rel(C, ref) < 2e-6
