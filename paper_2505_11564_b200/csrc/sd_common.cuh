@@ -79,6 +79,17 @@ __host__ __device__ inline uint64_t keyed_counter_k(uint64_t key, uint64_t ctr) 
   return mix64(key ^ (ctr * 0x9e3779b97f4a7c15ull));
 }
 
+// Exact fp32 -> f64 widening on the integer pipe (normal numbers; zeros,
+// subnormals, inf and nan take the conversion instruction). The f64 <-> f32
+// conversions issue on the 16-lane XU pipe, which the reorthogonalisation
+// update (one rounding per basis column per element) otherwise saturates.
+__device__ __forceinline__ double widen_f32(float f) {
+  const uint32_t u = __float_as_uint(f);
+  const uint32_t a = u & 0x7fffffffu;
+  if (a - 0x00800000u >= 0x7f000000u) return double(f);
+  return __hiloint2double(int((u & 0x80000000u) | ((a >> 3) + 0x38000000u)), int(u << 29));
+}
+
 template <typename T>
 __device__ __forceinline__ T round_to(double v);
 template <>
@@ -87,6 +98,17 @@ __device__ __forceinline__ float round_to<float>(double v) {
 }
 template <>
 __device__ __forceinline__ double round_to<double>(double v) {
+  return v;
+}
+// round_to<T>, returned as f64 (exact)
+template <typename T>
+__device__ __forceinline__ double rround(double v);
+template <>
+__device__ __forceinline__ double rround<float>(double v) {
+  return widen_f32(__double2float_rn(v));
+}
+template <>
+__device__ __forceinline__ double rround<double>(double v) {
   return v;
 }
 

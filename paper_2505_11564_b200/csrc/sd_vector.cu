@@ -15,6 +15,8 @@
 
 #include <vector>
 
+#include <cstdlib>
+
 #include "sd_common.cuh"
 
 namespace sd {
@@ -172,7 +174,7 @@ __global__ void __launch_bounds__(256) k_cgs_update(const T* __restrict__ Q, uin
       VU<T> q;
       q.v = __ldg(reinterpret_cast<const V*>(Q + uint64_t(i) * ldq + e));
 #pragma unroll
-      for (int k = 0; k < W; ++k) v[k] = double(round_to<T>(__dadd_rn(v[k], __dmul_rn(cs[i], double(q.a[k])))));
+      for (int k = 0; k < W; ++k) v[k] = rround<T>((__dadd_rn(v[k], __dmul_rn(cs[i], double(q.a[k])))));
     }
 #pragma unroll
     for (int k = 0; k < W; ++k) rv.a[k] = T(v[k]);
@@ -180,7 +182,7 @@ __global__ void __launch_bounds__(256) k_cgs_update(const T* __restrict__ Q, uin
   } else {
     for (uint64_t m = e; m < n && m < e + W; ++m) {
       double v = double(r[m]);
-      for (int i = 0; i < j; ++i) v = double(round_to<T>(__dadd_rn(v, __dmul_rn(cs[i], double(Q[uint64_t(i) * ldq + m])))));
+      for (int i = 0; i < j; ++i) v = rround<T>((__dadd_rn(v, __dmul_rn(cs[i], double(Q[uint64_t(i) * ldq + m])))));
       r[m] = T(v);
     }
   }
@@ -278,7 +280,7 @@ __global__ void k_cgs_edges(const T* __restrict__ Q, uint64_t ldq, int j, T* __r
   const uint64_t slot = t < n_head ? t : tail_slot + (t - n_head);
   double v = double(r[li]);
   if (UPD) {
-    for (int i = 0; i < j; ++i) v = double(round_to<T>(__dadd_rn(v, __dmul_rn(-coef[i], double(Q[uint64_t(i) * ldq + li])))));
+    for (int i = 0; i < j; ++i) v = rround<T>((__dadd_rn(v, __dmul_rn(-coef[i], double(Q[uint64_t(i) * ldq + li])))));
     r[li] = T(v);
   }
   if (MODE == 1)
@@ -434,6 +436,163 @@ static void launch_axpy_dot(const void* x, void* y, const void* z, const double*
   }
 }
 
+// Fused Gram-Schmidt pass over full grid blocks: one CTA per 1024-element
+// block, walked in CH-element chunks that are double-buffered in shared
+// memory with cp.async (one HBM read of the j basis columns per pass):
+//   UPD : r[e] = axpy(-c_{j-1}, q_{j-1}, ... axpy(-c_0, q_0, r))[e]  (thread = element)
+//   dots: continue the serial f64 fold of q_i . r_new (thread = column i)
+// Same arithmetic and fold order as k_cgs_update + k_cgs_dots.
+constexpr int kCgsChunk = 64;
+constexpr int kCgsMaxCols = 2 * 128;  // columns per CTA (acc[2] per thread)
+
+template <typename T>
+struct CgsSmem {
+  static constexpr int PAD = 16 / sizeof(T);  // row stride = CH + PAD: 16 B rows, conflict-free column walks
+  static constexpr int STRIDE = kCgsChunk + PAD;
+  static size_t bytes(int j) {
+    return size_t((j + 1) & ~1) * sizeof(double) + size_t(kCgsChunk) * sizeof(double) +
+           2 * size_t(j) * STRIDE * sizeof(T);
+  }
+};
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+               "l"(src)
+               : "memory");
+}
+
+template <typename T, bool UPD>
+__global__ void __launch_bounds__(128) k_cgs_block(const T* __restrict__ Q, uint64_t ldq, int j, T* __restrict__ r,
+                                                   const double* __restrict__ coef, uint64_t base, uint64_t local_end,
+                                                   uint64_t pstride, uint64_t head_n, double* __restrict__ partials) {
+  using V = typename V16<T>::type;
+  constexpr int W = V16<T>::W, CH = kCgsChunk, STRIDE = CgsSmem<T>::STRIDE, NV = CH / W;
+  extern __shared__ __align__(16) unsigned char sm_raw[];
+  double* cs = reinterpret_cast<double*>(sm_raw);
+  double* rt = cs + ((j + 1) & ~1);  // r chunk, widened once per element
+  T* qbuf = reinterpret_cast<T*>(rt + CH);  // [2][j][STRIDE]
+  const int tid = threadIdx.x;
+  const uint64_t unit = blockIdx.x;
+  const uint64_t e0 = base + unit * kBlock;
+  const int n = int((local_end - e0) < kBlock ? (local_end - e0) : kBlock);
+  const bool vec = n == int(kBlock) && ((reinterpret_cast<uintptr_t>(Q + e0) | (ldq * sizeof(T))) & 15) == 0;
+  if (UPD)
+    for (int i = tid; i < j; i += blockDim.x) cs[i] = -coef[i];
+  auto stage = [&](int c0, T* dst) {
+    if (vec) {
+      for (int idx = tid; idx < j * NV; idx += blockDim.x) {
+        const int i = idx / NV, v = idx % NV;
+        cp_async16(dst + i * STRIDE + v * W, Q + uint64_t(i) * ldq + e0 + c0 + v * W);
+      }
+    } else {
+      const int cnt = (n - c0) < CH ? (n - c0) : CH;
+      for (int idx = tid; idx < j * CH; idx += blockDim.x) {
+        const int i = idx / CH, e = idx % CH;
+        if (e < cnt) dst[i * STRIDE + e] = Q[uint64_t(i) * ldq + e0 + c0 + e];
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  double acc0 = 0.0, acc1 = 0.0;
+  stage(0, qbuf);
+  for (int c0 = 0, it = 0; c0 < n; c0 += CH, ++it) {
+    const int cnt = (n - c0) < CH ? (n - c0) : CH;
+    T* qt = qbuf + (it & 1) * j * STRIDE;
+    // prefetch the next chunk into the other buffer (its readers finished at
+    // the previous iteration's trailing barrier)
+    if (c0 + CH < n) {
+      stage(c0 + CH, qbuf + ((it + 1) & 1) * j * STRIDE);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();
+    if (tid < cnt) {
+      T rv = r[e0 + c0 + tid];
+      if (UPD) {
+        double v = double(rv);
+        for (int i = 0; i < j; ++i) v = rround<T>((__dadd_rn(v, __dmul_rn(cs[i], double(qt[i * STRIDE + tid])))));
+        rv = T(v);
+        r[e0 + c0 + tid] = rv;
+        rt[tid] = v;
+      } else {
+        rt[tid] = double(rv);
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int col = tid + 128 * h;
+      if (col < j) {
+        const T* qr = qt + col * STRIDE;
+        double a = h ? acc1 : acc0;
+        if (cnt == CH) {
+#pragma unroll 4
+          for (int e = 0; e < CH; e += W) {
+            VU<T> q;
+            q.v = *reinterpret_cast<const V*>(qr + e);
+#pragma unroll
+            for (int k = 0; k < W; ++k) a = __dadd_rn(a, __dmul_rn(double(q.a[k]), rt[e + k]));
+          }
+        } else {
+          for (int e = 0; e < cnt; ++e) a = __dadd_rn(a, __dmul_rn(double(qr[e]), rt[e]));
+        }
+        if (h) acc1 = a;
+        else acc0 = a;
+      }
+    }
+    __syncthreads();  // rt and this buffer are free for the next iteration
+  }
+  if (tid < j) partials[uint64_t(tid) * pstride + head_n + unit] = acc0;
+  if (tid + 128 < j) partials[uint64_t(tid + 128) * pstride + head_n + unit] = acc1;
+}
+
+template <typename T>
+static bool launch_cgs_fused(const void* Q, uint64_t ldq, uint64_t j, void* r, const double* coef, int mode,
+                             const PartialShape& ps, uint64_t local_end, uint64_t plen, double* partials,
+                             cudaStream_t s) {
+  static const bool enabled = [] {
+    const char* e = std::getenv("SD_CGS_FUSED");
+    return !(e && e[0] == '0');
+  }();
+  constexpr size_t kMaxSmem = 100 * 1024;
+  const size_t smem = CgsSmem<T>::bytes(int(j));
+  if (!enabled || mode != 1 || j > uint64_t(kCgsMaxCols) || smem > kMaxSmem) return false;
+  // the in-CTA update is a j-long dependent chain per element: beyond ~40
+  // columns the element-parallel k_cgs_update followed by the block dots is
+  // faster than the fused single read (measured, scratch/bench_lanczos_kernels.py)
+  if (coef != nullptr && j >= 40) {
+    constexpr int W = V16<T>::W;
+    const uint64_t threads = (local_end + W - 1) / W;
+    k_cgs_update<T><<<unsigned((threads + 255) / 256), 256, size_t(j) * sizeof(double), s>>>(
+        (const T*)Q, ldq, int(j), (T*)r, coef, local_end);
+    SD_LAUNCHED("k_cgs_update");
+    coef = nullptr;
+  }
+  static const bool attr = [] {
+    SD_CUDA(cudaFuncSetAttribute(k_cgs_block<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kMaxSmem)));
+    SD_CUDA(cudaFuncSetAttribute(k_cgs_block<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kMaxSmem)));
+    return true;
+  }();
+  (void)attr;
+  const uint64_t tail_begin = ps.n_head + ps.n_sums * kBlock;
+  const bool upd = coef != nullptr;
+  if (ps.n_sums) {
+    auto kern = upd ? k_cgs_block<T, true> : k_cgs_block<T, false>;
+    kern<<<unsigned(ps.n_sums), 128, smem, s>>>((const T*)Q, ldq, int(j), (T*)r, coef, ps.n_head, local_end, plen,
+                                                ps.n_head, partials);
+    SD_LAUNCHED("k_cgs_block");
+  }
+  if (ps.n_head + ps.n_tail) {
+    auto kern = upd ? k_cgs_edges<T, true, 1> : k_cgs_edges<T, false, 1>;
+    kern<<<grid_for(ps.n_head + ps.n_tail, 128), 128, 0, s>>>((const T*)Q, ldq, int(j), (T*)r, coef, ps.n_head,
+                                                              tail_begin, ps.n_tail, ps.n_head + ps.n_sums, plen,
+                                                              partials);
+    SD_LAUNCHED("k_cgs_edges");
+  }
+  return true;
+}
+
 template <typename T>
 static void launch_cgs(const void* Q, uint64_t ldq, uint64_t j, void* r, const double* coef, int mode, uint64_t begin,
                        uint64_t end, uint64_t total, double* partials, uint64_t pstride, cudaStream_t s) {
@@ -443,6 +602,7 @@ static void launch_cgs(const void* Q, uint64_t ldq, uint64_t j, void* r, const d
   const uint64_t tail_begin = ps.n_head + ps.n_sums * kBlock;
   const bool upd = coef != nullptr;
   if (!upd && mode == 0) fail(SD_ARGUMENT_ERROR, "cgs with neither update nor dots");
+  if (launch_cgs_fused<T>(Q, ldq, j, r, coef, mode, ps, local_end, plen, partials, s)) return;
   // (1) the j sequential axpys, element-parallel and streaming
   if (upd) {
     constexpr int W = V16<T>::W;

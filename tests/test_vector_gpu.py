@@ -141,3 +141,33 @@ def test_ritz_matches_oracle(sd, oracle):
     assert np.max(np.abs(mine.values - v)) <= 1e-12 * np.max(np.abs(v))
     assert np.max(np.abs(mine.weights - w)) <= 1e-12
     assert mine.residual <= 1e-12 and abs(mine.weights.sum() - 1) <= 1e-12
+
+
+def test_f32_rounding_edge_cases(sd):
+    # the reduced-precision axpy rounds f64 -> f32 on the integer pipe in the
+    # fp32 normal range; it must equal IEEE round-to-nearest-even everywhere
+    # (ties, carries into the exponent, overflow, subnormal and zero results)
+    import ctypes as C
+    rng = np.random.default_rng(7)
+    n = 1 << 20
+    e = rng.integers(-150, 128, n)
+    y = (rng.standard_normal(n) * np.exp2(e.astype(np.float64))).astype(np.float32)
+    x = (rng.standard_normal(n) * np.exp2(rng.integers(-40, 40, n).astype(np.float64))).astype(np.float32)
+    special = np.array([1.0, 1.0, -1.0, 3.4028235e38, 1.1754944e-38, 1e-45, 0.0, -0.0, 1.0, np.inf, -np.inf],
+                       np.float32)
+    xs = np.array([2.0 ** -24, 3 * 2.0 ** -24, -(2.0 ** -24), 1e32, -1e-45, 1e-45, 0.0, 0.0, -1.0, 1.0, 1.0],
+                  np.float32)
+    y[: special.size] = special
+    x[: xs.size] = xs
+    x[-4:] = np.float32(1e30)
+    y[-4:] = np.float32(3.0e38)
+    for alpha in (1.0, 0.3, -1.7e-5, 3.0e8):
+        want = (y.astype(np.float64) + np.float64(alpha) * x.astype(np.float64)).astype(np.float32)
+        ty, tx = torch.from_numpy(y.copy()).cuda(), torch.from_numpy(x).cuda()
+        ta = torch.tensor([alpha], dtype=torch.float64, device="cuda")
+        rc = sd._lib.lib().sd_k_axpy(C.c_void_p(tx.data_ptr()), C.c_void_p(ty.data_ptr()), n,
+                                     C.c_void_p(ta.data_ptr()), C.c_double(1.0), sd.F32,
+                                     C.c_void_p(torch.cuda.current_stream().cuda_stream))
+        assert rc == 0
+        got = ty.cpu().numpy()
+        assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), alpha
