@@ -204,6 +204,24 @@ sd_status sd_gpt_hvp(sd_gpt g, const float* v, float* hv, sd_stream s);
 sd_status sd_gpt_last_loss(sd_gpt g, double* loss, sd_stream s);
 sd_status sd_gpt_destroy(sd_gpt g);
 
+/* ---------------------------------------------------------- MLP HVP engine
+ * SPEC.md:179 mlp(layer_widths): tanh hidden layers, linear output, mse
+ * loss; flat parameters W_0 [w0 x w1] row-major, b_0 [w1], W_1, b_1, ...
+ * (declaration order). Same forward-over-reverse HVP as the GPT
+ * engine; the engine owns its (small) device workspace. */
+typedef struct sd_mlp_s* sd_mlp;
+uint64_t sd_mlp_param_count(const uint64_t* widths, int n_widths);
+/* theta: caller-owned device parameters (P floats); n_max: batch capacity */
+sd_status sd_mlp_create(const uint64_t* widths, int n_widths, int n_max, const float* theta, sd_stream s,
+                        sd_mlp* out);
+/* host f32 features [n x w0] and targets [n x w_last], row-major; Hv is
+ * scaled by loss_scale relative to the SUM of squared errors
+ * (loss_scale = 1/(n*w_last) for the mean of SPEC's mse) */
+sd_status sd_mlp_set_batch(sd_mlp m, const float* x, const float* y, int n, float loss_scale, sd_stream s);
+sd_status sd_mlp_hvp(sd_mlp m, const float* v, float* hv, sd_stream s);
+sd_status sd_mlp_last_loss(sd_mlp m, double* loss);
+sd_status sd_mlp_destroy(sd_mlp m);
+
 /* ------------------------------------------------------------ operators
  * OperatorHandle (operators.hpp:15-21): apply(x, y) on this rank's shard.
  * x_full is the gathered logical vector when the operator needs it. */
@@ -218,6 +236,8 @@ sd_status sd_operator_diag(uint64_t dim, const void* d_dev, int prec, sd_operato
 /* Lanczos operator y = H x of a GPT engine; with comm, per-rank Hv over
  * data-sharded batches are summed with an NCCL all-reduce (Alg. 1). */
 sd_status sd_operator_gpt(sd_gpt g, sd_comm comm, sd_operator* out);
+/* Lanczos operator y = H x of an MLP engine (all-reduced over comm if given) */
+sd_status sd_operator_mlp(sd_mlp m, sd_comm comm, sd_operator* out);
 sd_status sd_operator_apply(sd_operator op, const void* x, void* y, int prec, sd_stream s);
 uint64_t sd_operator_dim(sd_operator op);
 sd_status sd_operator_destroy(sd_operator op);

@@ -117,3 +117,16 @@ def test_quadrature_known_answers(sd, oracle):
     assert mine.residual <= 1e-12 and abs(mine.weights.sum() - 1) <= 1e-12
     avg = sd.average_spectra([mine, mine])
     assert np.allclose(np.unique(avg.values), np.unique(mine.values)) and abs(avg.weights.sum() - 1) < 1e-12
+
+
+def test_columnar_loader(tmp_path):
+    # SPEC.md:227 columnar batches: features then target, whitespace separated
+    from paper_2505_11564_b200 import mlp
+    from paper_2505_11564_b200._lib import ConfigError
+    p = tmp_path / "b.txt"
+    p.write_text("# x0 x1 y\n1 2 3\n4.5 -1 0.25\n\n")
+    x, y = mlp.load_columnar(str(p))
+    assert x.tolist() == [[1, 2], [4.5, -1]] and y.tolist() == [[3], [0.25]]
+    p.write_text("1 2 3\n4 5\n")
+    with pytest.raises(ConfigError):
+        mlp.load_columnar(str(p))
