@@ -110,6 +110,16 @@ sd_status sd_k_cgs(const void* Q, uint64_t ldq, uint64_t j, void* r, const doubl
  * n x n f64 on device; rows [row_begin, row_end). */
 sd_status sd_k_dense_apply(const double* a, uint64_t n, const void* x_full, void* y, uint64_t row_begin,
                            uint64_t row_end, int prec, sd_stream s);
+/* column_report statistics of one shard (SPEC.md column_probe module):
+ * counts[t] = #{i : |x_i| < thresholds[t]} (strict, <= 32 thresholds) and
+ * max_abs = max |x_i|; then the histogram of |x| over [0, max_abs] in `bins`
+ * uniform bins, bin = min(bins-1, floor(|x|/max_abs*bins)) in f64 (all in bin
+ * 0 when max_abs == 0). Host outputs; both calls synchronise the stream.
+ * Across shards: max of maxima, sums of counts (integer, layout-invariant). */
+sd_status sd_k_abs_stats(const void* x, uint64_t n, int prec, const double* thresholds, int n_thresholds,
+                         uint64_t* counts, double* max_abs, sd_stream s);
+sd_status sd_k_abs_histogram(const void* x, uint64_t n, int prec, double max_abs, int bins, uint64_t* counts,
+                             sd_stream s);
 
 /* ------------------------------------------------------- quadrature (host)
  * ritz_decompose: implicit-shift QL, f64. values ascending;
@@ -287,6 +297,9 @@ sd_status sd_lanczos_result(sd_lanczos L, double* alphas, double* betas, sd_lanc
  * (column-major, ld = shard length; *ncols columns; NULL if not stored). */
 const void* sd_lanczos_current(sd_lanczos L);
 sd_status sd_lanczos_basis(sd_lanczos L, const void** basis, uint64_t* ncols);
+/* loss_of_orthogonality: max_{i!=j} |q_i^T q_j| over the
+ * stored basis (full reorth only; state error otherwise), reference dots. */
+sd_status sd_lanczos_orthogonality(sd_lanczos L, double* out);
 sd_status sd_lanczos_end(sd_lanczos L);
 
 #ifdef __cplusplus

@@ -417,3 +417,20 @@ def oracle() -> Oracle:
 
 def nthreads() -> int:
     return int(os.environ.get("ORACLE_THREADS", os.cpu_count() or 1))
+
+
+def column_report(x, thresholds, bins=50):
+    """CPU restatement of SPEC.md column_probe.column_report (strict |x| < t
+    fractions; `bins` uniform bins over [0, max|x|], bin = min(bins-1,
+    floor(|x| / max * bins)) in f64, all in bin 0 for an all-zero column).
+    Test infrastructure only: the checker for sd_k_abs_stats/_histogram."""
+    a = np.abs(np.asarray(x, np.float64))
+    thr = np.asarray(thresholds, np.float64)
+    below = np.array([(a < t).sum() for t in thr], np.uint64)
+    mx = float(a.max()) if a.size else 0.0
+    if mx > 0:
+        b = np.minimum(np.floor(a / mx * float(bins)), bins - 1).astype(np.int64)
+    else:
+        b = np.zeros(a.size, np.int64)
+    counts = np.bincount(b, minlength=bins).astype(np.uint64)
+    return below, counts, mx

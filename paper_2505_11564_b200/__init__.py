@@ -14,4 +14,4 @@ from .core import (F32, F64, GAUSSIAN, ONE_HOT, RADEMACHER, REORTH_FULL, REORTH_
                    LanczosConfig, LanczosResult, OperatorHandle, ProbeSpec, RitzSpectrum, ShardedVector, ShardLayout,
                    WorkerPool)
 
-from . import gemm, gpt, mlp  # noqa: E402,F401
+from . import column_probe, diagnostics, gemm, gpt, mlp, slq  # noqa: E402,F401

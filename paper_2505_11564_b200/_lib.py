@@ -96,6 +96,8 @@ _SIGS = {
     "sd_k_axpy_dot": (i32, [vp, vp, vp, vp, u64, u64, u64, i32, vp, vp]),
     "sd_k_cgs": (i32, [vp, u64, u64, vp, vp, i32, u64, u64, u64, i32, vp, vp]),
     "sd_k_dense_apply": (i32, [vp, u64, vp, vp, u64, u64, i32, vp]),
+    "sd_k_abs_stats": (i32, [vp, u64, i32, vp, i32, vp, vp, vp]),
+    "sd_k_abs_histogram": (i32, [vp, u64, i32, C.c_double, i32, vp, vp]),
     "sd_ritz_decompose": (i32, [u64, dp, dp, dp, dp, dp]),
     "sd_smooth_density": (i32, [u64, dp, dp, C.c_double, u64, dp, dp, dp]),
     "sd_wigner_dense": (i32, [u64, C.c_double, u64, dp]),
@@ -119,6 +121,7 @@ _SIGS = {
     "sd_lanczos_result": (i32, [vp, dp, dp, C.POINTER(LanczosInfo)]),
     "sd_lanczos_current": (vp, [vp]),
     "sd_lanczos_basis": (i32, [vp, C.POINTER(vp), u64p]),
+    "sd_lanczos_orthogonality": (i32, [vp, dp]),
     "sd_lanczos_end": (i32, [vp]),
 }
 

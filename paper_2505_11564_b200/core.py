@@ -442,6 +442,13 @@ class Lanczos:
             res.basis = Q.double().cpu().numpy()
         return res
 
+    def loss_of_orthogonality(self) -> float:
+        """max_{i != j} |q_i^T q_j| over the stored basis
+        (reference dots on the device); StateError without a stored basis."""
+        out = C.c_double()
+        check(lib().sd_lanczos_orthogonality(self.h, C.byref(out)))
+        return out.value
+
     def close(self):
         if self.h:
             lib().sd_lanczos_end(self.h)

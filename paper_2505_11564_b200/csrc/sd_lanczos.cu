@@ -14,6 +14,7 @@
 // host once per step for the breakdown test (beta < eps).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <memory>
 #include <string>
@@ -299,6 +300,28 @@ sd_status sd_lanczos_basis(sd_lanczos L, const void** basis, uint64_t* ncols) {
     if (L->cfg.reorth != SD_REORTH_FULL) sd::fail(SD_STATE_ERROR, "basis was not stored (reorth = none)");
     *basis = L->col(0);
     *ncols = L->ncols;
+  });
+}
+
+// loss_of_orthogonality: max_{i != j} |q_i^T q_j| over the
+// stored columns, every dot the reference's blocked f64 fold (rank-ordered
+// across shards); column i is dotted against columns 0..i-1 in one pass.
+sd_status sd_lanczos_orthogonality(sd_lanczos L, double* out) {
+  return sd::guard([&] {
+    if (!L || !out) sd::fail(SD_ARGUMENT_ERROR, "null argument");
+    if (L->cfg.reorth != SD_REORTH_FULL) sd::fail(SD_STATE_ERROR, "basis was not stored (reorth = none)");
+    const uint64_t B = L->begin(), E = L->end();
+    double worst = 0.0;
+    std::vector<double> h(L->plan.m_max);
+    for (uint64_t i = 1; i < L->ncols; ++i) {
+      sd::cgs(L->col(0), L->plan.P, i, L->col(i), nullptr, 1, B, E, L->total, L->cfg.prec, L->send(),
+              L->plan.pstride, L->s);
+      L->reduce(i, L->d_c1(), 0);
+      SD_CUDA(cudaMemcpyAsync(h.data(), L->d_c1(), i * sizeof(double), cudaMemcpyDeviceToHost, L->s));
+      SD_CUDA(cudaStreamSynchronize(L->s));
+      for (uint64_t j = 0; j < i; ++j) worst = std::max(worst, std::fabs(h[j]));
+    }
+    *out = worst;
   });
 }
 

@@ -15,6 +15,7 @@
 
 #include <vector>
 
+#include <cmath>
 #include <cstdlib>
 
 #include "sd_common.cuh"
@@ -710,6 +711,110 @@ void diag_apply(const void* d, const void* x, void* y, uint64_t n, int prec, cud
   SD_LAUNCHED("k_diag_apply");
 }
 
+// ------------------------------------------------------ column statistics
+// column_report (SPEC.md column_probe): strict threshold counts |x| < t_k and
+// max |x| in one pass; then a histogram of |x| over [0, max] in `bins`
+// uniform bins, bin = min(bins - 1, floor(|x| / max * bins)) in f64 (max == 0:
+// everything in bin 0). Integer counts: layout-invariant and bit-exact.
+constexpr int kMaxThr = 32;
+template <typename T>
+__global__ void __launch_bounds__(256) k_abs_stats(const T* __restrict__ x, uint64_t n, const double* __restrict__ thr,
+                                                   int n_thr, unsigned long long* __restrict__ counts,
+                                                   unsigned long long* __restrict__ max_bits) {
+  __shared__ unsigned int sc[kMaxThr];
+  __shared__ unsigned long long smax;
+  if (threadIdx.x < kMaxThr) sc[threadIdx.x] = 0;
+  if (threadIdx.x == 0) smax = 0;
+  __syncthreads();
+  unsigned int c[kMaxThr];
+#pragma unroll
+  for (int k = 0; k < kMaxThr; ++k) c[k] = 0;
+  double m = 0.0;
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
+    const double a = fabs(double(x[i]));
+    m = fmax(m, a);
+#pragma unroll
+    for (int k = 0; k < kMaxThr; ++k)
+      if (k < n_thr && a < thr[k]) ++c[k];
+  }
+  for (int k = 0; k < n_thr; ++k) atomicAdd(&sc[k], c[k]);
+  atomicMax(&smax, static_cast<unsigned long long>(__double_as_longlong(m)));
+  __syncthreads();
+  if (threadIdx.x < n_thr) atomicAdd(&counts[threadIdx.x], (unsigned long long)sc[threadIdx.x]);
+  if (threadIdx.x == 0) atomicMax(max_bits, smax);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_abs_hist(const T* __restrict__ x, uint64_t n, double mx, int bins,
+                                                  unsigned long long* __restrict__ counts) {
+  extern __shared__ unsigned int sh[];
+  for (int b = threadIdx.x; b < bins; b += blockDim.x) sh[b] = 0;
+  __syncthreads();
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
+    int b = 0;
+    if (mx > 0.0) {
+      const double t = floor(__dmul_rn(__ddiv_rn(fabs(double(x[i])), mx), double(bins)));
+      b = t >= double(bins - 1) ? bins - 1 : int(t);
+    }
+    atomicAdd(&sh[b], 1u);
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < bins; b += blockDim.x)
+    if (sh[b]) atomicAdd(&counts[b], (unsigned long long)sh[b]);
+}
+
+unsigned stats_grid(uint64_t n) {
+  const uint64_t g = (n + 255) / 256;
+  return unsigned(g < 148 * 8 ? (g ? g : 1) : 148 * 8);
+}
+
+void abs_stats(const void* x, uint64_t n, int prec, const double* thr_host, int n_thr, uint64_t* counts_host,
+               double* max_host, cudaStream_t s) {
+  if (n_thr < 0 || n_thr > kMaxThr) fail(SD_ARGUMENT_ERROR, "column stats: 0..32 thresholds");
+  void* buf = nullptr;
+  const size_t bytes = sizeof(double) * kMaxThr + sizeof(unsigned long long) * (kMaxThr + 1);
+  SD_CUDA(cudaMallocAsync(&buf, bytes, s));
+  double* thr = static_cast<double*>(buf);
+  auto* cnt = reinterpret_cast<unsigned long long*>(thr + kMaxThr);
+  SD_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * (kMaxThr + 1), s));
+  if (n_thr) SD_CUDA(cudaMemcpyAsync(thr, thr_host, sizeof(double) * n_thr, cudaMemcpyHostToDevice, s));
+  if (n) {
+    if (prec == SD_F32)
+      k_abs_stats<float><<<stats_grid(n), 256, 0, s>>>((const float*)x, n, thr, n_thr, cnt, cnt + kMaxThr);
+    else
+      k_abs_stats<double><<<stats_grid(n), 256, 0, s>>>((const double*)x, n, thr, n_thr, cnt, cnt + kMaxThr);
+    SD_LAUNCHED("k_abs_stats");
+  }
+  unsigned long long h[kMaxThr + 1];
+  SD_CUDA(cudaMemcpyAsync(h, cnt, sizeof(h), cudaMemcpyDeviceToHost, s));
+  SD_CUDA(cudaFreeAsync(buf, s));
+  SD_CUDA(cudaStreamSynchronize(s));
+  for (int k = 0; k < n_thr; ++k) counts_host[k] = h[k];
+  *max_host = __builtin_bit_cast(double, h[kMaxThr]);
+}
+
+void abs_hist(const void* x, uint64_t n, int prec, double mx, int bins, uint64_t* counts_host, cudaStream_t s) {
+  if (bins < 1 || bins > 4096) fail(SD_ARGUMENT_ERROR, "column histogram: 1..4096 bins");
+  if (!(mx >= 0.0) || !std::isfinite(mx)) fail(SD_ARGUMENT_ERROR, "column histogram: max must be finite");
+  void* buf = nullptr;
+  SD_CUDA(cudaMallocAsync(&buf, sizeof(unsigned long long) * bins, s));
+  auto* cnt = static_cast<unsigned long long*>(buf);
+  SD_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * bins, s));
+  if (n) {
+    const size_t sm = sizeof(unsigned int) * bins;
+    if (prec == SD_F32)
+      k_abs_hist<float><<<stats_grid(n), 256, sm, s>>>((const float*)x, n, mx, bins, cnt);
+    else
+      k_abs_hist<double><<<stats_grid(n), 256, sm, s>>>((const double*)x, n, mx, bins, cnt);
+    SD_LAUNCHED("k_abs_hist");
+  }
+  std::vector<unsigned long long> h(bins);
+  SD_CUDA(cudaMemcpyAsync(h.data(), cnt, sizeof(unsigned long long) * bins, cudaMemcpyDeviceToHost, s));
+  SD_CUDA(cudaFreeAsync(buf, s));
+  SD_CUDA(cudaStreamSynchronize(s));
+  for (int b = 0; b < bins; ++b) counts_host[b] = h[b];
+}
+
 }  // namespace sd
 
 // ------------------------------------------------------------------ C-ABI
@@ -762,6 +867,16 @@ sd_status sd_k_axpy_dot(const void* x, void* y, const void* z, const double* coe
 sd_status sd_k_cgs(const void* Q, uint64_t ldq, uint64_t j, void* r, const double* coef, int mode, uint64_t begin,
                    uint64_t end, uint64_t total, int prec, double* partials, sd_stream s) {
   return guard([&] { cgs(Q, ldq, j, r, coef, mode, begin, end, total, prec, partials, 0, (cudaStream_t)s); });
+}
+
+sd_status sd_k_abs_stats(const void* x, uint64_t n, int prec, const double* thresholds, int n_thresholds,
+                         uint64_t* counts, double* max_abs, sd_stream s) {
+  return guard([&] { abs_stats(x, n, prec, thresholds, n_thresholds, counts, max_abs, (cudaStream_t)s); });
+}
+
+sd_status sd_k_abs_histogram(const void* x, uint64_t n, int prec, double max_abs, int bins, uint64_t* counts,
+                             sd_stream s) {
+  return guard([&] { abs_hist(x, n, prec, max_abs, bins, counts, (cudaStream_t)s); });
 }
 
 sd_status sd_k_dense_apply(const double* a, uint64_t n, const void* x_full, void* y, uint64_t row_begin,

@@ -1,0 +1,165 @@
+"""The consumers of the path on the GPU: SLQ runs + artifacts
+(SPEC cmd_slq / compare_ortho), column probes (SPEC column_probe) and the
+basis diagnostics (loss_of_orthogonality), checked against the oracle, dense
+eigensolvers and the SPEC acceptance criteria 2, 4, 7, 8, 9."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle.pyoracle import F32, F64, RADEMACHER, column_report  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def sd():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_2505_11564_b200 as sd
+    return sd
+
+
+def cfg_of(sd, k, reorth, prec=F64, seed=0):
+    return sd.LanczosConfig(k_max=k, reorthogonalize=reorth, prec=prec,
+                            probe=sd.ProbeSpec(seed=seed, distribution=RADEMACHER))
+
+
+def test_probe_column_exact(sd):
+    from paper_2505_11564_b200 import column_probe as cp
+    op = sd.dense_operator(np.diag([1.0, 2.0, 3.0]))
+    pool = sd.make_pool(3, 1)
+    assert sd.gather(pool, cp.probe_column(op, pool, 1, F64)).tolist() == [0.0, 2.0, 0.0]
+    A = sd.wigner_dense(64, 1.0, 3)
+    op = sd.dense_operator(A)
+    for workers in (1, 4):
+        pool = sd.make_pool(64, workers)
+        for k in (0, 17, 63):
+            assert np.array_equal(sd.gather(pool, cp.probe_column(op, pool, k, F64)), A[:, k])
+    with pytest.raises(sd.ArgumentError):
+        cp.probe_column(op, sd.make_pool(64, 1), 64, F64)
+
+
+@pytest.mark.parametrize("prec", [F32, F64])
+def test_column_report_matches_oracle_and_is_layout_invariant(sd, prec):
+    from paper_2505_11564_b200 import column_probe as cp
+    rng = np.random.default_rng(5)
+    n = 300007
+    x = rng.standard_normal(n) * np.exp2(rng.integers(-45, 3, n))
+    x[:1000] = 0.0
+    x[1000] = -np.abs(x).max() * 1.5                    # the max lands in the last bin
+    x[1001:1100] = x[1000] * (np.arange(99) / 50.0 - 1.0)  # exact bin-edge multiples
+    x = x.astype(np.float32 if prec == F32 else np.float64)
+    want_below, want_counts, want_max = column_report(x, cp.THRESHOLDS, 50)
+    reports = []
+    for workers in (1, 3, 8):
+        pool = sd.make_pool(n, workers)
+        v = sd.scatter(pool, x.astype(np.float64), prec)
+        r = cp.column_report(v, 0, bins=50)
+        assert r.max_abs == want_max
+        assert r.below.tolist() == want_below.tolist() and r.counts.tolist() == want_counts.tolist()
+        assert np.all(np.diff(r.fractions) >= 0) and int(r.counts.sum()) == n
+        reports.append(r)
+    assert all(np.array_equal(reports[0].fractions, r.fractions) for r in reports)
+    z = cp.column_report(sd.scatter(sd.make_pool(10, 2), np.zeros(10), prec), 3)
+    assert z.counts[0] == 10 and np.all(z.fractions == 1.0)
+    t = cp.column_report(sd.scatter(sd.make_pool(3, 1), np.array([0.0, 0.0, 1.0]), prec), 2)
+    assert t.fractions[-1] == 2.0 / 3.0  # fraction below 1e-1
+
+
+def test_multi_seed_probe_and_report_files(sd, tmp_path):
+    from paper_2505_11564_b200 import column_probe as cp
+    op = sd.dense_operator(np.eye(64) * 2.0)
+    pool = sd.make_pool(64, 2)
+    reps = cp.multi_seed_probe(op, pool, [1, 2, 3, 4, 5], F64)
+    assert len(reps) == 5 and all(r.fractions[-1] == 63 / 64 for r in reps)  # identity-like: (P-1)/P
+    a, b = cp.write_report(reps[0], str(tmp_path))
+    text = open(a).read()
+    assert text.startswith("threshold,fraction\n1e-12,") and len(text.strip().split("\n")) == 13
+    assert open(b).read().count("\n") == 51
+
+
+def test_loss_of_orthogonality(sd):
+    op = sd.spiked_operator(256, 1.0 / 16, [100.0, -100.0], 7)
+    L = sd.Lanczos(op, cfg_of(sd, 25, sd.REORTH_FULL))
+    while not L.step():
+        pass
+    Q = L.result(with_basis=True).basis
+    lo = L.loss_of_orthogonality()
+    G = Q @ Q.T
+    assert lo <= 1e-10 and abs(lo - np.max(np.abs(G - np.diag(np.diag(G))))) <= 1e-12
+    L.close()
+    L = sd.Lanczos(op, cfg_of(sd, 5, sd.REORTH_NONE))
+    L.step()
+    with pytest.raises(sd.StateError):
+        L.loss_of_orthogonality()
+    L.close()
+
+
+def test_slq_exactness_and_moments(sd, tmp_path):
+    # acceptance 2: dense 64x64 from a file, k=64, full ortho -> Ritz == eigvalsh within 1e-8;
+    # Gauss moments sum w theta^m == q0^T A^m q0 for m <= 2k-1 (k in {5, 10}, 256x256) at 1e-8 rel
+    from paper_2505_11564_b200 import slq
+    A = sd.wigner_dense(64, 1.0, 11)
+    p = tmp_path / "a.txt"
+    p.write_text("dim 64\n" + "\n".join(" ".join(repr(float(x)) for x in row) for row in A) + "\n")
+    op = sd.dense_operator(slq.load_dense(str(p)))
+    art = slq.slq(op, cfg_of(sd, 64, sd.REORTH_FULL), [0])
+    lam = np.linalg.eigvalsh(A)
+    assert art.spectrum.values.size == 64 and np.max(np.abs(np.sort(art.spectrum.values) - lam)) < 1e-8
+    B = sd.wigner_dense(256, 1.0, 12)
+    opb = sd.dense_operator(B)
+    pool = sd.make_pool(256, 1)
+    q0 = sd.gather(pool, sd.draw_probe(pool, sd.ProbeSpec(seed=0, distribution=RADEMACHER), F64))
+    for k in (5, 10):
+        s = slq.slq(opb, cfg_of(sd, k, sd.REORTH_FULL), [0]).spectrum
+        assert abs(s.weights.sum() - 1.0) < 1e-12
+        x = q0.copy()
+        for m in range(2 * k):
+            mom = q0 @ x
+            got = np.sum(s.weights * s.values ** m)
+            assert abs(got - mom) <= 1e-8 * max(1.0, abs(mom)), (k, m)
+            x = B @ x
+
+
+def test_slq_artifacts_are_deterministic(sd, tmp_path):
+    # acceptance 9 and cmd_slq example: wigner n=256, k=10, one seed
+    from paper_2505_11564_b200 import slq
+    op = sd.wigner_operator(256, 1.0, 0)
+    a1 = slq.slq(op, cfg_of(sd, 10, sd.REORTH_NONE), [0, 1, 2], out_dir=str(tmp_path / "a"))
+    slq.slq(op, cfg_of(sd, 10, sd.REORTH_NONE), [0, 1, 2], out_dir=str(tmp_path / "b"))
+    for name in ("spectrum.csv", "density.csv", "report.txt", "spectrum_seed1.csv"):
+        assert (tmp_path / "a" / name).read_bytes() == (tmp_path / "b" / name).read_bytes()
+    assert all(r.spectrum.values.size == 10 and abs(r.spectrum.weights.sum() - 1) < 1e-12 for r in a1.runs)
+    assert abs(a1.spectrum.weights.sum() - 1.0) < 1e-12
+    # SLQ estimates q^T A^2 q ~ tr(A^2)/n = n sigma^2 for the averaged measure
+    m2 = np.sum(a1.spectrum.weights * a1.spectrum.values ** 2)
+    assert abs(m2 / 256.0 - 1.0) < 0.1
+
+
+def test_ghost_reproduction(sd):
+    # acceptance 4 on a spiked operator (well-separated outliers converge first):
+    # no-ortho k=25 shows flagged ghosts, full-ortho none; at k=10 none on >= 9/10 seeds.
+    # The device run is bitwise the oracle's (test_vector_gpu), so the counts are the oracle's.
+    from paper_2505_11564_b200 import slq
+    op = sd.spiked_operator(256, 1.0 / 16, [100.0, -100.0], 7)
+    none25 = [slq.slq(op, cfg_of(sd, 25, sd.REORTH_NONE, seed=s), [s]).ghosts.n_ghosts for s in range(10)]
+    full25 = [slq.slq(op, cfg_of(sd, 25, sd.REORTH_FULL, seed=s), [s]).ghosts.n_ghosts for s in range(10)]
+    none10 = [slq.slq(op, cfg_of(sd, 10, sd.REORTH_NONE, seed=s), [s]).ghosts.n_ghosts for s in range(10)]
+    assert sum(g > 0 for g in none25) >= 5 and sum(full25) == 0 and sum(g == 0 for g in none10) >= 9
+    cmp = slq.compare_ortho(op, cfg_of(sd, 25, sd.REORTH_NONE), seed=0)
+    assert cmp.none.ghosts.n_ghosts > 0 and cmp.full.ghosts.n_ghosts == 0
+    assert cmp.table().startswith("no_ortho_value,")
+
+
+def test_outlier_recovery(sd):
+    # acceptance 7: spikes +-50 over a unit-radius-scale Wigner bulk, k=10
+    from paper_2505_11564_b200 import slq
+    S = sd.spiked_dense(512, 1.0 / np.sqrt(512), [50.0, -50.0], 3)
+    lam = np.linalg.eigvalsh(S)
+    # one probe's weight at an outlier is (u . q0)^2 ~ chi2_1 / n: average 5 probes (SLQ)
+    s = slq.slq(sd.dense_operator(S), cfg_of(sd, 10, sd.REORTH_NONE), [0, 1, 2, 3, 4]).spectrum
+    assert abs(s.values.max() - lam.max()) <= 0.02 * abs(lam.max())
+    assert abs(s.values.min() - lam.min()) <= 0.02 * abs(lam.min())
+    # the weight of each outlier (summed over its Ritz copies within 2%)
+    for ext in (lam.max(), lam.min()):
+        assert s.weights[np.abs(s.values - ext) <= 0.02 * abs(ext)].sum() > 1e-4
