@@ -178,6 +178,12 @@ sd_status sd_gemm_tf32(const sd_gemm_desc* d, sd_stream s);
  * alpha/beta and the first pair; d2 only its a/b operands, lds and strides
  * (m, n, k, majors and precision must match d1). */
 sd_status sd_gemm_tf32_dual(const sd_gemm_desc* d1, const sd_gemm_desc* d2, sd_stream s);
+/* General form: d2 optional (dual source); flags SD_GEMM_ONCHIP_RESIDUAL =
+ * 3xTF32 with the tf32 residuals of the raw operand tiles computed in shared
+ * memory (a_small/b_small ignored; same result bits as passing
+ * sd_split_tf32(mode 0) residuals, half the operand traffic). */
+enum { SD_GEMM_ONCHIP_RESIDUAL = 1 };
+sd_status sd_gemm_tf32_ex(const sd_gemm_desc* d1, const sd_gemm_desc* d2, int flags, sd_stream s);
 /* small[i] = x[i] - hi(x[i]); mode 0: hi = trunc_tf32 (what the MMA reads),
  * mode 1: hi = round-to-nearest-away tf32. */
 sd_status sd_split_tf32(const float* x, float* small, uint64_t n, int mode, sd_stream s);

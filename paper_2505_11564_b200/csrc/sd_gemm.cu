@@ -8,12 +8,16 @@
 //   A.B ~= A_b.B_b + A_b.B_s + A_s.B_b        (3 tcgen05.mma kind::tf32)
 // which carries ~21-22 significant bits per product (fp32-faithful).
 //
-// Persistent warp-specialised kernel, one CTA per SM, 128 x 128 output tiles
+// Persistent warp-specialised kernel, one CTA per SM, 128 x BN output tiles
 // walked in a static round-robin schedule:
 //   warp 0   : TMA producer (cp.async.bulk.tensor) into a STAGES-deep smem
 //              ring (full/empty mbarriers), running ahead across tiles;
 //   warp 1   : TMEM allocator + single-thread tcgen05.mma issuer;
-//   warps 2-5: epilogue: drain TMEM chunks (tcgen05.ld 32x32b) into
+//   warps 2-3: residual warps: with on-chip residuals (GemmArgs::onchip)
+//              they write x - trunc_tf32(x) of each landed raw tile into its
+//              residual slot (half the bytes through L2/TMA, no residual
+//              arrays in HBM), then release the stage to the MMA (conv[s]);
+//   warps 4-11: epilogue: drain TMEM chunks (tcgen05.ld 32x32b) into
 //              round-to-nearest fp32 registers, then alpha/beta/bias,
 //              residual and store — overlapped with the next tile's MMAs.
 // Operand majors: A is K-major (row-major M x K) or MN-major (row-major K x M);
@@ -87,17 +91,19 @@ void operand_maps(const GemmArgs& g, bool a_mn, bool b_mn, bool three, int box_n
     if (b_mn) make_map(o, p, g.N, g.K, ld, g.Z1, s1, g.Z2, s2, 32, BK, true);
     else make_map(o, p, g.K, g.N, ld, g.Z1, s1, g.Z2, s2, BK, box_n, false);
   };
+  // residual maps only when the residuals come from memory (not on chip)
+  const bool mem_res = three && !g.onchip;
   amap(&m[0], g.A, g.lda, g.sa1, g.sa2);
-  amap(&m[1], three ? g.As : g.A, g.lda, g.sa1, g.sa2);
+  amap(&m[1], mem_res ? g.As : g.A, g.lda, g.sa1, g.sa2);
   bmap(&m[2], g.B, g.ldb, g.sb1, g.sb2);
-  bmap(&m[3], three ? g.Bs : g.B, g.ldb, g.sb1, g.sb2);
+  bmap(&m[3], mem_res ? g.Bs : g.B, g.ldb, g.sb1, g.sb2);
   if (g.A2) {
-    if (!g.B2 || (three && (!g.A2s || !g.B2s)))
+    if (!g.B2 || (mem_res && (!g.A2s || !g.B2s)))
       fail(SD_ARGUMENT_ERROR, "dual-source gemm needs A2, B2 (and their residuals for 3xTF32)");
     amap(&m[4], g.A2, g.lda2, g.sa1_2, g.sa2_2);
-    amap(&m[5], three ? g.A2s : g.A2, g.lda2, g.sa1_2, g.sa2_2);
+    amap(&m[5], mem_res ? g.A2s : g.A2, g.lda2, g.sa1_2, g.sa2_2);
     bmap(&m[6], g.B2, g.ldb2, g.sb1_2, g.sb2_2);
-    bmap(&m[7], three ? g.B2s : g.B2, g.ldb2, g.sb1_2, g.sb2_2);
+    bmap(&m[7], mem_res ? g.B2s : g.B2, g.ldb2, g.sb1_2, g.sb2_2);
   } else {
     for (int i = 0; i < 4; ++i) m[4 + i] = m[i];
   }
@@ -248,7 +254,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   constexpr int STAGE_BYTES = (THREE ? 2 : 1) * (A_BYTES + B_BYTES);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
   uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;  // [2]
+  uint64_t* conv = empty + STAGES;   // [STAGES] residual tiles ready
+  uint64_t* tfull = conv + STAGES;   // [2]
   uint64_t* tempty = tfull + 2;      // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
@@ -258,6 +265,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
+      mbar_init(&conv[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
@@ -289,7 +297,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const uint32_t ph = (g / STAGES) & 1;
           mbar_wait(&empty[s], ph ^ 1);
           unsigned char* st = smem + s * STAGE_BYTES;
-          mbar_expect_tx(&full[s], STAGE_BYTES);
+          mbar_expect_tx(&full[s], ep.res ? A_BYTES + B_BYTES : STAGE_BYTES);
           // dual source: the second product's k-blocks follow the first's
           const bool src2 = kk >= ti.num_kb;
           const int kb = src2 ? kk - ti.num_kb : kk;
@@ -302,26 +310,49 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
             for (int c = 0; c < BM / 32; ++c) {
               tma_load_4d(pA, &full[s], st + c * 2048, ti.m0 + 32 * c, k0, z1, z2);
-              if (THREE) tma_load_4d(pAs, &full[s], st + A_BYTES + c * 2048, ti.m0 + 32 * c, k0, z1, z2);
+              if (THREE && !ep.res) tma_load_4d(pAs, &full[s], st + A_BYTES + c * 2048, ti.m0 + 32 * c, k0, z1, z2);
             }
           } else {
             tma_load_4d(pA, &full[s], st, k0, ti.m0, z1, z2);
-            if (THREE) tma_load_4d(pAs, &full[s], st + A_BYTES, k0, ti.m0, z1, z2);
+            if (THREE && !ep.res) tma_load_4d(pAs, &full[s], st + A_BYTES, k0, ti.m0, z1, z2);
           }
           unsigned char* sb = st + (THREE ? 2 : 1) * A_BYTES;
           if (B_MN) {
 #pragma unroll
             for (int c = 0; c < BN / 32; ++c) {
               tma_load_4d(pB, &full[s], sb + c * 2048, ti.n0 + 32 * c, k0, z1, z2);
-              if (THREE) tma_load_4d(pBs, &full[s], sb + B_BYTES + c * 2048, ti.n0 + 32 * c, k0, z1, z2);
+              if (THREE && !ep.res) tma_load_4d(pBs, &full[s], sb + B_BYTES + c * 2048, ti.n0 + 32 * c, k0, z1, z2);
             }
           } else {
             tma_load_4d(pB, &full[s], sb, k0, ti.n0, z1, z2);
-            if (THREE) tma_load_4d(pBs, &full[s], sb + B_BYTES, k0, ti.n0, z1, z2);
+            if (THREE && !ep.res) tma_load_4d(pBs, &full[s], sb + B_BYTES, k0, ti.n0, z1, z2);
           }
         }
       }
     }
+  } else if (warp >= 2 && warp < 2 + kConvWarps) {
+    // residual warps: once a stage lands, write x - trunc_tf32(x) of the raw
+    // A and B tiles into their residual slots (3xTF32 without residual arrays
+    // in memory: half the operand bytes through L2 and TMA), then release it
+    // (warp w takes the stages with g % kConvWarps == w - 2: two stages in flight)
+    const int cw = warp - 2;
+    uint32_t g = 0;
+    if (THREE && ep.res)
+      for (int t = blockIdx.x; t < ep.n_tiles; t += gridDim.x) {
+        const TileInfo ti = tile_info<BN, CAUSAL>(ep, t, K);
+        if (ti.skip) continue;
+        for (int kk = 0; kk < ep.nsrc * ti.num_kb; ++kk, ++g) {
+          if (int(g % kConvWarps) != cw) continue;
+          const int s = g % STAGES;
+          mbar_wait(&full[s], (g / STAGES) & 1);
+          unsigned char* st = smem + s * STAGE_BYTES;
+          stage_residual(st, st + A_BYTES, A_BYTES, lane, 32);
+          stage_residual(st + 2 * A_BYTES, st + 2 * A_BYTES + B_BYTES, B_BYTES, lane, 32);
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&conv[s]);
+        }
+      }
   } else if (warp == 1) {
     constexpr uint32_t idesc = make_idesc(A_MN, B_MN, BN);
     uint32_t g = 0, chunk = 0;
@@ -336,7 +367,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const bool last = (kb % KC) == KC - 1 || kb == nkb - 1;
         const uint32_t buf = chunk & 1;
         if (first && chunk >= 2) mbar_wait(&tempty[buf], ((chunk >> 1) - 1) & 1);
-        mbar_wait(&full[s], ph);
+        mbar_wait(ep.res ? &conv[s] : &full[s], ph);  // stage landed (and its residuals written)
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         if (lane == 0) {
           const uint32_t d = tmem + buf * BN;
@@ -362,11 +393,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
     }
   } else {
-    // epilogue: 8 warps; warp w drains TMEM lanes 32*(w%4) .. +31 (its
-    // sub-partition) and the column half (w-2)/4 of the tile: thread = one
+    // epilogue: 8 warps (4-11); warp w drains TMEM lanes 32*(w%4) .. +31 (its
+    // sub-partition) and the column half (w-4)/4 of the tile: thread = one
     // output row, EC = BN/2 fp32 accumulators in registers.
     const int sub = warp & 3;
-    const int cb = ((warp - 2) >> 2) * EC;
+    const int cb = ((warp - 2 - kConvWarps) >> 2) * EC;
     uint32_t chunk = 0;
     for (int t = blockIdx.x; t < ep.n_tiles; t += gridDim.x) {
       const TileInfo ti = tile_info<BN, CAUSAL>(ep, t, K);
@@ -447,8 +478,8 @@ void launch(const GemmArgs& g, cudaStream_t s) {
   float* ws = nullptr;
   if (splits > 1) ws = splitk_workspace(size_t(splits) * zc * size_t(g.M) * g.N);
   EpiParams ep{g.C, g.ldc, g.sc1, g.sc2, g.M, g.N, g.Z1, g.alpha, g.beta, g.bias, g.Cs, g.dbg, zc, kb_per, ws,
-               g.causal, tn, tm, tiles * splits, dual ? 2 : 1};
-  const size_t smem = 1024 + size_t(Cf::STAGES) * (THREE ? 2 : 1) * (Cf::A_BYTES + Cf::B_BYTES) + 256;
+               g.causal, tn, tm, tiles * splits, dual ? 2 : 1, g.onchip ? 1 : 0};
+  const size_t smem = 1024 + size_t(Cf::STAGES) * (THREE ? 2 : 1) * (Cf::A_BYTES + Cf::B_BYTES) + 512;
   auto kern = g.causal ? k_gemm_tf32<A_MN, B_MN, THREE, BN, true> : k_gemm_tf32<A_MN, B_MN, THREE, BN, false>;
   static bool attr_set = false;
   if (!attr_set) {
@@ -487,12 +518,25 @@ bool sd_gemm_pair_enabled() {
 
 }  // namespace
 
-void gemm(const GemmArgs& g, cudaStream_t s) {
-  if (g.M <= 0 || g.N <= 0 || g.K <= 0) return;
-  const bool three = g.As != nullptr && g.Bs != nullptr;
+void gemm(const GemmArgs& g_in, cudaStream_t s) {
+  if (g_in.M <= 0 || g_in.N <= 0 || g_in.K <= 0) return;
+  GemmArgs g = g_in;
+  const bool pair = g.causal == 0 && g.M >= 256 && g.N >= 256 && sd_gemm_pair_enabled();
+  // On-chip residuals (onchip = allowed): they halve the operand bytes through
+  // L2 and TMA, which pays where a kernel is operand-bandwidth bound (64-wide
+  // and causal attention tiles, MN-major A in the weight products); the
+  // K-major pair products keep memory residuals when the caller has them
+  // (measured: the per-stage residual hand-off costs more than it saves there).
+  if (g.onchip) {
+    const bool have = g.As && g.Bs && (!g.A2 || (g.A2s && g.B2s));
+    const bool prefer = !pair || g.a_mn;
+    if (have && !prefer) g.onchip = false;
+    else g.As = g.Bs = g.A2s = g.B2s = nullptr;
+  }
+  const bool three = (g.As != nullptr && g.Bs != nullptr) || g.onchip;
   // large non-causal products: 256 x 256 tiles on CTA pairs (half the
   // operand bytes per flop per SM)
-  if (g.causal == 0 && g.M >= 256 && g.N >= 256 && sd_gemm_pair_enabled()) return gemm_pair(g, s);
+  if (pair) return gemm_pair(g, s);
   const bool narrow = g.N <= 64;  // head-dimension outputs: 64-wide tiles
   // 256-wide tiles halve the shared-memory operand traffic per MMA flop (the
   // tf32 SS-MMA at N=128 is shared-memory-bandwidth bound) when there are
@@ -561,20 +605,38 @@ sd_status sd_gemm_tf32(const sd_gemm_desc* d, sd_stream s) {
   return sd::guard([&] { sd::gemm(args_from(d), (cudaStream_t)s); });
 }
 
+// Extended entry: optional dual source (d2) and flags (SD_GEMM_ONCHIP_RESIDUAL:
+// 3xTF32 with the residual tiles computed in shared memory, a_small/b_small
+// ignored). C = alpha (op(A1) op(B1) [+ op(A2) op(B2)]) + beta C, one launch.
+sd_status sd_gemm_tf32_ex(const sd_gemm_desc* d1, const sd_gemm_desc* d2, int flags, sd_stream s) {
+  return sd::guard([&] {
+    if (!d1) sd::fail(SD_ARGUMENT_ERROR, "null gemm descriptor");
+    const bool onchip = (flags & SD_GEMM_ONCHIP_RESIDUAL) != 0;
+    sd::GemmArgs g = args_from(d1);
+    g.onchip = onchip;
+    if (onchip) g.As = g.Bs = nullptr;
+    if (d2) {
+      if (d1->m != d2->m || d1->n != d2->n || d1->k != d2->k || d1->a_mn != d2->a_mn || d1->b_mn != d2->b_mn ||
+          (!onchip && ((d1->a_small == nullptr) != (d2->a_small == nullptr) ||
+                       (d1->b_small == nullptr) != (d2->b_small == nullptr))))
+        sd::fail(SD_ARGUMENT_ERROR, "dual gemm: both products need the same shape, majors and precision");
+      g.A2 = d2->a, g.lda2 = d2->lda;
+      g.B2 = d2->b, g.ldb2 = d2->ldb;
+      if (!onchip) g.A2s = d2->a_small, g.B2s = d2->b_small;
+      g.sa1_2 = d2->sa1, g.sa2_2 = d2->sa2, g.sb1_2 = d2->sb1, g.sb2_2 = d2->sb2;
+    }
+    sd::gemm(g, (cudaStream_t)s);
+  });
+}
+
 // Dual-source product C = alpha (op(A1) op(B1) + op(A2) op(B2)) + beta C in
 // one launch (one TMEM accumulation); d2 supplies the second operand pair.
 sd_status sd_gemm_tf32_dual(const sd_gemm_desc* d1, const sd_gemm_desc* d2, sd_stream s) {
-  return sd::guard([&] {
-    if (!d1 || !d2) sd::fail(SD_ARGUMENT_ERROR, "null gemm descriptor");
-    if (d1->m != d2->m || d1->n != d2->n || d1->k != d2->k || d1->a_mn != d2->a_mn || d1->b_mn != d2->b_mn ||
-        (d1->a_small == nullptr) != (d2->a_small == nullptr) || (d1->b_small == nullptr) != (d2->b_small == nullptr))
-      sd::fail(SD_ARGUMENT_ERROR, "dual gemm: both products need the same shape, majors and precision");
-    sd::GemmArgs g = args_from(d1);
-    g.A2 = d2->a, g.A2s = d2->a_small, g.lda2 = d2->lda;
-    g.B2 = d2->b, g.B2s = d2->b_small, g.ldb2 = d2->ldb;
-    g.sa1_2 = d2->sa1, g.sa2_2 = d2->sa2, g.sb1_2 = d2->sb1, g.sb2_2 = d2->sb2;
-    sd::gemm(g, (cudaStream_t)s);
-  });
+  if (!d2) {
+    sd::set_last_error("null gemm descriptor");
+    return SD_ARGUMENT_ERROR;
+  }
+  return sd_gemm_tf32_ex(d1, d2, 0, s);
 }
 
 // GEMM profiling window: begin() clears; end() synchronises and returns the

@@ -6,7 +6,8 @@ namespace sd {
 struct GemmArgs {
   int M = 0, N = 0, K = 0;
   const float* A = nullptr;   // raw fp32 operand
-  const float* As = nullptr;  // residual (3xTF32); nullptr -> 1xTF32
+  const float* As = nullptr;  // residual (3xTF32); nullptr -> 1xTF32 (unless onchip)
+  bool onchip = false;        // 3xTF32 with on-chip residuals allowed (required if As/Bs are null)
   long long lda = 0;
   bool a_mn = false;          // false: A row-major M x K; true: row-major K x M
   const float* B = nullptr;

@@ -17,7 +17,8 @@ namespace gk {
 // BK = 16 fp32 (64 B) per stage keeps a 6-deep ring of 4 operand tiles in
 // 192 KB of shared memory: enough bytes in flight to cover TMA latency.
 constexpr int BM = 128, BK = 16;
-constexpr int NUM_THREADS = 320;  // producer, MMA, 8 epilogue warps
+constexpr int NUM_THREADS = 384;  // producer, MMA, 2 residual warps, 8 epilogue warps
+constexpr int kConvWarps = 2;     // warps 2-3: on-chip tf32 residuals of the staged operands
 constexpr int kNumSMs = 148;
 
 // Tile-width dependent constants: BN = 128 for general products, BN = 64 for
@@ -128,7 +129,29 @@ struct EpiParams {
   int causal;          // 0 none, 1 lower output, 2 lower-triangular A, 3 upper-triangular A
   int n_tiles_n, n_tiles_m, n_tiles;  // tile grid (n fastest), n_tiles over all (split, z)
   int nsrc;                           // 1, or 2 for a dual-source product
+  int res;                            // 3xTF32 residuals computed on chip from the staged raw tiles
 };
+
+// x - trunc_tf32(x) over a staged operand tile (any smem layout: the residual
+// is elementwise), written to the tile's residual slot; threads t of nt.
+__device__ __forceinline__ void stage_residual(const unsigned char* src, unsigned char* dst, int bytes, int t, int nt) {
+  const float4* s4 = reinterpret_cast<const float4*>(src);
+  float4* d4 = reinterpret_cast<float4*>(dst);
+#pragma unroll 4
+  for (int i = t; i < bytes / 16; i += nt) {
+    const float4 v = s4[i];
+    float4 r;
+    r.x = v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+    r.y = v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+    r.z = v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+    r.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+    d4[i] = r;
+  }
+}
+// generic-proxy smem writes -> visible to the tensor core (async proxy)
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
 
 // Descriptor of k-step `ks` (8 tf32 = 32 B of K) of an operand tile.
 // K-major: 128 rows x 64 B, SWIZZLE_64B in 8-row (512 B) atoms: advance 32 B

@@ -8,9 +8,10 @@
 // 128 x 256 tile: the 3xTF32 products (raw + residual operands, 2x the bytes
 // of a plain GEMM) are otherwise bound by L2 -> SM bandwidth.
 //
-// Roles per CTA: warp 0 TMA producer (both CTAs; bytes land on the leader's
-// full barrier), warp 1 TMEM allocator + (leader only) MMA issuer, warps
-// 2..17 epilogue (16 warps: lane quadrant warp % 4, 64 columns each).
+// Roles per CTA: warp 0 TMA producer (own stage, own full barrier), warp 1
+// TMEM allocator + (leader only) MMA issuer, warps 2-3 residual warps (write
+// the tf32 residual tiles on chip, then arrive on the leader's conv barrier),
+// warps 4..19 epilogue (16 warps: lane quadrant warp % 4, 64 columns each).
 // Same 3xTF32 scheme, chunked round-to-nearest drain (KC), dual-source and
 // split-K support as the single-CTA kernel in sd_gemm.cu.
 #include <algorithm>
@@ -25,7 +26,7 @@ namespace {
 constexpr int kPairN = 256;                           // pair tile N (each CTA stages 128 columns of B)
 constexpr int kPairM = 256;                           // pair tile M (each CTA stages 128 rows of A)
 constexpr int kEpiWarps = 16;
-constexpr int kPairThreads = 64 + 32 * kEpiWarps;     // producer, MMA, epilogue
+constexpr int kPairThreads = 32 * (2 + kConvWarps + kEpiWarps);  // producer, MMA, residual, epilogue
 constexpr int kHalfB = kPairN / 2;
 constexpr int PA_BYTES = BM * BK * 4;                 // 8 KB
 constexpr int PB_BYTES = kHalfB * BK * 4;             // 8 KB
@@ -112,7 +113,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
   uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;  // [2]
+  uint64_t* conv = empty + STAGES;   // [STAGES] (leader) both CTAs' stage s landed + residuals written
+  uint64_t* tfull = conv + STAGES;   // [2]
   uint64_t* tempty = tfull + 2;      // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
@@ -124,6 +126,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
+      mbar_init(&conv[s], 2);  // one residual warp of each CTA per stage
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
@@ -155,9 +158,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
           const uint32_t ph = (g / STAGES) & 1;
           mbar_wait(&empty[s], ph ^ 1);
           unsigned char* st = smem + s * STAGE_BYTES;
-          // the leader's barrier counts the bytes of both CTAs
-          if (rank == 0) mbar_expect_tx(&full[s], 2 * STAGE_BYTES);
-          const uint32_t bar = full_leader + 8u * s;
+          // residuals from memory: both CTAs' bytes land on the leader's full
+          // barrier. On chip: each CTA's raw bytes land on its own barrier and
+          // its residual warp releases the stage to the leader (conv[s]).
+          uint32_t bar;
+          if (ep.res) {
+            mbar_expect_tx(&full[s], PA_BYTES + PB_BYTES);
+            bar = smem_u32(&full[s]);
+          } else {
+            if (rank == 0) mbar_expect_tx(&full[s], 2 * STAGE_BYTES);
+            bar = full_leader + 8u * s;
+          }
           const bool src2 = kk >= ti.num_kb;
           const int kb = src2 ? kk - ti.num_kb : kk;
           const CUtensorMap* pA = src2 ? &mA2 : &mA;
@@ -169,26 +180,48 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
 #pragma unroll
             for (int c = 0; c < BM / 32; ++c) {
               tma_load_4d_pair(pA, bar, st + c * 2048, m_own + 32 * c, k0, z1, z2);
-              if (THREE) tma_load_4d_pair(pAs, bar, st + PA_BYTES + c * 2048, m_own + 32 * c, k0, z1, z2);
+              if (THREE && !ep.res) tma_load_4d_pair(pAs, bar, st + PA_BYTES + c * 2048, m_own + 32 * c, k0, z1, z2);
             }
           } else {
             tma_load_4d_pair(pA, bar, st, k0, m_own, z1, z2);
-            if (THREE) tma_load_4d_pair(pAs, bar, st + PA_BYTES, k0, m_own, z1, z2);
+            if (THREE && !ep.res) tma_load_4d_pair(pAs, bar, st + PA_BYTES, k0, m_own, z1, z2);
           }
           unsigned char* sb = st + (THREE ? 2 : 1) * PA_BYTES;
           if (B_MN) {
 #pragma unroll
             for (int c = 0; c < kHalfB / 32; ++c) {
               tma_load_4d_pair(pB, bar, sb + c * 2048, n_own + 32 * c, k0, z1, z2);
-              if (THREE) tma_load_4d_pair(pBs, bar, sb + PB_BYTES + c * 2048, n_own + 32 * c, k0, z1, z2);
+              if (THREE && !ep.res) tma_load_4d_pair(pBs, bar, sb + PB_BYTES + c * 2048, n_own + 32 * c, k0, z1, z2);
             }
           } else {
             tma_load_4d_pair(pB, bar, sb, k0, n_own, z1, z2);
-            if (THREE) tma_load_4d_pair(pBs, bar, sb + PB_BYTES, k0, n_own, z1, z2);
+            if (THREE && !ep.res) tma_load_4d_pair(pBs, bar, sb + PB_BYTES, k0, n_own, z1, z2);
           }
         }
       }
     }
+  } else if (warp >= 2 && warp < 2 + kConvWarps) {
+    // residual warps (both CTAs): stage landed -> residual tiles -> tell the leader
+    // (warp w takes the stages with g % kConvWarps == w - 2: two stages in flight)
+    const int cw = warp - 2;
+    const uint32_t conv_leader = leader_addr(conv);
+    uint32_t g = 0;
+    if (THREE && ep.res)
+      for (int t = cid; t < ep.n_tiles; t += ncl) {
+        const TileInfo ti = pair_tile(ep, t, K);
+        if (ti.skip) continue;
+        for (int kk = 0; kk < ep.nsrc * ti.num_kb; ++kk, ++g) {
+          if (int(g % kConvWarps) != cw) continue;
+          const int s = g % STAGES;
+          mbar_wait(&full[s], (g / STAGES) & 1);
+          unsigned char* st = smem + s * STAGE_BYTES;
+          stage_residual(st, st + PA_BYTES, PA_BYTES, lane, 32);
+          stage_residual(st + 2 * PA_BYTES, st + 2 * PA_BYTES + PB_BYTES, PB_BYTES, lane, 32);
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_remote(conv_leader + 8u * s);
+        }
+      }
   } else if (warp == 1) {
     if (rank == 0) {
       constexpr uint32_t idesc = make_idesc(A_MN, B_MN, kPairN, kPairM);
@@ -204,7 +237,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
           const bool last = (kb % KC) == KC - 1 || kb == nkb - 1;
           const uint32_t buf = chunk & 1;
           if (first && chunk >= 2) mbar_wait(&tempty[buf], ((chunk >> 1) - 1) & 1);
-          mbar_wait(&full[s], ph);
+          mbar_wait(ep.res ? &conv[s] : &full[s], ph);  // both CTAs' stage s (and residuals) ready
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           if (lane == 0) {
             const uint32_t d = tmem + buf * kPairN;
@@ -234,7 +267,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     // epilogue: warp w drains TMEM lanes 32 (w % 4) .. +31 and the column
     // group (w - 2) / 4 (EC = 64 columns) of this CTA's 128 accumulator rows
     const int sub = warp & 3;
-    const int cb = ((warp - 2) >> 2) * EC;
+    const int cb = ((warp - 2 - kConvWarps) >> 2) * EC;
     const uint32_t tempty_leader = leader_addr(tempty);
     uint32_t chunk = 0;
     for (int t = cid; t < ep.n_tiles; t += ncl) {
@@ -297,7 +330,7 @@ void launch_pair_t(const GemmArgs& g, cudaStream_t s) {
   const int zc = g.Z1 * g.Z2;
   const int tn = (g.N + kPairN - 1) / kPairN, tm = (g.M + kPairM - 1) / kPairM;
   const int tiles = tn * tm * zc;
-  const size_t smem = 1024 + size_t(kPairStages) * (THREE ? 2 : 1) * (PA_BYTES + PB_BYTES) + 256;
+  const size_t smem = 1024 + size_t(kPairStages) * (THREE ? 2 : 1) * (PA_BYTES + PB_BYTES) + 512;
   auto kern = k_gemm_pair<A_MN, B_MN, THREE>;
   static int clusters = 0;
   if (!clusters) {
@@ -313,7 +346,7 @@ void launch_pair_t(const GemmArgs& g, cudaStream_t s) {
   float* ws = nullptr;
   if (splits > 1) ws = splitk_workspace(size_t(splits) * zc * size_t(g.M) * g.N);
   EpiParams ep{g.C, g.ldc, g.sc1, g.sc2, g.M, g.N, g.Z1, g.alpha, g.beta, g.bias, g.Cs, g.dbg, zc, kb_per, ws,
-               0, tn, tm, tiles * splits, dual ? 2 : 1};
+               0, tn, tm, tiles * splits, dual ? 2 : 1, g.onchip ? 1 : 0};
   const int grid = 2 * std::min(ep.n_tiles, clusters);
   if (prof_on())
     prof_tag(std::to_string(g.M) + "," + std::to_string(g.N) + "," + std::to_string(g.K) + "," + std::to_string(zc) +
@@ -330,7 +363,7 @@ void launch_pair_t(const GemmArgs& g, cudaStream_t s) {
 }  // namespace
 
 void gemm_pair(const GemmArgs& g, cudaStream_t s) {
-  const bool three = g.As != nullptr && g.Bs != nullptr;
+  const bool three = (g.As != nullptr && g.Bs != nullptr) || g.onchip;
 #define SD_PAIR_CASE(AM, BMJ, TH) \
   if (g.a_mn == AM && g.b_mn == BMJ && three == TH) return launch_pair_t<AM, BMJ, TH>(g, s);
   SD_PAIR_CASE(false, false, true)

@@ -17,6 +17,8 @@
 // data-sharded sum of per-rank Hv equals the global mean, Alg. 1 line 14-17).
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include <algorithm>
 #include <cmath>
 #include <memory>
@@ -177,6 +179,7 @@ struct sd_gpt_s {
     g.C = C, g.ldc = ldc, g.alpha = alpha, g.beta = beta, g.bias = bias, g.Cs = Cs;
     g.Z1 = Z1, g.Z2 = Z2, g.sa1 = A.s1, g.sa2 = A.s2, g.sb1 = Bo.s1, g.sb2 = Bo.s2, g.sc1 = c1, g.sc2 = c2;
     g.causal = cmode;
+    onchip_residuals(g);
     sd::gemm(g, st);
   }
   // dual source: C = alpha (op(A) op(B) + op(A2) op(B2)) + beta C (+bias), one
@@ -194,9 +197,21 @@ struct sd_gpt_s {
     g.C = C, g.ldc = ldc, g.alpha = alpha, g.beta = beta, g.bias = bias, g.Cs = Cs;
     g.Z1 = Z1, g.Z2 = Z2, g.sa1 = A.s1, g.sa2 = A.s2, g.sb1 = Bo.s1, g.sb2 = Bo.s2, g.sc1 = c1, g.sc2 = c2;
     g.causal = cmode;
+    onchip_residuals(g);
     sd::gemm(g, st);
   }
   int cmode = 0;  // causal tile/K skipping for the per-head S x S products (sd_gemm.cu)
+  // SD_GEMM_ONCHIP=1 lets the GEMM compute the operand residuals in shared
+  // memory where it judges it faster (sd_gemm.cu gemm()); measured neutral on
+  // the GPT-2 HVP (137 vs 138 ms), so the residual arrays stay the default.
+  static void onchip_residuals(sd::GemmArgs& g) {
+    static const bool onchip = [] {
+      const char* e = std::getenv("SD_GEMM_ONCHIP");
+      return e && e[0] == '1';
+    }();
+    if (!onchip) return;
+    g.onchip = true;
+  }
 
   const float* th(int i) const { return theta + slots[i].off; }
   const float* ths(int i) const { return theta_s + slots[i].off; }

@@ -262,6 +262,11 @@ __global__ void k_gelu_bwd(const float* __restrict__ f, const float* __restrict_
 // --------------------------------------------------------- attention softmax
 // Row (z, i) of the per-head score matrix (already scaled), causal: columns
 // j <= i. P = softmax, dP = P (dS - sum_j P dS); masked entries -> 0.
+// Causal score products are tiled in 128-row blocks (sd_gemm.cu BM, causal
+// modes 1-3): entries right of the diagonal but inside the diagonal tile are
+// read (as zeros), entries beyond the tile never are -- so they are not written.
+constexpr int kCausalTile = 128;
+
 __global__ void k_attn_softmax_fwd(float* __restrict__ Sm, float* __restrict__ dS, float* __restrict__ Ps,
                                    float* __restrict__ dPs, int S, long long rows) {
   const long long row = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -284,7 +289,9 @@ __global__ void k_attn_softmax_fwd(float* __restrict__ Sm, float* __restrict__ d
   const float inv = 1.f / z, mean_d = zd * inv;
   float* ps = Ps + row * S;
   float* dps = dPs + row * S;
-  for (int j = lane; j < S; j += 32) {
+  // the causal GEMMs read P only up to the end of the row's 128-row tile
+  const int jend = min(S, (i / kCausalTile + 1) * kCausalTile);
+  for (int j = lane; j < jend; j += 32) {
     float p = 0.f, dp = 0.f;
     if (j <= i) {
       p = __expf(s[j] - m) * inv;
@@ -314,7 +321,8 @@ __global__ void k_attn_softmax_bwd(const float* __restrict__ P, const float* __r
   }
   c = warp_sum(c);
   dc = warp_sum(dc);
-  for (int j = lane; j < S; j += 32) {
+  const int jend = min(S, (i / kCausalTile + 1) * kCausalTile);
+  for (int j = lane; j < jend; j += 32) {
     float a = 0.f, b = 0.f;
     if (j <= i) {
       const float gp = gP[o + j];
@@ -335,20 +343,46 @@ __global__ void __launch_bounds__(256) k_ce(float* __restrict__ z, float* __rest
                                             float* __restrict__ dzs, const int* __restrict__ tgt, int V, long long ld,
                                             float scale, double* __restrict__ loss_rows) {
   __shared__ float red[8];
+  __shared__ float rm[8], rs[8], rsd[8];
   const long long t = blockIdx.x;
   float* zr = z + t * ld;
   float* dzr = dz + t * ld;
-  float m = -INFINITY;
-  for (int j = threadIdx.x; j < V; j += 256) m = fmaxf(m, zr[j]);
-  m = block_max<8>(m, red);
-  float s = 0.f, sd = 0.f;
+  // one streaming pass for max, sum e^(z-m) and sum e^(z-m) dz (online
+  // rescaling), then the write pass: the row is read twice, not three times
+  float m = -INFINITY, s = 0.f, sd = 0.f;
   for (int j = threadIdx.x; j < V; j += 256) {
-    const float e = __expf(zr[j] - m);
+    const float zj = zr[j], dj = dzr[j];
+    if (zj > m) {
+      const float c = __expf(m - zj);
+      s *= c;
+      sd *= c;
+      m = zj;
+    }
+    const float e = __expf(zj - m);
     s += e;
-    sd += e * dzr[j];
+    sd += e * dj;
   }
-  s = block_sum<8>(s, red);
-  sd = block_sum<8>(sd, red);
+  // warp then block combine of (m, s, sd)
+  for (int o = 16; o > 0; o >>= 1) {
+    const float m2 = __shfl_xor_sync(0xffffffffu, m, o), s2 = __shfl_xor_sync(0xffffffffu, s, o),
+                sd2 = __shfl_xor_sync(0xffffffffu, sd, o);
+    const float mn = fmaxf(m, m2);
+    const float c1 = m == -INFINITY ? 0.f : __expf(m - mn), c2 = m2 == -INFINITY ? 0.f : __expf(m2 - mn);
+    s = s * c1 + s2 * c2;
+    sd = sd * c1 + sd2 * c2;
+    m = mn;
+  }
+  if ((threadIdx.x & 31) == 0) rm[threadIdx.x >> 5] = m, rs[threadIdx.x >> 5] = s, rsd[threadIdx.x >> 5] = sd;
+  __syncthreads();
+  m = rm[0];
+  for (int w = 1; w < 8; ++w) m = fmaxf(m, rm[w]);
+  s = 0.f, sd = 0.f;
+  for (int w = 0; w < 8; ++w) {
+    const float c = rm[w] == -INFINITY ? 0.f : __expf(rm[w] - m);
+    s += rs[w] * c;
+    sd += rsd[w] * c;
+  }
+  (void)red;
   const float inv = 1.f / s, md = sd * inv;
   const int y = tgt[t];
   if (threadIdx.x == 0) loss_rows[t] = double(logf(s) + m - zr[y]);

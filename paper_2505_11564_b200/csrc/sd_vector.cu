@@ -427,8 +427,13 @@ static void launch_axpy_dot(const void* x, void* y, const void* z, const double*
   using D1 = std::integral_constant<int, 1>;
   using D2 = std::integral_constant<int, 2>;
   if (upd) {
-    if (dot == 0) run(TT{}, D0{});
-    else if (dot == 1) run(TT{}, D1{});
+    if (dot == 0) {
+      // update only: element-parallel (no block folds to keep in order)
+      if (local_end) {
+        k_axpy<T><<<grid_for(local_end, 256), 256, 0, s>>>((const T*)x, (T*)y, local_end, coef, -1.0);
+        SD_LAUNCHED("k_axpy");
+      }
+    } else if (dot == 1) run(TT{}, D1{});
     else run(TT{}, D2{});
   } else {
     if (dot == 0) fail(SD_ARGUMENT_ERROR, "axpy_dot with neither update nor dot");

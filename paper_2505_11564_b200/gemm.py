@@ -29,6 +29,9 @@ def _cfg():
         L.sd_gemm_tf32.restype = C.c_int
         L.sd_gemm_tf32_dual.argtypes = [C.POINTER(GemmDesc), C.POINTER(GemmDesc), C.c_void_p]
         L.sd_gemm_tf32_dual.restype = C.c_int
+        if hasattr(L, "sd_gemm_tf32_ex"):
+            L.sd_gemm_tf32_ex.argtypes = [C.POINTER(GemmDesc), C.POINTER(GemmDesc), C.c_int, C.c_void_p]
+            L.sd_gemm_tf32_ex.restype = C.c_int
         L.sd_split_tf32.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_int, C.c_void_p]
         L.sd_split_tf32.restype = C.c_int
         _configured = True
@@ -46,22 +49,31 @@ def split(x: torch.Tensor, mode: int = 0) -> torch.Tensor:
     return s
 
 
+ONCHIP_RESIDUAL = 1
+
+
 def gemm(m, n, k, a, lda, a_mn, b, ldb, b_mn, c, ldc, alpha=1.0, beta=0.0, a_small=None, b_small=None,
-         z1=1, z2=1, sa=(0, 0), sb=(0, 0), sc=(0, 0)):
+         z1=1, z2=1, sa=(0, 0), sb=(0, 0), sc=(0, 0), onchip=False):
+    """onchip=True: 3xTF32 with the operand residuals computed in shared memory."""
     d = GemmDesc(m, n, k, _ptr(a), _ptr(a_small), lda, int(a_mn), _ptr(b), _ptr(b_small), ldb, int(b_mn), _ptr(c),
                  ldc, alpha, beta, z1, z2, sa[0], sa[1], sb[0], sb[1], sc[0], sc[1])
-    check(_cfg().sd_gemm_tf32(C.byref(d), torch.cuda.current_stream().cuda_stream))
+    stream = torch.cuda.current_stream().cuda_stream
+    if onchip:
+        check(_cfg().sd_gemm_tf32_ex(C.byref(d), None, ONCHIP_RESIDUAL, stream))
+    else:
+        check(_cfg().sd_gemm_tf32(C.byref(d), stream))
 
 
 def gemm_dual(m, n, k, a, lda, a_mn, b, ldb, b_mn, a2, lda2, b2, ldb2, c, ldc, alpha=1.0, beta=0.0,
               a_small=None, b_small=None, a2_small=None, b2_small=None, z1=1, z2=1, sa=(0, 0), sb=(0, 0),
-              sa2=(0, 0), sb2=(0, 0), sc=(0, 0)):
+              sa2=(0, 0), sb2=(0, 0), sc=(0, 0), onchip=False):
     """C = alpha (op(A) op(B) + op(A2) op(B2)) + beta C in one launch."""
     d1 = GemmDesc(m, n, k, _ptr(a), _ptr(a_small), lda, int(a_mn), _ptr(b), _ptr(b_small), ldb, int(b_mn), _ptr(c),
                   ldc, alpha, beta, z1, z2, sa[0], sa[1], sb[0], sb[1], sc[0], sc[1])
     d2 = GemmDesc(m, n, k, _ptr(a2), _ptr(a2_small), lda2, int(a_mn), _ptr(b2), _ptr(b2_small), ldb2, int(b_mn),
                   _ptr(c), ldc, alpha, beta, z1, z2, sa2[0], sa2[1], sb2[0], sb2[1], sc[0], sc[1])
-    check(_cfg().sd_gemm_tf32_dual(C.byref(d1), C.byref(d2), torch.cuda.current_stream().cuda_stream))
+    check(_cfg().sd_gemm_tf32_ex(C.byref(d1), C.byref(d2), ONCHIP_RESIDUAL if onchip else 0,
+                                 torch.cuda.current_stream().cuda_stream))
 
 
 def matmul(A: torch.Tensor, B: torch.Tensor, three: bool = True, a_t: bool = False, b_t: bool = False,

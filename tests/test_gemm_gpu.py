@@ -110,3 +110,29 @@ def test_gemm_dual_source(G, a_t, b_t, shape):
                 alpha=alpha, beta=beta, a_small=G.split(A1), b_small=G.split(B1), a2_small=G.split(A2),
                 b2_small=G.split(B2))
     assert rel(C, ref) < 2e-6
+
+
+@pytest.mark.parametrize("a_t", [False, True])
+@pytest.mark.parametrize("b_t", [False, True])
+@pytest.mark.parametrize("shape", [(256, 384, 768), (200, 300, 100), (1024, 64, 1024), (768, 768, 8192), (8192, 256, 64)])
+def test_gemm_onchip_residual_bitwise(G, a_t, b_t, shape):
+    # residual tiles computed in shared memory == residual arrays from sd_split_tf32(mode 0), bit for bit
+    M, N, K = shape
+    g = torch.Generator(device="cuda").manual_seed(M * 3 + N + 7 * K)
+    A = torch.randn(*((K, M) if a_t else (M, K)), device="cuda", generator=g)
+    B = torch.randn(*((N, K) if b_t else (K, N)), device="cuda", generator=g)
+    A2 = torch.randn_like(A)
+    B2 = torch.randn_like(B)
+    args = (M, N, K, A, A.shape[1], a_t, B, B.shape[1], not b_t)
+    C0 = torch.empty(M, N, device="cuda")
+    C1 = torch.empty(M, N, device="cuda")
+    G.gemm(*args, C0, N, a_small=G.split(A), b_small=G.split(B))
+    G.gemm(*args, C1, N, onchip=True)
+    assert torch.equal(C0, C1)
+    D0 = torch.zeros(M, N, device="cuda")
+    D1 = torch.zeros(M, N, device="cuda")
+    G.gemm_dual(M, N, K, A, A.shape[1], a_t, B, B.shape[1], not b_t, A2, A2.shape[1], B2, B2.shape[1], D0, N,
+                alpha=0.5, a_small=G.split(A), b_small=G.split(B), a2_small=G.split(A2), b2_small=G.split(B2))
+    G.gemm_dual(M, N, K, A, A.shape[1], a_t, B, B.shape[1], not b_t, A2, A2.shape[1], B2, B2.shape[1], D1, N,
+                alpha=0.5, onchip=True)
+    assert torch.equal(D0, D1)
