@@ -252,6 +252,11 @@ sd_status sd_operator_diag(uint64_t dim, const void* d_dev, int prec, sd_operato
 /* Lanczos operator y = H x of a GPT engine; with comm, per-rank Hv over
  * data-sharded batches are summed with an NCCL all-reduce (Alg. 1). */
 sd_status sd_operator_gpt(sd_gpt g, sd_comm comm, sd_operator* out);
+/* Parameter-sharded form: the Lanczos vectors are split over
+ * the comm's ranks by (begins, ends); apply() all-gathers x, runs this
+ * rank's batch HVP on the full vector and reduce-scatters Hv into y (f32). */
+sd_status sd_operator_gpt_sharded(sd_gpt g, sd_comm comm, const uint64_t* begins, const uint64_t* ends,
+                                  sd_operator* out);
 /* Lanczos operator y = H x of an MLP engine (all-reduced over comm if given) */
 sd_status sd_operator_mlp(sd_mlp m, sd_comm comm, sd_operator* out);
 sd_status sd_operator_apply(sd_operator op, const void* x, void* y, int prec, sd_stream s);

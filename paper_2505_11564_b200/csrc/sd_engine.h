@@ -21,6 +21,7 @@ void dense_apply(const double* a, uint64_t n, const void* xf, void* y, uint64_t 
 void diag_apply(const void* d, const void* x, void* y, uint64_t n, int prec, cudaStream_t s);
 void comm_allgather(sd_comm c, const void* send, void* recv, uint64_t bytes, cudaStream_t s);
 void comm_allreduce_f32(sd_comm c, float* buf, uint64_t n, cudaStream_t s);
+void comm_reducescatter_f32(sd_comm c, const float* send, float* recv, uint64_t n, cudaStream_t s);
 int comm_rank(sd_comm c);
 int comm_size(sd_comm c);
 void operator_apply(sd_operator op, const void* x, void* y, int prec, cudaStream_t s, uint64_t row_begin,

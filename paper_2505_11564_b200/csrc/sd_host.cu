@@ -160,6 +160,8 @@ struct NcclApi {
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                             cudaStream_t) = nullptr;
   ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*ReduceScatter)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                                cudaStream_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
 };
 static NcclApi& nccl() {
@@ -173,6 +175,7 @@ static NcclApi& nccl() {
     a.CommDestroy = (decltype(a.CommDestroy))dlsym(h, "ncclCommDestroy");
     a.AllReduce = (decltype(a.AllReduce))dlsym(h, "ncclAllReduce");
     a.AllGather = (decltype(a.AllGather))dlsym(h, "ncclAllGather");
+    a.ReduceScatter = (decltype(a.ReduceScatter))dlsym(h, "ncclReduceScatter");
     a.GetErrorString = (decltype(a.GetErrorString))dlsym(h, "ncclGetErrorString");
     return a;
   }();
@@ -192,8 +195,10 @@ struct sd_comm_s {
 
 namespace sd {
 
+// No communicator: single rank, the collectives are identities. A real
+// communicator (even of one rank) always goes through NCCL.
 void comm_allgather(sd_comm c, const void* send, void* recv, uint64_t bytes, cudaStream_t s) {
-  if (!c || c->nranks == 1) {
+  if (!c) {
     if (recv != send) SD_CUDA(cudaMemcpyAsync(recv, send, bytes, cudaMemcpyDeviceToDevice, s));
     return;
   }
@@ -201,8 +206,18 @@ void comm_allgather(sd_comm c, const void* send, void* recv, uint64_t bytes, cud
 }
 
 void comm_allreduce_f32(sd_comm c, float* buf, uint64_t n, cudaStream_t s) {
-  if (!c || c->nranks == 1) return;
+  if (!c) return;
   nccl_check(nccl().AllReduce(buf, buf, n, ncclFloat32, ncclSum, c->comm, s), "ncclAllReduce");
+}
+
+// sum over ranks of send[r * n .. r * n + n) lands in rank r's recv[0 .. n)
+void comm_reducescatter_f32(sd_comm c, const float* send, float* recv, uint64_t n, cudaStream_t s) {
+  if (!c) {
+    if (recv != send) SD_CUDA(cudaMemcpyAsync(recv, send, n * sizeof(float), cudaMemcpyDeviceToDevice, s));
+    return;
+  }
+  if (!nccl().ReduceScatter) fail(SD_NCCL_ERROR, "ncclReduceScatter unavailable");
+  nccl_check(nccl().ReduceScatter(send, recv, n, ncclFloat32, ncclSum, c->comm, s), "ncclReduceScatter");
 }
 
 int comm_rank(sd_comm c) { return c ? c->rank : 0; }
@@ -238,7 +253,7 @@ void operator_apply(sd_operator op, const void* x, void* y, int prec, cudaStream
     diag_apply(op->diag, x, y, row_end - row_begin, prec, s);
   } else {
     const sd_status st = op->fn(op->ctx, x, y, (sd_stream)s);
-    if (st != SD_OK) fail(st, "operator apply failed");
+    if (st != SD_OK) fail(st, std::string("operator apply failed: ") + sd_last_error());
   }
 }
 
@@ -401,11 +416,10 @@ sd_status sd_comm_nccl_create(const unsigned char id[128], int nranks, int rank,
     auto c = std::make_unique<sd_comm_s>();
     c->nranks = nranks;
     c->rank = rank;
-    if (nranks > 1) {
-      ncclUniqueId uid;
-      std::memcpy(&uid, id, sizeof(uid));
-      nccl_check(nccl().CommInitRank(&c->comm, nranks, uid, rank), "ncclCommInitRank");
-    }
+    if (nranks < 1 || rank < 0 || rank >= nranks) fail(SD_ARGUMENT_ERROR, "bad rank/size");
+    ncclUniqueId uid;
+    std::memcpy(&uid, id, sizeof(uid));
+    nccl_check(nccl().CommInitRank(&c->comm, nranks, uid, rank), "ncclCommInitRank");
     *out = c.release();
   });
 }

@@ -45,6 +45,8 @@ def _L():
             "sd_gpt_last_loss": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.c_void_p]),
             "sd_gpt_destroy": (C.c_int, [C.c_void_p]),
             "sd_operator_gpt": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_void_p)]),
+            "sd_operator_gpt_sharded": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_uint64),
+                                                  C.POINTER(C.c_uint64), C.POINTER(C.c_void_p)]),
         }
         for n, (r, a) in sig.items():
             f = getattr(L, n)
@@ -151,9 +153,18 @@ class GptHvp:
     def tokens_numpy(self):
         return self._tok.astype(np.uint32), self._tgt.astype(np.uint32)
 
-    def operator(self, comm=None) -> OperatorHandle:
+    def operator(self, comm=None, layout=None) -> OperatorHandle:
+        """y = H x over this rank's batch, summed over `comm`'s ranks. With a
+        `layout` the Lanczos vectors are parameter-sharded: x/y are this rank's
+        shard, Hv is reduce-scattered (sd_operator_gpt_sharded)."""
         h = C.c_void_p()
-        check(_L().sd_operator_gpt(self.h, comm.handle if comm is not None else None, C.byref(h)))
+        ch = comm.handle if comm is not None else None
+        if layout is not None:
+            b = (C.c_uint64 * len(layout.begins))(*layout.begins)
+            e = (C.c_uint64 * len(layout.ends))(*layout.ends)
+            check(_L().sd_operator_gpt_sharded(self.h, ch, b, e, C.byref(h)))
+        else:
+            check(_L().sd_operator_gpt(self.h, ch, C.byref(h)))
         return OperatorHandle(self.P, f"gpt_hvp(L={self.cfg['n_layer']},d={self.cfg['d']})", h, keepalive=self)
 
     def close(self):
