@@ -113,3 +113,48 @@ def test_data_sharded_hvp_allreduce_weighting():
     for r in res.values():
         assert isinstance(r, dict), r
         assert r["rel"] < 1e-12
+
+
+def _sharded_apply(rank, world):
+    # the index math of gpt_shard_apply (csrc/sd_gpt.cu) on CPU: all-gather the
+    # x shards into maxlen slots, compact, run this rank's batch HVP on the
+    # full vector, lay Hv out in rank-major maxlen slots, reduce-scatter
+    import sys
+    from pathlib import Path
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+    from oracle.pyoracle import Oracle, RADEMACHER
+    from paper_2505_11564_b200 import core
+    from paper_2505_11564_b200.gpt import synthetic_tokens
+    o = Oracle()
+    B, S = 4, 8
+    th = o.gpt_init(CFG, 0, 0.1, 0.1)
+    P = th.size
+    v = o.draw_probe(P, 5, RADEMACHER)
+    tok, tgt = synthetic_tokens(CFG["vocab"], B, S, 1, 0)
+    lay = core.split_evenly(P, world)
+    b0, e0 = lay.shard_bounds[rank]
+    ml = max(e - b for b, e in lay.shard_bounds)
+    slot = torch.zeros(ml, dtype=torch.float64)
+    slot[:e0 - b0] = torch.tensor(v[b0:e0])
+    slots = [torch.zeros(ml, dtype=torch.float64) for _ in range(world)]
+    dist.all_gather(slots, slot)
+    full = np.concatenate([slots[r].numpy()[:e - b] for r, (b, e) in enumerate(lay.shard_bounds)])
+    bl = B // world
+    sl = slice(rank * bl * S, (rank + 1) * bl * S)
+    hv = o.gpt_hvp(CFG, th, tok[sl].astype(np.uint32), tgt[sl].astype(np.uint32), bl, S, full) * (bl / B)
+    send = torch.zeros(world * ml, dtype=torch.float64)
+    for r, (b, e) in enumerate(lay.shard_bounds):
+        send[r * ml:r * ml + (e - b)] = torch.tensor(hv[b:e])
+    mine = torch.zeros(ml, dtype=torch.float64)
+    dist.reduce_scatter_tensor(mine, send)
+    whole = o.gpt_hvp(CFG, th, tok.astype(np.uint32), tgt.astype(np.uint32), B, S, v)
+    ref = whole[b0:e0]
+    return {"rel": float(np.linalg.norm(mine.numpy()[:e0 - b0] - ref) / np.linalg.norm(ref)),
+            "gathered_exact": bool(np.array_equal(full, v))}
+
+
+def test_parameter_sharded_lanczos_apply():
+    res = run_world(_sharded_apply)
+    for r in res.values():
+        assert isinstance(r, dict), r
+        assert r["gathered_exact"] and r["rel"] < 1e-12
