@@ -137,7 +137,8 @@ struct sd_gpt_s {
       l.r1 = p.take<float>(T_), l.dr1 = p.take<float>(T_);
       l.a = p.take<float>(T_ * 3 * d), l.as = p.take<float>(T_ * 3 * d);
       l.da = p.take<float>(T_ * 3 * d), l.das = p.take<float>(T_ * 3 * d);
-      l.P = p.take<float>(BHSS), l.Ps = p.take<float>(BHSS), l.dP = p.take<float>(BHSS), l.dPs = p.take<float>(BHSS);
+      // P, dP residuals are formed on chip by their (64-wide attention) consumers
+      l.P = p.take<float>(BHSS), l.Ps = nullptr, l.dP = p.take<float>(BHSS), l.dPs = nullptr;
       l.o = td(), l.os = td(), l.dO = td(), l.dOs = td();
       l.xh2 = td(), l.dxh2 = td(), l.h2 = td(), l.h2s = td(), l.dh2 = td(), l.dh2s = td();
       l.r2 = p.take<float>(T_), l.dr2 = p.take<float>(T_);
@@ -153,7 +154,7 @@ struct sd_gpt_s {
     go = td(), gos = td(), gdo = td(), gdos = td();
     ga = p.take<float>(T_ * 3 * d), gas = p.take<float>(T_ * 3 * d);
     gda = p.take<float>(T_ * 3 * d), gdas = p.take<float>(T_ * 3 * d);
-    gP = p.take<float>(BHSS), gPs = p.take<float>(BHSS), gdP = p.take<float>(BHSS), gdPs = p.take<float>(BHSS);
+    gP = p.take<float>(BHSS), gPs = nullptr, gdP = p.take<float>(BHSS), gdPs = nullptr;
     gu = p.take<float>(T_ * ff), gus = p.take<float>(T_ * ff), gdu = p.take<float>(T_ * ff), gdus = p.take<float>(T_ * ff);
     theta_s = p.take<float>(P), v_s = p.take<float>(P);
     loss_rows = p.take<double>(T_);
@@ -205,6 +206,11 @@ struct sd_gpt_s {
   // memory where it judges it faster (sd_gemm.cu gemm()); measured neutral on
   // the GPT-2 HVP (137 vs 138 ms), so the residual arrays stay the default.
   static void onchip_residuals(sd::GemmArgs& g) {
+    // an operand without a residual array (P, dP, gS, gdS) -> on-chip residuals
+    if (!g.As || !g.Bs || (g.A2 && (!g.A2s || !g.B2s))) {
+      g.onchip = true;
+      return;
+    }
     static const bool onchip = [] {
       const char* e = std::getenv("SD_GEMM_ONCHIP");
       return e && e[0] == '1';

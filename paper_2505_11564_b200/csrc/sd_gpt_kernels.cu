@@ -299,8 +299,10 @@ __global__ void k_attn_softmax_fwd(float* __restrict__ Sm, float* __restrict__ d
     }
     s[j] = p;
     ds[j] = dp;
-    ps[j] = tf32_res(p);
-    dps[j] = tf32_res(dp);
+    if (Ps) {  // residual arrays only for consumers without on-chip residuals
+      ps[j] = tf32_res(p);
+      dps[j] = tf32_res(dp);
+    }
   }
 }
 
@@ -331,8 +333,10 @@ __global__ void k_attn_softmax_bwd(const float* __restrict__ P, const float* __r
     }
     gP[o + j] = a;
     gdP[o + j] = b;
-    gPs[o + j] = tf32_res(a);
-    gdPs[o + j] = tf32_res(b);
+    if (gPs) {
+      gPs[o + j] = tf32_res(a);
+      gdPs[o + j] = tf32_res(b);
+    }
   }
 }
 
