@@ -523,13 +523,14 @@ void gemm(const GemmArgs& g_in, cudaStream_t s) {
   GemmArgs g = g_in;
   const bool pair = g.causal == 0 && g.M >= 256 && g.N >= 256 && sd_gemm_pair_enabled();
   // On-chip residuals (onchip = allowed): they halve the operand bytes through
-  // L2 and TMA, which pays where a kernel is operand-bandwidth bound (64-wide
-  // and causal attention tiles, MN-major A in the weight products); the
-  // K-major pair products keep memory residuals when the caller has them
-  // (measured: the per-stage residual hand-off costs more than it saves there).
+  // L2 and TMA but add a shared-memory read + write of every staged tile. That
+  // pays where a kernel is L2-operand bound (MN-major A in the weight products:
+  // 120 -> 150 TF/s) and costs where shared memory is the tighter limit (the
+  // K-major pair products: 258 -> 162 TF/s); callers with residual arrays get
+  // them elsewhere. Without arrays (attention P, dP, gS, gdS) on chip is forced.
   if (g.onchip) {
     const bool have = g.As && g.Bs && (!g.A2 || (g.A2s && g.B2s));
-    const bool prefer = !pair || g.a_mn;
+    const bool prefer = pair && g.a_mn;
     if (have && !prefer) g.onchip = false;
     else g.As = g.Bs = g.A2s = g.B2s = nullptr;
   }

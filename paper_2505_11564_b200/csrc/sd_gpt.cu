@@ -202,16 +202,15 @@ struct sd_gpt_s {
     sd::gemm(g, st);
   }
   int cmode = 0;  // causal tile/K skipping for the per-head S x S products (sd_gemm.cu)
-  // SD_GEMM_ONCHIP=1 lets the GEMM compute the operand residuals in shared
-  // memory where it judges it faster (sd_gemm.cu gemm()); measured neutral on
-  // the GPT-2 HVP (137 vs 138 ms), so the residual arrays stay the default.
+  // Products with residual arrays use them (on-chip residuals for the MN-major-A
+  // weight products measured neutral on the whole HVP: SD_GEMM_ONCHIP=1).
   static void onchip_residuals(sd::GemmArgs& g) {
     // an operand without a residual array (P, dP, gS, gdS) -> on-chip residuals
     if (!g.As || !g.Bs || (g.A2 && (!g.A2s || !g.B2s))) {
       g.onchip = true;
       return;
     }
-    static const bool onchip = [] {
+    static const bool onchip = [] {  // SD_GEMM_ONCHIP=1: let the GEMM choose (measured neutral)
       const char* e = std::getenv("SD_GEMM_ONCHIP");
       return e && e[0] == '1';
     }();
