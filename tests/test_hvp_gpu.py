@@ -107,3 +107,23 @@ def test_hvp_gpt2_small_dims_vs_torch_f64(sd):
     e = float((hv - ref).norm() / ref.norm())
     print(f"GPT-2-small HVP rel-L2 vs torch f64: {e:.3e}")
     assert e < TOL
+
+
+def test_c3_shape_runs_and_is_symmetric():
+    # BASELINE C3 decoder shape (1.3B: 24L, d2048, ff8192, V50257, ctx2048, tied) at
+    # 1 x 2048 tokens on one GPU: finite, symmetric u^T H w == w^T H u, linear
+    from paper_2505_11564_b200 import gpt
+    C3 = dict(n_layer=24, d=2048, n_head=16, ff=8192, vocab=50257, ctx=2048)
+    eng = gpt.GptHvp(C3, 1, 2048)
+    assert eng.P == 1315723264
+    g = torch.Generator(device="cuda").manual_seed(0)
+    u = torch.randn(eng.P, device="cuda", generator=g) * 1e-3
+    w = torch.randn(eng.P, device="cuda", generator=g) * 1e-3
+    hu, hw = eng.hvp(u), eng.hvp(w)
+    assert bool(torch.isfinite(hu).all()) and bool(torch.isfinite(hw).all())
+    a, b = float(torch.dot(hu.double(), w.double())), float(torch.dot(u.double(), hw.double()))
+    assert abs(a - b) <= 1e-4 * max(abs(a), abs(b))
+    hs = eng.hvp((0.5 * u - 2.0 * w).contiguous())
+    lin = 0.5 * hu.double() - 2.0 * hw.double()
+    assert float((hs.double() - lin).norm() / lin.norm()) < 1e-5
+    eng.close()
