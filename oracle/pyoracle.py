@@ -191,7 +191,7 @@ class Oracle:
         self._chk(self.lib.oracle_dense_apply(_ll(x.size), _p(a), _p(x), prec, _p(out)))
         return out
 
-    def lanczos_dense(self, a, k_max, eps=-1.0, reorth=False, seed=42, dist=GAUSSIAN, prec=F64, basis=False):
+    def lanczos_dense(self, a, k_max, eps=-1.0, reorth=False, seed=42, dist=GAUSSIAN, prec=F64, basis=False, window=0):
         a = np.ascontiguousarray(a, np.float64)
         n = a.shape[0]
         al = np.zeros(k_max, np.float64)
@@ -199,7 +199,7 @@ class Oracle:
         sb = np.zeros(k_max, np.float64)
         info = np.zeros(5, np.int64)
         Q = np.zeros((k_max + 1, n), np.float64) if basis else None
-        self._chk(self.lib.oracle_lanczos_dense(_ll(n), _p(a), _ll(k_max), _d(eps), int(reorth), _ull(seed), dist,
+        self._chk(self.lib.oracle_lanczos_dense(_ll(n), _p(a), _ll(k_max), _d(eps), int(reorth), _ll(window), _ull(seed), dist,
                                                 prec, _p(al), _p(be), _p(sb), _p(Q) if basis else None, _pl(info)))
         res = {"alphas": al[:info[0]].copy(), "betas": be[:info[1]].copy(), "step_beta": sb[:info[0]].copy(),
                "breakdown": bool(info[2]), "numerical_failure": bool(info[3])}
@@ -207,12 +207,13 @@ class Oracle:
             res["basis"] = Q[:info[4]].copy()
         return res
 
-    def lanczos_diag(self, d, k_max, eps=-1.0, reorth=False, seed=42, dist=RADEMACHER, prec=F32):
+    def lanczos_diag(self, d, k_max, eps=-1.0, reorth=False, seed=42, dist=RADEMACHER, prec=F32, window=0):
         d = np.ascontiguousarray(d, np.float64)
         al = np.zeros(k_max, np.float64)
         be = np.zeros(k_max, np.float64)
         info = np.zeros(4, np.int64)
-        self._chk(self.lib.oracle_lanczos_diag(_ll(d.size), _p(d), _ll(k_max), _d(eps), int(reorth), _ull(seed), dist,
+        self._chk(self.lib.oracle_lanczos_diag(_ll(d.size), _p(d), _ll(k_max), _d(eps), int(reorth), _ll(window), _ull(seed),
+                                               dist,
                                                prec, _p(al), _p(be), _pl(info)))
         return {"alphas": al[:info[0]].copy(), "betas": be[:info[1]].copy(), "breakdown": bool(info[2])}
 

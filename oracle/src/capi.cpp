@@ -189,7 +189,8 @@ int oracle_dense_apply(long long n, const double* a, const double* x, int prec, 
 // Lanczos over a dense operator. out_alpha/out_beta sized k_max; out_basis
 // (optional) sized (k_max+1)*n. info[0]=#alphas, info[1]=#betas,
 // info[2]=breakdown, info[3]=numerical failure, info[4]=#basis columns.
-int oracle_lanczos_dense(long long n, const double* a, long long k_max, double eps, int reorth, unsigned long long seed,
+int oracle_lanczos_dense(long long n, const double* a, long long k_max, double eps, int reorth, long long window,
+                         unsigned long long seed,
                          int dist, int prec, double* out_alpha, double* out_beta, double* out_step_beta,
                          double* out_basis, long long* info) {
   ORACLE_TRY({
@@ -200,6 +201,7 @@ int oracle_lanczos_dense(long long n, const double* a, long long k_max, double e
     cfg.k_max = size_t(k_max);
     cfg.eps = eps;
     cfg.reorth = Reorth(reorth);
+    cfg.window = size_t(window);
     cfg.probe.seed = seed;
     cfg.probe.dist = ProbeDist(dist);
     cfg.prec = Precision(prec);
@@ -220,13 +222,15 @@ int oracle_lanczos_dense(long long n, const double* a, long long k_max, double e
 }
 
 // Lanczos over the diagonal operator y_i = round(d_i * x_i) (exact product, one rounding).
-int oracle_lanczos_diag(long long n, const double* d, long long k_max, double eps, int reorth, unsigned long long seed,
+int oracle_lanczos_diag(long long n, const double* d, long long k_max, double eps, int reorth, long long window,
+                        unsigned long long seed,
                         int dist, int prec, double* out_alpha, double* out_beta, long long* info) {
   ORACLE_TRY({
     LanczosConfig cfg;
     cfg.k_max = size_t(k_max);
     cfg.eps = eps;
     cfg.reorth = Reorth(reorth);
+    cfg.window = size_t(window);
     cfg.probe.seed = seed;
     cfg.probe.dist = ProbeDist(dist);
     cfg.prec = Precision(prec);

@@ -245,10 +245,19 @@ LanczosResult lanczos_run(size_t dim, const ApplyFn& apply, const LanczosConfig&
   if (cfg.k_max < 1) fail(Err::config, "k_max must be >= 1");
   const double eps = cfg.eps > 0 ? cfg.eps : (cfg.prec == Precision::f64 ? 1e-12 : 1e-7);
   const bool keep = cfg.store_basis || cfg.reorth == Reorth::full;
+  // selective (this project's definition, SURVEY 8(a) row 20 -- the SPEC
+  // leaves it to the builder): two classical Gram-Schmidt passes over the
+  // most recent W columns, kept in a ring (column i in slot i % W) and swept
+  // in slot order 0..min(k+1, W)-1; memory is W vectors instead of k+1.
+  const bool sel = cfg.reorth == Reorth::selective;
+  const size_t W = cfg.window;
+  if (sel && W < 2) fail(Err::config, "selective reorthogonalisation needs a window >= 2");
   LanczosResult res;
   Vec q = draw_probe(dim, cfg.probe, cfg.prec), q_prev;
-  std::vector<Vec> Q;
+  std::vector<Vec> Q, ring(sel ? W : 0);
+  size_t stored = 1;
   Q.push_back(q);
+  if (sel) ring[0] = q;
   for (size_t k = 0; k < cfg.k_max; ++k) {
     Vec r;
     r.prec = cfg.prec;
@@ -268,6 +277,12 @@ LanczosResult lanczos_run(size_t dim, const ApplyFn& apply, const LanczosConfig&
         for (size_t i = 0; i < Q.size(); ++i) c[i] = dot(Q[i], r);
         for (size_t i = 0; i < Q.size(); ++i) r = axpy(-c[i], Q[i], r);
       }
+    } else if (sel) {
+      for (int pass = 0; pass < 2; ++pass) {
+        std::vector<double> c(stored);
+        for (size_t i = 0; i < stored; ++i) c[i] = dot(ring[i], r);
+        for (size_t i = 0; i < stored; ++i) r = axpy(-c[i], ring[i], r);
+      }
     }
     const double beta = norm2(r);
     res.alphas.push_back(alpha);
@@ -286,6 +301,10 @@ LanczosResult lanczos_run(size_t dim, const ApplyFn& apply, const LanczosConfig&
     q_prev = q;
     q = scale(r, 1.0 / beta);
     if (keep) Q.push_back(q);
+    if (sel) {
+      ring[(k + 1) % W] = q;
+      stored = std::min(stored + 1, W);
+    }
   }
   if (keep) res.basis = std::move(Q);
   return res;

@@ -124,7 +124,7 @@ Dense spiked_dense(size_t n, double sigma, const std::vector<double>& spikes, ui
 Vec dense_apply(const Dense& m, const Vec& x);
 
 // ---- Lanczos: Alg. 2 ------------------------------
-enum class Reorth { none = 0, full = 1 };
+enum class Reorth { none = 0, full = 1, selective = 2 };
 struct LanczosConfig {
   size_t k_max = 10;
   double eps = -1.0;  // <0: default 1e-12 (f64) / 1e-7 (f32)
@@ -132,6 +132,7 @@ struct LanczosConfig {
   ProbeSpec probe;
   Precision prec = Precision::f64;
   bool store_basis = false;  // forced on by full reorth
+  size_t window = 0;         // selective: the most recent `window` columns (>= 2)
 };
 struct LanczosResult {
   std::vector<double> alphas, betas;

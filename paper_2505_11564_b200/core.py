@@ -28,7 +28,7 @@ from ._lib import (ArgumentError, ConfigError, LayoutError, NumericalError, Prot
 
 F32, F64 = 0, 1
 GAUSSIAN, RADEMACHER, ONE_HOT = 0, 1, 2
-REORTH_NONE, REORTH_FULL = 0, 1
+REORTH_NONE, REORTH_FULL, REORTH_SELECTIVE = 0, 1, 2
 _DTYPE = {F32: torch.float32, F64: torch.float64}
 
 
@@ -370,10 +370,11 @@ class LanczosConfig:
     reorthogonalize: int = REORTH_NONE
     probe: ProbeSpec = field(default_factory=ProbeSpec)
     prec: int = F64
+    selective_window: int = 0  # REORTH_SELECTIVE: 2xCGS over the most recent W columns (ring of W)
 
     def native(self) -> _lib.LanczosConfig:
         return _lib.LanczosConfig(self.k_max, self.eps, self.reorthogonalize, self.prec, self.probe.seed,
-                                  self.probe.distribution, 0)
+                                  self.probe.distribution, self.selective_window)
 
 
 @dataclass

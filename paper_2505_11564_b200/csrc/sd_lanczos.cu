@@ -39,8 +39,10 @@ Plan make_plan(const uint64_t* begins, const uint64_t* ends, uint64_t total, con
   if (!cfg) sd::fail(SD_CONFIG_ERROR, "null lanczos config");
   if (cfg->k_max < 1) sd::fail(SD_CONFIG_ERROR, "k_max must be >= 1");
   if (cfg->prec != SD_F32 && cfg->prec != SD_F64) sd::fail(SD_CONFIG_ERROR, "precision must be f32 or f64");
-  if (cfg->reorth != SD_REORTH_NONE && cfg->reorth != SD_REORTH_FULL)
-    sd::fail(SD_CONFIG_ERROR, "reorth must be none or full in this build");
+  if (cfg->reorth != SD_REORTH_NONE && cfg->reorth != SD_REORTH_FULL && cfg->reorth != SD_REORTH_SELECTIVE)
+    sd::fail(SD_CONFIG_ERROR, "reorth must be none, full or selective");
+  if (cfg->reorth == SD_REORTH_SELECTIVE && cfg->selective_window < 2)
+    sd::fail(SD_CONFIG_ERROR, "selective reorthogonalisation needs a window >= 2");
   if (nranks < 1 || rank < 0 || rank >= nranks) sd::fail(SD_ARGUMENT_ERROR, "bad rank/size");
   uint64_t at = 0;
   for (int r = 0; r < nranks; ++r) {
@@ -53,8 +55,10 @@ Plan make_plan(const uint64_t* begins, const uint64_t* ends, uint64_t total, con
   p.P = ends[rank] - begins[rank];
   p.esize = cfg->prec == SD_F32 ? 4 : 8;
   const bool keep = cfg->reorth == SD_REORTH_FULL;
-  p.ncols_alloc = keep ? cfg->k_max + 1 : 2;
-  p.m_max = keep ? cfg->k_max + 1 : 1;
+  const bool sel = cfg->reorth == SD_REORTH_SELECTIVE;
+  const uint64_t W = std::min<uint64_t>(cfg->selective_window, cfg->k_max + 1);
+  p.ncols_alloc = keep ? cfg->k_max + 1 : (sel ? std::max<uint64_t>(W, 2) : 2);
+  p.m_max = keep ? cfg->k_max + 1 : (sel ? std::max<uint64_t>(W, 2) : 1);
   uint64_t o = 0;
   p.off_Q = o;
   o = align_up(o + p.ncols_alloc * p.P * p.esize);
@@ -92,8 +96,12 @@ struct sd_lanczos_s {
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   double ms_apply = 0, ms_rec = 0, ms_reorth = 0;
 
+  // full: column i in slot i; selective: a ring of W slots (column i in slot
+  // i % W, swept in slot order -- oracle/src/core.cpp lanczos_run); none: 2 slots
   void* col(uint64_t i) const {
-    const uint64_t slot = cfg.reorth == SD_REORTH_FULL ? i : (i & 1);
+    const uint64_t slot = cfg.reorth == SD_REORTH_FULL ? i
+                          : cfg.reorth == SD_REORTH_SELECTIVE ? i % plan.ncols_alloc
+                                                              : (i & 1);
     return ws + plan.off_Q + slot * plan.P * plan.esize;
   }
   void* r() const { return ws + plan.off_r; }
@@ -215,6 +223,7 @@ struct sd_lanczos_s {
     sd::scale(r(), col(k + 1), plan.P, d_beta() + k, 1, cfg.prec, s);
     ++k;
     if (cfg.reorth == SD_REORTH_FULL) ++ncols;
+    if (cfg.reorth == SD_REORTH_SELECTIVE) ncols = std::min<uint64_t>(ncols + 1, plan.ncols_alloc);
   }
 
   ~sd_lanczos_s() {

@@ -208,3 +208,23 @@ def test_gpt_batched_hvp_weighting(oracle):
     whole = oracle.gpt_hvp(TINY, th, tok, tgt, 4, 8, v)
     split = oracle.gpt_batched_hvp(TINY, th, [(1, tok[:8], tgt[:8]), (3, tok[8:], tgt[8:])], 8, v)
     assert np.linalg.norm(split - whole) / np.linalg.norm(whole) < 1e-10
+
+
+def test_selective_reorth_sits_between_none_and_full(oracle):
+    # the oracle's selective variant: its basis loses orthogonality more slowly
+    # than no reorth and a window covering the whole run equals full reorth
+    from oracle.pyoracle import F64, RADEMACHER
+    S = oracle.spiked(256, 1.0 / 16, [100.0, -100.0], 7)
+    def lo(reorth, window=0):
+        r = oracle.lanczos_dense(S, 25, reorth=reorth, seed=1, dist=RADEMACHER, prec=F64, basis=True, window=window)
+        Q = r["basis"]
+        G = Q @ Q.T
+        return np.max(np.abs(G - np.eye(G.shape[0]))), r
+    # (a local window only helps once it covers the early, converged
+    # directions: W = 4 leaves this spiked run as non-orthogonal as none)
+    l_none, _ = lo(0)
+    l_sel, _ = lo(2, 20)
+    l_full, rf = lo(1)
+    assert l_full < l_sel < 1e-9 < l_none
+    _, rw = lo(2, 26)
+    assert np.array_equal(rw["alphas"], rf["alphas"]) and np.array_equal(rw["betas"], rf["betas"])

@@ -171,3 +171,19 @@ def test_f32_rounding_edge_cases(sd):
         assert rc == 0
         got = ty.cpu().numpy()
         assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), alpha
+
+
+@pytest.mark.parametrize("prec", [F32, F64])
+@pytest.mark.parametrize("window", [2, 5, 40])
+def test_lanczos_selective_bitwise(sd, oracle, prec, window):
+    # selective reorth (2x CGS over the most recent W columns, ring order) ==
+    # the oracle's restatement bit for bit; orthogonality between none and full
+    S = sd.spiked_dense(256, 1.0, [50.0, -50.0], 5)
+    op = sd.dense_operator(S)
+    cfg = sd.LanczosConfig(k_max=30, reorthogonalize=sd.REORTH_SELECTIVE, prec=prec, selective_window=window,
+                           probe=sd.ProbeSpec(seed=42, distribution=RADEMACHER))
+    r = sd.lanczos_run(op, cfg)
+    o = oracle.lanczos_dense(S, 30, reorth=2, seed=42, dist=RADEMACHER, prec=prec, window=window)
+    assert np.array_equal(r.alphas, o["alphas"]) and np.array_equal(r.betas, o["betas"])
+    with pytest.raises(sd.ConfigError):
+        sd.lanczos_run(op, sd.LanczosConfig(k_max=5, reorthogonalize=sd.REORTH_SELECTIVE, selective_window=1))
