@@ -78,6 +78,19 @@ void make_map(CUtensorMap* m, const float* base, long long inner, long long oute
   if (r != CUDA_SUCCESS) fail(SD_CUDA_ERROR, "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
 }
 
+void make_store_map(CUtensorMap* m, float* C, const GemmArgs& g) {
+  cuuint64_t dims[4] = {cuuint64_t(g.N), cuuint64_t(g.M), cuuint64_t(g.Z1), cuuint64_t(g.Z2)};
+  const long long whole = ((g.ldc * (long long)g.M * 4 + 15) / 16) * 16;
+  cuuint64_t strides[3] = {cuuint64_t(g.ldc * 4), cuuint64_t(g.Z1 > 1 ? g.sc1 * 4 : whole),
+                           cuuint64_t(g.Z2 > 1 ? g.sc2 * 4 : whole)};
+  cuuint32_t box[4] = {32, 32, 1, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  const CUresult r = encoder()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, C, dims, strides, box, es,
+                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(SD_CUDA_ERROR, "cuTensorMapEncodeTiled (C) failed (" + std::to_string(int(r)) + ")");
+}
+
 // The eight operand maps of a launch: A, A_small, B, B_small, then the same
 // for the second product of a dual-source GEMM (copies of the first if none).
 // K-major tiles are box_m (A) / box_n (B) rows of BK elements; MN-major tiles
@@ -237,13 +250,16 @@ void launch_splitk_reduce(const float* ws, int splits, int zc, const GemmArgs& g
 
 namespace {
 using namespace gk;
+bool sd_gemm_tma_store_enabled();
 
 template <bool A_MN, bool B_MN, bool THREE, int BN_, bool CAUSAL>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     k_gemm_tf32(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mAs,
                 const __grid_constant__ CUtensorMap mB, const __grid_constant__ CUtensorMap mBs,
                 const __grid_constant__ CUtensorMap mA2, const __grid_constant__ CUtensorMap mAs2,
-                const __grid_constant__ CUtensorMap mB2, const __grid_constant__ CUtensorMap mBs2, int K, EpiParams ep) {
+                const __grid_constant__ CUtensorMap mB2, const __grid_constant__ CUtensorMap mBs2,
+                const __grid_constant__ CUtensorMap mC, const __grid_constant__ CUtensorMap mCs, int K,
+                EpiParams ep) {
   using Cf = Cfg<BN_>;
   constexpr int BN = Cf::BN, STAGES = Cf::STAGES, EC = Cf::EC;
   constexpr int A_BYTES = Cf::A_BYTES, B_BYTES = Cf::B_BYTES;
@@ -252,7 +268,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   // 1024-byte aligned ring: per stage [A | As | B | Bs]
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   constexpr int STAGE_BYTES = (THREE ? 2 : 1) * (A_BYTES + B_BYTES);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  // [ring | 8 epilogue staging boxes of 4 KB (TMA store) | barriers]
+  float* epi_stage = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES + 8 * 4096);
   uint64_t* empty = full + STAGES;
   uint64_t* conv = empty + STAGES;   // [STAGES] residual tiles ready
   uint64_t* tfull = conv + STAGES;   // [2]
@@ -423,9 +441,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[buf]);
       }
-      store_row<EC>(ep, ti, row, ti.n0 + cb, acc);
+      if (ep.tma_store) {
+        const int ew = warp - 2 - kConvWarps;  // 0..7: its staging box
+        warp_tma_store<EC>(&mC, ep.Cs ? &mCs : nullptr, epi_stage + ew * 1024, acc, ep.alpha,
+                           ep.bias, lane, ti.m0 + sub * 32, ti.n0 + cb, ti.z % ep.Z1, ti.z / ep.Z1);
+        if (lane == 0) bulk_wait_read0();  // staging box free for the next tile
+        __syncwarp();
+      } else {
+        store_row<EC>(ep, ti, row, ti.n0 + cb, acc);
+      }
     }
   }
+  if (ep.tma_store && lane == 0) bulk_wait0();  // (no-op for non-epilogue warps: nothing committed)
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == 1) {
@@ -479,7 +506,19 @@ void launch(const GemmArgs& g, cudaStream_t s) {
   if (splits > 1) ws = splitk_workspace(size_t(splits) * zc * size_t(g.M) * g.N);
   EpiParams ep{g.C, g.ldc, g.sc1, g.sc2, g.M, g.N, g.Z1, g.alpha, g.beta, g.bias, g.Cs, g.dbg, zc, kb_per, ws,
                g.causal, tn, tm, tiles * splits, dual ? 2 : 1, g.onchip ? 1 : 0};
-  const size_t smem = 1024 + size_t(Cf::STAGES) * (THREE ? 2 : 1) * (Cf::A_BYTES + Cf::B_BYTES) + 512;
+  const size_t smem = 1024 + size_t(Cf::STAGES) * (THREE ? 2 : 1) * (Cf::A_BYTES + Cf::B_BYTES) + 8 * 4096 + 512;
+  // TMA-store epilogue: plain C = alpha op(A) op(B) tiles (no accumulate/bias/residual/split)
+  CUtensorMap mC = maps[0], mCs = maps[0];
+  const bool tma_store = sd_gemm_tma_store_enabled() && splits == 1 && g.beta == 0.0f &&
+                         (reinterpret_cast<uintptr_t>(g.C) & 15) == 0 && (g.ldc % 4) == 0 &&
+                         (!g.Cs || (reinterpret_cast<uintptr_t>(g.Cs) & 15) == 0) &&
+                         (!g.bias || ((reinterpret_cast<uintptr_t>(g.bias) & 15) == 0 && g.N % 32 == 0)) &&
+                         (zc == 1 || ((g.Z1 == 1 || g.sc1 % 4 == 0) && (g.Z2 == 1 || g.sc2 % 4 == 0)));
+  if (tma_store) {
+    make_store_map(&mC, g.C, g);
+    if (g.Cs) make_store_map(&mCs, g.Cs, g);
+  }
+  ep.tma_store = tma_store ? 1 : 0;
   auto kern = g.causal ? k_gemm_tf32<A_MN, B_MN, THREE, BN, true> : k_gemm_tf32<A_MN, B_MN, THREE, BN, false>;
   static bool attr_set = false;
   if (!attr_set) {
@@ -495,7 +534,8 @@ void launch(const GemmArgs& g, cudaStream_t s) {
                       std::to_string(zc) + "," + std::to_string(int(A_MN)) + "," + std::to_string(int(B_MN)) + "," +
                       std::to_string(g.causal) + "," + std::to_string(splits) + (dual ? ",2" : ",1");
   prof_begin(s);
-  kern<<<grid, NUM_THREADS, smem, s>>>(maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], maps[6], maps[7], g.K, ep);
+  kern<<<grid, NUM_THREADS, smem, s>>>(maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], maps[6], maps[7], mC,
+                                       mCs, g.K, ep);
   SD_LAUNCHED("k_gemm_tf32");
   if (splits > 1) {
     launch_splitk_reduce(ws, splits, zc, g, s);
@@ -509,6 +549,10 @@ bool env_on(const char* name) {
 }
 bool sd_gemm_wide_enabled() {
   static const bool on = env_on("SD_GEMM_WIDE");
+  return on;
+}
+bool sd_gemm_tma_store_enabled() {
+  static const bool on = env_on("SD_GEMM_TMA_STORE");
   return on;
 }
 bool sd_gemm_pair_enabled() {

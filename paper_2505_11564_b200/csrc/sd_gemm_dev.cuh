@@ -130,7 +130,72 @@ struct EpiParams {
   int n_tiles_n, n_tiles_m, n_tiles;  // tile grid (n fastest), n_tiles over all (split, z)
   int nsrc;                           // 1, or 2 for a dual-source product
   int res;                            // 3xTF32 residuals computed on chip from the staged raw tiles
+  int tma_store;                      // C = alpha acc written by TMA from smem (beta 0, no bias/Cs/split)
 };
+
+__device__ __forceinline__ void fence_proxy_async_smem_decl() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+// TMA store of a staged 32 x 32 fp32 box (128B-swizzled smem) to C
+__device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, const void* src, int c0, int c1, int c2, int c3) {
+  asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(map),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+// One warp's 32 rows x EC columns (thread = row) of o = alpha*acc (+ bias)
+// -- and, if requested, the tf32 residual of o into Cs -- through a 4 KB
+// 128B-swizzled staging box and TMA stores (full lines; OOB clipped).
+template <int EC>
+__device__ __forceinline__ void warp_tma_store(const CUtensorMap* mC, const CUtensorMap* mCs, float* stage,
+                                               const float (&acc)[EC], float alpha, const float* bias, int lane,
+                                               int row0, int col0, int z1, int z2) {
+  float4* rowp = reinterpret_cast<float4*>(stage + lane * 32);
+  bool pending = false;
+#pragma unroll
+  for (int c0 = 0; c0 < EC; c0 += 32) {
+    float o[32];
+#pragma unroll
+    for (int q = 0; q < 32; ++q) o[q] = alpha * acc[c0 + q];
+    if (bias) {
+      const float4* b4 = reinterpret_cast<const float4*>(bias + col0 + c0);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const float4 bb = b4[q];
+        o[4 * q] += bb.x, o[4 * q + 1] += bb.y, o[4 * q + 2] += bb.z, o[4 * q + 3] += bb.w;
+      }
+    }
+#pragma unroll
+    for (int pass = 0; pass < 2; ++pass) {
+      if (pass == 1 && !mCs) break;
+      if (pending) {  // the previous box must have left the staging buffer
+        if (lane == 0) bulk_wait_read0();
+        __syncwarp();
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        float4 v = make_float4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
+        if (pass == 1) {
+          v.x -= __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+          v.y -= __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+          v.z -= __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+          v.w -= __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+        }
+        rowp[q ^ (lane & 7)] = v;
+      }
+      fence_proxy_async_smem_decl();
+      __syncwarp();
+      if (lane == 0) {
+        tma_store_4d(pass ? mCs : mC, stage, col0 + c0, row0, z1, z2);
+        bulk_commit();
+      }
+      pending = true;
+    }
+  }
+}
 
 // x - trunc_tf32(x) over a staged operand tile (any smem layout: the residual
 // is elementwise), written to the tile's residual slot; threads t of nt.
@@ -305,6 +370,8 @@ __device__ __forceinline__ void store_row(const EpiParams& ep, const TileInfo& t
 // ---- host helpers (sd_gemm.cu)
 void make_map(CUtensorMap* m, const float* base, long long inner, long long outer, long long ld, int Z1,
               long long s1, int Z2, long long s2, int box_inner, int box_outer, bool mn_major);
+// 32 x 32 fp32 boxes, 128B swizzle: the epilogue's TMA store map of C
+void make_store_map(CUtensorMap* m, float* C, const GemmArgs& g);
 float* splitk_workspace(size_t floats);
 int choose_splits(int tiles, int units, int total_kb, int nsrc, double t_kb, double out_bytes);
 void operand_maps(const GemmArgs& g, bool a_mn, bool b_mn, bool three, int box_n, CUtensorMap* m);
