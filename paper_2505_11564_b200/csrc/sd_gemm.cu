@@ -78,15 +78,31 @@ void make_map(CUtensorMap* m, const float* base, long long inner, long long oute
   if (r != CUDA_SUCCESS) fail(SD_CUDA_ERROR, "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
 }
 
-void make_store_map(CUtensorMap* m, float* C, const GemmArgs& g) {
+bool sd_gemm_tma_store_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("SD_GEMM_TMA_STORE");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+bool tma_store_ok(const GemmArgs& g, int splits, int bias_cols) {
+  return sd_gemm_tma_store_enabled() && splits == 1 && g.beta == 0.0f &&
+         (reinterpret_cast<uintptr_t>(g.C) & 15) == 0 && (g.ldc % 4) == 0 &&
+         (!g.Cs || (reinterpret_cast<uintptr_t>(g.Cs) & 15) == 0) &&
+         (!g.bias || ((reinterpret_cast<uintptr_t>(g.bias) & 15) == 0 && g.N % bias_cols == 0)) &&
+         (g.Z1 * g.Z2 == 1 || ((g.Z1 == 1 || g.sc1 % 4 == 0) && (g.Z2 == 1 || g.sc2 % 4 == 0)));
+}
+
+void make_store_map(CUtensorMap* m, float* C, const GemmArgs& g, int box_cols) {
   cuuint64_t dims[4] = {cuuint64_t(g.N), cuuint64_t(g.M), cuuint64_t(g.Z1), cuuint64_t(g.Z2)};
   const long long whole = ((g.ldc * (long long)g.M * 4 + 15) / 16) * 16;
   cuuint64_t strides[3] = {cuuint64_t(g.ldc * 4), cuuint64_t(g.Z1 > 1 ? g.sc1 * 4 : whole),
                            cuuint64_t(g.Z2 > 1 ? g.sc2 * 4 : whole)};
-  cuuint32_t box[4] = {32, 32, 1, 1};
+  cuuint32_t box[4] = {cuuint32_t(box_cols), 32, 1, 1};
   cuuint32_t es[4] = {1, 1, 1, 1};
   const CUresult r = encoder()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, C, dims, strides, box, es,
-                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                               CU_TENSOR_MAP_INTERLEAVE_NONE,
+                               box_cols == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) fail(SD_CUDA_ERROR, "cuTensorMapEncodeTiled (C) failed (" + std::to_string(int(r)) + ")");
 }
@@ -250,7 +266,6 @@ void launch_splitk_reduce(const float* ws, int splits, int zc, const GemmArgs& g
 
 namespace {
 using namespace gk;
-bool sd_gemm_tma_store_enabled();
 
 template <bool A_MN, bool B_MN, bool THREE, int BN_, bool CAUSAL>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
@@ -509,11 +524,7 @@ void launch(const GemmArgs& g, cudaStream_t s) {
   const size_t smem = 1024 + size_t(Cf::STAGES) * (THREE ? 2 : 1) * (Cf::A_BYTES + Cf::B_BYTES) + 8 * 4096 + 512;
   // TMA-store epilogue: plain C = alpha op(A) op(B) tiles (no accumulate/bias/residual/split)
   CUtensorMap mC = maps[0], mCs = maps[0];
-  const bool tma_store = sd_gemm_tma_store_enabled() && splits == 1 && g.beta == 0.0f &&
-                         (reinterpret_cast<uintptr_t>(g.C) & 15) == 0 && (g.ldc % 4) == 0 &&
-                         (!g.Cs || (reinterpret_cast<uintptr_t>(g.Cs) & 15) == 0) &&
-                         (!g.bias || ((reinterpret_cast<uintptr_t>(g.bias) & 15) == 0 && g.N % 32 == 0)) &&
-                         (zc == 1 || ((g.Z1 == 1 || g.sc1 % 4 == 0) && (g.Z2 == 1 || g.sc2 % 4 == 0)));
+  const bool tma_store = tma_store_ok(g, splits, 32);
   if (tma_store) {
     make_store_map(&mC, g.C, g);
     if (g.Cs) make_store_map(&mCs, g.Cs, g);
@@ -549,10 +560,6 @@ bool env_on(const char* name) {
 }
 bool sd_gemm_wide_enabled() {
   static const bool on = env_on("SD_GEMM_WIDE");
-  return on;
-}
-bool sd_gemm_tma_store_enabled() {
-  static const bool on = env_on("SD_GEMM_TMA_STORE");
   return on;
 }
 bool sd_gemm_pair_enabled() {

@@ -149,21 +149,25 @@ __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_
 // One warp's 32 rows x EC columns (thread = row) of o = alpha*acc (+ bias)
 // -- and, if requested, the tf32 residual of o into Cs -- through a 4 KB
 // 128B-swizzled staging box and TMA stores (full lines; OOB clipped).
-template <int EC>
+// BOXC = 32 (128 B rows, SWIZZLE_128B: chunk c of row r at c ^ (r & 7)) or
+// 16 (64 B rows, SWIZZLE_64B: chunk c at c ^ ((r >> 1) & 3)).
+template <int EC, int BOXC = 32>
 __device__ __forceinline__ void warp_tma_store(const CUtensorMap* mC, const CUtensorMap* mCs, float* stage,
                                                const float (&acc)[EC], float alpha, const float* bias, int lane,
                                                int row0, int col0, int z1, int z2) {
-  float4* rowp = reinterpret_cast<float4*>(stage + lane * 32);
+  constexpr int NQ = BOXC / 4;  // 16 B chunks per staged row
+  const int sw = BOXC == 32 ? (lane & 7) : ((lane >> 1) & 3);
+  float4* rowp = reinterpret_cast<float4*>(stage + lane * BOXC);
   bool pending = false;
 #pragma unroll
-  for (int c0 = 0; c0 < EC; c0 += 32) {
-    float o[32];
+  for (int c0 = 0; c0 < EC; c0 += BOXC) {
+    float o[BOXC];
 #pragma unroll
-    for (int q = 0; q < 32; ++q) o[q] = alpha * acc[c0 + q];
+    for (int q = 0; q < BOXC; ++q) o[q] = alpha * acc[c0 + q];
     if (bias) {
       const float4* b4 = reinterpret_cast<const float4*>(bias + col0 + c0);
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
+      for (int q = 0; q < NQ; ++q) {
         const float4 bb = b4[q];
         o[4 * q] += bb.x, o[4 * q + 1] += bb.y, o[4 * q + 2] += bb.z, o[4 * q + 3] += bb.w;
       }
@@ -176,7 +180,7 @@ __device__ __forceinline__ void warp_tma_store(const CUtensorMap* mC, const CUte
         __syncwarp();
       }
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
+      for (int q = 0; q < NQ; ++q) {
         float4 v = make_float4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
         if (pass == 1) {
           v.x -= __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
@@ -184,7 +188,7 @@ __device__ __forceinline__ void warp_tma_store(const CUtensorMap* mC, const CUte
           v.z -= __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
           v.w -= __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
         }
-        rowp[q ^ (lane & 7)] = v;
+        rowp[q ^ sw] = v;
       }
       fence_proxy_async_smem_decl();
       __syncwarp();
@@ -370,8 +374,10 @@ __device__ __forceinline__ void store_row(const EpiParams& ep, const TileInfo& t
 // ---- host helpers (sd_gemm.cu)
 void make_map(CUtensorMap* m, const float* base, long long inner, long long outer, long long ld, int Z1,
               long long s1, int Z2, long long s2, int box_inner, int box_outer, bool mn_major);
-// 32 x 32 fp32 boxes, 128B swizzle: the epilogue's TMA store map of C
-void make_store_map(CUtensorMap* m, float* C, const GemmArgs& g);
+// box_cols x 32 fp32 boxes (32: 128B swizzle, 16: 64B): the epilogue's TMA store map of C
+void make_store_map(CUtensorMap* m, float* C, const GemmArgs& g, int box_cols = 32);
+// whether a product may take the TMA-store epilogue (beta 0, aligned C/Cs/bias, no split)
+bool tma_store_ok(const GemmArgs& g, int splits, int bias_cols);
 float* splitk_workspace(size_t floats);
 int choose_splits(int tiles, int units, int total_kb, int nsrc, double t_kb, double out_bytes);
 void operand_maps(const GemmArgs& g, bool a_mn, bool b_mn, bool three, int box_n, CUtensorMap* m);

@@ -106,12 +106,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     k_gemm_pair(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mAs,
                 const __grid_constant__ CUtensorMap mB, const __grid_constant__ CUtensorMap mBs,
                 const __grid_constant__ CUtensorMap mA2, const __grid_constant__ CUtensorMap mAs2,
-                const __grid_constant__ CUtensorMap mB2, const __grid_constant__ CUtensorMap mBs2, int K, EpiParams ep) {
+                const __grid_constant__ CUtensorMap mB2, const __grid_constant__ CUtensorMap mBs2,
+                const __grid_constant__ CUtensorMap mC, const __grid_constant__ CUtensorMap mCs, int K, EpiParams ep) {
   constexpr int STAGES = kPairStages, EC = kPairEC;
   constexpr int STAGE_BYTES = (THREE ? 2 : 1) * (PA_BYTES + PB_BYTES);
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  // [ring | 16 epilogue staging boxes of 2 KB (TMA store, 16 x 32 fp32) | barriers]
+  float* epi_stage = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES + kEpiWarps * 2048);
   uint64_t* empty = full + STAGES;
   uint64_t* conv = empty + STAGES;   // [STAGES] (leader) both CTAs' stage s landed + residuals written
   uint64_t* tfull = conv + STAGES;   // [2]
@@ -294,9 +297,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive_remote(tempty_leader + 8u * buf);
       }
-      store_row<EC>(ep, ti, row, ti.n0 + cb, acc);
+      if (ep.tma_store) {
+        const int ew = warp - 2 - kConvWarps;  // 0..15: its staging box
+        warp_tma_store<EC, 16>(&mC, ep.Cs ? &mCs : nullptr, epi_stage + ew * 512, acc, ep.alpha, ep.bias, lane,
+                               ti.m0 + int(rank) * BM + sub * 32, ti.n0 + cb, ti.z % ep.Z1, ti.z / ep.Z1);
+        if (lane == 0) bulk_wait_read0();  // staging box free for the next tile
+        __syncwarp();
+      } else {
+        store_row<EC>(ep, ti, row, ti.n0 + cb, acc);
+      }
     }
   }
+  if (ep.tma_store && lane == 0) bulk_wait0();
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   cluster_sync();  // no CTA leaves while its peer may still touch its smem / barriers
   if (warp == 1) {
@@ -330,7 +342,7 @@ void launch_pair_t(const GemmArgs& g, cudaStream_t s) {
   const int zc = g.Z1 * g.Z2;
   const int tn = (g.N + kPairN - 1) / kPairN, tm = (g.M + kPairM - 1) / kPairM;
   const int tiles = tn * tm * zc;
-  const size_t smem = 1024 + size_t(kPairStages) * (THREE ? 2 : 1) * (PA_BYTES + PB_BYTES) + 512;
+  const size_t smem = 1024 + size_t(kPairStages) * (THREE ? 2 : 1) * (PA_BYTES + PB_BYTES) + kEpiWarps * 2048 + 512;
   auto kern = k_gemm_pair<A_MN, B_MN, THREE>;
   static int clusters = 0;
   if (!clusters) {
@@ -353,7 +365,14 @@ void launch_pair_t(const GemmArgs& g, cudaStream_t s) {
              "," + std::to_string(int(A_MN)) + "," + std::to_string(int(B_MN)) + ",pair," + std::to_string(splits) +
              (dual ? ",2" : ",1"));
   prof_begin(s);
-  kern<<<grid, kPairThreads, smem, s>>>(maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], maps[6], maps[7], g.K,
+  CUtensorMap mC = maps[0], mCs = maps[0];
+  if (tma_store_ok(g, splits, 16)) {
+    make_store_map(&mC, g.C, g, 16);
+    if (g.Cs) make_store_map(&mCs, g.Cs, g, 16);
+    ep.tma_store = 1;
+  }
+  kern<<<grid, kPairThreads, smem, s>>>(maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], maps[6], maps[7], mC, mCs,
+                                        g.K,
                                         ep);
   SD_LAUNCHED("k_gemm_pair");
   if (splits > 1) launch_splitk_reduce(ws, splits, zc, g, s);
