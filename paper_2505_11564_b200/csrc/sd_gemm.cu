@@ -574,14 +574,14 @@ void gemm(const GemmArgs& g_in, cudaStream_t s) {
   GemmArgs g = g_in;
   const bool pair = g.causal == 0 && g.M >= 256 && g.N >= 256 && sd_gemm_pair_enabled();
   // On-chip residuals (onchip = allowed): they halve the operand bytes through
-  // L2 and TMA but add a shared-memory read + write of every staged tile. That
-  // pays where a kernel is L2-operand bound (MN-major A in the weight products:
-  // 120 -> 150 TF/s) and costs where shared memory is the tighter limit (the
-  // K-major pair products: 258 -> 162 TF/s); callers with residual arrays get
-  // them elsewhere. Without arrays (attention P, dP, gS, gdS) on chip is forced.
+  // L2 and TMA but add a shared-memory read + write of every staged tile, and
+  // measured slower wherever residual arrays exist (K-major pair products 258
+  // -> 162 TF/s; the dual weight products 176 -> 158, scratch/ab_wgrad.py).
+  // So they are used where arrays do not exist (attention P, dP, gS, gdS).
+  (void)pair;
   if (g.onchip) {
     const bool have = g.As && g.Bs && (!g.A2 || (g.A2s && g.B2s));
-    const bool prefer = pair && g.a_mn;
+    const bool prefer = false;
     if (have && !prefer) g.onchip = false;
     else g.As = g.Bs = g.A2s = g.B2s = nullptr;
   }
