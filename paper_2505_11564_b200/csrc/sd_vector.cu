@@ -442,6 +442,9 @@ static void launch_axpy_dot(const void* x, void* y, const void* z, const double*
   }
 }
 
+__device__ __forceinline__ double to_d_alu(float x) { return widen_f32(x); }
+__device__ __forceinline__ double to_d_alu(double x) { return x; }
+
 // Fused Gram-Schmidt pass over full grid blocks: one CTA per 1024-element
 // block, walked in CH-element chunks that are double-buffered in shared
 // memory with cp.async (one HBM read of the j basis columns per pass):
@@ -517,7 +520,9 @@ __global__ void __launch_bounds__(128) k_cgs_block(const T* __restrict__ Q, uint
       T rv = r[e0 + c0 + tid];
       if (UPD) {
         double v = double(rv);
-        for (int i = 0; i < j; ++i) v = rround<T>((__dadd_rn(v, __dmul_rn(cs[i], double(qt[i * STRIDE + tid])))));
+        // widening of the staged column entries on the integer pipe (the XU
+        // pipe carries the f64 -> f32 rounding and the dot phase's widening)
+        for (int i = 0; i < j; ++i) v = rround<T>((__dadd_rn(v, __dmul_rn(cs[i], to_d_alu(qt[i * STRIDE + tid])))));
         rv = T(v);
         r[e0 + c0 + tid] = rv;
         rt[tid] = v;
@@ -553,6 +558,14 @@ __global__ void __launch_bounds__(128) k_cgs_block(const T* __restrict__ Q, uint
   if (tid + 128 < j) partials[uint64_t(tid + 128) * pstride + head_n + unit] = acc1;
 }
 
+static uint64_t fused_update_max_cols() {
+  static const uint64_t v = [] {
+    const char* e = std::getenv("SD_CGS_FUSED_UPDATE_MAX");
+    return e ? uint64_t(std::strtoull(e, nullptr, 10)) : uint64_t(40);
+  }();
+  return v;
+}
+
 template <typename T>
 static bool launch_cgs_fused(const void* Q, uint64_t ldq, uint64_t j, void* r, const double* coef, int mode,
                              const PartialShape& ps, uint64_t local_end, uint64_t plen, double* partials,
@@ -567,7 +580,7 @@ static bool launch_cgs_fused(const void* Q, uint64_t ldq, uint64_t j, void* r, c
   // the in-CTA update is a j-long dependent chain per element: beyond ~40
   // columns the element-parallel k_cgs_update followed by the block dots is
   // faster than the fused single read (measured, scratch/bench_lanczos_kernels.py)
-  if (coef != nullptr && j >= 40) {
+  if (coef != nullptr && j >= fused_update_max_cols()) {
     constexpr int W = V16<T>::W;
     const uint64_t threads = (local_end + W - 1) / W;
     k_cgs_update<T><<<unsigned((threads + 255) / 256), 256, size_t(j) * sizeof(double), s>>>(
