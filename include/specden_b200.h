@@ -200,7 +200,11 @@ sd_status sd_gemm_profile_end(double* ms, double* flops, uint64_t* launches);
  * parameter order = declaration order, row-major. */
 typedef struct {
   int n_layer, d, n_head, ff, vocab, ctx;
+  int arch;        /* SD_ARCH_GPT2 (pre-LN, biases, GELU, learned positions, tied head) or
+                      SD_ARCH_LLAMA (RMSNorm, RoPE, SwiGLU, no biases, untied head) */
+  float rope_base; /* RoPE base (SD_ARCH_LLAMA), e.g. 10000 */
 } sd_gpt_config;
+enum { SD_ARCH_GPT2 = 0, SD_ARCH_LLAMA = 1 };
 typedef struct sd_gpt_s* sd_gpt;
 uint64_t sd_gpt_param_count(const sd_gpt_config* c);
 sd_status sd_gpt_param_layout(const sd_gpt_config* c, uint64_t* offsets, uint64_t* rows, uint64_t* cols, int* kinds,

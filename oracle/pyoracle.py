@@ -239,7 +239,8 @@ class Oracle:
     # ---- GPT / MLP autodiff
     @staticmethod
     def _cfg(cfg) -> np.ndarray:
-        return np.array([cfg["n_layer"], cfg["d"], cfg["n_head"], cfg["ff"], cfg["vocab"], cfg["ctx"]], np.int64)
+        return np.array([cfg["n_layer"], cfg["d"], cfg["n_head"], cfg["ff"], cfg["vocab"], cfg["ctx"],
+                         cfg.get("arch", 0), cfg.get("rope_base", 10000)], np.int64)
 
     def gpt_param_count(self, cfg) -> int:
         c = self._cfg(cfg)
@@ -247,7 +248,7 @@ class Oracle:
 
     def gpt_layout(self, cfg):
         c = self._cfg(cfg)
-        n = 4 + 12 * cfg["n_layer"]
+        n = (4 + 12 * cfg["n_layer"]) if cfg.get("arch", 0) == 0 else (3 + 6 * cfg["n_layer"])
         off = np.zeros(n, np.int64)
         r = np.zeros(n, np.int64)
         co = np.zeros(n, np.int64)

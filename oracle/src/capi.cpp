@@ -30,6 +30,8 @@ static GptConfig gcfg(const long long* c) {
   g.ff = size_t(c[3]);
   g.vocab = size_t(c[4]);
   g.ctx = size_t(c[5]);
+  g.arch = int(c[6]);
+  g.rope_base = double(c[7]);
   return g;
 }
 

@@ -15,6 +15,23 @@ std::vector<ParamSlot> gpt_layout(const GptConfig& c) {
     s.push_back({name, off, r, cc, kind});
     off += r * cc;
   };
+  if (c.arch == 1) {
+    // Llama-style (this project's declaration order; [in][out] matrices, the
+    // q|k|v and gate|up projections fused column-wise, untied head [V][d])
+    add("tok_embeddings", c.vocab, c.d, 0);
+    for (size_t l = 0; l < c.n_layer; ++l) {
+      const std::string p = "layers." + std::to_string(l) + ".";
+      add(p + "attention_norm.weight", 1, c.d, 1);
+      add(p + "attention.wqkv", c.d, 3 * c.d, 0);
+      add(p + "attention.wo", c.d, c.d, 0);
+      add(p + "ffn_norm.weight", 1, c.d, 1);
+      add(p + "feed_forward.w_gate_up", c.d, 2 * c.ff, 0);
+      add(p + "feed_forward.w_down", c.ff, c.d, 0);
+    }
+    add("norm.weight", 1, c.d, 1);
+    add("output", c.vocab, c.d, 0);
+    return s;
+  }
   add("wte", c.vocab, c.d, 0);
   add("wpe", c.ctx, c.d, 0);
   for (size_t l = 0; l < c.n_layer; ++l) {
@@ -93,6 +110,19 @@ int layernorm(Graph& g, int x, int gamma, int beta, size_t T, size_t d, double e
   return g.addrow(g.mul(xh, g.matmul(g.ones(T, 1), gamma)), beta);
 }
 
+// RMSNorm: h = gamma * x * (mean(x^2) + eps)^-1/2 (exp(-1/2 log) as in layernorm)
+int rmsnorm(Graph& g, int x, int gamma, size_t T, size_t d, double eps) {
+  const int ms = g.smul(g.sum_cols(g.mul(x, x)), 1.0 / double(d));
+  const int r = g.exp_(g.smul(g.log_(g.add(ms, g.constant(Tensor(T, 1, eps)))), -0.5));
+  return g.mul(g.mulcol(x, r), g.matmul(g.ones(T, 1), gamma));
+}
+
+// SiLU: x * 1 / (1 + exp(-x))
+int silu(Graph& g, int x) {
+  const Tensor& xv = g.val(x);
+  return g.mul(x, g.recip(g.add(g.ones(xv.rows, xv.cols), g.exp_(g.smul(x, -1.0)))));
+}
+
 int gelu_tanh(Graph& g, int x) {
   const Tensor& xv = g.val(x);
   const double k = std::sqrt(2.0 / 3.141592653589793);
@@ -102,7 +132,10 @@ int gelu_tanh(Graph& g, int x) {
   return g.mul(g.smul(x, 0.5), g.add(g.ones(xv.rows, xv.cols), t));
 }
 
+GptNodes build_llama(Graph& g, const GptConfig& c, const std::vector<double>& theta, const Batch& bt);
+
 GptNodes build_gpt(Graph& g, const GptConfig& c, const std::vector<double>& theta, const Batch& bt) {
+  if (c.arch == 1) return build_llama(g, c, theta, bt);
   const auto slots = gpt_layout(c);
   GptNodes out;
   for (const auto& s : slots) out.params.push_back(g.param(slice(theta, s)));
@@ -170,6 +203,99 @@ GptNodes build_gpt(Graph& g, const GptConfig& c, const std::vector<double>& thet
   const int gf = out.params[pi++], bfn = out.params[pi++];
   const int hf = layernorm(g, x, gf, bfn, T, d, c.ln_eps);
   const int logits = g.matmul(hf, wte, false, true);
+  out.loss = g.cross_entropy(logits, g.constant(tgt));
+  return out;
+}
+
+// Llama-style decoder in the same primitives: RMSNorm (pre-norm), RoPE on q/k
+// (rotate-half convention: t*cos + (t R)*sin with the constant R), causal
+// softmax attention, SwiGLU MLP (silu(gate) * up), untied output head.
+GptNodes build_llama(Graph& g, const GptConfig& c, const std::vector<double>& theta, const Batch& bt) {
+  const auto slots = gpt_layout(c);
+  GptNodes out;
+  for (const auto& s : slots) out.params.push_back(g.param(slice(theta, s)));
+  const size_t B = bt.B, S = bt.S, T = B * S, d = c.d, H = c.n_head, dh = d / H, ff = c.ff;
+  if (d % H || dh % 2) fail(Err::argument, "d must be divisible by n_head (even head dim)");
+  Tensor tok(T, c.vocab), tgt(T, c.vocab);
+  for (size_t t = 0; t < T; ++t) {
+    tok.at(t, bt.tokens[t]) = 1.0;
+    tgt.at(t, bt.targets[t]) = 1.0;
+  }
+  size_t pi = 0;
+  const int emb = out.params[pi++];
+  int x = g.matmul(g.constant(tok), emb);
+  Tensor mask(S, S), cosT(S, dh), sinT(S, dh), rot(dh, dh);
+  for (size_t i = 0; i < S; ++i)
+    for (size_t j = i + 1; j < S; ++j) mask.at(i, j) = -1e30;
+  const size_t half = dh / 2;
+  for (size_t p = 0; p < S; ++p)
+    for (size_t i = 0; i < half; ++i) {
+      const double theta_i = std::pow(c.rope_base, -2.0 * double(i) / double(dh));
+      const double ang = double(p) * theta_i;
+      cosT.at(p, i) = cosT.at(p, i + half) = std::cos(ang);
+      sinT.at(p, i) = sinT.at(p, i + half) = std::sin(ang);
+    }
+  for (size_t i = 0; i < half; ++i) {
+    rot.at(i + half, i) = -1.0;  // (t R)[i] = -t[i + half]
+    rot.at(i, i + half) = 1.0;   // (t R)[i + half] = t[i]
+  }
+  const int maskn = g.constant(mask), cosn = g.constant(cosT), sinn = g.constant(sinT), rotn = g.constant(rot);
+  auto rope = [&](int t) { return g.add(g.mul(t, cosn), g.mul(g.matmul(t, rotn), sinn)); };
+  std::vector<int> rsel(B);
+  for (size_t b = 0; b < B; ++b) {
+    Tensor r(S, T);
+    for (size_t s2 = 0; s2 < S; ++s2) r.at(s2, b * S + s2) = 1.0;
+    rsel[b] = g.constant(r);
+  }
+  std::vector<int> qsel(H), ksel(H), vsel(H), place(H);
+  for (size_t h = 0; h < H; ++h) {
+    Tensor q(3 * d, dh), k(3 * d, dh), v(3 * d, dh), p(dh, d);
+    for (size_t e = 0; e < dh; ++e) {
+      q.at(h * dh + e, e) = 1.0;
+      k.at(d + h * dh + e, e) = 1.0;
+      v.at(2 * d + h * dh + e, e) = 1.0;
+      p.at(e, h * dh + e) = 1.0;
+    }
+    qsel[h] = g.constant(q);
+    ksel[h] = g.constant(k);
+    vsel[h] = g.constant(v);
+    place[h] = g.constant(p);
+  }
+  Tensor gsel(2 * ff, ff), usel(2 * ff, ff);
+  for (size_t e = 0; e < ff; ++e) {
+    gsel.at(e, e) = 1.0;
+    usel.at(ff + e, e) = 1.0;
+  }
+  const int gseln = g.constant(gsel), useln = g.constant(usel);
+  const double sc = 1.0 / std::sqrt(double(dh));
+  for (size_t l = 0; l < c.n_layer; ++l) {
+    const int g1 = out.params[pi++], wqkv = out.params[pi++], wo = out.params[pi++];
+    const int g2 = out.params[pi++], wgu = out.params[pi++], wd = out.params[pi++];
+    const int h1 = rmsnorm(g, x, g1, T, d, c.ln_eps);
+    const int qkv = g.matmul(h1, wqkv);
+    int att = -1;
+    for (size_t b = 0; b < B; ++b) {
+      const int xb = g.matmul(rsel[b], qkv);
+      int ob = -1;
+      for (size_t h = 0; h < H; ++h) {
+        const int q = rope(g.matmul(xb, qsel[h])), k = rope(g.matmul(xb, ksel[h])), v = g.matmul(xb, vsel[h]);
+        const int s2 = g.add(g.smul(g.matmul(q, k, false, true), sc), maskn);
+        const int o = g.matmul(g.softmax_rows(s2), v);
+        const int oh = g.matmul(o, place[h]);
+        ob = ob < 0 ? oh : g.add(ob, oh);
+      }
+      const int back = g.matmul(rsel[b], ob, true, false);
+      att = att < 0 ? back : g.add(att, back);
+    }
+    x = g.add(x, g.matmul(att, wo));
+    const int h2 = rmsnorm(g, x, g2, T, d, c.ln_eps);
+    const int fu = g.matmul(h2, wgu);
+    const int a = g.mul(silu(g, g.matmul(fu, gseln)), g.matmul(fu, useln));
+    x = g.add(x, g.matmul(a, wd));
+  }
+  const int gf = out.params[pi++], head = out.params[pi++];
+  const int hf = rmsnorm(g, x, gf, T, d, c.ln_eps);
+  const int logits = g.matmul(hf, head, false, true);
   out.loss = g.cross_entropy(logits, g.constant(tgt));
   return out;
 }

@@ -226,6 +226,8 @@ class Graph {
 struct GptConfig {
   size_t n_layer = 1, d = 64, n_head = 4, ff = 256, vocab = 64, ctx = 32;
   double ln_eps = 1e-5;
+  int arch = 0;              // 0: GPT-2 block; 1: Llama-style (RMSNorm, RoPE, SwiGLU, untied head, no biases)
+  double rope_base = 10000.0;
 };
 struct ParamSlot {
   std::string name;

@@ -48,6 +48,23 @@ std::vector<Slot> layout(const sd_gpt_config& c) {
     s.push_back({off, r, cc, k});
     off += r * cc;
   };
+  if (c.arch == SD_ARCH_LLAMA) {
+    // oracle/src/models.cpp gpt_layout (arch 1): tok_embeddings, per layer
+    // [attention_norm, wqkv [d][3d], wo, ffn_norm, w_gate_up [d][2ff], w_down],
+    // norm, output [V][d]
+    add(c.vocab, c.d, 0);
+    for (int l = 0; l < c.n_layer; ++l) {
+      add(1, c.d, 1);
+      add(c.d, 3 * c.d, 0);
+      add(c.d, c.d, 0);
+      add(1, c.d, 1);
+      add(c.d, 2 * c.ff, 0);
+      add(c.ff, c.d, 0);
+    }
+    add(1, c.d, 1);
+    add(c.vocab, c.d, 0);
+    return s;
+  }
   add(c.vocab, c.d, 0);
   add(c.ctx, c.d, 0);
   for (int l = 0; l < c.n_layer; ++l) {
@@ -82,6 +99,8 @@ void check_cfg(const sd_gpt_config& c, int B, int S) {
   if (B < 1 || S < 1) fail(SD_ARGUMENT_ERROR, "empty batch");
   if (S > c.ctx) fail(SD_ARGUMENT_ERROR, "sequence longer than context");
   if (S % 4) fail(SD_CONFIG_ERROR, "sequence length must be a multiple of 4");
+  if (c.arch != SD_ARCH_GPT2 && c.arch != SD_ARCH_LLAMA) fail(SD_CONFIG_ERROR, "unknown architecture");
+  if (c.arch == SD_ARCH_LLAMA && !(c.rope_base > 1.0f)) fail(SD_CONFIG_ERROR, "rope_base must exceed 1");
 }
 
 struct Layer {
@@ -120,6 +139,7 @@ struct sd_gpt_s {
   float *gx, *gdx, *gxs, *gdxs, *gh, *ghs, *gdh, *gdhs;
   float *go, *gos, *gdo, *gdos, *ga, *gas, *gda, *gdas;
   float *gP, *gPs, *gdP, *gdPs, *gu, *gus, *gdu, *gdus;
+  float *ga_mlp = nullptr, *gda_mlp = nullptr;
   double* loss_rows = nullptr;
   float* red = nullptr;  // column-reduction scratch
   int *tok = nullptr, *tgt = nullptr, *uniq = nullptr, *ustart = nullptr, *upos = nullptr;
@@ -129,7 +149,7 @@ struct sd_gpt_s {
   std::vector<double> h_loss;
 
   void carve(Plan& p) {
-    const long long T_ = T, d = c.d, ff = c.ff;
+    const long long T_ = T, d = c.d, ff = c.ff, ffw = c.arch == SD_ARCH_LLAMA ? 2 * ff : ff;
     auto td = [&] { return p.take<float>(T_ * d); };
     L.resize(c.n_layer);
     for (auto& l : L) {
@@ -142,7 +162,8 @@ struct sd_gpt_s {
       l.o = td(), l.os = td(), l.dO = td(), l.dOs = td();
       l.xh2 = td(), l.dxh2 = td(), l.h2 = td(), l.h2s = td(), l.dh2 = td(), l.dh2s = td();
       l.r2 = p.take<float>(T_), l.dr2 = p.take<float>(T_);
-      l.f = p.take<float>(T_ * ff), l.df = p.take<float>(T_ * ff);
+      // GPT-2: MLP pre-activation [T, ff]; Llama: [gate | up] pre-activations [T, 2ff]
+      l.f = p.take<float>(T_ * ffw), l.df = p.take<float>(T_ * ffw);
       l.u = p.take<float>(T_ * ff), l.us = p.take<float>(T_ * ff);
       l.du = p.take<float>(T_ * ff), l.dus = p.take<float>(T_ * ff);
     }
@@ -155,7 +176,11 @@ struct sd_gpt_s {
     ga = p.take<float>(T_ * 3 * d), gas = p.take<float>(T_ * 3 * d);
     gda = p.take<float>(T_ * 3 * d), gdas = p.take<float>(T_ * 3 * d);
     gP = p.take<float>(BHSS), gPs = nullptr, gdP = p.take<float>(BHSS), gdPs = nullptr;
-    gu = p.take<float>(T_ * ff), gus = p.take<float>(T_ * ff), gdu = p.take<float>(T_ * ff), gdus = p.take<float>(T_ * ff);
+    gu = p.take<float>(T_ * ffw), gus = p.take<float>(T_ * ffw), gdu = p.take<float>(T_ * ffw),
+    gdus = p.take<float>(T_ * ffw);
+    if (c.arch == SD_ARCH_LLAMA) {  // adjoint (+ tangent) of the SwiGLU output [T, ff]
+      ga_mlp = p.take<float>(T_ * ff), gda_mlp = p.take<float>(T_ * ff);
+    }
     theta_s = p.take<float>(P), v_s = p.take<float>(P);
     loss_rows = p.take<double>(T_);
     red = p.take<float>(2LL * 64 * std::max(3 * d, ff));
@@ -223,6 +248,7 @@ struct sd_gpt_s {
 
   void hvp(const float* v, float* hv, cudaStream_t st) {
     if (!have_batch) fail(SD_STATE_ERROR, "gpt: set_batch was not called");
+    if (c.arch == SD_ARCH_LLAMA) return hvp_llama(v, hv, st);
     const int d = c.d, ff = c.ff, V = c.vocab;
     const long long Td = (long long)T * d;
     const float sc = 1.0f / std::sqrt(float(dh));
@@ -320,6 +346,105 @@ struct sd_gpt_s {
     // embeddings (wte also carries the head contribution written above)
     SD_CUDA(cudaMemsetAsync(HV(1), 0, slots[1].rows * slots[1].cols * sizeof(float), st));
     sd::gpt_embed_bwd(uniq, ustart, upos, n_uniq, B, S, d, gdx, HV(0), HV(1), st);
+  }
+
+  // Llama-style decoder (oracle/src/models.cpp build_llama): same forward-over-
+  // reverse scheme as hvp(); RMSNorm via the LN kernels' rms mode, RoPE on q/k
+  // after the fused QKV product (inverse rotation on their adjoints), SwiGLU on
+  // the fused [gate | up] product, untied head, no biases.
+  void hvp_llama(const float* v, float* hv, cudaStream_t st) {
+    const int d = c.d, ff = c.ff, V = c.vocab;
+    const long long Td = (long long)T * d;
+    const float sc = 1.0f / std::sqrt(float(dh)), eps = 1e-5f;
+    auto V_ = [&](int i) { return v + slots[i].off; };
+    auto Vs = [&](int i) { return v_s + slots[i].off; };
+    auto HV = [&](int i) { return hv + slots[i].off; };
+    const int fL = 1 + 6 * c.n_layer, head = fL + 1;  // final norm, output head
+    sd::gpt_residual(v, v_s, P, st);
+    // ------------------------------------------------------------ forward
+    sd::gpt_embed(tok, T, S, d, th(0), nullptr, V_(0), nullptr, x, dx, st);
+    for (int l = 0; l < c.n_layer; ++l) {
+      Layer& Ly = L[l];
+      const int b = 1 + 6 * l;  // attention_norm
+      sd::LnArgs la{x, dx, th(b), nullptr, V_(b), nullptr, T, d, eps,
+                    Ly.h1, Ly.h1s, Ly.dh1, Ly.dh1s, Ly.xh1, Ly.dxh1, Ly.r1, Ly.dr1, 1};
+      sd::gpt_ln_fwd(la, st);
+      mm(T, 3 * d, d, {Ly.h1, Ly.h1s, d, false}, {th(b + 1), ths(b + 1), 3 * d, true}, Ly.a, 3 * d, 1, 0, st,
+         nullptr, Ly.as);
+      mm2(T, 3 * d, d, {Ly.dh1, Ly.dh1s, d, false}, {th(b + 1), ths(b + 1), 3 * d, true}, {Ly.h1, Ly.h1s, d, false},
+          {V_(b + 1), Vs(b + 1), 3 * d, true}, Ly.da, 3 * d, 1, 0, st, nullptr, Ly.das);
+      sd::llama_rope(Ly.a, Ly.as, Ly.da, Ly.das, T, S, d, dh, c.rope_base, 0, st);
+      attention_fwd(Ly, sc, st);
+      mm(T, d, d, {Ly.o, Ly.os, d, false}, {th(b + 2), ths(b + 2), d, true}, x, d, 1, 1, st);
+      mm2(T, d, d, {Ly.dO, Ly.dOs, d, false}, {th(b + 2), ths(b + 2), d, true}, {Ly.o, Ly.os, d, false},
+          {V_(b + 2), Vs(b + 2), d, true}, dx, d, 1, 1, st);
+      sd::LnArgs lb{x, dx, th(b + 3), nullptr, V_(b + 3), nullptr, T, d, eps,
+                    Ly.h2, Ly.h2s, Ly.dh2, Ly.dh2s, Ly.xh2, Ly.dxh2, Ly.r2, Ly.dr2, 1};
+      sd::gpt_ln_fwd(lb, st);
+      mm(T, 2 * ff, d, {Ly.h2, Ly.h2s, d, false}, {th(b + 4), ths(b + 4), 2 * ff, true}, Ly.f, 2 * ff, 1, 0, st);
+      mm2(T, 2 * ff, d, {Ly.dh2, Ly.dh2s, d, false}, {th(b + 4), ths(b + 4), 2 * ff, true},
+          {Ly.h2, Ly.h2s, d, false}, {V_(b + 4), Vs(b + 4), 2 * ff, true}, Ly.df, 2 * ff, 1, 0, st);
+      sd::llama_swiglu_fwd(Ly.f, Ly.df, Ly.u, Ly.us, Ly.du, Ly.dus, T, ff, st);
+      mm(T, d, ff, {Ly.u, Ly.us, ff, false}, {th(b + 5), ths(b + 5), d, true}, x, d, 1, 1, st);
+      mm2(T, d, ff, {Ly.du, Ly.dus, ff, false}, {th(b + 5), ths(b + 5), d, true}, {Ly.u, Ly.us, ff, false},
+          {V_(b + 5), Vs(b + 5), d, true}, dx, d, 1, 1, st);
+    }
+    sd::LnArgs lf{x, dx, th(fL), nullptr, V_(fL), nullptr, T, d, eps, hf, hfs, dhf, dhfs, xhf, dxhf, rf, drf, 1};
+    sd::gpt_ln_fwd(lf, st);
+    // logits z = hf W_out^T ; dz = dhf W_out^T + hf VW_out^T
+    mm(T, V, d, {hf, hfs, d, false}, {th(head), ths(head), d, false}, z, Vp, 1, 0, st);
+    mm2(T, V, d, {dhf, dhfs, d, false}, {th(head), ths(head), d, false}, {hf, hfs, d, false},
+        {V_(head), Vs(head), d, false}, dz, Vp, 1, 0, st);
+    sd::gpt_ce(z, dz, zs, dzs, tgt, T, V, Vp, loss_scale, loss_rows, st);
+    // ----------------------------------------------------------- backward
+    mm(T, d, V, {z, zs, Vp, false}, {th(head), ths(head), d, true}, gh, d, 1, 0, st);
+    mm2(T, d, V, {dz, dzs, Vp, false}, {th(head), ths(head), d, true}, {z, zs, Vp, false},
+        {V_(head), Vs(head), d, true}, gdh, d, 1, 0, st);
+    mm2(V, d, T, {dz, dzs, Vp, true}, {hf, hfs, d, true}, {z, zs, Vp, true}, {dhf, dhfs, d, true}, HV(head), d, 1, 0,
+        st);
+    SD_CUDA(cudaMemsetAsync(gx, 0, Td * sizeof(float), st));
+    SD_CUDA(cudaMemsetAsync(gdx, 0, Td * sizeof(float), st));
+    sd::LnBwdArgs bf{gh, gdh, th(fL), V_(fL), xhf, dxhf, rf, drf, T, d, gx, gdx, gxs, gdxs, HV(fL), nullptr, red, 1};
+    sd::gpt_ln_bwd(bf, st);
+    for (int l = c.n_layer - 1; l >= 0; --l) {
+      Layer& Ly = L[l];
+      const int b = 1 + 6 * l;
+      // down projection: ga = gx Wd^T ; gda = gdx Wd^T + gx VWd^T ; Hv_Wd = da^T gx + a^T gdx
+      mm(T, ff, d, {gx, gxs, d, false}, {th(b + 5), ths(b + 5), d, false}, ga_mlp, ff, 1, 0, st);
+      mm2(T, ff, d, {gdx, gdxs, d, false}, {th(b + 5), ths(b + 5), d, false}, {gx, gxs, d, false},
+          {V_(b + 5), Vs(b + 5), d, false}, gda_mlp, ff, 1, 0, st);
+      mm2(ff, d, T, {Ly.du, Ly.dus, ff, true}, {gx, gxs, d, true}, {Ly.u, Ly.us, ff, true}, {gdx, gdxs, d, true},
+          HV(b + 5), d, 1, 0, st);
+      sd::llama_swiglu_bwd(Ly.f, Ly.df, ga_mlp, gda_mlp, gu, gus, gdu, gdus, T, ff, st);
+      // gate|up: gh = gfu Wgu^T ; gdh = gdfu Wgu^T + gfu VWgu^T ; Hv_Wgu = dh2^T gfu + h2^T gdfu
+      mm(T, d, 2 * ff, {gu, gus, 2 * ff, false}, {th(b + 4), ths(b + 4), 2 * ff, false}, gh, d, 1, 0, st);
+      mm2(T, d, 2 * ff, {gdu, gdus, 2 * ff, false}, {th(b + 4), ths(b + 4), 2 * ff, false},
+          {gu, gus, 2 * ff, false}, {V_(b + 4), Vs(b + 4), 2 * ff, false}, gdh, d, 1, 0, st);
+      mm2(d, 2 * ff, T, {Ly.dh2, Ly.dh2s, d, true}, {gu, gus, 2 * ff, true}, {Ly.h2, Ly.h2s, d, true},
+          {gdu, gdus, 2 * ff, true}, HV(b + 4), 2 * ff, 1, 0, st);
+      sd::LnBwdArgs b2{gh, gdh, th(b + 3), V_(b + 3), Ly.xh2, Ly.dxh2, Ly.r2, Ly.dr2, T, d,
+                       gx, gdx, gxs, gdxs, HV(b + 3), nullptr, red, 1};
+      sd::gpt_ln_bwd(b2, st);
+      // attention output projection
+      mm(T, d, d, {gx, gxs, d, false}, {th(b + 2), ths(b + 2), d, false}, go, d, 1, 0, st, nullptr, gos);
+      mm2(T, d, d, {gdx, gdxs, d, false}, {th(b + 2), ths(b + 2), d, false}, {gx, gxs, d, false},
+          {V_(b + 2), Vs(b + 2), d, false}, gdo, d, 1, 0, st, nullptr, gdos);
+      mm2(d, d, T, {Ly.dO, Ly.dOs, d, true}, {gx, gxs, d, true}, {Ly.o, Ly.os, d, true}, {gdx, gdxs, d, true},
+          HV(b + 2), d, 1, 0, st);
+      attention_bwd(Ly, sc, st);
+      // adjoints of the pre-rotation q, k: the inverse rotation
+      sd::llama_rope(ga, gas, gda, gdas, T, S, d, dh, c.rope_base, 1, st);
+      mm(T, d, 3 * d, {ga, gas, 3 * d, false}, {th(b + 1), ths(b + 1), 3 * d, false}, gh, d, 1, 0, st);
+      mm2(T, d, 3 * d, {gda, gdas, 3 * d, false}, {th(b + 1), ths(b + 1), 3 * d, false}, {ga, gas, 3 * d, false},
+          {V_(b + 1), Vs(b + 1), 3 * d, false}, gdh, d, 1, 0, st);
+      mm2(d, 3 * d, T, {Ly.dh1, Ly.dh1s, d, true}, {ga, gas, 3 * d, true}, {Ly.h1, Ly.h1s, d, true},
+          {gda, gdas, 3 * d, true}, HV(b + 1), 3 * d, 1, 0, st);
+      sd::LnBwdArgs b1{gh, gdh, th(b), V_(b), Ly.xh1, Ly.dxh1, Ly.r1, Ly.dr1, T, d,
+                       gx, gdx, gxs, gdxs, HV(b), nullptr, red, 1};
+      sd::gpt_ln_bwd(b1, st);
+    }
+    SD_CUDA(cudaMemsetAsync(HV(0), 0, slots[0].rows * slots[0].cols * sizeof(float), st));
+    sd::gpt_embed_bwd(uniq, ustart, upos, n_uniq, B, S, d, gdx, HV(0), nullptr, st);
   }
 
   // per (batch b, head h): S = sc q k^T ; dS = sc (dq k^T + q dk^T) ; P, dP = softmax R-op ;

@@ -10,6 +10,7 @@ struct LnArgs {
   int T, d;
   float eps;
   float *h, *hs, *dh, *dhs, *xh, *dxh, *r, *dr;
+  int rms = 0;  // RMSNorm: no centring, no bias (b, vb null)
 };
 struct LnBwdArgs {
   const float *gy, *gdy, *g, *vg, *xh, *dxh, *r, *dr;
@@ -17,10 +18,21 @@ struct LnBwdArgs {
   float *gx, *gdx, *gxs, *gdxs;
   float *hv_g, *hv_b;
   float* scratch;  // >= 2 * 64 * d floats
+  int rms = 0;
 };
 
 void gpt_embed(const int* tok, int T, int S, int d, const float* wte, const float* wpe, const float* vwte,
                const float* vwpe, float* x, float* dx, cudaStream_t s);
+// RoPE (rotate-half) on the q and k parts of a [T, 3d] q|k|v buffer and its
+// tangent, in place (inverse = backward adjoint); residuals rewritten.
+void llama_rope(float* a, float* as, float* da, float* das, int T, int S, int d, int dh, float base, int inverse,
+                cudaStream_t s);
+// SwiGLU: fu = [gate | up] [T, 2ff] -> a = silu(gate) * up (and tangent, residuals)
+void llama_swiglu_fwd(const float* fu, const float* dfu, float* a, float* as, float* da, float* das, int T, int ff,
+                      cudaStream_t s);
+// adjoints of [gate | up] from ga (and tangents), residuals
+void llama_swiglu_bwd(const float* fu, const float* dfu, const float* ga, const float* gda, float* gfu, float* gfus,
+                      float* gdfu, float* gdfus, int T, int ff, cudaStream_t s);
 void gpt_ln_fwd(const LnArgs& a, cudaStream_t s);
 void gpt_ln_bwd(const LnBwdArgs& a, cudaStream_t s);
 void gpt_colsum(const float* a, int T, int n, long long lda, float* out, float* scratch, cudaStream_t s);

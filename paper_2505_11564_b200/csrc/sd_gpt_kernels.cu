@@ -66,8 +66,8 @@ __global__ void k_embed(const int* __restrict__ tok, int S, int d, const float* 
   const int e = int(i - t * d);
   const int s = int(t % S);
   const long long tk = tok[t];
-  x[i] = wte[tk * d + e] + wpe[(long long)s * d + e];
-  dx[i] = vwte[tk * d + e] + vwpe[(long long)s * d + e];
+  x[i] = wte[tk * d + e] + (wpe ? wpe[(long long)s * d + e] : 0.f);
+  dx[i] = vwte[tk * d + e] + (vwpe ? vwpe[(long long)s * d + e] : 0.f);
 }
 
 // ------------------------------------------------------------- LayerNorm
@@ -78,18 +78,21 @@ __global__ void k_ln_fwd(const float* __restrict__ x, const float* __restrict__ 
                          const float* __restrict__ b, const float* __restrict__ vg, const float* __restrict__ vb,
                          int T, int d, float eps, float* __restrict__ h, float* __restrict__ hs,
                          float* __restrict__ dh, float* __restrict__ dhs, float* __restrict__ xh,
-                         float* __restrict__ dxh, float* __restrict__ r_out, float* __restrict__ dr_out) {
+                         float* __restrict__ dxh, float* __restrict__ r_out, float* __restrict__ dr_out, int rms) {
   const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= T) return;
   const float* xr = x + (long long)row * d;
   const float* dxr = dx + (long long)row * d;
-  float s = 0.f, ds = 0.f;
-  for (int e = lane; e < d; e += 32) {
-    s += xr[e];
-    ds += dxr[e];
+  float mu = 0.f, dmu = 0.f;  // RMSNorm: no centring
+  if (!rms) {
+    float s = 0.f, ds = 0.f;
+    for (int e = lane; e < d; e += 32) {
+      s += xr[e];
+      ds += dxr[e];
+    }
+    mu = warp_sum(s) / d, dmu = warp_sum(ds) / d;
   }
-  const float mu = warp_sum(s) / d, dmu = warp_sum(ds) / d;
   float v = 0.f;
   for (int e = lane; e < d; e += 32) {
     const float c = xr[e] - mu;
@@ -104,8 +107,8 @@ __global__ void k_ln_fwd(const float* __restrict__ x, const float* __restrict__ 
   for (int e = lane; e < d; e += 32) {
     const float xhv = (xr[e] - mu) * r;
     const float dxhv = r * (dxr[e] - dmu - xhv * mxd);
-    const float hv = g[e] * xhv + b[e];
-    const float dhv = vg[e] * xhv + g[e] * dxhv + vb[e];
+    const float hv = g[e] * xhv + (b ? b[e] : 0.f);
+    const float dhv = vg[e] * xhv + g[e] * dxhv + (vb ? vb[e] : 0.f);
     xh[o + e] = xhv;
     dxh[o + e] = dxhv;
     h[o + e] = hv;
@@ -128,7 +131,7 @@ __global__ void k_ln_bwd(const float* __restrict__ gy, const float* __restrict__
                          const float* __restrict__ vg, const float* __restrict__ xh, const float* __restrict__ dxh,
                          const float* __restrict__ rr, const float* __restrict__ drr, int T, int d,
                          float* __restrict__ gx, float* __restrict__ gdx, float* __restrict__ gxs,
-                         float* __restrict__ gdxs) {
+                         float* __restrict__ gdxs, int rms) {
   const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= T) return;
@@ -143,7 +146,7 @@ __global__ void k_ln_bwd(const float* __restrict__ gy, const float* __restrict__
     s4 += gdq * xh[o + e];
     s5 += gq * dxh[o + e];
   }
-  const float m_g = warp_sum(s1) / d, m_gx = warp_sum(s2) / d, m_d = warp_sum(s3) / d;
+  const float m_g = rms ? 0.f : warp_sum(s1) / d, m_gx = warp_sum(s2) / d, m_d = rms ? 0.f : warp_sum(s3) / d;
   const float m_dx = warp_sum(s4) / d, m_gdx = warp_sum(s5) / d;
   const float r = rr[row], dr = drr[row];
   for (int e = lane; e < d; e += 32) {
@@ -402,6 +405,85 @@ __global__ void __launch_bounds__(256) k_ce(float* __restrict__ z, float* __rest
   }
 }
 
+// ------------------------------------------------------------------ RoPE
+// Pair (i, i + dh/2) of every q and k head at position p = t % S rotates by
+// p * base^(-2i/dh) (rotate-half convention); f64 angle and rotation, one
+// rounding per stored value. inverse: the transpose (backward adjoint).
+__global__ void k_rope(float* __restrict__ a, float* __restrict__ as, float* __restrict__ da, float* __restrict__ das,
+                       int T, int S, int d, int dh, float base, int inverse) {
+  const int half = dh / 2;
+  const long long n = (long long)T * 2 * (d / 2);  // (t, q|k, head, i) pairs
+  const long long id = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (id >= n) return;
+  const int per_t = d;                             // 2 parts x H heads x half pairs = d
+  const long long t = id / per_t;
+  const int rem = int(id % per_t);
+  const int part = rem / (d / 2), hp = rem % (d / 2);
+  const int h = hp / half, i = hp % half;
+  const int p = int(t % S);
+  const double theta = pow(double(base), -2.0 * double(i) / double(dh));
+  double sn, cs;
+  sincos(double(p) * theta, &sn, &cs);
+  if (inverse) sn = -sn;
+  const long long o = t * 3LL * d + (long long)part * d + (long long)h * dh + i;
+  const double x1 = a[o], x2 = a[o + half];
+  const float y1 = float(x1 * cs - x2 * sn), y2 = float(x2 * cs + x1 * sn);
+  a[o] = y1;
+  a[o + half] = y2;
+  if (as) as[o] = tf32_res(y1), as[o + half] = tf32_res(y2);
+  const double u1 = da[o], u2 = da[o + half];
+  const float w1 = float(u1 * cs - u2 * sn), w2 = float(u2 * cs + u1 * sn);
+  da[o] = w1;
+  da[o + half] = w2;
+  if (das) das[o] = tf32_res(w1), das[o + half] = tf32_res(w2);
+}
+
+// --------------------------------------------------------------- SwiGLU
+// s = silu(f) = f sig(f); s1 = silu'(f); s2 = silu''(f); a = s u.
+__device__ __forceinline__ void silu_derivs(double f, double& s, double& s1, double& s2) {
+  const double sg = 1.0 / (1.0 + exp(-f));
+  s = f * sg;
+  s1 = sg * (1.0 + f * (1.0 - sg));
+  s2 = sg * (1.0 - sg) * (2.0 + f * (1.0 - 2.0 * sg));
+}
+__global__ void k_swiglu_fwd(const float* __restrict__ fu, const float* __restrict__ dfu, float* __restrict__ a,
+                             float* __restrict__ as, float* __restrict__ da, float* __restrict__ das, int ff,
+                             long long n) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const long long t = i / ff;
+  const int e = int(i % ff);
+  const long long og = t * 2LL * ff + e, ou = og + ff;
+  double s, s1, s2;
+  silu_derivs(fu[og], s, s1, s2);
+  const double u = fu[ou];
+  const float av = float(s * u);
+  const float dv = float(s1 * double(dfu[og]) * u + s * double(dfu[ou]));
+  a[i] = av, as[i] = tf32_res(av);
+  da[i] = dv, das[i] = tf32_res(dv);
+}
+//   g_up = ga s ; g_gate = ga u s1
+//   gd_up = gda s + ga s1 df ; gd_gate = gda u s1 + ga du s1 + ga u s2 df
+__global__ void k_swiglu_bwd(const float* __restrict__ fu, const float* __restrict__ dfu, const float* __restrict__ ga,
+                             const float* __restrict__ gda, float* __restrict__ gfu, float* __restrict__ gfus,
+                             float* __restrict__ gdfu, float* __restrict__ gdfus, int ff, long long n) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const long long t = i / ff;
+  const int e = int(i % ff);
+  const long long og = t * 2LL * ff + e, ou = og + ff;
+  double s, s1, s2;
+  silu_derivs(fu[og], s, s1, s2);
+  const double u = fu[ou], df = dfu[og], du = dfu[ou], g = ga[i], gd = gda[i];
+  const float gu = float(g * s), gg = float(g * u * s1);
+  const float gdu = float(gd * s + g * s1 * df);
+  const float gdg = float(gd * u * s1 + g * du * s1 + g * u * s2 * df);
+  gfu[og] = gg, gfu[ou] = gu;
+  gfus[og] = tf32_res(gg), gfus[ou] = tf32_res(gu);
+  gdfu[og] = gdg, gdfu[ou] = gdu;
+  gdfus[og] = tf32_res(gdg), gdfus[ou] = tf32_res(gdu);
+}
+
 // ------------------------------------------------------ embedding backward
 // Hv_wte[v] += sum over positions with token v of gdx (CSR by token, fixed
 // order), one warp per (token, 32-column slab). Hv_wpe[s] = sum_b gdx[b,s].
@@ -468,13 +550,13 @@ void gpt_embed(const int* tok, int T, int S, int d, const float* wte, const floa
 
 void gpt_ln_fwd(const LnArgs& a, cudaStream_t s) {
   k_ln_fwd<<<g1(a.T, 8), 256, 0, s>>>(a.x, a.dx, a.g, a.b, a.vg, a.vb, a.T, a.d, a.eps, a.h, a.hs, a.dh, a.dhs, a.xh,
-                                      a.dxh, a.r, a.dr);
+                                      a.dxh, a.r, a.dr, a.rms);
   SD_LAUNCHED("k_ln_fwd");
 }
 
 void gpt_ln_bwd(const LnBwdArgs& a, cudaStream_t s) {
   k_ln_bwd<<<g1(a.T, 8), 256, 0, s>>>(a.gy, a.gdy, a.g, a.vg, a.xh, a.dxh, a.r, a.dr, a.T, a.d, a.gx, a.gdx, a.gxs,
-                                      a.gdxs);
+                                      a.gdxs, a.rms);
   SD_LAUNCHED("k_ln_bwd");
   const int groups = std::min(kRowGroups, std::max(1, a.T / 64));
   k_colred1<1><<<dim3(unsigned((a.d + 31) / 32), unsigned(groups)), 256, 0, s>>>(a.gy, a.gdy, a.xh, a.dxh, a.T, a.d,
@@ -529,8 +611,31 @@ void gpt_embed_bwd(const int* uniq, const int* start, const int* pos, int n_uniq
     k_embed_bwd_wte<<<g1(warps, 8), 256, 0, s>>>(uniq, start, pos, n_uniq, d, gdx, hv_wte);
     SD_LAUNCHED("k_embed_bwd_wte");
   }
-  k_embed_bwd_wpe<<<g1((long long)S * d), 256, 0, s>>>(gdx, B, S, d, hv_wpe);
-  SD_LAUNCHED("k_embed_bwd_wpe");
+  if (hv_wpe) {
+    k_embed_bwd_wpe<<<g1((long long)S * d), 256, 0, s>>>(gdx, B, S, d, hv_wpe);
+    SD_LAUNCHED("k_embed_bwd_wpe");
+  }
+}
+
+void llama_rope(float* a, float* as, float* da, float* das, int T, int S, int d, int dh, float base, int inverse,
+                cudaStream_t s) {
+  const long long n = (long long)T * d;
+  k_rope<<<g1(n), 256, 0, s>>>(a, as, da, das, T, S, d, dh, base, inverse);
+  SD_LAUNCHED("k_rope");
+}
+
+void llama_swiglu_fwd(const float* fu, const float* dfu, float* a, float* as, float* da, float* das, int T, int ff,
+                      cudaStream_t s) {
+  const long long n = (long long)T * ff;
+  k_swiglu_fwd<<<g1(n), 256, 0, s>>>(fu, dfu, a, as, da, das, ff, n);
+  SD_LAUNCHED("k_swiglu_fwd");
+}
+
+void llama_swiglu_bwd(const float* fu, const float* dfu, const float* ga, const float* gda, float* gfu, float* gfus,
+                      float* gdfu, float* gdfus, int T, int ff, cudaStream_t s) {
+  const long long n = (long long)T * ff;
+  k_swiglu_bwd<<<g1(n), 256, 0, s>>>(fu, dfu, ga, gda, gfu, gfus, gdfu, gdfus, ff, n);
+  SD_LAUNCHED("k_swiglu_bwd");
 }
 
 void gpt_residual(const float* x, float* xs, long long n, cudaStream_t s) {

@@ -127,3 +127,63 @@ def test_c3_shape_runs_and_is_symmetric():
     lin = 0.5 * hu.double() - 2.0 * hw.double()
     assert float((hs.double() - lin).norm() / lin.norm()) < 1e-5
     eng.close()
+
+
+LTINY = dict(n_layer=2, d=64, n_head=4, ff=96, vocab=96, ctx=32, arch=1, rope_base=10000)
+
+
+def test_llama_layout_matches_oracle(sd, oracle):
+    from paper_2505_11564_b200 import gpt
+    for cfg in (LTINY, gpt.LLAMA2_7B):
+        assert gpt.param_count(cfg) == oracle.gpt_param_count(cfg)
+    assert gpt.param_count(gpt.LLAMA2_7B) == 6738415616  # Llama-2-7B parameter count
+    assert gpt.param_layout(LTINY) == oracle.gpt_layout(LTINY)
+
+
+@pytest.mark.parametrize("cfg,B,S", [(LTINY, 2, 32), (dict(LTINY, n_layer=1, n_head=2, d=32, ff=40), 3, 16)])
+def test_llama_hvp_vs_oracle(sd, oracle, cfg, B, S):
+    # Llama-style decoder (RMSNorm, RoPE, SwiGLU, untied head; BASELINE C4/C5 family)
+    from paper_2505_11564_b200 import gpt
+    eng = gpt.GptHvp(cfg, B, S, init_seed=0, gain_scale=0.1, bias_scale=0.1)
+    th = eng.theta_numpy()
+    assert np.array_equal(th, oracle.gpt_init(cfg, 0, 0.1, 0.1, prec=0))
+    tok, tgt = eng.tokens_numpy()
+    for seed in (3, 4):
+        v = oracle.draw_probe(eng.P, seed, 1, prec=0)
+        hv = eng.hvp_numpy(v)
+        ref = oracle.gpt_hvp(cfg, th, tok, tgt, B, S, v)
+        assert rel(hv, ref) < TOL, rel(hv, ref)
+    assert abs(eng.loss() - oracle.gpt_loss(cfg, th, tok, tgt, B, S)) < 1e-5
+
+
+def test_llama_finite_differences_and_symmetry(sd, oracle):
+    from paper_2505_11564_b200 import gpt
+    cfg, B, S = LTINY, 2, 32
+    eng = gpt.GptHvp(cfg, B, S, init_seed=1, gain_scale=0.1)
+    th = eng.theta_numpy()
+    tok, tgt = eng.tokens_numpy()
+    rng = np.random.default_rng(1)
+    v = rng.standard_normal(eng.P).astype(np.float32).astype(np.float64)
+    hv = eng.hvp_numpy(v)
+    e = 1e-5
+    fd = (oracle.gpt_grad(cfg, th + e * v, tok, tgt, B, S) - oracle.gpt_grad(cfg, th - e * v, tok, tgt, B, S)) / (2 * e)
+    assert rel(hv, fd) < 2e-5
+    u = rng.standard_normal(eng.P).astype(np.float32).astype(np.float64)
+    hu = eng.hvp_numpy(u)
+    assert abs(hu @ v - u @ hv) <= 1e-5 * np.linalg.norm(hu) * np.linalg.norm(v)
+
+
+def test_llama2_7b_layer_shape_runs():
+    # two decoder layers of the Llama-2-7B shape (d4096, ff11008, 32 heads, V32000)
+    # at 1 x 1024 tokens: finite, symmetric Hv through the Lanczos-facing operator
+    from paper_2505_11564_b200 import gpt
+    cfg = dict(gpt.LLAMA2_7B, n_layer=2)
+    eng = gpt.GptHvp(cfg, 1, 1024)
+    g = torch.Generator(device="cuda").manual_seed(0)
+    u = torch.randn(eng.P, device="cuda", generator=g) * 1e-3
+    w = torch.randn(eng.P, device="cuda", generator=g) * 1e-3
+    hu, hw = eng.hvp(u), eng.hvp(w)
+    assert bool(torch.isfinite(hu).all()) and bool(torch.isfinite(hw).all())
+    a, b = float(torch.dot(hu.double(), w.double())), float(torch.dot(u.double(), hw.double()))
+    assert abs(a - b) <= 1e-4 * max(abs(a), abs(b))
+    eng.close()
