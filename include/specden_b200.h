@@ -203,6 +203,7 @@ typedef struct {
   int arch;        /* SD_ARCH_GPT2 (pre-LN, biases, GELU, learned positions, tied head) or
                       SD_ARCH_LLAMA (RMSNorm, RoPE, SwiGLU, no biases, untied head) */
   float rope_base; /* RoPE base (SD_ARCH_LLAMA), e.g. 10000 */
+  int n_kv_head;   /* SD_ARCH_LLAMA grouped-query attention: key/value heads (0 = n_head) */
 } sd_gpt_config;
 enum { SD_ARCH_GPT2 = 0, SD_ARCH_LLAMA = 1 };
 typedef struct sd_gpt_s* sd_gpt;

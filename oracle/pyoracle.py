@@ -240,7 +240,7 @@ class Oracle:
     @staticmethod
     def _cfg(cfg) -> np.ndarray:
         return np.array([cfg["n_layer"], cfg["d"], cfg["n_head"], cfg["ff"], cfg["vocab"], cfg["ctx"],
-                         cfg.get("arch", 0), cfg.get("rope_base", 10000)], np.int64)
+                         cfg.get("arch", 0), cfg.get("rope_base", 10000), cfg.get("n_kv_head", 0)], np.int64)
 
     def gpt_param_count(self, cfg) -> int:
         c = self._cfg(cfg)

@@ -32,6 +32,7 @@ static GptConfig gcfg(const long long* c) {
   g.ctx = size_t(c[5]);
   g.arch = int(c[6]);
   g.rope_base = double(c[7]);
+  g.n_kv_head = size_t(c[8]);
   return g;
 }
 

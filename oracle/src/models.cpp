@@ -22,7 +22,8 @@ std::vector<ParamSlot> gpt_layout(const GptConfig& c) {
     for (size_t l = 0; l < c.n_layer; ++l) {
       const std::string p = "layers." + std::to_string(l) + ".";
       add(p + "attention_norm.weight", 1, c.d, 1);
-      add(p + "attention.wqkv", c.d, 3 * c.d, 0);
+      const size_t kvd = (c.n_kv_head ? c.n_kv_head : c.n_head) * (c.d / c.n_head);
+      add(p + "attention.wqkv", c.d, c.d + 2 * kvd, 0);
       add(p + "attention.wo", c.d, c.d, 0);
       add(p + "ffn_norm.weight", 1, c.d, 1);
       add(p + "feed_forward.w_gate_up", c.d, 2 * c.ff, 0);
@@ -247,13 +248,18 @@ GptNodes build_llama(Graph& g, const GptConfig& c, const std::vector<double>& th
     for (size_t s2 = 0; s2 < S; ++s2) r.at(s2, b * S + s2) = 1.0;
     rsel[b] = g.constant(r);
   }
+  // grouped-query attention: query head h reads key/value head h / (H / KV)
+  const size_t KV = c.n_kv_head ? c.n_kv_head : H;
+  if (H % KV) fail(Err::argument, "n_head must be a multiple of n_kv_head");
+  const size_t kvd = KV * dh, W = d + 2 * kvd, G = H / KV;
   std::vector<int> qsel(H), ksel(H), vsel(H), place(H);
   for (size_t h = 0; h < H; ++h) {
-    Tensor q(3 * d, dh), k(3 * d, dh), v(3 * d, dh), p(dh, d);
+    Tensor q(W, dh), k(W, dh), v(W, dh), p(dh, d);
+    const size_t kv = h / G;
     for (size_t e = 0; e < dh; ++e) {
       q.at(h * dh + e, e) = 1.0;
-      k.at(d + h * dh + e, e) = 1.0;
-      v.at(2 * d + h * dh + e, e) = 1.0;
+      k.at(d + kv * dh + e, e) = 1.0;
+      v.at(d + kvd + kv * dh + e, e) = 1.0;
       p.at(e, h * dh + e) = 1.0;
     }
     qsel[h] = g.constant(q);

@@ -228,6 +228,7 @@ struct GptConfig {
   double ln_eps = 1e-5;
   int arch = 0;              // 0: GPT-2 block; 1: Llama-style (RMSNorm, RoPE, SwiGLU, untied head, no biases)
   double rope_base = 10000.0;
+  size_t n_kv_head = 0;      // Llama: key/value heads (grouped-query attention); 0 = n_head
 };
 struct ParamSlot {
   std::string name;

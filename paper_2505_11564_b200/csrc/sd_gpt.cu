@@ -52,10 +52,11 @@ std::vector<Slot> layout(const sd_gpt_config& c) {
     // oracle/src/models.cpp gpt_layout (arch 1): tok_embeddings, per layer
     // [attention_norm, wqkv [d][3d], wo, ffn_norm, w_gate_up [d][2ff], w_down],
     // norm, output [V][d]
+    const uint64_t kvd = uint64_t(c.n_kv_head > 0 ? c.n_kv_head : c.n_head) * (c.d / c.n_head);
     add(c.vocab, c.d, 0);
     for (int l = 0; l < c.n_layer; ++l) {
       add(1, c.d, 1);
-      add(c.d, 3 * c.d, 0);
+      add(c.d, c.d + 2 * kvd, 0);
       add(c.d, c.d, 0);
       add(1, c.d, 1);
       add(c.d, 2 * c.ff, 0);
@@ -101,6 +102,9 @@ void check_cfg(const sd_gpt_config& c, int B, int S) {
   if (S % 4) fail(SD_CONFIG_ERROR, "sequence length must be a multiple of 4");
   if (c.arch != SD_ARCH_GPT2 && c.arch != SD_ARCH_LLAMA) fail(SD_CONFIG_ERROR, "unknown architecture");
   if (c.arch == SD_ARCH_LLAMA && !(c.rope_base > 1.0f)) fail(SD_CONFIG_ERROR, "rope_base must exceed 1");
+  if (c.n_kv_head < 0 || (c.n_kv_head > 0 && (c.arch != SD_ARCH_LLAMA || c.n_head % c.n_kv_head)))
+    fail(SD_CONFIG_ERROR, "n_kv_head must divide n_head (Llama-style only)");
+  if (c.arch == SD_ARCH_LLAMA && (c.d / c.n_head) % 2) fail(SD_CONFIG_ERROR, "RoPE needs an even head dim");
 }
 
 struct Layer {
@@ -110,6 +114,7 @@ struct Layer {
   float *o, *os, *dO, *dOs;
   float *xh2, *dxh2, *r2, *dr2, *h2, *h2s, *dh2, *dh2s;
   float *f, *df, *u, *us, *du, *dus;
+  float *qkv = nullptr, *qkvs = nullptr, *dqkv = nullptr, *dqkvs = nullptr;  // GQA raw q|k|v (+tangent)
 };
 
 struct Plan {
@@ -140,6 +145,10 @@ struct sd_gpt_s {
   float *go, *gos, *gdo, *gdos, *ga, *gas, *gda, *gdas;
   float *gP, *gPs, *gdP, *gdPs, *gu, *gus, *gdu, *gdus;
   float *ga_mlp = nullptr, *gda_mlp = nullptr;
+  // grouped-query attention: adjoints of the raw [T, d + 2 kvd] q|k|v product
+  float *gqkv = nullptr, *gqkvs = nullptr, *gdqkv = nullptr, *gdqkvs = nullptr;
+  int KV = 0, W = 0;  // key/value heads, raw q|k|v width
+  bool gqa() const { return KV != H; }
   double* loss_rows = nullptr;
   float* red = nullptr;  // column-reduction scratch
   int *tok = nullptr, *tgt = nullptr, *uniq = nullptr, *ustart = nullptr, *upos = nullptr;
@@ -180,6 +189,13 @@ struct sd_gpt_s {
     gdus = p.take<float>(T_ * ffw);
     if (c.arch == SD_ARCH_LLAMA) {  // adjoint (+ tangent) of the SwiGLU output [T, ff]
       ga_mlp = p.take<float>(T_ * ff), gda_mlp = p.take<float>(T_ * ff);
+    }
+    if (gqa()) {
+      for (auto& l : L)
+        l.qkv = p.take<float>(T_ * W), l.qkvs = p.take<float>(T_ * W), l.dqkv = p.take<float>(T_ * W),
+        l.dqkvs = p.take<float>(T_ * W);
+      gqkv = p.take<float>(T_ * W), gqkvs = p.take<float>(T_ * W), gdqkv = p.take<float>(T_ * W),
+      gdqkvs = p.take<float>(T_ * W);
     }
     theta_s = p.take<float>(P), v_s = p.take<float>(P);
     loss_rows = p.take<double>(T_);
@@ -369,10 +385,14 @@ struct sd_gpt_s {
       sd::LnArgs la{x, dx, th(b), nullptr, V_(b), nullptr, T, d, eps,
                     Ly.h1, Ly.h1s, Ly.dh1, Ly.dh1s, Ly.xh1, Ly.dxh1, Ly.r1, Ly.dr1, 1};
       sd::gpt_ln_fwd(la, st);
-      mm(T, 3 * d, d, {Ly.h1, Ly.h1s, d, false}, {th(b + 1), ths(b + 1), 3 * d, true}, Ly.a, 3 * d, 1, 0, st,
-         nullptr, Ly.as);
-      mm2(T, 3 * d, d, {Ly.dh1, Ly.dh1s, d, false}, {th(b + 1), ths(b + 1), 3 * d, true}, {Ly.h1, Ly.h1s, d, false},
-          {V_(b + 1), Vs(b + 1), 3 * d, true}, Ly.da, 3 * d, 1, 0, st, nullptr, Ly.das);
+      // q|k|v = h1 Wqkv (width W = d + 2 kvd); grouped-query attention expands
+      // the KV heads to the MHA [T, 3d] layout the attention products use
+      float *qa = gqa() ? Ly.qkv : Ly.a, *qas = gqa() ? Ly.qkvs : Ly.as;
+      float *qd = gqa() ? Ly.dqkv : Ly.da, *qds = gqa() ? Ly.dqkvs : Ly.das;
+      mm(T, W, d, {Ly.h1, Ly.h1s, d, false}, {th(b + 1), ths(b + 1), W, true}, qa, W, 1, 0, st, nullptr, qas);
+      mm2(T, W, d, {Ly.dh1, Ly.dh1s, d, false}, {th(b + 1), ths(b + 1), W, true}, {Ly.h1, Ly.h1s, d, false},
+          {V_(b + 1), Vs(b + 1), W, true}, qd, W, 1, 0, st, nullptr, qds);
+      if (gqa()) sd::llama_gqa_expand(Ly.qkv, Ly.qkvs, Ly.dqkv, Ly.dqkvs, Ly.a, Ly.as, Ly.da, Ly.das, T, d, dh, KV, H, st);
       sd::llama_rope(Ly.a, Ly.as, Ly.da, Ly.das, T, S, d, dh, c.rope_base, 0, st);
       attention_fwd(Ly, sc, st);
       mm(T, d, d, {Ly.o, Ly.os, d, false}, {th(b + 2), ths(b + 2), d, true}, x, d, 1, 1, st);
@@ -432,13 +452,19 @@ struct sd_gpt_s {
       mm2(d, d, T, {Ly.dO, Ly.dOs, d, true}, {gx, gxs, d, true}, {Ly.o, Ly.os, d, true}, {gdx, gdxs, d, true},
           HV(b + 2), d, 1, 0, st);
       attention_bwd(Ly, sc, st);
-      // adjoints of the pre-rotation q, k: the inverse rotation
+      // adjoints of the pre-rotation q, k: the inverse rotation; GQA: sum the
+      // expanded heads' k/v adjoints back into their KV heads
       sd::llama_rope(ga, gas, gda, gdas, T, S, d, dh, c.rope_base, 1, st);
-      mm(T, d, 3 * d, {ga, gas, 3 * d, false}, {th(b + 1), ths(b + 1), 3 * d, false}, gh, d, 1, 0, st);
-      mm2(T, d, 3 * d, {gda, gdas, 3 * d, false}, {th(b + 1), ths(b + 1), 3 * d, false}, {ga, gas, 3 * d, false},
-          {V_(b + 1), Vs(b + 1), 3 * d, false}, gdh, d, 1, 0, st);
-      mm2(d, 3 * d, T, {Ly.dh1, Ly.dh1s, d, true}, {ga, gas, 3 * d, true}, {Ly.h1, Ly.h1s, d, true},
-          {gda, gdas, 3 * d, true}, HV(b + 1), 3 * d, 1, 0, st);
+      const float *qg = ga, *qgs = gas, *qgd = gda, *qgds = gdas;
+      if (gqa()) {
+        sd::llama_gqa_reduce(ga, gda, gqkv, gqkvs, gdqkv, gdqkvs, T, d, dh, KV, H, st);
+        qg = gqkv, qgs = gqkvs, qgd = gdqkv, qgds = gdqkvs;
+      }
+      mm(T, d, W, {qg, qgs, W, false}, {th(b + 1), ths(b + 1), W, false}, gh, d, 1, 0, st);
+      mm2(T, d, W, {qgd, qgds, W, false}, {th(b + 1), ths(b + 1), W, false}, {qg, qgs, W, false},
+          {V_(b + 1), Vs(b + 1), W, false}, gdh, d, 1, 0, st);
+      mm2(d, W, T, {Ly.dh1, Ly.dh1s, d, true}, {qg, qgs, W, true}, {Ly.h1, Ly.h1s, d, true}, {qgd, qgds, W, true},
+          HV(b + 1), W, 1, 0, st);
       sd::LnBwdArgs b1{gh, gdh, th(b), V_(b), Ly.xh1, Ly.dxh1, Ly.r1, Ly.dr1, T, d,
                        gx, gdx, gxs, gdxs, HV(b), nullptr, red, 1};
       sd::gpt_ln_bwd(b1, st);
@@ -515,6 +541,8 @@ Plan plan_for(const sd_gpt_config& c, int B, int S, char* base, sd_gpt_s* g) {
   e->Vp = (c.vocab + 7) / 8 * 8;
   e->BHSS = (long long)B * c.n_head * S * S;
   e->P = (long long)param_count(c);
+  e->KV = c.n_kv_head > 0 ? c.n_kv_head : c.n_head;
+  e->W = c.d + 2 * e->KV * e->dh;
   Plan p;
   p.base = base;
   e->carve(p);

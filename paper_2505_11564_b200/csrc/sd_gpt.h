@@ -27,6 +27,13 @@ void gpt_embed(const int* tok, int T, int S, int d, const float* wte, const floa
 // tangent, in place (inverse = backward adjoint); residuals rewritten.
 void llama_rope(float* a, float* as, float* da, float* das, int T, int S, int d, int dh, float base, int inverse,
                 cudaStream_t s);
+// grouped-query attention: raw [T, d + 2 KV dh] q|k|v (+tangent, residuals) ->
+// the MHA [T, 3d] layout (query head h reads KV head h / (H / KV)); and the
+// adjoint reduction back (sums over each KV head's query group; residuals)
+void llama_gqa_expand(const float* raw, const float* raws, const float* draw, const float* draws, float* a, float* as,
+                      float* da, float* das, int T, int d, int dh, int KV, int H, cudaStream_t s);
+void llama_gqa_reduce(const float* ga, const float* gda, float* graw, float* graws, float* gdraw, float* gdraws, int T,
+                      int d, int dh, int KV, int H, cudaStream_t s);
 // SwiGLU: fu = [gate | up] [T, 2ff] -> a = silu(gate) * up (and tangent, residuals)
 void llama_swiglu_fwd(const float* fu, const float* dfu, float* a, float* as, float* da, float* das, int T, int ff,
                       cudaStream_t s);

@@ -438,6 +438,54 @@ __global__ void k_rope(float* __restrict__ a, float* __restrict__ as, float* __r
   if (das) das[o] = tf32_res(w1), das[o + half] = tf32_res(w2);
 }
 
+// ------------------------------------------------- grouped-query attention
+__global__ void k_gqa_expand(const float* __restrict__ raw, const float* __restrict__ raws,
+                             const float* __restrict__ draw, const float* __restrict__ draws, float* __restrict__ a,
+                             float* __restrict__ as, float* __restrict__ da, float* __restrict__ das, int d, int dh,
+                             int KV, int H, long long n) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int W = d + 2 * KV * dh;
+  const long long t = i / (3LL * d);
+  const int col = int(i % (3LL * d));
+  int src;
+  if (col < d) {
+    src = col;
+  } else {
+    const int part = (col - d) / d, c2 = (col - d) % d;  // 0: k, 1: v
+    const int h = c2 / dh, e = c2 % dh, kv = h / (H / KV);
+    src = d + part * KV * dh + kv * dh + e;
+  }
+  const long long o = t * W + src;
+  a[i] = raw[o], as[i] = raws[o], da[i] = draw[o], das[i] = draws[o];
+}
+__global__ void k_gqa_reduce(const float* __restrict__ ga, const float* __restrict__ gda, float* __restrict__ graw,
+                             float* __restrict__ graws, float* __restrict__ gdraw, float* __restrict__ gdraws, int d,
+                             int dh, int KV, int H, long long n) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int W = d + 2 * KV * dh, G = H / KV;
+  const long long t = i / W;
+  const int col = int(i % W);
+  const float* gr = ga + t * 3LL * d;
+  const float* gdr = gda + t * 3LL * d;
+  float a, b;
+  if (col < d) {
+    a = gr[col], b = gdr[col];
+  } else {
+    const int part = (col - d) / (KV * dh), c2 = (col - d) % (KV * dh);
+    const int kv = c2 / dh, e = c2 % dh;
+    double sa = 0.0, sb = 0.0;  // the group's query heads in ascending order
+    for (int g = 0; g < G; ++g) {
+      const int mc = d + part * d + (kv * G + g) * dh + e;
+      sa += gr[mc], sb += gdr[mc];
+    }
+    a = float(sa), b = float(sb);
+  }
+  graw[i] = a, graws[i] = tf32_res(a);
+  gdraw[i] = b, gdraws[i] = tf32_res(b);
+}
+
 // --------------------------------------------------------------- SwiGLU
 // s = silu(f) = f sig(f); s1 = silu'(f); s2 = silu''(f); a = s u.
 __device__ __forceinline__ void silu_derivs(double f, double& s, double& s1, double& s2) {
@@ -622,6 +670,20 @@ void llama_rope(float* a, float* as, float* da, float* das, int T, int S, int d,
   const long long n = (long long)T * d;
   k_rope<<<g1(n), 256, 0, s>>>(a, as, da, das, T, S, d, dh, base, inverse);
   SD_LAUNCHED("k_rope");
+}
+
+void llama_gqa_expand(const float* raw, const float* raws, const float* draw, const float* draws, float* a, float* as,
+                      float* da, float* das, int T, int d, int dh, int KV, int H, cudaStream_t s) {
+  const long long n = (long long)T * 3 * d;
+  k_gqa_expand<<<g1(n), 256, 0, s>>>(raw, raws, draw, draws, a, as, da, das, d, dh, KV, H, n);
+  SD_LAUNCHED("k_gqa_expand");
+}
+
+void llama_gqa_reduce(const float* ga, const float* gda, float* graw, float* graws, float* gdraw, float* gdraws, int T,
+                      int d, int dh, int KV, int H, cudaStream_t s) {
+  const long long n = (long long)T * (d + 2 * KV * dh);
+  k_gqa_reduce<<<g1(n), 256, 0, s>>>(ga, gda, graw, graws, gdraw, gdraws, d, dh, KV, H, n);
+  SD_LAUNCHED("k_gqa_reduce");
 }
 
 void llama_swiglu_fwd(const float* fu, const float* dfu, float* a, float* as, float* da, float* das, int T, int ff,

@@ -20,12 +20,15 @@ _M64 = (1 << 64) - 1
 
 class GptConfig(C.Structure):
     _fields_ = [("n_layer", C.c_int), ("d", C.c_int), ("n_head", C.c_int), ("ff", C.c_int), ("vocab", C.c_int),
-                ("ctx", C.c_int), ("arch", C.c_int), ("rope_base", C.c_float)]
+                ("ctx", C.c_int), ("arch", C.c_int), ("rope_base", C.c_float), ("n_kv_head", C.c_int)]
 
 
 ARCH_GPT2, ARCH_LLAMA = 0, 1
 # BASELINE C4 (Llama-2-7B shape, MHA) -- the Llama-style decoder of this engine
 LLAMA2_7B = dict(n_layer=32, d=4096, n_head=32, ff=11008, vocab=32000, ctx=4096, arch=ARCH_LLAMA, rope_base=10000)
+# BASELINE C5 (R1-Distill-Llama-70B shape: 80L, d8192, ff28672, V128256, GQA 64/8)
+LLAMA_70B = dict(n_layer=80, d=8192, n_head=64, ff=28672, vocab=128256, ctx=8192, arch=ARCH_LLAMA,
+                 rope_base=500000, n_kv_head=8)
 
 
 GPT2_SMALL = dict(n_layer=12, d=768, n_head=12, ff=3072, vocab=50257, ctx=1024)
@@ -62,7 +65,7 @@ def _L():
 
 def _cfg(cfg: dict) -> GptConfig:
     return GptConfig(cfg["n_layer"], cfg["d"], cfg["n_head"], cfg["ff"], cfg["vocab"], cfg["ctx"],
-                     cfg.get("arch", ARCH_GPT2), float(cfg.get("rope_base", 10000.0)))
+                     cfg.get("arch", ARCH_GPT2), float(cfg.get("rope_base", 10000.0)), cfg.get("n_kv_head", 0))
 
 
 def param_count(cfg: dict) -> int:

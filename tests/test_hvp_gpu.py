@@ -134,13 +134,16 @@ LTINY = dict(n_layer=2, d=64, n_head=4, ff=96, vocab=96, ctx=32, arch=1, rope_ba
 
 def test_llama_layout_matches_oracle(sd, oracle):
     from paper_2505_11564_b200 import gpt
-    for cfg in (LTINY, gpt.LLAMA2_7B):
+    for cfg in (LTINY, dict(LTINY, n_kv_head=2), gpt.LLAMA2_7B, gpt.LLAMA_70B):
         assert gpt.param_count(cfg) == oracle.gpt_param_count(cfg)
     assert gpt.param_count(gpt.LLAMA2_7B) == 6738415616  # Llama-2-7B parameter count
+    assert gpt.param_count(gpt.LLAMA_70B) == 70553706496  # SURVEY C5 (R1-Distill-Llama-70B shape, GQA 64/8)
     assert gpt.param_layout(LTINY) == oracle.gpt_layout(LTINY)
+    assert gpt.param_layout(dict(LTINY, n_kv_head=2)) == oracle.gpt_layout(dict(LTINY, n_kv_head=2))
 
 
-@pytest.mark.parametrize("cfg,B,S", [(LTINY, 2, 32), (dict(LTINY, n_layer=1, n_head=2, d=32, ff=40), 3, 16)])
+@pytest.mark.parametrize("cfg,B,S", [(LTINY, 2, 32), (dict(LTINY, n_layer=1, n_head=2, d=32, ff=40), 3, 16),
+                                     (dict(LTINY, n_kv_head=2), 2, 32), (dict(LTINY, n_head=8, d=64, n_kv_head=1), 1, 24)])
 def test_llama_hvp_vs_oracle(sd, oracle, cfg, B, S):
     # Llama-style decoder (RMSNorm, RoPE, SwiGLU, untied head; BASELINE C4/C5 family)
     from paper_2505_11564_b200 import gpt
