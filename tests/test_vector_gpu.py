@@ -187,3 +187,40 @@ def test_lanczos_selective_bitwise(sd, oracle, prec, window):
     assert np.array_equal(r.alphas, o["alphas"]) and np.array_equal(r.betas, o["betas"])
     with pytest.raises(sd.ConfigError):
         sd.lanczos_run(op, sd.LanczosConfig(k_max=5, reorthogonalize=sd.REORTH_SELECTIVE, selective_window=1))
+
+
+def test_lanczos_edge_cases(sd):
+    # SPEC.md:263 identity -> alpha0 = 1, beta0 below eps, stops at k = 1 (benign breakdown)
+    op = sd.dense_operator(np.eye(64))
+    for prec in (F32, F64):
+        r = sd.lanczos_run(op, sd.LanczosConfig(k_max=10, reorthogonalize=sd.REORTH_FULL, prec=prec,
+                                                probe=sd.ProbeSpec(seed=1, distribution=RADEMACHER)))
+        assert r.alphas.tolist() == [1.0] and r.betas.size == 0 and r.breakdown
+    # k_max = 1: one alpha, no betas
+    S = sd.spiked_dense(128, 1.0, [10.0], 2)
+    r = sd.lanczos_run(sd.dense_operator(S), sd.LanczosConfig(k_max=1, prec=F64))
+    assert r.alphas.size == 1 and r.betas.size == 0 and not r.breakdown
+    # diag(1,2,3), q0 = (1,1,1)/sqrt(3), full ortho -> eig(T) = {1,2,3}
+    op3 = sd.dense_operator(np.diag([1.0, 2.0, 3.0]))
+    r = sd.lanczos_run(op3, sd.LanczosConfig(k_max=3, reorthogonalize=sd.REORTH_FULL, prec=F64,
+                                             probe=sd.ProbeSpec(seed=0, distribution=RADEMACHER)))
+    ritz = sd.ritz_decompose(r.alphas, r.betas)
+    assert np.max(np.abs(ritz.values - [1, 2, 3])) < 1e-10 and abs(ritz.weights.sum() - 1) < 1e-12
+    # a non-finite operator output -> NumericalError carrying the partial tridiagonal
+    import ctypes as C
+
+    def nan_apply(x, y, s):
+        t = torch.full((64,), float("nan"), dtype=torch.float64, device="cuda")
+        sd._lib.lib().sd_k_scale(C.c_void_p(t.data_ptr()), C.c_void_p(y), 64,
+                                 C.c_void_p(torch.ones(1, dtype=torch.float64, device="cuda").data_ptr()), 0, F64,
+                                 C.c_void_p(s))
+        torch.cuda.synchronize()
+        return 0
+    bad = sd.custom_operator(64, nan_apply, "nan")
+    with pytest.raises(sd.NumericalError) as ei:
+        sd.lanczos_run(bad, sd.LanczosConfig(k_max=5, prec=F64))
+    assert ei.value.result.alphas.size == 0 and ei.value.result.numerical_failure
+    # dimension mismatch between operator and vector -> layout error (operators.cpp:12-17)
+    pool = sd.make_pool(32, 1)
+    with pytest.raises(sd.LayoutError):
+        op.apply(pool, sd.draw_probe(pool, None, F64))
