@@ -111,13 +111,54 @@ void make_store_map(CUtensorMap* m, float* C, const GemmArgs& g, int box_cols) {
 // for the second product of a dual-source GEMM (copies of the first if none).
 // K-major tiles are box_m (A) / box_n (B) rows of BK elements; MN-major tiles
 // are loaded as 32-element chunks of BK rows.
-void operand_maps(const GemmArgs& g, bool a_mn, bool b_mn, bool three, int box_n, CUtensorMap* m) {
+// MN-major operand whose extent is a multiple of 32: one 5-D box loads the
+// whole tile -- dims (32 elements, K rows, 32-element chunks, z1, z2), box
+// (32, BK, chunks, 1, 1) lands chunk-major, exactly the 2 KB-per-chunk
+// SWIZZLE_128B_ATOM_32B layout the UMMA descriptors expect (one TMA
+// instruction instead of one per chunk).
+void make_map_mn5(CUtensorMap* m, const float* base, long long extent, long long K, long long ld, int Z1, long long s1,
+                  int Z2, long long s2, int chunks) {
+  if ((reinterpret_cast<uintptr_t>(base) & 15) != 0) fail(SD_ARGUMENT_ERROR, "gemm operand not 16-byte aligned");
+  if ((ld * 4) % 16 != 0 || (Z1 > 1 && (s1 * 4) % 16) || (Z2 > 1 && (s2 * 4) % 16))
+    fail(SD_ARGUMENT_ERROR, "gemm operand strides must be multiples of 16 bytes");
+  cuuint64_t dims[5] = {32, cuuint64_t(K), cuuint64_t((extent + 31) / 32), cuuint64_t(Z1), cuuint64_t(Z2)};
+  const long long whole = ((ld * K * 4 + 15) / 16) * 16;
+  cuuint64_t strides[4] = {cuuint64_t(ld * 4), 128, cuuint64_t(Z1 > 1 ? s1 * 4 : whole),
+                           cuuint64_t(Z2 > 1 ? s2 * 4 : whole)};
+  cuuint32_t box[5] = {32, cuuint32_t(BK), cuuint32_t(chunks), 1, 1};
+  cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  const CUresult r = encoder()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, const_cast<float*>(base), dims, strides, box, es,
+                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(SD_CUDA_ERROR, "cuTensorMapEncodeTiled (mn5) failed (" + std::to_string(int(r)) + ")");
+}
+
+bool sd_gemm_mn5_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("SD_GEMM_MN5");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+void operand_maps(const GemmArgs& g, bool a_mn, bool b_mn, bool three, int box_n, CUtensorMap* m, int* mn5) {
+  // (an extent that is not a multiple of 32 is fine when the rows have room for
+  // the last chunk: the extra columns only feed output rows/columns >= M/N,
+  // which the epilogue never stores)
+  const auto r32 = [](long long x) { return (x + 31) / 32 * 32; };
+  const bool a5 = a_mn && (g.M % 32 == 0 || g.lda >= r32(g.M)) && (!g.A2 || g.M % 32 == 0 || g.lda2 >= r32(g.M)) &&
+                  sd_gemm_mn5_enabled();
+  const bool b5 = b_mn && (g.N % 32 == 0 || g.ldb >= r32(g.N)) && (!g.A2 || g.N % 32 == 0 || g.ldb2 >= r32(g.N)) &&
+                  sd_gemm_mn5_enabled();
+  if (mn5) *mn5 = (a5 ? 1 : 0) | (b5 ? 2 : 0);
   auto amap = [&](CUtensorMap* o, const float* p, long long ld, long long s1, long long s2) {
-    if (a_mn) make_map(o, p, g.M, g.K, ld, g.Z1, s1, g.Z2, s2, 32, BK, true);
+    if (a5) make_map_mn5(o, p, g.M, g.K, ld, g.Z1, s1, g.Z2, s2, BM / 32);
+    else if (a_mn) make_map(o, p, g.M, g.K, ld, g.Z1, s1, g.Z2, s2, 32, BK, true);
     else make_map(o, p, g.K, g.M, ld, g.Z1, s1, g.Z2, s2, BK, BM, false);
   };
   auto bmap = [&](CUtensorMap* o, const float* p, long long ld, long long s1, long long s2) {
-    if (b_mn) make_map(o, p, g.N, g.K, ld, g.Z1, s1, g.Z2, s2, 32, BK, true);
+    if (b5) make_map_mn5(o, p, g.N, g.K, ld, g.Z1, s1, g.Z2, s2, box_n / 32);
+    else if (b_mn) make_map(o, p, g.N, g.K, ld, g.Z1, s1, g.Z2, s2, 32, BK, true);
     else make_map(o, p, g.K, g.N, ld, g.Z1, s1, g.Z2, s2, BK, box_n, false);
   };
   // residual maps only when the residuals come from memory (not on chip)
@@ -339,7 +380,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const CUtensorMap* pB = src2 ? &mB2 : &mB;
           const CUtensorMap* pBs = src2 ? &mBs2 : &mBs;
           const int k0 = (ti.kb0 + kb) * BK;
-          if (A_MN) {
+          if (A_MN && (ep.mn5 & 1)) {
+            tma_load_5d(pA, &full[s], st, 0, k0, ti.m0 / 32, z1, z2);
+            if (THREE && !ep.res) tma_load_5d(pAs, &full[s], st + A_BYTES, 0, k0, ti.m0 / 32, z1, z2);
+          } else if (A_MN) {
 #pragma unroll
             for (int c = 0; c < BM / 32; ++c) {
               tma_load_4d(pA, &full[s], st + c * 2048, ti.m0 + 32 * c, k0, z1, z2);
@@ -350,7 +394,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             if (THREE && !ep.res) tma_load_4d(pAs, &full[s], st + A_BYTES, k0, ti.m0, z1, z2);
           }
           unsigned char* sb = st + (THREE ? 2 : 1) * A_BYTES;
-          if (B_MN) {
+          if (B_MN && (ep.mn5 & 2)) {
+            tma_load_5d(pB, &full[s], sb, 0, k0, ti.n0 / 32, z1, z2);
+            if (THREE && !ep.res) tma_load_5d(pBs, &full[s], sb + B_BYTES, 0, k0, ti.n0 / 32, z1, z2);
+          } else if (B_MN) {
 #pragma unroll
             for (int c = 0; c < BN / 32; ++c) {
               tma_load_4d(pB, &full[s], sb + c * 2048, ti.n0 + 32 * c, k0, z1, z2);
@@ -497,7 +544,8 @@ template <bool A_MN, bool B_MN, bool THREE, int BN>
 void launch(const GemmArgs& g, cudaStream_t s) {
   using Cf = Cfg<BN>;
   CUtensorMap maps[8];
-  operand_maps(g, A_MN, B_MN, THREE, BN, maps);
+  int mn5 = 0;
+  operand_maps(g, A_MN, B_MN, THREE, BN, maps, &mn5);
   const bool dual = g.A2 != nullptr;
   const int zc = g.Z1 * g.Z2;
   const int tn = (g.N + BN - 1) / BN, tm = (g.M + BM - 1) / BM;
@@ -530,6 +578,7 @@ void launch(const GemmArgs& g, cudaStream_t s) {
     if (g.Cs) make_store_map(&mCs, g.Cs, g);
   }
   ep.tma_store = tma_store ? 1 : 0;
+  ep.mn5 = mn5;
   auto kern = g.causal ? k_gemm_tf32<A_MN, B_MN, THREE, BN, true> : k_gemm_tf32<A_MN, B_MN, THREE, BN, false>;
   static bool attr_set = false;
   if (!attr_set) {

@@ -67,6 +67,15 @@ __device__ __forceinline__ void tma_load_4d(const CUtensorMap* map, uint64_t* ba
       : "memory");
 }
 
+__device__ __forceinline__ void tma_load_5d(const CUtensorMap* map, uint64_t* bar, void* dst, int c0, int c1, int c2,
+                                            int c3, int c4) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6, %7}], "
+      "[%2];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
+      : "memory");
+}
+
 // UMMA shared-memory matrix descriptor. Layout codes: 4 = SWIZZLE_64B (K-major
 // tiles), 1 = SWIZZLE_128B_BASE32B (MN-major tf32 tiles: the only MN-major
 // smem layout the tf32 MMA accepts).
@@ -131,6 +140,7 @@ struct EpiParams {
   int nsrc;                           // 1, or 2 for a dual-source product
   int res;                            // 3xTF32 residuals computed on chip from the staged raw tiles
   int tma_store;                      // C = alpha acc written by TMA from smem (beta 0, no bias/Cs/split)
+  int mn5;                            // bit 0 / 1: MN-major A / B tile as one 5-D TMA box
 };
 
 __device__ __forceinline__ void fence_proxy_async_smem_decl() {
@@ -380,7 +390,7 @@ void make_store_map(CUtensorMap* m, float* C, const GemmArgs& g, int box_cols = 
 bool tma_store_ok(const GemmArgs& g, int splits, int bias_cols);
 float* splitk_workspace(size_t floats);
 int choose_splits(int tiles, int units, int total_kb, int nsrc, double t_kb, double out_bytes);
-void operand_maps(const GemmArgs& g, bool a_mn, bool b_mn, bool three, int box_n, CUtensorMap* m);
+void operand_maps(const GemmArgs& g, bool a_mn, bool b_mn, bool three, int box_n, CUtensorMap* m, int* mn5);
 bool prof_on();
 void prof_tag(const std::string& tag);
 void prof_begin(cudaStream_t s);

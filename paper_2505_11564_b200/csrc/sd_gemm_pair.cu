@@ -56,6 +56,14 @@ __device__ __forceinline__ void tma_load_4d_pair(const CUtensorMap* map, uint32_
       "l"(map), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
       : "memory");
 }
+__device__ __forceinline__ void tma_load_5d_pair(const CUtensorMap* map, uint32_t bar, void* dst, int c0, int c1,
+                                                 int c2, int c3, int c4) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, "
+      "%5, %6, %7}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
+      : "memory");
+}
 __device__ __forceinline__ void mma_tf32_pair(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
                                               uint32_t acc) {
   asm volatile(
@@ -179,7 +187,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
           const CUtensorMap* pB = src2 ? &mB2 : &mB;
           const CUtensorMap* pBs = src2 ? &mBs2 : &mBs;
           const int k0 = (ti.kb0 + kb) * BK;
-          if (A_MN) {
+          if (A_MN && (ep.mn5 & 1)) {
+            tma_load_5d_pair(pA, bar, st, 0, k0, m_own / 32, z1, z2);
+            if (THREE && !ep.res) tma_load_5d_pair(pAs, bar, st + PA_BYTES, 0, k0, m_own / 32, z1, z2);
+          } else if (A_MN) {
 #pragma unroll
             for (int c = 0; c < BM / 32; ++c) {
               tma_load_4d_pair(pA, bar, st + c * 2048, m_own + 32 * c, k0, z1, z2);
@@ -190,7 +201,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
             if (THREE && !ep.res) tma_load_4d_pair(pAs, bar, st + PA_BYTES, k0, m_own, z1, z2);
           }
           unsigned char* sb = st + (THREE ? 2 : 1) * PA_BYTES;
-          if (B_MN) {
+          if (B_MN && (ep.mn5 & 2)) {
+            tma_load_5d_pair(pB, bar, sb, 0, k0, n_own / 32, z1, z2);
+            if (THREE && !ep.res) tma_load_5d_pair(pBs, bar, sb + PB_BYTES, 0, k0, n_own / 32, z1, z2);
+          } else if (B_MN) {
 #pragma unroll
             for (int c = 0; c < kHalfB / 32; ++c) {
               tma_load_4d_pair(pB, bar, sb + c * 2048, n_own + 32 * c, k0, z1, z2);
@@ -337,7 +351,8 @@ int max_clusters(const void* kern, size_t smem) {
 template <bool A_MN, bool B_MN, bool THREE>
 void launch_pair_t(const GemmArgs& g, cudaStream_t s) {
   CUtensorMap maps[8];
-  operand_maps(g, A_MN, B_MN, THREE, kHalfB, maps);
+  int mn5 = 0;
+  operand_maps(g, A_MN, B_MN, THREE, kHalfB, maps, &mn5);
   const bool dual = g.A2 != nullptr;
   const int zc = g.Z1 * g.Z2;
   const int tn = (g.N + kPairN - 1) / kPairN, tm = (g.M + kPairM - 1) / kPairM;
@@ -365,6 +380,7 @@ void launch_pair_t(const GemmArgs& g, cudaStream_t s) {
              "," + std::to_string(int(A_MN)) + "," + std::to_string(int(B_MN)) + ",pair," + std::to_string(splits) +
              (dual ? ",2" : ",1"));
   prof_begin(s);
+  ep.mn5 = mn5;
   CUtensorMap mC = maps[0], mCs = maps[0];
   if (tma_store_ok(g, splits, 16)) {
     make_store_map(&mC, g.C, g, 16);

@@ -538,7 +538,7 @@ Plan plan_for(const sd_gpt_config& c, int B, int S, char* base, sd_gpt_s* g) {
   sd_gpt_s* e = g ? g : &tmp;
   e->c = c;
   e->B = B, e->S = S, e->T = B * S, e->H = c.n_head, e->dh = c.d / c.n_head;
-  e->Vp = (c.vocab + 7) / 8 * 8;
+  e->Vp = (c.vocab + 31) / 32 * 32;  // logits rows padded to 32: whole 5-D TMA boxes for the head products
   e->BHSS = (long long)B * c.n_head * S * S;
   e->P = (long long)param_count(c);
   e->KV = c.n_kv_head > 0 ? c.n_kv_head : c.n_head;
