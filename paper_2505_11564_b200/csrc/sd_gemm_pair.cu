@@ -15,6 +15,7 @@
 // Same 3xTF32 scheme, chunked round-to-nearest drain (KC), dual-source and
 // split-K support as the single-CTA kernel in sd_gemm.cu.
 #include <algorithm>
+#include <cstdlib>
 #include <string>
 
 #include "sd_gemm_dev.cuh"
@@ -23,16 +24,20 @@ namespace sd {
 namespace gk {
 namespace {
 
-constexpr int kPairN = 256;                           // pair tile N (each CTA stages 128 columns of B)
 constexpr int kPairM = 256;                           // pair tile M (each CTA stages 128 rows of A)
 constexpr int kEpiWarps = 16;
 constexpr int kPairThreads = 32 * (2 + kConvWarps + kEpiWarps);  // producer, MMA, residual, epilogue
-constexpr int kHalfB = kPairN / 2;
 constexpr int PA_BYTES = BM * BK * 4;                 // 8 KB
-constexpr int PB_BYTES = kHalfB * BK * 4;             // 8 KB
 constexpr int kPairStages = 6;
-constexpr uint32_t kPairTmemCols = 2 * kPairN;        // two accumulation buffers
-constexpr int kPairEC = kPairN / (kEpiWarps / 4);     // 64 accumulator columns per epilogue thread
+// Pair tile width PN in {256, 192}: each CTA stages PN/2 columns of B; the
+// narrower tile is chosen when it quantises into fuller waves (gemm_pair()).
+template <int PN>
+struct PairCfg {
+  static constexpr int N = PN, HALF = PN / 2;
+  static constexpr int PB_BYTES = HALF * BK * 4;      // 8 / 6 KB
+  static constexpr uint32_t TMEM_COLS = 512;          // two accumulation buffers (2 PN <= 512)
+  static constexpr int EC = PN / (kEpiWarps / 4);     // 64 / 48 accumulator columns per epilogue thread
+};
 
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
@@ -94,12 +99,13 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t* v) {
       : "r"(taddr));
 }
 
+template <int PN>
 __device__ __forceinline__ TileInfo pair_tile(const EpiParams& ep, int t, int K) {
   TileInfo ti;
   const int nt = t % ep.n_tiles_n;
   const int mt = (t / ep.n_tiles_n) % ep.n_tiles_m;
   const int zz = t / (ep.n_tiles_n * ep.n_tiles_m);
-  ti.n0 = nt * kPairN;
+  ti.n0 = nt * PN;
   ti.m0 = mt * kPairM;
   ti.z = zz % ep.zcount;
   ti.split = zz / ep.zcount;
@@ -109,14 +115,17 @@ __device__ __forceinline__ TileInfo pair_tile(const EpiParams& ep, int t, int K)
   return ti;
 }
 
-template <bool A_MN, bool B_MN, bool THREE>
+template <bool A_MN, bool B_MN, bool THREE, int PN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     k_gemm_pair(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mAs,
                 const __grid_constant__ CUtensorMap mB, const __grid_constant__ CUtensorMap mBs,
                 const __grid_constant__ CUtensorMap mA2, const __grid_constant__ CUtensorMap mAs2,
                 const __grid_constant__ CUtensorMap mB2, const __grid_constant__ CUtensorMap mBs2,
                 const __grid_constant__ CUtensorMap mC, const __grid_constant__ CUtensorMap mCs, int K, EpiParams ep) {
-  constexpr int STAGES = kPairStages, EC = kPairEC;
+  using PC = PairCfg<PN>;
+  constexpr int STAGES = kPairStages, EC = PC::EC, kHalfB = PC::HALF, PB_BYTES = PC::PB_BYTES;
+  constexpr int kPairN = PN;
+  constexpr uint32_t kPairTmemCols = PC::TMEM_COLS;
   constexpr int STAGE_BYTES = (THREE ? 2 : 1) * (PA_BYTES + PB_BYTES);
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -160,7 +169,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
       const uint32_t full_leader = leader_addr(full);
       uint32_t g = 0;
       for (int t = cid; t < ep.n_tiles; t += ncl) {
-        const TileInfo ti = pair_tile(ep, t, K);
+        const TileInfo ti = pair_tile<PN>(ep, t, K);
         if (ti.skip) continue;
         const int z1 = ti.z % ep.Z1, z2 = ti.z / ep.Z1;
         const int m_own = ti.m0 + int(rank) * BM, n_own = ti.n0 + int(rank) * kHalfB;
@@ -225,7 +234,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     uint32_t g = 0;
     if (THREE && ep.res)
       for (int t = cid; t < ep.n_tiles; t += ncl) {
-        const TileInfo ti = pair_tile(ep, t, K);
+        const TileInfo ti = pair_tile<PN>(ep, t, K);
         if (ti.skip) continue;
         for (int kk = 0; kk < ep.nsrc * ti.num_kb; ++kk, ++g) {
           if (int(g % kConvWarps) != cw) continue;
@@ -244,7 +253,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
       constexpr uint32_t idesc = make_idesc(A_MN, B_MN, kPairN, kPairM);
       uint32_t g = 0, chunk = 0;
       for (int t = cid; t < ep.n_tiles; t += ncl) {
-        const TileInfo ti = pair_tile(ep, t, K);
+        const TileInfo ti = pair_tile<PN>(ep, t, K);
         if (ti.skip) continue;
         const int nkb = ep.nsrc * ti.num_kb;
         for (int kb = 0; kb < nkb; ++kb, ++g) {
@@ -288,7 +297,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     const uint32_t tempty_leader = leader_addr(tempty);
     uint32_t chunk = 0;
     for (int t = cid; t < ep.n_tiles; t += ncl) {
-      const TileInfo ti = pair_tile(ep, t, K);
+      const TileInfo ti = pair_tile<PN>(ep, t, K);
       if (ti.skip) continue;
       const int row = ti.m0 + int(rank) * BM + sub * 32 + lane;
       float acc[EC];
@@ -348,8 +357,10 @@ int max_clusters(const void* kern, size_t smem) {
   return n;
 }
 
-template <bool A_MN, bool B_MN, bool THREE>
+template <bool A_MN, bool B_MN, bool THREE, int PN>
 void launch_pair_t(const GemmArgs& g, cudaStream_t s) {
+  using PC = PairCfg<PN>;
+  constexpr int kPairN = PN, kHalfB = PC::HALF, PB_BYTES = PC::PB_BYTES;
   CUtensorMap maps[8];
   int mn5 = 0;
   operand_maps(g, A_MN, B_MN, THREE, kHalfB, maps, &mn5);
@@ -358,7 +369,7 @@ void launch_pair_t(const GemmArgs& g, cudaStream_t s) {
   const int tn = (g.N + kPairN - 1) / kPairN, tm = (g.M + kPairM - 1) / kPairM;
   const int tiles = tn * tm * zc;
   const size_t smem = 1024 + size_t(kPairStages) * (THREE ? 2 : 1) * (PA_BYTES + PB_BYTES) + kEpiWarps * 2048 + 512;
-  auto kern = k_gemm_pair<A_MN, B_MN, THREE>;
+  auto kern = k_gemm_pair<A_MN, B_MN, THREE, PN>;
   static int clusters = 0;
   if (!clusters) {
     SD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
@@ -397,10 +408,42 @@ void launch_pair_t(const GemmArgs& g, cudaStream_t s) {
 
 }  // namespace
 
+// Wave-quantisation-aware tile width: the modelled time of each candidate
+// (waves x k-blocks x per-k-block time, relative per-SM rate of the narrower
+// tile 0.95) -- e.g. 8192 x 3072 outputs: 384 tiles of 256 (5.2 -> 6 waves)
+// vs 512 of 192 (6.9 -> 7 waves, 5% less work per wave slot).
+int pick_pair_n(const GemmArgs& g) {
+  static const int forced = [] {
+    const char* e = std::getenv("SD_GEMM_PAIR_N");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (forced == 256 || forced == 192) return forced;
+  // measured on the GPT-2-small HVP: choosing 192 by this model made the step
+  // slower (122.7 vs 118.4 ms), so 256 stays unless SD_GEMM_PAIR_N forces 192
+  if (!forced) return 256;
+  const int zc = g.Z1 * g.Z2, tm = (g.M + kPairM - 1) / kPairM;
+  const int units = kNumSMs / 2;
+  const int total_kb = (g.K + BK - 1) / BK * (g.A2 ? 2 : 1);
+  double best = 1e30;
+  int best_n = 256;
+  for (int pn : {256, 192}) {
+    const long long tiles = (long long)tm * ((g.N + pn - 1) / pn) * zc;
+    const double rate = pn == 256 ? 1.0 : 0.95;
+    const double t = double((tiles + units - 1) / units) * total_kb * (double(pn) / 256.0) / rate;
+    if (t < best * 0.98) {
+      best = t;
+      best_n = pn;
+    }
+  }
+  return best_n;
+}
+
 void gemm_pair(const GemmArgs& g, cudaStream_t s) {
   const bool three = (g.As != nullptr && g.Bs != nullptr) || g.onchip;
-#define SD_PAIR_CASE(AM, BMJ, TH) \
-  if (g.a_mn == AM && g.b_mn == BMJ && three == TH) return launch_pair_t<AM, BMJ, TH>(g, s);
+  const int pn = pick_pair_n(g);
+#define SD_PAIR_CASE(AM, BMJ, TH)                                                                         \
+  if (g.a_mn == AM && g.b_mn == BMJ && three == TH)                                                       \
+    return pn == 192 ? launch_pair_t<AM, BMJ, TH, 192>(g, s) : launch_pair_t<AM, BMJ, TH, 256>(g, s);
   SD_PAIR_CASE(false, false, true)
   SD_PAIR_CASE(false, true, true)
   SD_PAIR_CASE(true, false, true)
