@@ -62,6 +62,12 @@ uint64_t sd_uniform_index(uint64_t seed, uint64_t i, uint64_t n);
  * split_evenly (layout.hpp:59-72), validate_layout (layout.hpp:45-55),
  * ShardLayout::owner (layout.hpp:28-32). `begins/ends` hold >= n entries. */
 sd_status sd_split_evenly(uint64_t dim, uint64_t n, uint64_t* begins, uint64_t* ends, uint64_t* count);
+/* 1F1B pipeline schedule of one stage (host only): *count (kind, micro-batch)
+ * int pairs in ops[2*i], ops[2*i+1]; GROUP_BEGIN/END bracket exchanges that
+ * must progress together. ops == NULL returns the count only. */
+enum { SD_PIPE_F = 0, SD_PIPE_B = 1, SD_PIPE_SEND_F = 2, SD_PIPE_RECV_F = 3, SD_PIPE_SEND_B = 4, SD_PIPE_RECV_B = 5,
+       SD_PIPE_GROUP_BEGIN = 6, SD_PIPE_GROUP_END = 7 };
+sd_status sd_pipeline_schedule(int n_stages, int stage, int n_micro, int* ops, uint64_t cap, uint64_t* count);
 sd_status sd_validate_layout(uint64_t total, uint64_t n, const uint64_t* begins, const uint64_t* ends);
 sd_status sd_layout_owner(uint64_t n, const uint64_t* ends, uint64_t i, uint64_t* owner);
 
@@ -221,6 +227,27 @@ sd_status sd_gpt_create(const sd_gpt_config* c, int batch, int seq, const float*
 /* host int32 tokens/targets (batch*seq each); Hv is scaled by loss_scale/1
  * relative to the per-token SUM (loss_scale = 1/global_tokens for the mean) */
 sd_status sd_gpt_set_batch(sd_gpt g, const int* tokens, const int* targets, float loss_scale, sd_stream s);
+/* Pipeline stages (SD_ARCH_LLAMA; PAPER.md:95-96,121-125 place contiguous
+ * layers per device): a stage owns layers [layer_begin, layer_end), the token
+ * embedding if layer_begin == 0, the final norm + head + loss if layer_end ==
+ * n_layer; its parameters are the contiguous slice sd_gpt_stage_params of the
+ * flat layout (theta_stage, v and Hv are that slice). n_micro micro-batches
+ * of micro_batch x seq tokens (set_batch takes all of them) run through
+ * n_sets activation sets (micro-batch m uses set m % n_sets). The whole model
+ * with n_micro > 1 is a memory-bounded single-device HVP. */
+uint64_t sd_gpt_stage_workspace_bytes(const sd_gpt_config* c, int micro_batch, int seq, int n_micro, int layer_begin,
+                                      int layer_end, int n_sets);
+sd_status sd_gpt_stage_params(const sd_gpt_config* c, int layer_begin, int layer_end, uint64_t* begin, uint64_t* end);
+sd_status sd_gpt_stage_create(const sd_gpt_config* c, int micro_batch, int seq, int n_micro, int layer_begin,
+                              int layer_end, int n_sets, const float* theta_stage, void* workspace,
+                              uint64_t workspace_bytes, sd_stream s, sd_gpt* out);
+/* one Hv pass: begin (v, Hv = stage slices), then forward/backward per
+ * micro-batch in a 1F1B order; Hv of micro-batches after the first accumulates */
+sd_status sd_gpt_stage_begin(sd_gpt g, const float* v_stage, float* hv_stage, sd_stream s);
+sd_status sd_gpt_stage_forward(sd_gpt g, int m, const float* x_in, const float* dx_in, float* x_out, float* dx_out,
+                               sd_stream s);
+sd_status sd_gpt_stage_backward(sd_gpt g, int m, const float* gx_in, const float* gdx_in, float* gx_out,
+                                float* gdx_out, sd_stream s);
 sd_status sd_gpt_hvp(sd_gpt g, const float* v, float* hv, sd_stream s);
 sd_status sd_gpt_last_loss(sd_gpt g, double* loss, sd_stream s);
 sd_status sd_gpt_destroy(sd_gpt g);
@@ -260,6 +287,12 @@ sd_status sd_operator_gpt(sd_gpt g, sd_comm comm, sd_operator* out);
 /* Parameter-sharded form: the Lanczos vectors are split over
  * the comm's ranks by (begins, ends); apply() all-gathers x, runs this
  * rank's batch HVP on the full vector and reduce-scatters Hv into y (f32). */
+/* Pipeline-parallel operator: comm rank r runs stage r (engine built by
+ * sd_gpt_stage_create with rank r's layers); the Lanczos vectors are sharded
+ * by the stages' parameter slices, so x/y are this stage's slice and only the
+ * stage-boundary activations (primal|tangent, adjoint|adjoint tangent) move,
+ * by NCCL send/recv along the 1F1B schedule. */
+sd_status sd_operator_gpt_pipeline(sd_gpt g, sd_comm comm, sd_operator* out);
 sd_status sd_operator_gpt_sharded(sd_gpt g, sd_comm comm, const uint64_t* begins, const uint64_t* ends,
                                   sd_operator* out);
 /* Lanczos operator y = H x of an MLP engine (all-reduced over comm if given) */

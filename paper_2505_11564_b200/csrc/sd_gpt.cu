@@ -137,11 +137,23 @@ struct sd_gpt_s {
   std::vector<Slot> slots;
   const float* theta = nullptr;
   float *theta_s = nullptr, *v_s = nullptr;
-  std::vector<Layer> L;
+  // Pipeline stage (Llama-style family; the whole model is the one-stage
+  // case): layers [l0, l1), the token embedding on the first stage, the final
+  // norm + head + loss on the last. The stage's parameters are the contiguous
+  // slice [pbase, pbase + Pst) of the flat declaration-order layout, so theta,
+  // v and Hv are stage-local. Micro-batches (nmb of B x S tokens) run through
+  // `nsets` activation sets (set = micro-batch % nsets: a 1F1B schedule keeps
+  // at most n_stages - stage micro-batches in flight on a stage).
+  int l0 = 0, l1 = 0, nmb = 1, nsets = 1;
+  bool first = true, last = true;
+  long long pbase = 0, Pst = 0;
+  Layer* L = nullptr;  // layers of the current set, indexed l - l0
+  std::vector<std::vector<Layer>> LS;
+  std::vector<float*> XS;  // per set: [x | dx] (2 T d, contiguous: one message)
   float *x, *dx;
   float *xhf, *dxhf, *rf, *drf, *hf, *hfs, *dhf, *dhfs;
   float *z, *zs, *dz, *dzs;
-  float *gx, *gdx, *gxs, *gdxs, *gh, *ghs, *gdh, *gdhs;
+  float *gx, *gdx, *gxs, *gdxs, *gh, *ghs, *gdh, *gdhs;  // gx | gdx contiguous (2 T d)
   float *go, *gos, *gdo, *gdos, *ga, *gas, *gda, *gdas;
   float *gP, *gPs, *gdP, *gdPs, *gu, *gus, *gdu, *gdus;
   float *ga_mlp = nullptr, *gda_mlp = nullptr;
@@ -149,38 +161,54 @@ struct sd_gpt_s {
   float *gqkv = nullptr, *gqkvs = nullptr, *gdqkv = nullptr, *gdqkvs = nullptr;
   int KV = 0, W = 0;  // key/value heads, raw q|k|v width
   bool gqa() const { return KV != H; }
-  double* loss_rows = nullptr;
+  double* loss_rows = nullptr;  // nmb * T (last stage)
   float* red = nullptr;  // column-reduction scratch
+  // per micro-batch m: tok/tgt/upos at m T, uniq/ustart at m (T + 1)
   int *tok = nullptr, *tgt = nullptr, *uniq = nullptr, *ustart = nullptr, *upos = nullptr;
-  int n_uniq = 0;
+  std::vector<int> n_uniq_mb;
   float loss_scale = 1.0f;
   bool have_batch = false;
   std::vector<double> h_loss;
+  // current stage pass: v, Hv (stage-local), micro-batch accumulation flag
+  const float* vcur = nullptr;
+  float* hvcur = nullptr;
+  bool acc = false;
 
   void carve(Plan& p) {
     const long long T_ = T, d = c.d, ff = c.ff, ffw = c.arch == SD_ARCH_LLAMA ? 2 * ff : ff;
     auto td = [&] { return p.take<float>(T_ * d); };
-    L.resize(c.n_layer);
-    for (auto& l : L) {
-      l.xh1 = td(), l.dxh1 = td(), l.h1 = td(), l.h1s = td(), l.dh1 = td(), l.dh1s = td();
-      l.r1 = p.take<float>(T_), l.dr1 = p.take<float>(T_);
-      l.a = p.take<float>(T_ * 3 * d), l.as = p.take<float>(T_ * 3 * d);
-      l.da = p.take<float>(T_ * 3 * d), l.das = p.take<float>(T_ * 3 * d);
-      // P, dP residuals are formed on chip by their (64-wide attention) consumers
-      l.P = p.take<float>(BHSS), l.Ps = nullptr, l.dP = p.take<float>(BHSS), l.dPs = nullptr;
-      l.o = td(), l.os = td(), l.dO = td(), l.dOs = td();
-      l.xh2 = td(), l.dxh2 = td(), l.h2 = td(), l.h2s = td(), l.dh2 = td(), l.dh2s = td();
-      l.r2 = p.take<float>(T_), l.dr2 = p.take<float>(T_);
-      // GPT-2: MLP pre-activation [T, ff]; Llama: [gate | up] pre-activations [T, 2ff]
-      l.f = p.take<float>(T_ * ffw), l.df = p.take<float>(T_ * ffw);
-      l.u = p.take<float>(T_ * ff), l.us = p.take<float>(T_ * ff);
-      l.du = p.take<float>(T_ * ff), l.dus = p.take<float>(T_ * ff);
+    LS.assign(nsets, std::vector<Layer>(l1 - l0));
+    XS.assign(nsets, nullptr);
+    for (int si = 0; si < nsets; ++si) {
+      for (auto& l : LS[si]) {
+        l.xh1 = td(), l.dxh1 = td(), l.h1 = td(), l.h1s = td(), l.dh1 = td(), l.dh1s = td();
+        l.r1 = p.take<float>(T_), l.dr1 = p.take<float>(T_);
+        l.a = p.take<float>(T_ * 3 * d), l.as = p.take<float>(T_ * 3 * d);
+        l.da = p.take<float>(T_ * 3 * d), l.das = p.take<float>(T_ * 3 * d);
+        // P, dP residuals are formed on chip by their (64-wide attention) consumers
+        l.P = p.take<float>(BHSS), l.Ps = nullptr, l.dP = p.take<float>(BHSS), l.dPs = nullptr;
+        l.o = td(), l.os = td(), l.dO = td(), l.dOs = td();
+        l.xh2 = td(), l.dxh2 = td(), l.h2 = td(), l.h2s = td(), l.dh2 = td(), l.dh2s = td();
+        l.r2 = p.take<float>(T_), l.dr2 = p.take<float>(T_);
+        // GPT-2: MLP pre-activation [T, ff]; Llama: [gate | up] pre-activations [T, 2ff]
+        l.f = p.take<float>(T_ * ffw), l.df = p.take<float>(T_ * ffw);
+        l.u = p.take<float>(T_ * ff), l.us = p.take<float>(T_ * ff);
+        l.du = p.take<float>(T_ * ff), l.dus = p.take<float>(T_ * ff);
+        if (gqa())
+          l.qkv = p.take<float>(T_ * W), l.qkvs = p.take<float>(T_ * W), l.dqkv = p.take<float>(T_ * W),
+          l.dqkvs = p.take<float>(T_ * W);
+      }
+      XS[si] = p.take<float>(2 * T_ * d);
     }
-    x = td(), dx = td();
-    xhf = td(), dxhf = td(), hf = td(), hfs = td(), dhf = td(), dhfs = td();
-    rf = p.take<float>(T_), drf = p.take<float>(T_);
-    z = p.take<float>(T_ * Vp), zs = p.take<float>(T_ * Vp), dz = p.take<float>(T_ * Vp), dzs = p.take<float>(T_ * Vp);
-    gx = td(), gdx = td(), gxs = td(), gdxs = td(), gh = td(), ghs = td(), gdh = td(), gdhs = td();
+    if (last) {
+      xhf = td(), dxhf = td(), hf = td(), hfs = td(), dhf = td(), dhfs = td();
+      rf = p.take<float>(T_), drf = p.take<float>(T_);
+      z = p.take<float>(T_ * Vp), zs = p.take<float>(T_ * Vp), dz = p.take<float>(T_ * Vp),
+      dzs = p.take<float>(T_ * Vp);
+      loss_rows = p.take<double>(T_ * nmb);
+    }
+    gx = p.take<float>(2 * T_ * d), gdx = gx ? gx + T_ * d : nullptr;
+    gxs = td(), gdxs = td(), gh = td(), ghs = td(), gdh = td(), gdhs = td();
     go = td(), gos = td(), gdo = td(), gdos = td();
     ga = p.take<float>(T_ * 3 * d), gas = p.take<float>(T_ * 3 * d);
     gda = p.take<float>(T_ * 3 * d), gdas = p.take<float>(T_ * 3 * d);
@@ -190,18 +218,23 @@ struct sd_gpt_s {
     if (c.arch == SD_ARCH_LLAMA) {  // adjoint (+ tangent) of the SwiGLU output [T, ff]
       ga_mlp = p.take<float>(T_ * ff), gda_mlp = p.take<float>(T_ * ff);
     }
-    if (gqa()) {
-      for (auto& l : L)
-        l.qkv = p.take<float>(T_ * W), l.qkvs = p.take<float>(T_ * W), l.dqkv = p.take<float>(T_ * W),
-        l.dqkvs = p.take<float>(T_ * W);
+    if (gqa())
       gqkv = p.take<float>(T_ * W), gqkvs = p.take<float>(T_ * W), gdqkv = p.take<float>(T_ * W),
       gdqkvs = p.take<float>(T_ * W);
-    }
-    theta_s = p.take<float>(P), v_s = p.take<float>(P);
-    loss_rows = p.take<double>(T_);
+    theta_s = p.take<float>(Pst), v_s = p.take<float>(Pst);
     red = p.take<float>(2LL * 64 * std::max(3 * d, ff));
-    tok = p.take<int>(T_), tgt = p.take<int>(T_), uniq = p.take<int>(T_ + 1), ustart = p.take<int>(T_ + 1);
-    upos = p.take<int>(T_);
+    if (first) {
+      tok = p.take<int>(T_ * nmb), uniq = p.take<int>((T_ + 1) * nmb), ustart = p.take<int>((T_ + 1) * nmb);
+      upos = p.take<int>(T_ * nmb);
+    }
+    if (last) tgt = p.take<int>(T_ * nmb);
+    use_set(0);
+  }
+  void use_set(int m) {
+    const int si = m % nsets;
+    L = LS[si].data();
+    x = XS[si];
+    dx = x ? x + (long long)T * c.d : nullptr;
   }
 
   // ---- GEMM helper: C = alpha op(A) op(B) + beta C (+bias), 3xTF32
@@ -259,8 +292,8 @@ struct sd_gpt_s {
     g.onchip = true;
   }
 
-  const float* th(int i) const { return theta + slots[i].off; }
-  const float* ths(int i) const { return theta_s + slots[i].off; }
+  const float* th(int i) const { return theta + (slots[i].off - pbase); }
+  const float* ths(int i) const { return theta_s + (slots[i].off - pbase); }
 
   void hvp(const float* v, float* hv, cudaStream_t st) {
     if (!have_batch) fail(SD_STATE_ERROR, "gpt: set_batch was not called");
@@ -361,26 +394,43 @@ struct sd_gpt_s {
     }
     // embeddings (wte also carries the head contribution written above)
     SD_CUDA(cudaMemsetAsync(HV(1), 0, slots[1].rows * slots[1].cols * sizeof(float), st));
-    sd::gpt_embed_bwd(uniq, ustart, upos, n_uniq, B, S, d, gdx, HV(0), HV(1), st);
+    sd::gpt_embed_bwd(uniq, ustart, upos, n_uniq_mb[0], B, S, d, gdx, HV(0), HV(1), st);
   }
 
   // Llama-style decoder (oracle/src/models.cpp build_llama): same forward-over-
   // reverse scheme as hvp(); RMSNorm via the LN kernels' rms mode, RoPE on q/k
   // after the fused QKV product (inverse rotation on their adjoints), SwiGLU on
-  // the fused [gate | up] product, untied head, no biases.
+  // the fused [gate | up] product, untied head, no biases. The whole model is
+  // the one-stage pipeline: begin, then forward + backward of each micro-batch.
   void hvp_llama(const float* v, float* hv, cudaStream_t st) {
-    const int d = c.d, ff = c.ff, V = c.vocab;
-    const long long Td = (long long)T * d;
+    stage_begin(v, hv, st);
+    for (int m = 0; m < nmb; ++m) {
+      stage_fwd(m, st);
+      stage_bwd(m, st);
+    }
+  }
+
+  // stage-local views of v, its tf32 residual and Hv for parameter slot i
+  const float* V_(int i) const { return vcur + (slots[i].off - pbase); }
+  const float* Vs(int i) const { return v_s + (slots[i].off - pbase); }
+  float* HV(int i) const { return hvcur + (slots[i].off - pbase); }
+
+  void stage_begin(const float* v, float* hv, cudaStream_t st) {
+    if (!have_batch) fail(SD_STATE_ERROR, "gpt: set_batch was not called");
+    vcur = v, hvcur = hv;
+    sd::gpt_residual(v, v_s, Pst, st);
+  }
+
+  // Forward (primal + tangent) of micro-batch m through layers [l0, l1). The
+  // set's [x | dx] holds the stage input (the first stage embeds the tokens)
+  // and, on return, the stage output.
+  void stage_fwd(int m, cudaStream_t st) {
+    const int d = c.d, ff = c.ff;
     const float sc = 1.0f / std::sqrt(float(dh)), eps = 1e-5f;
-    auto V_ = [&](int i) { return v + slots[i].off; };
-    auto Vs = [&](int i) { return v_s + slots[i].off; };
-    auto HV = [&](int i) { return hv + slots[i].off; };
-    const int fL = 1 + 6 * c.n_layer, head = fL + 1;  // final norm, output head
-    sd::gpt_residual(v, v_s, P, st);
-    // ------------------------------------------------------------ forward
-    sd::gpt_embed(tok, T, S, d, th(0), nullptr, V_(0), nullptr, x, dx, st);
-    for (int l = 0; l < c.n_layer; ++l) {
-      Layer& Ly = L[l];
+    use_set(m);
+    if (first) sd::gpt_embed(tok + (long long)m * T, T, S, d, th(0), nullptr, V_(0), nullptr, x, dx, st);
+    for (int l = l0; l < l1; ++l) {
+      Layer& Ly = L[l - l0];
       const int b = 1 + 6 * l;  // attention_norm
       sd::LnArgs la{x, dx, th(b), nullptr, V_(b), nullptr, T, d, eps,
                     Ly.h1, Ly.h1s, Ly.dh1, Ly.dh1s, Ly.xh1, Ly.dxh1, Ly.r1, Ly.dr1, 1};
@@ -409,48 +459,67 @@ struct sd_gpt_s {
       mm2(T, d, ff, {Ly.du, Ly.dus, ff, false}, {th(b + 5), ths(b + 5), d, true}, {Ly.u, Ly.us, ff, false},
           {V_(b + 5), Vs(b + 5), d, true}, dx, d, 1, 1, st);
     }
-    sd::LnArgs lf{x, dx, th(fL), nullptr, V_(fL), nullptr, T, d, eps, hf, hfs, dhf, dhfs, xhf, dxhf, rf, drf, 1};
-    sd::gpt_ln_fwd(lf, st);
-    // logits z = hf W_out^T ; dz = dhf W_out^T + hf VW_out^T
-    mm(T, V, d, {hf, hfs, d, false}, {th(head), ths(head), d, false}, z, Vp, 1, 0, st);
-    mm2(T, V, d, {dhf, dhfs, d, false}, {th(head), ths(head), d, false}, {hf, hfs, d, false},
-        {V_(head), Vs(head), d, false}, dz, Vp, 1, 0, st);
-    sd::gpt_ce(z, dz, zs, dzs, tgt, T, V, Vp, loss_scale, loss_rows, st);
-    // ----------------------------------------------------------- backward
-    mm(T, d, V, {z, zs, Vp, false}, {th(head), ths(head), d, true}, gh, d, 1, 0, st);
-    mm2(T, d, V, {dz, dzs, Vp, false}, {th(head), ths(head), d, true}, {z, zs, Vp, false},
-        {V_(head), Vs(head), d, true}, gdh, d, 1, 0, st);
-    mm2(V, d, T, {dz, dzs, Vp, true}, {hf, hfs, d, true}, {z, zs, Vp, true}, {dhf, dhfs, d, true}, HV(head), d, 1, 0,
-        st);
-    SD_CUDA(cudaMemsetAsync(gx, 0, Td * sizeof(float), st));
-    SD_CUDA(cudaMemsetAsync(gdx, 0, Td * sizeof(float), st));
-    sd::LnBwdArgs bf{gh, gdh, th(fL), V_(fL), xhf, dxhf, rf, drf, T, d, gx, gdx, gxs, gdxs, HV(fL), nullptr, red, 1};
-    sd::gpt_ln_bwd(bf, st);
-    for (int l = c.n_layer - 1; l >= 0; --l) {
-      Layer& Ly = L[l];
+  }
+
+  // Backward (adjoint + adjoint tangent) of micro-batch m. The last stage
+  // forms the adjoint from the head and the loss; other stages find the
+  // adjoint of their output in [gx | gdx]. On return [gx | gdx] holds the
+  // adjoint of the stage input (the first stage scatters it into the
+  // embedding's Hv instead). Hv of micro-batch m > 0 accumulates.
+  void stage_bwd(int m, cudaStream_t st) {
+    const int d = c.d, ff = c.ff, V = c.vocab;
+    const long long Td = (long long)T * d;
+    const float sc = 1.0f / std::sqrt(float(dh)), eps = 1e-5f;
+    const float hb = m > 0 ? 1.0f : 0.0f;  // beta of the Hv products
+    const int fL = 1 + 6 * c.n_layer, head = fL + 1;  // final norm, output head
+    use_set(m);
+    acc = m > 0;
+    if (last) {
+      sd::LnArgs lf{x, dx, th(fL), nullptr, V_(fL), nullptr, T, d, eps, hf, hfs, dhf, dhfs, xhf, dxhf, rf, drf, 1};
+      sd::gpt_ln_fwd(lf, st);
+      // logits z = hf W_out^T ; dz = dhf W_out^T + hf VW_out^T
+      mm(T, V, d, {hf, hfs, d, false}, {th(head), ths(head), d, false}, z, Vp, 1, 0, st);
+      mm2(T, V, d, {dhf, dhfs, d, false}, {th(head), ths(head), d, false}, {hf, hfs, d, false},
+          {V_(head), Vs(head), d, false}, dz, Vp, 1, 0, st);
+      sd::gpt_ce(z, dz, zs, dzs, tgt + (long long)m * T, T, V, Vp, loss_scale, loss_rows + (long long)m * T, st);
+      mm(T, d, V, {z, zs, Vp, false}, {th(head), ths(head), d, true}, gh, d, 1, 0, st);
+      mm2(T, d, V, {dz, dzs, Vp, false}, {th(head), ths(head), d, true}, {z, zs, Vp, false},
+          {V_(head), Vs(head), d, true}, gdh, d, 1, 0, st);
+      mm2(V, d, T, {dz, dzs, Vp, true}, {hf, hfs, d, true}, {z, zs, Vp, true}, {dhf, dhfs, d, true}, HV(head), d, 1,
+          hb, st);
+      SD_CUDA(cudaMemsetAsync(gx, 0, 2 * Td * sizeof(float), st));
+      sd::LnBwdArgs bf{gh, gdh, th(fL), V_(fL), xhf, dxhf, rf, drf, T, d, gx, gdx, gxs, gdxs, HV(fL), nullptr, red, 1,
+                       int(acc)};
+      sd::gpt_ln_bwd(bf, st);
+    } else {  // received adjoint: its tf32 residuals (what the producing ln_bwd wrote)
+      sd::gpt_residual(gx, gxs, Td, st);
+      sd::gpt_residual(gdx, gdxs, Td, st);
+    }
+    for (int l = l1 - 1; l >= l0; --l) {
+      Layer& Ly = L[l - l0];
       const int b = 1 + 6 * l;
       // down projection: ga = gx Wd^T ; gda = gdx Wd^T + gx VWd^T ; Hv_Wd = da^T gx + a^T gdx
       mm(T, ff, d, {gx, gxs, d, false}, {th(b + 5), ths(b + 5), d, false}, ga_mlp, ff, 1, 0, st);
       mm2(T, ff, d, {gdx, gdxs, d, false}, {th(b + 5), ths(b + 5), d, false}, {gx, gxs, d, false},
           {V_(b + 5), Vs(b + 5), d, false}, gda_mlp, ff, 1, 0, st);
       mm2(ff, d, T, {Ly.du, Ly.dus, ff, true}, {gx, gxs, d, true}, {Ly.u, Ly.us, ff, true}, {gdx, gdxs, d, true},
-          HV(b + 5), d, 1, 0, st);
+          HV(b + 5), d, 1, hb, st);
       sd::llama_swiglu_bwd(Ly.f, Ly.df, ga_mlp, gda_mlp, gu, gus, gdu, gdus, T, ff, st);
       // gate|up: gh = gfu Wgu^T ; gdh = gdfu Wgu^T + gfu VWgu^T ; Hv_Wgu = dh2^T gfu + h2^T gdfu
       mm(T, d, 2 * ff, {gu, gus, 2 * ff, false}, {th(b + 4), ths(b + 4), 2 * ff, false}, gh, d, 1, 0, st);
       mm2(T, d, 2 * ff, {gdu, gdus, 2 * ff, false}, {th(b + 4), ths(b + 4), 2 * ff, false},
           {gu, gus, 2 * ff, false}, {V_(b + 4), Vs(b + 4), 2 * ff, false}, gdh, d, 1, 0, st);
       mm2(d, 2 * ff, T, {Ly.dh2, Ly.dh2s, d, true}, {gu, gus, 2 * ff, true}, {Ly.h2, Ly.h2s, d, true},
-          {gdu, gdus, 2 * ff, true}, HV(b + 4), 2 * ff, 1, 0, st);
+          {gdu, gdus, 2 * ff, true}, HV(b + 4), 2 * ff, 1, hb, st);
       sd::LnBwdArgs b2{gh, gdh, th(b + 3), V_(b + 3), Ly.xh2, Ly.dxh2, Ly.r2, Ly.dr2, T, d,
-                       gx, gdx, gxs, gdxs, HV(b + 3), nullptr, red, 1};
+                       gx, gdx, gxs, gdxs, HV(b + 3), nullptr, red, 1, int(acc)};
       sd::gpt_ln_bwd(b2, st);
       // attention output projection
       mm(T, d, d, {gx, gxs, d, false}, {th(b + 2), ths(b + 2), d, false}, go, d, 1, 0, st, nullptr, gos);
       mm2(T, d, d, {gdx, gdxs, d, false}, {th(b + 2), ths(b + 2), d, false}, {gx, gxs, d, false},
           {V_(b + 2), Vs(b + 2), d, false}, gdo, d, 1, 0, st, nullptr, gdos);
       mm2(d, d, T, {Ly.dO, Ly.dOs, d, true}, {gx, gxs, d, true}, {Ly.o, Ly.os, d, true}, {gdx, gdxs, d, true},
-          HV(b + 2), d, 1, 0, st);
+          HV(b + 2), d, 1, hb, st);
       attention_bwd(Ly, sc, st);
       // adjoints of the pre-rotation q, k: the inverse rotation; GQA: sum the
       // expanded heads' k/v adjoints back into their KV heads
@@ -464,13 +533,16 @@ struct sd_gpt_s {
       mm2(T, d, W, {qgd, qgds, W, false}, {th(b + 1), ths(b + 1), W, false}, {qg, qgs, W, false},
           {V_(b + 1), Vs(b + 1), W, false}, gdh, d, 1, 0, st);
       mm2(d, W, T, {Ly.dh1, Ly.dh1s, d, true}, {qg, qgs, W, true}, {Ly.h1, Ly.h1s, d, true}, {qgd, qgds, W, true},
-          HV(b + 1), W, 1, 0, st);
+          HV(b + 1), W, 1, hb, st);
       sd::LnBwdArgs b1{gh, gdh, th(b), V_(b), Ly.xh1, Ly.dxh1, Ly.r1, Ly.dr1, T, d,
-                       gx, gdx, gxs, gdxs, HV(b), nullptr, red, 1};
+                       gx, gdx, gxs, gdxs, HV(b), nullptr, red, 1, int(acc)};
       sd::gpt_ln_bwd(b1, st);
     }
-    SD_CUDA(cudaMemsetAsync(HV(0), 0, slots[0].rows * slots[0].cols * sizeof(float), st));
-    sd::gpt_embed_bwd(uniq, ustart, upos, n_uniq, B, S, d, gdx, HV(0), nullptr, st);
+    if (first) {
+      if (!acc) SD_CUDA(cudaMemsetAsync(HV(0), 0, slots[0].rows * slots[0].cols * sizeof(float), st));
+      sd::gpt_embed_bwd(uniq + (long long)m * (T + 1), ustart + (long long)m * (T + 1), upos + (long long)m * T,
+                        n_uniq_mb[m], B, S, d, gdx, HV(0), nullptr, st);
+    }
   }
 
   // per (batch b, head h): S = sc q k^T ; dS = sc (dq k^T + q dk^T) ; P, dP = softmax R-op ;
@@ -533,7 +605,21 @@ struct sd_gpt_s {
 
 namespace {
 
-Plan plan_for(const sd_gpt_config& c, int B, int S, char* base, sd_gpt_s* g) {
+// First parameter slot of layer l (l = n_layer: the final norm) in the Llama layout.
+int llama_slot(const sd_gpt_config& c, int l) { return l == 0 ? 0 : 1 + 6 * l; }
+
+// Stage parameter slice [begin, end) of the flat layout: the embedding goes
+// with layer 0, the final norm and head with the last layer.
+void stage_range(const sd_gpt_config& c, int l0, int l1, const std::vector<Slot>& s, uint64_t* b, uint64_t* e) {
+  *b = s[llama_slot(c, l0)].off;
+  *e = l1 == c.n_layer ? s.back().off + s.back().rows * s.back().cols : s[1 + 6 * l1].off;
+}
+
+struct StageSpec {
+  int l0 = 0, l1 = -1, nmb = 1, nsets = 1;
+};
+
+Plan plan_for(const sd_gpt_config& c, int B, int S, char* base, sd_gpt_s* g, StageSpec sp = {}) {
   sd_gpt_s tmp;
   sd_gpt_s* e = g ? g : &tmp;
   e->c = c;
@@ -543,10 +629,28 @@ Plan plan_for(const sd_gpt_config& c, int B, int S, char* base, sd_gpt_s* g) {
   e->P = (long long)param_count(c);
   e->KV = c.n_kv_head > 0 ? c.n_kv_head : c.n_head;
   e->W = c.d + 2 * e->KV * e->dh;
+  e->l0 = sp.l0, e->l1 = sp.l1 < 0 ? c.n_layer : sp.l1;
+  e->nmb = sp.nmb, e->nsets = sp.nsets;
+  e->first = e->l0 == 0, e->last = e->l1 == c.n_layer;
+  if (e->first && e->last) {
+    e->pbase = 0, e->Pst = e->P;
+  } else {
+    uint64_t b0, b1;
+    stage_range(c, e->l0, e->l1, layout(c), &b0, &b1);
+    e->pbase = (long long)b0, e->Pst = (long long)(b1 - b0);
+  }
   Plan p;
   p.base = base;
   e->carve(p);
   return p;
+}
+
+void check_stage(const sd_gpt_config& c, const StageSpec& sp) {
+  const bool whole = sp.l0 == 0 && sp.l1 == c.n_layer;
+  if (sp.l0 < 0 || sp.l1 > c.n_layer || sp.l0 >= sp.l1) fail(SD_LAYOUT_ERROR, "stage layer range out of bounds");
+  if (sp.nmb < 1 || sp.nsets < 1 || sp.nsets > sp.nmb) fail(SD_ARGUMENT_ERROR, "need 1 <= n_sets <= n_micro");
+  if ((!whole || sp.nmb > 1) && c.arch != SD_ARCH_LLAMA)
+    fail(SD_CONFIG_ERROR, "pipeline stages / micro-batches need the untied Llama-style layout");
 }
 
 struct GptOpCtx {
@@ -587,6 +691,41 @@ sd_status gpt_shard_apply(void* ctx, const void* x, void* y, sd_stream st) {
                               cudaMemcpyDeviceToDevice, s));
     sd::comm_reducescatter_f32(c->comm, c->slots, c->mine, ml, s);
     SD_CUDA(cudaMemcpyAsync(y, c->mine, n * sizeof(float), cudaMemcpyDeviceToDevice, s));
+  });
+}
+
+// Pipeline-parallel apply (sd_operator_gpt_pipeline): stage = comm rank; x, y
+// are this stage's parameter slice of the Lanczos vectors. The 1F1B schedule
+// (sd_pipeline_schedule) drives the engine's per-micro-batch forward and
+// backward; [x | dx] of a set and [gx | gdx] are the boundary messages.
+struct GptPipeCtx {
+  sd_gpt g;
+  sd_comm comm;
+  int nst = 1, st = 0;
+  std::vector<int> ops;
+};
+
+sd_status gpt_pipe_apply(void* ctx, const void* x, void* y, sd_stream sp) {
+  auto* c = static_cast<GptPipeCtx*>(ctx);
+  return sd::guard([&] {
+    const cudaStream_t s = (cudaStream_t)sp;
+    sd_gpt g = c->g;
+    const uint64_t n2 = 2ull * uint64_t(g->T) * uint64_t(g->c.d);
+    g->stage_begin(static_cast<const float*>(x), static_cast<float*>(y), s);
+    for (size_t i = 0; i < c->ops.size(); i += 2) {
+      const int m = c->ops[i + 1];
+      switch (c->ops[i]) {
+        case SD_PIPE_F: g->stage_fwd(m, s); break;
+        case SD_PIPE_B: g->stage_bwd(m, s); break;
+        case SD_PIPE_SEND_F: g->use_set(m), sd::comm_send_f32(c->comm, g->x, n2, c->st + 1, s); break;
+        case SD_PIPE_RECV_F: g->use_set(m), sd::comm_recv_f32(c->comm, g->x, n2, c->st - 1, s); break;
+        case SD_PIPE_SEND_B: sd::comm_send_f32(c->comm, g->gx, n2, c->st - 1, s); break;
+        case SD_PIPE_RECV_B: sd::comm_recv_f32(c->comm, g->gx, n2, c->st + 1, s); break;
+        case SD_PIPE_GROUP_BEGIN: sd::comm_group_begin(c->comm); break;
+        case SD_PIPE_GROUP_END: sd::comm_group_end(c->comm); break;
+        default: fail(SD_PROTOCOL_ERROR, "pipeline: unknown schedule op");
+      }
+    }
   });
 }
 
@@ -632,79 +771,170 @@ sd_status sd_gpt_init_params(const sd_gpt_config* c, uint64_t seed, double gain_
 }
 
 uint64_t sd_gpt_workspace_bytes(const sd_gpt_config* c, int batch, int seq) {
+  return sd_gpt_stage_workspace_bytes(c, batch, seq, 1, 0, c ? c->n_layer : 0, 1);
+}
+
+uint64_t sd_gpt_stage_workspace_bytes(const sd_gpt_config* c, int micro_batch, int seq, int n_micro, int layer_begin,
+                                      int layer_end, int n_sets) {
   try {
-    check_cfg(*c, batch, seq);
-    return plan_for(*c, batch, seq, nullptr, nullptr).bytes;
+    if (!c) fail(SD_ARGUMENT_ERROR, "null config");
+    check_cfg(*c, micro_batch, seq);
+    const StageSpec sp{layer_begin, layer_end, n_micro, n_sets};
+    check_stage(*c, sp);
+    return plan_for(*c, micro_batch, seq, nullptr, nullptr, sp).bytes;
   } catch (const std::exception& e) {
     sd::set_last_error(e.what());
     return 0;
   }
 }
 
-sd_status sd_gpt_create(const sd_gpt_config* c, int batch, int seq, const float* theta, void* ws, uint64_t bytes,
-                        sd_stream s, sd_gpt* out) {
+sd_status sd_gpt_stage_params(const sd_gpt_config* c, int layer_begin, int layer_end, uint64_t* begin,
+                              uint64_t* end) {
   return sd::guard([&] {
-    check_cfg(*c, batch, seq);
+    if (!c || !begin || !end) fail(SD_ARGUMENT_ERROR, "null argument");
+    check_cfg(*c, 1, 4);
+    check_stage(*c, StageSpec{layer_begin, layer_end, 1, 1});
+    if (layer_begin == 0 && layer_end == c->n_layer) {
+      *begin = 0, *end = param_count(*c);
+      return;
+    }
+    stage_range(*c, layer_begin, layer_end, layout(*c), begin, end);
+  });
+}
+
+sd_status sd_gpt_stage_create(const sd_gpt_config* c, int micro_batch, int seq, int n_micro, int layer_begin,
+                              int layer_end, int n_sets, const float* theta_stage, void* ws, uint64_t bytes,
+                              sd_stream s, sd_gpt* out) {
+  return sd::guard([&] {
+    if (!c || !out) fail(SD_ARGUMENT_ERROR, "null argument");
+    check_cfg(*c, micro_batch, seq);
+    const StageSpec sp{layer_begin, layer_end, n_micro, n_sets};
+    check_stage(*c, sp);
     auto g = std::make_unique<sd_gpt_s>();
-    const Plan p = plan_for(*c, batch, seq, static_cast<char*>(ws), g.get());
+    const Plan p = plan_for(*c, micro_batch, seq, static_cast<char*>(ws), g.get(), sp);
     if (bytes < p.bytes) fail(SD_ARGUMENT_ERROR, "gpt workspace too small");
     g->slots = layout(*c);
-    g->theta = theta;
-    sd::gpt_residual(theta, g->theta_s, g->P, (cudaStream_t)s);
-    // padded logits columns are never read as values but feed TMA boxes: zero them once
-    SD_CUDA(cudaMemsetAsync(g->z, 0, size_t(g->T) * g->Vp * 4, (cudaStream_t)s));
-    SD_CUDA(cudaMemsetAsync(g->zs, 0, size_t(g->T) * g->Vp * 4, (cudaStream_t)s));
-    SD_CUDA(cudaMemsetAsync(g->dz, 0, size_t(g->T) * g->Vp * 4, (cudaStream_t)s));
-    SD_CUDA(cudaMemsetAsync(g->dzs, 0, size_t(g->T) * g->Vp * 4, (cudaStream_t)s));
+    g->theta = theta_stage;
+    sd::gpt_residual(theta_stage, g->theta_s, g->Pst, (cudaStream_t)s);
+    if (g->last) {  // padded logits columns are never read as values but feed TMA boxes: zero them once
+      for (float* z : {g->z, g->zs, g->dz, g->dzs})
+        SD_CUDA(cudaMemsetAsync(z, 0, size_t(g->T) * g->Vp * 4, (cudaStream_t)s));
+    }
     *out = g.release();
   });
 }
 
-// Uploads a batch (host int32 tokens/targets, batch*seq each) and builds the
-// token -> positions CSR used by the deterministic embedding backward.
+sd_status sd_gpt_create(const sd_gpt_config* c, int batch, int seq, const float* theta, void* ws, uint64_t bytes,
+                        sd_stream s, sd_gpt* out) {
+  return sd_gpt_stage_create(c, batch, seq, 1, 0, c ? c->n_layer : 0, 1, theta, ws, bytes, s, out);
+}
+
+// Uploads a batch (host int32 tokens/targets, n_micro * batch * seq each) and
+// builds per micro-batch the token -> positions CSR of the deterministic
+// embedding backward. Tokens are used by the first stage, targets by the last.
 sd_status sd_gpt_set_batch(sd_gpt g, const int* tokens, const int* targets, float loss_scale, sd_stream s) {
   return sd::guard([&] {
-    const int T = g->T;
-    for (int t = 0; t < T; ++t)
+    const int T = g->T, M = g->nmb;
+    for (long long t = 0; t < (long long)T * M; ++t)
       if (tokens[t] < 0 || tokens[t] >= g->c.vocab || targets[t] < 0 || targets[t] >= g->c.vocab)
         fail(SD_ARGUMENT_ERROR, "token id out of range");
-    std::vector<int> order(T);
-    std::iota(order.begin(), order.end(), 0);
-    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return tokens[a] < tokens[b]; });
-    std::vector<int> uniq, start;
-    for (int i = 0; i < T; ++i)
-      if (i == 0 || tokens[order[i]] != tokens[order[i - 1]]) {
-        uniq.push_back(tokens[order[i]]);
-        start.push_back(i);
-      }
-    start.push_back(T);
     cudaStream_t st = (cudaStream_t)s;
-    SD_CUDA(cudaMemcpyAsync(g->tok, tokens, T * sizeof(int), cudaMemcpyHostToDevice, st));
-    SD_CUDA(cudaMemcpyAsync(g->tgt, targets, T * sizeof(int), cudaMemcpyHostToDevice, st));
-    SD_CUDA(cudaMemcpyAsync(g->uniq, uniq.data(), uniq.size() * sizeof(int), cudaMemcpyHostToDevice, st));
-    SD_CUDA(cudaMemcpyAsync(g->ustart, start.data(), start.size() * sizeof(int), cudaMemcpyHostToDevice, st));
-    SD_CUDA(cudaMemcpyAsync(g->upos, order.data(), T * sizeof(int), cudaMemcpyHostToDevice, st));
+    g->n_uniq_mb.assign(M, 0);
+    if (g->first) {
+      std::vector<int> uniq(size_t(T + 1) * M, 0), start(size_t(T + 1) * M, 0), order(size_t(T) * M);
+      for (int m = 0; m < M; ++m) {
+        const int* tk = tokens + (long long)m * T;
+        int* ord = order.data() + (long long)m * T;
+        std::iota(ord, ord + T, 0);
+        std::stable_sort(ord, ord + T, [&](int a, int b) { return tk[a] < tk[b]; });
+        int* u = uniq.data() + (long long)m * (T + 1);
+        int* st0 = start.data() + (long long)m * (T + 1);
+        int n = 0;
+        for (int i = 0; i < T; ++i)
+          if (i == 0 || tk[ord[i]] != tk[ord[i - 1]]) u[n] = tk[ord[i]], st0[n++] = i;
+        st0[n] = T;
+        g->n_uniq_mb[m] = n;
+      }
+      SD_CUDA(cudaMemcpyAsync(g->tok, tokens, size_t(T) * M * sizeof(int), cudaMemcpyHostToDevice, st));
+      SD_CUDA(cudaMemcpyAsync(g->uniq, uniq.data(), uniq.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+      SD_CUDA(cudaMemcpyAsync(g->ustart, start.data(), start.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+      SD_CUDA(cudaMemcpyAsync(g->upos, order.data(), order.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+    }
+    if (g->last)
+      SD_CUDA(cudaMemcpyAsync(g->tgt, targets, size_t(T) * M * sizeof(int), cudaMemcpyHostToDevice, st));
     SD_CUDA(cudaStreamSynchronize(st));
-    g->n_uniq = int(uniq.size());
     g->loss_scale = loss_scale;
     g->have_batch = true;
   });
 }
 
 sd_status sd_gpt_hvp(sd_gpt g, const float* v, float* hv, sd_stream s) {
-  return sd::guard([&] { g->hvp(v, hv, (cudaStream_t)s); });
+  return sd::guard([&] {
+    if (!g->first || !g->last) fail(SD_STATE_ERROR, "gpt: a pipeline stage runs through the stage calls");
+    g->hvp(v, hv, (cudaStream_t)s);
+  });
+}
+
+sd_status sd_gpt_stage_begin(sd_gpt g, const float* v_stage, float* hv_stage, sd_stream s) {
+  return sd::guard([&] {
+    if (g->c.arch != SD_ARCH_LLAMA) fail(SD_CONFIG_ERROR, "pipeline stages need the Llama-style layout");
+    g->stage_begin(v_stage, hv_stage, (cudaStream_t)s);
+  });
+}
+
+// x_in/dx_in: stage input (ignored on the first stage); x_out/dx_out: stage
+// output (may be null; the last stage keeps it for its backward).
+sd_status sd_gpt_stage_forward(sd_gpt g, int m, const float* x_in, const float* dx_in, float* x_out, float* dx_out,
+                               sd_stream s) {
+  return sd::guard([&] {
+    if (!g->vcur) fail(SD_STATE_ERROR, "gpt: stage_begin was not called");
+    if (m < 0 || m >= g->nmb) fail(SD_ARGUMENT_ERROR, "micro-batch index out of range");
+    const cudaStream_t st = (cudaStream_t)s;
+    const size_t n = size_t(g->T) * g->c.d * sizeof(float);
+    g->use_set(m);
+    if (!g->first) {
+      if (!x_in || !dx_in) fail(SD_ARGUMENT_ERROR, "stage input missing");
+      SD_CUDA(cudaMemcpyAsync(g->x, x_in, n, cudaMemcpyDeviceToDevice, st));
+      SD_CUDA(cudaMemcpyAsync(g->dx, dx_in, n, cudaMemcpyDeviceToDevice, st));
+    }
+    g->stage_fwd(m, st);
+    if (x_out) SD_CUDA(cudaMemcpyAsync(x_out, g->x, n, cudaMemcpyDeviceToDevice, st));
+    if (dx_out) SD_CUDA(cudaMemcpyAsync(dx_out, g->dx, n, cudaMemcpyDeviceToDevice, st));
+  });
+}
+
+// gx_in/gdx_in: adjoint of the stage output (ignored on the last stage);
+// gx_out/gdx_out: adjoint of the stage input (may be null).
+sd_status sd_gpt_stage_backward(sd_gpt g, int m, const float* gx_in, const float* gdx_in, float* gx_out,
+                                float* gdx_out, sd_stream s) {
+  return sd::guard([&] {
+    if (!g->vcur) fail(SD_STATE_ERROR, "gpt: stage_begin was not called");
+    if (m < 0 || m >= g->nmb) fail(SD_ARGUMENT_ERROR, "micro-batch index out of range");
+    const cudaStream_t st = (cudaStream_t)s;
+    const size_t n = size_t(g->T) * g->c.d * sizeof(float);
+    if (!g->last) {
+      if (!gx_in || !gdx_in) fail(SD_ARGUMENT_ERROR, "stage adjoint input missing");
+      SD_CUDA(cudaMemcpyAsync(g->gx, gx_in, n, cudaMemcpyDeviceToDevice, st));
+      SD_CUDA(cudaMemcpyAsync(g->gdx, gdx_in, n, cudaMemcpyDeviceToDevice, st));
+    }
+    g->stage_bwd(m, st);
+    if (gx_out) SD_CUDA(cudaMemcpyAsync(gx_out, g->gx, n, cudaMemcpyDeviceToDevice, st));
+    if (gdx_out) SD_CUDA(cudaMemcpyAsync(gdx_out, g->gdx, n, cudaMemcpyDeviceToDevice, st));
+  });
 }
 
 // mean per-token loss of the most recent hvp (synchronises the stream)
 sd_status sd_gpt_last_loss(sd_gpt g, double* loss, sd_stream s) {
   return sd::guard([&] {
-    g->h_loss.resize(g->T);
-    SD_CUDA(cudaMemcpyAsync(g->h_loss.data(), g->loss_rows, g->T * sizeof(double), cudaMemcpyDeviceToHost,
+    if (!g->last) fail(SD_STATE_ERROR, "gpt: the loss lives on the last pipeline stage");
+    const size_t n = size_t(g->T) * g->nmb;
+    g->h_loss.resize(n);
+    SD_CUDA(cudaMemcpyAsync(g->h_loss.data(), g->loss_rows, n * sizeof(double), cudaMemcpyDeviceToHost,
                             (cudaStream_t)s));
     SD_CUDA(cudaStreamSynchronize((cudaStream_t)s));
     double acc = 0.0;
     for (double x : g->h_loss) acc += x;
-    *loss = acc / g->T;
+    *loss = acc / double(n);
   });
 }
 
@@ -716,9 +946,31 @@ sd_status sd_gpt_destroy(sd_gpt g) {
 // (data-sharded HVP; the loss_scale of every rank is 1/global_tokens).
 sd_status sd_operator_gpt(sd_gpt g, sd_comm comm, sd_operator* out) {
   return sd::guard([&] {
+    if (!g || !g->first || !g->last) fail(SD_ARGUMENT_ERROR, "gpt operator needs a whole-model engine");
     auto* ctx = new GptOpCtx{g, comm};  // lives as long as the process (tiny)
     const sd_status st = sd_operator_custom(uint64_t(g->P), gpt_apply, ctx, out);
     if (st != SD_OK) fail(st, "operator_custom failed");
+  });
+}
+
+sd_status sd_operator_gpt_pipeline(sd_gpt g, sd_comm comm, sd_operator* out) {
+  return sd::guard([&] {
+    if (!g || !out) fail(SD_ARGUMENT_ERROR, "null argument");
+    auto c = std::make_unique<GptPipeCtx>();
+    c->g = g, c->comm = comm;
+    c->nst = sd::comm_size(comm), c->st = sd::comm_rank(comm);
+    if (g->first != (c->st == 0) || g->last != (c->st == c->nst - 1))
+      fail(SD_LAYOUT_ERROR, "pipeline: the engine's layers do not match this rank's stage");
+    const int need = std::min(g->nmb, c->nst - c->st);
+    if (g->nsets < need) fail(SD_CONFIG_ERROR, "pipeline: stage needs min(n_micro, n_stages - stage) activation sets");
+    uint64_t n = 0;
+    if (sd_pipeline_schedule(c->nst, c->st, g->nmb, nullptr, 0, &n) != SD_OK) fail(SD_ARGUMENT_ERROR, sd_last_error());
+    c->ops.resize(2 * n);
+    if (sd_pipeline_schedule(c->nst, c->st, g->nmb, c->ops.data(), n, &n) != SD_OK)
+      fail(SD_ARGUMENT_ERROR, sd_last_error());
+    const sd_status st = sd_operator_custom(uint64_t(g->P), gpt_pipe_apply, c.get(), out);
+    if (st != SD_OK) fail(st, "operator_custom failed");
+    c.release();  // lives as long as the process (one per engine)
   });
 }
 
@@ -728,6 +980,7 @@ sd_status sd_operator_gpt_sharded(sd_gpt g, sd_comm comm, const uint64_t* begins
                                   sd_operator* out) {
   return sd::guard([&] {
     if (!g || !begins || !ends) sd::fail(SD_ARGUMENT_ERROR, "null argument");
+    if (!g->first || !g->last) fail(SD_ARGUMENT_ERROR, "sharded gpt operator needs a whole-model engine");
     auto* c = new GptShardCtx();  // lives as long as the process (one per engine)
     c->g = g;
     c->comm = comm;

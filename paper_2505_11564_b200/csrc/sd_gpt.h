@@ -19,6 +19,7 @@ struct LnBwdArgs {
   float *hv_g, *hv_b;
   float* scratch;  // >= 2 * 64 * d floats
   int rms = 0;
+  int acc = 0;  // hv_g/hv_b += (micro-batch accumulation) instead of =
 };
 
 void gpt_embed(const int* tok, int T, int S, int d, const float* wte, const float* wpe, const float* vwte,
@@ -42,7 +43,8 @@ void llama_swiglu_bwd(const float* fu, const float* dfu, const float* ga, const 
                       float* gdfu, float* gdfus, int T, int ff, cudaStream_t s);
 void gpt_ln_fwd(const LnArgs& a, cudaStream_t s);
 void gpt_ln_bwd(const LnBwdArgs& a, cudaStream_t s);
-void gpt_colsum(const float* a, int T, int n, long long lda, float* out, float* scratch, cudaStream_t s);
+void gpt_colsum(const float* a, int T, int n, long long lda, float* out, float* scratch, cudaStream_t s,
+                int acc = 0);
 void gpt_gelu_fwd(const float* f, const float* df, float* u, float* us, float* du, float* dus, long long n,
                   cudaStream_t s);
 void gpt_gelu_bwd(const float* f, const float* df, float* gu, float* gdu, float* gus, float* gdus, long long n,

@@ -206,15 +206,15 @@ __global__ void k_colred1(const float* __restrict__ a, const float* __restrict__
 }
 
 __global__ void k_colred2(const float* __restrict__ part, int groups, int n, float* __restrict__ out0,
-                          float* __restrict__ out1) {
+                          float* __restrict__ out1, int acc) {
   const int col = blockIdx.x * blockDim.x + threadIdx.x;
   if (col >= n) return;
   float t0 = 0.f, t1 = 0.f;
   for (int g = 0; g < groups; ++g) t0 += part[(long long)g * n + col];
-  out0[col] = t0;
+  out0[col] = acc ? out0[col] + t0 : t0;  // acc: micro-batch accumulation (pipeline stages)
   if (out1) {
     for (int g = 0; g < groups; ++g) t1 += part[(long long)(groups + g) * n + col];
-    out1[col] = t1;
+    out1[col] = acc ? out1[col] + t1 : t1;
   }
 }
 
@@ -610,16 +610,16 @@ void gpt_ln_bwd(const LnBwdArgs& a, cudaStream_t s) {
   k_colred1<1><<<dim3(unsigned((a.d + 31) / 32), unsigned(groups)), 256, 0, s>>>(a.gy, a.gdy, a.xh, a.dxh, a.T, a.d,
                                                                                  a.d, a.scratch);
   SD_LAUNCHED("k_colred1");
-  k_colred2<<<unsigned((a.d + 255) / 256), 256, 0, s>>>(a.scratch, groups, a.d, a.hv_g, a.hv_b);
+  k_colred2<<<unsigned((a.d + 255) / 256), 256, 0, s>>>(a.scratch, groups, a.d, a.hv_g, a.hv_b, a.acc);
   SD_LAUNCHED("k_colred2");
 }
 
-void gpt_colsum(const float* a, int T, int n, long long lda, float* out, float* scratch, cudaStream_t s) {
+void gpt_colsum(const float* a, int T, int n, long long lda, float* out, float* scratch, cudaStream_t s, int acc) {
   const int groups = std::min(kRowGroups, std::max(1, T / 64));
   k_colred1<0><<<dim3(unsigned((n + 31) / 32), unsigned(groups)), 256, 0, s>>>(a, nullptr, nullptr, nullptr, T, n, lda,
                                                                               scratch);
   SD_LAUNCHED("k_colred1");
-  k_colred2<<<unsigned((n + 255) / 256), 256, 0, s>>>(scratch, groups, n, out, nullptr);
+  k_colred2<<<unsigned((n + 255) / 256), 256, 0, s>>>(scratch, groups, n, out, nullptr, acc);
   SD_LAUNCHED("k_colred2");
 }
 

@@ -162,6 +162,10 @@ struct NcclApi {
   ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*ReduceScatter)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                                 cudaStream_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
 };
 static NcclApi& nccl() {
@@ -176,6 +180,10 @@ static NcclApi& nccl() {
     a.AllReduce = (decltype(a.AllReduce))dlsym(h, "ncclAllReduce");
     a.AllGather = (decltype(a.AllGather))dlsym(h, "ncclAllGather");
     a.ReduceScatter = (decltype(a.ReduceScatter))dlsym(h, "ncclReduceScatter");
+    a.Send = (decltype(a.Send))dlsym(h, "ncclSend");
+    a.Recv = (decltype(a.Recv))dlsym(h, "ncclRecv");
+    a.GroupStart = (decltype(a.GroupStart))dlsym(h, "ncclGroupStart");
+    a.GroupEnd = (decltype(a.GroupEnd))dlsym(h, "ncclGroupEnd");
     a.GetErrorString = (decltype(a.GetErrorString))dlsym(h, "ncclGetErrorString");
     return a;
   }();
@@ -218,6 +226,24 @@ void comm_reducescatter_f32(sd_comm c, const float* send, float* recv, uint64_t 
   }
   if (!nccl().ReduceScatter) fail(SD_NCCL_ERROR, "ncclReduceScatter unavailable");
   nccl_check(nccl().ReduceScatter(send, recv, n, ncclFloat32, ncclSum, c->comm, s), "ncclReduceScatter");
+}
+
+// Point-to-point (pipeline stages): f32 payloads to/from a peer rank; between
+// group_begin/group_end the sends and receives progress together (NCCL group
+// semantics), which is what makes the 1F1B exchanges deadlock-free.
+void comm_send_f32(sd_comm c, const float* buf, uint64_t n, int peer, cudaStream_t s) {
+  if (!c || !c->comm) fail(SD_STATE_ERROR, "point-to-point send without a communicator");
+  nccl_check(nccl().Send(buf, n, ncclFloat32, peer, c->comm, s), "ncclSend");
+}
+void comm_recv_f32(sd_comm c, float* buf, uint64_t n, int peer, cudaStream_t s) {
+  if (!c || !c->comm) fail(SD_STATE_ERROR, "point-to-point receive without a communicator");
+  nccl_check(nccl().Recv(buf, n, ncclFloat32, peer, c->comm, s), "ncclRecv");
+}
+void comm_group_begin(sd_comm c) {
+  if (c && c->comm) nccl_check(nccl().GroupStart(), "ncclGroupStart");
+}
+void comm_group_end(sd_comm c) {
+  if (c && c->comm) nccl_check(nccl().GroupEnd(), "ncclGroupEnd");
 }
 
 int comm_rank(sd_comm c) { return c ? c->rank : 0; }
@@ -283,6 +309,55 @@ sd_status sd_split_evenly(uint64_t dim, uint64_t n, uint64_t* begins, uint64_t* 
     }
     *count = w;
     validate(dim, w, begins, ends);
+  });
+}
+
+// One-forward-one-backward pipeline schedule of `stage` among `n_stages` for
+// `n_micro` micro-batches: (kind, micro-batch) pairs, kinds SD_PIPE_*. Warm-up
+// forwards (n_stages - stage - 1 of them), then alternating F/B with the
+// boundary exchanges grouped as {send F, recv B} and {send B, recv F} so that
+// neighbouring stages post matching groups, then the cool-down backwards.
+// Micro-batches finish in order, so a stage holds at most n_stages - stage of
+// them (its activation sets). ops == NULL: only *count is returned.
+sd_status sd_pipeline_schedule(int n_stages, int stage, int n_micro, int* ops, uint64_t cap, uint64_t* count) {
+  return guard([&] {
+    if (n_stages < 1 || stage < 0 || stage >= n_stages || n_micro < 1)
+      fail(SD_ARGUMENT_ERROR, "pipeline schedule: need 0 <= stage < n_stages and n_micro >= 1");
+    std::vector<int> v;
+    auto op = [&](int k, int m) { v.push_back(k), v.push_back(m); };
+    const bool has_prev = stage > 0, has_next = stage < n_stages - 1;
+    const int warm = std::min(n_stages - stage - 1, n_micro), rest = n_micro - warm;
+    for (int i = 0; i < warm; ++i) {
+      if (has_prev) op(SD_PIPE_RECV_F, i);
+      op(SD_PIPE_F, i);
+      if (has_next) op(SD_PIPE_SEND_F, i);
+    }
+    if (rest > 0 && has_prev) op(SD_PIPE_RECV_F, warm);
+    for (int i = 0; i < rest; ++i) {
+      op(SD_PIPE_F, warm + i);
+      if (has_next) {
+        op(SD_PIPE_GROUP_BEGIN, -1), op(SD_PIPE_SEND_F, warm + i), op(SD_PIPE_RECV_B, i), op(SD_PIPE_GROUP_END, -1);
+      }
+      op(SD_PIPE_B, i);
+      if (has_prev) {
+        if (i == rest - 1) {
+          op(SD_PIPE_SEND_B, i);
+        } else {
+          op(SD_PIPE_GROUP_BEGIN, -1), op(SD_PIPE_SEND_B, i), op(SD_PIPE_RECV_F, warm + i + 1);
+          op(SD_PIPE_GROUP_END, -1);
+        }
+      }
+    }
+    for (int i = rest; i < n_micro; ++i) {
+      if (has_next) op(SD_PIPE_RECV_B, i);
+      op(SD_PIPE_B, i);
+      if (has_prev) op(SD_PIPE_SEND_B, i);
+    }
+    *count = v.size() / 2;
+    if (ops) {
+      if (cap < v.size() / 2) fail(SD_ARGUMENT_ERROR, "pipeline schedule: output too small");
+      std::copy(v.begin(), v.end(), ops);
+    }
   });
 }
 

@@ -55,6 +55,18 @@ def _L():
             "sd_operator_gpt": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_void_p)]),
             "sd_operator_gpt_sharded": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_uint64),
                                                   C.POINTER(C.c_uint64), C.POINTER(C.c_void_p)]),
+            "sd_gpt_stage_workspace_bytes": (C.c_uint64, [cp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int]),
+            "sd_gpt_stage_params": (C.c_int, [cp, C.c_int, C.c_int, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
+            "sd_gpt_stage_create": (C.c_int, [cp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p,
+                                              C.c_void_p, C.c_uint64, C.c_void_p, C.POINTER(C.c_void_p)]),
+            "sd_gpt_stage_begin": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+            "sd_gpt_stage_forward": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                               C.c_void_p]),
+            "sd_gpt_stage_backward": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                                C.c_void_p]),
+            "sd_operator_gpt_pipeline": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_void_p)]),
+            "sd_pipeline_schedule": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_uint64,
+                                               C.POINTER(C.c_uint64)]),
         }
         for n, (r, a) in sig.items():
             f = getattr(L, n)
@@ -175,6 +187,125 @@ class GptHvp:
         else:
             check(_L().sd_operator_gpt(self.h, ch, C.byref(h)))
         return OperatorHandle(self.P, f"gpt_hvp(L={self.cfg['n_layer']},d={self.cfg['d']})", h, keepalive=self)
+
+    def close(self):
+        if self.h:
+            _L().sd_gpt_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# ------------------------------------------------------------ pipeline stages
+PIPE_F, PIPE_B, PIPE_SEND_F, PIPE_RECV_F, PIPE_SEND_B, PIPE_RECV_B, PIPE_GROUP_BEGIN, PIPE_GROUP_END = range(8)
+PIPE_NAMES = ["F", "B", "SEND_F", "RECV_F", "SEND_B", "RECV_B", "GROUP_BEGIN", "GROUP_END"]
+
+
+def pipeline_schedule(n_stages: int, stage: int, n_micro: int):
+    """1F1B schedule of one stage as [(kind, micro_batch)] (sd_pipeline_schedule; host only)."""
+    n = C.c_uint64()
+    check(_L().sd_pipeline_schedule(n_stages, stage, n_micro, None, 0, C.byref(n)))
+    ops = np.zeros(2 * n.value, np.int32)
+    check(_L().sd_pipeline_schedule(n_stages, stage, n_micro, ops.ctypes.data, n.value, C.byref(n)))
+    return [(int(ops[2 * i]), int(ops[2 * i + 1])) for i in range(n.value)]
+
+
+def pipeline_layers(n_layer: int, n_stages: int):
+    """Contiguous layer ranges per stage: split_evenly over the layers
+    (layout.hpp:59-72 semantics: the first n_layer % n_stages get one more)."""
+    from .core import split_evenly
+    lay = split_evenly(n_layer, n_stages)
+    if len(lay.begins) != n_stages:
+        raise ValueError("more pipeline stages than layers")
+    return list(zip(lay.begins, lay.ends))
+
+
+def stage_params(cfg: dict, layer_begin: int, layer_end: int):
+    """[begin, end) of the stage's slice of the flat parameter vector."""
+    b, e = C.c_uint64(), C.c_uint64()
+    check(_L().sd_gpt_stage_params(C.byref(_cfg(cfg)), layer_begin, layer_end, C.byref(b), C.byref(e)))
+    return int(b.value), int(e.value)
+
+
+def pipeline_layout(cfg: dict, n_stages: int):
+    """The Lanczos ShardLayout of a pipeline: shard r = stage r's parameters."""
+    from .core import ShardLayout, validate_layout
+    lay = ShardLayout(param_count(cfg), tuple(stage_params(cfg, a, b)
+                                              for a, b in pipeline_layers(cfg["n_layer"], n_stages)))
+    validate_layout(lay)
+    return lay
+
+
+class GptStage:
+    """One pipeline stage (layers [layer_begin, layer_end)) of the Llama-style
+    engine on the current device: stage-local theta (a slice of the flat
+    parameters), n_micro micro-batches through n_sets activation sets."""
+
+    def __init__(self, cfg: dict, micro_batch: int, seq: int, n_micro: int, layer_begin: int, layer_end: int,
+                 theta_stage: torch.Tensor, n_sets: int | None = None, tokens=None, targets=None,
+                 loss_scale: float | None = None, stream=None):
+        self.cfg = dict(cfg)
+        self.B, self.S, self.M = micro_batch, seq, n_micro
+        self.l0, self.l1 = layer_begin, layer_end
+        self.n_sets = n_micro if n_sets is None else n_sets
+        self._c = _cfg(cfg)
+        self.P = param_count(cfg)
+        self.begin, self.end = stage_params(cfg, layer_begin, layer_end)
+        self.device = torch.device("cuda", torch.cuda.current_device())
+        self.stream = stream or torch.cuda.current_stream()
+        assert theta_stage.dtype == torch.float32 and theta_stage.numel() == self.end - self.begin
+        self.theta = theta_stage
+        nbytes = _L().sd_gpt_stage_workspace_bytes(C.byref(self._c), micro_batch, seq, n_micro, layer_begin,
+                                                   layer_end, self.n_sets)
+        if nbytes == 0:  # invalid shape: the create call raises the precise error class
+            check(_L().sd_gpt_stage_create(C.byref(self._c), micro_batch, seq, n_micro, layer_begin, layer_end,
+                                           self.n_sets, None, None, 0, self._s(), C.byref(C.c_void_p())))
+        self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        self.h = C.c_void_p()
+        check(_L().sd_gpt_stage_create(C.byref(self._c), micro_batch, seq, n_micro, layer_begin, layer_end,
+                                       self.n_sets, theta_stage.data_ptr(), self.workspace.data_ptr(), nbytes,
+                                       self._s(), C.byref(self.h)))
+        if tokens is None:
+            tokens, targets = synthetic_tokens(cfg["vocab"], micro_batch * n_micro, seq)
+        tok = np.ascontiguousarray(tokens, dtype=np.int32)
+        tgt = np.ascontiguousarray(targets, dtype=np.int32)
+        assert tok.size == n_micro * micro_batch * seq == tgt.size
+        scale = 1.0 / tok.size if loss_scale is None else loss_scale
+        check(_L().sd_gpt_set_batch(self.h, tok.ctypes.data, tgt.ctypes.data, scale, self._s()))
+
+    def _s(self):
+        return C.c_void_p(self.stream.cuda_stream)
+
+    @staticmethod
+    def _p(t):
+        return None if t is None else t.data_ptr()
+
+    def begin_pass(self, v_stage: torch.Tensor, hv_stage: torch.Tensor):
+        check(_L().sd_gpt_stage_begin(self.h, v_stage.data_ptr(), hv_stage.data_ptr(), self._s()))
+
+    def forward(self, m: int, x_in=None, dx_in=None, x_out=None, dx_out=None):
+        check(_L().sd_gpt_stage_forward(self.h, m, self._p(x_in), self._p(dx_in), self._p(x_out), self._p(dx_out),
+                                        self._s()))
+
+    def backward(self, m: int, gx_in=None, gdx_in=None, gx_out=None, gdx_out=None):
+        check(_L().sd_gpt_stage_backward(self.h, m, self._p(gx_in), self._p(gdx_in), self._p(gx_out),
+                                         self._p(gdx_out), self._s()))
+
+    def loss(self) -> float:
+        x = C.c_double()
+        check(_L().sd_gpt_last_loss(self.h, C.byref(x), self._s()))
+        return x.value
+
+    def operator(self, comm) -> OperatorHandle:
+        """Pipeline operator: comm rank r = this stage; x/y are the stage's slice."""
+        h = C.c_void_p()
+        check(_L().sd_operator_gpt_pipeline(self.h, comm.handle if comm is not None else None, C.byref(h)))
+        return OperatorHandle(self.P, f"gpt_pipeline(L={self.cfg['n_layer']},stage={self.l0}-{self.l1})", h,
+                              keepalive=self)
 
     def close(self):
         if self.h:
