@@ -14,6 +14,7 @@
 
 #include <cmath>
 #include <cstdint>
+#include <map>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -411,13 +412,14 @@ inline OperatorHandle spiked_operator(std::size_t n, double sigma, const std::ve
 }
 
 // ---- lanczos and quadrature
-enum class Reorthogonalize { none, full };
+enum class Reorthogonalize { none, full, selective };
 struct LanczosConfig {
   std::size_t k_max = 10;
   double breakdown_tol = -1.0;  // <= 0: 1e-12 (f64) / 1e-7 (f32)
   Reorthogonalize reorthogonalize = Reorthogonalize::none;
   ProbeSpec probe;
   Precision prec = Precision::f64;
+  std::size_t window = 0;  // selective: keep the W >= 2 most recent basis vectors (extension)
 };
 struct TridiagonalMatrix {
   std::vector<double> alphas, betas;
@@ -430,9 +432,12 @@ struct LanczosRun {
 };
 
 inline LanczosRun lanczos_run(const OperatorHandle& op, const LanczosConfig& cfg, WorkerPool& pool) {
-  sd_lanczos_config c{cfg.k_max, cfg.breakdown_tol,
-                      cfg.reorthogonalize == Reorthogonalize::full ? SD_REORTH_FULL : SD_REORTH_NONE,
-                      prec_code(cfg.prec), cfg.probe.seed, dist_code(cfg.probe.distribution), 0};
+  const int ro = cfg.reorthogonalize == Reorthogonalize::full        ? SD_REORTH_FULL
+                 : cfg.reorthogonalize == Reorthogonalize::selective ? SD_REORTH_SELECTIVE
+                                                                     : SD_REORTH_NONE;
+  sd_lanczos_config c{cfg.k_max, cfg.breakdown_tol, ro, prec_code(cfg.prec), cfg.probe.seed,
+                      dist_code(cfg.probe.distribution), 0};
+  c.selective_window = cfg.window;
   const uint64_t b = 0, e = op.dim;
   const uint64_t bytes = sd_lanczos_workspace_bytes(&b, &e, op.dim, &c, 1, 0);
   if (!bytes) check(SD_CONFIG_ERROR);
@@ -463,6 +468,219 @@ inline RitzSpectrum ritz_decompose(const TridiagonalMatrix& t) {
   check(sd_ritz_decompose(t.k(), t.alphas.data(), t.betas.empty() ? nullptr : t.betas.data(), s.values.data(),
                           s.weights.data(), &s.residual));
   return s;
+}
+
+
+// ---- autodiff: hvp / batched_hvp (Alg. 1)
+// ModelSpec architectures: mlp(layer_widths) with mse and the
+// decoder family the SPEC's attention_block grows into (GPT-2 style, or
+// Llama style: sd_gpt_config.arch). The device engine computes in fp32
+// (3xTF32 tensor-core GEMMs), so vectors must be Precision::f32.
+struct ModelSpec {
+  enum class Arch { mlp, transformer } arch = Arch::mlp;
+  std::vector<std::uint64_t> layer_widths;  // mlp
+  sd_gpt_config transformer{};              // transformer
+  static ModelSpec mlp(std::vector<std::uint64_t> widths) {
+    ModelSpec m;
+    m.arch = Arch::mlp;
+    m.layer_widths = std::move(widths);
+    return m;
+  }
+  static ModelSpec decoder(const sd_gpt_config& c) {
+    ModelSpec m;
+    m.arch = Arch::transformer;
+    m.transformer = c;
+    return m;
+  }
+  std::size_t parameter_count() const {
+    return arch == Arch::mlp ? sd_mlp_param_count(layer_widths.data(), int(layer_widths.size()))
+                             : sd_gpt_param_count(&transformer);
+  }
+};
+
+// One batch: token rows (transformer: rows x seq tokens and next-token
+// targets) or feature rows (mlp: rows x w0 features, rows x w_last targets).
+struct Batch {
+  int rows = 0, seq = 0;
+  std::vector<int> tokens, token_targets;
+  std::vector<float> x, y;
+  // the samples Alg. 1 weights by: tokens (cross-entropy) or rows (mse)
+  std::size_t samples() const { return tokens.empty() ? std::size_t(rows) : tokens.size(); }
+};
+
+// Parameters (device, f32) plus the HVP engines of one model; transformer
+// engines are built per batch shape on first use and share the parameters.
+class Model {
+ public:
+  // transformer with the synthetic counter-keyed init (sd_gpt_init_params)
+  Model(WorkerPool& pool, const ModelSpec& spec, std::uint64_t init_seed, double gain_scale = 0.0,
+        double bias_scale = 0.0)
+      : spec_(spec), P_(spec.parameter_count()), theta_(P_ * 4) {
+    if (spec.arch != ModelSpec::Arch::transformer) throw config_error("this constructor builds transformer models");
+    if (P_ == 0) check(SD_CONFIG_ERROR);
+    check(sd_gpt_init_params(&spec_.transformer, init_seed, gain_scale, bias_scale,
+                             static_cast<float*>(theta_.get()), pool.stream()));
+    pool.sync();
+  }
+  // mlp with caller parameters (flat declaration order, f32-representable), n_max rows per batch
+  Model(WorkerPool& pool, const ModelSpec& spec, const std::vector<double>& params, int n_max)
+      : spec_(spec), P_(spec.parameter_count()), theta_(P_ * 4) {
+    (void)pool;
+    if (spec.arch != ModelSpec::Arch::mlp) throw config_error("this constructor builds mlp models");
+    if (params.size() != P_) throw layout_error("parameter count does not match the model");
+    std::vector<float> f(params.begin(), params.end());
+    cuda_ok(cudaMemcpy(theta_.get(), f.data(), P_ * 4, cudaMemcpyHostToDevice));
+    sd_mlp m = nullptr;
+    check(sd_mlp_create(spec_.layer_widths.data(), int(spec_.layer_widths.size()), n_max,
+                        static_cast<const float*>(theta_.get()), pool.stream(), &m));
+    mlp_.reset(m, sd_mlp_destroy);
+    n_max_ = n_max;
+  }
+  std::size_t parameter_count() const { return P_; }
+  const ModelSpec& spec() const { return spec_; }
+
+  // Hv (full logical vectors on device) of one batch with loss weight `scale`
+  void hvp_device(WorkerPool& pool, const Batch& b, float scale, const float* v, float* hv) {
+    if (spec_.arch == ModelSpec::Arch::mlp) {
+      const int w0 = int(spec_.layer_widths.front()), wl = int(spec_.layer_widths.back());
+      if (b.rows < 1) throw argument_error("empty batch");
+      if (b.rows > n_max_) throw argument_error("batch exceeds the engine's row capacity");
+      if (b.x.size() != std::size_t(b.rows) * w0 || b.y.size() != std::size_t(b.rows) * wl)
+        throw argument_error("inconsistent sample dimensions");
+      check(sd_mlp_set_batch(mlp_.get(), b.x.data(), b.y.data(), b.rows, scale, pool.stream()));
+      check(sd_mlp_hvp(mlp_.get(), v, hv, pool.stream()));
+      return;
+    }
+    if (b.rows < 1 || b.seq < 1) throw argument_error("empty batch");
+    if (b.tokens.size() != std::size_t(b.rows) * b.seq || b.token_targets.size() != b.tokens.size())
+      throw argument_error("inconsistent sample dimensions");
+    Engine& e = engine(pool, b.rows, b.seq);
+    check(sd_gpt_set_batch(e.g.get(), b.tokens.data(), b.token_targets.data(), scale, pool.stream()));
+    check(sd_gpt_hvp(e.g.get(), v, hv, pool.stream()));
+  }
+
+ private:
+  struct Engine {
+    DeviceBuffer ws;
+    std::shared_ptr<sd_gpt_s> g;
+  };
+  Engine& engine(WorkerPool& pool, int rows, int seq) {
+    const auto key = std::make_pair(rows, seq);
+    auto it = engines_.find(key);
+    if (it != engines_.end()) return it->second;
+    const uint64_t bytes = sd_gpt_workspace_bytes(&spec_.transformer, rows, seq);
+    if (!bytes) {  // invalid shape: the create call reports the precise error class
+      sd_gpt g = nullptr;
+      check(sd_gpt_create(&spec_.transformer, rows, seq, static_cast<const float*>(theta_.get()), nullptr, 0,
+                          pool.stream(), &g));
+    }
+    // built in place: the engine keeps pointers into its workspace (DeviceBuffer copies, it does not move)
+    Engine& e = engines_[key];
+    try {
+      e.ws = DeviceBuffer(bytes);
+      sd_gpt g = nullptr;
+      check(sd_gpt_create(&spec_.transformer, rows, seq, static_cast<const float*>(theta_.get()), e.ws.get(), bytes,
+                          pool.stream(), &g));
+      e.g.reset(g, sd_gpt_destroy);
+    } catch (...) {
+      engines_.erase(key);
+      throw;
+    }
+    return e;
+  }
+  ModelSpec spec_;
+  std::size_t P_ = 0;
+  DeviceBuffer theta_;
+  std::shared_ptr<sd_mlp_s> mlp_;
+  int n_max_ = 0;
+  std::map<std::pair<int, int>, Engine> engines_;
+};
+
+namespace detail {
+inline DeviceBuffer gather_device(const ShardedVector& x) {
+  const std::size_t es = x.esize();
+  DeviceBuffer full(x.dim() * es);
+  for (std::size_t w = 0; w < x.layout.worker_count(); ++w)
+    cuda_ok(cudaMemcpy(static_cast<char*>(full.get()) + x.layout.shard_bounds[w].begin * es, x.shards[w].get(),
+                       x.layout.shard_bounds[w].size() * es, cudaMemcpyDeviceToDevice));
+  return full;
+}
+inline void scatter_device(const DeviceBuffer& full, ShardedVector& y) {
+  const std::size_t es = y.esize();
+  for (std::size_t w = 0; w < y.layout.worker_count(); ++w)
+    cuda_ok(cudaMemcpy(y.shards[w].get(), static_cast<const char*>(full.get()) + y.layout.shard_bounds[w].begin * es,
+                       y.layout.shard_bounds[w].size() * es, cudaMemcpyDeviceToDevice));
+}
+inline void check_model_vector(WorkerPool& pool, const Model& m, const ShardedVector& v) {
+  check_pool(pool, v);
+  if (v.dim() != m.parameter_count()) throw layout_error("vector dimension does not match the model");
+  if (v.prec != Precision::f32) throw config_error("the HVP engine computes in f32: use Precision::f32 vectors");
+}
+}  // namespace detail
+
+// Hv of the batch-mean loss (Pearlmutter, forward-over-reverse on device)
+inline ShardedVector hvp(WorkerPool& pool, Model& m, const Batch& batch, const ShardedVector& v) {
+  detail::check_model_vector(pool, m, v);
+  DeviceBuffer xf = detail::gather_device(v), yf(v.dim() * 4);
+  const double n = double(batch.samples()) *
+                   (m.spec().arch == ModelSpec::Arch::mlp ? double(m.spec().layer_widths.back()) : 1.0);
+  m.hvp_device(pool, batch, float(1.0 / n), static_cast<const float*>(xf.get()), static_cast<float*>(yf.get()));
+  pool.sync();
+  ShardedVector y = make_sharded(v.layout, v.prec);
+  detail::scatter_device(yf, y);
+  return y;
+}
+
+// SPEC.md:202-210 / Alg. 1 lines 5-16: sum_b |B_b| u_b / N -- every batch's
+// loss is weighted 1/N_total so its Hv already carries |B_b|/N; the per-batch
+// results are summed in loader order with the f32 axpy kernel.
+inline ShardedVector batched_hvp(WorkerPool& pool, Model& m, const std::vector<Batch>& loader,
+                                 const ShardedVector& v) {
+  detail::check_model_vector(pool, m, v);
+  if (loader.empty()) throw argument_error("batched_hvp needs at least one batch");
+  double N = 0;
+  for (const Batch& b : loader) N += double(b.samples());
+  if (m.spec().arch == ModelSpec::Arch::mlp) N *= double(m.spec().layer_widths.back());
+  DeviceBuffer xf = detail::gather_device(v), tmp(v.dim() * 4), acc(v.dim() * 4);
+  cuda_ok(cudaMemset(acc.get(), 0, v.dim() * 4));
+  detail::DevScalar one(1.0);
+  for (const Batch& b : loader) {
+    m.hvp_device(pool, b, float(1.0 / N), static_cast<const float*>(xf.get()), static_cast<float*>(tmp.get()));
+    check(sd_k_axpy(tmp.get(), acc.get(), v.dim(), one.p(), 1.0, SD_F32, pool.stream()));
+  }
+  pool.sync();
+  ShardedVector y = make_sharded(v.layout, v.prec);
+  detail::scatter_device(acc, y);
+  return y;
+}
+
+// The model's Hessian on one batch as an OperatorHandle (what lanczos_run drives).
+inline OperatorHandle hvp_operator(WorkerPool& pool, Model& m, const Batch& batch) {
+  struct Ctx {
+    Model* m;
+    Batch b;
+    WorkerPool* pool;
+    float scale;
+  };
+  const double n = double(batch.samples()) *
+                   (m.spec().arch == ModelSpec::Arch::mlp ? double(m.spec().layer_widths.back()) : 1.0);
+  auto* ctx = new Ctx{&m, batch, &pool, float(1.0 / n)};
+  static const sd_apply_fn fn = [](void* c, const void* x, void* y, sd_stream) -> sd_status {
+    auto* k = static_cast<Ctx*>(c);
+    try {
+      k->m->hvp_device(*k->pool, k->b, k->scale, static_cast<const float*>(x), static_cast<float*>(y));
+    } catch (const std::exception&) {
+      return SD_ARGUMENT_ERROR;
+    }
+    return SD_OK;
+  };
+  sd_operator op = nullptr;
+  check(sd_operator_custom(m.parameter_count(), fn, ctx, &op));
+  std::shared_ptr<sd_operator_s> h(op, [ctx](sd_operator o) {
+    sd_operator_destroy(o);
+    delete ctx;
+  });
+  return OperatorHandle{m.parameter_count(), "hvp", std::move(h)};
 }
 
 }  // namespace specden

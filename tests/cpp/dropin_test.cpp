@@ -138,3 +138,115 @@ TEST_CASE("lanczos on diag(1,2,3) with full reorth recovers its eigenvalues") {
   for (double x : s.weights) w += x;
   CHECK(std::abs(w - 1) < 1e-12);
 }
+
+// ---- autodiff surface: hvp / batched_hvp on the device engines
+static sd_gpt_config tiny_decoder() {
+  sd_gpt_config c{};
+  c.n_layer = 1, c.d = 32, c.n_head = 2, c.ff = 64, c.vocab = 48, c.ctx = 16, c.arch = SD_ARCH_GPT2;
+  c.rope_base = 10000.f, c.n_kv_head = 0;
+  return c;
+}
+static Batch token_batch(int rows, int seq, int vocab, std::uint64_t seed) {
+  Batch b;
+  b.rows = rows, b.seq = seq;
+  for (int i = 0; i < rows * seq; ++i) {
+    b.tokens.push_back(int(sd_uniform_index(seed, 2 * i, vocab)));
+    b.token_targets.push_back(int(sd_uniform_index(seed, 2 * i + 1, vocab)));
+  }
+  return b;
+}
+static Batch concat(const Batch& a, const Batch& b) {
+  Batch c = a;
+  c.rows += b.rows;
+  c.tokens.insert(c.tokens.end(), b.tokens.begin(), b.tokens.end());
+  c.token_targets.insert(c.token_targets.end(), b.token_targets.begin(), b.token_targets.end());
+  c.x.insert(c.x.end(), b.x.begin(), b.x.end());
+  c.y.insert(c.y.end(), b.y.begin(), b.y.end());
+  return c;
+}
+static double host_dot(const std::vector<double>& a, const std::vector<double>& b) {
+  double s = 0;
+  for (std::size_t i = 0; i < a.size(); ++i) s += a[i] * b[i];
+  return s;
+}
+static double rel_l2(const std::vector<double>& a, const std::vector<double>& b) {
+  double n = 0, d = 0;
+  for (std::size_t i = 0; i < a.size(); ++i) n += (a[i] - b[i]) * (a[i] - b[i]), d += b[i] * b[i];
+  return std::sqrt(n / d);
+}
+
+TEST_CASE("hvp on a decoder is symmetric and linear; batched_hvp weights batches by size") {
+  const ModelSpec spec = ModelSpec::decoder(tiny_decoder());
+  const std::size_t P = spec.parameter_count();
+  std::unique_ptr<WorkerPool> pool(pool_ptr(P, 3));
+  Model m(*pool, spec, 0, 0.1, 0.1);
+  const Batch b = token_batch(2, 16, 48, 7);
+  auto u = random_vector(*pool, 31, Precision::f32), w = random_vector(*pool, 32, Precision::f32);
+  auto hu = gather(*pool, hvp(*pool, m, b, u)), hw = gather(*pool, hvp(*pool, m, b, w));
+  const double a = host_dot(hu, gather(*pool, w)), c = host_dot(gather(*pool, u), hw);
+  CHECK(std::abs(a - c) <= 1e-5 * std::max(std::abs(a), std::abs(c)));
+  // linearity: H(u + w) = Hu + Hw
+  auto uw = hvp(*pool, m, b, axpy(*pool, 1.0, u, w));
+  std::vector<double> sum(hu.size());
+  for (std::size_t i = 0; i < sum.size(); ++i) sum[i] = hu[i] + hw[i];
+  CHECK(rel_l2(gather(*pool, uw), sum) < 1e-5);
+  // batches of 1 and 3 sequences == hvp over the concatenated 4
+  const Batch b1 = token_batch(1, 16, 48, 11), b3 = token_batch(3, 16, 48, 12);
+  auto split = gather(*pool, batched_hvp(*pool, m, {b1, b3}, u));
+  auto whole = gather(*pool, hvp(*pool, m, concat(b1, b3), u));
+  CHECK(rel_l2(split, whole) < 1e-5);
+  // a single batch is identical to hvp
+  CHECK(gather(*pool, batched_hvp(*pool, m, {b}, u)) == hu);
+  // errors
+  CHECK_THROWS_AS(hvp(*pool, m, b, random_vector(*pool, 1, Precision::f64)), config_error);
+  std::unique_ptr<WorkerPool> small(pool_ptr(P - 1, 1));
+  CHECK_THROWS_AS(hvp(*small, m, b, random_vector(*small, 1, Precision::f32)), layout_error);
+  CHECK_THROWS_AS(batched_hvp(*pool, m, {}, u), argument_error);
+  Batch bad = b;
+  bad.token_targets.pop_back();
+  CHECK_THROWS_AS(hvp(*pool, m, bad, u), argument_error);
+}
+
+TEST_CASE("mlp [4,8,1] with mse: batched_hvp over rows {1, 3} equals the 4-row batch") {
+  const ModelSpec spec = ModelSpec::mlp({4, 8, 1});
+  const std::size_t P = spec.parameter_count();
+  CHECK(P == 4 * 8 + 8 + 8 * 1 + 1);
+  std::unique_ptr<WorkerPool> pool(pool_ptr(P, 2));
+  std::vector<double> theta(P);
+  for (std::size_t i = 0; i < P; ++i) theta[i] = double(float(0.5 * sd_rademacher(3, i) * (1.0 + (i % 7) / 7.0)));
+  Model m(*pool, spec, theta, 8);
+  auto rows = [](int n, std::uint64_t seed) {
+    Batch b;
+    b.rows = n;
+    for (int i = 0; i < 4 * n; ++i) b.x.push_back(float(sd_rademacher(seed, i) * 0.25 * (1 + i % 3)));
+    for (int i = 0; i < n; ++i) b.y.push_back(float(0.1 * (i + 1)));
+    return b;
+  };
+  const Batch r1 = rows(1, 5), r3 = rows(3, 6);
+  auto v = random_vector(*pool, 41, Precision::f32);
+  auto split = gather(*pool, batched_hvp(*pool, m, {r1, r3}, v));
+  auto whole = gather(*pool, hvp(*pool, m, concat(r1, r3), v));
+  CHECK(rel_l2(split, whole) < 1e-6);
+  Batch too_big = rows(9, 1);
+  CHECK_THROWS_AS(hvp(*pool, m, too_big, v), argument_error);
+}
+
+TEST_CASE("lanczos_run drives the model's Hessian (full and selective reorth)") {
+  const ModelSpec spec = ModelSpec::decoder(tiny_decoder());
+  std::unique_ptr<WorkerPool> pool(pool_ptr(spec.parameter_count(), 1));
+  Model m(*pool, spec, 1, 0.1, 0.1);
+  auto op = hvp_operator(*pool, m, token_batch(2, 16, 48, 9));
+  LanczosConfig cfg;
+  cfg.k_max = 8;
+  cfg.prec = Precision::f32;
+  cfg.probe.distribution = ProbeDist::rademacher;
+  cfg.reorthogonalize = Reorthogonalize::full;
+  auto full = lanczos_run(op, cfg, *pool);
+  CHECK(full.t.k() == 8);
+  for (double a : full.t.alphas) CHECK(std::isfinite(a));
+  cfg.reorthogonalize = Reorthogonalize::selective;
+  cfg.window = 9;  // window >= k_max + 1 keeps every column: identical to full
+  auto sel = lanczos_run(op, cfg, *pool);
+  CHECK(sel.t.alphas == full.t.alphas);
+  CHECK(sel.t.betas == full.t.betas);
+}

@@ -130,3 +130,18 @@ def test_columnar_loader(tmp_path):
     p.write_text("1 2 3\n4 5\n")
     with pytest.raises(ConfigError):
         mlp.load_columnar(str(p))
+
+
+def test_cpp_dropin_header_compiles():
+    # the C++ drop-in layer (reference names, exception types, hvp/batched_hvp)
+    # and the reference-style C++ tests compile on the CPU box; they run on the GPU
+    import shutil
+    import subprocess
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    if shutil.which("g++") is None:
+        pytest.skip("no g++")
+    cmd = ["g++", "-std=c++20", "-fsyntax-only", "-Wall", "-Wextra", f"-I{root / 'include'}",
+           f"-I{root / 'oracle' / 'shims'}", "-I/usr/local/cuda/include", str(root / "tests" / "cpp" / "dropin_test.cpp")]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr[-3000:]
