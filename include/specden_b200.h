@@ -188,7 +188,10 @@ sd_status sd_gemm_tf32_dual(const sd_gemm_desc* d1, const sd_gemm_desc* d2, sd_s
  * 3xTF32 with the tf32 residuals of the raw operand tiles computed in shared
  * memory (a_small/b_small ignored; same result bits as passing
  * sd_split_tf32(mode 0) residuals, half the operand traffic). */
-enum { SD_GEMM_ONCHIP_RESIDUAL = 1 };
+/* SD_GEMM_B_EXACT / SD_GEMM_B2_EXACT: B (B2) holds tf32-exact values (e.g.
+ * bf16-valued weights): b_small may be NULL and the A.B_lo product is skipped
+ * (2 MMAs instead of 3; bit-identical to passing its all-zero residual). */
+enum { SD_GEMM_ONCHIP_RESIDUAL = 1, SD_GEMM_B_EXACT = 2, SD_GEMM_B2_EXACT = 4 };
 sd_status sd_gemm_tf32_ex(const sd_gemm_desc* d1, const sd_gemm_desc* d2, int flags, sd_stream s);
 /* small[i] = x[i] - hi(x[i]); mode 0: hi = trunc_tf32 (what the MMA reads),
  * mode 1: hi = round-to-nearest-away tf32. */
@@ -210,6 +213,9 @@ typedef struct {
                       SD_ARCH_LLAMA (RMSNorm, RoPE, SwiGLU, no biases, untied head) */
   float rope_base; /* RoPE base (SD_ARCH_LLAMA), e.g. 10000 */
   int n_kv_head;   /* SD_ARCH_LLAMA grouped-query attention: key/value heads (0 = n_head) */
+  int bf16_weights; /* parameters are bf16-valued (BASELINE C5 "bf16 weights"): exact in tf32, so the
+                       engine keeps no weight residuals and the weight products run 2 MMAs, not 3;
+                       sd_gpt_init_params rounds to bf16, sd_gpt_create checks */
 } sd_gpt_config;
 enum { SD_ARCH_GPT2 = 0, SD_ARCH_LLAMA = 1 };
 typedef struct sd_gpt_s* sd_gpt;

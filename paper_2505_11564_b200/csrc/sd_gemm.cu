@@ -371,9 +371,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const uint32_t ph = (g / STAGES) & 1;
           mbar_wait(&empty[s], ph ^ 1);
           unsigned char* st = smem + s * STAGE_BYTES;
-          mbar_expect_tx(&full[s], ep.res ? A_BYTES + B_BYTES : STAGE_BYTES);
           // dual source: the second product's k-blocks follow the first's
           const bool src2 = kk >= ti.num_kb;
+          const bool bex = THREE && !ep.res && ((ep.bexact >> (src2 ? 1 : 0)) & 1);
+          mbar_expect_tx(&full[s], ep.res ? A_BYTES + B_BYTES : STAGE_BYTES - (bex ? B_BYTES : 0));
           const int kb = src2 ? kk - ti.num_kb : kk;
           const CUtensorMap* pA = src2 ? &mA2 : &mA;
           const CUtensorMap* pAs = src2 ? &mAs2 : &mAs;
@@ -396,16 +397,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           unsigned char* sb = st + (THREE ? 2 : 1) * A_BYTES;
           if (B_MN && (ep.mn5 & 2)) {
             tma_load_5d(pB, &full[s], sb, 0, k0, ti.n0 / 32, z1, z2);
-            if (THREE && !ep.res) tma_load_5d(pBs, &full[s], sb + B_BYTES, 0, k0, ti.n0 / 32, z1, z2);
+            if (THREE && !ep.res && !bex) tma_load_5d(pBs, &full[s], sb + B_BYTES, 0, k0, ti.n0 / 32, z1, z2);
           } else if (B_MN) {
 #pragma unroll
             for (int c = 0; c < BN / 32; ++c) {
               tma_load_4d(pB, &full[s], sb + c * 2048, ti.n0 + 32 * c, k0, z1, z2);
-              if (THREE && !ep.res) tma_load_4d(pBs, &full[s], sb + B_BYTES + c * 2048, ti.n0 + 32 * c, k0, z1, z2);
+              if (THREE && !ep.res && !bex) tma_load_4d(pBs, &full[s], sb + B_BYTES + c * 2048, ti.n0 + 32 * c, k0, z1, z2);
             }
           } else {
             tma_load_4d(pB, &full[s], sb, k0, ti.n0, z1, z2);
-            if (THREE && !ep.res) tma_load_4d(pBs, &full[s], sb + B_BYTES, k0, ti.n0, z1, z2);
+            if (THREE && !ep.res && !bex) tma_load_4d(pBs, &full[s], sb + B_BYTES, k0, ti.n0, z1, z2);
           }
         }
       }
@@ -454,12 +455,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const uint32_t st = smem_u32(smem + s * STAGE_BYTES);
           const uint32_t a = st, as = st + A_BYTES;
           const uint32_t b = st + (THREE ? 2 : 1) * A_BYTES, bs = b + B_BYTES;
+          const bool bex = THREE && !ep.res && ((ep.bexact >> (kb >= ti.num_kb ? 1 : 0)) & 1);
 #pragma unroll
           for (int ks = 0; ks < BK / 8; ++ks) {
             const uint32_t acc0 = (first && ks == 0) ? 0u : 1u;
             if (THREE) {
               mma_tf32(d, tile_desc<A_MN>(as, ks), tile_desc<B_MN>(b, ks), idesc, acc0);
-              mma_tf32(d, tile_desc<A_MN>(a, ks), tile_desc<B_MN>(bs, ks), idesc, 1u);
+              if (!bex) mma_tf32(d, tile_desc<A_MN>(a, ks), tile_desc<B_MN>(bs, ks), idesc, 1u);
               mma_tf32(d, tile_desc<A_MN>(a, ks), tile_desc<B_MN>(b, ks), idesc, 1u);
             } else {
               mma_tf32(d, tile_desc<A_MN>(a, ks), tile_desc<B_MN>(b, ks), idesc, acc0);
@@ -579,6 +581,7 @@ void launch(const GemmArgs& g, cudaStream_t s) {
   }
   ep.tma_store = tma_store ? 1 : 0;
   ep.mn5 = mn5;
+  ep.bexact = (g.b_exact ? 1 : 0) | (g.b2_exact ? 2 : 0);
   auto kern = g.causal ? k_gemm_tf32<A_MN, B_MN, THREE, BN, true> : k_gemm_tf32<A_MN, B_MN, THREE, BN, false>;
   static bool attr_set = false;
   if (!attr_set) {
@@ -621,6 +624,11 @@ bool sd_gemm_pair_enabled() {
 void gemm(const GemmArgs& g_in, cudaStream_t s) {
   if (g_in.M <= 0 || g_in.N <= 0 || g_in.K <= 0) return;
   GemmArgs g = g_in;
+  // tf32-exact B operands: their (zero) residual is never loaded; the B map
+  // stands in for the residual map so the 3xTF32 path applies
+  if (g.b_exact && g.As && !g.Bs) g.Bs = g.B;
+  if (g.A2 && g.b2_exact && g.A2s && !g.B2s) g.B2s = g.B2;
+  if (!g.A2) g.b2_exact = false;
   const bool pair = g.causal == 0 && g.M >= 256 && g.N >= 256 && sd_gemm_pair_enabled();
   // On-chip residuals (onchip = allowed): they halve the operand bytes through
   // L2 and TMA but add a shared-memory read + write of every staged tile, and
@@ -715,11 +723,13 @@ sd_status sd_gemm_tf32_ex(const sd_gemm_desc* d1, const sd_gemm_desc* d2, int fl
     const bool onchip = (flags & SD_GEMM_ONCHIP_RESIDUAL) != 0;
     sd::GemmArgs g = args_from(d1);
     g.onchip = onchip;
+    g.b_exact = (flags & SD_GEMM_B_EXACT) != 0;
+    g.b2_exact = (flags & SD_GEMM_B2_EXACT) != 0;
     if (onchip) g.As = g.Bs = nullptr;
     if (d2) {
       if (d1->m != d2->m || d1->n != d2->n || d1->k != d2->k || d1->a_mn != d2->a_mn || d1->b_mn != d2->b_mn ||
           (!onchip && ((d1->a_small == nullptr) != (d2->a_small == nullptr) ||
-                       (d1->b_small == nullptr) != (d2->b_small == nullptr))))
+                       (d1->b_small == nullptr && !g.b_exact) != (d2->b_small == nullptr && !g.b2_exact))))
         sd::fail(SD_ARGUMENT_ERROR, "dual gemm: both products need the same shape, majors and precision");
       g.A2 = d2->a, g.lda2 = d2->lda;
       g.B2 = d2->b, g.ldb2 = d2->ldb;

@@ -27,6 +27,9 @@ struct GemmArgs {
   //   C = alpha (op(A) op(B) + op(A2) op(B2)) + beta C ; same M, N, K, majors
   const float *A2 = nullptr, *A2s = nullptr, *B2 = nullptr, *B2s = nullptr;
   long long lda2 = 0, ldb2 = 0, sa1_2 = 0, sa2_2 = 0, sb1_2 = 0, sb2_2 = 0;
+  // B (B2) holds tf32-exact values (bf16-valued weights): its residual is zero,
+  // so 3xTF32 needs neither its residual array nor the A . B_lo product
+  bool b_exact = false, b2_exact = false;
 };
 void gemm(const GemmArgs& g, cudaStream_t s);
 void split_tf32(const float* x, float* small, long long n, int mode, cudaStream_t s);

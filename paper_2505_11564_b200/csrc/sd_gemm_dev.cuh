@@ -141,6 +141,8 @@ struct EpiParams {
   int res;                            // 3xTF32 residuals computed on chip from the staged raw tiles
   int tma_store;                      // C = alpha acc written by TMA from smem (beta 0, no bias/Cs/split)
   int mn5;                            // bit 0 / 1: MN-major A / B tile as one 5-D TMA box
+  int bexact;                         // bit 0 / 1: source 1 / 2 B operand exact in tf32 (bf16-valued
+                                      // weights): no B residual load, no A.B_lo MMA
 };
 
 __device__ __forceinline__ void fence_proxy_async_smem_decl() {

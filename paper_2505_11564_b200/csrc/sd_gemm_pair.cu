@@ -181,15 +181,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
           // residuals from memory: both CTAs' bytes land on the leader's full
           // barrier. On chip: each CTA's raw bytes land on its own barrier and
           // its residual warp releases the stage to the leader (conv[s]).
+          const bool src2 = kk >= ti.num_kb;
+          const bool bex = THREE && !ep.res && ((ep.bexact >> (src2 ? 1 : 0)) & 1);
           uint32_t bar;
           if (ep.res) {
             mbar_expect_tx(&full[s], PA_BYTES + PB_BYTES);
             bar = smem_u32(&full[s]);
           } else {
-            if (rank == 0) mbar_expect_tx(&full[s], 2 * STAGE_BYTES);
+            if (rank == 0) mbar_expect_tx(&full[s], 2 * (STAGE_BYTES - (bex ? PB_BYTES : 0)));
             bar = full_leader + 8u * s;
           }
-          const bool src2 = kk >= ti.num_kb;
           const int kb = src2 ? kk - ti.num_kb : kk;
           const CUtensorMap* pA = src2 ? &mA2 : &mA;
           const CUtensorMap* pAs = src2 ? &mAs2 : &mAs;
@@ -212,16 +213,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
           unsigned char* sb = st + (THREE ? 2 : 1) * PA_BYTES;
           if (B_MN && (ep.mn5 & 2)) {
             tma_load_5d_pair(pB, bar, sb, 0, k0, n_own / 32, z1, z2);
-            if (THREE && !ep.res) tma_load_5d_pair(pBs, bar, sb + PB_BYTES, 0, k0, n_own / 32, z1, z2);
+            if (THREE && !ep.res && !bex) tma_load_5d_pair(pBs, bar, sb + PB_BYTES, 0, k0, n_own / 32, z1, z2);
           } else if (B_MN) {
 #pragma unroll
             for (int c = 0; c < kHalfB / 32; ++c) {
               tma_load_4d_pair(pB, bar, sb + c * 2048, n_own + 32 * c, k0, z1, z2);
-              if (THREE && !ep.res) tma_load_4d_pair(pBs, bar, sb + PB_BYTES + c * 2048, n_own + 32 * c, k0, z1, z2);
+              if (THREE && !ep.res && !bex) tma_load_4d_pair(pBs, bar, sb + PB_BYTES + c * 2048, n_own + 32 * c, k0, z1, z2);
             }
           } else {
             tma_load_4d_pair(pB, bar, sb, k0, n_own, z1, z2);
-            if (THREE && !ep.res) tma_load_4d_pair(pBs, bar, sb + PB_BYTES, k0, n_own, z1, z2);
+            if (THREE && !ep.res && !bex) tma_load_4d_pair(pBs, bar, sb + PB_BYTES, k0, n_own, z1, z2);
           }
         }
       }
@@ -270,12 +271,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
             const uint32_t st = smem_u32(smem + s * STAGE_BYTES);
             const uint32_t a = st, as = st + PA_BYTES;
             const uint32_t b = st + (THREE ? 2 : 1) * PA_BYTES, bs = b + PB_BYTES;
+            const bool bex = THREE && !ep.res && ((ep.bexact >> (kb >= ti.num_kb ? 1 : 0)) & 1);
 #pragma unroll
             for (int ks = 0; ks < BK / 8; ++ks) {
               const uint32_t acc0 = (first && ks == 0) ? 0u : 1u;
               if (THREE) {
                 mma_tf32_pair(d, tile_desc<A_MN>(as, ks), tile_desc<B_MN>(b, ks), idesc, acc0);
-                mma_tf32_pair(d, tile_desc<A_MN>(a, ks), tile_desc<B_MN>(bs, ks), idesc, 1u);
+                if (!bex) mma_tf32_pair(d, tile_desc<A_MN>(a, ks), tile_desc<B_MN>(bs, ks), idesc, 1u);
                 mma_tf32_pair(d, tile_desc<A_MN>(a, ks), tile_desc<B_MN>(b, ks), idesc, 1u);
               } else {
                 mma_tf32_pair(d, tile_desc<A_MN>(a, ks), tile_desc<B_MN>(b, ks), idesc, acc0);
@@ -392,6 +394,7 @@ void launch_pair_t(const GemmArgs& g, cudaStream_t s) {
              (dual ? ",2" : ",1"));
   prof_begin(s);
   ep.mn5 = mn5;
+  ep.bexact = (g.b_exact ? 1 : 0) | (g.b2_exact ? 2 : 0);
   CUtensorMap mC = maps[0], mCs = maps[0];
   if (tma_store_ok(g, splits, 16)) {
     make_store_map(&mC, g.C, g, 16);

@@ -221,7 +221,8 @@ struct sd_gpt_s {
     if (gqa())
       gqkv = p.take<float>(T_ * W), gqkvs = p.take<float>(T_ * W), gdqkv = p.take<float>(T_ * W),
       gdqkvs = p.take<float>(T_ * W);
-    theta_s = p.take<float>(Pst), v_s = p.take<float>(Pst);
+    theta_s = c.bf16_weights ? nullptr : p.take<float>(Pst);  // bf16 weights: exact in tf32, no residual
+    v_s = p.take<float>(Pst);
     red = p.take<float>(2LL * 64 * std::max(3 * d, ff));
     if (first) {
       tok = p.take<int>(T_ * nmb), uniq = p.take<int>((T_ + 1) * nmb), ustart = p.take<int>((T_ + 1) * nmb);
@@ -243,14 +244,17 @@ struct sd_gpt_s {
     long long ld;
     bool mn;
     long long s1 = 0, s2 = 0;
+    bool exact = false;  // tf32-exact values (bf16 weights): no residual
   };
+  // weight operand of parameter slot i
+  Op Wt(int i, long long ld, bool mn) const { return Op{th(i), ths(i), ld, mn, 0, 0, c.bf16_weights != 0}; }
   void mm(int M, int N, int K, Op A, Op Bo, float* C, long long ldc, float alpha, float beta, cudaStream_t st,
           const float* bias = nullptr, float* Cs = nullptr, int Z1 = 1, int Z2 = 1, long long c1 = 0,
           long long c2 = 0) {
     sd::GemmArgs g;
     g.M = M, g.N = N, g.K = K;
     g.A = A.p, g.As = A.s, g.lda = A.ld, g.a_mn = A.mn;
-    g.B = Bo.p, g.Bs = Bo.s, g.ldb = Bo.ld, g.b_mn = Bo.mn;
+    g.B = Bo.p, g.Bs = Bo.s, g.ldb = Bo.ld, g.b_mn = Bo.mn, g.b_exact = Bo.exact;
     g.C = C, g.ldc = ldc, g.alpha = alpha, g.beta = beta, g.bias = bias, g.Cs = Cs;
     g.Z1 = Z1, g.Z2 = Z2, g.sa1 = A.s1, g.sa2 = A.s2, g.sb1 = Bo.s1, g.sb2 = Bo.s2, g.sc1 = c1, g.sc2 = c2;
     g.causal = cmode;
@@ -265,9 +269,9 @@ struct sd_gpt_s {
     sd::GemmArgs g;
     g.M = M, g.N = N, g.K = K;
     g.A = A.p, g.As = A.s, g.lda = A.ld, g.a_mn = A.mn;
-    g.B = Bo.p, g.Bs = Bo.s, g.ldb = Bo.ld, g.b_mn = Bo.mn;
+    g.B = Bo.p, g.Bs = Bo.s, g.ldb = Bo.ld, g.b_mn = Bo.mn, g.b_exact = Bo.exact;
     if (A2.mn != A.mn || B2.mn != Bo.mn) fail(SD_ARGUMENT_ERROR, "gpt: dual product majors differ");
-    g.A2 = A2.p, g.A2s = A2.s, g.lda2 = A2.ld, g.B2 = B2.p, g.B2s = B2.s, g.ldb2 = B2.ld;
+    g.A2 = A2.p, g.A2s = A2.s, g.lda2 = A2.ld, g.B2 = B2.p, g.B2s = B2.s, g.ldb2 = B2.ld, g.b2_exact = B2.exact;
     g.sa1_2 = A2.s1, g.sa2_2 = A2.s2, g.sb1_2 = B2.s1, g.sb2_2 = B2.s2;
     g.C = C, g.ldc = ldc, g.alpha = alpha, g.beta = beta, g.bias = bias, g.Cs = Cs;
     g.Z1 = Z1, g.Z2 = Z2, g.sa1 = A.s1, g.sa2 = A.s2, g.sb1 = Bo.s1, g.sb2 = Bo.s2, g.sc1 = c1, g.sc2 = c2;
@@ -280,7 +284,7 @@ struct sd_gpt_s {
   // weight products measured neutral on the whole HVP: SD_GEMM_ONCHIP=1).
   static void onchip_residuals(sd::GemmArgs& g) {
     // an operand without a residual array (P, dP, gS, gdS) -> on-chip residuals
-    if (!g.As || !g.Bs || (g.A2 && (!g.A2s || !g.B2s))) {
+    if (!g.As || (!g.Bs && !g.b_exact) || (g.A2 && (!g.A2s || (!g.B2s && !g.b2_exact)))) {
       g.onchip = true;
       return;
     }
@@ -293,7 +297,7 @@ struct sd_gpt_s {
   }
 
   const float* th(int i) const { return theta + (slots[i].off - pbase); }
-  const float* ths(int i) const { return theta_s + (slots[i].off - pbase); }
+  const float* ths(int i) const { return theta_s ? theta_s + (slots[i].off - pbase) : nullptr; }
 
   void hvp(const float* v, float* hv, cudaStream_t st) {
     if (!have_batch) fail(SD_STATE_ERROR, "gpt: set_batch was not called");
@@ -314,38 +318,38 @@ struct sd_gpt_s {
                     Ly.h1, Ly.h1s, Ly.dh1, Ly.dh1s, Ly.xh1, Ly.dxh1, Ly.r1, Ly.dr1};
       sd::gpt_ln_fwd(la, st);
       // qkv = h Wa + ba ; dqkv = dh Wa + h VWa + Vba
-      mm(T, 3 * d, d, {Ly.h1, Ly.h1s, d, false}, {th(b + 2), ths(b + 2), 3 * d, true}, Ly.a, 3 * d, 1, 0, st,
+      mm(T, 3 * d, d, {Ly.h1, Ly.h1s, d, false}, Wt(b + 2, 3 * d, true), Ly.a, 3 * d, 1, 0, st,
          th(b + 3), Ly.as);
-      mm2(T, 3 * d, d, {Ly.dh1, Ly.dh1s, d, false}, {th(b + 2), ths(b + 2), 3 * d, true}, {Ly.h1, Ly.h1s, d, false},
+      mm2(T, 3 * d, d, {Ly.dh1, Ly.dh1s, d, false}, Wt(b + 2, 3 * d, true), {Ly.h1, Ly.h1s, d, false},
           {V_(b + 2), Vs(b + 2), 3 * d, true}, Ly.da, 3 * d, 1, 0, st, V_(b + 3), Ly.das);
       attention_fwd(Ly, sc, st);
       // x += o Wp + bp ; dx += do Wp + o VWp + Vbp
-      mm(T, d, d, {Ly.o, Ly.os, d, false}, {th(b + 4), ths(b + 4), d, true}, x, d, 1, 1, st, th(b + 5));
-      mm2(T, d, d, {Ly.dO, Ly.dOs, d, false}, {th(b + 4), ths(b + 4), d, true}, {Ly.o, Ly.os, d, false},
+      mm(T, d, d, {Ly.o, Ly.os, d, false}, Wt(b + 4, d, true), x, d, 1, 1, st, th(b + 5));
+      mm2(T, d, d, {Ly.dO, Ly.dOs, d, false}, Wt(b + 4, d, true), {Ly.o, Ly.os, d, false},
           {V_(b + 4), Vs(b + 4), d, true}, dx, d, 1, 1, st, V_(b + 5));
       sd::LnArgs lb{x, dx, th(b + 6), th(b + 7), V_(b + 6), V_(b + 7), T, d, 1e-5f,
                     Ly.h2, Ly.h2s, Ly.dh2, Ly.dh2s, Ly.xh2, Ly.dxh2, Ly.r2, Ly.dr2};
       sd::gpt_ln_fwd(lb, st);
-      mm(T, ff, d, {Ly.h2, Ly.h2s, d, false}, {th(b + 8), ths(b + 8), ff, true}, Ly.f, ff, 1, 0, st, th(b + 9));
-      mm2(T, ff, d, {Ly.dh2, Ly.dh2s, d, false}, {th(b + 8), ths(b + 8), ff, true}, {Ly.h2, Ly.h2s, d, false},
+      mm(T, ff, d, {Ly.h2, Ly.h2s, d, false}, Wt(b + 8, ff, true), Ly.f, ff, 1, 0, st, th(b + 9));
+      mm2(T, ff, d, {Ly.dh2, Ly.dh2s, d, false}, Wt(b + 8, ff, true), {Ly.h2, Ly.h2s, d, false},
           {V_(b + 8), Vs(b + 8), ff, true}, Ly.df, ff, 1, 0, st, V_(b + 9));
       sd::gpt_gelu_fwd(Ly.f, Ly.df, Ly.u, Ly.us, Ly.du, Ly.dus, (long long)T * ff, st);
-      mm(T, d, ff, {Ly.u, Ly.us, ff, false}, {th(b + 10), ths(b + 10), d, true}, x, d, 1, 1, st, th(b + 11));
-      mm2(T, d, ff, {Ly.du, Ly.dus, ff, false}, {th(b + 10), ths(b + 10), d, true}, {Ly.u, Ly.us, ff, false},
+      mm(T, d, ff, {Ly.u, Ly.us, ff, false}, Wt(b + 10, d, true), x, d, 1, 1, st, th(b + 11));
+      mm2(T, d, ff, {Ly.du, Ly.dus, ff, false}, Wt(b + 10, d, true), {Ly.u, Ly.us, ff, false},
           {V_(b + 10), Vs(b + 10), d, true}, dx, d, 1, 1, st, V_(b + 11));
     }
     const int fL = 2 + 12 * c.n_layer;
     sd::LnArgs lf{x, dx, th(fL), th(fL + 1), V_(fL), V_(fL + 1), T, d, 1e-5f, hf, hfs, dhf, dhfs, xhf, dxhf, rf, drf};
     sd::gpt_ln_fwd(lf, st);
     // logits z = hf wte^T ; dz = dhf wte^T + hf Vwte^T
-    mm(T, V, d, {hf, hfs, d, false}, {th(0), ths(0), d, false}, z, Vp, 1, 0, st);
-    mm2(T, V, d, {dhf, dhfs, d, false}, {th(0), ths(0), d, false}, {hf, hfs, d, false}, {V_(0), Vs(0), d, false}, dz,
+    mm(T, V, d, {hf, hfs, d, false}, Wt(0, d, false), z, Vp, 1, 0, st);
+    mm2(T, V, d, {dhf, dhfs, d, false}, Wt(0, d, false), {hf, hfs, d, false}, {V_(0), Vs(0), d, false}, dz,
         Vp, 1, 0, st);
     sd::gpt_ce(z, dz, zs, dz == nullptr ? nullptr : dzs, tgt, T, V, Vp, loss_scale, loss_rows, st);
     // ----------------------------------------------------------- backward
     // ghf = gz wte ; gdhf = gdz wte + gz Vwte ; Hv_wte(head) = gdz^T hf + gz^T dhf
-    mm(T, d, V, {z, zs, Vp, false}, {th(0), ths(0), d, true}, gh, d, 1, 0, st);
-    mm2(T, d, V, {dz, dzs, Vp, false}, {th(0), ths(0), d, true}, {z, zs, Vp, false}, {V_(0), Vs(0), d, true}, gdh, d,
+    mm(T, d, V, {z, zs, Vp, false}, Wt(0, d, true), gh, d, 1, 0, st);
+    mm2(T, d, V, {dz, dzs, Vp, false}, Wt(0, d, true), {z, zs, Vp, false}, {V_(0), Vs(0), d, true}, gdh, d,
         1, 0, st);
     mm2(V, d, T, {dz, dzs, Vp, true}, {hf, hfs, d, true}, {z, zs, Vp, true}, {dhf, dhfs, d, true}, HV(0), d, 1, 0, st);
     SD_CUDA(cudaMemsetAsync(gx, 0, Td * sizeof(float), st));
@@ -356,16 +360,16 @@ struct sd_gpt_s {
       Layer& Ly = L[l];
       const int b = 2 + 12 * l;
       // MLP out: gu = gx Wq^T ; gdu = gdx Wq^T + gx VWq^T ; Hv_Wq = du^T gx + u^T gdx
-      mm(T, ff, d, {gx, gxs, d, false}, {th(b + 10), ths(b + 10), d, false}, gu, ff, 1, 0, st);
-      mm2(T, ff, d, {gdx, gdxs, d, false}, {th(b + 10), ths(b + 10), d, false}, {gx, gxs, d, false},
+      mm(T, ff, d, {gx, gxs, d, false}, Wt(b + 10, d, false), gu, ff, 1, 0, st);
+      mm2(T, ff, d, {gdx, gdxs, d, false}, Wt(b + 10, d, false), {gx, gxs, d, false},
           {V_(b + 10), Vs(b + 10), d, false}, gdu, ff, 1, 0, st);
       mm2(ff, d, T, {Ly.du, Ly.dus, ff, true}, {gx, gxs, d, true}, {Ly.u, Ly.us, ff, true}, {gdx, gdxs, d, true},
           HV(b + 10), d, 1, 0, st);
       sd::gpt_colsum(gdx, T, d, d, HV(b + 11), red, st);
       sd::gpt_gelu_bwd(Ly.f, Ly.df, gu, gdu, gus, gdus, (long long)T * ff, st);
       // MLP in: gh = gf Wf^T ; gdh = gdf Wf^T + gf VWf^T ; Hv_Wf = dh2^T gf + h2^T gdf
-      mm(T, d, ff, {gu, gus, ff, false}, {th(b + 8), ths(b + 8), ff, false}, gh, d, 1, 0, st);
-      mm2(T, d, ff, {gdu, gdus, ff, false}, {th(b + 8), ths(b + 8), ff, false}, {gu, gus, ff, false},
+      mm(T, d, ff, {gu, gus, ff, false}, Wt(b + 8, ff, false), gh, d, 1, 0, st);
+      mm2(T, d, ff, {gdu, gdus, ff, false}, Wt(b + 8, ff, false), {gu, gus, ff, false},
           {V_(b + 8), Vs(b + 8), ff, false}, gdh, d, 1, 0, st);
       mm2(d, ff, T, {Ly.dh2, Ly.dh2s, d, true}, {gu, gus, ff, true}, {Ly.h2, Ly.h2s, d, true}, {gdu, gdus, ff, true},
           HV(b + 8), ff, 1, 0, st);
@@ -374,16 +378,16 @@ struct sd_gpt_s {
                        gx, gdx, gxs, gdxs, HV(b + 6), HV(b + 7), red};
       sd::gpt_ln_bwd(b2, st);
       // attention out-projection
-      mm(T, d, d, {gx, gxs, d, false}, {th(b + 4), ths(b + 4), d, false}, go, d, 1, 0, st, nullptr, gos);
-      mm2(T, d, d, {gdx, gdxs, d, false}, {th(b + 4), ths(b + 4), d, false}, {gx, gxs, d, false},
+      mm(T, d, d, {gx, gxs, d, false}, Wt(b + 4, d, false), go, d, 1, 0, st, nullptr, gos);
+      mm2(T, d, d, {gdx, gdxs, d, false}, Wt(b + 4, d, false), {gx, gxs, d, false},
           {V_(b + 4), Vs(b + 4), d, false}, gdo, d, 1, 0, st, nullptr, gdos);
       mm2(d, d, T, {Ly.dO, Ly.dOs, d, true}, {gx, gxs, d, true}, {Ly.o, Ly.os, d, true}, {gdx, gdxs, d, true},
           HV(b + 4), d, 1, 0, st);
       sd::gpt_colsum(gdx, T, d, d, HV(b + 5), red, st);
       attention_bwd(Ly, sc, st);
       // QKV: gh = ga Wa^T ; gdh = gda Wa^T + ga VWa^T ; Hv_Wa = dh1^T ga + h1^T gda
-      mm(T, d, 3 * d, {ga, gas, 3 * d, false}, {th(b + 2), ths(b + 2), 3 * d, false}, gh, d, 1, 0, st);
-      mm2(T, d, 3 * d, {gda, gdas, 3 * d, false}, {th(b + 2), ths(b + 2), 3 * d, false}, {ga, gas, 3 * d, false},
+      mm(T, d, 3 * d, {ga, gas, 3 * d, false}, Wt(b + 2, 3 * d, false), gh, d, 1, 0, st);
+      mm2(T, d, 3 * d, {gda, gdas, 3 * d, false}, Wt(b + 2, 3 * d, false), {ga, gas, 3 * d, false},
           {V_(b + 2), Vs(b + 2), 3 * d, false}, gdh, d, 1, 0, st);
       mm2(d, 3 * d, T, {Ly.dh1, Ly.dh1s, d, true}, {ga, gas, 3 * d, true}, {Ly.h1, Ly.h1s, d, true},
           {gda, gdas, 3 * d, true}, HV(b + 2), 3 * d, 1, 0, st);
@@ -439,24 +443,24 @@ struct sd_gpt_s {
       // the KV heads to the MHA [T, 3d] layout the attention products use
       float *qa = gqa() ? Ly.qkv : Ly.a, *qas = gqa() ? Ly.qkvs : Ly.as;
       float *qd = gqa() ? Ly.dqkv : Ly.da, *qds = gqa() ? Ly.dqkvs : Ly.das;
-      mm(T, W, d, {Ly.h1, Ly.h1s, d, false}, {th(b + 1), ths(b + 1), W, true}, qa, W, 1, 0, st, nullptr, qas);
-      mm2(T, W, d, {Ly.dh1, Ly.dh1s, d, false}, {th(b + 1), ths(b + 1), W, true}, {Ly.h1, Ly.h1s, d, false},
+      mm(T, W, d, {Ly.h1, Ly.h1s, d, false}, Wt(b + 1, W, true), qa, W, 1, 0, st, nullptr, qas);
+      mm2(T, W, d, {Ly.dh1, Ly.dh1s, d, false}, Wt(b + 1, W, true), {Ly.h1, Ly.h1s, d, false},
           {V_(b + 1), Vs(b + 1), W, true}, qd, W, 1, 0, st, nullptr, qds);
       if (gqa()) sd::llama_gqa_expand(Ly.qkv, Ly.qkvs, Ly.dqkv, Ly.dqkvs, Ly.a, Ly.as, Ly.da, Ly.das, T, d, dh, KV, H, st);
       sd::llama_rope(Ly.a, Ly.as, Ly.da, Ly.das, T, S, d, dh, c.rope_base, 0, st);
       attention_fwd(Ly, sc, st);
-      mm(T, d, d, {Ly.o, Ly.os, d, false}, {th(b + 2), ths(b + 2), d, true}, x, d, 1, 1, st);
-      mm2(T, d, d, {Ly.dO, Ly.dOs, d, false}, {th(b + 2), ths(b + 2), d, true}, {Ly.o, Ly.os, d, false},
+      mm(T, d, d, {Ly.o, Ly.os, d, false}, Wt(b + 2, d, true), x, d, 1, 1, st);
+      mm2(T, d, d, {Ly.dO, Ly.dOs, d, false}, Wt(b + 2, d, true), {Ly.o, Ly.os, d, false},
           {V_(b + 2), Vs(b + 2), d, true}, dx, d, 1, 1, st);
       sd::LnArgs lb{x, dx, th(b + 3), nullptr, V_(b + 3), nullptr, T, d, eps,
                     Ly.h2, Ly.h2s, Ly.dh2, Ly.dh2s, Ly.xh2, Ly.dxh2, Ly.r2, Ly.dr2, 1};
       sd::gpt_ln_fwd(lb, st);
-      mm(T, 2 * ff, d, {Ly.h2, Ly.h2s, d, false}, {th(b + 4), ths(b + 4), 2 * ff, true}, Ly.f, 2 * ff, 1, 0, st);
-      mm2(T, 2 * ff, d, {Ly.dh2, Ly.dh2s, d, false}, {th(b + 4), ths(b + 4), 2 * ff, true},
+      mm(T, 2 * ff, d, {Ly.h2, Ly.h2s, d, false}, Wt(b + 4, 2 * ff, true), Ly.f, 2 * ff, 1, 0, st);
+      mm2(T, 2 * ff, d, {Ly.dh2, Ly.dh2s, d, false}, Wt(b + 4, 2 * ff, true),
           {Ly.h2, Ly.h2s, d, false}, {V_(b + 4), Vs(b + 4), 2 * ff, true}, Ly.df, 2 * ff, 1, 0, st);
       sd::llama_swiglu_fwd(Ly.f, Ly.df, Ly.u, Ly.us, Ly.du, Ly.dus, T, ff, st);
-      mm(T, d, ff, {Ly.u, Ly.us, ff, false}, {th(b + 5), ths(b + 5), d, true}, x, d, 1, 1, st);
-      mm2(T, d, ff, {Ly.du, Ly.dus, ff, false}, {th(b + 5), ths(b + 5), d, true}, {Ly.u, Ly.us, ff, false},
+      mm(T, d, ff, {Ly.u, Ly.us, ff, false}, Wt(b + 5, d, true), x, d, 1, 1, st);
+      mm2(T, d, ff, {Ly.du, Ly.dus, ff, false}, Wt(b + 5, d, true), {Ly.u, Ly.us, ff, false},
           {V_(b + 5), Vs(b + 5), d, true}, dx, d, 1, 1, st);
     }
   }
@@ -478,12 +482,12 @@ struct sd_gpt_s {
       sd::LnArgs lf{x, dx, th(fL), nullptr, V_(fL), nullptr, T, d, eps, hf, hfs, dhf, dhfs, xhf, dxhf, rf, drf, 1};
       sd::gpt_ln_fwd(lf, st);
       // logits z = hf W_out^T ; dz = dhf W_out^T + hf VW_out^T
-      mm(T, V, d, {hf, hfs, d, false}, {th(head), ths(head), d, false}, z, Vp, 1, 0, st);
-      mm2(T, V, d, {dhf, dhfs, d, false}, {th(head), ths(head), d, false}, {hf, hfs, d, false},
+      mm(T, V, d, {hf, hfs, d, false}, Wt(head, d, false), z, Vp, 1, 0, st);
+      mm2(T, V, d, {dhf, dhfs, d, false}, Wt(head, d, false), {hf, hfs, d, false},
           {V_(head), Vs(head), d, false}, dz, Vp, 1, 0, st);
       sd::gpt_ce(z, dz, zs, dzs, tgt + (long long)m * T, T, V, Vp, loss_scale, loss_rows + (long long)m * T, st);
-      mm(T, d, V, {z, zs, Vp, false}, {th(head), ths(head), d, true}, gh, d, 1, 0, st);
-      mm2(T, d, V, {dz, dzs, Vp, false}, {th(head), ths(head), d, true}, {z, zs, Vp, false},
+      mm(T, d, V, {z, zs, Vp, false}, Wt(head, d, true), gh, d, 1, 0, st);
+      mm2(T, d, V, {dz, dzs, Vp, false}, Wt(head, d, true), {z, zs, Vp, false},
           {V_(head), Vs(head), d, true}, gdh, d, 1, 0, st);
       mm2(V, d, T, {dz, dzs, Vp, true}, {hf, hfs, d, true}, {z, zs, Vp, true}, {dhf, dhfs, d, true}, HV(head), d, 1,
           hb, st);
@@ -499,15 +503,15 @@ struct sd_gpt_s {
       Layer& Ly = L[l - l0];
       const int b = 1 + 6 * l;
       // down projection: ga = gx Wd^T ; gda = gdx Wd^T + gx VWd^T ; Hv_Wd = da^T gx + a^T gdx
-      mm(T, ff, d, {gx, gxs, d, false}, {th(b + 5), ths(b + 5), d, false}, ga_mlp, ff, 1, 0, st);
-      mm2(T, ff, d, {gdx, gdxs, d, false}, {th(b + 5), ths(b + 5), d, false}, {gx, gxs, d, false},
+      mm(T, ff, d, {gx, gxs, d, false}, Wt(b + 5, d, false), ga_mlp, ff, 1, 0, st);
+      mm2(T, ff, d, {gdx, gdxs, d, false}, Wt(b + 5, d, false), {gx, gxs, d, false},
           {V_(b + 5), Vs(b + 5), d, false}, gda_mlp, ff, 1, 0, st);
       mm2(ff, d, T, {Ly.du, Ly.dus, ff, true}, {gx, gxs, d, true}, {Ly.u, Ly.us, ff, true}, {gdx, gdxs, d, true},
           HV(b + 5), d, 1, hb, st);
       sd::llama_swiglu_bwd(Ly.f, Ly.df, ga_mlp, gda_mlp, gu, gus, gdu, gdus, T, ff, st);
       // gate|up: gh = gfu Wgu^T ; gdh = gdfu Wgu^T + gfu VWgu^T ; Hv_Wgu = dh2^T gfu + h2^T gdfu
-      mm(T, d, 2 * ff, {gu, gus, 2 * ff, false}, {th(b + 4), ths(b + 4), 2 * ff, false}, gh, d, 1, 0, st);
-      mm2(T, d, 2 * ff, {gdu, gdus, 2 * ff, false}, {th(b + 4), ths(b + 4), 2 * ff, false},
+      mm(T, d, 2 * ff, {gu, gus, 2 * ff, false}, Wt(b + 4, 2 * ff, false), gh, d, 1, 0, st);
+      mm2(T, d, 2 * ff, {gdu, gdus, 2 * ff, false}, Wt(b + 4, 2 * ff, false),
           {gu, gus, 2 * ff, false}, {V_(b + 4), Vs(b + 4), 2 * ff, false}, gdh, d, 1, 0, st);
       mm2(d, 2 * ff, T, {Ly.dh2, Ly.dh2s, d, true}, {gu, gus, 2 * ff, true}, {Ly.h2, Ly.h2s, d, true},
           {gdu, gdus, 2 * ff, true}, HV(b + 4), 2 * ff, 1, hb, st);
@@ -515,8 +519,8 @@ struct sd_gpt_s {
                        gx, gdx, gxs, gdxs, HV(b + 3), nullptr, red, 1, int(acc)};
       sd::gpt_ln_bwd(b2, st);
       // attention output projection
-      mm(T, d, d, {gx, gxs, d, false}, {th(b + 2), ths(b + 2), d, false}, go, d, 1, 0, st, nullptr, gos);
-      mm2(T, d, d, {gdx, gdxs, d, false}, {th(b + 2), ths(b + 2), d, false}, {gx, gxs, d, false},
+      mm(T, d, d, {gx, gxs, d, false}, Wt(b + 2, d, false), go, d, 1, 0, st, nullptr, gos);
+      mm2(T, d, d, {gdx, gdxs, d, false}, Wt(b + 2, d, false), {gx, gxs, d, false},
           {V_(b + 2), Vs(b + 2), d, false}, gdo, d, 1, 0, st, nullptr, gdos);
       mm2(d, d, T, {Ly.dO, Ly.dOs, d, true}, {gx, gxs, d, true}, {Ly.o, Ly.os, d, true}, {gdx, gdxs, d, true},
           HV(b + 2), d, 1, hb, st);
@@ -529,8 +533,8 @@ struct sd_gpt_s {
         sd::llama_gqa_reduce(ga, gda, gqkv, gqkvs, gdqkv, gdqkvs, T, d, dh, KV, H, st);
         qg = gqkv, qgs = gqkvs, qgd = gdqkv, qgds = gdqkvs;
       }
-      mm(T, d, W, {qg, qgs, W, false}, {th(b + 1), ths(b + 1), W, false}, gh, d, 1, 0, st);
-      mm2(T, d, W, {qgd, qgds, W, false}, {th(b + 1), ths(b + 1), W, false}, {qg, qgs, W, false},
+      mm(T, d, W, {qg, qgs, W, false}, Wt(b + 1, W, false), gh, d, 1, 0, st);
+      mm2(T, d, W, {qgd, qgds, W, false}, Wt(b + 1, W, false), {qg, qgs, W, false},
           {V_(b + 1), Vs(b + 1), W, false}, gdh, d, 1, 0, st);
       mm2(d, W, T, {Ly.dh1, Ly.dh1s, d, true}, {qg, qgs, W, true}, {Ly.h1, Ly.h1s, d, true}, {qgd, qgds, W, true},
           HV(b + 1), W, 1, hb, st);
@@ -765,7 +769,8 @@ sd_status sd_gpt_init_params(const sd_gpt_config* c, uint64_t seed, double gain_
     for (const Slot& sl : layout(*c)) {
       const double base = sl.kind == 1 ? 1.0 : 0.0;
       const double sc = sl.kind == 0 ? 0.02 : (sl.kind == 1 ? gain_scale : bias_scale);
-      sd::gpt_init_slot(theta, (long long)sl.off, (long long)(sl.rows * sl.cols), seed, base, sc, (cudaStream_t)s);
+      sd::gpt_init_slot(theta, (long long)sl.off, (long long)(sl.rows * sl.cols), seed, base, sc, (cudaStream_t)s,
+                        c->bf16_weights != 0);
     }
   });
 }
@@ -815,7 +820,13 @@ sd_status sd_gpt_stage_create(const sd_gpt_config* c, int micro_batch, int seq, 
     if (bytes < p.bytes) fail(SD_ARGUMENT_ERROR, "gpt workspace too small");
     g->slots = layout(*c);
     g->theta = theta_stage;
-    sd::gpt_residual(theta_stage, g->theta_s, g->Pst, (cudaStream_t)s);
+    if (c->bf16_weights) {
+      if (sd::gpt_count_not_bf16(theta_stage, g->Pst, reinterpret_cast<unsigned long long*>(g->red),
+                                 (cudaStream_t)s) != 0)
+        fail(SD_CONFIG_ERROR, "bf16_weights: the parameters are not bf16-valued");
+    } else {
+      sd::gpt_residual(theta_stage, g->theta_s, g->Pst, (cudaStream_t)s);
+    }
     if (g->last) {  // padded logits columns are never read as values but feed TMA boxes: zero them once
       for (float* z : {g->z, g->zs, g->dz, g->dzs})
         SD_CUDA(cudaMemsetAsync(z, 0, size_t(g->T) * g->Vp * 4, (cudaStream_t)s));

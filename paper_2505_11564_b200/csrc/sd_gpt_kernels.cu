@@ -6,6 +6,7 @@
 // (x - trunc_tf32(x)) for the 3xTF32 product.
 //
 // Notation: X primal, dX tangent (R-op), gX adjoint, gdX adjoint tangent.
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
@@ -572,7 +573,7 @@ __global__ void k_fill(float* __restrict__ x, float v, long long n) {
 
 // synthetic init theta[i] = base + scale * gaussian(seed, i) (float), per slot
 __global__ void k_init_slot(float* __restrict__ th, long long off, long long n, uint64_t key, double base,
-                            double scale) {
+                            double scale, int bf16) {
   const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (e >= n) return;
   const uint64_t i = uint64_t(off + e);
@@ -583,7 +584,17 @@ __global__ void k_init_slot(float* __restrict__ th, long long off, long long n, 
     const double gsn = __dmul_rn(__dsqrt_rn(__dmul_rn(-2.0, log(u1))), cos(__dmul_rn(6.283185307179586, u2)));
     v = __dadd_rn(base, __dmul_rn(scale, gsn));
   }
-  th[off + e] = __double2float_rn(v);
+  const float f = __double2float_rn(v);
+  th[off + e] = bf16 ? __bfloat162float(__float2bfloat16_rn(f)) : f;  // bf16 weights: the f32 value rounded RNE
+}
+
+// number of elements that are not bf16-valued (low 16 mantissa bits set)
+__global__ void k_count_not_bf16(const float* __restrict__ x, long long n, unsigned long long* __restrict__ cnt) {
+  unsigned long long c = 0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    c += (__float_as_uint(x[i]) & 0xFFFFu) != 0u;
+  c = __reduce_add_sync(0xffffffffu, unsigned(c));
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(cnt, c);
 }
 
 // ------------------------------------------------------------- launchers
@@ -712,10 +723,23 @@ void gpt_fill(float* x, float v, long long n, cudaStream_t s) {
   SD_LAUNCHED("k_fill");
 }
 
-void gpt_init_slot(float* th, long long off, long long n, uint64_t seed, double base, double scale, cudaStream_t s) {
+void gpt_init_slot(float* th, long long off, long long n, uint64_t seed, double base, double scale, cudaStream_t s,
+                   bool bf16) {
   if (n <= 0) return;
-  k_init_slot<<<g1(n), 256, 0, s>>>(th, off, n, mix64(seed), base, scale);
+  k_init_slot<<<g1(n), 256, 0, s>>>(th, off, n, mix64(seed), base, scale, bf16 ? 1 : 0);
   SD_LAUNCHED("k_init_slot");
+}
+
+unsigned long long gpt_count_not_bf16(const float* x, long long n, unsigned long long* scratch, cudaStream_t s) {
+  SD_CUDA(cudaMemsetAsync(scratch, 0, sizeof(unsigned long long), s));
+  if (n > 0) {
+    k_count_not_bf16<<<unsigned(std::min<long long>(g1(n), 148 * 16)), 256, 0, s>>>(x, n, scratch);
+    SD_LAUNCHED("k_count_not_bf16");
+  }
+  unsigned long long h = 0;
+  SD_CUDA(cudaMemcpyAsync(&h, scratch, sizeof(h), cudaMemcpyDeviceToHost, s));
+  SD_CUDA(cudaStreamSynchronize(s));
+  return h;
 }
 
 }  // namespace sd

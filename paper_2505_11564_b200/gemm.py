@@ -49,17 +49,19 @@ def split(x: torch.Tensor, mode: int = 0) -> torch.Tensor:
     return s
 
 
-ONCHIP_RESIDUAL = 1
+ONCHIP_RESIDUAL, B_EXACT, B2_EXACT = 1, 2, 4
 
 
 def gemm(m, n, k, a, lda, a_mn, b, ldb, b_mn, c, ldc, alpha=1.0, beta=0.0, a_small=None, b_small=None,
-         z1=1, z2=1, sa=(0, 0), sb=(0, 0), sc=(0, 0), onchip=False):
-    """onchip=True: 3xTF32 with the operand residuals computed in shared memory."""
+         z1=1, z2=1, sa=(0, 0), sb=(0, 0), sc=(0, 0), onchip=False, b_exact=False):
+    """onchip=True: 3xTF32 with the operand residuals computed in shared memory.
+    b_exact=True: B is tf32-exact (bf16-valued); b_small may be None, 2 MMAs per product."""
     d = GemmDesc(m, n, k, _ptr(a), _ptr(a_small), lda, int(a_mn), _ptr(b), _ptr(b_small), ldb, int(b_mn), _ptr(c),
                  ldc, alpha, beta, z1, z2, sa[0], sa[1], sb[0], sb[1], sc[0], sc[1])
     stream = torch.cuda.current_stream().cuda_stream
-    if onchip:
-        check(_cfg().sd_gemm_tf32_ex(C.byref(d), None, ONCHIP_RESIDUAL, stream))
+    if onchip or b_exact:
+        flags = (ONCHIP_RESIDUAL if onchip else 0) | (B_EXACT if b_exact else 0)
+        check(_cfg().sd_gemm_tf32_ex(C.byref(d), None, flags, stream))
     else:
         check(_cfg().sd_gemm_tf32(C.byref(d), stream))
 

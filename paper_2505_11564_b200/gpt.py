@@ -20,7 +20,8 @@ _M64 = (1 << 64) - 1
 
 class GptConfig(C.Structure):
     _fields_ = [("n_layer", C.c_int), ("d", C.c_int), ("n_head", C.c_int), ("ff", C.c_int), ("vocab", C.c_int),
-                ("ctx", C.c_int), ("arch", C.c_int), ("rope_base", C.c_float), ("n_kv_head", C.c_int)]
+                ("ctx", C.c_int), ("arch", C.c_int), ("rope_base", C.c_float), ("n_kv_head", C.c_int),
+                ("bf16_weights", C.c_int)]
 
 
 ARCH_GPT2, ARCH_LLAMA = 0, 1
@@ -77,7 +78,8 @@ def _L():
 
 def _cfg(cfg: dict) -> GptConfig:
     return GptConfig(cfg["n_layer"], cfg["d"], cfg["n_head"], cfg["ff"], cfg["vocab"], cfg["ctx"],
-                     cfg.get("arch", ARCH_GPT2), float(cfg.get("rope_base", 10000.0)), cfg.get("n_kv_head", 0))
+                     cfg.get("arch", ARCH_GPT2), float(cfg.get("rope_base", 10000.0)), cfg.get("n_kv_head", 0),
+                     int(cfg.get("bf16_weights", 0)))
 
 
 def param_count(cfg: dict) -> int:

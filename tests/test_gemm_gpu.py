@@ -136,3 +136,25 @@ def test_gemm_onchip_residual_bitwise(G, a_t, b_t, shape):
     G.gemm_dual(M, N, K, A, A.shape[1], a_t, B, B.shape[1], not b_t, A2, A2.shape[1], B2, B2.shape[1], D1, N,
                 alpha=0.5, onchip=True)
     assert torch.equal(D0, D1)
+
+
+@pytest.mark.parametrize("a_t", [False, True])
+@pytest.mark.parametrize("b_t", [False, True])
+@pytest.mark.parametrize("shape", [(256, 384, 768), (200, 300, 100), (1024, 64, 1024), (768, 768, 8192), (8192, 512, 64)])
+def test_gemm_b_exact_bitwise(G, a_t, b_t, shape):
+    # bf16-valued B (tf32-exact): SD_GEMM_B_EXACT skips the zero residual's load
+    # and its MMA -- bit-identical to passing the all-zero residual array, and
+    # still fp32-faithful against float64
+    M, N, K = shape
+    g = torch.Generator(device="cuda").manual_seed(M + 5 * N + 11 * K)
+    A = torch.randn(*((K, M) if a_t else (M, K)), device="cuda", generator=g)
+    B = torch.randn(*((N, K) if b_t else (K, N)), device="cuda", generator=g).bfloat16().float()
+    assert torch.count_nonzero(G.split(B)) == 0
+    args = (M, N, K, A, A.shape[1], a_t, B, B.shape[1], not b_t)
+    C0 = torch.empty(M, N, device="cuda")
+    C1 = torch.empty(M, N, device="cuda")
+    G.gemm(*args, C0, N, a_small=G.split(A), b_small=G.split(B))
+    G.gemm(*args, C1, N, a_small=G.split(A), b_exact=True)
+    assert torch.equal(C0, C1)
+    ref = (A.double().t() if a_t else A.double()) @ (B.double().t() if b_t else B.double())
+    assert rel(C1, ref) < 2e-6

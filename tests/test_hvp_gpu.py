@@ -190,3 +190,27 @@ def test_llama2_7b_layer_shape_runs():
     a, b = float(torch.dot(hu.double(), w.double())), float(torch.dot(u.double(), hw.double()))
     assert abs(a - b) <= 1e-4 * max(abs(a), abs(b))
     eng.close()
+
+
+@pytest.mark.parametrize("cfg", [dict(LTINY, n_kv_head=2, bf16_weights=1), dict(TINY, bf16_weights=1)])
+def test_bf16_weights_engine(sd, oracle, cfg):
+    # BASELINE C5 "bf16 weights": bf16-valued parameters are exact in tf32, so the
+    # engine keeps no weight residuals and runs the weight products with 2 MMAs.
+    # Bit-identical to the residual engine on the same parameters; f64 oracle 1e-5.
+    from paper_2505_11564_b200 import gpt
+    B, S = 2, 32
+    eng = gpt.GptHvp(cfg, B, S, init_seed=0, gain_scale=0.1, bias_scale=0.1)
+    th = eng.theta
+    assert bool(((th.view(torch.int32) & 0xFFFF) == 0).all())  # bf16-valued
+    ref_cfg = dict(cfg, bf16_weights=0)
+    eng32 = gpt.GptHvp(ref_cfg, B, S, theta=th.clone())
+    assert eng.workspace.numel() < eng32.workspace.numel()  # no weight residuals
+    v = torch.tensor(oracle.draw_probe(eng.P, 3, 1, prec=0), dtype=torch.float32, device="cuda")
+    hv = eng.hvp(v)
+    assert torch.equal(hv, eng32.hvp(v))
+    tok, tgt = eng.tokens_numpy()
+    ref = oracle.gpt_hvp(cfg, eng.theta_numpy(), tok, tgt, B, S, v.double().cpu().numpy())
+    assert rel(hv.double().cpu().numpy(), ref) < TOL
+    # non-bf16 parameters are refused
+    with pytest.raises(sd.ConfigError):
+        gpt.GptHvp(cfg, B, S, theta=th + 1e-3)
