@@ -241,11 +241,17 @@ sd_status sd_gpt_set_batch(sd_gpt g, const int* tokens, const int* targets, floa
  * of micro_batch x seq tokens (set_batch takes all of them) run through
  * n_sets activation sets (micro-batch m uses set m % n_sets). The whole model
  * with n_micro > 1 is a memory-bounded single-device HVP. */
+/* engine flags (SD_ARCH_LLAMA): SD_GPT_RECOMPUTE keeps only each layer's input
+ * per in-flight micro-batch and re-runs the layer in the backward (bit-identical
+ * Hv, one extra layer forward); SD_GPT_NO_PROBE_RESIDUAL keeps no tf32 residual
+ * of v (the tangent products form it on chip). Together with bf16_weights they
+ * take the per-stage memory of BASELINE C5 under 180 GB. */
+enum { SD_GPT_RECOMPUTE = 1, SD_GPT_NO_PROBE_RESIDUAL = 2 };
 uint64_t sd_gpt_stage_workspace_bytes(const sd_gpt_config* c, int micro_batch, int seq, int n_micro, int layer_begin,
-                                      int layer_end, int n_sets);
+                                      int layer_end, int n_sets, int flags);
 sd_status sd_gpt_stage_params(const sd_gpt_config* c, int layer_begin, int layer_end, uint64_t* begin, uint64_t* end);
 sd_status sd_gpt_stage_create(const sd_gpt_config* c, int micro_batch, int seq, int n_micro, int layer_begin,
-                              int layer_end, int n_sets, const float* theta_stage, void* workspace,
+                              int layer_end, int n_sets, int flags, const float* theta_stage, void* workspace,
                               uint64_t workspace_bytes, sd_stream s, sd_gpt* out);
 /* one Hv pass: begin (v, Hv = stage slices), then forward/backward per
  * micro-batch in a 1F1B order; Hv of micro-batches after the first accumulates */

@@ -173,14 +173,23 @@ struct sd_gpt_s {
   const float* vcur = nullptr;
   float* hvcur = nullptr;
   bool acc = false;
+  // SD_GPT_RECOMPUTE: a set keeps only each layer's input [x | dx] (XIN) and
+  // the backward re-runs the layer into the one scratch layer (Lscratch, xr);
+  // SD_GPT_NO_PROBE_RESIDUAL: no v residual array (v_s), the tangent products
+  // form all residuals on chip
+  bool recompute = false, probe_res = true;
+  Layer Lscratch{};
+  std::vector<std::vector<float*>> XIN;
+  float* xr = nullptr;
+  int set_of(int m) const { return m % nsets; }
 
   void carve(Plan& p) {
     const long long T_ = T, d = c.d, ff = c.ff, ffw = c.arch == SD_ARCH_LLAMA ? 2 * ff : ff;
     auto td = [&] { return p.take<float>(T_ * d); };
-    LS.assign(nsets, std::vector<Layer>(l1 - l0));
+    LS.assign(nsets, std::vector<Layer>(recompute ? 0 : l1 - l0));
     XS.assign(nsets, nullptr);
-    for (int si = 0; si < nsets; ++si) {
-      for (auto& l : LS[si]) {
+    XIN.assign(nsets, std::vector<float*>(recompute ? l1 - l0 : 0, nullptr));
+    auto layer_arrays = [&](Layer& l) {
         l.xh1 = td(), l.dxh1 = td(), l.h1 = td(), l.h1s = td(), l.dh1 = td(), l.dh1s = td();
         l.r1 = p.take<float>(T_), l.dr1 = p.take<float>(T_);
         l.a = p.take<float>(T_ * 3 * d), l.as = p.take<float>(T_ * 3 * d);
@@ -197,8 +206,15 @@ struct sd_gpt_s {
         if (gqa())
           l.qkv = p.take<float>(T_ * W), l.qkvs = p.take<float>(T_ * W), l.dqkv = p.take<float>(T_ * W),
           l.dqkvs = p.take<float>(T_ * W);
-      }
+    };
+    for (int si = 0; si < nsets; ++si) {
+      for (auto& l : LS[si]) layer_arrays(l);
+      for (auto& xi : XIN[si]) xi = p.take<float>(2 * T_ * d);
       XS[si] = p.take<float>(2 * T_ * d);
+    }
+    if (recompute) {
+      layer_arrays(Lscratch);
+      xr = p.take<float>(2 * T_ * d);
     }
     if (last) {
       xhf = td(), dxhf = td(), hf = td(), hfs = td(), dhf = td(), dhfs = td();
@@ -222,7 +238,7 @@ struct sd_gpt_s {
       gqkv = p.take<float>(T_ * W), gqkvs = p.take<float>(T_ * W), gdqkv = p.take<float>(T_ * W),
       gdqkvs = p.take<float>(T_ * W);
     theta_s = c.bf16_weights ? nullptr : p.take<float>(Pst);  // bf16 weights: exact in tf32, no residual
-    v_s = p.take<float>(Pst);
+    v_s = probe_res ? p.take<float>(Pst) : nullptr;
     red = p.take<float>(2LL * 64 * std::max(3 * d, ff));
     if (first) {
       tok = p.take<int>(T_ * nmb), uniq = p.take<int>((T_ + 1) * nmb), ustart = p.take<int>((T_ + 1) * nmb);
@@ -233,7 +249,7 @@ struct sd_gpt_s {
   }
   void use_set(int m) {
     const int si = m % nsets;
-    L = LS[si].data();
+    L = recompute ? nullptr : LS[si].data();
     x = XS[si];
     dx = x ? x + (long long)T * c.d : nullptr;
   }
@@ -416,25 +432,38 @@ struct sd_gpt_s {
 
   // stage-local views of v, its tf32 residual and Hv for parameter slot i
   const float* V_(int i) const { return vcur + (slots[i].off - pbase); }
-  const float* Vs(int i) const { return v_s + (slots[i].off - pbase); }
+  const float* Vs(int i) const { return v_s ? v_s + (slots[i].off - pbase) : nullptr; }
   float* HV(int i) const { return hvcur + (slots[i].off - pbase); }
 
   void stage_begin(const float* v, float* hv, cudaStream_t st) {
     if (!have_batch) fail(SD_STATE_ERROR, "gpt: set_batch was not called");
     vcur = v, hvcur = hv;
-    sd::gpt_residual(v, v_s, Pst, st);
+    if (v_s) sd::gpt_residual(v, v_s, Pst, st);
   }
 
   // Forward (primal + tangent) of micro-batch m through layers [l0, l1). The
   // set's [x | dx] holds the stage input (the first stage embeds the tokens)
   // and, on return, the stage output.
   void stage_fwd(int m, cudaStream_t st) {
+    use_set(m);
+    if (first) sd::gpt_embed(tok + (long long)m * T, T, S, c.d, th(0), nullptr, V_(0), nullptr, x, dx, st);
+    const size_t xb = 2ull * size_t(T) * c.d * sizeof(float);
+    for (int l = l0; l < l1; ++l) {
+      if (recompute) {  // keep only the layer input; the backward re-runs the layer
+        SD_CUDA(cudaMemcpyAsync(XIN[set_of(m)][l - l0], x, xb, cudaMemcpyDeviceToDevice, st));
+        layer_fwd(Lscratch, l, x, dx, st);
+      } else {
+        layer_fwd(L[l - l0], l, x, dx, st);
+      }
+    }
+  }
+
+  // one Llama layer, primal + tangent: [x | dx] += attention and MLP blocks;
+  // the layer's activations (those the double backward reads) land in Ly
+  void layer_fwd(Layer& Ly, int l, float* x, float* dx, cudaStream_t st) {
     const int d = c.d, ff = c.ff;
     const float sc = 1.0f / std::sqrt(float(dh)), eps = 1e-5f;
-    use_set(m);
-    if (first) sd::gpt_embed(tok + (long long)m * T, T, S, d, th(0), nullptr, V_(0), nullptr, x, dx, st);
-    for (int l = l0; l < l1; ++l) {
-      Layer& Ly = L[l - l0];
+    {
       const int b = 1 + 6 * l;  // attention_norm
       sd::LnArgs la{x, dx, th(b), nullptr, V_(b), nullptr, T, d, eps,
                     Ly.h1, Ly.h1s, Ly.dh1, Ly.dh1s, Ly.xh1, Ly.dxh1, Ly.r1, Ly.dr1, 1};
@@ -500,7 +529,28 @@ struct sd_gpt_s {
       sd::gpt_residual(gdx, gdxs, Td, st);
     }
     for (int l = l1 - 1; l >= l0; --l) {
-      Layer& Ly = L[l - l0];
+      if (recompute) {  // re-run the layer from its saved input (bit-identical activations)
+        SD_CUDA(cudaMemcpyAsync(xr, XIN[set_of(m)][l - l0], 2ull * size_t(T) * c.d * sizeof(float),
+                                cudaMemcpyDeviceToDevice, st));
+        layer_fwd(Lscratch, l, xr, xr + (long long)T * c.d, st);
+        layer_bwd(Lscratch, l, hb, st);
+      } else {
+        layer_bwd(L[l - l0], l, hb, st);
+      }
+    }
+    if (first) {
+      if (!acc) SD_CUDA(cudaMemsetAsync(HV(0), 0, slots[0].rows * slots[0].cols * sizeof(float), st));
+      sd::gpt_embed_bwd(uniq + (long long)m * (T + 1), ustart + (long long)m * (T + 1), upos + (long long)m * T,
+                        n_uniq_mb[m], B, S, d, gdx, HV(0), nullptr, st);
+    }
+  }
+
+  // one Llama layer backward: [gx | gdx] hold the adjoint of the layer output
+  // and, on return, of its input; Hv of the layer's parameters (beta hb)
+  void layer_bwd(Layer& Ly, int l, float hb, cudaStream_t st) {
+    const int d = c.d, ff = c.ff;
+    const float sc = 1.0f / std::sqrt(float(dh));
+    {
       const int b = 1 + 6 * l;
       // down projection: ga = gx Wd^T ; gda = gdx Wd^T + gx VWd^T ; Hv_Wd = da^T gx + a^T gdx
       mm(T, ff, d, {gx, gxs, d, false}, Wt(b + 5, d, false), ga_mlp, ff, 1, 0, st);
@@ -541,11 +591,6 @@ struct sd_gpt_s {
       sd::LnBwdArgs b1{gh, gdh, th(b), V_(b), Ly.xh1, Ly.dxh1, Ly.r1, Ly.dr1, T, d,
                        gx, gdx, gxs, gdxs, HV(b), nullptr, red, 1, int(acc)};
       sd::gpt_ln_bwd(b1, st);
-    }
-    if (first) {
-      if (!acc) SD_CUDA(cudaMemsetAsync(HV(0), 0, slots[0].rows * slots[0].cols * sizeof(float), st));
-      sd::gpt_embed_bwd(uniq + (long long)m * (T + 1), ustart + (long long)m * (T + 1), upos + (long long)m * T,
-                        n_uniq_mb[m], B, S, d, gdx, HV(0), nullptr, st);
     }
   }
 
@@ -620,7 +665,7 @@ void stage_range(const sd_gpt_config& c, int l0, int l1, const std::vector<Slot>
 }
 
 struct StageSpec {
-  int l0 = 0, l1 = -1, nmb = 1, nsets = 1;
+  int l0 = 0, l1 = -1, nmb = 1, nsets = 1, flags = 0;
 };
 
 Plan plan_for(const sd_gpt_config& c, int B, int S, char* base, sd_gpt_s* g, StageSpec sp = {}) {
@@ -635,6 +680,8 @@ Plan plan_for(const sd_gpt_config& c, int B, int S, char* base, sd_gpt_s* g, Sta
   e->W = c.d + 2 * e->KV * e->dh;
   e->l0 = sp.l0, e->l1 = sp.l1 < 0 ? c.n_layer : sp.l1;
   e->nmb = sp.nmb, e->nsets = sp.nsets;
+  e->recompute = (sp.flags & SD_GPT_RECOMPUTE) != 0;
+  e->probe_res = (sp.flags & SD_GPT_NO_PROBE_RESIDUAL) == 0;
   e->first = e->l0 == 0, e->last = e->l1 == c.n_layer;
   if (e->first && e->last) {
     e->pbase = 0, e->Pst = e->P;
@@ -653,8 +700,9 @@ void check_stage(const sd_gpt_config& c, const StageSpec& sp) {
   const bool whole = sp.l0 == 0 && sp.l1 == c.n_layer;
   if (sp.l0 < 0 || sp.l1 > c.n_layer || sp.l0 >= sp.l1) fail(SD_LAYOUT_ERROR, "stage layer range out of bounds");
   if (sp.nmb < 1 || sp.nsets < 1 || sp.nsets > sp.nmb) fail(SD_ARGUMENT_ERROR, "need 1 <= n_sets <= n_micro");
-  if ((!whole || sp.nmb > 1) && c.arch != SD_ARCH_LLAMA)
-    fail(SD_CONFIG_ERROR, "pipeline stages / micro-batches need the untied Llama-style layout");
+  if ((!whole || sp.nmb > 1 || sp.flags) && c.arch != SD_ARCH_LLAMA)
+    fail(SD_CONFIG_ERROR, "pipeline stages / micro-batches / engine flags need the untied Llama-style layout");
+  if (sp.flags & ~(SD_GPT_RECOMPUTE | SD_GPT_NO_PROBE_RESIDUAL)) fail(SD_ARGUMENT_ERROR, "unknown engine flags");
 }
 
 struct GptOpCtx {
@@ -776,15 +824,15 @@ sd_status sd_gpt_init_params(const sd_gpt_config* c, uint64_t seed, double gain_
 }
 
 uint64_t sd_gpt_workspace_bytes(const sd_gpt_config* c, int batch, int seq) {
-  return sd_gpt_stage_workspace_bytes(c, batch, seq, 1, 0, c ? c->n_layer : 0, 1);
+  return sd_gpt_stage_workspace_bytes(c, batch, seq, 1, 0, c ? c->n_layer : 0, 1, 0);
 }
 
 uint64_t sd_gpt_stage_workspace_bytes(const sd_gpt_config* c, int micro_batch, int seq, int n_micro, int layer_begin,
-                                      int layer_end, int n_sets) {
+                                      int layer_end, int n_sets, int flags) {
   try {
     if (!c) fail(SD_ARGUMENT_ERROR, "null config");
     check_cfg(*c, micro_batch, seq);
-    const StageSpec sp{layer_begin, layer_end, n_micro, n_sets};
+    const StageSpec sp{layer_begin, layer_end, n_micro, n_sets, flags};
     check_stage(*c, sp);
     return plan_for(*c, micro_batch, seq, nullptr, nullptr, sp).bytes;
   } catch (const std::exception& e) {
@@ -798,7 +846,7 @@ sd_status sd_gpt_stage_params(const sd_gpt_config* c, int layer_begin, int layer
   return sd::guard([&] {
     if (!c || !begin || !end) fail(SD_ARGUMENT_ERROR, "null argument");
     check_cfg(*c, 1, 4);
-    check_stage(*c, StageSpec{layer_begin, layer_end, 1, 1});
+    check_stage(*c, StageSpec{layer_begin, layer_end, 1, 1, 0});
     if (layer_begin == 0 && layer_end == c->n_layer) {
       *begin = 0, *end = param_count(*c);
       return;
@@ -808,12 +856,12 @@ sd_status sd_gpt_stage_params(const sd_gpt_config* c, int layer_begin, int layer
 }
 
 sd_status sd_gpt_stage_create(const sd_gpt_config* c, int micro_batch, int seq, int n_micro, int layer_begin,
-                              int layer_end, int n_sets, const float* theta_stage, void* ws, uint64_t bytes,
-                              sd_stream s, sd_gpt* out) {
+                              int layer_end, int n_sets, int flags, const float* theta_stage, void* ws,
+                              uint64_t bytes, sd_stream s, sd_gpt* out) {
   return sd::guard([&] {
     if (!c || !out) fail(SD_ARGUMENT_ERROR, "null argument");
     check_cfg(*c, micro_batch, seq);
-    const StageSpec sp{layer_begin, layer_end, n_micro, n_sets};
+    const StageSpec sp{layer_begin, layer_end, n_micro, n_sets, flags};
     check_stage(*c, sp);
     auto g = std::make_unique<sd_gpt_s>();
     const Plan p = plan_for(*c, micro_batch, seq, static_cast<char*>(ws), g.get(), sp);
@@ -837,7 +885,7 @@ sd_status sd_gpt_stage_create(const sd_gpt_config* c, int micro_batch, int seq, 
 
 sd_status sd_gpt_create(const sd_gpt_config* c, int batch, int seq, const float* theta, void* ws, uint64_t bytes,
                         sd_stream s, sd_gpt* out) {
-  return sd_gpt_stage_create(c, batch, seq, 1, 0, c ? c->n_layer : 0, 1, theta, ws, bytes, s, out);
+  return sd_gpt_stage_create(c, batch, seq, 1, 0, c ? c->n_layer : 0, 1, 0, theta, ws, bytes, s, out);
 }
 
 // Uploads a batch (host int32 tokens/targets, n_micro * batch * seq each) and

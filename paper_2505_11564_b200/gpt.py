@@ -56,10 +56,11 @@ def _L():
             "sd_operator_gpt": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_void_p)]),
             "sd_operator_gpt_sharded": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_uint64),
                                                   C.POINTER(C.c_uint64), C.POINTER(C.c_void_p)]),
-            "sd_gpt_stage_workspace_bytes": (C.c_uint64, [cp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int]),
+            "sd_gpt_stage_workspace_bytes": (C.c_uint64, [cp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                                          C.c_int]),
             "sd_gpt_stage_params": (C.c_int, [cp, C.c_int, C.c_int, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
-            "sd_gpt_stage_create": (C.c_int, [cp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p,
-                                              C.c_void_p, C.c_uint64, C.c_void_p, C.POINTER(C.c_void_p)]),
+            "sd_gpt_stage_create": (C.c_int, [cp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                              C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.POINTER(C.c_void_p)]),
             "sd_gpt_stage_begin": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
             "sd_gpt_stage_forward": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                                C.c_void_p]),
@@ -205,6 +206,17 @@ class GptHvp:
 # ------------------------------------------------------------ pipeline stages
 PIPE_F, PIPE_B, PIPE_SEND_F, PIPE_RECV_F, PIPE_SEND_B, PIPE_RECV_B, PIPE_GROUP_BEGIN, PIPE_GROUP_END = range(8)
 PIPE_NAMES = ["F", "B", "SEND_F", "RECV_F", "SEND_B", "RECV_B", "GROUP_BEGIN", "GROUP_END"]
+RECOMPUTE, NO_PROBE_RESIDUAL = 1, 2  # engine flags (sd_gpt_stage_create)
+
+
+def stage_workspace_bytes(cfg: dict, micro_batch: int, seq: int, n_micro: int, layer_begin: int, layer_end: int,
+                          n_sets: int, flags: int = 0) -> int:
+    """Device workspace of one stage (host-side planning; no GPU needed)."""
+    n = _L().sd_gpt_stage_workspace_bytes(C.byref(_cfg(cfg)), micro_batch, seq, n_micro, layer_begin, layer_end,
+                                          n_sets, flags)
+    if n == 0:
+        check(3)
+    return int(n)
 
 
 def pipeline_schedule(n_stages: int, stage: int, n_micro: int):
@@ -249,7 +261,8 @@ class GptStage:
 
     def __init__(self, cfg: dict, micro_batch: int, seq: int, n_micro: int, layer_begin: int, layer_end: int,
                  theta_stage: torch.Tensor, n_sets: int | None = None, tokens=None, targets=None,
-                 loss_scale: float | None = None, stream=None):
+                 loss_scale: float | None = None, stream=None, recompute: bool = False,
+                 probe_residual: bool = True):
         self.cfg = dict(cfg)
         self.B, self.S, self.M = micro_batch, seq, n_micro
         self.l0, self.l1 = layer_begin, layer_end
@@ -261,16 +274,18 @@ class GptStage:
         self.stream = stream or torch.cuda.current_stream()
         assert theta_stage.dtype == torch.float32 and theta_stage.numel() == self.end - self.begin
         self.theta = theta_stage
+        self.flags = (RECOMPUTE if recompute else 0) | (0 if probe_residual else NO_PROBE_RESIDUAL)
         nbytes = _L().sd_gpt_stage_workspace_bytes(C.byref(self._c), micro_batch, seq, n_micro, layer_begin,
-                                                   layer_end, self.n_sets)
+                                                   layer_end, self.n_sets, self.flags)
         if nbytes == 0:  # invalid shape: the create call raises the precise error class
             check(_L().sd_gpt_stage_create(C.byref(self._c), micro_batch, seq, n_micro, layer_begin, layer_end,
-                                           self.n_sets, None, None, 0, self._s(), C.byref(C.c_void_p())))
+                                           self.n_sets, self.flags, None, None, 0, self._s(),
+                                           C.byref(C.c_void_p())))
         self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
         self.h = C.c_void_p()
         check(_L().sd_gpt_stage_create(C.byref(self._c), micro_batch, seq, n_micro, layer_begin, layer_end,
-                                       self.n_sets, theta_stage.data_ptr(), self.workspace.data_ptr(), nbytes,
-                                       self._s(), C.byref(self.h)))
+                                       self.n_sets, self.flags, theta_stage.data_ptr(), self.workspace.data_ptr(),
+                                       nbytes, self._s(), C.byref(self.h)))
         if tokens is None:
             tokens, targets = synthetic_tokens(cfg["vocab"], micro_batch * n_micro, seq)
         tok = np.ascontiguousarray(tokens, dtype=np.int32)

@@ -35,14 +35,14 @@ def rel(a, b):
     return float(np.linalg.norm(a - b) / np.linalg.norm(b))
 
 
-def run_pipeline(gpt, cfg, B, S, M, n_stages, theta, v, tokens, targets, n_sets=None):
+def run_pipeline(gpt, cfg, B, S, M, n_stages, theta, v, tokens, targets, n_sets=None, **flags):
     """All stages in one process in 1F1B order; returns the full Hv (concatenated stage slices)."""
     ranges = gpt.pipeline_layers(cfg["n_layer"], n_stages)
     stages, hv = [], torch.zeros_like(v)
     for s, (a, b) in enumerate(ranges):
         pb, pe = gpt.stage_params(cfg, a, b)
         ns = min(M, n_stages - s) if n_sets is None else n_sets
-        st = gpt.GptStage(cfg, B, S, M, a, b, theta[pb:pe], n_sets=ns, tokens=tokens, targets=targets)
+        st = gpt.GptStage(cfg, B, S, M, a, b, theta[pb:pe], n_sets=ns, tokens=tokens, targets=targets, **flags)
         st.begin_pass(v[pb:pe], hv[pb:pe])
         stages.append(st)
     Td = B * S * cfg["d"]
@@ -178,3 +178,17 @@ def test_pipeline_operator_one_rank_lanczos(gpt):
         comm.close()
         if own:
             dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("bf16", [0, 1])
+def test_lean_modes_bitwise(gpt, bf16):
+    # the memory modes that fit BASELINE C5 per GPU: layer recomputation in the
+    # backward and on-chip probe residuals (and bf16-valued weights) change no bit of Hv
+    cfg, B, S, M, n_st = dict(LT, n_kv_head=2, bf16_weights=bf16), 1, 32, 3, 2
+    eng, v, tok, tgt = _setup(gpt, cfg, B, S, M, seed=7)
+    base, _ = run_pipeline(gpt, cfg, B, S, M, n_st, eng.theta, v, tok, tgt)
+    for rc, pr in ((True, True), (False, False), (True, False)):
+        hv, st = run_pipeline(gpt, cfg, B, S, M, n_st, eng.theta, v, tok, tgt, recompute=rc, probe_residual=pr)
+        assert torch.equal(hv, base), (rc, pr)
+    lean = gpt.stage_workspace_bytes(cfg, B, S, M, 0, 2, 2, gpt.RECOMPUTE | gpt.NO_PROBE_RESIDUAL)
+    assert lean < gpt.stage_workspace_bytes(cfg, B, S, M, 0, 2, 2, 0)
