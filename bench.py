@@ -357,6 +357,101 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+# ------------------------------------------------- pipeline workloads (C4/C5)
+PIPE_WORKLOADS = {
+    # BASELINE configs[3]: 7B Llama-style decoder, parameter-sharded Lanczos vectors,
+    # scalar-dot allreduce, selective reorth (window of the 8 most recent columns)
+    "c4": dict(model="LLAMA2_7B", bf16=0, flags=0, reorth="selective", window=8, k_max=32),
+    # BASELINE configs[4]: 70B architecture, bf16 weights / fp32 Lanczos, 3-term recurrence
+    "c5": dict(model="LLAMA_70B", bf16=1, flags=3, reorth="none", window=0, k_max=10),
+}
+
+
+def run_pipeline_workload(args):
+    """C4/C5: pipeline-parallel HVP over the N ranks (stage r = layers
+    split_evenly(n_layer, N)[r]), Lanczos vectors sharded by the stages'
+    parameter slices, M micro-batches of 1 x seq tokens per HVP on the 1F1B
+    schedule. --layers shrinks the depth (to run the path on fewer GPUs)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2505_11564_b200 as sd
+    from paper_2505_11564_b200 import gpt
+    from paper_2505_11564_b200._lib import lib
+
+    wl = PIPE_WORKLOADS[args.workload]
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29543")
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", local))
+    comm = sd.nccl_comm()
+    cfg = dict(getattr(gpt, wl["model"]), bf16_weights=wl["bf16"])
+    if args.layers:
+        cfg["n_layer"] = args.layers
+    M, S = args.micro_batches, args.seq
+    l0, l1 = gpt.pipeline_layers(cfg["n_layer"], world)[rank]
+    b, e = gpt.stage_params(cfg, l0, l1)
+    theta = gpt.init_params_range(cfg, b, e, init_seed=0)
+    tok, tgt = gpt.synthetic_tokens(cfg["vocab"], M, S, seed=1)
+    st = gpt.GptStage(cfg, 1, S, M, l0, l1, theta, n_sets=min(M, world - rank), tokens=tok, targets=tgt,
+                      recompute=bool(wl["flags"] & 1), probe_residual=not (wl["flags"] & 2))
+    layout = gpt.pipeline_layout(cfg, world)
+    reorth = {"selective": sd.REORTH_SELECTIVE, "none": sd.REORTH_NONE}[wl["reorth"]]
+    k_max = max(args.k_max if args.k_max != 100 else wl["k_max"], args.steps + args.warmup + 1)
+    lc = sd.LanczosConfig(k_max=k_max, reorthogonalize=reorth, prec=sd.F32,
+                          probe=sd.ProbeSpec(seed=0, distribution=sd.RADEMACHER), selective_window=wl["window"])
+    L = sd.Lanczos(st.operator(comm), lc, layout=layout, comm=comm)
+    for _ in range(args.warmup):
+        L.step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    L0 = lib()
+    check = sd._lib.check
+    check(L0.sd_gemm_profile_begin())
+    launches0 = L0.sd_launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(args.steps):
+            L.step()
+        e1.record()
+        torch.cuda.synchronize()
+    dist.barrier()
+    g_ms, g_fl, g_n = C.c_double(), C.c_double(), C.c_uint64()
+    check(L0.sd_gemm_profile_end(C.byref(g_ms), C.byref(g_fl), C.byref(g_n)))
+    launches = L0.sd_launch_count() - launches0
+    t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_step = float(t.item()) / args.steps
+    hbm, bf16, basis = peaks()
+    tf32, tf32_basis = tf32_peak(bf16)
+    achieved = g_fl.value / (g_ms.value * 1e-3) / 1e12 if g_ms.value > 0 else 0.0
+    line = {
+        "metric": METRIC, "value": 1000.0 / ms_step, "unit": "steps/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32 (3xTF32 GEMMs" + (", bf16-valued weights" if wl["bf16"] else "") + ")",
+        "data": "synthetic (counter-keyed tokens, random-init weights)",
+        "config": {"workload": f"BASELINE {args.workload.upper()}: pipeline-parallel HVP, {world} stage(s)",
+                   "model": wl["model"], "n_layer": cfg["n_layer"], "params": gpt.param_count(cfg),
+                   "micro_batches": M, "seq_len": S, "tokens_per_hvp": M * S, "reorth": wl["reorth"],
+                   "k_max": k_max, "engine_flags": wl["flags"], "parallelism": f"pp{world}",
+                   "bubble_bound": M / (M + world - 1)},
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": tf32 / 3.0, "unit": "TFLOP/s",
+                     "frac": achieved / (tf32 / 3.0), "traffic": None,
+                     "kernel": "all GEMM launches of rank 0's stage", "peak_note": f"{tf32_basis} / 3"},
+        "gpu_launches": int(launches), "clocks": clk.summary(),
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    L.close()
+    comm.close()
+    dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -369,11 +464,17 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--comm", action="store_true", help="use the NCCL/sharded path even on one rank")
+    ap.add_argument("--workload", default="c2", choices=["c2", "c4", "c5"],
+                    help="c2 (default, the metric's config) or the C4/C5 pipeline-parallel workloads")
+    ap.add_argument("--layers", type=int, default=0, help="C4/C5: override the depth (0 = the model's)")
+    ap.add_argument("--micro-batches", type=int, default=32, help="C4/C5: micro-batches per HVP")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
     if args.impl == "reference":
         run_reference(args)
+    elif args.workload != "c2":
+        run_pipeline_workload(args)
     else:
         run_ours(args)
 

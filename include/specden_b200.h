@@ -226,6 +226,9 @@ sd_status sd_gpt_param_layout(const sd_gpt_config* c, uint64_t* offsets, uint64_
  * bias_scale*N, N = gaussian(seed, flat index) (rng.hpp:37-41) */
 sd_status sd_gpt_init_params(const sd_gpt_config* c, uint64_t seed, double gain_scale, double bias_scale,
                              float* theta, sd_stream s);
+/* the same values for the flat range [begin, end) only: theta_slice[i - begin] */
+sd_status sd_gpt_init_params_range(const sd_gpt_config* c, uint64_t seed, double gain_scale, double bias_scale,
+                                   uint64_t begin, uint64_t end, float* theta_slice, sd_stream s);
 uint64_t sd_gpt_workspace_bytes(const sd_gpt_config* c, int batch, int seq);
 /* theta: caller-owned device parameters (P floats), must outlive the engine */
 sd_status sd_gpt_create(const sd_gpt_config* c, int batch, int seq, const float* theta, void* workspace,

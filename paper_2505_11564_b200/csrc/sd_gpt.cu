@@ -823,6 +823,26 @@ sd_status sd_gpt_init_params(const sd_gpt_config* c, uint64_t seed, double gain_
   });
 }
 
+// The same values for the flat-index range [begin, end) only (a pipeline
+// stage's slice: theta_slice[i - begin]); bit-identical to the full init.
+sd_status sd_gpt_init_params_range(const sd_gpt_config* c, uint64_t seed, double gain_scale, double bias_scale,
+                                   uint64_t begin, uint64_t end, float* theta_slice, sd_stream s) {
+  return sd::guard([&] {
+    if (!c || !theta_slice) fail(SD_ARGUMENT_ERROR, "null argument");
+    const auto lay = layout(*c);
+    const uint64_t P = lay.back().off + lay.back().rows * lay.back().cols;
+    if (begin >= end || end > P) fail(SD_LAYOUT_ERROR, "init range out of bounds");
+    for (const Slot& sl : lay) {
+      const uint64_t a = std::max<uint64_t>(sl.off, begin), b = std::min<uint64_t>(sl.off + sl.rows * sl.cols, end);
+      if (a >= b) continue;
+      const double base = sl.kind == 1 ? 1.0 : 0.0;
+      const double sc = sl.kind == 0 ? 0.02 : (sl.kind == 1 ? gain_scale : bias_scale);
+      sd::gpt_init_slot(theta_slice, (long long)a, (long long)(b - a), seed, base, sc, (cudaStream_t)s,
+                        c->bf16_weights != 0, (long long)begin);
+    }
+  });
+}
+
 uint64_t sd_gpt_workspace_bytes(const sd_gpt_config* c, int batch, int seq) {
   return sd_gpt_stage_workspace_bytes(c, batch, seq, 1, 0, c ? c->n_layer : 0, 1, 0);
 }

@@ -58,8 +58,9 @@ void gpt_embed_bwd(const int* uniq, const int* start, const int* pos, int n_uniq
                    const float* gdx, float* hv_wte, float* hv_wpe, cudaStream_t s);
 void gpt_residual(const float* x, float* xs, long long n, cudaStream_t s);
 void gpt_fill(float* x, float v, long long n, cudaStream_t s);
+// theta[i - th_base] for global flat indices i in [off, off + n)
 void gpt_init_slot(float* th, long long off, long long n, uint64_t seed, double base, double scale, cudaStream_t s,
-                   bool bf16 = false);
+                   bool bf16 = false, long long th_base = 0);
 // elements of x that are not bf16-valued (synchronises the stream; scratch: one u64 on device)
 unsigned long long gpt_count_not_bf16(const float* x, long long n, unsigned long long* scratch, cudaStream_t s);
 

@@ -573,10 +573,10 @@ __global__ void k_fill(float* __restrict__ x, float v, long long n) {
 
 // synthetic init theta[i] = base + scale * gaussian(seed, i) (float), per slot
 __global__ void k_init_slot(float* __restrict__ th, long long off, long long n, uint64_t key, double base,
-                            double scale, int bf16) {
+                            double scale, int bf16, long long th_base) {
   const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (e >= n) return;
-  const uint64_t i = uint64_t(off + e);
+  const uint64_t i = uint64_t(off + e);  // global flat index (the counter): layout-invariant values
   double v = base;
   if (scale != 0.0) {
     const double u1 = __dadd_rn(__dmul_rn(double(keyed_counter_k(key, 2 * i) >> 11), 0x1p-53), 0x1p-54);
@@ -585,7 +585,7 @@ __global__ void k_init_slot(float* __restrict__ th, long long off, long long n, 
     v = __dadd_rn(base, __dmul_rn(scale, gsn));
   }
   const float f = __double2float_rn(v);
-  th[off + e] = bf16 ? __bfloat162float(__float2bfloat16_rn(f)) : f;  // bf16 weights: the f32 value rounded RNE
+  th[off + e - th_base] = bf16 ? __bfloat162float(__float2bfloat16_rn(f)) : f;  // bf16: the f32 value rounded RNE
 }
 
 // number of elements that are not bf16-valued (low 16 mantissa bits set)
@@ -724,9 +724,9 @@ void gpt_fill(float* x, float v, long long n, cudaStream_t s) {
 }
 
 void gpt_init_slot(float* th, long long off, long long n, uint64_t seed, double base, double scale, cudaStream_t s,
-                   bool bf16) {
+                   bool bf16, long long th_base) {
   if (n <= 0) return;
-  k_init_slot<<<g1(n), 256, 0, s>>>(th, off, n, mix64(seed), base, scale, bf16 ? 1 : 0);
+  k_init_slot<<<g1(n), 256, 0, s>>>(th, off, n, mix64(seed), base, scale, bf16 ? 1 : 0, th_base);
   SD_LAUNCHED("k_init_slot");
 }
 

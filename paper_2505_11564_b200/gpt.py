@@ -67,6 +67,8 @@ def _L():
             "sd_gpt_stage_backward": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                                 C.c_void_p]),
             "sd_operator_gpt_pipeline": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_void_p)]),
+            "sd_gpt_init_params_range": (C.c_int, [cp, C.c_uint64, C.c_double, C.c_double, C.c_uint64, C.c_uint64,
+                                                   C.c_void_p, C.c_void_p]),
             "sd_pipeline_schedule": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_uint64,
                                                C.POINTER(C.c_uint64)]),
         }
@@ -243,6 +245,17 @@ def stage_params(cfg: dict, layer_begin: int, layer_end: int):
     b, e = C.c_uint64(), C.c_uint64()
     check(_L().sd_gpt_stage_params(C.byref(_cfg(cfg)), layer_begin, layer_end, C.byref(b), C.byref(e)))
     return int(b.value), int(e.value)
+
+
+def init_params_range(cfg: dict, begin: int, end: int, init_seed: int = 0, gain_scale: float = 0.0,
+                      bias_scale: float = 0.0, out: torch.Tensor | None = None) -> torch.Tensor:
+    """Synthetic parameters of the flat range [begin, end) (a stage's slice),
+    bit-identical to that slice of the full init."""
+    if out is None:
+        out = torch.empty(end - begin, dtype=torch.float32, device=torch.device("cuda", torch.cuda.current_device()))
+    check(_L().sd_gpt_init_params_range(C.byref(_cfg(cfg)), init_seed, gain_scale, bias_scale, begin, end,
+                                        out.data_ptr(), C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    return out
 
 
 def pipeline_layout(cfg: dict, n_stages: int):

@@ -192,3 +192,13 @@ def test_lean_modes_bitwise(gpt, bf16):
         assert torch.equal(hv, base), (rc, pr)
     lean = gpt.stage_workspace_bytes(cfg, B, S, M, 0, 2, 2, gpt.RECOMPUTE | gpt.NO_PROBE_RESIDUAL)
     assert lean < gpt.stage_workspace_bytes(cfg, B, S, M, 0, 2, 2, 0)
+
+
+def test_init_params_range_matches_full_init(gpt):
+    # a stage initialises only its slice: bit-identical to that slice of the full init
+    for cfg in (dict(LT, n_kv_head=2), dict(LT, bf16_weights=1)):
+        full = gpt.GptHvp(cfg, 1, 32, init_seed=5, gain_scale=0.1).theta
+        for a, b in gpt.pipeline_layers(cfg["n_layer"], 3):
+            pb, pe = gpt.stage_params(cfg, a, b)
+            assert torch.equal(gpt.init_params_range(cfg, pb, pe, init_seed=5, gain_scale=0.1), full[pb:pe])
+        assert torch.equal(gpt.init_params_range(cfg, 7, 1000, init_seed=5, gain_scale=0.1), full[7:1000])
