@@ -150,6 +150,12 @@ typedef struct sd_comm_s* sd_comm;
 sd_status sd_nccl_unique_id(unsigned char out_id[128]);
 sd_status sd_comm_nccl_create(const unsigned char id[128], int nranks, int rank, sd_comm* out);
 sd_status sd_comm_destroy(sd_comm c);
+/* n in-process workers on one device (the reference's WorkerPool model): out[r]
+ * is worker r's communicator, driven by its own host thread and stream; the
+ * collectives synchronise the caller's stream, meet at a host barrier and
+ * exchange by device copies (rank-ordered sums); point-to-point sends complete
+ * when the receiver has copied them, groups batch them like NCCL groups. */
+sd_status sd_comm_local_create(int nranks, sd_comm* out);
 /* In-place sum all-reduce of n floats (data-sharded HVP, C1 of SURVEY §2.1). */
 sd_status sd_comm_allreduce_f32(sd_comm c, float* buf, uint64_t n, sd_stream s);
 /* All-gather of `bytes` per rank (ordered scalar partial exchange). */

@@ -560,3 +560,43 @@ def nccl_comm() -> Comm:
     h = C.c_void_p()
     check(lib().sd_comm_nccl_create(C.create_string_buffer(obj[0], 128), n, rank, C.byref(h)))
     return Comm(h, rank, n)
+
+
+def local_comms(n: int) -> list:
+    """n in-process workers on the current device (the reference's WorkerPool
+    model, pool.hpp:47-94): worker r's Comm, to be driven from its own thread
+    with its own CUDA stream (see run_workers)."""
+    arr = (C.c_void_p * n)()
+    check(lib().sd_comm_local_create(n, arr))
+    return [Comm(C.c_void_p(arr[r]), r, n) for r in range(n)]
+
+
+def run_workers(n: int, fn):
+    """Runs fn(rank, comm) on n worker threads of this process, each with its
+    own CUDA stream on the current device; returns the results in rank order
+    and re-raises the lowest-rank worker's exception (pool.cpp:54-64)."""
+    import threading
+    comms = local_comms(n)
+    dev = torch.cuda.current_device()
+    out, err = [None] * n, [None] * n
+
+    def body(r):
+        torch.cuda.set_device(dev)
+        try:
+            with torch.cuda.stream(torch.cuda.Stream()):
+                out[r] = fn(r, comms[r])
+                torch.cuda.current_stream().synchronize()
+        except BaseException as e:  # noqa: BLE001 -- surfaced below in rank order
+            err[r] = e
+    ts = [threading.Thread(target=body, args=(r,)) for r in range(n)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    for c in comms:
+        c.close()
+    for e in err:
+        if e is not None:
+            raise e
+    return out
+

@@ -25,7 +25,7 @@ void comm_reducescatter_f32(sd_comm c, const float* send, float* recv, uint64_t 
 void comm_send_f32(sd_comm c, const float* buf, uint64_t n, int peer, cudaStream_t s);
 void comm_recv_f32(sd_comm c, float* buf, uint64_t n, int peer, cudaStream_t s);
 void comm_group_begin(sd_comm c);
-void comm_group_end(sd_comm c);
+void comm_group_end(sd_comm c, cudaStream_t s);
 int comm_rank(sd_comm c);
 int comm_size(sd_comm c);
 void operator_apply(sd_operator op, const void* x, void* y, int prec, cudaStream_t s, uint64_t row_begin,

@@ -774,7 +774,7 @@ sd_status gpt_pipe_apply(void* ctx, const void* x, void* y, sd_stream sp) {
         case SD_PIPE_SEND_B: sd::comm_send_f32(c->comm, g->gx, n2, c->st - 1, s); break;
         case SD_PIPE_RECV_B: sd::comm_recv_f32(c->comm, g->gx, n2, c->st + 1, s); break;
         case SD_PIPE_GROUP_BEGIN: sd::comm_group_begin(c->comm); break;
-        case SD_PIPE_GROUP_END: sd::comm_group_end(c->comm); break;
+        case SD_PIPE_GROUP_END: sd::comm_group_end(c->comm, s); break;
         default: fail(SD_PROTOCOL_ERROR, "pipeline: unknown schedule op");
       }
     }

@@ -8,6 +8,9 @@
 
 #include <algorithm>
 #include <atomic>
+#include <condition_variable>
+#include <deque>
+#include <mutex>
 #include <cmath>
 #include <cstring>
 #include <memory>
@@ -196,10 +199,123 @@ static void nccl_check(ncclResult_t r, const char* what) {
 
 }  // namespace sd
 
+// In-process worker group (sd_comm_local_create): the reference's WorkerPool
+// model -- n workers of ONE process, each a host thread with its own stream on
+// the same device, exchanging through device copies between host barriers.
+// No kernel ever waits on another worker's kernel: every exchange first
+// synchronises the caller's stream, meets the other workers at a host
+// barrier, then copies/reduces published buffers in rank order.
+struct LocalMsg {
+  const float* p = nullptr;
+  uint64_t n = 0;
+  bool done = false;
+};
+struct LocalGroup {
+  int n = 1;
+  std::mutex m;
+  std::condition_variable cv;
+  int arrived = 0;
+  uint64_t gen = 0;
+  std::vector<const void*> slot;
+  // point-to-point: FIFO of posted sends per (src, dst); a send completes when
+  // the receiver has copied it (blocking semantics, like NCCL's)
+  std::vector<std::vector<std::deque<LocalMsg*>>> q;
+  void barrier() {
+    std::unique_lock<std::mutex> lk(m);
+    const uint64_t g = gen;
+    if (++arrived == n) {
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return gen != g; });
+    }
+  }
+};
+
+struct LocalP2p {
+  bool send;
+  const float* sp;
+  float* rp;
+  uint64_t n;
+  int peer;
+};
 struct sd_comm_s {
   int nranks = 1, rank = 0;
   ncclComm_t comm = nullptr;
+  std::shared_ptr<LocalGroup> local;
+  const float** d_ptrs = nullptr;  // local group: device copy of the published pointers
+  bool in_group = false;           // local group: deferred point-to-point ops of a group
+  std::vector<LocalP2p> pending;
 };
+
+namespace {
+// out[i] = sum over q (rank order) of src[q][off + i]
+__global__ void k_sum_ranks(const float* const* __restrict__ src, int nranks, uint64_t off, uint64_t n,
+                            float* __restrict__ out) {
+  const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  float acc = src[0][off + i];
+  for (int q = 1; q < nranks; ++q) acc += src[q][off + i];
+  out[i] = acc;
+}
+
+void local_publish(sd_comm c, const void* p, cudaStream_t s) {
+  SD_CUDA(cudaStreamSynchronize(s));
+  c->local->slot[c->rank] = p;
+  c->local->barrier();
+}
+
+// rank-ordered sum of the published f32 buffers (at element offset off) into out
+void local_sum(sd_comm c, uint64_t off, uint64_t n, float* out, cudaStream_t s) {
+  if (!c->d_ptrs) SD_CUDA(cudaMalloc(&c->d_ptrs, sizeof(float*) * c->nranks));
+  std::vector<const float*> h(c->nranks);
+  for (int q = 0; q < c->nranks; ++q) h[q] = static_cast<const float*>(c->local->slot[q]);
+  SD_CUDA(cudaMemcpyAsync(c->d_ptrs, h.data(), sizeof(float*) * c->nranks, cudaMemcpyHostToDevice, s));
+  if (n) k_sum_ranks<<<unsigned((n + 255) / 256), 256, 0, s>>>(c->d_ptrs, c->nranks, off, n, out);
+  SD_CUDA(cudaGetLastError());
+}
+// Point-to-point between in-process workers: all sends of a unit are posted
+// (after the stream has produced them), then every receive waits for its
+// matching send, copies it on the receiver's stream and acknowledges, then the
+// unit waits for its own sends to be acknowledged. A group is one unit (the
+// NCCL group semantics the 1F1B schedule relies on); a lone op is its own.
+void local_p2p(sd_comm c, std::vector<LocalP2p>& ops, cudaStream_t s) {
+  LocalGroup& g = *c->local;
+  SD_CUDA(cudaStreamSynchronize(s));
+  std::vector<LocalMsg> msgs(ops.size());
+  {
+    std::lock_guard<std::mutex> lk(g.m);
+    for (size_t i = 0; i < ops.size(); ++i)
+      if (ops[i].send) {
+        msgs[i].p = ops[i].sp, msgs[i].n = ops[i].n;
+        g.q[c->rank][ops[i].peer].push_back(&msgs[i]);
+      }
+  }
+  g.cv.notify_all();
+  for (auto& o : ops) {
+    if (o.send) continue;
+    LocalMsg* m = nullptr;
+    {
+      std::unique_lock<std::mutex> lk(g.m);
+      g.cv.wait(lk, [&] { return !g.q[o.peer][c->rank].empty(); });
+      m = g.q[o.peer][c->rank].front();
+      g.q[o.peer][c->rank].pop_front();
+    }
+    if (m->n != o.n) sd::fail(SD_PROTOCOL_ERROR, "point-to-point size mismatch");
+    SD_CUDA(cudaMemcpyAsync(o.rp, m->p, o.n * sizeof(float), cudaMemcpyDeviceToDevice, s));
+    SD_CUDA(cudaStreamSynchronize(s));
+    {
+      std::lock_guard<std::mutex> lk(g.m);
+      m->done = true;
+    }
+    g.cv.notify_all();
+  }
+  std::unique_lock<std::mutex> lk(g.m);
+  for (size_t i = 0; i < ops.size(); ++i)
+    if (ops[i].send) g.cv.wait(lk, [&] { return msgs[i].done; });
+}
+}  // namespace
 
 namespace sd {
 
@@ -210,11 +326,31 @@ void comm_allgather(sd_comm c, const void* send, void* recv, uint64_t bytes, cud
     if (recv != send) SD_CUDA(cudaMemcpyAsync(recv, send, bytes, cudaMemcpyDeviceToDevice, s));
     return;
   }
+  if (c->local) {
+    local_publish(c, send, s);
+    for (int q = 0; q < c->nranks; ++q)
+      SD_CUDA(cudaMemcpyAsync(static_cast<char*>(recv) + uint64_t(q) * bytes, c->local->slot[q], bytes,
+                              cudaMemcpyDeviceToDevice, s));
+    SD_CUDA(cudaStreamSynchronize(s));
+    c->local->barrier();  // every worker has read every slot
+    return;
+  }
   nccl_check(nccl().AllGather(send, recv, bytes, ncclUint8, c->comm, s), "ncclAllGather");
 }
 
 void comm_allreduce_f32(sd_comm c, float* buf, uint64_t n, cudaStream_t s) {
   if (!c) return;
+  if (c->local) {
+    float* tmp = nullptr;
+    SD_CUDA(cudaMallocAsync(&tmp, n * sizeof(float), s));
+    local_publish(c, buf, s);
+    local_sum(c, 0, n, tmp, s);
+    SD_CUDA(cudaStreamSynchronize(s));
+    c->local->barrier();  // all sums formed before any buffer is overwritten
+    SD_CUDA(cudaMemcpyAsync(buf, tmp, n * sizeof(float), cudaMemcpyDeviceToDevice, s));
+    SD_CUDA(cudaFreeAsync(tmp, s));
+    return;
+  }
   nccl_check(nccl().AllReduce(buf, buf, n, ncclFloat32, ncclSum, c->comm, s), "ncclAllReduce");
 }
 
@@ -222,6 +358,13 @@ void comm_allreduce_f32(sd_comm c, float* buf, uint64_t n, cudaStream_t s) {
 void comm_reducescatter_f32(sd_comm c, const float* send, float* recv, uint64_t n, cudaStream_t s) {
   if (!c) {
     if (recv != send) SD_CUDA(cudaMemcpyAsync(recv, send, n * sizeof(float), cudaMemcpyDeviceToDevice, s));
+    return;
+  }
+  if (c->local) {
+    local_publish(c, send, s);
+    local_sum(c, uint64_t(c->rank) * n, n, recv, s);
+    SD_CUDA(cudaStreamSynchronize(s));
+    c->local->barrier();
     return;
   }
   if (!nccl().ReduceScatter) fail(SD_NCCL_ERROR, "ncclReduceScatter unavailable");
@@ -232,17 +375,41 @@ void comm_reducescatter_f32(sd_comm c, const float* send, float* recv, uint64_t 
 // group_begin/group_end the sends and receives progress together (NCCL group
 // semantics), which is what makes the 1F1B exchanges deadlock-free.
 void comm_send_f32(sd_comm c, const float* buf, uint64_t n, int peer, cudaStream_t s) {
+  if (c && c->local) {
+    if (peer < 0 || peer >= c->nranks || peer == c->rank) fail(SD_ARGUMENT_ERROR, "bad peer");
+    c->pending.push_back({true, buf, nullptr, n, peer});
+    if (!c->in_group) {
+      local_p2p(c, c->pending, s);
+      c->pending.clear();
+    }
+    return;
+  }
   if (!c || !c->comm) fail(SD_STATE_ERROR, "point-to-point send without a communicator");
   nccl_check(nccl().Send(buf, n, ncclFloat32, peer, c->comm, s), "ncclSend");
 }
 void comm_recv_f32(sd_comm c, float* buf, uint64_t n, int peer, cudaStream_t s) {
+  if (c && c->local) {
+    if (peer < 0 || peer >= c->nranks || peer == c->rank) fail(SD_ARGUMENT_ERROR, "bad peer");
+    c->pending.push_back({false, nullptr, buf, n, peer});
+    if (!c->in_group) {
+      local_p2p(c, c->pending, s);
+      c->pending.clear();
+    }
+    return;
+  }
   if (!c || !c->comm) fail(SD_STATE_ERROR, "point-to-point receive without a communicator");
   nccl_check(nccl().Recv(buf, n, ncclFloat32, peer, c->comm, s), "ncclRecv");
 }
 void comm_group_begin(sd_comm c) {
+  if (c && c->local) c->in_group = true;
   if (c && c->comm) nccl_check(nccl().GroupStart(), "ncclGroupStart");
 }
-void comm_group_end(sd_comm c) {
+void comm_group_end(sd_comm c, cudaStream_t s) {
+  if (c && c->local) {
+    c->in_group = false;
+    local_p2p(c, c->pending, s);
+    c->pending.clear();
+  }
   if (c && c->comm) nccl_check(nccl().GroupEnd(), "ncclGroupEnd");
 }
 
@@ -502,7 +669,26 @@ sd_status sd_comm_nccl_create(const unsigned char id[128], int nranks, int rank,
 sd_status sd_comm_destroy(sd_comm c) {
   return guard([&] {
     if (c && c->comm) nccl_check(nccl().CommDestroy(c->comm), "ncclCommDestroy");
+    if (c && c->d_ptrs) cudaFree(c->d_ptrs);
     delete c;
+  });
+}
+
+// n in-process workers sharing one device (the reference's WorkerPool,
+// pool.hpp:47-94): out[r] is worker r's communicator, to be driven by its own
+// host thread with its own stream.
+sd_status sd_comm_local_create(int nranks, sd_comm* out) {
+  return guard([&] {
+    if (nranks < 1 || !out) fail(SD_ARGUMENT_ERROR, "bad worker count");
+    auto g = std::make_shared<LocalGroup>();
+    g->n = nranks;
+    g->slot.assign(nranks, nullptr);
+    g->q.assign(nranks, std::vector<std::deque<LocalMsg*>>(nranks));
+    for (int r = 0; r < nranks; ++r) {
+      auto c = std::make_unique<sd_comm_s>();
+      c->nranks = nranks, c->rank = r, c->local = g;
+      out[r] = c.release();
+    }
   });
 }
 
