@@ -123,6 +123,134 @@ __global__ void k_ln_fwd(const float* __restrict__ x, const float* __restrict__ 
   }
 }
 
+// Register-resident forms for d = 128 NV <= 1024 (GPT-2 d = 768: NV = 6): one
+// warp per row, lane l owns the float4 groups l, l + 32, ... of the row, which
+// it loads ONCE (16-byte coalesced) and keeps in registers through every pass;
+// same math as k_ln_fwd / k_ln_bwd.
+template <int NV>
+__global__ void __launch_bounds__(256) k_ln_fwd_reg(const float* __restrict__ x, const float* __restrict__ dx,
+    const float* __restrict__ g, const float* __restrict__ b, const float* __restrict__ vg,
+    const float* __restrict__ vb, int T, float eps, float* __restrict__ h, float* __restrict__ hs,
+    float* __restrict__ dh, float* __restrict__ dhs, float* __restrict__ xh, float* __restrict__ dxh,
+    float* __restrict__ r_out, float* __restrict__ dr_out, int rms) {
+  constexpr int d = 128 * NV;
+  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= T) return;
+  const long long o4 = (long long)row * (d / 4);
+  float4 xv[NV], dv[NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    xv[i] = reinterpret_cast<const float4*>(x)[o4 + lane + 32 * i];
+    dv[i] = reinterpret_cast<const float4*>(dx)[o4 + lane + 32 * i];
+  }
+  float mu = 0.f, dmu = 0.f;
+  if (!rms) {
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      s1 += (xv[i].x + xv[i].y) + (xv[i].z + xv[i].w);
+      s2 += (dv[i].x + dv[i].y) + (dv[i].z + dv[i].w);
+    }
+    mu = warp_sum(s1) / d, dmu = warp_sum(s2) / d;
+  }
+  float v = 0.f;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const float a0 = xv[i].x - mu, a1 = xv[i].y - mu, a2 = xv[i].z - mu, a3 = xv[i].w - mu;
+    v += (a0 * a0 + a1 * a1) + (a2 * a2 + a3 * a3);
+  }
+  const float r = rsqrtf(warp_sum(v) / d + eps);
+  float m2 = 0.f;
+#pragma unroll
+  for (int i = 0; i < NV; ++i)
+    m2 += ((xv[i].x - mu) * r * (dv[i].x - dmu) + (xv[i].y - mu) * r * (dv[i].y - dmu)) +
+          ((xv[i].z - mu) * r * (dv[i].z - dmu) + (xv[i].w - mu) * r * (dv[i].w - dmu));
+  const float mxd = warp_sum(m2) / d;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int c4 = lane + 32 * i;
+    const float4 gg = reinterpret_cast<const float4*>(g)[c4], vgg = reinterpret_cast<const float4*>(vg)[c4];
+    const float4 bb = b ? reinterpret_cast<const float4*>(b)[c4] : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 vbb = vb ? reinterpret_cast<const float4*>(vb)[c4] : make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 xo, dxo, ho, hso, dho, dhso;
+#define SD_LN_LANE(f)                                              \
+    {                                                              \
+      const float xhv = (xv[i].f - mu) * r;                        \
+      const float dxhv = r * (dv[i].f - dmu - xhv * mxd);          \
+      const float hv = gg.f * xhv + bb.f;                          \
+      const float dhv = vgg.f * xhv + gg.f * dxhv + vbb.f;         \
+      xo.f = xhv, dxo.f = dxhv, ho.f = hv, hso.f = tf32_res(hv);   \
+      dho.f = dhv, dhso.f = tf32_res(dhv);                         \
+    }
+    SD_LN_LANE(x) SD_LN_LANE(y) SD_LN_LANE(z) SD_LN_LANE(w)
+#undef SD_LN_LANE
+    reinterpret_cast<float4*>(xh)[o4 + c4] = xo;
+    reinterpret_cast<float4*>(dxh)[o4 + c4] = dxo;
+    reinterpret_cast<float4*>(h)[o4 + c4] = ho;
+    reinterpret_cast<float4*>(hs)[o4 + c4] = hso;
+    reinterpret_cast<float4*>(dh)[o4 + c4] = dho;
+    reinterpret_cast<float4*>(dhs)[o4 + c4] = dhso;
+  }
+  if (lane == 0) {
+    r_out[row] = r;
+    dr_out[row] = -r * mxd;
+  }
+}
+
+template <int NV>
+__global__ void __launch_bounds__(256) k_ln_bwd_reg(const float* __restrict__ gy, const float* __restrict__ gdy,
+    const float* __restrict__ g, const float* __restrict__ vg, const float* __restrict__ xh,
+    const float* __restrict__ dxh, const float* __restrict__ rr, const float* __restrict__ drr, int T,
+    float* __restrict__ gx, float* __restrict__ gdx, float* __restrict__ gxs, float* __restrict__ gdxs, int rms) {
+  constexpr int d = 128 * NV;
+  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= T) return;
+  const long long o4 = (long long)row * (d / 4);
+  float4 gq[NV], gdq[NV], xhv[NV], dxhv[NV];
+  float s1 = 0.f, s2 = 0.f, s3 = 0.f, s4 = 0.f, s5 = 0.f;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int c4 = lane + 32 * i;
+    const float4 a = reinterpret_cast<const float4*>(gy)[o4 + c4], ad = reinterpret_cast<const float4*>(gdy)[o4 + c4];
+    const float4 gg = reinterpret_cast<const float4*>(g)[c4], vgg = reinterpret_cast<const float4*>(vg)[c4];
+    xhv[i] = reinterpret_cast<const float4*>(xh)[o4 + c4];
+    dxhv[i] = reinterpret_cast<const float4*>(dxh)[o4 + c4];
+#define SD_LNB_LANE(f)                                  \
+    gq[i].f = a.f * gg.f;                               \
+    gdq[i].f = ad.f * gg.f + a.f * vgg.f;               \
+    s1 += gq[i].f, s2 += gq[i].f * xhv[i].f, s3 += gdq[i].f; \
+    s4 += gdq[i].f * xhv[i].f, s5 += gq[i].f * dxhv[i].f;
+    SD_LNB_LANE(x) SD_LNB_LANE(y) SD_LNB_LANE(z) SD_LNB_LANE(w)
+#undef SD_LNB_LANE
+  }
+  const float m_g = rms ? 0.f : warp_sum(s1) / d, m_gx = warp_sum(s2) / d, m_d = rms ? 0.f : warp_sum(s3) / d;
+  const float m_dx = warp_sum(s4) / d, m_gdx = warp_sum(s5) / d;
+  const float r = rr[row], dr = drr[row];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int c4 = lane + 32 * i;
+    float4 ox = reinterpret_cast<const float4*>(gx)[o4 + c4], od = reinterpret_cast<const float4*>(gdx)[o4 + c4];
+    float4 oxs, ods;
+#define SD_LNB_OUT(f)                                                                              \
+    {                                                                                              \
+      const float base = gq[i].f - m_g - xhv[i].f * m_gx;                                          \
+      ox.f = ox.f + r * base;                                                                      \
+      od.f = od.f + dr * r * base + r * (gdq[i].f - m_d - dxhv[i].f * m_gx - xhv[i].f * (m_dx + m_gdx)); \
+      oxs.f = tf32_res(ox.f), ods.f = tf32_res(od.f);                                              \
+    }
+    SD_LNB_OUT(x) SD_LNB_OUT(y) SD_LNB_OUT(z) SD_LNB_OUT(w)
+#undef SD_LNB_OUT
+    reinterpret_cast<float4*>(gx)[o4 + c4] = ox;
+    reinterpret_cast<float4*>(gdx)[o4 + c4] = od;
+    if (gxs) {
+      reinterpret_cast<float4*>(gxs)[o4 + c4] = oxs;
+      reinterpret_cast<float4*>(gdxs)[o4 + c4] = ods;
+    }
+  }
+}
+
 // Backward of LN with its tangent, accumulating into the residual adjoints:
 //   gq = gy*g;      gdq = gdy*g + gy*Vg
 //   gx += r (gq - mean(gq) - xh mean(gq xh))
@@ -607,16 +735,38 @@ void gpt_embed(const int* tok, int T, int S, int d, const float* wte, const floa
   SD_LAUNCHED("k_embed");
 }
 
+#define SD_LN_REG_CASES(X) X(2) X(4) X(6) X(8)
 void gpt_ln_fwd(const LnArgs& a, cudaStream_t s) {
+#define SD_LNF(NV)                                                                                                 \
+  if (a.d == 128 * NV) {                                                                                           \
+    k_ln_fwd_reg<NV><<<g1(a.T, 8), 256, 0, s>>>(a.x, a.dx, a.g, a.b, a.vg, a.vb, a.T, a.eps, a.h, a.hs, a.dh, a.dhs, \
+                                                a.xh, a.dxh, a.r, a.dr, a.rms);                                    \
+    SD_LAUNCHED("k_ln_fwd_reg");                                                                                   \
+    return;                                                                                                        \
+  }
+  SD_LN_REG_CASES(SD_LNF)
+#undef SD_LNF
   k_ln_fwd<<<g1(a.T, 8), 256, 0, s>>>(a.x, a.dx, a.g, a.b, a.vg, a.vb, a.T, a.d, a.eps, a.h, a.hs, a.dh, a.dhs, a.xh,
                                       a.dxh, a.r, a.dr, a.rms);
   SD_LAUNCHED("k_ln_fwd");
 }
 
 void gpt_ln_bwd(const LnBwdArgs& a, cudaStream_t s) {
-  k_ln_bwd<<<g1(a.T, 8), 256, 0, s>>>(a.gy, a.gdy, a.g, a.vg, a.xh, a.dxh, a.r, a.dr, a.T, a.d, a.gx, a.gdx, a.gxs,
-                                      a.gdxs, a.rms);
-  SD_LAUNCHED("k_ln_bwd");
+  bool done = false;
+#define SD_LNB(NV)                                                                                                 \
+  if (!done && a.d == 128 * NV) {                                                                                  \
+    k_ln_bwd_reg<NV><<<g1(a.T, 8), 256, 0, s>>>(a.gy, a.gdy, a.g, a.vg, a.xh, a.dxh, a.r, a.dr, a.T, a.gx, a.gdx,  \
+                                                a.gxs, a.gdxs, a.rms);                                             \
+    SD_LAUNCHED("k_ln_bwd_reg");                                                                                   \
+    done = true;                                                                                                   \
+  }
+  SD_LN_REG_CASES(SD_LNB)
+#undef SD_LNB
+  if (!done) {
+    k_ln_bwd<<<g1(a.T, 8), 256, 0, s>>>(a.gy, a.gdy, a.g, a.vg, a.xh, a.dxh, a.r, a.dr, a.T, a.d, a.gx, a.gdx, a.gxs,
+                                        a.gdxs, a.rms);
+    SD_LAUNCHED("k_ln_bwd");
+  }
   const int groups = std::min(kRowGroups, std::max(1, a.T / 64));
   k_colred1<1><<<dim3(unsigned((a.d + 31) / 32), unsigned(groups)), 256, 0, s>>>(a.gy, a.gdy, a.xh, a.dxh, a.T, a.d,
                                                                                  a.d, a.scratch);

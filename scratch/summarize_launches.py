@@ -20,9 +20,14 @@ for i, m in per.items():
     tot += m.get("gpu__time_duration.sum", 0.0)
 lines = [f"# Launch list summary ({src.split('/')[-1]})", "",
          f"{len(per)} launches, {tot / 1e3:.1f} ms summed kernel time (ncu-serialised, cold caches).", "",
-         "| kernel | launches | ms | share | DRAM GB |", "|---|---|---|---|---|"]
+         "DRAM GB/s = that kernel's DRAM bytes / its summed duration; % of the measured 6536.4 GB/s "
+         "copy peak (MEASURED_PEAKS.json). For the HBM-bound kernels (Lanczos recurrence and reorth, "
+         "elementwise R-op, softmax, CE) this is the roofline fraction; the GEMMs are tensor-bound.", "",
+         "| kernel | launches | ms | share | DRAM GB | DRAM GB/s | % HBM peak |", "|---|---|---|---|---|---|---|"]
 for k, (c, t, b) in sorted(agg.items(), key=lambda x: -x[1][1]):
-    lines.append(f"| `{k}` | {c} | {t / 1e3:.3f} | {100 * t / tot:.1f}% | {b / 1e9:.2f} |")
+    gbs = b / (t * 1e-6) / 1e9 if t else 0.0
+    lines.append(f"| `{k}` | {c} | {t / 1e3:.3f} | {100 * t / tot:.1f}% | {b / 1e9:.2f} | {gbs:.0f} | "
+                 f"{100 * gbs / 6536.4:.0f}% |")
 open(md_out, "w").write("\n".join(lines) + "\n")
 g = [(c, t, b) for k, (c, t, b) in agg.items() if "k_gemm" in k]
 n, t, b = sum(x[0] for x in g), sum(x[1] for x in g), sum(x[2] for x in g)
