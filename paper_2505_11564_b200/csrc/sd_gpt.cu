@@ -239,7 +239,7 @@ struct sd_gpt_s {
       gdqkvs = p.take<float>(T_ * W);
     theta_s = c.bf16_weights ? nullptr : p.take<float>(Pst);  // bf16 weights: exact in tf32, no residual
     v_s = probe_res ? p.take<float>(Pst) : nullptr;
-    red = p.take<float>(2LL * 64 * std::max(3 * d, ff));
+    red = p.take<float>(sd::kColredReserve + 2LL * 64 * std::max(3 * d, ff));
     if (first) {
       tok = p.take<int>(T_ * nmb), uniq = p.take<int>((T_ + 1) * nmb), ustart = p.take<int>((T_ + 1) * nmb);
       upos = p.take<int>(T_ * nmb);
@@ -895,6 +895,7 @@ sd_status sd_gpt_stage_create(const sd_gpt_config* c, int micro_batch, int seq, 
     } else {
       sd::gpt_residual(theta_stage, g->theta_s, g->Pst, (cudaStream_t)s);
     }
+    SD_CUDA(cudaMemsetAsync(g->red, 0, sd::kColredReserve * sizeof(float), (cudaStream_t)s));  // colred counters
     if (g->last) {  // padded logits columns are never read as values but feed TMA boxes: zero them once
       for (float* z : {g->z, g->zs, g->dz, g->dzs})
         SD_CUDA(cudaMemsetAsync(z, 0, size_t(g->T) * g->Vp * 4, (cudaStream_t)s));

@@ -17,7 +17,7 @@ struct LnBwdArgs {
   int T, d;
   float *gx, *gdx, *gxs, *gdxs;
   float *hv_g, *hv_b;
-  float* scratch;  // >= 2 * 64 * d floats
+  float* scratch;  // >= kColredReserve + 2 * 64 * d floats, the first kColredReserve zeroed once
   int rms = 0;
   int acc = 0;  // hv_g/hv_b += (micro-batch accumulation) instead of =
 };
@@ -43,6 +43,9 @@ void llama_swiglu_bwd(const float* fu, const float* dfu, const float* ga, const 
                       float* gdfu, float* gdfus, int T, int ff, cudaStream_t s);
 void gpt_ln_fwd(const LnArgs& a, cudaStream_t s);
 void gpt_ln_bwd(const LnBwdArgs& a, cudaStream_t s);
+// column-reduction scratch: kColredReserve floats of arrival counters (zeroed
+// once at creation; each reduction leaves them zero) + 2 * 64 * n partials
+constexpr int kColredReserve = 4096;
 void gpt_colsum(const float* a, int T, int n, long long lda, float* out, float* scratch, cudaStream_t s,
                 int acc = 0);
 void gpt_gelu_fwd(const float* f, const float* df, float* u, float* us, float* du, float* dus, long long n,

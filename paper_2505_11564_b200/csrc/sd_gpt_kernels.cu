@@ -303,8 +303,10 @@ constexpr int kRowGroups = 64;
 // mode 0: sum a ; mode 1: sum (gdy*xh + gy*dxh) and sum gdy (two outputs)
 template <int MODE>
 __global__ void k_colred1(const float* __restrict__ a, const float* __restrict__ b, const float* __restrict__ c,
-                          const float* __restrict__ e, int T, int n, long long lda, float* __restrict__ part) {
+                          const float* __restrict__ e, int T, int n, long long lda, float* __restrict__ part,
+                          unsigned* __restrict__ cnt, float* __restrict__ out0, float* __restrict__ out1, int acc) {
   __shared__ float s0[8][33], s1[8][33];
+  __shared__ bool last;
   const int col = blockIdx.x * 32 + (threadIdx.x & 31);
   const int rl = threadIdx.x >> 5;
   const int rows = (T + gridDim.y - 1) / gridDim.y;
@@ -332,19 +334,26 @@ __global__ void k_colred1(const float* __restrict__ a, const float* __restrict__
     part[(long long)blockIdx.y * n + col] = t0;
     if (MODE == 1) part[(long long)(gridDim.y + blockIdx.y) * n + col] = t1;
   }
-}
-
-__global__ void k_colred2(const float* __restrict__ part, int groups, int n, float* __restrict__ out0,
-                          float* __restrict__ out1, int acc) {
-  const int col = blockIdx.x * blockDim.x + threadIdx.x;
-  if (col >= n) return;
-  float t0 = 0.f, t1 = 0.f;
-  for (int g = 0; g < groups; ++g) t0 += part[(long long)g * n + col];
-  out0[col] = acc ? out0[col] + t0 : t0;  // acc: micro-batch accumulation (pipeline stages)
-  if (out1) {
-    for (int g = 0; g < groups; ++g) t1 += part[(long long)(groups + g) * n + col];
-    out1[col] = acc ? out1[col] + t1 : t1;
+  // stage 2 in the last-arriving row-group block of this column slab: the
+  // row-group partials summed in ascending order (deterministic), then the
+  // slab's arrival counter is reset for the next reduction
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(&cnt[blockIdx.x], 1u) == gridDim.y - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (rl == 0 && col < n) {
+    const int groups = gridDim.y;
+    float t0 = 0.f, t1 = 0.f;
+    for (int g = 0; g < groups; ++g) t0 += __ldcg(&part[(long long)g * n + col]);
+    out0[col] = acc ? out0[col] + t0 : t0;  // acc: micro-batch accumulation (pipeline stages)
+    if (MODE == 1 && out1) {
+      for (int g = 0; g < groups; ++g) t1 += __ldcg(&part[(long long)(groups + g) * n + col]);
+      out1[col] = acc ? out1[col] + t1 : t1;
+    }
   }
+  if (threadIdx.x == 0) cnt[blockIdx.x] = 0u;
 }
 
 // ------------------------------------------------------------------ GELU
@@ -768,20 +777,18 @@ void gpt_ln_bwd(const LnBwdArgs& a, cudaStream_t s) {
     SD_LAUNCHED("k_ln_bwd");
   }
   const int groups = std::min(kRowGroups, std::max(1, a.T / 64));
-  k_colred1<1><<<dim3(unsigned((a.d + 31) / 32), unsigned(groups)), 256, 0, s>>>(a.gy, a.gdy, a.xh, a.dxh, a.T, a.d,
-                                                                                 a.d, a.scratch);
+  k_colred1<1><<<dim3(unsigned((a.d + 31) / 32), unsigned(groups)), 256, 0, s>>>(
+      a.gy, a.gdy, a.xh, a.dxh, a.T, a.d, a.d, a.scratch + kColredReserve, reinterpret_cast<unsigned*>(a.scratch),
+      a.hv_g, a.hv_b, a.acc);
   SD_LAUNCHED("k_colred1");
-  k_colred2<<<unsigned((a.d + 255) / 256), 256, 0, s>>>(a.scratch, groups, a.d, a.hv_g, a.hv_b, a.acc);
-  SD_LAUNCHED("k_colred2");
 }
 
 void gpt_colsum(const float* a, int T, int n, long long lda, float* out, float* scratch, cudaStream_t s, int acc) {
   const int groups = std::min(kRowGroups, std::max(1, T / 64));
-  k_colred1<0><<<dim3(unsigned((n + 31) / 32), unsigned(groups)), 256, 0, s>>>(a, nullptr, nullptr, nullptr, T, n, lda,
-                                                                              scratch);
+  k_colred1<0><<<dim3(unsigned((n + 31) / 32), unsigned(groups)), 256, 0, s>>>(
+      a, nullptr, nullptr, nullptr, T, n, lda, scratch + kColredReserve, reinterpret_cast<unsigned*>(scratch), out,
+      nullptr, acc);
   SD_LAUNCHED("k_colred1");
-  k_colred2<<<unsigned((n + 255) / 256), 256, 0, s>>>(scratch, groups, n, out, nullptr, acc);
-  SD_LAUNCHED("k_colred2");
 }
 
 void gpt_gelu_fwd(const float* f, const float* df, float* u, float* us, float* du, float* dus, long long n,

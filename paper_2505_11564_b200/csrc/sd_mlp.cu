@@ -276,7 +276,8 @@ sd_status sd_mlp_create(const uint64_t* widths, int n_widths, int n_max, const f
     m->y = m->alloc((long long)n_max * m->wp[Ln]);
     m->g = m->alloc(nm), m->gs = m->alloc(nm), m->gd = m->alloc(nm), m->gds = m->alloc(nm);
     m->ga = m->alloc(nm), m->gda = m->alloc(nm);
-    m->red = m->alloc(2LL * 64 * wmax);
+    m->red = m->alloc(sd::kColredReserve + 2LL * 64 * wmax);
+    SD_CUDA(cudaMemset(m->red, 0, sd::kColredReserve * sizeof(float)));  // column-reduction arrival counters
     void* lp = nullptr;
     SD_CUDA(cudaMalloc(&lp, size_t((nm + 255) / 256 + 1) * sizeof(double)));
     m->owned.push_back(lp);
