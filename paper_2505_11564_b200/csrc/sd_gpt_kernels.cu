@@ -343,14 +343,24 @@ __global__ void k_colred1(const float* __restrict__ a, const float* __restrict__
   __syncthreads();
   if (!last) return;
   __threadfence();
-  if (rl == 0 && col < n) {
+  // all eight warps take part: warp w loads the partials of groups w, w + 8, ...
+  // (independent loads in flight), then lane-column sums run in group order
+  {
     const int groups = gridDim.y;
-    float t0 = 0.f, t1 = 0.f;
-    for (int g = 0; g < groups; ++g) t0 += __ldcg(&part[(long long)g * n + col]);
-    out0[col] = acc ? out0[col] + t0 : t0;  // acc: micro-batch accumulation (pipeline stages)
-    if (MODE == 1 && out1) {
-      for (int g = 0; g < groups; ++g) t1 += __ldcg(&part[(long long)(groups + g) * n + col]);
-      out1[col] = acc ? out1[col] + t1 : t1;
+    __shared__ float pg[2][kRowGroups][33];
+    for (int g = rl; g < groups; g += 8) {
+      pg[0][g][threadIdx.x & 31] = col < n ? __ldcg(&part[(long long)g * n + col]) : 0.f;
+      if (MODE == 1) pg[1][g][threadIdx.x & 31] = col < n ? __ldcg(&part[(long long)(groups + g) * n + col]) : 0.f;
+    }
+    __syncthreads();
+    if (rl == 0 && col < n) {
+      float t0 = 0.f, t1 = 0.f;
+      for (int g = 0; g < groups; ++g) t0 += pg[0][g][threadIdx.x];
+      out0[col] = acc ? out0[col] + t0 : t0;  // acc: micro-batch accumulation (pipeline stages)
+      if (MODE == 1 && out1) {
+        for (int g = 0; g < groups; ++g) t1 += pg[1][g][threadIdx.x];
+        out1[col] = acc ? out1[col] + t1 : t1;
+      }
     }
   }
   if (threadIdx.x == 0) cnt[blockIdx.x] = 0u;
@@ -702,6 +712,12 @@ __global__ void k_res(const float* __restrict__ x, float* __restrict__ xs, long 
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i < n) xs[i] = tf32_res(x[i]);
 }
+__global__ void k_res4(const float4* __restrict__ x, float4* __restrict__ xs, long long n4) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n4) return;
+  const float4 v = __ldg(x + i);
+  xs[i] = make_float4(tf32_res(v.x), tf32_res(v.y), tf32_res(v.z), tf32_res(v.w));
+}
 
 __global__ void k_fill(float* __restrict__ x, float v, long long n) {
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -870,8 +886,17 @@ void llama_swiglu_bwd(const float* fu, const float* dfu, const float* ga, const 
 
 void gpt_residual(const float* x, float* xs, long long n, cudaStream_t s) {
   if (n <= 0) return;
-  k_res<<<g1(n), 256, 0, s>>>(x, xs, n);
-  SD_LAUNCHED("k_res");
+  long long done = 0;
+  if ((reinterpret_cast<uintptr_t>(x) & 15) == 0 && (reinterpret_cast<uintptr_t>(xs) & 15) == 0 && n >= 4) {
+    const long long n4 = n / 4;
+    k_res4<<<g1(n4), 256, 0, s>>>(reinterpret_cast<const float4*>(x), reinterpret_cast<float4*>(xs), n4);
+    SD_LAUNCHED("k_res4");
+    done = n4 * 4;
+  }
+  if (done < n) {
+    k_res<<<g1(n - done), 256, 0, s>>>(x + done, xs + done, n - done);
+    SD_LAUNCHED("k_res");
+  }
 }
 
 void gpt_fill(float* x, float v, long long n, cudaStream_t s) {

@@ -70,7 +70,7 @@ union VU {
   typename V16<T>::type v;
   T a[V16<T>::W];
 };
-__device__ __forceinline__ bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+__host__ __device__ __forceinline__ bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 // One THREAD per full grid block: it streams its 1024 elements with 16 B
 // loads (several in flight, unroll 4), applies the update element by element
@@ -365,6 +365,37 @@ __global__ void k_axpy(const T* __restrict__ x, T* __restrict__ y, uint64_t n, c
   y[i] = round_to<T>(__dadd_rn(double(y[i]), __dmul_rn(alpha, double(x[i]))));
 }
 
+// 16-byte vector forms of axpy / scale (one V16 group per thread; the
+// reciprocal of scale is computed once per thread, not per element)
+template <typename T>
+__global__ void k_axpy_v(const T* __restrict__ x, T* __restrict__ y, uint64_t nv, const double* alphap, double sign) {
+  using V = typename V16<T>::type;
+  constexpr int W = V16<T>::W;
+  const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (i >= nv) return;
+  const double alpha = sign * (*alphap);
+  VU<T> yv, xv;
+  yv.v = reinterpret_cast<const V*>(y)[i];
+  xv.v = __ldg(reinterpret_cast<const V*>(x) + i);
+#pragma unroll
+  for (int k = 0; k < W; ++k) yv.a[k] = round_to<T>(__dadd_rn(double(yv.a[k]), __dmul_rn(alpha, double(xv.a[k]))));
+  reinterpret_cast<V*>(y)[i] = yv.v;
+}
+
+template <typename T>
+__global__ void k_scale_v(const T* __restrict__ x, T* __restrict__ out, uint64_t nv, const double* cp, int recip) {
+  using V = typename V16<T>::type;
+  constexpr int W = V16<T>::W;
+  const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (i >= nv) return;
+  const double c = recip ? __ddiv_rn(1.0, *cp) : *cp;
+  VU<T> xv;
+  xv.v = __ldg(reinterpret_cast<const V*>(x) + i);
+#pragma unroll
+  for (int k = 0; k < W; ++k) xv.a[k] = round_to<T>(__dmul_rn(c, double(xv.a[k])));
+  reinterpret_cast<V*>(out)[i] = xv.v;
+}
+
 template <typename T>
 __global__ void k_scale(const T* __restrict__ x, T* __restrict__ out, uint64_t n, const double* cp, int recip) {
   const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
@@ -372,6 +403,41 @@ __global__ void k_scale(const T* __restrict__ x, T* __restrict__ out, uint64_t n
   const double c = recip ? __ddiv_rn(1.0, *cp) : *cp;
   out[i] = round_to<T>(__dmul_rn(c, double(x[i])));
 }
+
+static unsigned grid_for(uint64_t n, unsigned threads) { return unsigned((n + threads - 1) / threads); }
+
+template <typename T>
+static void scale_t(const T* x, T* out, uint64_t n, const double* c, int recip, cudaStream_t s) {
+  constexpr int W = V16<T>::W;
+  uint64_t done = 0;
+  if (al16(x) && al16(out) && n >= W) {
+    const uint64_t nv = n / W;
+    k_scale_v<T><<<grid_for(nv, 256), 256, 0, s>>>(x, out, nv, c, recip);
+    SD_LAUNCHED("k_scale_v");
+    done = nv * W;
+  }
+  if (done < n) {
+    k_scale<T><<<grid_for(n - done, 256), 256, 0, s>>>(x + done, out + done, n - done, c, recip);
+    SD_LAUNCHED("k_scale");
+  }
+}
+
+template <typename T>
+static void axpy_t(const T* x, T* y, uint64_t n, const double* alpha, double sign, cudaStream_t s) {
+  constexpr int W = V16<T>::W;
+  uint64_t done = 0;
+  if (al16(x) && al16(y) && n >= W) {
+    const uint64_t nv = n / W;
+    k_axpy_v<T><<<grid_for(nv, 256), 256, 0, s>>>(x, y, nv, alpha, sign);
+    SD_LAUNCHED("k_axpy_v");
+    done = nv * W;
+  }
+  if (done < n) {
+    k_axpy<T><<<grid_for(n - done, 256), 256, 0, s>>>(x + done, y + done, n - done, alpha, sign);
+    SD_LAUNCHED("k_axpy");
+  }
+}
+
 
 // dense_operator apply, operators.cpp:39-44: serial f64 fold over the full row.
 template <typename T>
@@ -396,7 +462,6 @@ __global__ void k_diag_apply(const T* __restrict__ d, const T* __restrict__ x, T
 }
 
 // ------------------------------------------------------------ launchers
-static unsigned grid_for(uint64_t n, unsigned threads) { return unsigned((n + threads - 1) / threads); }
 
 template <typename T>
 static void launch_axpy_dot(const void* x, void* y, const void* z, const double* coef, uint64_t begin, uint64_t end,
@@ -430,8 +495,7 @@ static void launch_axpy_dot(const void* x, void* y, const void* z, const double*
     if (dot == 0) {
       // update only: element-parallel (no block folds to keep in order)
       if (local_end) {
-        k_axpy<T><<<grid_for(local_end, 256), 256, 0, s>>>((const T*)x, (T*)y, local_end, coef, -1.0);
-        SD_LAUNCHED("k_axpy");
+        axpy_t<T>((const T*)x, (T*)y, local_end, coef, -1.0, s);
       }
     } else if (dot == 1) run(TT{}, D1{});
     else run(TT{}, D2{});
@@ -697,16 +761,14 @@ void probe_fill(void* x, uint64_t begin, uint64_t end, uint64_t seed, int dist, 
 
 void scale(const void* x, void* out, uint64_t n, const double* c, int recip, int prec, cudaStream_t s) {
   if (n == 0) return;
-  if (prec == SD_F32) k_scale<float><<<grid_for(n, 256), 256, 0, s>>>((const float*)x, (float*)out, n, c, recip);
-  else k_scale<double><<<grid_for(n, 256), 256, 0, s>>>((const double*)x, (double*)out, n, c, recip);
-  SD_LAUNCHED("k_scale");
+  if (prec == SD_F32) scale_t((const float*)x, (float*)out, n, c, recip, s);
+  else scale_t((const double*)x, (double*)out, n, c, recip, s);
 }
 
 void axpy(const void* x, void* y, uint64_t n, const double* alpha, double sign, int prec, cudaStream_t s) {
   if (n == 0) return;
-  if (prec == SD_F32) k_axpy<float><<<grid_for(n, 256), 256, 0, s>>>((const float*)x, (float*)y, n, alpha, sign);
-  else k_axpy<double><<<grid_for(n, 256), 256, 0, s>>>((const double*)x, (double*)y, n, alpha, sign);
-  SD_LAUNCHED("k_axpy");
+  if (prec == SD_F32) axpy_t((const float*)x, (float*)y, n, alpha, sign, s);
+  else axpy_t((const double*)x, (double*)y, n, alpha, sign, s);
 }
 
 void dense_apply(const double* a, uint64_t n, const void* xf, void* y, uint64_t rb, uint64_t re, int prec,
