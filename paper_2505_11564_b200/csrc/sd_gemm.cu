@@ -85,6 +85,14 @@ bool sd_gemm_tma_store_enabled() {
   }();
   return on;
 }
+bool sd_gemm_tmem_a_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("SD_GEMM_TMEM_A");
+    return !(e && e[0] == '0');  // SD_GEMM_TMEM_A=0: A from shared memory (bit-identical results)
+  }();
+  return on;
+}
+
 bool tma_store_ok(const GemmArgs& g, int splits, int bias_cols) {
   return sd_gemm_tma_store_enabled() && splits == 1 && g.beta == 0.0f &&
          (reinterpret_cast<uintptr_t>(g.C) & 15) == 0 && (g.ldc % 4) == 0 &&
@@ -308,8 +316,16 @@ void launch_splitk_reduce(const float* ws, int splits, int zc, const GemmArgs& g
 namespace {
 using namespace gk;
 
-template <bool A_MN, bool B_MN, bool THREE, int BN_, bool CAUSAL>
-__global__ void __launch_bounds__(NUM_THREADS, 1)
+// TA: the A operand (K-major, 64-wide attention products with on-chip
+// residuals) goes to tensor memory instead of being re-read from shared memory
+// by every MMA: four residual warps (one per TMEM lane quarter) read each
+// landed A row once, write its tf32 high part and residual into a per-stage
+// TMEM slot (tcgen05.st), and the MMAs take A from there.
+template <bool TA>
+constexpr int kThreadsFor() { return TA ? 32 * (2 + 4 + 8) : NUM_THREADS; }
+
+template <bool A_MN, bool B_MN, bool THREE, int BN_, bool CAUSAL, bool TA = false>
+__global__ void __launch_bounds__(kThreadsFor<TA>(), 1)
     k_gemm_tf32(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mAs,
                 const __grid_constant__ CUtensorMap mB, const __grid_constant__ CUtensorMap mBs,
                 const __grid_constant__ CUtensorMap mA2, const __grid_constant__ CUtensorMap mAs2,
@@ -319,7 +335,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   using Cf = Cfg<BN_>;
   constexpr int BN = Cf::BN, STAGES = Cf::STAGES, EC = Cf::EC;
   constexpr int A_BYTES = Cf::A_BYTES, B_BYTES = Cf::B_BYTES;
-  constexpr uint32_t TMEM_COLS = Cf::TMEM_COLS;
+  static_assert(!TA || (!A_MN && THREE && BN_ == 64), "TMEM-A: K-major A, 3xTF32, 64-wide tiles");
+  constexpr int CONV = TA ? 4 : kConvWarps;
+  constexpr uint32_t TA_COL0 = 2 * BN_;                       // A slots after the two accumulators
+  constexpr uint32_t TMEM_COLS = TA ? 512 : Cf::TMEM_COLS;   // TA: 128 + STAGES x (16 hi + 16 lo)
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // 1024-byte aligned ring: per stage [A | As | B | Bs]
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -339,7 +358,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
-      mbar_init(&conv[s], 1);
+      mbar_init(&conv[s], TA ? 4 : 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
@@ -411,7 +430,45 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
       }
     }
-  } else if (warp >= 2 && warp < 2 + kConvWarps) {
+  } else if (TA && warp >= 2 && warp < 2 + CONV) {
+    // TMEM-A residual warps: warp w owns TMEM lanes / A rows 32 (w % 4) .. +31
+    // and a quarter of the B tile; every stage goes through all four
+    const int q = warp & 3, m = 32 * q + lane;
+    uint32_t g = 0;
+    for (int t = blockIdx.x; t < ep.n_tiles; t += gridDim.x) {
+      const TileInfo ti = tile_info<BN, CAUSAL>(ep, t, K);
+      if (ti.skip) continue;
+      for (int kk = 0; kk < ep.nsrc * ti.num_kb; ++kk, ++g) {
+        const int s = g % STAGES;
+        mbar_wait(&full[s], (g / STAGES) & 1);
+        unsigned char* st = smem + s * STAGE_BYTES;
+        // row m of the K-major A tile: 64 B, SWIZZLE_64B (16 B chunk c at c ^ ((m >> 1) & 3))
+        const float4* row = reinterpret_cast<const float4*>(st + m * 64);
+        uint32_t hi[16], lo[16];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const float4 v = row[c ^ ((m >> 1) & 3)];
+          const float e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const uint32_t h = __float_as_uint(e[u]) & 0xFFFFE000u;
+            hi[4 * c + u] = h;
+            lo[4 * c + u] = __float_as_uint(e[u] - __uint_as_float(h));
+          }
+        }
+        const uint32_t ta = tmem + (uint32_t(32 * q) << 16) + TA_COL0 + uint32_t(s) * 32u;
+        tmem_st16(ta, hi);
+        tmem_st16(ta + 16, lo);
+        stage_residual(st + 2 * A_BYTES + q * (B_BYTES / 4), st + 2 * A_BYTES + B_BYTES + q * (B_BYTES / 4),
+                       B_BYTES / 4, lane, 32);
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        fence_proxy_async_smem();
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&conv[s]);
+      }
+    }
+  } else if (!TA && warp >= 2 && warp < 2 + kConvWarps) {
     // residual warps: once a stage lands, write x - trunc_tf32(x) of the raw
     // A and B tiles into their residual slots (3xTF32 without residual arrays
     // in memory: half the operand bytes through L2 and TMA), then release it
@@ -459,7 +516,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
           for (int ks = 0; ks < BK / 8; ++ks) {
             const uint32_t acc0 = (first && ks == 0) ? 0u : 1u;
-            if (THREE) {
+            if (TA) {
+              const uint32_t ta = tmem + TA_COL0 + uint32_t(s) * 32u + uint32_t(ks) * 8u;
+              mma_tf32_ta(d, ta + 16, tile_desc<B_MN>(b, ks), idesc, acc0);  // A_lo . B
+              mma_tf32_ta(d, ta, tile_desc<B_MN>(bs, ks), idesc, 1u);        // A_hi . B_lo
+              mma_tf32_ta(d, ta, tile_desc<B_MN>(b, ks), idesc, 1u);         // A_hi . B
+            } else if (THREE) {
               mma_tf32(d, tile_desc<A_MN>(as, ks), tile_desc<B_MN>(b, ks), idesc, acc0);
               if (!bex) mma_tf32(d, tile_desc<A_MN>(a, ks), tile_desc<B_MN>(bs, ks), idesc, 1u);
               mma_tf32(d, tile_desc<A_MN>(a, ks), tile_desc<B_MN>(b, ks), idesc, 1u);
@@ -479,7 +541,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // sub-partition) and the column half (w-4)/4 of the tile: thread = one
     // output row, EC = BN/2 fp32 accumulators in registers.
     const int sub = warp & 3;
-    const int cb = ((warp - 2 - kConvWarps) >> 2) * EC;
+    const int cb = ((warp - 2 - CONV) >> 2) * EC;
     uint32_t chunk = 0;
     for (int t = blockIdx.x; t < ep.n_tiles; t += gridDim.x) {
       const TileInfo ti = tile_info<BN, CAUSAL>(ep, t, K);
@@ -506,7 +568,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (lane == 0) mbar_arrive(&tempty[buf]);
       }
       if (ep.tma_store) {
-        const int ew = warp - 2 - kConvWarps;  // 0..7: its staging box
+        const int ew = warp - 2 - CONV;  // 0..7: its staging box
         warp_tma_store<EC>(&mC, ep.Cs ? &mCs : nullptr, epi_stage + ew * 1024, acc, ep.alpha,
                            ep.bias, lane, ti.m0 + sub * 32, ti.n0 + cb, ti.z % ep.Z1, ti.z / ep.Z1);
         if (lane == 0) bulk_wait_read0();  // staging box free for the next tile
@@ -583,6 +645,7 @@ void launch(const GemmArgs& g, cudaStream_t s) {
   ep.mn5 = mn5;
   ep.bexact = (g.b_exact ? 1 : 0) | (g.b2_exact ? 2 : 0);
   auto kern = g.causal ? k_gemm_tf32<A_MN, B_MN, THREE, BN, true> : k_gemm_tf32<A_MN, B_MN, THREE, BN, false>;
+  int threads = NUM_THREADS;
   static bool attr_set = false;
   if (!attr_set) {
     SD_CUDA(cudaFuncSetAttribute(k_gemm_tf32<A_MN, B_MN, THREE, BN, true>,
@@ -591,14 +654,29 @@ void launch(const GemmArgs& g, cudaStream_t s) {
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     attr_set = true;
   }
+  if constexpr (!A_MN && THREE && BN == 64) {
+    // on-chip residuals of a K-major A: A through tensor memory (SD_GEMM_TMEM_A=0 disables)
+    if (g.onchip && sd_gemm_tmem_a_enabled()) {
+      kern = g.causal ? k_gemm_tf32<A_MN, B_MN, THREE, BN, true, true> : k_gemm_tf32<A_MN, B_MN, THREE, BN, false, true>;
+      threads = kThreadsFor<true>();
+      static bool attr_ta = false;
+      if (!attr_ta) {
+        SD_CUDA(cudaFuncSetAttribute(k_gemm_tf32<A_MN, B_MN, THREE, BN, true, true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        SD_CUDA(cudaFuncSetAttribute(k_gemm_tf32<A_MN, B_MN, THREE, BN, false, true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        attr_ta = true;
+      }
+    }
+  }
   const int grid = std::min(ep.n_tiles, kNumSMs);
   if (prof().on)
     prof().next_tag = std::to_string(g.M) + "," + std::to_string(g.N) + "," + std::to_string(g.K) + "," +
                       std::to_string(zc) + "," + std::to_string(int(A_MN)) + "," + std::to_string(int(B_MN)) + "," +
                       std::to_string(g.causal) + "," + std::to_string(splits) + (dual ? ",2" : ",1");
   prof_begin(s);
-  kern<<<grid, NUM_THREADS, smem, s>>>(maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], maps[6], maps[7], mC,
-                                       mCs, g.K, ep);
+  kern<<<grid, threads, smem, s>>>(maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], maps[6], maps[7], mC,
+                                   mCs, g.K, ep);
   SD_LAUNCHED("k_gemm_tf32");
   if (splits > 1) {
     launch_splitk_reduce(ws, splits, zc, g, s);
