@@ -335,7 +335,7 @@ __global__ void __launch_bounds__(kThreadsFor<TA>(), 1)
   using Cf = Cfg<BN_>;
   constexpr int BN = Cf::BN, STAGES = Cf::STAGES, EC = Cf::EC;
   constexpr int A_BYTES = Cf::A_BYTES, B_BYTES = Cf::B_BYTES;
-  static_assert(!TA || (!A_MN && THREE && BN_ == 64), "TMEM-A: K-major A, 3xTF32, 64-wide tiles");
+  static_assert(!TA || (THREE && BN_ == 64), "TMEM-A: 3xTF32, 64-wide tiles");
   constexpr int CONV = TA ? 4 : kConvWarps;
   constexpr uint32_t TA_COL0 = 2 * BN_;                       // A slots after the two accumulators
   constexpr uint32_t TMEM_COLS = TA ? 512 : Cf::TMEM_COLS;   // TA: 128 + STAGES x (16 hi + 16 lo)
@@ -442,18 +442,31 @@ __global__ void __launch_bounds__(kThreadsFor<TA>(), 1)
         const int s = g % STAGES;
         mbar_wait(&full[s], (g / STAGES) & 1);
         unsigned char* st = smem + s * STAGE_BYTES;
-        // row m of the K-major A tile: 64 B, SWIZZLE_64B (16 B chunk c at c ^ ((m >> 1) & 3))
-        const float4* row = reinterpret_cast<const float4*>(st + m * 64);
         uint32_t hi[16], lo[16];
+        if (!A_MN) {
+          // row m of the K-major A tile: 64 B, SWIZZLE_64B (16 B chunk c at c ^ ((m >> 1) & 3))
+          const float4* row = reinterpret_cast<const float4*>(st + m * 64);
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const float4 v = row[c ^ ((m >> 1) & 3)];
-          const float e[4] = {v.x, v.y, v.z, v.w};
+          for (int c = 0; c < 4; ++c) {
+            const float4 v = row[c ^ ((m >> 1) & 3)];
+            const float e[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const uint32_t h = __float_as_uint(e[u]) & 0xFFFFE000u;
-            hi[4 * c + u] = h;
-            lo[4 * c + u] = __float_as_uint(e[u] - __uint_as_float(h));
+            for (int u = 0; u < 4; ++u) {
+              const uint32_t h = __float_as_uint(e[u]) & 0xFFFFE000u;
+              hi[4 * c + u] = h;
+              lo[4 * c + u] = __float_as_uint(e[u] - __uint_as_float(h));
+            }
+          }
+        } else {
+          // MN-major A tile: 32-row chunk q (= this warp) at q * 2048, k-row k of
+          // 128 B, 32 B granule (m % 32) / 8 swizzled with k & 3 (SWIZZLE_128B_ATOM_32B)
+          const unsigned char* ch = st + q * 2048 + (lane & 7) * 4;
+#pragma unroll
+          for (int k = 0; k < 16; ++k) {
+            const float x = *reinterpret_cast<const float*>(ch + k * 128 + (((lane >> 3) ^ (k & 3)) << 5));
+            const uint32_t h = __float_as_uint(x) & 0xFFFFE000u;
+            hi[k] = h;
+            lo[k] = __float_as_uint(x - __uint_as_float(h));
           }
         }
         const uint32_t ta = tmem + (uint32_t(32 * q) << 16) + TA_COL0 + uint32_t(s) * 32u;
@@ -492,7 +505,7 @@ __global__ void __launch_bounds__(kThreadsFor<TA>(), 1)
         }
       }
   } else if (warp == 1) {
-    constexpr uint32_t idesc = make_idesc(A_MN, B_MN, BN);
+    constexpr uint32_t idesc = make_idesc(TA ? false : A_MN, B_MN, BN);  // TMEM A: lane = row, column = k
     uint32_t g = 0, chunk = 0;
     for (int t = blockIdx.x; t < ep.n_tiles; t += gridDim.x) {
       const TileInfo ti = tile_info<BN, CAUSAL>(ep, t, K);
@@ -654,8 +667,8 @@ void launch(const GemmArgs& g, cudaStream_t s) {
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     attr_set = true;
   }
-  if constexpr (!A_MN && THREE && BN == 64) {
-    // on-chip residuals of a K-major A: A through tensor memory (SD_GEMM_TMEM_A=0 disables)
+  if constexpr (THREE && BN == 64) {
+    // on-chip residuals: A through tensor memory (SD_GEMM_TMEM_A=0 disables)
     if (g.onchip && sd_gemm_tmem_a_enabled()) {
       kern = g.causal ? k_gemm_tf32<A_MN, B_MN, THREE, BN, true, true> : k_gemm_tf32<A_MN, B_MN, THREE, BN, false, true>;
       threads = kThreadsFor<true>();
