@@ -81,6 +81,28 @@ __device__ __forceinline__ void mma_tf32_pair(uint32_t tmem_d, uint64_t da, uint
 }
 // arrive on the barrier at this offset in BOTH CTAs of the pair once the
 // leader's previously issued MMAs complete
+// warp-wide issue: uniform descriptor math on every lane, one elected lane issues
+__device__ __forceinline__ void mma_tf32_pair_e(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
+                                                uint32_t acc) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t"
+      "}" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void mma_commit_pair_e(uint64_t* bar) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t"
+      "}" ::"r"(smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
 __device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
   asm volatile(
       "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
@@ -266,7 +288,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
           if (first && chunk >= 2) mbar_wait(&tempty[buf], ((chunk >> 1) - 1) & 1);
           mbar_wait(ep.res ? &conv[s] : &full[s], ph);  // both CTAs' stage s (and residuals) ready
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          if (lane == 0) {
+          {  // whole warp: elected issue
             const uint32_t d = tmem + buf * kPairN;
             const uint32_t st = smem_u32(smem + s * STAGE_BYTES);
             const uint32_t a = st, as = st + PA_BYTES;
@@ -276,15 +298,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
             for (int ks = 0; ks < BK / 8; ++ks) {
               const uint32_t acc0 = (first && ks == 0) ? 0u : 1u;
               if (THREE) {
-                mma_tf32_pair(d, tile_desc<A_MN>(as, ks), tile_desc<B_MN>(b, ks), idesc, acc0);
-                if (!bex) mma_tf32_pair(d, tile_desc<A_MN>(a, ks), tile_desc<B_MN>(bs, ks), idesc, 1u);
-                mma_tf32_pair(d, tile_desc<A_MN>(a, ks), tile_desc<B_MN>(b, ks), idesc, 1u);
+                mma_tf32_pair_e(d, tile_desc<A_MN>(as, ks), tile_desc<B_MN>(b, ks), idesc, acc0);
+                if (!bex) mma_tf32_pair_e(d, tile_desc<A_MN>(a, ks), tile_desc<B_MN>(bs, ks), idesc, 1u);
+                mma_tf32_pair_e(d, tile_desc<A_MN>(a, ks), tile_desc<B_MN>(b, ks), idesc, 1u);
               } else {
-                mma_tf32_pair(d, tile_desc<A_MN>(a, ks), tile_desc<B_MN>(b, ks), idesc, acc0);
+                mma_tf32_pair_e(d, tile_desc<A_MN>(a, ks), tile_desc<B_MN>(b, ks), idesc, acc0);
               }
             }
-            mma_commit_pair(&empty[s]);
-            if (last) mma_commit_pair(&tfull[buf]);
+            mma_commit_pair_e(&empty[s]);
+            if (last) mma_commit_pair_e(&tfull[buf]);
           }
           __syncwarp();
           if (last) ++chunk;
