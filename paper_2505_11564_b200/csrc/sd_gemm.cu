@@ -377,7 +377,7 @@ __global__ void __launch_bounds__(kThreadsFor<TA>(), 1)
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
-    if (lane == 0) {
+    {  // whole warp; elected lane issues (no waterfall loops around TMA)
       asm volatile("prefetch.tensormap [%0];" ::"l"(&mA) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(&mB) : "memory");
       uint32_t g = 0;  // global k-block counter (ring position)
@@ -393,7 +393,7 @@ __global__ void __launch_bounds__(kThreadsFor<TA>(), 1)
           // dual source: the second product's k-blocks follow the first's
           const bool src2 = kk >= ti.num_kb;
           const bool bex = THREE && !ep.res && ((ep.bexact >> (src2 ? 1 : 0)) & 1);
-          mbar_expect_tx(&full[s], ep.res ? A_BYTES + B_BYTES : STAGE_BYTES - (bex ? B_BYTES : 0));
+          mbar_expect_tx_e(&full[s], ep.res ? A_BYTES + B_BYTES : STAGE_BYTES - (bex ? B_BYTES : 0));
           const int kb = src2 ? kk - ti.num_kb : kk;
           const CUtensorMap* pA = src2 ? &mA2 : &mA;
           const CUtensorMap* pAs = src2 ? &mAs2 : &mAs;
@@ -401,31 +401,31 @@ __global__ void __launch_bounds__(kThreadsFor<TA>(), 1)
           const CUtensorMap* pBs = src2 ? &mBs2 : &mBs;
           const int k0 = (ti.kb0 + kb) * BK;
           if (A_MN && (ep.mn5 & 1)) {
-            tma_load_5d(pA, &full[s], st, 0, k0, ti.m0 / 32, z1, z2);
-            if (THREE && !ep.res) tma_load_5d(pAs, &full[s], st + A_BYTES, 0, k0, ti.m0 / 32, z1, z2);
+            tma_load_5d_e(pA, &full[s], st, 0, k0, ti.m0 / 32, z1, z2);
+            if (THREE && !ep.res) tma_load_5d_e(pAs, &full[s], st + A_BYTES, 0, k0, ti.m0 / 32, z1, z2);
           } else if (A_MN) {
 #pragma unroll
             for (int c = 0; c < BM / 32; ++c) {
-              tma_load_4d(pA, &full[s], st + c * 2048, ti.m0 + 32 * c, k0, z1, z2);
-              if (THREE && !ep.res) tma_load_4d(pAs, &full[s], st + A_BYTES + c * 2048, ti.m0 + 32 * c, k0, z1, z2);
+              tma_load_4d_e(pA, &full[s], st + c * 2048, ti.m0 + 32 * c, k0, z1, z2);
+              if (THREE && !ep.res) tma_load_4d_e(pAs, &full[s], st + A_BYTES + c * 2048, ti.m0 + 32 * c, k0, z1, z2);
             }
           } else {
-            tma_load_4d(pA, &full[s], st, k0, ti.m0, z1, z2);
-            if (THREE && !ep.res) tma_load_4d(pAs, &full[s], st + A_BYTES, k0, ti.m0, z1, z2);
+            tma_load_4d_e(pA, &full[s], st, k0, ti.m0, z1, z2);
+            if (THREE && !ep.res) tma_load_4d_e(pAs, &full[s], st + A_BYTES, k0, ti.m0, z1, z2);
           }
           unsigned char* sb = st + (THREE ? 2 : 1) * A_BYTES;
           if (B_MN && (ep.mn5 & 2)) {
-            tma_load_5d(pB, &full[s], sb, 0, k0, ti.n0 / 32, z1, z2);
-            if (THREE && !ep.res && !bex) tma_load_5d(pBs, &full[s], sb + B_BYTES, 0, k0, ti.n0 / 32, z1, z2);
+            tma_load_5d_e(pB, &full[s], sb, 0, k0, ti.n0 / 32, z1, z2);
+            if (THREE && !ep.res && !bex) tma_load_5d_e(pBs, &full[s], sb + B_BYTES, 0, k0, ti.n0 / 32, z1, z2);
           } else if (B_MN) {
 #pragma unroll
             for (int c = 0; c < BN / 32; ++c) {
-              tma_load_4d(pB, &full[s], sb + c * 2048, ti.n0 + 32 * c, k0, z1, z2);
-              if (THREE && !ep.res && !bex) tma_load_4d(pBs, &full[s], sb + B_BYTES + c * 2048, ti.n0 + 32 * c, k0, z1, z2);
+              tma_load_4d_e(pB, &full[s], sb + c * 2048, ti.n0 + 32 * c, k0, z1, z2);
+              if (THREE && !ep.res && !bex) tma_load_4d_e(pBs, &full[s], sb + B_BYTES + c * 2048, ti.n0 + 32 * c, k0, z1, z2);
             }
           } else {
-            tma_load_4d(pB, &full[s], sb, k0, ti.n0, z1, z2);
-            if (THREE && !ep.res && !bex) tma_load_4d(pBs, &full[s], sb + B_BYTES, k0, ti.n0, z1, z2);
+            tma_load_4d_e(pB, &full[s], sb, k0, ti.n0, z1, z2);
+            if (THREE && !ep.res && !bex) tma_load_4d_e(pBs, &full[s], sb + B_BYTES, k0, ti.n0, z1, z2);
           }
         }
       }

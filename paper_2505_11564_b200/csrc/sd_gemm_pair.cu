@@ -69,6 +69,24 @@ __device__ __forceinline__ void tma_load_5d_pair(const CUtensorMap* map, uint32_
       "l"(map), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
       : "memory");
 }
+__device__ __forceinline__ void tma_load_4d_pair_e(const CUtensorMap* map, uint32_t bar, void* dst, int c0, int c1,
+                                                   int c2, int c3) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+      "%4, %5, %6}], [%2];\n\t}" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_5d_pair_e(const CUtensorMap* map, uint32_t bar, void* dst, int c0, int c1,
+                                                   int c2, int c3, int c4) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e cp.async.bulk.tensor.5d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+      "%4, %5, %6, %7}], [%2];\n\t}" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
+      : "memory");
+}
 __device__ __forceinline__ void mma_tf32_pair(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
                                               uint32_t acc) {
   asm volatile(
@@ -187,7 +205,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
-    if (lane == 0) {
+    {  // whole warp; elected lane issues (no waterfall loops around TMA)
       const uint32_t full_leader = leader_addr(full);
       uint32_t g = 0;
       for (int t = cid; t < ep.n_tiles; t += ncl) {
@@ -207,10 +225,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
           const bool bex = THREE && !ep.res && ((ep.bexact >> (src2 ? 1 : 0)) & 1);
           uint32_t bar;
           if (ep.res) {
-            mbar_expect_tx(&full[s], PA_BYTES + PB_BYTES);
+            mbar_expect_tx_e(&full[s], PA_BYTES + PB_BYTES);
             bar = smem_u32(&full[s]);
           } else {
-            if (rank == 0) mbar_expect_tx(&full[s], 2 * (STAGE_BYTES - (bex ? PB_BYTES : 0)));
+            if (rank == 0) mbar_expect_tx_e(&full[s], 2 * (STAGE_BYTES - (bex ? PB_BYTES : 0)));
             bar = full_leader + 8u * s;
           }
           const int kb = src2 ? kk - ti.num_kb : kk;
@@ -220,31 +238,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
           const CUtensorMap* pBs = src2 ? &mBs2 : &mBs;
           const int k0 = (ti.kb0 + kb) * BK;
           if (A_MN && (ep.mn5 & 1)) {
-            tma_load_5d_pair(pA, bar, st, 0, k0, m_own / 32, z1, z2);
-            if (THREE && !ep.res) tma_load_5d_pair(pAs, bar, st + PA_BYTES, 0, k0, m_own / 32, z1, z2);
+            tma_load_5d_pair_e(pA, bar, st, 0, k0, m_own / 32, z1, z2);
+            if (THREE && !ep.res) tma_load_5d_pair_e(pAs, bar, st + PA_BYTES, 0, k0, m_own / 32, z1, z2);
           } else if (A_MN) {
 #pragma unroll
             for (int c = 0; c < BM / 32; ++c) {
-              tma_load_4d_pair(pA, bar, st + c * 2048, m_own + 32 * c, k0, z1, z2);
-              if (THREE && !ep.res) tma_load_4d_pair(pAs, bar, st + PA_BYTES + c * 2048, m_own + 32 * c, k0, z1, z2);
+              tma_load_4d_pair_e(pA, bar, st + c * 2048, m_own + 32 * c, k0, z1, z2);
+              if (THREE && !ep.res) tma_load_4d_pair_e(pAs, bar, st + PA_BYTES + c * 2048, m_own + 32 * c, k0, z1, z2);
             }
           } else {
-            tma_load_4d_pair(pA, bar, st, k0, m_own, z1, z2);
-            if (THREE && !ep.res) tma_load_4d_pair(pAs, bar, st + PA_BYTES, k0, m_own, z1, z2);
+            tma_load_4d_pair_e(pA, bar, st, k0, m_own, z1, z2);
+            if (THREE && !ep.res) tma_load_4d_pair_e(pAs, bar, st + PA_BYTES, k0, m_own, z1, z2);
           }
           unsigned char* sb = st + (THREE ? 2 : 1) * PA_BYTES;
           if (B_MN && (ep.mn5 & 2)) {
-            tma_load_5d_pair(pB, bar, sb, 0, k0, n_own / 32, z1, z2);
-            if (THREE && !ep.res && !bex) tma_load_5d_pair(pBs, bar, sb + PB_BYTES, 0, k0, n_own / 32, z1, z2);
+            tma_load_5d_pair_e(pB, bar, sb, 0, k0, n_own / 32, z1, z2);
+            if (THREE && !ep.res && !bex) tma_load_5d_pair_e(pBs, bar, sb + PB_BYTES, 0, k0, n_own / 32, z1, z2);
           } else if (B_MN) {
 #pragma unroll
             for (int c = 0; c < kHalfB / 32; ++c) {
-              tma_load_4d_pair(pB, bar, sb + c * 2048, n_own + 32 * c, k0, z1, z2);
-              if (THREE && !ep.res && !bex) tma_load_4d_pair(pBs, bar, sb + PB_BYTES + c * 2048, n_own + 32 * c, k0, z1, z2);
+              tma_load_4d_pair_e(pB, bar, sb + c * 2048, n_own + 32 * c, k0, z1, z2);
+              if (THREE && !ep.res && !bex) tma_load_4d_pair_e(pBs, bar, sb + PB_BYTES + c * 2048, n_own + 32 * c, k0, z1, z2);
             }
           } else {
-            tma_load_4d_pair(pB, bar, sb, k0, n_own, z1, z2);
-            if (THREE && !ep.res && !bex) tma_load_4d_pair(pBs, bar, sb + PB_BYTES, k0, n_own, z1, z2);
+            tma_load_4d_pair_e(pB, bar, sb, k0, n_own, z1, z2);
+            if (THREE && !ep.res && !bex) tma_load_4d_pair_e(pBs, bar, sb + PB_BYTES, k0, n_own, z1, z2);
           }
         }
       }
