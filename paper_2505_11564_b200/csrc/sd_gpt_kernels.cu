@@ -457,6 +457,123 @@ __global__ void k_attn_softmax_fwd(float* __restrict__ Sm, float* __restrict__ d
   }
 }
 
+// Register-resident forms for S = 128 NV <= 1024 (rows 16-byte aligned): lane
+// l owns the float4 groups l, l + 32, ... of its row; a row is read once into
+// registers (only the groups up to the causal end), exponentials are formed
+// once, and the writes stop at the end of the row's 128-row tile.
+template <int NV>
+__global__ void __launch_bounds__(256) k_attn_softmax_fwd_reg(float* __restrict__ Sm, float* __restrict__ dS,
+                                                              long long rows) {
+  constexpr int S = 128 * NV;
+  const long long row = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const int i = int(row % S);
+  float4* s4 = reinterpret_cast<float4*>(Sm + row * S);
+  float4* d4 = reinterpret_cast<float4*>(dS + row * S);
+  float4 sv[NV], dv[NV];
+  float m = -INFINITY;
+#pragma unroll
+  for (int t = 0; t < NV; ++t) {
+    const int j0 = 4 * (lane + 32 * t);
+    if (j0 <= i) {
+      sv[t] = s4[lane + 32 * t];
+      dv[t] = d4[lane + 32 * t];
+      m = fmaxf(m, sv[t].x);
+      if (j0 + 1 <= i) m = fmaxf(m, sv[t].y);
+      if (j0 + 2 <= i) m = fmaxf(m, sv[t].z);
+      if (j0 + 3 <= i) m = fmaxf(m, sv[t].w);
+    }
+  }
+  m = warp_max(m);
+  float z = 0.f, zd = 0.f;
+#pragma unroll
+  for (int t = 0; t < NV; ++t) {
+    const int j0 = 4 * (lane + 32 * t);
+    if (j0 <= i) {
+#define SD_SMX(f, o)                                   \
+      {                                                \
+        const float e = j0 + o <= i ? __expf(sv[t].f - m) : 0.f; \
+        sv[t].f = e;                                   \
+        z += e;                                        \
+        zd += e * dv[t].f;                             \
+      }
+      SD_SMX(x, 0) SD_SMX(y, 1) SD_SMX(z, 2) SD_SMX(w, 3)
+#undef SD_SMX
+    }
+  }
+  z = warp_sum(z);
+  zd = warp_sum(zd);
+  const float inv = 1.f / z, mean_d = zd * inv;
+  const int jend = min(S, (i / kCausalTile + 1) * kCausalTile);
+#pragma unroll
+  for (int t = 0; t < NV; ++t) {
+    const int j0 = 4 * (lane + 32 * t);
+    if (j0 < jend) {
+      float4 p = make_float4(0.f, 0.f, 0.f, 0.f), dp = p;
+      if (j0 <= i) {  // masked entries hold e = 0
+        p = make_float4(sv[t].x * inv, sv[t].y * inv, sv[t].z * inv, sv[t].w * inv);
+        dp = make_float4(p.x * (dv[t].x - mean_d), p.y * (dv[t].y - mean_d), p.z * (dv[t].z - mean_d),
+                         p.w * (dv[t].w - mean_d));
+        if (j0 + 1 > i) dp.y = 0.f;
+        if (j0 + 2 > i) dp.z = 0.f;
+        if (j0 + 3 > i) dp.w = 0.f;
+      }
+      s4[lane + 32 * t] = p;
+      d4[lane + 32 * t] = dp;
+    }
+  }
+}
+
+template <int NV>
+__global__ void __launch_bounds__(256) k_attn_softmax_bwd_reg(const float* __restrict__ P,
+                                                              const float* __restrict__ dP, float* __restrict__ gP,
+                                                              float* __restrict__ gdP, long long rows) {
+  constexpr int S = 128 * NV;
+  const long long row = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const int i = int(row % S);
+  const float4* p4 = reinterpret_cast<const float4*>(P + row * S);
+  const float4* dp4 = reinterpret_cast<const float4*>(dP + row * S);
+  float4* g4 = reinterpret_cast<float4*>(gP + row * S);
+  float4* gd4 = reinterpret_cast<float4*>(gdP + row * S);
+  float4 pv[NV], dpv[NV], gv[NV], gdv[NV];
+  float c = 0.f, dc = 0.f;
+#pragma unroll
+  for (int t = 0; t < NV; ++t) {
+    const int j0 = 4 * (lane + 32 * t);
+    if (j0 <= i) {  // P, dP are zero past the diagonal (written so by the forward)
+      pv[t] = p4[lane + 32 * t], dpv[t] = dp4[lane + 32 * t];
+      gv[t] = g4[lane + 32 * t], gdv[t] = gd4[lane + 32 * t];
+#define SD_SMB(f)                                              \
+      c += pv[t].f * gv[t].f;                                  \
+      dc += dpv[t].f * gv[t].f + pv[t].f * gdv[t].f;
+      SD_SMB(x) SD_SMB(y) SD_SMB(z) SD_SMB(w)
+#undef SD_SMB
+    }
+  }
+  c = warp_sum(c);
+  dc = warp_sum(dc);
+  const int jend = min(S, (i / kCausalTile + 1) * kCausalTile);
+#pragma unroll
+  for (int t = 0; t < NV; ++t) {
+    const int j0 = 4 * (lane + 32 * t);
+    if (j0 < jend) {
+      float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
+      if (j0 <= i) {
+#define SD_SMB2(f)                                                                   \
+        a.f = pv[t].f * (gv[t].f - c);                                               \
+        b.f = dpv[t].f * (gv[t].f - c) + pv[t].f * (gdv[t].f - dc);
+        SD_SMB2(x) SD_SMB2(y) SD_SMB2(z) SD_SMB2(w)
+#undef SD_SMB2
+      }
+      g4[lane + 32 * t] = a;
+      gd4[lane + 32 * t] = b;
+    }
+  }
+}
+
 // gS = P (gP - c), gdS = dP (gP - c) + P (gdP - dc),  c = sum P gP,
 // dc = sum (dP gP + P gdP). In place over gP, gdP.
 __global__ void k_attn_softmax_bwd(const float* __restrict__ P, const float* __restrict__ dP, float* __restrict__ gP,
@@ -820,12 +937,34 @@ void gpt_gelu_bwd(const float* f, const float* df, float* gu, float* gdu, float*
 }
 
 void gpt_attn_softmax_fwd(float* Sm, float* dS, float* Ps, float* dPs, int S, long long rows, cudaStream_t s) {
+  if (!Ps && S % 128 == 0 && S <= 1024) {
+    switch (S / 128) {
+#define SD_SMF(NV)                                                                  \
+  case NV:                                                                          \
+    k_attn_softmax_fwd_reg<NV><<<g1(rows, 8), 256, 0, s>>>(Sm, dS, rows);           \
+    SD_LAUNCHED("k_attn_softmax_fwd_reg");                                          \
+    return;
+      SD_SMF(1) SD_SMF(2) SD_SMF(3) SD_SMF(4) SD_SMF(5) SD_SMF(6) SD_SMF(7) SD_SMF(8)
+#undef SD_SMF
+    }
+  }
   k_attn_softmax_fwd<<<g1(rows, 8), 256, 0, s>>>(Sm, dS, Ps, dPs, S, rows);
   SD_LAUNCHED("k_attn_softmax_fwd");
 }
 
 void gpt_attn_softmax_bwd(const float* P, const float* dP, float* gP, float* gdP, float* gPs, float* gdPs, int S,
                           long long rows, cudaStream_t s) {
+  if (!gPs && S % 128 == 0 && S <= 1024) {
+    switch (S / 128) {
+#define SD_SMBW(NV)                                                                 \
+  case NV:                                                                          \
+    k_attn_softmax_bwd_reg<NV><<<g1(rows, 8), 256, 0, s>>>(P, dP, gP, gdP, rows);    \
+    SD_LAUNCHED("k_attn_softmax_bwd_reg");                                          \
+    return;
+      SD_SMBW(1) SD_SMBW(2) SD_SMBW(3) SD_SMBW(4) SD_SMBW(5) SD_SMBW(6) SD_SMBW(7) SD_SMBW(8)
+#undef SD_SMBW
+    }
+  }
   k_attn_softmax_bwd<<<g1(rows, 8), 256, 0, s>>>(P, dP, gP, gdP, gPs, gdPs, S, rows);
   SD_LAUNCHED("k_attn_softmax_bwd");
 }
