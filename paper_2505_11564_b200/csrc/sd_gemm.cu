@@ -520,10 +520,8 @@ __global__ void __launch_bounds__(kThreadsFor<TA>(), 1)
         if (first && chunk >= 2) mbar_wait(&tempty[buf], ((chunk >> 1) - 1) & 1);
         mbar_wait(ep.res ? &conv[s] : &full[s], ph);  // stage landed (and its residuals written)
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-#ifndef SD_MMA_ELECT
-#define SD_MMA_ELECT 1
-#endif
-        if (SD_MMA_ELECT || lane == 0) {
+        {  // whole warp: uniform descriptor math, one elect.sync-elected lane issues (a lane-0
+           // branch here makes the compiler wrap every MMA in a waterfall loop)
           const uint32_t d = tmem + buf * BN;
           const uint32_t st = smem_u32(smem + s * STAGE_BYTES);
           const uint32_t a = st, as = st + A_BYTES;
@@ -532,39 +530,21 @@ __global__ void __launch_bounds__(kThreadsFor<TA>(), 1)
 #pragma unroll
           for (int ks = 0; ks < BK / 8; ++ks) {
             const uint32_t acc0 = (first && ks == 0) ? 0u : 1u;
-            if (SD_MMA_ELECT) {
-              if (TA) {
-                const uint32_t ta = tmem + TA_COL0 + uint32_t(s) * 32u + uint32_t(ks) * 8u;
-                mma_tf32_ta_e(d, ta + 16, tile_desc<B_MN>(b, ks), idesc, acc0);
-                mma_tf32_ta_e(d, ta, tile_desc<B_MN>(bs, ks), idesc, 1u);
-                mma_tf32_ta_e(d, ta, tile_desc<B_MN>(b, ks), idesc, 1u);
-              } else if (THREE) {
-                mma_tf32_e(d, tile_desc<A_MN>(as, ks), tile_desc<B_MN>(b, ks), idesc, acc0);
-                if (!bex) mma_tf32_e(d, tile_desc<A_MN>(a, ks), tile_desc<B_MN>(bs, ks), idesc, 1u);
-                mma_tf32_e(d, tile_desc<A_MN>(a, ks), tile_desc<B_MN>(b, ks), idesc, 1u);
-              } else {
-                mma_tf32_e(d, tile_desc<A_MN>(a, ks), tile_desc<B_MN>(b, ks), idesc, acc0);
-              }
-            } else if (TA) {
+            if (TA) {
               const uint32_t ta = tmem + TA_COL0 + uint32_t(s) * 32u + uint32_t(ks) * 8u;
-              mma_tf32_ta(d, ta + 16, tile_desc<B_MN>(b, ks), idesc, acc0);  // A_lo . B
-              mma_tf32_ta(d, ta, tile_desc<B_MN>(bs, ks), idesc, 1u);        // A_hi . B_lo
-              mma_tf32_ta(d, ta, tile_desc<B_MN>(b, ks), idesc, 1u);         // A_hi . B
+              mma_tf32_ta_e(d, ta + 16, tile_desc<B_MN>(b, ks), idesc, acc0);
+              mma_tf32_ta_e(d, ta, tile_desc<B_MN>(bs, ks), idesc, 1u);
+              mma_tf32_ta_e(d, ta, tile_desc<B_MN>(b, ks), idesc, 1u);
             } else if (THREE) {
-              mma_tf32(d, tile_desc<A_MN>(as, ks), tile_desc<B_MN>(b, ks), idesc, acc0);
-              if (!bex) mma_tf32(d, tile_desc<A_MN>(a, ks), tile_desc<B_MN>(bs, ks), idesc, 1u);
-              mma_tf32(d, tile_desc<A_MN>(a, ks), tile_desc<B_MN>(b, ks), idesc, 1u);
+              mma_tf32_e(d, tile_desc<A_MN>(as, ks), tile_desc<B_MN>(b, ks), idesc, acc0);
+              if (!bex) mma_tf32_e(d, tile_desc<A_MN>(a, ks), tile_desc<B_MN>(bs, ks), idesc, 1u);
+              mma_tf32_e(d, tile_desc<A_MN>(a, ks), tile_desc<B_MN>(b, ks), idesc, 1u);
             } else {
-              mma_tf32(d, tile_desc<A_MN>(a, ks), tile_desc<B_MN>(b, ks), idesc, acc0);
+              mma_tf32_e(d, tile_desc<A_MN>(a, ks), tile_desc<B_MN>(b, ks), idesc, acc0);
             }
           }
-          if (SD_MMA_ELECT) {
-            mma_commit_e(&empty[s]);
-            if (last) mma_commit_e(&tfull[buf]);
-          } else {
-            mma_commit(&empty[s]);
-            if (last) mma_commit(&tfull[buf]);
-          }
+          mma_commit_e(&empty[s]);
+          if (last) mma_commit_e(&tfull[buf]);
         }
         __syncwarp();
         if (last) ++chunk;
