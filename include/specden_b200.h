@@ -156,6 +156,9 @@ sd_status sd_comm_destroy(sd_comm c);
  * exchange by device copies (rank-ordered sums); point-to-point sends complete
  * when the receiver has copied them, groups batch them like NCCL groups. */
 sd_status sd_comm_local_create(int nranks, sd_comm* out);
+/* a failing in-process worker aborts its group: the others' pending and
+ * future collectives fail with SD_PROTOCOL_ERROR instead of waiting forever */
+sd_status sd_comm_abort(sd_comm c);
 /* In-place sum all-reduce of n floats (data-sharded HVP, C1 of SURVEY §2.1). */
 sd_status sd_comm_allreduce_f32(sd_comm c, float* buf, uint64_t n, sd_stream s);
 /* All-gather of `bytes` per rank (ordered scalar partial exchange). */

@@ -106,6 +106,7 @@ _SIGS = {
     "sd_comm_nccl_create": (i32, [C.c_char_p, i32, i32, C.POINTER(vp)]),
     "sd_comm_destroy": (i32, [vp]),
     "sd_comm_local_create": (i32, [i32, C.POINTER(vp)]),
+    "sd_comm_abort": (i32, [vp]),
     "sd_comm_allreduce_f32": (i32, [vp, vp, u64, vp]),
     "sd_comm_allgather": (i32, [vp, vp, vp, u64, vp]),
     "sd_operator_custom": (i32, [u64, APPLY_FN, vp, C.POINTER(vp)]),

@@ -588,6 +588,7 @@ def run_workers(n: int, fn):
                 torch.cuda.current_stream().synchronize()
         except BaseException as e:  # noqa: BLE001 -- surfaced below in rank order
             err[r] = e
+            lib().sd_comm_abort(comms[r].handle)  # release the workers waiting on this one
     ts = [threading.Thread(target=body, args=(r,)) for r in range(n)]
     for t in ts:
         t.start()
@@ -595,8 +596,10 @@ def run_workers(n: int, fn):
         t.join()
     for c in comms:
         c.close()
-    for e in err:
-        if e is not None:
-            raise e
+    # the lowest-rank ORIGINAL failure (pool.cpp:54-64); workers released by the
+    # abort only report the abort
+    real = [e for e in err if e is not None and not (isinstance(e, ProtocolError) and "aborted" in str(e))]
+    for e in real or [e for e in err if e is not None]:
+        raise e
     return out
 

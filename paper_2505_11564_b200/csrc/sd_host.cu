@@ -220,16 +220,31 @@ struct LocalGroup {
   // point-to-point: FIFO of posted sends per (src, dst); a send completes when
   // the receiver has copied it (blocking semantics, like NCCL's)
   std::vector<std::vector<std::deque<LocalMsg*>>> q;
+  // a worker that fails outside a collective aborts the group, so that the
+  // others leave their waits with a protocol error instead of hanging
+  bool aborted = false;
+  void check_abort() const {
+    if (aborted) sd::fail(SD_PROTOCOL_ERROR, "worker group aborted by another worker's failure");
+  }
   void barrier() {
     std::unique_lock<std::mutex> lk(m);
+    check_abort();
     const uint64_t g = gen;
     if (++arrived == n) {
       arrived = 0;
       ++gen;
       cv.notify_all();
     } else {
-      cv.wait(lk, [&] { return gen != g; });
+      cv.wait(lk, [&] { return gen != g || aborted; });
+      check_abort();
     }
+  }
+  void abort() {
+    {
+      std::lock_guard<std::mutex> lk(m);
+      aborted = true;
+    }
+    cv.notify_all();
   }
 };
 
@@ -298,7 +313,8 @@ void local_p2p(sd_comm c, std::vector<LocalP2p>& ops, cudaStream_t s) {
     LocalMsg* m = nullptr;
     {
       std::unique_lock<std::mutex> lk(g.m);
-      g.cv.wait(lk, [&] { return !g.q[o.peer][c->rank].empty(); });
+      g.cv.wait(lk, [&] { return !g.q[o.peer][c->rank].empty() || g.aborted; });
+      g.check_abort();
       m = g.q[o.peer][c->rank].front();
       g.q[o.peer][c->rank].pop_front();
     }
@@ -313,7 +329,16 @@ void local_p2p(sd_comm c, std::vector<LocalP2p>& ops, cudaStream_t s) {
   }
   std::unique_lock<std::mutex> lk(g.m);
   for (size_t i = 0; i < ops.size(); ++i)
-    if (ops[i].send) g.cv.wait(lk, [&] { return msgs[i].done; });
+    if (ops[i].send) {
+      g.cv.wait(lk, [&] { return msgs[i].done || g.aborted; });
+      if (!msgs[i].done) {
+        // withdraw the un-received message (it lives on this stack frame)
+        for (auto& qq : g.q[c->rank])
+          for (auto it = qq.begin(); it != qq.end();)
+            it = (*it == &msgs[i]) ? qq.erase(it) : it + 1;
+        g.check_abort();
+      }
+    }
 }
 }  // namespace
 
@@ -671,6 +696,12 @@ sd_status sd_comm_destroy(sd_comm c) {
     if (c && c->comm) nccl_check(nccl().CommDestroy(c->comm), "ncclCommDestroy");
     if (c && c->d_ptrs) cudaFree(c->d_ptrs);
     delete c;
+  });
+}
+
+sd_status sd_comm_abort(sd_comm c) {
+  return guard([&] {
+    if (c && c->local) c->local->abort();
   });
 }
 

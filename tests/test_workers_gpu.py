@@ -124,3 +124,25 @@ def test_pipeline_operator_workers(sd, n_stages, M):
         out = sd.run_workers(n_stages, worker)
         for res in out:
             assert np.array_equal(res.alphas, a.alphas) and np.array_equal(res.betas, a.betas)
+
+
+@pytest.mark.timeout(120)
+def test_failing_worker_aborts_the_group(sd):
+    # pool.cpp:54-64: every worker replies, the first (lowest-rank) exception is
+    # rethrown. A worker failing outside a collective aborts the group, so the
+    # others leave their waits instead of hanging; the original error surfaces.
+    op = sd.wigner_operator(128, 1.0, 3)
+    cfg = sd.LanczosConfig(k_max=5, prec=sd.F64, probe=sd.ProbeSpec(seed=0, distribution=sd.RADEMACHER))
+    lay = sd.split_evenly(128, 3)
+
+    def worker(r, comm):
+        if r == 1:
+            raise ValueError("worker 1 failed")
+        return sd.lanczos_run(op, cfg, layout=lay, comm=comm)
+
+    with pytest.raises(ValueError, match="worker 1 failed"):
+        sd.run_workers(3, worker)
+    # the device and new groups are still usable afterwards
+    out = sd.run_workers(3, lambda r, c: sd.lanczos_run(op, cfg, layout=lay, comm=c))
+    ref = sd.lanczos_run(op, cfg)
+    assert np.array_equal(out[2].alphas, ref.alphas)
