@@ -31,4 +31,6 @@ int comm_size(sd_comm c);
 void operator_apply(sd_operator op, const void* x, void* y, int prec, cudaStream_t s, uint64_t row_begin,
                     uint64_t row_end, const void* x_full);
 bool operator_needs_full(sd_operator op);
+// ctx release on sd_operator_destroy (operators the engines create around their contexts)
+void operator_set_dtor(sd_operator op, void (*dtor)(void*));
 }  // namespace sd

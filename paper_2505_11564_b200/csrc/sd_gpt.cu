@@ -1027,9 +1027,13 @@ sd_status sd_gpt_destroy(sd_gpt g) {
 sd_status sd_operator_gpt(sd_gpt g, sd_comm comm, sd_operator* out) {
   return sd::guard([&] {
     if (!g || !g->first || !g->last) fail(SD_ARGUMENT_ERROR, "gpt operator needs a whole-model engine");
-    auto* ctx = new GptOpCtx{g, comm};  // lives as long as the process (tiny)
+    auto* ctx = new GptOpCtx{g, comm};
     const sd_status st = sd_operator_custom(uint64_t(g->P), gpt_apply, ctx, out);
-    if (st != SD_OK) fail(st, "operator_custom failed");
+    if (st != SD_OK) {
+      delete ctx;
+      fail(st, "operator_custom failed");
+    }
+    sd::operator_set_dtor(*out, [](void* p) { delete static_cast<GptOpCtx*>(p); });
   });
 }
 
@@ -1050,7 +1054,8 @@ sd_status sd_operator_gpt_pipeline(sd_gpt g, sd_comm comm, sd_operator* out) {
       fail(SD_ARGUMENT_ERROR, sd_last_error());
     const sd_status st = sd_operator_custom(uint64_t(g->P), gpt_pipe_apply, c.get(), out);
     if (st != SD_OK) fail(st, "operator_custom failed");
-    c.release();  // lives as long as the process (one per engine)
+    c.release();  // owned by the operator from here on
+    sd::operator_set_dtor(*out, [](void* p) { delete static_cast<GptPipeCtx*>(p); });
   });
 }
 
@@ -1061,7 +1066,7 @@ sd_status sd_operator_gpt_sharded(sd_gpt g, sd_comm comm, const uint64_t* begins
   return sd::guard([&] {
     if (!g || !begins || !ends) sd::fail(SD_ARGUMENT_ERROR, "null argument");
     if (!g->first || !g->last) fail(SD_ARGUMENT_ERROR, "sharded gpt operator needs a whole-model engine");
-    auto* c = new GptShardCtx();  // lives as long as the process (one per engine)
+    auto* c = new GptShardCtx();  // owned by the operator (released by sd_operator_destroy)
     c->g = g;
     c->comm = comm;
     c->nranks = sd::comm_size(comm);
@@ -1082,6 +1087,12 @@ sd_status sd_operator_gpt_sharded(sd_gpt g, sd_comm comm, const uint64_t* begins
     SD_CUDA(cudaMalloc(&c->mine, c->maxlen * sizeof(float)));
     const sd_status st = sd_operator_custom(uint64_t(g->P), gpt_shard_apply, c, out);
     if (st != SD_OK) sd::fail(st, "operator_custom failed");
+    sd::operator_set_dtor(*out, [](void* p) {
+      auto* k = static_cast<GptShardCtx*>(p);
+      for (float* b : {k->slots, k->full, k->hv, k->mine})
+        if (b) cudaFree(b);
+      delete k;
+    });
   });
 }
 

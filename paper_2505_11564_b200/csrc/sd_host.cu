@@ -454,7 +454,14 @@ struct sd_operator_s {
   double* a_dev = nullptr;
   void* xfull = nullptr;  // gather scratch (dense)
   size_t xfull_bytes = 0;
+  void (*dtor)(void*) = nullptr;  // releases ctx (operators built by the engines)
 };
+
+namespace sd {
+void operator_set_dtor(sd_operator op, void (*dtor)(void*)) {
+  if (op) op->dtor = dtor;
+}
+}  // namespace sd
 
 namespace sd {
 
@@ -776,6 +783,7 @@ sd_status sd_operator_destroy(sd_operator op) {
   return guard([&] {
     if (!op) return;
     if (op->a_dev) cudaFree(op->a_dev);
+    if (op->dtor) op->dtor(op->ctx);
     delete op;
   });
 }

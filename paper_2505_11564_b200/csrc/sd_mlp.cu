@@ -330,7 +330,11 @@ sd_status sd_operator_mlp(sd_mlp m, sd_comm comm, sd_operator* out) {
   return sd::guard([&] {
     auto* ctx = new MlpOpCtx{m, comm};
     const sd_status st = sd_operator_custom(uint64_t(m->P), mlp_apply, ctx, out);
-    if (st != SD_OK) sd::fail(st, "operator_custom failed");
+    if (st != SD_OK) {
+      delete ctx;
+      sd::fail(st, "operator_custom failed");
+    }
+    sd::operator_set_dtor(*out, [](void* p) { delete static_cast<MlpOpCtx*>(p); });
   });
 }
 
