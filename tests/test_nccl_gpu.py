@@ -62,3 +62,22 @@ def test_sharded_gpt_operator_one_rank(comm):
     a = sd.lanczos_run(eng.operator(), lc)
     b = sd.lanczos_run(eng.operator(comm, layout=layout), lc, layout=layout, comm=comm)
     assert np.array_equal(a.alphas, b.alphas) and np.array_equal(a.betas, b.betas)
+
+
+def test_operator_destroy_releases_contexts(comm):
+    # the sharded operator owns three full-length scratch vectors: creating and
+    # dropping it repeatedly must not grow device memory
+    import gc
+    import paper_2505_11564_b200 as sd
+    from paper_2505_11564_b200 import gpt
+    cfg = dict(n_layer=1, d=64, n_head=4, ff=256, vocab=96, ctx=32)
+    eng = gpt.GptHvp(cfg, 2, 32)
+    layout = sd.split_evenly(eng.P, 1)
+    torch.cuda.synchronize()
+    free0 = torch.cuda.mem_get_info()[0]
+    for _ in range(40):
+        op = eng.operator(comm, layout=layout)
+        del op
+        gc.collect()
+    torch.cuda.synchronize()
+    assert free0 - torch.cuda.mem_get_info()[0] < 8 * eng.P * 4  # would be 40 x 3 x P floats if leaked
