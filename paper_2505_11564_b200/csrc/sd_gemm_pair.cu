@@ -33,7 +33,7 @@ constexpr int kPairStages = 6;
 // narrower tile is chosen when it quantises into fuller waves (gemm_pair()).
 template <int PN>
 struct PairCfg {
-  static constexpr int N = PN, HALF = PN / 2;
+  static constexpr int HALF = PN / 2;
   static constexpr int PB_BYTES = HALF * BK * 4;      // 8 / 6 KB
   static constexpr uint32_t TMEM_COLS = 512;          // two accumulation buffers (2 PN <= 512)
   static constexpr int EC = PN / (kEpiWarps / 4);     // 64 / 48 accumulator columns per epilogue thread

@@ -500,7 +500,7 @@ struct sd_gpt_s {
   // adjoint of the stage input (the first stage scatters it into the
   // embedding's Hv instead). Hv of micro-batch m > 0 accumulates.
   void stage_bwd(int m, cudaStream_t st) {
-    const int d = c.d, ff = c.ff, V = c.vocab;
+    const int d = c.d, V = c.vocab;
     const long long Td = (long long)T * d;
     const float sc = 1.0f / std::sqrt(float(dh)), eps = 1e-5f;
     const float hb = m > 0 ? 1.0f : 0.0f;  // beta of the Hv products

@@ -614,7 +614,6 @@ __global__ void k_attn_softmax_bwd(const float* __restrict__ P, const float* __r
 __global__ void __launch_bounds__(256) k_ce(float* __restrict__ z, float* __restrict__ dz, float* __restrict__ zs,
                                             float* __restrict__ dzs, const int* __restrict__ tgt, int V, long long ld,
                                             float scale, double* __restrict__ loss_rows) {
-  __shared__ float red[8];
   __shared__ float rm[8], rs[8], rsd[8];
   const long long t = blockIdx.x;
   float* zr = z + t * ld;
@@ -654,7 +653,6 @@ __global__ void __launch_bounds__(256) k_ce(float* __restrict__ z, float* __rest
     s += rs[w] * c;
     sd += rsd[w] * c;
   }
-  (void)red;
   const float inv = 1.f / s, md = sd * inv;
   const int y = tgt[t];
   if (threadIdx.x == 0) loss_rows[t] = double(logf(s) + m - zr[y]);

@@ -22,7 +22,6 @@
 
 namespace sd {
 
-constexpr int kThreads = 128;
 
 // ------------------------------------------------------------------ probes
 // draw_probe fill, proj/src/sharded.cpp:67-75 (normalisation composes later).
