@@ -199,7 +199,7 @@ __global__ void __launch_bounds__(256) k_ln_fwd_reg(const float* __restrict__ x,
 }
 
 template <int NV>
-__global__ void __launch_bounds__(256) k_ln_bwd_reg(const float* __restrict__ gy, const float* __restrict__ gdy,
+__global__ void __launch_bounds__(256, NV <= 6 ? 2 : 1) k_ln_bwd_reg(const float* __restrict__ gy, const float* __restrict__ gdy,
     const float* __restrict__ g, const float* __restrict__ vg, const float* __restrict__ xh,
     const float* __restrict__ dxh, const float* __restrict__ rr, const float* __restrict__ drr, int T,
     float* __restrict__ gx, float* __restrict__ gdx, float* __restrict__ gxs, float* __restrict__ gdxs, int rms) {
