@@ -128,7 +128,7 @@ __global__ void k_ln_fwd(const float* __restrict__ x, const float* __restrict__ 
 // it loads ONCE (16-byte coalesced) and keeps in registers through every pass;
 // same math as k_ln_fwd / k_ln_bwd.
 template <int NV>
-__global__ void __launch_bounds__(256) k_ln_fwd_reg(const float* __restrict__ x, const float* __restrict__ dx,
+__global__ void __launch_bounds__(128) k_ln_fwd_reg(const float* __restrict__ x, const float* __restrict__ dx,
     const float* __restrict__ g, const float* __restrict__ b, const float* __restrict__ vg,
     const float* __restrict__ vb, int T, float eps, float* __restrict__ h, float* __restrict__ hs,
     float* __restrict__ dh, float* __restrict__ dhs, float* __restrict__ xh, float* __restrict__ dxh,
@@ -462,7 +462,7 @@ __global__ void k_attn_softmax_fwd(float* __restrict__ Sm, float* __restrict__ d
 // registers (only the groups up to the causal end), exponentials are formed
 // once, and the writes stop at the end of the row's 128-row tile.
 template <int NV>
-__global__ void __launch_bounds__(256) k_attn_softmax_fwd_reg(float* __restrict__ Sm, float* __restrict__ dS,
+__global__ void __launch_bounds__(128) k_attn_softmax_fwd_reg(float* __restrict__ Sm, float* __restrict__ dS,
                                                               long long rows) {
   constexpr int S = 128 * NV;
   const long long row = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -526,7 +526,7 @@ __global__ void __launch_bounds__(256) k_attn_softmax_fwd_reg(float* __restrict_
 }
 
 template <int NV>
-__global__ void __launch_bounds__(256) k_attn_softmax_bwd_reg(const float* __restrict__ P,
+__global__ void __launch_bounds__(128) k_attn_softmax_bwd_reg(const float* __restrict__ P,
                                                               const float* __restrict__ dP, float* __restrict__ gP,
                                                               float* __restrict__ gdP, long long rows) {
   constexpr int S = 128 * NV;
@@ -879,7 +879,7 @@ void gpt_embed(const int* tok, int T, int S, int d, const float* wte, const floa
 void gpt_ln_fwd(const LnArgs& a, cudaStream_t s) {
 #define SD_LNF(NV)                                                                                                 \
   if (a.d == 128 * NV) {                                                                                           \
-    k_ln_fwd_reg<NV><<<g1(a.T, 8), 256, 0, s>>>(a.x, a.dx, a.g, a.b, a.vg, a.vb, a.T, a.eps, a.h, a.hs, a.dh, a.dhs, \
+    k_ln_fwd_reg<NV><<<g1(a.T, 4), 128, 0, s>>>(a.x, a.dx, a.g, a.b, a.vg, a.vb, a.T, a.eps, a.h, a.hs, a.dh, a.dhs, \
                                                 a.xh, a.dxh, a.r, a.dr, a.rms);                                    \
     SD_LAUNCHED("k_ln_fwd_reg");                                                                                   \
     return;                                                                                                        \
@@ -939,7 +939,7 @@ void gpt_attn_softmax_fwd(float* Sm, float* dS, float* Ps, float* dPs, int S, lo
     switch (S / 128) {
 #define SD_SMF(NV)                                                                  \
   case NV:                                                                          \
-    k_attn_softmax_fwd_reg<NV><<<g1(rows, 8), 256, 0, s>>>(Sm, dS, rows);           \
+    k_attn_softmax_fwd_reg<NV><<<g1(rows, 4), 128, 0, s>>>(Sm, dS, rows);           \
     SD_LAUNCHED("k_attn_softmax_fwd_reg");                                          \
     return;
       SD_SMF(1) SD_SMF(2) SD_SMF(3) SD_SMF(4) SD_SMF(5) SD_SMF(6) SD_SMF(7) SD_SMF(8)
@@ -956,7 +956,7 @@ void gpt_attn_softmax_bwd(const float* P, const float* dP, float* gP, float* gdP
     switch (S / 128) {
 #define SD_SMBW(NV)                                                                 \
   case NV:                                                                          \
-    k_attn_softmax_bwd_reg<NV><<<g1(rows, 8), 256, 0, s>>>(P, dP, gP, gdP, rows);    \
+    k_attn_softmax_bwd_reg<NV><<<g1(rows, 4), 128, 0, s>>>(P, dP, gP, gdP, rows);    \
     SD_LAUNCHED("k_attn_softmax_bwd_reg");                                          \
     return;
       SD_SMBW(1) SD_SMBW(2) SD_SMBW(3) SD_SMBW(4) SD_SMBW(5) SD_SMBW(6) SD_SMBW(7) SD_SMBW(8)
