@@ -12,6 +12,8 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdlib>
+#include <initializer_list>
 
 #include "sd_common.cuh"
 #include "sd_gpt.h"
@@ -362,6 +364,73 @@ __global__ void k_colred1(const float* __restrict__ a, const float* __restrict__
         out1[col] = acc ? out1[col] + t1 : t1;
       }
     }
+  }
+  if (threadIdx.x == 0) cnt[blockIdx.x] = 0u;
+}
+
+// k_colred1 with 16-byte loads: a CTA covers 128 columns (lane = 4 adjacent
+// columns) x 8 row-lanes, so each load instruction moves 4x the bytes. Every
+// column is summed in exactly k_colred1's order (row-lane strided fold, the 8
+// row-lanes in order, then the row groups in order). Stage 2 runs in the
+// last-arriving CTA: thread t folds one (output, column) over the groups.
+// Needs n % 4 == 0, lda % 4 == 0 and 16-byte aligned operands.
+template <int MODE>
+__global__ void __launch_bounds__(256) k_colred4(const float* __restrict__ a, const float* __restrict__ b,
+                                                 const float* __restrict__ c, const float* __restrict__ e, int T,
+                                                 int n, long long lda, float* __restrict__ part,
+                                                 unsigned* __restrict__ cnt, float* __restrict__ out0,
+                                                 float* __restrict__ out1, int acc) {
+  __shared__ float4 s0[8][32], s1[8][32];
+  __shared__ bool last;
+  const int lane = threadIdx.x & 31, rl = threadIdx.x >> 5;
+  const int col = blockIdx.x * 128 + lane * 4;
+  const int rows = (T + gridDim.y - 1) / gridDim.y;
+  const int r0 = blockIdx.y * rows, r1 = min(T, r0 + rows);
+  float4 x0 = make_float4(0.f, 0.f, 0.f, 0.f), x1 = x0;
+  if (col < n)
+    for (int t = r0 + rl; t < r1; t += 8) {
+      const long long o = ((long long)t * lda + col) >> 2;
+      if (MODE == 0) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(a) + o);
+        x0.x += v.x, x0.y += v.y, x0.z += v.z, x0.w += v.w;
+      } else {  // a = gy, b = gdy, c = xh, e = dxh
+        const float4 va = __ldg(reinterpret_cast<const float4*>(a) + o), vb = __ldg(reinterpret_cast<const float4*>(b) + o);
+        const float4 vc = __ldg(reinterpret_cast<const float4*>(c) + o), ve = __ldg(reinterpret_cast<const float4*>(e) + o);
+        x0.x += vb.x * vc.x + va.x * ve.x, x1.x += vb.x;
+        x0.y += vb.y * vc.y + va.y * ve.y, x1.y += vb.y;
+        x0.z += vb.z * vc.z + va.z * ve.z, x1.z += vb.z;
+        x0.w += vb.w * vc.w + va.w * ve.w, x1.w += vb.w;
+      }
+    }
+  s0[rl][lane] = x0;
+  s1[rl][lane] = x1;
+  __syncthreads();
+  if (rl == 0 && col < n) {
+    float4 t0 = make_float4(0.f, 0.f, 0.f, 0.f), t1 = t0;
+    for (int i = 0; i < 8; ++i) {
+      const float4 u = s0[i][lane], w = s1[i][lane];
+      t0.x += u.x, t0.y += u.y, t0.z += u.z, t0.w += u.w;
+      t1.x += w.x, t1.y += w.y, t1.z += w.z, t1.w += w.w;
+    }
+    reinterpret_cast<float4*>(part + (long long)blockIdx.y * n)[col >> 2] = t0;
+    if (MODE == 1) reinterpret_cast<float4*>(part + (long long)(gridDim.y + blockIdx.y) * n)[col >> 2] = t1;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(&cnt[blockIdx.x], 1u) == gridDim.y - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const int groups = gridDim.y;
+  const int which = threadIdx.x >> 7;  // 0: out0, 1: out1
+  const int cc = blockIdx.x * 128 + (threadIdx.x & 127);
+  if ((MODE == 1 || which == 0) && cc < n && (which == 0 || out1)) {
+    const float* p = part + (long long)which * groups * n + cc;
+    float t = 0.f;
+#pragma unroll 8
+    for (int g = 0; g < groups; ++g) t += __ldcg(p + (long long)g * n);
+    float* o = which ? out1 : out0;
+    o[cc] = acc ? o[cc] + t : t;  // acc: micro-batch accumulation (pipeline stages)
   }
   if (threadIdx.x == 0) cnt[blockIdx.x] = 0u;
 }
@@ -891,6 +960,19 @@ void gpt_ln_fwd(const LnArgs& a, cudaStream_t s) {
   SD_LAUNCHED("k_ln_fwd");
 }
 
+// 16-byte path of the column reductions (k_colred4): n and lda multiples of 4,
+// operands 16-byte aligned; SD_COLRED1=1 forces the scalar kernel (A/B)
+static bool colred4_ok(int n, long long lda, std::initializer_list<const float*> ps) {
+  static const bool off = [] {
+    const char* e = std::getenv("SD_COLRED1");
+    return e && e[0] == '1';
+  }();
+  if (off || (n & 3) || (lda & 3)) return false;
+  for (const float* p : ps)
+    if (reinterpret_cast<uintptr_t>(p) & 15) return false;
+  return true;
+}
+
 void gpt_ln_bwd(const LnBwdArgs& a, cudaStream_t s) {
   bool done = false;
 #define SD_LNB(NV)                                                                                                 \
@@ -908,6 +990,13 @@ void gpt_ln_bwd(const LnBwdArgs& a, cudaStream_t s) {
     SD_LAUNCHED("k_ln_bwd");
   }
   const int groups = std::min(kRowGroups, std::max(1, a.T / 64));
+  if (colred4_ok(a.d, a.d, {a.gy, a.gdy, a.xh, a.dxh})) {
+    k_colred4<1><<<dim3(unsigned((a.d + 127) / 128), unsigned(groups)), 256, 0, s>>>(
+        a.gy, a.gdy, a.xh, a.dxh, a.T, a.d, a.d, a.scratch + kColredReserve, reinterpret_cast<unsigned*>(a.scratch),
+        a.hv_g, a.hv_b, a.acc);
+    SD_LAUNCHED("k_colred4");
+    return;
+  }
   k_colred1<1><<<dim3(unsigned((a.d + 31) / 32), unsigned(groups)), 256, 0, s>>>(
       a.gy, a.gdy, a.xh, a.dxh, a.T, a.d, a.d, a.scratch + kColredReserve, reinterpret_cast<unsigned*>(a.scratch),
       a.hv_g, a.hv_b, a.acc);
@@ -916,6 +1005,13 @@ void gpt_ln_bwd(const LnBwdArgs& a, cudaStream_t s) {
 
 void gpt_colsum(const float* a, int T, int n, long long lda, float* out, float* scratch, cudaStream_t s, int acc) {
   const int groups = std::min(kRowGroups, std::max(1, T / 64));
+  if (colred4_ok(n, lda, {a})) {
+    k_colred4<0><<<dim3(unsigned((n + 127) / 128), unsigned(groups)), 256, 0, s>>>(
+        a, nullptr, nullptr, nullptr, T, n, lda, scratch + kColredReserve, reinterpret_cast<unsigned*>(scratch), out,
+        nullptr, acc);
+    SD_LAUNCHED("k_colred4");
+    return;
+  }
   k_colred1<0><<<dim3(unsigned((n + 31) / 32), unsigned(groups)), 256, 0, s>>>(
       a, nullptr, nullptr, nullptr, T, n, lda, scratch + kColredReserve, reinterpret_cast<unsigned*>(scratch), out,
       nullptr, acc);
