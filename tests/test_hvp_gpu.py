@@ -214,3 +214,33 @@ def test_bf16_weights_engine(sd, oracle, cfg):
     # non-bf16 parameters are refused
     with pytest.raises(sd.ConfigError):
         gpt.GptHvp(cfg, B, S, theta=th + 1e-3)
+
+
+_AB_SCRIPT = r"""
+import sys, hashlib
+import numpy as np
+sys.path.insert(0, sys.argv[1])
+from paper_2505_11564_b200 import gpt
+cfg = dict(n_layer=2, d=64, n_head=4, ff=256, vocab=96, ctx=64)
+eng = gpt.GptHvp(cfg, 8, 64, init_seed=2, gain_scale=0.1, bias_scale=0.1)
+v = np.random.default_rng(7).standard_normal(eng.P).astype(np.float32).astype(np.float64)
+hv = np.ascontiguousarray(eng.hvp_numpy(v))
+print(hashlib.sha256(hv.tobytes()).hexdigest())
+"""
+
+
+def test_column_reduction_paths_bitwise(sd):
+    """The 16-byte column reductions (k_colred4) sum every column in the scalar
+    kernel's order (k_colred1, forced by SD_COLRED1=1): Hv is bit-identical.
+    T = 512 token rows -> 8 row groups, so the ordered stage-2 fold runs."""
+    import os, subprocess, sys
+    from pathlib import Path
+    root = str(Path(__file__).resolve().parents[1])
+    out = {}
+    for tag, extra in (("vec", {}), ("scalar", {"SD_COLRED1": "1"})):
+        env = dict(os.environ, **extra)
+        r = subprocess.run([sys.executable, "-c", _AB_SCRIPT, root], env=env, capture_output=True, text=True,
+                           timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        out[tag] = r.stdout.strip().splitlines()[-1]
+    assert out["vec"] == out["scalar"], out
