@@ -300,6 +300,13 @@ void prof_end(cudaStream_t s, double flops) {
   p.used += 2;
 }
 bool prof_on() { return prof().on; }
+bool pdl_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("SD_GEMM_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 void prof_tag(const std::string& tag) { prof().next_tag = tag; }
 
 void launch_splitk_reduce(const float* ws, int splits, int zc, const GemmArgs& g, cudaStream_t s) {
@@ -375,6 +382,12 @@ __global__ void __launch_bounds__(kThreadsFor<TA>(), 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
+  // programmatic dependent launch: the set-up above (barriers, TMEM) overlaps
+  // the previous kernel's tail; no global memory is read or written before
+  // the previous grid has completed. Dependents may be scheduled right away
+  // (every CTA of this persistent grid is resident).
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   if (warp == 0) {
     {  // whole warp; elected lane issues (no waterfall loops around TMA)
@@ -689,8 +702,8 @@ void launch(const GemmArgs& g, cudaStream_t s) {
                       std::to_string(zc) + "," + std::to_string(int(A_MN)) + "," + std::to_string(int(B_MN)) + "," +
                       std::to_string(g.causal) + "," + std::to_string(splits) + (dual ? ",2" : ",1");
   prof_begin(s);
-  kern<<<grid, threads, smem, s>>>(maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], maps[6], maps[7], mC,
-                                   mCs, g.K, ep);
+  launch_gemm_kernel(kern, unsigned(grid), unsigned(threads), smem, s, maps[0], maps[1], maps[2], maps[3], maps[4],
+                     maps[5], maps[6], maps[7], mC, mCs, g.K, ep);
   SD_LAUNCHED("k_gemm_tf32");
   if (splits > 1) {
     launch_splitk_reduce(ws, splits, zc, g, s);

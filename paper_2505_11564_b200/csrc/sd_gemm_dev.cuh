@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <string>
+#include <utility>
 
 #include "sd_common.cuh"
 #include "sd_gemm.h"
@@ -435,6 +436,26 @@ void prof_end(cudaStream_t s, double flops);
 void launch_splitk_reduce(const float* ws, int splits, int zc, const GemmArgs& g, cudaStream_t s);
 // CTA-pair (cta_group::2) 256 x 256 tiles (sd_gemm_pair.cu)
 void gemm_pair(const GemmArgs& g, cudaStream_t s);
+
+// GEMM launches carry the programmatic-stream-serialization attribute (PDL):
+// the kernel's prologue may start during the previous kernel's tail and waits
+// (griddepcontrol.wait) before touching global memory. SD_GEMM_PDL=0 turns it off.
+bool pdl_on();
+template <typename... P, typename... A>
+void launch_gemm_kernel(void (*kern)(P...), unsigned grid, unsigned threads, size_t smem, cudaStream_t s,
+                        A&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_on() ? 1 : 0;
+  SD_CUDA(cudaLaunchKernelEx(&cfg, kern, std::forward<A>(args)...));
+}
 
 }  // namespace gk
 }  // namespace sd

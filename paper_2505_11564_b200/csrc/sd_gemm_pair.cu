@@ -170,6 +170,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
   cluster_sync();  // both CTAs' barriers initialised and TMEM allocated
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
+  // programmatic dependent launch: the set-up above (barriers, TMEM) overlaps
+  // the previous kernel's tail; no global memory is read or written before
+  // the previous grid has completed. Dependents may be scheduled right away
+  // (every CTA of this persistent grid is resident).
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   if (warp == 0) {
     {  // whole warp; elected lane issues (no waterfall loops around TMA)
@@ -408,9 +414,8 @@ void launch_pair_t(const GemmArgs& g, cudaStream_t s) {
     if (g.Cs) make_store_map(&mCs, g.Cs, g, 16);
     ep.tma_store = 1;
   }
-  kern<<<grid, kPairThreads, smem, s>>>(maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], maps[6], maps[7], mC, mCs,
-                                        g.K,
-                                        ep);
+  launch_gemm_kernel(kern, unsigned(grid), unsigned(kPairThreads), size_t(smem), s, maps[0], maps[1], maps[2], maps[3],
+                     maps[4], maps[5], maps[6], maps[7], mC, mCs, g.K, ep);
   SD_LAUNCHED("k_gemm_pair");
   if (splits > 1) launch_splitk_reduce(ws, splits, zc, g, s);
   prof_end(s, (dual ? 4.0 : 2.0) * double(g.M) * g.N * g.K * g.Z1 * g.Z2);
