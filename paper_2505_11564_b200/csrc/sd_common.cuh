@@ -29,6 +29,30 @@ void count_launch();
 
 void set_last_error(const std::string& m);
 
+// Programmatic dependent launch (PDL) for the kernels that follow GEMMs: the
+// launch carries cudaLaunchAttributeProgrammaticStreamSerialization and the
+// kernel calls pdl_wait() before its first global-memory access, so its
+// launch overlaps the previous kernel's tail (GEMMs trigger their dependents
+// once every CTA is resident). SD_GEMM_PDL=0 turns it off (gk::pdl_on).
+namespace gk {
+bool pdl_on();
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+template <typename... P, typename... A>
+void launch_pdl(void (*kern)(P...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, A&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = gk::pdl_on() ? 1 : 0;
+  cuda_check(cudaLaunchKernelEx(&cfg, kern, static_cast<P>(args)...), "cudaLaunchKernelEx");
+}
+
 // Every C-ABI body runs inside this guard.
 template <class F>
 sd_status guard(F&& f) {

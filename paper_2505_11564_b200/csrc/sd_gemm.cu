@@ -219,6 +219,7 @@ __global__ void __launch_bounds__(128) k_splitk_reduce(const float* __restrict__
                                                       int N, float* __restrict__ C, long long ldc, long long sc1,
                                                       long long sc2, float alpha, float beta,
                                                       const float* __restrict__ bias, float* __restrict__ Cs, int vec) {
+  pdl_wait();  // PDL: nothing global is touched before the previous kernel completes
   const int col = 4 * (blockIdx.x * blockDim.x + threadIdx.x);
   if (col >= N) return;
   const int row = blockIdx.y, z = blockIdx.z;
@@ -313,7 +314,7 @@ void launch_splitk_reduce(const float* ws, int splits, int zc, const GemmArgs& g
   const bool vec = g.N % 4 == 0 && g.ldc % 4 == 0 && (zc == 1 || (g.sc1 % 4 == 0 && g.sc2 % 4 == 0)) &&
                    (reinterpret_cast<uintptr_t>(g.C) & 15) == 0 && (!g.Cs || (reinterpret_cast<uintptr_t>(g.Cs) & 15) == 0);
   const dim3 grid(unsigned((g.N + 511) / 512), unsigned(g.M), unsigned(zc));
-  k_splitk_reduce<<<grid, 128, 0, s>>>(ws, splits, zc, g.Z1, g.M, g.N, g.C, g.ldc, g.sc1, g.sc2, g.alpha, g.beta, g.bias,
+  launch_pdl(k_splitk_reduce, dim3(grid), dim3(128), 0, s, ws, splits, zc, g.Z1, g.M, g.N, g.C, g.ldc, g.sc1, g.sc2, g.alpha, g.beta, g.bias,
                                        g.Cs, int(vec));
   SD_LAUNCHED("k_splitk_reduce");
 }

@@ -135,6 +135,7 @@ __global__ void __launch_bounds__(128) k_ln_fwd_reg(const float* __restrict__ x,
     const float* __restrict__ vb, int T, float eps, float* __restrict__ h, float* __restrict__ hs,
     float* __restrict__ dh, float* __restrict__ dhs, float* __restrict__ xh, float* __restrict__ dxh,
     float* __restrict__ r_out, float* __restrict__ dr_out, int rms) {
+  pdl_wait();  // PDL: nothing global is touched before the previous kernel completes
   constexpr int d = 128 * NV;
   const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -205,6 +206,7 @@ __global__ void __launch_bounds__(256, NV <= 6 ? 2 : 1) k_ln_bwd_reg(const float
     const float* __restrict__ g, const float* __restrict__ vg, const float* __restrict__ xh,
     const float* __restrict__ dxh, const float* __restrict__ rr, const float* __restrict__ drr, int T,
     float* __restrict__ gx, float* __restrict__ gdx, float* __restrict__ gxs, float* __restrict__ gdxs, int rms) {
+  pdl_wait();  // PDL: nothing global is touched before the previous kernel completes
   constexpr int d = 128 * NV;
   const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -380,6 +382,7 @@ __global__ void __launch_bounds__(256) k_colred4(const float* __restrict__ a, co
                                                  int n, long long lda, float* __restrict__ part,
                                                  unsigned* __restrict__ cnt, float* __restrict__ out0,
                                                  float* __restrict__ out1, int acc) {
+  pdl_wait();  // PDL: nothing global is touched before the previous kernel completes
   __shared__ float4 s0[8][32], s1[8][32];
   __shared__ bool last;
   const int lane = threadIdx.x & 31, rl = threadIdx.x >> 5;
@@ -467,6 +470,7 @@ __global__ void k_gelu_fwd(const float* __restrict__ f, const float* __restrict_
 // arithmetic): more bytes in flight per load instruction
 __global__ void k_gelu_fwd4(const float4* __restrict__ f, const float4* __restrict__ df, float4* __restrict__ u,
                             float4* __restrict__ us, float4* __restrict__ du, float4* __restrict__ dus, long long n4) {
+  pdl_wait();  // PDL: nothing global is touched before the previous kernel completes
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i >= n4) return;
   const float4 fv = __ldg(f + i), dv = __ldg(df + i);
@@ -484,6 +488,7 @@ __global__ void k_gelu_fwd4(const float4* __restrict__ f, const float4* __restri
 // gf = gu g'(f); gdf = gdu g'(f) + gu g''(f) df   (in place over gu, gdu)
 __global__ void k_gelu_bwd(const float* __restrict__ f, const float* __restrict__ df, float* __restrict__ gu,
                            float* __restrict__ gdu, float* __restrict__ gus, float* __restrict__ gdus, long long n) {
+  pdl_wait();  // PDL: nothing global is touched before the previous kernel completes
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i >= n) return;
   float y, d1, d2;
@@ -551,6 +556,7 @@ __global__ void k_attn_softmax_fwd(float* __restrict__ Sm, float* __restrict__ d
 template <int NV>
 __global__ void __launch_bounds__(128) k_attn_softmax_fwd_reg(float* __restrict__ Sm, float* __restrict__ dS,
                                                               long long rows) {
+  pdl_wait();  // PDL: nothing global is touched before the previous kernel completes
   constexpr int S = 128 * NV;
   const long long row = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -616,6 +622,7 @@ template <int NV>
 __global__ void __launch_bounds__(128) k_attn_softmax_bwd_reg(const float* __restrict__ P,
                                                               const float* __restrict__ dP, float* __restrict__ gP,
                                                               float* __restrict__ gdP, long long rows) {
+  pdl_wait();  // PDL: nothing global is touched before the previous kernel completes
   constexpr int S = 128 * NV;
   const long long row = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -966,7 +973,7 @@ void gpt_embed(const int* tok, int T, int S, int d, const float* wte, const floa
 void gpt_ln_fwd(const LnArgs& a, cudaStream_t s) {
 #define SD_LNF(NV)                                                                                                 \
   if (a.d == 128 * NV) {                                                                                           \
-    k_ln_fwd_reg<NV><<<g1(a.T, 4), 128, 0, s>>>(a.x, a.dx, a.g, a.b, a.vg, a.vb, a.T, a.eps, a.h, a.hs, a.dh, a.dhs, \
+    launch_pdl(k_ln_fwd_reg<NV>, dim3(g1(a.T, 4)), dim3(128), 0, s, a.x, a.dx, a.g, a.b, a.vg, a.vb, a.T, a.eps, a.h, a.hs, a.dh, a.dhs, \
                                                 a.xh, a.dxh, a.r, a.dr, a.rms);                                    \
     SD_LAUNCHED("k_ln_fwd_reg");                                                                                   \
     return;                                                                                                        \
@@ -995,7 +1002,7 @@ void gpt_ln_bwd(const LnBwdArgs& a, cudaStream_t s) {
   bool done = false;
 #define SD_LNB(NV)                                                                                                 \
   if (!done && a.d == 128 * NV) {                                                                                  \
-    k_ln_bwd_reg<NV><<<g1(a.T, 8), 256, 0, s>>>(a.gy, a.gdy, a.g, a.vg, a.xh, a.dxh, a.r, a.dr, a.T, a.gx, a.gdx,  \
+    launch_pdl(k_ln_bwd_reg<NV>, dim3(g1(a.T, 8)), dim3(256), 0, s, a.gy, a.gdy, a.g, a.vg, a.xh, a.dxh, a.r, a.dr, a.T, a.gx, a.gdx,  \
                                                 a.gxs, a.gdxs, a.rms);                                             \
     SD_LAUNCHED("k_ln_bwd_reg");                                                                                   \
     done = true;                                                                                                   \
@@ -1009,7 +1016,7 @@ void gpt_ln_bwd(const LnBwdArgs& a, cudaStream_t s) {
   }
   const int groups = std::min(kRowGroups, std::max(1, a.T / 64));
   if (colred4_ok(a.d, a.d, {a.gy, a.gdy, a.xh, a.dxh})) {
-    k_colred4<1><<<dim3(unsigned((a.d + 127) / 128), unsigned(groups)), 256, 0, s>>>(
+    launch_pdl(k_colred4<1>, dim3(dim3(unsigned((a.d + 127) / 128), unsigned(groups))), dim3(256), 0, s, 
         a.gy, a.gdy, a.xh, a.dxh, a.T, a.d, a.d, a.scratch + kColredReserve, reinterpret_cast<unsigned*>(a.scratch),
         a.hv_g, a.hv_b, a.acc);
     SD_LAUNCHED("k_colred4");
@@ -1024,7 +1031,7 @@ void gpt_ln_bwd(const LnBwdArgs& a, cudaStream_t s) {
 void gpt_colsum(const float* a, int T, int n, long long lda, float* out, float* scratch, cudaStream_t s, int acc) {
   const int groups = std::min(kRowGroups, std::max(1, T / 64));
   if (colred4_ok(n, lda, {a})) {
-    k_colred4<0><<<dim3(unsigned((n + 127) / 128), unsigned(groups)), 256, 0, s>>>(
+    launch_pdl(k_colred4<0>, dim3(dim3(unsigned((n + 127) / 128), unsigned(groups))), dim3(256), 0, s, 
         a, nullptr, nullptr, nullptr, T, n, lda, scratch + kColredReserve, reinterpret_cast<unsigned*>(scratch), out,
         nullptr, acc);
     SD_LAUNCHED("k_colred4");
@@ -1042,7 +1049,7 @@ void gpt_gelu_fwd(const float* f, const float* df, float* u, float* us, float* d
                                    reinterpret_cast<uintptr_t>(u) | reinterpret_cast<uintptr_t>(us) |
                                    reinterpret_cast<uintptr_t>(du) | reinterpret_cast<uintptr_t>(dus)) & 15) == 0;
   if (v4) {
-    k_gelu_fwd4<<<g1(n / 4), 256, 0, s>>>(reinterpret_cast<const float4*>(f), reinterpret_cast<const float4*>(df),
+    launch_pdl(k_gelu_fwd4, dim3(g1(n / 4)), dim3(256), 0, s, reinterpret_cast<const float4*>(f), reinterpret_cast<const float4*>(df),
                                           reinterpret_cast<float4*>(u), reinterpret_cast<float4*>(us),
                                           reinterpret_cast<float4*>(du), reinterpret_cast<float4*>(dus), n / 4);
     SD_LAUNCHED("k_gelu_fwd4");
@@ -1054,7 +1061,7 @@ void gpt_gelu_fwd(const float* f, const float* df, float* u, float* us, float* d
 
 void gpt_gelu_bwd(const float* f, const float* df, float* gu, float* gdu, float* gus, float* gdus, long long n,
                   cudaStream_t s) {
-  k_gelu_bwd<<<g1(n), 256, 0, s>>>(f, df, gu, gdu, gus, gdus, n);
+  launch_pdl(k_gelu_bwd, dim3(g1(n)), dim3(256), 0, s, f, df, gu, gdu, gus, gdus, n);
   SD_LAUNCHED("k_gelu_bwd");
 }
 
@@ -1063,7 +1070,7 @@ void gpt_attn_softmax_fwd(float* Sm, float* dS, float* Ps, float* dPs, int S, lo
     switch (S / 128) {
 #define SD_SMF(NV)                                                                  \
   case NV:                                                                          \
-    k_attn_softmax_fwd_reg<NV><<<g1(rows, 4), 128, 0, s>>>(Sm, dS, rows);           \
+    launch_pdl(k_attn_softmax_fwd_reg<NV>, dim3(g1(rows, 4)), dim3(128), 0, s, Sm, dS, rows);           \
     SD_LAUNCHED("k_attn_softmax_fwd_reg");                                          \
     return;
       SD_SMF(1) SD_SMF(2) SD_SMF(3) SD_SMF(4) SD_SMF(5) SD_SMF(6) SD_SMF(7) SD_SMF(8)
@@ -1080,7 +1087,7 @@ void gpt_attn_softmax_bwd(const float* P, const float* dP, float* gP, float* gdP
     switch (S / 128) {
 #define SD_SMBW(NV)                                                                 \
   case NV:                                                                          \
-    k_attn_softmax_bwd_reg<NV><<<g1(rows, 4), 128, 0, s>>>(P, dP, gP, gdP, rows);    \
+    launch_pdl(k_attn_softmax_bwd_reg<NV>, dim3(g1(rows, 4)), dim3(128), 0, s, P, dP, gP, gdP, rows);    \
     SD_LAUNCHED("k_attn_softmax_bwd_reg");                                          \
     return;
       SD_SMBW(1) SD_SMBW(2) SD_SMBW(3) SD_SMBW(4) SD_SMBW(5) SD_SMBW(6) SD_SMBW(7) SD_SMBW(8)
