@@ -217,6 +217,23 @@ class Oracle:
                                                prec, _p(al), _p(be), _pl(info)))
         return {"alphas": al[:info[0]].copy(), "betas": be[:info[1]].copy(), "breakdown": bool(info[2])}
 
+    def lanczos_gpt(self, cfg, theta, tok, tgt, B, S, k_max, eps=-1.0, reorth=True, seed=42, dist=RADEMACHER,
+                    prec=F32, hvp_prec=F64, window=0):
+        """Lanczos (oracle restatement of SPEC.md:257-265) over the oracle's own
+        GPT HVP: the CPU leg of the C1 SLQ parity check."""
+        c = self._cfg(cfg)
+        th = np.ascontiguousarray(theta, np.float64)
+        tok = np.ascontiguousarray(tok, np.uint32)
+        tgt = np.ascontiguousarray(tgt, np.uint32)
+        al = np.zeros(k_max, np.float64)
+        be = np.zeros(k_max, np.float64)
+        info = np.zeros(4, np.int64)
+        self._chk(self.lib.oracle_lanczos_gpt(_pl(c), _p(th), _ll(B), _ll(S), _pu(tok), _pu(tgt), _ll(k_max), _d(eps),
+                                              int(reorth), _ll(window), _ull(seed), dist, prec, hvp_prec, _p(al),
+                                              _p(be), _pl(info)))
+        return {"alphas": al[:info[0]].copy(), "betas": be[:info[1]].copy(), "breakdown": bool(info[2]),
+                "numerical_failure": bool(info[3])}
+
     def ritz(self, alphas, betas):
         al = np.ascontiguousarray(alphas, np.float64)
         be = np.ascontiguousarray(betas, np.float64)

@@ -336,6 +336,44 @@ int oracle_gpt_hvp(const long long* cfg, const double* theta, long long B, long 
   })
 }
 
+// Lanczos (the same restatement as oracle_lanczos_dense)
+// driven by the oracle's own GPT Hessian-vector product (SPEC.md:193-210,
+// PAPER.md Alg. 1): the CPU side of the end-to-end SLQ parity check of
+// BASELINE configs[0]. Vectors in `prec`; the HVP tape runs in `hvp_prec` and
+// its output is rounded to `prec` (round_elem). info as oracle_lanczos_dense.
+int oracle_lanczos_gpt(const long long* cfg, const double* theta, long long B, long long S, const unsigned* tok,
+                       const unsigned* tgt, long long k_max, double eps, int reorth, long long window,
+                       unsigned long long seed, int dist, int prec, int hvp_prec, double* out_alpha, double* out_beta,
+                       long long* info) {
+  ORACLE_TRY({
+    const GptConfig c = gcfg(cfg);
+    const size_t P = gpt_param_count(c);
+    const std::vector<double> th(theta, theta + P);
+    const Batch bt = gbatch(B, S, tok, tgt);
+    LanczosConfig lc;
+    lc.k_max = size_t(k_max);
+    lc.eps = eps;
+    lc.reorth = Reorth(reorth);
+    lc.window = size_t(window);
+    lc.probe.seed = seed;
+    lc.probe.dist = ProbeDist(dist);
+    lc.prec = Precision(prec);
+    const LanczosResult r = lanczos_run(
+        P,
+        [&](const Vec& x, Vec& y) {
+          const auto h = gpt_hvp(c, th, bt, x.x, Precision(hvp_prec));
+          for (size_t i = 0; i < P; ++i) y.x[i] = round_elem(h[i], y.prec);
+        },
+        lc);
+    for (size_t i = 0; i < r.alphas.size(); ++i) out_alpha[i] = r.alphas[i];
+    for (size_t i = 0; i < r.betas.size(); ++i) out_beta[i] = r.betas[i];
+    info[0] = (long long)r.alphas.size();
+    info[1] = (long long)r.betas.size();
+    info[2] = r.breakdown;
+    info[3] = r.numerical_failure;
+  })
+}
+
 // loader: nb batches with sizes Bs[i] (all of length S), tokens concatenated.
 int oracle_gpt_batched_hvp(const long long* cfg, const double* theta, long long nb, const long long* Bs, long long S,
                            const unsigned* tok, const unsigned* tgt, const double* v, int prec, double* out) {

@@ -199,6 +199,23 @@ def test_gpt_hvp_finite_differences_and_torch(oracle):
     assert np.linalg.norm(ht - hv) / np.linalg.norm(hv) < 1e-12
 
 
+@pytest.mark.parametrize("kv", [0, 2])
+def test_torch_llama_restatement_matches_oracle(oracle, kv):
+    # the float64 torch Llama restatement (RMSNorm, rotate-half RoPE, GQA,
+    # SwiGLU, untied head) that pins the GPU engine at S >= 1024 equals the
+    # oracle's Graph HVP (oracle/src/models.cpp build_llama) at small shapes
+    import torch
+    import torch_gpt
+    cfg = dict(n_layer=2, d=64, n_head=8, ff=96, vocab=96, ctx=32, arch=1, rope_base=10000, n_kv_head=kv)
+    th = oracle.gpt_init(cfg, 0, 0.1, 0.1)
+    tok, tgt = oracle.gpt_batch(cfg, 2, 16)
+    v = oracle.draw_probe(th.size, 3, RADEMACHER)
+    hv = oracle.gpt_hvp(cfg, th, tok, tgt, 2, 16, v)
+    ht = torch_gpt.llama_hvp(cfg, torch.tensor(th), torch.tensor(tok.astype(np.int64)),
+                             torch.tensor(tgt.astype(np.int64)), 2, 16, torch.tensor(v)).numpy()
+    assert np.linalg.norm(ht - hv) / np.linalg.norm(hv) < 1e-12
+
+
 def test_gpt_batched_hvp_weighting(oracle):
     # batches of sizes 1 and 3 == one concatenated 4-sample batch, within 1e-10
     P = oracle.gpt_param_count(TINY)
@@ -228,3 +245,22 @@ def test_selective_reorth_sits_between_none_and_full(oracle):
     assert l_full < l_sel < 1e-9 < l_none
     _, rw = lo(2, 26)
     assert np.array_equal(rw["alphas"], rf["alphas"]) and np.array_equal(rw["betas"], rf["betas"])
+
+
+def test_lanczos_over_gpt_hvp_moments(oracle):
+    # the CPU leg of the C1 SLQ parity check (oracle_lanczos_gpt): Gauss
+    # quadrature of its tridiagonal reproduces q0^T H^m q0 for m <= 2k-1
+    # (SPEC.md:348), H applied by the oracle's own HVP in f64
+    import slq_c1
+    cfg, B, S, k = slq_c1.C1, 2, 16, 6
+    th = oracle.gpt_init(cfg, 0, 0.0, 0.0, prec=F64)
+    tok, tgt = oracle.gpt_batch(cfg, B, S)
+    r = oracle.lanczos_gpt(cfg, th, tok, tgt, B, S, k, reorth=True, seed=42, dist=RADEMACHER, prec=F64, hvp_prec=F64)
+    v, w = oracle.ritz(r["alphas"], r["betas"])
+    q0 = oracle.draw_probe(th.size, 42, RADEMACHER, prec=F64)
+    x = q0.copy()
+    for m in range(2 * k):
+        rhs = float(q0 @ x)
+        lhs = float(np.sum(w * v ** m))
+        assert abs(lhs - rhs) <= 1e-8 * float(np.sum(w * np.abs(v) ** m)), m
+        x = oracle.gpt_hvp(cfg, th, tok, tgt, B, S, x, prec=F64)

@@ -224,3 +224,59 @@ def test_lanczos_edge_cases(sd):
     pool = sd.make_pool(32, 1)
     with pytest.raises(sd.LayoutError):
         op.apply(pool, sd.draw_probe(pool, None, F64))
+
+
+_WIDE_REORTH = r"""
+import sys, json
+import numpy as np
+import torch
+sys.path.insert(0, sys.argv[1])
+import paper_2505_11564_b200 as sd
+P, k, prec = int(sys.argv[2]), int(sys.argv[3]), int(sys.argv[4])
+dt = torch.float32 if prec == 0 else torch.float64
+d64 = np.linspace(-3.0, 5.0, P)
+if prec == 0:
+    d64 = d64.astype(np.float32).astype(np.float64)
+d = torch.tensor(d64, dtype=dt, device="cuda")
+cfg = sd.LanczosConfig(k_max=k, reorthogonalize=sd.REORTH_FULL, prec=prec,
+                       probe=sd.ProbeSpec(seed=7, distribution=sd.RADEMACHER))
+r = sd.lanczos_run(sd.diag_operator(d), cfg)
+print(json.dumps({"a": [x.hex() for x in r.alphas.tolist()], "b": [x.hex() for x in r.betas.tolist()]}))
+"""
+
+
+@pytest.mark.parametrize("prec,k,variants", [
+    (F32, 64, ("default", "0", "1000")),
+    (F64, 48, ("default",)),
+])
+def test_lanczos_wide_reorth_bitwise(sd, oracle, prec, k, variants):
+    """Full reorthogonalisation at j >= 40 stored columns over full 1024-blocks
+    (P = 2^21 + 77: 2048 full grid blocks and a ragged tail) -- the path the
+    bench times (k_cgs_update + k_cgs_block<T,false> beyond
+    SD_CGS_FUSED_UPDATE_MAX columns, the fused in-CTA update below it) --
+    bitwise against the oracle's recurrence (reduction.hpp:76-107,
+    SPEC.md:260,284). SD_CGS_FUSED_UPDATE_MAX=0 forces the split kernels at
+    every width, =1000 the fused kernel at every width."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = str(Path(__file__).resolve().parents[1])
+    P = 2 ** 21 + 77
+    d64 = np.linspace(-3.0, 5.0, P)
+    if prec == F32:
+        d64 = d64.astype(np.float32).astype(np.float64)
+    ref = oracle.lanczos_diag(d64, k, reorth=True, seed=7, prec=prec)
+    assert len(ref["alphas"]) == k
+    for var in variants:
+        env = dict(os.environ)
+        if var != "default":
+            env["SD_CGS_FUSED_UPDATE_MAX"] = var
+        r = subprocess.run([sys.executable, "-c", _WIDE_REORTH, root, str(P), str(k), str(prec)], env=env,
+                           capture_output=True, text=True, timeout=900)
+        assert r.returncode == 0, r.stderr[-2000:]
+        got = json.loads(r.stdout.strip().splitlines()[-1])
+        a = np.array([float.fromhex(x) for x in got["a"]])
+        b = np.array([float.fromhex(x) for x in got["b"]])
+        assert np.array_equal(a, ref["alphas"]), (var, np.max(np.abs(a - ref["alphas"])))
+        assert np.array_equal(b, ref["betas"]), (var, np.max(np.abs(b - ref["betas"])))

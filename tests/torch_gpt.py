@@ -87,3 +87,87 @@ def grad(cfg, theta, tok, tgt, B, S):
     L = loss_fn(cfg, th, tok, tgt, B, S)
     (g,) = torch.autograd.grad(L, th)
     return g.detach(), float(L)
+
+
+# ---------------------------------------------------------------- Llama-style
+# Same decoder as oracle/src/models.cpp build_llama: RMSNorm (pre-norm,
+# (mean(x^2) + eps)^-1/2), RoPE rotate-half (theta_i = base^(-2i/dh)), causal
+# softmax attention with grouped-query heads (query head h reads kv head
+# h // (H / KV)), SwiGLU MLP silu(gate) * up with [gate | up] fused columns,
+# untied output head [V][d]; no biases.
+def llama_layout(cfg):
+    V, d, ff, H = cfg["vocab"], cfg["d"], cfg["ff"], cfg["n_head"]
+    KV = cfg.get("n_kv_head") or H
+    kvd = KV * (d // H)
+    out = [("tok_embeddings", (V, d))]
+    for l in range(cfg["n_layer"]):
+        p = f"layers.{l}."
+        out += [(p + "attention_norm.weight", (d,)), (p + "attention.wqkv", (d, d + 2 * kvd)),
+                (p + "attention.wo", (d, d)), (p + "ffn_norm.weight", (d,)),
+                (p + "feed_forward.w_gate_up", (d, 2 * ff)), (p + "feed_forward.w_down", (ff, d))]
+    out += [("norm.weight", (d,)), ("output", (V, d))]
+    return out
+
+
+def llama_loss_fn(cfg, flat, tok, tgt, B, S, eps=1e-5):
+    ps, off = {}, 0
+    for name, shape in llama_layout(cfg):
+        n = math.prod(shape)
+        ps[name] = flat[off:off + n].view(shape)
+        off += n
+    assert off == flat.numel()
+    d, H, ff = cfg["d"], cfg["n_head"], cfg["ff"]
+    KV = cfg.get("n_kv_head") or H
+    dh, G = d // H, H // KV
+    kvd = KV * dh
+    base = float(cfg.get("rope_base", 10000.0))
+    tok = tok.view(B, S).long()
+    tgt = tgt.view(B, S).long()
+    x = ps["tok_embeddings"][tok]
+    half = dh // 2
+    inv = base ** (-2.0 * torch.arange(half, dtype=torch.float64, device=flat.device) / dh)
+    ang = torch.arange(S, dtype=torch.float64, device=flat.device)[:, None] * inv[None, :]
+    cos = torch.cat([ang.cos(), ang.cos()], -1).to(flat.dtype)
+    sin = torch.cat([ang.sin(), ang.sin()], -1).to(flat.dtype)
+    mask = torch.triu(torch.ones(S, S, dtype=torch.bool, device=flat.device), 1)
+
+    def rms(x, g):
+        return x * torch.rsqrt((x * x).mean(-1, keepdim=True) + eps) * g
+
+    def rope(t):  # t: [B, h, S, dh]; (t R)[i] = -t[i + half], (t R)[i + half] = t[i]
+        rot = torch.cat([-t[..., half:], t[..., :half]], -1)
+        return t * cos + rot * sin
+
+    for l in range(cfg["n_layer"]):
+        p = f"layers.{l}."
+        h = rms(x, ps[p + "attention_norm.weight"])
+        qkv = h @ ps[p + "attention.wqkv"]
+        q = qkv[..., :d].reshape(B, S, H, dh).transpose(1, 2)
+        k = qkv[..., d:d + kvd].reshape(B, S, KV, dh).transpose(1, 2)
+        v = qkv[..., d + kvd:].reshape(B, S, KV, dh).transpose(1, 2)
+        q, k = rope(q), rope(k)
+        k = k.repeat_interleave(G, dim=1)
+        v = v.repeat_interleave(G, dim=1)
+        s = (q @ k.transpose(-1, -2)) / math.sqrt(dh)
+        s = s.masked_fill(mask, float("-inf"))
+        o = (torch.softmax(s, -1) @ v).transpose(1, 2).reshape(B, S, d)
+        x = x + o @ ps[p + "attention.wo"]
+        h = rms(x, ps[p + "ffn_norm.weight"])
+        gu = h @ ps[p + "feed_forward.w_gate_up"]
+        gate, up = gu[..., :ff], gu[..., ff:]
+        x = x + (gate * torch.sigmoid(gate) * up) @ ps[p + "feed_forward.w_down"]
+    h = rms(x, ps["norm.weight"])
+    logits = h @ ps["output"].t()
+    return torch.nn.functional.cross_entropy(logits.reshape(B * S, -1), tgt.reshape(-1))
+
+
+def llama_hvp(cfg, theta, tok, tgt, B, S, v):
+    th = theta.detach().clone().requires_grad_(True)
+    L = llama_loss_fn(cfg, th, tok, tgt, B, S)
+    (g,) = torch.autograd.grad(L, th, create_graph=True)
+    (hv,) = torch.autograd.grad((g * v).sum(), th)
+    return hv.detach()
+
+
+def any_hvp(cfg, theta, tok, tgt, B, S, v):
+    return (llama_hvp if cfg.get("arch", 0) == 1 else hvp)(cfg, theta, tok, tgt, B, S, v)
