@@ -11,11 +11,16 @@ Timed: K steps of the probe chain centred on column k_max/2 (probes restart
 every k_max steps), after W warm-up steps.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload c1|c2|c4|c5] [--reduction tree|ordered]
 
 N > 1 (torchrun, one rank per GPU): strong scaling of the same global batch,
-data-sharded HVP (each rank B/N sequences) with an NCCL all-reduce of Hv;
-Lanczos vectors are replicated (identical on every rank after the
-all-reduce), so the recurrence needs no further collective.
+data-sharded HVP (each rank B/N sequences); the Lanczos vectors are
+parameter-sharded by split_evenly(P, N): each apply all-gathers q and
+reduce-scatters Hv into the owners' shards, and every scalar set is one
+all-gather of f64 partials folded in rank order.
+
+The headline timed loop runs with no instrumentation; the GEMM share and
+TF/s come from a separate profiled pass of a few more steps.
 """
 from __future__ import annotations
 
@@ -37,6 +42,33 @@ import numpy as np  # noqa: E402
 MEASURED_PEAKS = ROOT / "MEASURED_PEAKS.json"
 TRAFFIC_FILE = ROOT / "profiles" / "gemm_traffic.json"
 METRIC = "Lanczos steps/sec (HVP+reorth) at 1/2/4/8 B200; HVP/Lanczos roofline fraction"
+
+# model dims of the workloads (plain dicts: the reference arm must not import the product package)
+GPT2_SMALL = dict(n_layer=12, d=768, n_head=12, ff=3072, vocab=50257, ctx=1024)
+C1_MODEL = dict(n_layer=1, d=64, n_head=4, ff=256, vocab=64, ctx=32)
+
+
+def workload_config(args):
+    """The config dict both arms print (identical by construction)."""
+    if args.workload == "c1":
+        return {"workload": "BASELINE configs[0] (C1): SPEC small transformer (1 block, d64, 4 heads, V64), "
+                            "batch 4x32 tokens, 1 Rademacher probe x 32 Lanczos steps, full reorth, fp32",
+                "model": "c1-small-transformer", "global_batch": 4, "seq_len": 32, "k_max": 32,
+                "reorth": "full", "probes": 1}
+    return {"workload": "BASELINE configs[1]: GPT-2-small shape 124M, batch 8x1024 tokens, "
+                        "Rademacher probes, k_max=100, full reorth",
+            "model": "gpt2-small", "params": 124439808, "global_batch": args.batch, "seq_len": args.seq,
+            "k_max": args.k_max, "reorth": "full", "probes": 10}
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def peaks():
@@ -116,74 +148,115 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ CPU side
-def cpu_sample(cfg, B, S, k_mid, reference_primitives: bool):
-    """Bounded CPU sample of one step of the same workload: the HVP of the
-    full GPT-2-small model on 1 x S_s tokens (oracle restatement, f64, all
-    host cores), scaled linearly to B x S tokens, plus the Lanczos recurrence
-    and 2x CGS at full P measured with the compiled reference's own
-    dot/axpy/scale (oracle/_ref) at j = 0 and j = 2 and extrapolated linearly
-    to j = k_mid."""
-    from oracle.pyoracle import Oracle, Reference, nthreads
-    o = Oracle()
-    S_s = 16
+def _hvp_seconds(o, cfg, S):
     th = o.gpt_init(cfg, 0, 0.0, 0.0, prec=0)
-    tok, tgt = o.gpt_batch(cfg, 1, S_s)
+    tok, tgt = o.gpt_batch(cfg, 1, S)
     v = o.draw_probe(th.size, 7, 1, prec=0)
     t0 = time.perf_counter()
-    o.gpt_hvp(cfg, th, tok, tgt, 1, S_s, v)
-    t_hvp = (time.perf_counter() - t0) * (B * S) / S_s
-    P = th.size
-    del th, v
-    kind = "port"
-    if reference_primitives:
-        try:
-            r = Reference()
-            w = nthreads()
-            t_j0 = r.time_recurrence(P, w, 0, 1)
-            t_j2 = r.time_recurrence(P, w, 2, 1)
-            t_rec = t_j0 + (t_j2 - t_j0) / 2.0 * k_mid
-            kind = "reference"
-        except Exception:
-            reference_primitives = False
-    if not reference_primitives:
-        x = o.draw_probe(P, 1, 1, prec=0)
-        y = o.draw_probe(P, 2, 1, prec=0)
+    o.gpt_hvp(cfg, th, tok, tgt, 1, S, v)
+    return time.perf_counter() - t0
+
+
+def cpu_c2_step(B, S, k_mid, seqs=(8, 16), full_recurrence=True):
+    """CPU seconds of one C2 Lanczos step, EXTRAPOLATED from bounded samples:
+    * HVP leg (the oracle's f64 restatement of the Graph HVP -- the reference
+      has no HVP of its own): one sequence at each length in `seqs`
+      on the full GPT-2-small model, fitted with t(S) = a*S + c*S^2 (token
+      work + attention's S^2 term; 3+ lengths add a constant), evaluated at S
+      and scaled by the B sequences of the batch;
+    * recurrence leg (the compiled REFERENCE's own dot/axpy/scale through its
+      WorkerPool on all host cores, oracle/_ref): one step's recurrence + 2x CGS
+      at the full P, timed at j = 0 and j = 2 stored columns, linear in j."""
+    from oracle.pyoracle import Oracle, Reference, nthreads
+    o = Oracle()
+    cfg = GPT2_SMALL
+    ts = [_hvp_seconds(o, cfg, q) for q in seqs]
+    X = np.array([[q, q * q] if len(seqs) < 3 else [1.0, q, q * q] for q in seqs], np.float64)
+    coef = np.linalg.lstsq(X, np.array(ts), rcond=None)[0]
+    x = np.array([S, S * S] if len(seqs) < 3 else [1.0, S, S * S], np.float64)
+    t_hvp = float(x @ coef) * B
+    P = 124439808
+    legs = {"hvp": {"kind": "port", "seconds": t_hvp,
+                    "sample": f"oracle f64 HVP, GPT-2-small, 1 sequence at S={list(seqs)} -> {[round(t, 2) for t in ts]} s, "
+                              f"fit a*S+c*S^2, evaluated at S={S} x {B} sequences"}}
+    try:
+        r = Reference()
+        w = nthreads()
+        P_rec = P if full_recurrence else P // 8
+        t_j0 = r.time_recurrence(P_rec, w, 0, 1)
+        t_j2 = r.time_recurrence(P_rec, w, 2, 1)
+        t_rec = (t_j0 + (t_j2 - t_j0) / 2.0 * k_mid) * (P / P_rec)
+        legs["recurrence"] = {"kind": "reference", "seconds": t_rec,
+                              "sample": f"reference dot/axpy/scale (oracle/_ref WorkerPool, {w} workers) at P={P_rec}, "
+                                        f"j=0 ({t_j0:.2f} s) and j=2 ({t_j2:.2f} s), linear to j={k_mid}"
+                                        + ("" if full_recurrence else f", x{P // P_rec} to P={P}")}
+    except Exception as exc:  # compiled reference unavailable: the oracle's port of the same primitives
+        x1 = o.draw_probe(P // 8, 1, 1, prec=0)
+        y1 = o.draw_probe(P // 8, 2, 1, prec=0)
         t0 = time.perf_counter()
-        o.dot(x, y)
-        o.axpy(-0.5, x, y, 0)
-        per_op = (time.perf_counter() - t0) / 2.0
+        o.dot(x1, y1)
+        o.axpy(-0.5, x1, y1, 0)
+        per_op = (time.perf_counter() - t0) / 2.0 * 8
         t_rec = per_op * (5 + 4 * k_mid)
-    sec = t_hvp + t_rec
-    return {"value": 1.0 / sec, "unit": "steps/s", "cores": nthreads(), "kind": kind,
-            "sample": (f"oracle f64 HVP of the full model on 1x{S_s} tokens scaled x{B * S // S_s} to {B}x{S}; "
-                       f"recurrence + 2xCGS at full P={P} ({'reference dot/axpy/scale' if kind == 'reference' else 'oracle port'})"
-                       f" at j=0,2 extrapolated to j={k_mid}"),
-            "hvp_s": t_hvp, "recurrence_s": t_rec}
+        legs["recurrence"] = {"kind": "port", "seconds": t_rec, "sample": f"oracle dot/axpy at P/8 x8 ({exc})"[:200]}
+    sec = t_hvp + legs["recurrence"]["seconds"]
+    return sec, legs
+
+
+def cpu_baseline_c2(B, S, k_mid):
+    from oracle.pyoracle import nthreads
+    sec, legs = cpu_c2_step(B, S, k_mid, seqs=(8, 16), full_recurrence=False)
+    return {"value": 1.0 / sec, "unit": "steps/s", "cores": nthreads(), "kind": "port", "extrapolated": True,
+            "cpu_model": cpu_model(), "legs": legs,
+            "sample": "one C2 step extrapolated from bounded samples: " + legs["hvp"]["sample"] + "; "
+                      + legs["recurrence"]["sample"]}
+
+
+def cpu_c1_run():
+    """C1 in full on the CPU: the oracle's Lanczos restatement over its own
+    Graph HVP, 1 Rademacher probe x 32 steps, full reorth, f32 vectors."""
+    from oracle.pyoracle import Oracle
+    o = Oracle()
+    th = o.gpt_init(C1_MODEL, 0, 0.0, 0.0, prec=0)
+    tok, tgt = o.gpt_batch(C1_MODEL, 4, 32)
+    t0 = time.perf_counter()
+    r = o.lanczos_gpt(C1_MODEL, th, tok, tgt, 4, 32, 32, reorth=True, seed=42, dist=1, prec=0, hvp_prec=1)
+    sec = time.perf_counter() - t0
+    return sec / len(r["alphas"]), len(r["alphas"])
 
 
 def run_reference(args):
-    """--impl reference: the reference CPU path (compiled reference primitives +
-    oracle HVP restatement; the reference has no HVP) timed on host cores."""
+    """--impl reference: the reference CPU path on the host cores, same
+    metric/config as the GPU arm. C1 is timed in full; C2 is one step
+    extrapolated from bounded samples (extrapolated: true). Never imports the
+    product package."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    from paper_2505_11564_b200.gpt import GPT2_SMALL
-    cfg = GPT2_SMALL
-    k_mid = args.k_max // 2  # same mean reorth width as the GPU arm's timed window
-    # each reference "step" is one bounded CPU sample (~1 min on 8 cores); at
-    # most two are run so the arm ends within a few minutes
-    n = max(1, min(args.steps, 2))
-    steps = [cpu_sample(cfg, args.batch, args.seq, k_mid, True) for _ in range(n)]
-    sec = float(np.mean([1.0 / s["value"] for s in steps]))
+    from oracle.pyoracle import nthreads
+    cfgd = workload_config(args)
+    if args.workload == "c1":
+        per_step, n = cpu_c1_run()
+        sec, extrap = per_step, False
+        cpu = {"kind": "port", "cores": nthreads(), "extrapolated": False, "cpu_model": cpu_model(),
+               "sample": f"C1 in full: oracle Lanczos restatement over its Graph HVP, {n} steps, full reorth, "
+                         f"{per_step * n:.2f} s"}
+        n_steps = n
+    else:
+        k_mid = args.k_max // 2  # the GPU arm's timed window is centred on column k_max/2
+        sec, legs = cpu_c2_step(args.batch, args.seq, k_mid, seqs=(8, 16, 32), full_recurrence=True)
+        extrap = True
+        cpu = {"kind": "port", "cores": nthreads(), "extrapolated": True, "cpu_model": cpu_model(), "legs": legs,
+               "sample": "one C2 step extrapolated from bounded samples: " + legs["hvp"]["sample"] + "; "
+                         + legs["recurrence"]["sample"]}
+        n_steps = 1
     val = 1.0 / sec
-    base = steps[-1]
+    cpu["value"] = val
+    cpu["unit"] = "steps/s"
     line = {"metric": METRIC, "value": val, "unit": "steps/s", "impl": "reference", "n_gpus": args.gpus,
-            "steps": n, "steps_requested": args.steps, "warmup": 0, "ms_per_step": sec * 1e3, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "gpt2-small 124M, synthetic tokens, batch 8x1024, full reorth",
-                       "global_batch": args.batch, "seq_len": args.seq, "k_mid": k_mid},
-            "cpu_baseline": {"value": val, "unit": "steps/s", "cores": base["cores"], "kind": base["kind"],
-                             "sample": base["sample"]},
+            "steps": n_steps, "steps_requested": args.steps, "warmup": 0, "ms_per_step": sec * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64 (HVP) / f32 vectors",
+            "data": "synthetic", "extrapolated": extrap, "config": cfgd, "cpu_baseline": cpu,
             "e2e": {"value": val, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -209,8 +282,10 @@ def run_ours(args):
             dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", local))
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    cfg = gpt.GPT2_SMALL
-    B, S = args.batch, args.seq
+    c1 = args.workload == "c1"
+    cfg = C1_MODEL if c1 else GPT2_SMALL
+    B, S = (4, 32) if c1 else (args.batch, args.seq)
+    k_max = 32 if c1 else args.k_max
     if B % world:
         raise SystemExit(f"global batch {B} not divisible by {world} ranks")
     b_loc = B // world
@@ -225,15 +300,14 @@ def run_ours(args):
     layout = sd.split_evenly(P, world) if use_comm else None
     op = eng.operator(comm, layout=layout)
     P_local = (layout.shard_bounds[rank][1] - layout.shard_bounds[rank][0]) if layout else P
-    lcfg = lambda seed: sd.LanczosConfig(k_max=args.k_max, reorthogonalize=sd.REORTH_FULL, prec=sd.F32,  # noqa: E731
-                                         probe=sd.ProbeSpec(seed=seed, distribution=sd.RADEMACHER))
-    ws_bytes = None
-    state = {"probe": 0, "L": None, "ws": None, "done_probes": 0, "alphas": []}
+    reduction = sd.REDUCE_TREE if args.reduction == "tree" else sd.REDUCE_ORDERED
+    lcfg = lambda seed: sd.LanczosConfig(k_max=k_max, reorthogonalize=sd.REORTH_FULL, prec=sd.F32,  # noqa: E731
+                                         probe=sd.ProbeSpec(seed=seed, distribution=sd.RADEMACHER),
+                                         reduction=reduction)
+    state = {"probe": 42 if c1 else 0, "L": None, "ws": None}
 
     def new_chain():
         if state["L"] is not None:
-            res = state["L"].result()
-            state["alphas"].append(res.alphas)
             state["L"].close()
         state["L"] = sd.Lanczos(op, lcfg(state["probe"]), layout=layout, comm=comm, workspace=state["ws"])
         state["ws"] = state["L"].workspace
@@ -248,16 +322,15 @@ def run_ours(args):
     # untimed: W warm-up steps, then advance the chain so the timed window is
     # centred on k_max/2 -- its mean reorthogonalisation width equals that of
     # a whole k_max chain (full reorth cost grows linearly with the column)
-    advance = max(0, args.k_max // 2 - args.steps // 2 - args.warmup) if args.steps < args.k_max else 0
+    advance = max(0, k_max // 2 - args.steps // 2 - args.warmup) if args.steps < k_max else 0
     for _ in range(args.warmup + advance):
         step()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     L0 = lib()
-    launches0 = L0.sd_launch_count()
     check = sd._lib.check
-    check(L0.sd_gemm_profile_begin())
+    launches0 = L0.sd_launch_count()
     j_first = state["L"].result().alphas.size + 1
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
@@ -270,8 +343,6 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     ms_total = e0.elapsed_time(e1)
-    g_ms, g_fl, g_n = C.c_double(), C.c_double(), C.c_uint64()
-    check(L0.sd_gemm_profile_end(C.byref(g_ms), C.byref(g_fl), C.byref(g_n)))
     launches = L0.sd_launch_count() - launches0
     res = state["L"].result()
     j_last = res.alphas.size
@@ -290,7 +361,6 @@ def run_ours(args):
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    e2 = time.perf_counter()
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     f0.record()
     for _ in range(e2e_steps):
@@ -303,7 +373,21 @@ def run_ours(args):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     e2e_ms = float(t.item())
-    del e2
+
+    # ---- profiled pass (separate from the headline): CUDA events around every
+    # GEMM launch give the GEMM share of the step and its TF/s
+    prof_steps = max(1, min(args.profile_steps, k_max - 2))
+    torch.cuda.synchronize()
+    check(L0.sd_gemm_profile_begin())
+    p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    p0.record()
+    for _ in range(prof_steps):
+        step()
+    p1.record()
+    torch.cuda.synchronize()
+    g_ms, g_fl, g_n = C.c_double(), C.c_double(), C.c_uint64()
+    check(L0.sd_gemm_profile_end(C.byref(g_ms), C.byref(g_fl), C.byref(g_n)))
+    prof_ms = p0.elapsed_time(p1)
 
     hbm, bf16, basis = peaks()
     tf32, tf32_basis, cublas_tf32 = tf32_peak(bf16)
@@ -316,20 +400,23 @@ def run_ours(args):
         except Exception:
             traffic = None
     k_mid = 0.5 * (j_first + j_last)
-    lanczos_bytes = 4.0 * P_local * (7 + 3 * k_mid)
+    # Lanczos bytes per step: tree mode 4 P (3 j + 8) (3 GEMV passes over j
+    # columns + r, scale), ordered mode 4 P (7 + 3 j)
+    lanczos_bytes = 4.0 * P_local * ((3 * k_mid + 8) if reduction == sd.REDUCE_TREE else (7 + 3 * k_mid))
     step_roof_ms = gemm_flops_per_step(cfg, B * S, S) / world / (tc_peak * 1e12) * 1e3 + lanczos_bytes / (hbm * 1e9) * 1e3
+    cfgd = workload_config(args)
     line = {
         "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32 (3xTF32 tensor-core GEMMs, fp32 storage, f64 Lanczos scalars)",
-        "data": "synthetic (counter-keyed tokens, random-init GPT-2-small weights)",
-        "config": {"workload": "BASELINE configs[1]: GPT-2-small shape 124M, batch 8x1024 tokens, "
-                               "Rademacher probes, k_max=100, full reorth",
-                   "model": "gpt2-small", "params": P, "global_batch": B, "seq_len": S, "k_max": args.k_max,
-                   "reorth_columns_timed": [j_first, j_last], "untimed_advance_steps": advance,
-                   "parallelism": (f"dp{world} batch x {world}-way sharded Lanczos (all-gather q, reduce-scatter Hv)"
-                                   if layout is not None else "dp1"),
-                   "l2": "inputs larger than L2 (0.5 GB Lanczos vectors, 45 GB activations)"},
+        "data": "synthetic (counter-keyed tokens, random-init weights)",
+        "config": cfgd,
+        "run": {"reorth_columns_timed": [j_first, j_last], "untimed_advance_steps": advance,
+                "reduction": args.reduction, "parallelism": (f"dp{world} batch x {world}-way sharded Lanczos "
+                                                             f"(all-gather q, reduce-scatter Hv)" if layout is not None
+                                                             else "dp1"),
+                "l2": "inputs larger than L2 (0.5 GB Lanczos vectors, 45 GB activations)" if not c1 else
+                      "C1 fits in L2 (226 KB vectors)"},
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": tc_peak, "unit": "TFLOP/s",
                      "frac": achieved / tc_peak if tc_peak else None, "traffic": traffic,
                      "kernel": "k_gemm_pair + k_gemm_tf32 (3xTF32 tcgen05), all GEMM launches of the step",
@@ -337,19 +424,27 @@ def run_ours(args):
                                   + (f"vs measured cuBLAS TF32 sustained {cublas_tf32:.1f} / 3 = "
                                      f"{cublas_tf32 / 3:.1f} TF/s the frac is {achieved / (cublas_tf32 / 3):.3f}"
                                      if cublas_tf32 else "no cuBLAS TF32 measurement"),
-                     "gemm_share_of_step": (g_ms.value / ms_total) if ms_total else None,
-                     "gemm_launches": int(g_n.value)},
+                     "measured_in": f"separate profiled pass of {prof_steps} steps (events around every GEMM)",
+                     "gemm_share_of_step": (g_ms.value / prof_ms) if prof_ms else None,
+                     "gemm_launches_per_step": int(g_n.value) / prof_steps},
         "roofline_step": {"bound": "tensor+hbm", "roofline_ms": step_roof_ms, "measured_ms": ms_step,
                           "frac": step_roof_ms / ms_step, "lanczos_bytes": lanczos_bytes, "hbm_peak_gbs": hbm},
         "e2e": {"value": 1000.0 / e2e_ms, "unit": "steps/s", "h2d_bytes_per_step": int(2 * tok_pin.numel() * 4),
                 "d2h_bytes_per_step": 16, "steps": e2e_steps},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
-        "lanczos_phase_ms": {"apply": res.ms_apply, "recurrence": res.ms_recurrence, "reorth": res.ms_reorth},
+        "lanczos_phase_ms_total": {"apply": res.ms_apply, "recurrence": res.ms_recurrence, "reorth": res.ms_reorth},
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            line["cpu_baseline"] = cpu_sample(cfg, B, S, int(k_mid), True)
+            if c1:
+                from oracle.pyoracle import nthreads
+                per_step, n = cpu_c1_run()
+                line["cpu_baseline"] = {"value": 1.0 / per_step, "unit": "steps/s", "cores": nthreads(), "kind": "port",
+                                        "extrapolated": False, "cpu_model": cpu_model(),
+                                        "sample": f"C1 in full: oracle Lanczos over its Graph HVP, {n} steps"}
+            else:
+                line["cpu_baseline"] = cpu_baseline_c2(B, S, int(k_mid))
         except Exception as exc:  # the CPU leg must not sink the GPU number
             line["cpu_baseline"] = {"value": None, "error": str(exc)[:200]}
     if rank == 0:
@@ -468,8 +563,13 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--comm", action="store_true", help="use the NCCL/sharded path even on one rank")
-    ap.add_argument("--workload", default="c2", choices=["c2", "c4", "c5"],
-                    help="c2 (default, the metric's config) or the C4/C5 pipeline-parallel workloads")
+    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c4", "c5"],
+                    help="c2 (default, the metric's config), c1 (BASELINE configs[0]) or the C4/C5 "
+                         "pipeline-parallel workloads")
+    ap.add_argument("--reduction", default="tree", choices=["tree", "ordered"],
+                    help="Lanczos reductions: tree (fused GEMV passes, fixed-order tree sums; HVP configs) or "
+                         "ordered (the reference's 1024-block fold, bitwise parity mode)")
+    ap.add_argument("--profile-steps", type=int, default=3, help="steps of the separate GEMM-profiled pass")
     ap.add_argument("--layers", type=int, default=0, help="C4/C5: override the depth (0 = the model's)")
     ap.add_argument("--micro-batches", type=int, default=32, help="C4/C5: micro-batches per HVP")
     args = ap.parse_args()
@@ -477,7 +577,7 @@ def main():
         args.warmup = 3
     if args.impl == "reference":
         run_reference(args)
-    elif args.workload != "c2":
+    elif args.workload in ("c4", "c5"):
         run_pipeline_workload(args)
     else:
         run_ours(args)

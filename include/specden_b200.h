@@ -339,7 +339,12 @@ typedef struct {
   uint64_t probe_seed;
   int probe_dist;
   uint64_t selective_window; /* SD_REORTH_SELECTIVE: columns kept (most recent) */
+  int reduction; /* SD_REDUCE_ORDERED (default): the reference's fixed 1024-block fold, bitwise
+                    (reduction.hpp:30-107); SD_REDUCE_TREE: fused GEMV passes with warp-shuffle +
+                    block reductions in a fixed order (deterministic, tolerance parity; <= 256
+                    stored basis columns) -- the mode for HVP operators */
 } sd_lanczos_config;
+enum { SD_REDUCE_ORDERED = 0, SD_REDUCE_TREE = 1 };
 
 typedef struct {
   uint64_t n_alpha, n_beta;
@@ -367,9 +372,12 @@ sd_status sd_lanczos_begin(sd_operator op, sd_comm comm, const uint64_t* begins,
 sd_status sd_lanczos_step(sd_lanczos L, int* done);
 sd_status sd_lanczos_result(sd_lanczos L, double* alphas, double* betas, sd_lanczos_info* info);
 /* Device pointers: current Lanczos vector q_k and the stored basis
- * (column-major, ld = shard length; *ncols columns; NULL if not stored). */
+ * (column-major, column stride sd_lanczos_basis_ld elements = the shard length
+ * rounded up to 32 so that every column is 128-byte aligned for TMA; *ncols
+ * columns; NULL if not stored). */
 const void* sd_lanczos_current(sd_lanczos L);
 sd_status sd_lanczos_basis(sd_lanczos L, const void** basis, uint64_t* ncols);
+uint64_t sd_lanczos_basis_ld(sd_lanczos L);
 /* loss_of_orthogonality: max_{i!=j} |q_i^T q_j| over the
  * stored basis (full reorth only; state error otherwise), reference dots. */
 sd_status sd_lanczos_orthogonality(sd_lanczos L, double* out);

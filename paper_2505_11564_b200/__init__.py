@@ -10,7 +10,8 @@ from ._lib import lib as _load
 _load()
 
 from .core import *  # noqa: E402,F401,F403
-from .core import (F32, F64, GAUSSIAN, ONE_HOT, RADEMACHER, REORTH_FULL, REORTH_NONE, REORTH_SELECTIVE,  # noqa: E402,F401
+from .core import (F32, F64, GAUSSIAN, ONE_HOT, RADEMACHER, REDUCE_ORDERED, REDUCE_TREE, REORTH_FULL, REORTH_NONE,  # noqa: E402,F401,E501
+                   REORTH_SELECTIVE,
                    Lanczos,
                    LanczosConfig, LanczosResult, OperatorHandle, ProbeSpec, RitzSpectrum, ShardedVector, ShardLayout,
                    WorkerPool)

@@ -62,7 +62,7 @@ i32 = C.c_int
 
 class LanczosConfig(C.Structure):
     _fields_ = [("k_max", u64), ("eps", C.c_double), ("reorth", i32), ("prec", i32), ("probe_seed", u64),
-                ("probe_dist", i32), ("selective_window", u64)]
+                ("probe_dist", i32), ("selective_window", u64), ("reduction", i32)]
 
 
 class LanczosInfo(C.Structure):
@@ -123,6 +123,7 @@ _SIGS = {
     "sd_lanczos_result": (i32, [vp, dp, dp, C.POINTER(LanczosInfo)]),
     "sd_lanczos_current": (vp, [vp]),
     "sd_lanczos_basis": (i32, [vp, C.POINTER(vp), u64p]),
+    "sd_lanczos_basis_ld": (u64, [vp]),
     "sd_lanczos_orthogonality": (i32, [vp, dp]),
     "sd_lanczos_end": (i32, [vp]),
 }

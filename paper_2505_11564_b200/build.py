@@ -24,7 +24,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall", "-Xcompiler", "-ffp-contract=off",
                 "--expt-relaxed-constexpr", f"-I{ROOT / 'include'}", f"-I{CSRC}"]
-SOURCES = ["sd_vector.cu", "sd_host.cu", "sd_lanczos.cu", "sd_gemm.cu", "sd_gemm_pair.cu", "sd_gpt_kernels.cu", "sd_mlp.cu",
+SOURCES = ["sd_vector.cu", "sd_host.cu", "sd_lanczos.cu", "sd_lanczos_tree.cu", "sd_gemm.cu", "sd_gemm_pair.cu", "sd_gpt_kernels.cu", "sd_mlp.cu",
            "sd_gpt.cu"]
 
 

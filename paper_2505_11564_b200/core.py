@@ -29,6 +29,7 @@ from ._lib import (ArgumentError, ConfigError, LayoutError, NumericalError, Prot
 F32, F64 = 0, 1
 GAUSSIAN, RADEMACHER, ONE_HOT = 0, 1, 2
 REORTH_NONE, REORTH_FULL, REORTH_SELECTIVE = 0, 1, 2
+REDUCE_ORDERED, REDUCE_TREE = 0, 1
 _DTYPE = {F32: torch.float32, F64: torch.float64}
 
 
@@ -371,10 +372,13 @@ class LanczosConfig:
     probe: ProbeSpec = field(default_factory=ProbeSpec)
     prec: int = F64
     selective_window: int = 0  # REORTH_SELECTIVE: 2xCGS over the most recent W columns (ring of W)
+    # REDUCE_ORDERED: the reference's 1024-block fold (bitwise parity mode);
+    # REDUCE_TREE: fused GEMV passes with fixed-order tree reductions (HVP operators)
+    reduction: int = 0
 
     def native(self) -> _lib.LanczosConfig:
         return _lib.LanczosConfig(self.k_max, self.eps, self.reorthogonalize, self.prec, self.probe.seed,
-                                  self.probe.distribution, self.selective_window)
+                                  self.probe.distribution, self.selective_window, self.reduction)
 
 
 @dataclass
@@ -437,9 +441,10 @@ class Lanczos:
             nc = C.c_uint64()
             check(lib().sd_lanczos_basis(self.h, C.byref(ptr), C.byref(nc)))
             P = self.layout.shard_bounds[0][1] - self.layout.shard_bounds[0][0]
+            ld = int(lib().sd_lanczos_basis_ld(self.h))
             off = (ptr.value - self.workspace.data_ptr())
             es = 4 if self.cfg.prec == F32 else 8
-            Q = self.workspace[off:off + nc.value * P * es].view(_DTYPE[self.cfg.prec]).view(nc.value, P)
+            Q = self.workspace[off:off + nc.value * ld * es].view(_DTYPE[self.cfg.prec]).view(nc.value, ld)[:, :P]
             res.basis = Q.double().cpu().numpy()
         return res
 

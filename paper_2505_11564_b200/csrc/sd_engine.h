@@ -31,6 +31,16 @@ int comm_size(sd_comm c);
 void operator_apply(sd_operator op, const void* x, void* y, int prec, cudaStream_t s, uint64_t row_begin,
                     uint64_t row_end, const void* x_full);
 bool operator_needs_full(sd_operator op);
+// tree-mode Lanczos passes (sd_lanczos_tree.cu): mode 0 = single-column
+// axpy update + dots over jb columns, 1 = GEMV update + dots, 2 = GEMV update +
+// norm; the per-CTA partial rows live in `part` (tree_part_bytes(n) bytes,
+// followed by the counter the last CTA resets)
+uint64_t tree_part_bytes(uint64_t n);
+void tree_pass(int prec, int mode, const void* Q, uint64_t ldq, int jb, void* r, uint64_t n, const double* coef,
+               int ucol, int xcol, double* part, unsigned* counter, double* out, double* alpha_out, int alpha_col,
+               int post_sqrt, cudaStream_t s);
+void tree_rank_fold(const double* recv, int nranks, int m, double* out, int post_sqrt, double* alpha_out,
+                    int alpha_col, cudaStream_t s);
 // ctx release on sd_operator_destroy (operators the engines create around their contexts)
 void operator_set_dtor(sd_operator op, void (*dtor)(void*));
 }  // namespace sd

@@ -29,8 +29,10 @@ constexpr uint64_t kAlign = 256;
 uint64_t align_up(uint64_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 
 struct Plan {
-  uint64_t P = 0, esize = 0, ncols_alloc = 0, pstride = 0, m_max = 0, maxlen = 0;
-  uint64_t off_Q = 0, off_r = 0, off_xfull = 0, off_send = 0, off_recv = 0, off_scal = 0, total_bytes = 0;
+  uint64_t P = 0, ldq = 0, esize = 0, ncols_alloc = 0, pstride = 0, m_max = 0, maxlen = 0;
+  uint64_t off_Q = 0, off_r = 0, off_xfull = 0, off_send = 0, off_recv = 0, off_scal = 0, off_part = 0,
+           total_bytes = 0;
+  bool tree = false;
 };
 
 Plan make_plan(const uint64_t* begins, const uint64_t* ends, uint64_t total, const sd_lanczos_config* cfg, int nranks,
@@ -43,6 +45,8 @@ Plan make_plan(const uint64_t* begins, const uint64_t* ends, uint64_t total, con
     sd::fail(SD_CONFIG_ERROR, "reorth must be none, full or selective");
   if (cfg->reorth == SD_REORTH_SELECTIVE && cfg->selective_window < 2)
     sd::fail(SD_CONFIG_ERROR, "selective reorthogonalisation needs a window >= 2");
+  if (cfg->reduction != SD_REDUCE_ORDERED && cfg->reduction != SD_REDUCE_TREE)
+    sd::fail(SD_CONFIG_ERROR, "reduction must be ordered or tree");
   if (nranks < 1 || rank < 0 || rank >= nranks) sd::fail(SD_ARGUMENT_ERROR, "bad rank/size");
   uint64_t at = 0;
   for (int r = 0; r < nranks; ++r) {
@@ -53,15 +57,22 @@ Plan make_plan(const uint64_t* begins, const uint64_t* ends, uint64_t total, con
   }
   if (at != total) sd::fail(SD_LAYOUT_ERROR, "shard bounds do not cover total_dim");
   p.P = ends[rank] - begins[rank];
+  p.ldq = (p.P + 31) / 32 * 32;  // 128-byte aligned columns (TMA boxes in tree mode)
   p.esize = cfg->prec == SD_F32 ? 4 : 8;
+  p.tree = cfg->reduction == SD_REDUCE_TREE;
   const bool keep = cfg->reorth == SD_REORTH_FULL;
   const bool sel = cfg->reorth == SD_REORTH_SELECTIVE;
   const uint64_t W = std::min<uint64_t>(cfg->selective_window, cfg->k_max + 1);
   p.ncols_alloc = keep ? cfg->k_max + 1 : (sel ? std::max<uint64_t>(W, 2) : 2);
   p.m_max = keep ? cfg->k_max + 1 : (sel ? std::max<uint64_t>(W, 2) : 1);
+  if (p.tree) {
+    p.m_max = std::max<uint64_t>(p.m_max, 2);
+    if (p.ncols_alloc > 256)
+      sd::fail(SD_CONFIG_ERROR, "tree reduction keeps at most 256 basis columns (k_max <= 255 with full reorth)");
+  }
   uint64_t o = 0;
   p.off_Q = o;
-  o = align_up(o + p.ncols_alloc * p.P * p.esize);
+  o = align_up(o + p.ncols_alloc * p.ldq * p.esize);
   p.off_r = o;
   o = align_up(o + p.P * p.esize);
   p.off_xfull = o;
@@ -72,6 +83,8 @@ Plan make_plan(const uint64_t* begins, const uint64_t* ends, uint64_t total, con
   o = align_up(o + (nranks > 1 ? uint64_t(nranks) * p.m_max * p.pstride * 8 : 0));
   p.off_scal = o;
   o = align_up(o + (4 + 2 * cfg->k_max + 2 * p.m_max) * 8);
+  p.off_part = o;
+  if (p.tree) o = align_up(o + sd::tree_part_bytes(p.P));
   p.total_bytes = o;
   return p;
 }
@@ -102,7 +115,14 @@ struct sd_lanczos_s {
     const uint64_t slot = cfg.reorth == SD_REORTH_FULL ? i
                           : cfg.reorth == SD_REORTH_SELECTIVE ? i % plan.ncols_alloc
                                                               : (i & 1);
-    return ws + plan.off_Q + slot * plan.P * plan.esize;
+    return ws + plan.off_Q + slot * plan.ldq * plan.esize;
+  }
+  uint64_t slot_of(uint64_t i) const {
+    return cfg.reorth == SD_REORTH_FULL ? i : cfg.reorth == SD_REORTH_SELECTIVE ? i % plan.ncols_alloc : (i & 1);
+  }
+  double* part() const { return reinterpret_cast<double*>(ws + plan.off_part); }
+  unsigned* counter() const {
+    return reinterpret_cast<unsigned*>(ws + plan.off_part + sd::tree_part_bytes(plan.P) - 256);
   }
   void* r() const { return ws + plan.off_r; }
   double* send() const { return reinterpret_cast<double*>(ws + plan.off_send); }
@@ -162,8 +182,54 @@ struct sd_lanczos_s {
     ncols = 1;
   }
 
+  // one tree-mode pass over `jb` slots starting at slot 0; m results land in
+  // `out` (rank-ordered fold of the ranks' results when sharded)
+  void tpass(int mode, int jb, int ucol, int xcol, const double* coef, double* out, int m, int post_sqrt,
+             double* alpha_out, int alpha_col, const void* base = nullptr) {
+    const void* Q = base ? base : col(0);
+    if (nranks == 1) {
+      sd::tree_pass(cfg.prec, mode, Q, plan.ldq, jb, r(), plan.P, coef, ucol, xcol, part(), counter(), out, alpha_out,
+                    alpha_col, post_sqrt, s);
+      return;
+    }
+    sd::tree_pass(cfg.prec, mode, Q, plan.ldq, jb, r(), plan.P, coef, ucol, xcol, part(), counter(), send(), nullptr,
+                  -1, 0, s);
+    sd::comm_allgather(comm, send(), recv(), uint64_t(m) * 8, s);
+    sd::tree_rank_fold(recv(), nranks, m, out, post_sqrt, alpha_out, alpha_col, s);
+  }
+
+  void step_tree() {
+    void* q = col(k);
+    SD_CUDA(cudaEventRecord(ev[0], s));
+    apply(q, r());
+    SD_CUDA(cudaEventRecord(ev[1], s));
+    const int up = k > 0 ? int(slot_of(k - 1)) : -1;
+    const double* bcoef = k > 0 ? d_beta() + (k - 1) : nullptr;
+    if (cfg.reorth == SD_REORTH_NONE) {
+      // r -= beta q_{k-1}; dots with {slot 0, slot 1}; alpha = the q_k one
+      const int jb = k > 0 ? 2 : 1;
+      tpass(0, jb, up, -1, bcoef, d_c1(), jb, 0, d_alpha() + k, int(slot_of(k)));
+      SD_CUDA(cudaEventRecord(ev[2], s));
+      // r -= alpha q_k (in f64: the dominant column); beta = ||r||
+      tpass(2, 1, 0, 0, d_alpha() + k, d_beta() + k, 1, 1, nullptr, -1, q);
+    } else {
+      const int jb = int(ncols);
+      tpass(0, jb, up, -1, bcoef, d_c1(), jb, 0, d_alpha() + k, int(slot_of(k)));
+      SD_CUDA(cudaEventRecord(ev[2], s));
+      // first Gram-Schmidt pass: q_k's coefficient (alpha) is the dominant one
+      tpass(1, jb, 0, int(slot_of(k)), d_c1(), d_c2(), jb, 0, nullptr, -1);
+      tpass(2, jb, 0, -1, d_c2(), d_beta() + k, 1, 1, nullptr, -1);
+    }
+    SD_CUDA(cudaEventRecord(ev[3], s));
+  }
+
   void step() {
     if (done) return;
+    if (plan.tree) {
+      step_tree();
+      finish_step();
+      return;
+    }
     const uint64_t B = begin(), E = end();
     void* q = col(k);
     void* qp = k > 0 ? col(k - 1) : nullptr;
@@ -182,14 +248,19 @@ struct sd_lanczos_s {
       sd::axpy_dot(q, r(), nullptr, d_alpha() + k, B, E, total, cfg.prec, nullptr, s);
       SD_CUDA(cudaEventRecord(ev[2], s));
       const uint64_t j = ncols;
-      sd::cgs(col(0), plan.P, j, r(), nullptr, 1, B, E, total, cfg.prec, send(), plan.pstride, s);
+      sd::cgs(col(0), plan.ldq, j, r(), nullptr, 1, B, E, total, cfg.prec, send(), plan.pstride, s);
       reduce(j, d_c1(), 0);
-      sd::cgs(col(0), plan.P, j, r(), d_c1(), 1, B, E, total, cfg.prec, send(), plan.pstride, s);
+      sd::cgs(col(0), plan.ldq, j, r(), d_c1(), 1, B, E, total, cfg.prec, send(), plan.pstride, s);
       reduce(j, d_c2(), 0);
-      sd::cgs(col(0), plan.P, j, r(), d_c2(), 2, B, E, total, cfg.prec, send(), plan.pstride, s);
+      sd::cgs(col(0), plan.ldq, j, r(), d_c2(), 2, B, E, total, cfg.prec, send(), plan.pstride, s);
       reduce(1, d_beta() + k, 1);
     }
     SD_CUDA(cudaEventRecord(ev[3], s));
+    finish_step();
+  }
+
+  // alpha/beta to the host, breakdown test, q_{k+1} = scale(r, 1/beta)
+  void finish_step() {
     SD_CUDA(cudaMemcpyAsync(h_scal, d_alpha() + k, 8, cudaMemcpyDeviceToHost, s));
     SD_CUDA(cudaMemcpyAsync(h_scal + 1, d_beta() + k, 8, cudaMemcpyDeviceToHost, s));
     SD_CUDA(cudaStreamSynchronize(s));
@@ -272,6 +343,7 @@ sd_status sd_lanczos_begin(sd_operator op, sd_comm comm, const uint64_t* begins,
     L->s = (cudaStream_t)s;
     L->eps = cfg->eps > 0 ? cfg->eps : (cfg->prec == SD_F64 ? 1e-12 : 1e-7);
     SD_CUDA(cudaMallocHost(&L->h_scal, 2 * sizeof(double)));
+    if (L->plan.tree) SD_CUDA(cudaMemsetAsync(L->counter(), 0, 256, L->s));
     for (auto& e : L->ev) SD_CUDA(cudaEventCreate(&e));
     L->start();
     *out = L.release();
@@ -303,6 +375,7 @@ sd_status sd_lanczos_result(sd_lanczos L, double* alphas, double* betas, sd_lanc
 }
 
 const void* sd_lanczos_current(sd_lanczos L) { return L ? L->col(L->k) : nullptr; }
+uint64_t sd_lanczos_basis_ld(sd_lanczos L) { return L ? L->plan.ldq : 0; }
 
 sd_status sd_lanczos_basis(sd_lanczos L, const void** basis, uint64_t* ncols) {
   return sd::guard([&] {
@@ -323,7 +396,7 @@ sd_status sd_lanczos_orthogonality(sd_lanczos L, double* out) {
     double worst = 0.0;
     std::vector<double> h(L->plan.m_max);
     for (uint64_t i = 1; i < L->ncols; ++i) {
-      sd::cgs(L->col(0), L->plan.P, i, L->col(i), nullptr, 1, B, E, L->total, L->cfg.prec, L->send(),
+      sd::cgs(L->col(0), L->plan.ldq, i, L->col(i), nullptr, 1, B, E, L->total, L->cfg.prec, L->send(),
               L->plan.pstride, L->s);
       L->reduce(i, L->d_c1(), 0);
       SD_CUDA(cudaMemcpyAsync(h.data(), L->d_c1(), i * sizeof(double), cudaMemcpyDeviceToHost, L->s));
