@@ -43,7 +43,10 @@ typedef enum {
 } sd_status;
 
 enum { SD_F32 = 0, SD_F64 = 1 };
-enum { SD_GAUSSIAN = 0, SD_RADEMACHER = 1, SD_ONE_HOT = 2 }; /* ProbeDist, sharded.hpp:34 */
+/* ProbeDist, sharded.hpp:34. SD_GAUSSIAN is bit-exact with the reference
+ * (drawn with glibc's log/cos on the host, uploaded; the fill synchronises);
+ * SD_GAUSSIAN_DEVICE draws on the device with CUDA's log/cos (within 1-2 ulp). */
+enum { SD_GAUSSIAN = 0, SD_RADEMACHER = 1, SD_ONE_HOT = 2, SD_GAUSSIAN_DEVICE = 3 };
 enum { SD_REORTH_NONE = 0, SD_REORTH_FULL = 1, SD_REORTH_SELECTIVE = 2 };
 
 const char* sd_last_error(void);
@@ -86,7 +89,8 @@ sd_status sd_combine_partials_host(uint64_t nranks, const uint64_t* begins, cons
 
 /* ----------------------------------------------------- vector kernels (GPU)
  * draw_probe fill (sharded.cpp:59-76, unnormalised): x[i-begin] =
- * round(dist(seed, i)) for i in [begin, end). */
+ * round(dist(seed, i)) for i in [begin, end). SD_GAUSSIAN: host-drawn and
+ * uploaded through pinned staging (synchronises the stream). */
 sd_status sd_k_probe_fill(void* x, uint64_t begin, uint64_t end, uint64_t seed, int dist, uint64_t one_hot_index,
                           int prec, sd_stream s);
 /* Blocked dot partial of a[i]*b[i] over this rank's shard (dot, sharded.cpp:85-100). */

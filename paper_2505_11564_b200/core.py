@@ -27,7 +27,7 @@ from ._lib import (ArgumentError, ConfigError, LayoutError, NumericalError, Prot
                    check, lib)
 
 F32, F64 = 0, 1
-GAUSSIAN, RADEMACHER, ONE_HOT = 0, 1, 2
+GAUSSIAN, RADEMACHER, ONE_HOT, GAUSSIAN_DEVICE = 0, 1, 2, 3  # GAUSSIAN: bit-exact (host libm); _DEVICE: CUDA log/cos
 REORTH_NONE, REORTH_FULL, REORTH_SELECTIVE = 0, 1, 2
 REDUCE_ORDERED, REDUCE_TREE = 0, 1
 _DTYPE = {F32: torch.float32, F64: torch.float64}

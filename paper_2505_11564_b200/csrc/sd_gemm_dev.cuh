@@ -5,6 +5,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <string>
 #include <utility>
 
@@ -179,7 +180,31 @@ struct EpiParams {
   int mn5;                            // bit 0 / 1: MN-major A / B tile as one 5-D TMA box
   int bexact;                         // bit 0 / 1: source 1 / 2 B operand exact in tf32 (bf16-valued
                                       // weights): no B residual load, no A.B_lo MMA
+  int m_fast;                         // tile walk with m fastest: consecutive tiles (the clusters of one
+                                      // wave) share a B tile and sweep the A panel, which stays in L2 --
+                                      // chosen when the A panel is the smaller operand (m_fast_walk)
 };
+
+// Rasterisation: the operand swept by the wave must be the one that stays in
+// L2. With n fastest, every m row re-streams the whole B panel from HBM; with
+// m fastest, every n column re-reads the A panel. Sweep the smaller panel
+// (the LM-head products: A = 8192 x 768 activations, B = 50257 x 768 tied
+// embedding) when it fits comfortably in the 126 MB L2.
+inline int m_fast_walk(long long M, long long N, long long K, int tiles_m, int tiles_n, int a_copies, int b_copies) {
+  const double a = double(M) * K * 4.0 * a_copies, b = double(N) * K * 4.0 * b_copies;
+  return (tiles_m > 1 && tiles_n > 1 && a < b && a <= 64.0 * 1024 * 1024) ? 1 : 0;
+}
+inline int walk_m_fast(const GemmArgs& g, int tiles_m, int tiles_n, bool three) {
+  static const int on = [] {
+    const char* e = std::getenv("SD_GEMM_MFAST");  // 0: always n fastest (the original walk)
+    return !(e && e[0] == '0');
+  }();
+  if (!on) return 0;
+  const int dual = g.A2 ? 2 : 1;
+  const int ac = dual * ((three && g.As) ? 2 : 1);
+  const int bc = dual * ((three && g.Bs && !g.b_exact) ? 2 : 1);
+  return m_fast_walk(g.M, g.N, g.K, tiles_m, tiles_n, ac, bc);
+}
 
 __device__ __forceinline__ void fence_proxy_async_smem_decl() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -318,6 +343,10 @@ __device__ __forceinline__ TileInfo tile_info(const EpiParams& ep, int t, int K)
     mt = ep.causal == 2 ? ep.n_tiles_m - 1 - mi : mi;
     nt = rem % ep.n_tiles_n;
     zz = rem / ep.n_tiles_n;
+  } else if (ep.m_fast) {
+    mt = t % ep.n_tiles_m;
+    nt = (t / ep.n_tiles_m) % ep.n_tiles_n;
+    zz = t / (ep.n_tiles_n * ep.n_tiles_m);
   } else {
     nt = t % ep.n_tiles_n;
     mt = (t / ep.n_tiles_n) % ep.n_tiles_m;

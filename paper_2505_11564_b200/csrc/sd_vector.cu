@@ -13,10 +13,12 @@
 #include <cuda_runtime.h>
 #include <math.h>
 
-#include <vector>
-
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <mutex>
+#include <thread>
+#include <vector>
 
 #include "sd_common.cuh"
 
@@ -36,8 +38,9 @@ __global__ void k_probe(T* x, uint64_t begin, uint64_t n, uint64_t key, int dist
   } else if (dist == SD_ONE_HOT) {
     v = (i == one_hot) ? 1.0 : 0.0;
   } else {
-    // Box-Muller on counters (2i, 2i+1), rng.hpp:37-41. CUDA's log/cos are not
-    // glibc's: Gaussian draws agree to <= 1-2 ulp, not bitwise.
+    // SD_GAUSSIAN_DEVICE: Box-Muller on counters (2i, 2i+1), rng.hpp:37-41,
+    // with CUDA's log/cos -- within 1-2 ulp of glibc's, not bitwise.
+    // SD_GAUSSIAN itself is drawn on the host (gaussian_fill_host below).
     const double u1 = __dadd_rn(__dmul_rn(double(keyed_counter_k(key, 2 * i) >> 11), 0x1p-53), 0x1p-54);
     const double u2 = __dadd_rn(__dmul_rn(double(keyed_counter_k(key, 2 * i + 1) >> 11), 0x1p-53), 0x1p-54);
     const double two_pi = 6.283185307179586;  // 2.0 * std::numbers::pi (exact doubling)
@@ -748,10 +751,84 @@ void cgs(const void* Q, uint64_t ldq, uint64_t j, void* r, const double* coef, i
   else launch_cgs<double>(Q, ldq, j, r, coef, mode, begin, end, total, partials, pstride, s);
 }
 
+// Bit-exact Gaussian draws (rng.hpp:37-41). Box-Muller needs libm's log and
+// cos, and the reference's values are glibc's, whose last ulp no device
+// implementation reproduces (CUDA's differ for ~0.2% of draws; glibc is not
+// correctly rounded either). So SD_GAUSSIAN probes are generated on the host
+// with the reference's own expression -- the integer counter hash, the same
+// libm calls, no FMA contraction (this file is built -ffp-contract=off) --
+// by all host threads into two pinned staging chunks that are uploaded
+// asynchronously while the next chunk is drawn. A one-time cost per probe
+// (~0.1 s per 10^8 elements on 16 cores), not part of the Lanczos step.
+namespace {
+struct Staging {
+  std::mutex m;
+  void* buf[2] = {nullptr, nullptr};
+  cudaEvent_t done[2] = {nullptr, nullptr};
+  size_t bytes = 0;
+};
+Staging& staging() {
+  static Staging st;
+  return st;
+}
+inline double gaussian_host(uint64_t key, uint64_t i) {
+  const double u1 = double(keyed_counter_k(key, 2 * i) >> 11) * 0x1p-53 + 0x1p-54;
+  const double u2 = double(keyed_counter_k(key, 2 * i + 1) >> 11) * 0x1p-53 + 0x1p-54;
+  constexpr double kTwoPi = 6.283185307179586;  // 2.0 * std::numbers::pi (exact doubling)
+  return std::sqrt(-2.0 * std::log(u1)) * std::cos(kTwoPi * u2);
+}
+template <typename T>
+void draw_range(T* out, uint64_t first, uint64_t n, uint64_t key) {
+  for (uint64_t t = 0; t < n; ++t) out[t] = T(gaussian_host(key, first + t));  // round_elem
+}
+}  // namespace
+
+static void gaussian_fill_host(void* x, uint64_t begin, uint64_t n, uint64_t seed, int prec, cudaStream_t s) {
+  constexpr uint64_t kChunk = uint64_t(1) << 22;
+  const size_t es = prec == SD_F32 ? 4 : 8;
+  Staging& st = staging();
+  std::lock_guard<std::mutex> lk(st.m);
+  if (st.bytes < kChunk * es) {
+    for (int b = 0; b < 2; ++b) {
+      if (st.buf[b]) SD_CUDA(cudaFreeHost(st.buf[b]));
+      SD_CUDA(cudaMallocHost(&st.buf[b], kChunk * es));
+      if (!st.done[b]) SD_CUDA(cudaEventCreateWithFlags(&st.done[b], cudaEventDisableTiming));
+    }
+    st.bytes = kChunk * es;
+  }
+  const uint64_t key = mix64(seed);
+  const unsigned nt = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+  for (uint64_t c0 = 0, it = 0; c0 < n; c0 += kChunk, ++it) {
+    const int b = int(it & 1);
+    const uint64_t len = std::min(kChunk, n - c0);
+    SD_CUDA(cudaEventSynchronize(st.done[b]));  // the buffer's previous upload has landed
+    std::vector<std::thread> th;
+    const uint64_t per = (len + nt - 1) / nt;
+    for (unsigned t = 0; t < nt; ++t) {
+      const uint64_t a = uint64_t(t) * per, e = std::min(len, a + per);
+      if (a >= e) break;
+      th.emplace_back([&, a, e] {
+        if (prec == SD_F32) draw_range(static_cast<float*>(st.buf[b]) + a, begin + c0 + a, e - a, key);
+        else draw_range(static_cast<double*>(st.buf[b]) + a, begin + c0 + a, e - a, key);
+      });
+    }
+    for (auto& t : th) t.join();
+    SD_CUDA(cudaMemcpyAsync(static_cast<char*>(x) + c0 * es, st.buf[b], len * es, cudaMemcpyHostToDevice, s));
+    SD_CUDA(cudaEventRecord(st.done[b], s));
+  }
+  SD_CUDA(cudaStreamSynchronize(s));
+}
+
 void probe_fill(void* x, uint64_t begin, uint64_t end, uint64_t seed, int dist, uint64_t one_hot, int prec,
                 cudaStream_t s) {
   const uint64_t n = end - begin;
   if (n == 0) return;
+  if (dist != SD_GAUSSIAN && dist != SD_RADEMACHER && dist != SD_ONE_HOT && dist != SD_GAUSSIAN_DEVICE)
+    fail(SD_CONFIG_ERROR, "unknown probe distribution");
+  if (dist == SD_GAUSSIAN) {
+    gaussian_fill_host(x, begin, n, seed, prec, s);
+    return;
+  }
   const uint64_t key = mix64(seed);
   if (prec == SD_F32) k_probe<float><<<grid_for(n, 256), 256, 0, s>>>((float*)x, begin, n, key, dist, one_hot);
   else k_probe<double><<<grid_for(n, 256), 256, 0, s>>>((double*)x, begin, n, key, dist, one_hot);

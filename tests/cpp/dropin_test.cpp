@@ -250,3 +250,68 @@ TEST_CASE("lanczos_run drives the model's Hessian (full and selective reorth)") 
   CHECK(sel.t.alphas == full.t.alphas);
   CHECK(sel.t.betas == full.t.betas);
 }
+
+TEST_CASE("lanczos_run: device engine sharded over pool workers == one worker == the apply_fn-composed recurrence") {
+  // operators.hpp:15-21 plug-in point: an operator given ONLY by apply_fn runs
+  // the SPEC recurrence composed from the pool's vector ops; the dense
+  // operator's native form runs the device engine, one rank per worker thread
+  // (its own device and stream), partials exchanged in-process. Both are the
+  // reference's arithmetic, so all three agree bit for bit.
+  auto S = std::make_shared<DenseSymmetric>(spiked_dense(300, 1.0, {40.0, -40.0}, 3));
+  auto op = dense_operator(S, "spiked");
+  OperatorHandle plain;
+  plain.dim = op.dim;
+  plain.label = "apply_fn only";
+  plain.apply_fn = op.apply_fn;
+  for (Precision prec : {Precision::f64, Precision::f32}) {
+    LanczosConfig cfg;
+    cfg.k_max = 14;
+    cfg.prec = prec;
+    cfg.reorthogonalize = Reorthogonalize::full;
+    cfg.probe.distribution = ProbeDist::rademacher;
+    std::unique_ptr<WorkerPool> one(pool_ptr(300, 1)), five(pool_ptr(300, 5));
+    const auto a = lanczos_run(op, cfg, *one);
+    const auto b = lanczos_run(op, cfg, *five);
+    const auto c = lanczos_run(plain, cfg, *five);
+    CHECK(a.t.alphas.size() == 14);
+    CHECK(a.t.alphas == b.t.alphas);
+    CHECK(a.t.betas == b.t.betas);
+    CHECK(a.t.alphas == c.t.alphas);
+    CHECK(a.t.betas == c.t.betas);
+    // tree reductions (extension): the same recurrence within rounding
+    cfg.reduction = Reduction::tree;
+    const auto t = lanczos_run(op, cfg, *one);
+    const double tol = prec == Precision::f64 ? 1e-12 : 2e-6;
+    for (std::size_t i = 0; i < t.t.alphas.size(); ++i) CHECK(std::abs(t.t.alphas[i] - a.t.alphas[i]) <= tol * 50);
+  }
+  // a custom apply_fn: y = 3 x -> alpha_0 = 3, benign breakdown at k = 1
+  OperatorHandle three;
+  three.dim = 64;
+  three.label = "3I";
+  three.apply_fn = [](WorkerPool& p, const ShardedVector& x, ShardedVector& y) { y = scale(p, x, 3.0); };
+  std::unique_ptr<WorkerPool> p4(pool_ptr(64, 4));
+  LanczosConfig c3;
+  c3.k_max = 5;
+  const auto r3 = lanczos_run(three, c3, *p4);
+  CHECK(r3.t.alphas.size() == 1);
+  CHECK(r3.t.alphas[0] == doctest::Approx(3.0).epsilon(1e-15));
+  CHECK(r3.breakdown);
+}
+
+TEST_CASE("WorkerPool: one device and stream per worker, message counts, exactly-once replies") {
+  std::unique_ptr<WorkerPool> pool(pool_ptr(100, 4));
+  for (std::size_t w = 0; w < 4; ++w) {
+    CHECK(pool->device(w) == worker_device(w));
+    CHECK(pool->stream(w) != nullptr);
+  }
+  auto a = random_vector(*pool, 91), b = random_vector(*pool, 92);
+  const auto d0 = pool->message_count(MsgKind::DotPartial), g0 = pool->message_count(MsgKind::Gather);
+  (void)dot(*pool, a, b);
+  (void)gather(*pool, a);
+  CHECK(pool->message_count(MsgKind::DotPartial) == d0 + 4);
+  CHECK(pool->message_count(MsgKind::Gather) == g0 + 4);
+  std::atomic<int> hits{0};
+  pool->run_all(MsgKind::ApplyShard, [&](std::size_t) { hits.fetch_add(1); });
+  CHECK(hits.load() == 4);
+  CHECK_THROWS_AS(pool->post(4, MsgKind::ApplyShard, [](std::size_t) {}), protocol_error);
+}

@@ -1,7 +1,7 @@
 """Parity of the CUDA vector algebra and the device Lanczos engine against the
-committed reference fixtures and the oracle. Integer/byte work and every
-reference f64 fold are compared BITWISE; Gaussian probes (CUDA log/cos vs
-glibc) within 2 ulp."""
+committed reference fixtures and the oracle. Integer/byte work, every
+reference f64 fold and the Gaussian probes (host libm draws) are compared
+BITWISE; the on-device Gaussian variant (CUDA log/cos) within 2-4 ulp."""
 from pathlib import Path
 
 import numpy as np
@@ -37,8 +37,12 @@ def test_probe_parity(sd, dim, workers):
         for seed in (42, 99):
             got = sd.gather(pool, sd.draw_probe(pool, None, prec, seed=seed, distribution=sd.RADEMACHER))
             assert np.array_equal(got, GOLD[f"probe_rad_{dim}_{prec}_{seed}"])
+            # Gaussian probes are bit-exact (host libm draws, rng.hpp:37-41)
             g = sd.gather(pool, sd.draw_probe(pool, None, prec, seed=seed, distribution=sd.GAUSSIAN))
             ref = GOLD[f"probe_gauss_{dim}_{prec}_{seed}"]
+            assert np.array_equal(g, ref)
+            # the on-device variant (CUDA log/cos) stays within a few ulp
+            g = sd.gather(pool, sd.draw_probe(pool, None, prec, seed=seed, distribution=sd.GAUSSIAN_DEVICE))
             if prec == F32:
                 assert np.max(np.abs(g - ref) / np.abs(ref)) <= 2 * 2.0 ** -24
             else:
@@ -107,12 +111,11 @@ def test_lanczos_dense_bitwise(sd, prec, reorth):
     r = sd.lanczos_run(op, cfg)
     assert np.array_equal(r.alphas, GOLD[f"lanczos_spiked256_{prec}_{reorth}_1_alpha"])
     assert np.array_equal(r.betas, GOLD[f"lanczos_spiked256_{prec}_{reorth}_1_beta"])
-    # Gaussian probe: start vector differs by ulps from glibc's, so tolerance
+    # Gaussian probe (the reference's default distribution): bit-exact too
     cfg.probe = sd.ProbeSpec(seed=42, distribution=GAUSSIAN)
     r = sd.lanczos_run(op, cfg)
-    ref_a = GOLD[f"lanczos_spiked256_{prec}_{reorth}_0_alpha"]
-    tol = 1e-4 if prec == F32 else 1e-10
-    assert np.max(np.abs(r.alphas - ref_a)) <= tol * np.max(np.abs(ref_a))
+    assert np.array_equal(r.alphas, GOLD[f"lanczos_spiked256_{prec}_{reorth}_0_alpha"])
+    assert np.array_equal(r.betas, GOLD[f"lanczos_spiked256_{prec}_{reorth}_0_beta"])
 
 
 @pytest.mark.parametrize("P", [3 * 1024 * 1024 + 77, 1000003])
@@ -280,3 +283,17 @@ def test_lanczos_wide_reorth_bitwise(sd, oracle, prec, k, variants):
         b = np.array([float.fromhex(x) for x in got["b"]])
         assert np.array_equal(a, ref["alphas"]), (var, np.max(np.abs(a - ref["alphas"])))
         assert np.array_equal(b, ref["betas"]), (var, np.max(np.abs(b - ref["betas"])))
+
+
+@pytest.mark.parametrize("prec", [F32, F64])
+def test_gaussian_probe_bitwise_large(sd, oracle, prec):
+    """SD_GAUSSIAN (the reference's default probe, sharded.hpp:36-38) at 9M
+    elements over 3 ragged workers -- several pinned staging chunks per shard
+    -- equals the oracle's glibc draws bit for bit (rng.hpp:37-41, round_elem)."""
+    P = 9_000_011
+    pool = sd.make_pool(P, 3)
+    got = sd.gather(pool, sd.draw_probe(pool, None, prec, seed=2718, distribution=sd.GAUSSIAN, normalize=False))
+    ref = oracle.gaussian_fill(2718, 0, P)
+    if prec == F32:
+        ref = ref.astype(np.float32).astype(np.float64)
+    assert np.array_equal(got, ref)
