@@ -40,7 +40,9 @@ sys.path.insert(0, str(ROOT))
 import numpy as np  # noqa: E402
 
 MEASURED_PEAKS = ROOT / "MEASURED_PEAKS.json"
-TRAFFIC_FILE = ROOT / "profiles" / "gemm_traffic.json"
+# measured per-launch DRAM bytes of the GEMMs (tools/gemm_traffic.py: ncu over every GEMM launch of one
+# HVP at the bench shape) next to their algorithmic bytes
+TRAFFIC_FILE = ROOT / "profiles" / "r02_gemm_traffic.json"
 METRIC = "Lanczos steps/sec (HVP+reorth) at 1/2/4/8 B200; HVP/Lanczos roofline fraction"
 
 # model dims of the workloads (plain dicts: the reference arm must not import the product package)
@@ -157,28 +159,32 @@ def _hvp_seconds(o, cfg, S):
     return time.perf_counter() - t0
 
 
-def cpu_c2_step(B, S, k_mid, seqs=(8, 16), full_recurrence=True):
+def cpu_c2_step(B, S, k_mid, seqs=(8, 64), full_recurrence=True):
     """CPU seconds of one C2 Lanczos step, EXTRAPOLATED from bounded samples:
     * HVP leg (the oracle's f64 restatement of the Graph HVP -- the reference
-      has no HVP of its own): one sequence at each length in `seqs`
-      on the full GPT-2-small model, fitted with t(S) = a*S + c*S^2 (token
-      work + attention's S^2 term; 3+ lengths add a constant), evaluated at S
-      and scaled by the B sequences of the batch;
+      has no HVP of its own): one sequence of the full GPT-2-small
+      model at each length in `seqs`, fitted with t = c0 + k * F(S), F the
+      algorithmic flops of that sequence (gemm_flops_per_step: 16 N_mm S for
+      the weight products + 36 L H S^2 dh for attention, so the S^2 term is
+      carried by the model, not by a fit of noisy small-S timings) and c0 the
+      token-independent part (weight-sized tape work); evaluated at B
+      sequences of length S: c0 + k * F(B x S);
     * recurrence leg (the compiled REFERENCE's own dot/axpy/scale through its
       WorkerPool on all host cores, oracle/_ref): one step's recurrence + 2x CGS
-      at the full P, timed at j = 0 and j = 2 stored columns, linear in j."""
+      at the full P (or P/8, scaled x8), timed at j = 0 and j = 2 stored
+      columns, linear in j."""
     from oracle.pyoracle import Oracle, Reference, nthreads
     o = Oracle()
     cfg = GPT2_SMALL
     ts = [_hvp_seconds(o, cfg, q) for q in seqs]
-    X = np.array([[q, q * q] if len(seqs) < 3 else [1.0, q, q * q] for q in seqs], np.float64)
-    coef = np.linalg.lstsq(X, np.array(ts), rcond=None)[0]
-    x = np.array([S, S * S] if len(seqs) < 3 else [1.0, S, S * S], np.float64)
-    t_hvp = float(x @ coef) * B
+    F = [gemm_flops_per_step(cfg, q, q) for q in seqs]
+    k = max((ts[-1] - ts[0]) / (F[-1] - F[0]), 0.0)
+    c0 = max(ts[0] - k * F[0], 0.0)
+    t_hvp = c0 + k * gemm_flops_per_step(cfg, B * S, S)
     P = 124439808
-    legs = {"hvp": {"kind": "port", "seconds": t_hvp,
-                    "sample": f"oracle f64 HVP, GPT-2-small, 1 sequence at S={list(seqs)} -> {[round(t, 2) for t in ts]} s, "
-                              f"fit a*S+c*S^2, evaluated at S={S} x {B} sequences"}}
+    legs = {"hvp": {"kind": "port", "seconds": t_hvp, "c0_s": c0, "s_per_tflop": k * 1e12,
+                    "sample": f"oracle f64 HVP, GPT-2-small, 1 sequence at S={list(seqs)} -> "
+                              f"{[round(t, 2) for t in ts]} s, t = c0 + k*flops(S), evaluated at {B}x{S} tokens"}}
     try:
         r = Reference()
         w = nthreads()
@@ -205,7 +211,7 @@ def cpu_c2_step(B, S, k_mid, seqs=(8, 16), full_recurrence=True):
 
 def cpu_baseline_c2(B, S, k_mid):
     from oracle.pyoracle import nthreads
-    sec, legs = cpu_c2_step(B, S, k_mid, seqs=(8, 16), full_recurrence=False)
+    sec, legs = cpu_c2_step(B, S, k_mid, seqs=(8, 64), full_recurrence=False)
     return {"value": 1.0 / sec, "unit": "steps/s", "cores": nthreads(), "kind": "port", "extrapolated": True,
             "cpu_model": cpu_model(), "legs": legs,
             "sample": "one C2 step extrapolated from bounded samples: " + legs["hvp"]["sample"] + "; "
@@ -244,7 +250,7 @@ def run_reference(args):
         n_steps = n
     else:
         k_mid = args.k_max // 2  # the GPU arm's timed window is centred on column k_max/2
-        sec, legs = cpu_c2_step(args.batch, args.seq, k_mid, seqs=(8, 16, 32), full_recurrence=True)
+        sec, legs = cpu_c2_step(args.batch, args.seq, k_mid, seqs=(8, 128), full_recurrence=True)
         extrap = True
         cpu = {"kind": "port", "cores": nthreads(), "extrapolated": True, "cpu_model": cpu_model(), "legs": legs,
                "sample": "one C2 step extrapolated from bounded samples: " + legs["hvp"]["sample"] + "; "
@@ -393,10 +399,11 @@ def run_ours(args):
     tf32, tf32_basis, cublas_tf32 = tf32_peak(bf16)
     tc_peak = tf32 / 3.0  # 3xTF32: 3 tf32 MMAs per algorithmic product
     achieved = g_fl.value / (g_ms.value * 1e-3) / 1e12 if g_ms.value > 0 else 0.0
-    traffic = None
-    if TRAFFIC_FILE.exists():
+    traffic = alg_bytes = None
+    if TRAFFIC_FILE.exists() and not c1:
         try:
-            traffic = json.loads(TRAFFIC_FILE.read_text()).get("bytes_per_launch")
+            tj = json.loads(TRAFFIC_FILE.read_text())
+            traffic, alg_bytes = tj.get("bytes_per_launch"), tj.get("algorithmic_bytes_per_launch")
         except Exception:
             traffic = None
     k_mid = 0.5 * (j_first + j_last)
@@ -419,6 +426,8 @@ def run_ours(args):
                       "C1 fits in L2 (226 KB vectors)"},
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": tc_peak, "unit": "TFLOP/s",
                      "frac": achieved / tc_peak if tc_peak else None, "traffic": traffic,
+                     "algorithmic_bytes": alg_bytes,
+                     "traffic_source": "profiles/r02_gemm_traffic.json (ncu dram bytes per GEMM launch, one HVP)",
                      "kernel": "k_gemm_pair + k_gemm_tf32 (3xTF32 tcgen05), all GEMM launches of the step",
                      "peak_note": f"3xTF32 roofline = {tf32_basis} ({basis}) = {tf32:.1f} TF/s / 3 (passes); "
                                   + (f"vs measured cuBLAS TF32 sustained {cublas_tf32:.1f} / 3 = "

@@ -671,7 +671,7 @@ void launch(const GemmArgs& g, cudaStream_t s) {
   }
   ep.tma_store = tma_store ? 1 : 0;
   ep.mn5 = mn5;
-  if (!g.causal) ep.m_fast = walk_m_fast(g, tm, tn, THREE);
+  if (!g.causal) ep.group = walk_group(g, BM, BN, tm, tn, THREE);
   ep.bexact = (g.b_exact ? 1 : 0) | (g.b2_exact ? 2 : 0);
   auto kern = g.causal ? k_gemm_tf32<A_MN, B_MN, THREE, BN, true> : k_gemm_tf32<A_MN, B_MN, THREE, BN, false>;
   int threads = NUM_THREADS;

@@ -109,9 +109,8 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t* v) {
 template <int PN>
 __device__ __forceinline__ TileInfo pair_tile(const EpiParams& ep, int t, int K) {
   TileInfo ti;
-  const int nt = ep.m_fast ? (t / ep.n_tiles_m) % ep.n_tiles_n : t % ep.n_tiles_n;
-  const int mt = ep.m_fast ? t % ep.n_tiles_m : (t / ep.n_tiles_n) % ep.n_tiles_m;
-  const int zz = t / (ep.n_tiles_n * ep.n_tiles_m);
+  int mt, nt, zz;
+  walk_tile(ep, t, mt, nt, zz);
   ti.n0 = nt * PN;
   ti.m0 = mt * kPairM;
   ti.z = zz % ep.zcount;
@@ -400,7 +399,7 @@ void launch_pair_t(const GemmArgs& g, cudaStream_t s) {
   if (splits > 1) ws = splitk_workspace(size_t(splits) * zc * size_t(g.M) * g.N);
   EpiParams ep{g.C, g.ldc, g.sc1, g.sc2, g.M, g.N, g.Z1, g.alpha, g.beta, g.bias, g.Cs, g.dbg, zc, kb_per, ws,
                0, tn, tm, tiles * splits, dual ? 2 : 1, g.onchip ? 1 : 0};
-  ep.m_fast = walk_m_fast(g, tm, tn, THREE);
+  ep.group = walk_group(g, kPairM, PN, tm, tn, THREE);
   const int grid = 2 * std::min(ep.n_tiles, clusters);
   if (prof_on())
     prof_tag(std::to_string(g.M) + "," + std::to_string(g.N) + "," + std::to_string(g.K) + "," + std::to_string(zc) +
