@@ -48,6 +48,11 @@ METRIC = "Lanczos steps/sec (HVP+reorth) at 1/2/4/8 B200; HVP/Lanczos roofline f
 # model dims of the workloads (plain dicts: the reference arm must not import the product package)
 GPT2_SMALL = dict(n_layer=12, d=768, n_head=12, ff=3072, vocab=50257, ctx=1024)
 C1_MODEL = dict(n_layer=1, d=64, n_head=4, ff=256, vocab=64, ctx=32)
+# BASELINE configs[2] (C3): SURVEY 8 proposal -- 1.3B GPT-2-architecture decoder (24L, d2048, ff8192, V50257,
+# ctx2048, tied head), 32 x 2048 = 65,536 tokens per HVP, data-sharded over the ranks in micro-batches of
+# 1 x 2048 (optionally with recomputation); Lanczos vectors parameter-sharded, selective reorth over the 16
+# newest columns (full reorth with the sharded basis from N >= 4)
+C3_MODEL = dict(n_layer=24, d=2048, n_head=16, ff=8192, vocab=50257, ctx=2048)
 
 
 def workload_config(args):
@@ -57,6 +62,12 @@ def workload_config(args):
                             "batch 4x32 tokens, 1 Rademacher probe x 32 Lanczos steps, full reorth, fp32",
                 "model": "c1-small-transformer", "global_batch": 4, "seq_len": 32, "k_max": 32,
                 "reorth": "full", "probes": 1}
+    if args.workload == "c3":
+        return {"workload": "BASELINE configs[2] (C3): 1.3B GPT-2-architecture decoder (24L d2048 ff8192 V50257), "
+                            "32x2048 tokens per HVP data-sharded in 1x2048 micro-batches, "
+                            f"k_max={args.k_max}, {args.c3_reorth} reorth",
+                "model": "c3-1.3b", "params": 1315723264, "global_batch": 32, "seq_len": 2048,
+                "micro_batch": 1, "k_max": args.k_max, "reorth": args.c3_reorth, "probes": 1}
     return {"workload": "BASELINE configs[1]: GPT-2-small shape 124M, batch 8x1024 tokens, "
                         "Rademacher probes, k_max=100, full reorth",
             "model": "gpt2-small", "params": 124439808, "global_batch": args.batch, "seq_len": args.seq,
@@ -288,9 +299,9 @@ def run_ours(args):
             dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", local))
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    c1 = args.workload == "c1"
-    cfg = C1_MODEL if c1 else GPT2_SMALL
-    B, S = (4, 32) if c1 else (args.batch, args.seq)
+    c1, c3 = args.workload == "c1", args.workload == "c3"
+    cfg = C1_MODEL if c1 else (C3_MODEL if c3 else GPT2_SMALL)
+    B, S = (4, 32) if c1 else ((32, 2048) if c3 else (args.batch, args.seq))
     k_max = 32 if c1 else args.k_max
     if B % world:
         raise SystemExit(f"global batch {B} not divisible by {world} ranks")
@@ -298,7 +309,12 @@ def run_ours(args):
     T_glob = B * S
     tok_all, tgt_all = gpt.synthetic_tokens(cfg["vocab"], B, S, seed=1)
     sl = slice(rank * b_loc * S, (rank + 1) * b_loc * S)
-    eng = gpt.GptHvp(cfg, b_loc, S, init_seed=0, tokens=tok_all[sl], targets=tgt_all[sl], loss_scale=1.0 / T_glob)
+    if c3:  # b_loc sequences as micro-batches of one sequence, layers recomputed in the backward
+        eng = gpt.GptHvp(cfg, 1, S, init_seed=0, tokens=tok_all[sl], targets=tgt_all[sl], loss_scale=1.0 / T_glob,
+                         micro_batches=b_loc, recompute=args.c3_recompute)
+    else:
+        eng = gpt.GptHvp(cfg, b_loc, S, init_seed=0, tokens=tok_all[sl], targets=tgt_all[sl],
+                         loss_scale=1.0 / T_glob)
     comm = sd.nccl_comm() if use_comm else None
     P = eng.P
     # N > 1: Lanczos vectors parameter-sharded over the ranks (split_evenly);
@@ -307,9 +323,11 @@ def run_ours(args):
     op = eng.operator(comm, layout=layout)
     P_local = (layout.shard_bounds[rank][1] - layout.shard_bounds[rank][0]) if layout else P
     reduction = sd.REDUCE_TREE if args.reduction == "tree" else sd.REDUCE_ORDERED
-    lcfg = lambda seed: sd.LanczosConfig(k_max=k_max, reorthogonalize=sd.REORTH_FULL, prec=sd.F32,  # noqa: E731
+    reorth = sd.REORTH_SELECTIVE if (c3 and args.c3_reorth == "selective") else sd.REORTH_FULL
+    window = args.window if reorth == sd.REORTH_SELECTIVE else 0
+    lcfg = lambda seed: sd.LanczosConfig(k_max=k_max, reorthogonalize=reorth, prec=sd.F32,  # noqa: E731
                                          probe=sd.ProbeSpec(seed=seed, distribution=sd.RADEMACHER),
-                                         reduction=reduction)
+                                         reduction=reduction, selective_window=window)
     state = {"probe": 42 if c1 else 0, "L": None, "ws": None}
 
     def new_chain():
@@ -400,7 +418,7 @@ def run_ours(args):
     tc_peak = tf32 / 3.0  # 3xTF32: 3 tf32 MMAs per algorithmic product
     achieved = g_fl.value / (g_ms.value * 1e-3) / 1e12 if g_ms.value > 0 else 0.0
     traffic = alg_bytes = None
-    if TRAFFIC_FILE.exists() and not c1:
+    if TRAFFIC_FILE.exists() and not c1 and not c3:
         try:
             tj = json.loads(TRAFFIC_FILE.read_text())
             traffic, alg_bytes = tj.get("bytes_per_launch"), tj.get("algorithmic_bytes_per_launch")
@@ -409,7 +427,8 @@ def run_ours(args):
     k_mid = 0.5 * (j_first + j_last)
     # Lanczos bytes per step: tree mode 4 P (3 j + 8) (3 GEMV passes over j
     # columns + r, scale), ordered mode 4 P (7 + 3 j)
-    lanczos_bytes = 4.0 * P_local * ((3 * k_mid + 8) if reduction == sd.REDUCE_TREE else (7 + 3 * k_mid))
+    j_eff = min(k_mid, window) if window else k_mid
+    lanczos_bytes = 4.0 * P_local * ((3 * j_eff + 8) if reduction == sd.REDUCE_TREE else (7 + 3 * j_eff))
     step_roof_ms = gemm_flops_per_step(cfg, B * S, S) / world / (tc_peak * 1e12) * 1e3 + lanczos_bytes / (hbm * 1e9) * 1e3
     cfgd = workload_config(args)
     line = {
@@ -422,8 +441,11 @@ def run_ours(args):
                 "reduction": args.reduction, "parallelism": (f"dp{world} batch x {world}-way sharded Lanczos "
                                                              f"(all-gather q, reduce-scatter Hv)" if layout is not None
                                                              else "dp1"),
-                "l2": "inputs larger than L2 (0.5 GB Lanczos vectors, 45 GB activations)" if not c1 else
-                      "C1 fits in L2 (226 KB vectors)"},
+                "l2": ("C1 fits in L2 (226 KB vectors)" if c1 else
+                       "inputs larger than L2 (Lanczos vectors >= 0.5 GB, activations >= 10 GB)"),
+                "memory_gb": {"hvp_workspace": eng.workspace.numel() / 1e9,
+                              "lanczos_workspace": state["ws"].numel() / 1e9,
+                              "device_peak": torch.cuda.max_memory_allocated() / 1e9}},
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": tc_peak, "unit": "TFLOP/s",
                      "frac": achieved / tc_peak if tc_peak else None, "traffic": traffic,
                      "algorithmic_bytes": alg_bytes,
@@ -444,7 +466,7 @@ def run_ours(args):
         "clocks": clk.summary(),
         "lanczos_phase_ms_total": {"apply": res.ms_apply, "recurrence": res.ms_recurrence, "reorth": res.ms_reorth},
     }
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not c3:
         try:
             if c1:
                 from oracle.pyoracle import nthreads
@@ -572,7 +594,12 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--comm", action="store_true", help="use the NCCL/sharded path even on one rank")
-    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c4", "c5"],
+    ap.add_argument("--c3-reorth", default="selective", choices=["selective", "full"],
+                    help="C3: selective (window --window, fits one GPU) or full (sharded basis, N >= 4)")
+    ap.add_argument("--window", type=int, default=16, help="selective reorth window (C3)")
+    ap.add_argument("--c3-recompute", action="store_true",
+                    help="C3: keep only layer inputs, re-run layers in the backward (less memory, ~1/3 more flops)")
+    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5"],
                     help="c2 (default, the metric's config), c1 (BASELINE configs[0]) or the C4/C5 "
                          "pipeline-parallel workloads")
     ap.add_argument("--reduction", default="tree", choices=["tree", "ordered"],

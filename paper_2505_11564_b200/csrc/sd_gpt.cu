@@ -315,120 +315,154 @@ struct sd_gpt_s {
   const float* th(int i) const { return theta + (slots[i].off - pbase); }
   const float* ths(int i) const { return theta_s ? theta_s + (slots[i].off - pbase) : nullptr; }
 
+  // Hv of the batch: the whole model as a one-stage pipeline -- begin, then
+  // forward + backward of each micro-batch (Hv of micro-batches after the
+  // first accumulates: GEMM beta = 1, accumulate flags of the column and
+  // embedding reductions; Alg. 1's h += u b over the loader)
   void hvp(const float* v, float* hv, cudaStream_t st) {
-    if (!have_batch) fail(SD_STATE_ERROR, "gpt: set_batch was not called");
-    if (c.arch == SD_ARCH_LLAMA) return hvp_llama(v, hv, st);
-    const int d = c.d, ff = c.ff, V = c.vocab;
-    const long long Td = (long long)T * d;
-    const float sc = 1.0f / std::sqrt(float(dh));
-    auto V_ = [&](int i) { return v + slots[i].off; };
-    auto Vs = [&](int i) { return v_s + slots[i].off; };
-    auto HV = [&](int i) { return hv + slots[i].off; };
-    sd::gpt_residual(v, v_s, P, st);
-    // ------------------------------------------------------------ forward
-    sd::gpt_embed(tok, T, S, d, th(0), th(1), V_(0), V_(1), x, dx, st);
-    for (int l = 0; l < c.n_layer; ++l) {
-      Layer& Ly = L[l];
-      const int b = 2 + 12 * l;  // slot index of h{l}.ln_1.weight
-      sd::LnArgs la{x, dx, th(b), th(b + 1), V_(b), V_(b + 1), T, d, 1e-5f,
-                    Ly.h1, Ly.h1s, Ly.dh1, Ly.dh1s, Ly.xh1, Ly.dxh1, Ly.r1, Ly.dr1};
-      sd::gpt_ln_fwd(la, st);
-      // qkv = h Wa + ba ; dqkv = dh Wa + h VWa + Vba
-      mm(T, 3 * d, d, {Ly.h1, Ly.h1s, d, false}, Wt(b + 2, 3 * d, true), Ly.a, 3 * d, 1, 0, st,
-         th(b + 3), Ly.as);
-      mm2(T, 3 * d, d, {Ly.dh1, Ly.dh1s, d, false}, Wt(b + 2, 3 * d, true), {Ly.h1, Ly.h1s, d, false},
-          {V_(b + 2), Vs(b + 2), 3 * d, true}, Ly.da, 3 * d, 1, 0, st, V_(b + 3), Ly.das);
-      attention_fwd(Ly, sc, st);
-      // x += o Wp + bp ; dx += do Wp + o VWp + Vbp
-      mm(T, d, d, {Ly.o, Ly.os, d, false}, Wt(b + 4, d, true), x, d, 1, 1, st, th(b + 5));
-      mm2(T, d, d, {Ly.dO, Ly.dOs, d, false}, Wt(b + 4, d, true), {Ly.o, Ly.os, d, false},
-          {V_(b + 4), Vs(b + 4), d, true}, dx, d, 1, 1, st, V_(b + 5));
-      sd::LnArgs lb{x, dx, th(b + 6), th(b + 7), V_(b + 6), V_(b + 7), T, d, 1e-5f,
-                    Ly.h2, Ly.h2s, Ly.dh2, Ly.dh2s, Ly.xh2, Ly.dxh2, Ly.r2, Ly.dr2};
-      sd::gpt_ln_fwd(lb, st);
-      mm(T, ff, d, {Ly.h2, Ly.h2s, d, false}, Wt(b + 8, ff, true), Ly.f, ff, 1, 0, st, th(b + 9));
-      mm2(T, ff, d, {Ly.dh2, Ly.dh2s, d, false}, Wt(b + 8, ff, true), {Ly.h2, Ly.h2s, d, false},
-          {V_(b + 8), Vs(b + 8), ff, true}, Ly.df, ff, 1, 0, st, V_(b + 9));
-      sd::gpt_gelu_fwd(Ly.f, Ly.df, Ly.u, Ly.us, Ly.du, Ly.dus, (long long)T * ff, st);
-      mm(T, d, ff, {Ly.u, Ly.us, ff, false}, Wt(b + 10, d, true), x, d, 1, 1, st, th(b + 11));
-      mm2(T, d, ff, {Ly.du, Ly.dus, ff, false}, Wt(b + 10, d, true), {Ly.u, Ly.us, ff, false},
-          {V_(b + 10), Vs(b + 10), d, true}, dx, d, 1, 1, st, V_(b + 11));
+    stage_begin(v, hv, st);
+    for (int m = 0; m < nmb; ++m) {
+      if (c.arch == SD_ARCH_LLAMA) {
+        stage_fwd(m, st);
+        stage_bwd(m, st);
+      } else {
+        gpt2_fwd(m, st);
+        gpt2_bwd(m, st);
+      }
     }
+  }
+
+  // ---- GPT-2 block (pre-LN, biases, GELU, learned positions, tied head).
+  // Whole-model stage only (the tied embedding is read by the first and the
+  // last layer); micro-batches and SD_GPT_RECOMPUTE as for the Llama family.
+  void gpt2_fwd(int m, cudaStream_t st) {
+    use_set(m);
+    sd::gpt_embed(tok + (long long)m * T, T, S, c.d, th(0), th(1), V_(0), V_(1), x, dx, st);
+    const size_t xb = 2ull * size_t(T) * c.d * sizeof(float);
+    for (int l = 0; l < c.n_layer; ++l) {
+      if (recompute) {
+        SD_CUDA(cudaMemcpyAsync(XIN[set_of(m)][l], x, xb, cudaMemcpyDeviceToDevice, st));
+        gpt2_layer_fwd(Lscratch, l, x, dx, st);
+      } else {
+        gpt2_layer_fwd(L[l], l, x, dx, st);
+      }
+    }
+  }
+
+  void gpt2_layer_fwd(Layer& Ly, int l, float* x, float* dx, cudaStream_t st) {
+    const int d = c.d, ff = c.ff;
+    const float sc = 1.0f / std::sqrt(float(dh));
+    const int b = 2 + 12 * l;  // slot index of h{l}.ln_1.weight
+    sd::LnArgs la{x, dx, th(b), th(b + 1), V_(b), V_(b + 1), T, d, 1e-5f,
+                  Ly.h1, Ly.h1s, Ly.dh1, Ly.dh1s, Ly.xh1, Ly.dxh1, Ly.r1, Ly.dr1};
+    sd::gpt_ln_fwd(la, st);
+    // qkv = h Wa + ba ; dqkv = dh Wa + h VWa + Vba
+    mm(T, 3 * d, d, {Ly.h1, Ly.h1s, d, false}, Wt(b + 2, 3 * d, true), Ly.a, 3 * d, 1, 0, st, th(b + 3), Ly.as);
+    mm2(T, 3 * d, d, {Ly.dh1, Ly.dh1s, d, false}, Wt(b + 2, 3 * d, true), {Ly.h1, Ly.h1s, d, false},
+        {V_(b + 2), Vs(b + 2), 3 * d, true}, Ly.da, 3 * d, 1, 0, st, V_(b + 3), Ly.das);
+    attention_fwd(Ly, sc, st);
+    // x += o Wp + bp ; dx += do Wp + o VWp + Vbp
+    mm(T, d, d, {Ly.o, Ly.os, d, false}, Wt(b + 4, d, true), x, d, 1, 1, st, th(b + 5));
+    mm2(T, d, d, {Ly.dO, Ly.dOs, d, false}, Wt(b + 4, d, true), {Ly.o, Ly.os, d, false},
+        {V_(b + 4), Vs(b + 4), d, true}, dx, d, 1, 1, st, V_(b + 5));
+    sd::LnArgs lb{x, dx, th(b + 6), th(b + 7), V_(b + 6), V_(b + 7), T, d, 1e-5f,
+                  Ly.h2, Ly.h2s, Ly.dh2, Ly.dh2s, Ly.xh2, Ly.dxh2, Ly.r2, Ly.dr2};
+    sd::gpt_ln_fwd(lb, st);
+    mm(T, ff, d, {Ly.h2, Ly.h2s, d, false}, Wt(b + 8, ff, true), Ly.f, ff, 1, 0, st, th(b + 9));
+    mm2(T, ff, d, {Ly.dh2, Ly.dh2s, d, false}, Wt(b + 8, ff, true), {Ly.h2, Ly.h2s, d, false},
+        {V_(b + 8), Vs(b + 8), ff, true}, Ly.df, ff, 1, 0, st, V_(b + 9));
+    sd::gpt_gelu_fwd(Ly.f, Ly.df, Ly.u, Ly.us, Ly.du, Ly.dus, (long long)T * ff, st);
+    mm(T, d, ff, {Ly.u, Ly.us, ff, false}, Wt(b + 10, d, true), x, d, 1, 1, st, th(b + 11));
+    mm2(T, d, ff, {Ly.du, Ly.dus, ff, false}, Wt(b + 10, d, true), {Ly.u, Ly.us, ff, false},
+        {V_(b + 10), Vs(b + 10), d, true}, dx, d, 1, 1, st, V_(b + 11));
+  }
+
+  void gpt2_bwd(int m, cudaStream_t st) {
+    const int d = c.d, V = c.vocab;
+    const long long Td = (long long)T * d;
+    const float hb = m > 0 ? 1.0f : 0.0f;  // beta of the Hv products
+    use_set(m);
+    acc = m > 0;
     const int fL = 2 + 12 * c.n_layer;
     sd::LnArgs lf{x, dx, th(fL), th(fL + 1), V_(fL), V_(fL + 1), T, d, 1e-5f, hf, hfs, dhf, dhfs, xhf, dxhf, rf, drf};
     sd::gpt_ln_fwd(lf, st);
     // logits z = hf wte^T ; dz = dhf wte^T + hf Vwte^T
     mm(T, V, d, {hf, hfs, d, false}, Wt(0, d, false), z, Vp, 1, 0, st);
-    mm2(T, V, d, {dhf, dhfs, d, false}, Wt(0, d, false), {hf, hfs, d, false}, {V_(0), Vs(0), d, false}, dz,
-        Vp, 1, 0, st);
-    sd::gpt_ce(z, dz, zs, dz == nullptr ? nullptr : dzs, tgt, T, V, Vp, loss_scale, loss_rows, st);
-    // ----------------------------------------------------------- backward
-    // ghf = gz wte ; gdhf = gdz wte + gz Vwte ; Hv_wte(head) = gdz^T hf + gz^T dhf
+    mm2(T, V, d, {dhf, dhfs, d, false}, Wt(0, d, false), {hf, hfs, d, false}, {V_(0), Vs(0), d, false}, dz, Vp, 1, 0,
+        st);
+    sd::gpt_ce(z, dz, zs, dzs, tgt + (long long)m * T, T, V, Vp, loss_scale, loss_rows + (long long)m * T, st);
+    // ghf = gz wte ; gdhf = gdz wte + gz Vwte ; Hv_wte(head) (+)= gdz^T hf + gz^T dhf
     mm(T, d, V, {z, zs, Vp, false}, Wt(0, d, true), gh, d, 1, 0, st);
-    mm2(T, d, V, {dz, dzs, Vp, false}, Wt(0, d, true), {z, zs, Vp, false}, {V_(0), Vs(0), d, true}, gdh, d,
-        1, 0, st);
-    mm2(V, d, T, {dz, dzs, Vp, true}, {hf, hfs, d, true}, {z, zs, Vp, true}, {dhf, dhfs, d, true}, HV(0), d, 1, 0, st);
-    SD_CUDA(cudaMemsetAsync(gx, 0, Td * sizeof(float), st));
-    SD_CUDA(cudaMemsetAsync(gdx, 0, Td * sizeof(float), st));
-    sd::LnBwdArgs bf{gh, gdh, th(fL), V_(fL), xhf, dxhf, rf, drf, T, d, gx, gdx, gxs, gdxs, HV(fL), HV(fL + 1), red};
+    mm2(T, d, V, {dz, dzs, Vp, false}, Wt(0, d, true), {z, zs, Vp, false}, {V_(0), Vs(0), d, true}, gdh, d, 1, 0, st);
+    mm2(V, d, T, {dz, dzs, Vp, true}, {hf, hfs, d, true}, {z, zs, Vp, true}, {dhf, dhfs, d, true}, HV(0), d, 1, hb,
+        st);
+    SD_CUDA(cudaMemsetAsync(gx, 0, 2 * Td * sizeof(float), st));
+    sd::LnBwdArgs bf{gh, gdh, th(fL), V_(fL), xhf, dxhf, rf, drf, T, d, gx, gdx, gxs, gdxs, HV(fL), HV(fL + 1), red, 0,
+                     int(acc)};
     sd::gpt_ln_bwd(bf, st);
     for (int l = c.n_layer - 1; l >= 0; --l) {
-      Layer& Ly = L[l];
-      const int b = 2 + 12 * l;
-      // MLP out: gu = gx Wq^T ; gdu = gdx Wq^T + gx VWq^T ; Hv_Wq = du^T gx + u^T gdx
-      mm(T, ff, d, {gx, gxs, d, false}, Wt(b + 10, d, false), gu, ff, 1, 0, st);
-      mm2(T, ff, d, {gdx, gdxs, d, false}, Wt(b + 10, d, false), {gx, gxs, d, false},
-          {V_(b + 10), Vs(b + 10), d, false}, gdu, ff, 1, 0, st);
-      mm2(ff, d, T, {Ly.du, Ly.dus, ff, true}, {gx, gxs, d, true}, {Ly.u, Ly.us, ff, true}, {gdx, gdxs, d, true},
-          HV(b + 10), d, 1, 0, st);
-      sd::gpt_colsum(gdx, T, d, d, HV(b + 11), red, st);
-      sd::gpt_gelu_bwd(Ly.f, Ly.df, gu, gdu, gus, gdus, (long long)T * ff, st);
-      // MLP in: gh = gf Wf^T ; gdh = gdf Wf^T + gf VWf^T ; Hv_Wf = dh2^T gf + h2^T gdf
-      mm(T, d, ff, {gu, gus, ff, false}, Wt(b + 8, ff, false), gh, d, 1, 0, st);
-      mm2(T, d, ff, {gdu, gdus, ff, false}, Wt(b + 8, ff, false), {gu, gus, ff, false},
-          {V_(b + 8), Vs(b + 8), ff, false}, gdh, d, 1, 0, st);
-      mm2(d, ff, T, {Ly.dh2, Ly.dh2s, d, true}, {gu, gus, ff, true}, {Ly.h2, Ly.h2s, d, true}, {gdu, gdus, ff, true},
-          HV(b + 8), ff, 1, 0, st);
-      sd::gpt_colsum(gdu, T, ff, ff, HV(b + 9), red, st);
-      sd::LnBwdArgs b2{gh, gdh, th(b + 6), V_(b + 6), Ly.xh2, Ly.dxh2, Ly.r2, Ly.dr2, T, d,
-                       gx, gdx, gxs, gdxs, HV(b + 6), HV(b + 7), red};
-      sd::gpt_ln_bwd(b2, st);
-      // attention out-projection
-      mm(T, d, d, {gx, gxs, d, false}, Wt(b + 4, d, false), go, d, 1, 0, st, nullptr, gos);
-      mm2(T, d, d, {gdx, gdxs, d, false}, Wt(b + 4, d, false), {gx, gxs, d, false},
-          {V_(b + 4), Vs(b + 4), d, false}, gdo, d, 1, 0, st, nullptr, gdos);
-      mm2(d, d, T, {Ly.dO, Ly.dOs, d, true}, {gx, gxs, d, true}, {Ly.o, Ly.os, d, true}, {gdx, gdxs, d, true},
-          HV(b + 4), d, 1, 0, st);
-      sd::gpt_colsum(gdx, T, d, d, HV(b + 5), red, st);
-      attention_bwd(Ly, sc, st);
-      // QKV: gh = ga Wa^T ; gdh = gda Wa^T + ga VWa^T ; Hv_Wa = dh1^T ga + h1^T gda
-      mm(T, d, 3 * d, {ga, gas, 3 * d, false}, Wt(b + 2, 3 * d, false), gh, d, 1, 0, st);
-      mm2(T, d, 3 * d, {gda, gdas, 3 * d, false}, Wt(b + 2, 3 * d, false), {ga, gas, 3 * d, false},
-          {V_(b + 2), Vs(b + 2), 3 * d, false}, gdh, d, 1, 0, st);
-      mm2(d, 3 * d, T, {Ly.dh1, Ly.dh1s, d, true}, {ga, gas, 3 * d, true}, {Ly.h1, Ly.h1s, d, true},
-          {gda, gdas, 3 * d, true}, HV(b + 2), 3 * d, 1, 0, st);
-      sd::gpt_colsum(gda, T, 3 * d, 3 * d, HV(b + 3), red, st);
-      sd::LnBwdArgs b1{gh, gdh, th(b), V_(b), Ly.xh1, Ly.dxh1, Ly.r1, Ly.dr1, T, d,
-                       gx, gdx, gxs, gdxs, HV(b), HV(b + 1), red};
-      sd::gpt_ln_bwd(b1, st);
+      if (recompute) {  // re-run the layer from its saved input (bit-identical activations)
+        SD_CUDA(cudaMemcpyAsync(xr, XIN[set_of(m)][l], 2ull * size_t(T) * c.d * sizeof(float),
+                                cudaMemcpyDeviceToDevice, st));
+        gpt2_layer_fwd(Lscratch, l, xr, xr + Td, st);
+        gpt2_layer_bwd(Lscratch, l, hb, st);
+      } else {
+        gpt2_layer_bwd(L[l], l, hb, st);
+      }
     }
     // embeddings (wte also carries the head contribution written above)
-    SD_CUDA(cudaMemsetAsync(HV(1), 0, slots[1].rows * slots[1].cols * sizeof(float), st));
-    sd::gpt_embed_bwd(uniq, ustart, upos, n_uniq_mb[0], B, S, d, gdx, HV(0), HV(1), st);
+    if (!acc) SD_CUDA(cudaMemsetAsync(HV(1), 0, slots[1].rows * slots[1].cols * sizeof(float), st));
+    sd::gpt_embed_bwd(uniq + (long long)m * (T + 1), ustart + (long long)m * (T + 1), upos + (long long)m * T,
+                      n_uniq_mb[m], B, S, d, gdx, HV(0), HV(1), st, int(acc));
   }
 
-  // Llama-style decoder (oracle/src/models.cpp build_llama): same forward-over-
-  // reverse scheme as hvp(); RMSNorm via the LN kernels' rms mode, RoPE on q/k
-  // after the fused QKV product (inverse rotation on their adjoints), SwiGLU on
-  // the fused [gate | up] product, untied head, no biases. The whole model is
-  // the one-stage pipeline: begin, then forward + backward of each micro-batch.
-  void hvp_llama(const float* v, float* hv, cudaStream_t st) {
-    stage_begin(v, hv, st);
-    for (int m = 0; m < nmb; ++m) {
-      stage_fwd(m, st);
-      stage_bwd(m, st);
-    }
+  void gpt2_layer_bwd(Layer& Ly, int l, float hb, cudaStream_t st) {
+    const int d = c.d, ff = c.ff;
+    const float sc = 1.0f / std::sqrt(float(dh));
+    const int b = 2 + 12 * l;
+    // MLP out: gu = gx Wq^T ; gdu = gdx Wq^T + gx VWq^T ; Hv_Wq = du^T gx + u^T gdx
+    mm(T, ff, d, {gx, gxs, d, false}, Wt(b + 10, d, false), gu, ff, 1, 0, st);
+    mm2(T, ff, d, {gdx, gdxs, d, false}, Wt(b + 10, d, false), {gx, gxs, d, false},
+        {V_(b + 10), Vs(b + 10), d, false}, gdu, ff, 1, 0, st);
+    mm2(ff, d, T, {Ly.du, Ly.dus, ff, true}, {gx, gxs, d, true}, {Ly.u, Ly.us, ff, true}, {gdx, gdxs, d, true},
+        HV(b + 10), d, 1, hb, st);
+    sd::gpt_colsum(gdx, T, d, d, HV(b + 11), red, st, int(acc));
+    sd::gpt_gelu_bwd(Ly.f, Ly.df, gu, gdu, gus, gdus, (long long)T * ff, st);
+    // MLP in: gh = gf Wf^T ; gdh = gdf Wf^T + gf VWf^T ; Hv_Wf = dh2^T gf + h2^T gdf
+    mm(T, d, ff, {gu, gus, ff, false}, Wt(b + 8, ff, false), gh, d, 1, 0, st);
+    mm2(T, d, ff, {gdu, gdus, ff, false}, Wt(b + 8, ff, false), {gu, gus, ff, false},
+        {V_(b + 8), Vs(b + 8), ff, false}, gdh, d, 1, 0, st);
+    mm2(d, ff, T, {Ly.dh2, Ly.dh2s, d, true}, {gu, gus, ff, true}, {Ly.h2, Ly.h2s, d, true}, {gdu, gdus, ff, true},
+        HV(b + 8), ff, 1, hb, st);
+    sd::gpt_colsum(gdu, T, ff, ff, HV(b + 9), red, st, int(acc));
+    sd::LnBwdArgs b2{gh, gdh, th(b + 6), V_(b + 6), Ly.xh2, Ly.dxh2, Ly.r2, Ly.dr2, T, d,
+                     gx, gdx, gxs, gdxs, HV(b + 6), HV(b + 7), red, 0, int(acc)};
+    sd::gpt_ln_bwd(b2, st);
+    // attention out-projection
+    mm(T, d, d, {gx, gxs, d, false}, Wt(b + 4, d, false), go, d, 1, 0, st, nullptr, gos);
+    mm2(T, d, d, {gdx, gdxs, d, false}, Wt(b + 4, d, false), {gx, gxs, d, false},
+        {V_(b + 4), Vs(b + 4), d, false}, gdo, d, 1, 0, st, nullptr, gdos);
+    mm2(d, d, T, {Ly.dO, Ly.dOs, d, true}, {gx, gxs, d, true}, {Ly.o, Ly.os, d, true}, {gdx, gdxs, d, true},
+        HV(b + 4), d, 1, hb, st);
+    sd::gpt_colsum(gdx, T, d, d, HV(b + 5), red, st, int(acc));
+    attention_bwd(Ly, sc, st);
+    // QKV: gh = ga Wa^T ; gdh = gda Wa^T + ga VWa^T ; Hv_Wa = dh1^T ga + h1^T gda
+    mm(T, d, 3 * d, {ga, gas, 3 * d, false}, Wt(b + 2, 3 * d, false), gh, d, 1, 0, st);
+    mm2(T, d, 3 * d, {gda, gdas, 3 * d, false}, Wt(b + 2, 3 * d, false), {ga, gas, 3 * d, false},
+        {V_(b + 2), Vs(b + 2), 3 * d, false}, gdh, d, 1, 0, st);
+    mm2(d, 3 * d, T, {Ly.dh1, Ly.dh1s, d, true}, {ga, gas, 3 * d, true}, {Ly.h1, Ly.h1s, d, true},
+        {gda, gdas, 3 * d, true}, HV(b + 2), 3 * d, 1, hb, st);
+    sd::gpt_colsum(gda, T, 3 * d, 3 * d, HV(b + 3), red, st, int(acc));
+    sd::LnBwdArgs b1{gh, gdh, th(b), V_(b), Ly.xh1, Ly.dxh1, Ly.r1, Ly.dr1, T, d,
+                     gx, gdx, gxs, gdxs, HV(b), HV(b + 1), red, 0, int(acc)};
+    sd::gpt_ln_bwd(b1, st);
   }
+
+  // Llama-style decoder (oracle/src/models.cpp build_llama): the same
+  // forward-over-reverse scheme, stage_fwd / stage_bwd below (RMSNorm via the
+  // LN kernels' rms mode, RoPE on q/k after the fused QKV product with the
+  // inverse rotation on their adjoints, SwiGLU on the fused [gate | up]
+  // product, untied head, no biases).
 
   // stage-local views of v, its tf32 residual and Hv for parameter slot i
   const float* V_(int i) const { return vcur + (slots[i].off - pbase); }
@@ -700,8 +734,10 @@ void check_stage(const sd_gpt_config& c, const StageSpec& sp) {
   const bool whole = sp.l0 == 0 && sp.l1 == c.n_layer;
   if (sp.l0 < 0 || sp.l1 > c.n_layer || sp.l0 >= sp.l1) fail(SD_LAYOUT_ERROR, "stage layer range out of bounds");
   if (sp.nmb < 1 || sp.nsets < 1 || sp.nsets > sp.nmb) fail(SD_ARGUMENT_ERROR, "need 1 <= n_sets <= n_micro");
-  if ((!whole || sp.nmb > 1 || sp.flags) && c.arch != SD_ARCH_LLAMA)
-    fail(SD_CONFIG_ERROR, "pipeline stages / micro-batches / engine flags need the untied Llama-style layout");
+  // the GPT-2 block ties the head to the token embedding (first and last
+  // layer): it runs micro-batches and the engine flags as one whole-model stage
+  if (!whole && c.arch != SD_ARCH_LLAMA)
+    fail(SD_CONFIG_ERROR, "pipeline stages need the untied Llama-style layout");
   if (sp.flags & ~(SD_GPT_RECOMPUTE | SD_GPT_NO_PROBE_RESIDUAL)) fail(SD_ARGUMENT_ERROR, "unknown engine flags");
 }
 

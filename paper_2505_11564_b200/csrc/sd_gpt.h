@@ -57,8 +57,10 @@ void gpt_attn_softmax_bwd(const float* P, const float* dP, float* gP, float* gdP
                           long long rows, cudaStream_t s);
 void gpt_ce(float* z, float* dz, float* zs, float* dzs, const int* tgt, int T, int V, long long ld, float scale,
             double* loss_rows, cudaStream_t s);
+// Hv of the embeddings: hv_wte rows += scattered adjoint tangents; hv_wpe
+// = (acc: +=) the per-position sums
 void gpt_embed_bwd(const int* uniq, const int* start, const int* pos, int n_uniq, int B, int S, int d,
-                   const float* gdx, float* hv_wte, float* hv_wpe, cudaStream_t s);
+                   const float* gdx, float* hv_wte, float* hv_wpe, cudaStream_t s, int acc = 0);
 void gpt_residual(const float* x, float* xs, long long n, cudaStream_t s);
 void gpt_fill(float* x, float v, long long n, cudaStream_t s);
 // theta[i - th_base] for global flat indices i in [off, off + n)

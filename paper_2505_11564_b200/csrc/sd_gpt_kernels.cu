@@ -908,13 +908,14 @@ __global__ void k_embed_bwd_wte(const int* __restrict__ uniq, const int* __restr
   *dst += acc;
 }
 
-__global__ void k_embed_bwd_wpe(const float* __restrict__ gdx, int B, int S, int d, float* __restrict__ hv_wpe) {
+__global__ void k_embed_bwd_wpe(const float* __restrict__ gdx, int B, int S, int d, float* __restrict__ hv_wpe,
+                                int accumulate) {
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i >= (long long)S * d) return;
   const int s = int(i / d), e = int(i % d);
   float acc = 0.f;
   for (int b = 0; b < B; ++b) acc += gdx[((long long)b * S + s) * d + e];
-  hv_wpe[i] = acc;
+  hv_wpe[i] = accumulate ? hv_wpe[i] + acc : acc;
 }
 
 __global__ void k_res(const float* __restrict__ x, float* __restrict__ xs, long long n) {
@@ -1105,14 +1106,14 @@ void gpt_ce(float* z, float* dz, float* zs, float* dzs, const int* tgt, int T, i
 }
 
 void gpt_embed_bwd(const int* uniq, const int* start, const int* pos, int n_uniq, int B, int S, int d,
-                   const float* gdx, float* hv_wte, float* hv_wpe, cudaStream_t s) {
+                   const float* gdx, float* hv_wte, float* hv_wpe, cudaStream_t s, int acc) {
   const long long warps = (long long)n_uniq * ((d + 31) / 32);
   if (warps > 0) {
     k_embed_bwd_wte<<<g1(warps, 8), 256, 0, s>>>(uniq, start, pos, n_uniq, d, gdx, hv_wte);
     SD_LAUNCHED("k_embed_bwd_wte");
   }
   if (hv_wpe) {
-    k_embed_bwd_wpe<<<g1((long long)S * d), 256, 0, s>>>(gdx, B, S, d, hv_wpe);
+    k_embed_bwd_wpe<<<g1((long long)S * d), 256, 0, s>>>(gdx, B, S, d, hv_wpe, acc);
     SD_LAUNCHED("k_embed_bwd_wpe");
   }
 }

@@ -35,6 +35,7 @@ LLAMA_70B = dict(n_layer=80, d=8192, n_head=64, ff=28672, vocab=128256, ctx=8192
 GPT2_SMALL = dict(n_layer=12, d=768, n_head=12, ff=3072, vocab=50257, ctx=1024)
 
 _ready = False
+RECOMPUTE, NO_PROBE_RESIDUAL = 1, 2  # engine flags (sd_gpt_stage_create)
 
 
 def _L():
@@ -121,13 +122,22 @@ def synthetic_tokens(vocab: int, B: int, S: int, seed: int = 1, first_seq: int =
 
 
 class GptHvp:
-    """HVP engine for one (batch, seq) shape on the current CUDA device."""
+    """HVP engine for one (batch, seq) shape on the current CUDA device.
+
+    ``micro_batches`` = M runs the batch as M micro-batches of ``batch``
+    sequences each (Alg. 1: Hv accumulated over the loader), so the
+    workspace holds one micro-batch's activations; ``recompute`` keeps only
+    each layer's input and re-runs the layer in the backward
+    (SD_GPT_RECOMPUTE); ``probe_residual=False`` forms the probe's tf32
+    residuals on chip (SD_GPT_NO_PROBE_RESIDUAL). Tokens are M * batch * seq."""
 
     def __init__(self, cfg: dict, batch: int, seq: int, init_seed: int = 0, gain_scale: float = 0.0,
                  bias_scale: float = 0.0, theta: torch.Tensor | None = None, tokens=None, targets=None,
-                 seed_tok: int = 1, first_seq: int = 0, loss_scale: float | None = None, stream=None):
+                 seed_tok: int = 1, first_seq: int = 0, loss_scale: float | None = None, stream=None,
+                 micro_batches: int = 1, recompute: bool = False, probe_residual: bool = True):
         self.cfg = dict(cfg)
-        self.B, self.S = batch, seq
+        self.mb, self.M = batch, micro_batches
+        self.B, self.S = batch * micro_batches, seq
         self._c = _cfg(cfg)
         self.P = param_count(cfg)
         self.device = torch.device("cuda", torch.cuda.current_device())
@@ -138,15 +148,18 @@ class GptHvp:
             check(_L().sd_gpt_init_params(C.byref(self._c), init_seed, gain_scale, bias_scale, theta.data_ptr(), s))
         assert theta.dtype == torch.float32 and theta.numel() == self.P and theta.is_contiguous()
         self.theta = theta
-        nbytes = _L().sd_gpt_workspace_bytes(C.byref(self._c), batch, seq)
-        if nbytes == 0:
-            check(1)
-        self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        self.flags = (RECOMPUTE if recompute else 0) | (0 if probe_residual else NO_PROBE_RESIDUAL)
+        L_ = cfg["n_layer"]
+        nbytes = _L().sd_gpt_stage_workspace_bytes(C.byref(self._c), batch, seq, micro_batches, 0, L_, 1, self.flags)
         self.h = C.c_void_p()
-        check(_L().sd_gpt_create(C.byref(self._c), batch, seq, theta.data_ptr(), self.workspace.data_ptr(), nbytes, s,
-                                 C.byref(self.h)))
+        if nbytes == 0:  # invalid shape: the create call raises the precise error class
+            check(_L().sd_gpt_stage_create(C.byref(self._c), batch, seq, micro_batches, 0, L_, 1, self.flags, None,
+                                           None, 0, s, C.byref(C.c_void_p())))
+        self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        check(_L().sd_gpt_stage_create(C.byref(self._c), batch, seq, micro_batches, 0, L_, 1, self.flags,
+                                       theta.data_ptr(), self.workspace.data_ptr(), nbytes, s, C.byref(self.h)))
         if tokens is None:
-            tokens, targets = synthetic_tokens(cfg["vocab"], batch, seq, seed_tok, first_seq)
+            tokens, targets = synthetic_tokens(cfg["vocab"], self.B, seq, seed_tok, first_seq)
         self.set_batch(tokens, targets, loss_scale)
 
     def set_batch(self, tokens, targets, loss_scale: float | None = None):
@@ -208,7 +221,6 @@ class GptHvp:
 # ------------------------------------------------------------ pipeline stages
 PIPE_F, PIPE_B, PIPE_SEND_F, PIPE_RECV_F, PIPE_SEND_B, PIPE_RECV_B, PIPE_GROUP_BEGIN, PIPE_GROUP_END = range(8)
 PIPE_NAMES = ["F", "B", "SEND_F", "RECV_F", "SEND_B", "RECV_B", "GROUP_BEGIN", "GROUP_END"]
-RECOMPUTE, NO_PROBE_RESIDUAL = 1, 2  # engine flags (sd_gpt_stage_create)
 
 
 def stage_workspace_bytes(cfg: dict, micro_batch: int, seq: int, n_micro: int, layer_begin: int, layer_end: int,

@@ -244,3 +244,71 @@ def test_column_reduction_paths_bitwise(sd):
         assert r.returncode == 0, r.stderr[-2000:]
         out[tag] = r.stdout.strip().splitlines()[-1]
     assert out["vec"] == out["scalar"], out
+
+
+@pytest.mark.parametrize("cfg", [TINY, dict(LTINY, n_kv_head=2)])
+def test_micro_batched_hvp_equals_whole_batch(sd, oracle, cfg):
+    """PAPER.md Alg. 1 over a loader of micro-batches (h += u b): 4 micro-batches
+    of 1 sequence == the 4-sequence batch (GPT-2 tied-head block and Llama);
+    recomputation and on-chip probe residuals change no bit; vs the f64 oracle."""
+    from paper_2505_11564_b200 import gpt
+    S = 32
+    tok, tgt = gpt.synthetic_tokens(cfg["vocab"], 4, S, seed=1)
+    whole = gpt.GptHvp(cfg, 4, S, init_seed=0, gain_scale=0.1, bias_scale=0.1, tokens=tok, targets=tgt)
+    mb = gpt.GptHvp(cfg, 1, S, theta=whole.theta, tokens=tok, targets=tgt, micro_batches=4)
+    rc = gpt.GptHvp(cfg, 1, S, theta=whole.theta, tokens=tok, targets=tgt, micro_batches=4, recompute=True,
+                    probe_residual=False)
+    assert mb.workspace.numel() < whole.workspace.numel() and rc.workspace.numel() < mb.workspace.numel()
+    v = torch.tensor(oracle.draw_probe(whole.P, 9, 1, prec=0), dtype=torch.float32, device="cuda")
+    a, b, c = whole.hvp(v), mb.hvp(v), rc.hvp(v)
+    assert torch.equal(b, c)
+    assert float((b - a).norm() / a.norm()) < 3e-6  # fp32 sums over micro-batches vs within one batch
+    ref = oracle.gpt_hvp(cfg, whole.theta_numpy(), tok.astype(np.uint32), tgt.astype(np.uint32), 4, S,
+                         v.double().cpu().numpy())
+    assert rel(b.double().cpu().numpy(), ref) < TOL
+    assert abs(mb.loss() - whole.loss()) < 1e-6
+
+
+def test_micro_batched_data_sharded_workers(sd):
+    """C3's data-sharded HVP with micro-batches: 2 in-process workers, each 2
+    micro-batches of 1 sequence, Lanczos vectors split between them (all-gather
+    q, reduce-scatter Hv) == one worker with the whole 4-sequence batch."""
+    from paper_2505_11564_b200 import gpt
+    cfg = dict(n_layer=2, d=64, n_head=4, ff=128, vocab=96, ctx=32)
+    B, S = 4, 32
+    tok, tgt = gpt.synthetic_tokens(cfg["vocab"], B, S, seed=1)
+    lc = sd.LanczosConfig(k_max=6, reorthogonalize=sd.REORTH_FULL, prec=sd.F32, reduction=sd.REDUCE_TREE,
+                          probe=sd.ProbeSpec(seed=5, distribution=sd.RADEMACHER))
+    whole = gpt.GptHvp(cfg, B, S, init_seed=0, gain_scale=0.1, tokens=tok, targets=tgt)
+    a = sd.lanczos_run(whole.operator(), lc)
+    lay = sd.split_evenly(whole.P, 2)
+
+    def worker(r, comm):
+        sl = slice(r * 2 * S, (r + 1) * 2 * S)
+        e = gpt.GptHvp(cfg, 1, S, theta=whole.theta.clone(), tokens=tok[sl], targets=tgt[sl], micro_batches=2,
+                       loss_scale=1.0 / (B * S))
+        res = sd.lanczos_run(e.operator(comm, layout=lay), lc, layout=lay, comm=comm)
+        e.close()
+        return res
+
+    out = sd.run_workers(2, worker)
+    for r in out:
+        assert np.max(np.abs(r.alphas - a.alphas)) <= 1e-5 * np.max(np.abs(a.alphas))
+
+
+def test_c3_shape_micro_batched_recompute():
+    # BASELINE C3 (1.3B GPT-2-architecture decoder) as it runs in bench.py
+    # --workload c3: micro-batches of 1 x 2048 tokens with recomputation;
+    # finite, symmetric, and the workspace of 2 micro-batches equals that of one
+    from paper_2505_11564_b200 import gpt
+    C3 = dict(n_layer=24, d=2048, n_head=16, ff=8192, vocab=50257, ctx=2048)
+    eng = gpt.GptHvp(C3, 1, 2048, micro_batches=2, recompute=True)
+    g = torch.Generator(device="cuda").manual_seed(0)
+    u = torch.randn(eng.P, device="cuda", generator=g) * 1e-3
+    w = torch.randn(eng.P, device="cuda", generator=g) * 1e-3
+    hu, hw = eng.hvp(u), eng.hvp(w)
+    assert bool(torch.isfinite(hu).all()) and bool(torch.isfinite(hw).all())
+    a, b = float(torch.dot(hu.double(), w.double())), float(torch.dot(u.double(), hw.double()))
+    assert abs(a - b) <= 1e-4 * max(abs(a), abs(b))
+    assert eng.workspace.numel() < 40e9
+    eng.close()
