@@ -161,8 +161,16 @@ sd_status sd_comm_destroy(sd_comm c);
  * when the receiver has copied them, groups batch them like NCCL groups. */
 sd_status sd_comm_local_create(int nranks, sd_comm* out);
 /* a failing in-process worker aborts its group: the others' pending and
- * future collectives fail with SD_PROTOCOL_ERROR instead of waiting forever */
+ * future collectives fail with SD_PROTOCOL_ERROR instead of waiting forever;
+ * on an NCCL communicator: ncclCommAbort */
 sd_status sd_comm_abort(sd_comm c);
+/* stream wait that, over NCCL, polls ncclCommGetAsyncError and aborts the
+ * communicator on an asynchronous error or after SD_NCCL_TIMEOUT_S (default
+ * 1800 s): SD_NCCL_ERROR instead of a hang when a peer fails. The Lanczos
+ * engine waits this way once per step. Reductions over NCCL are rank-ordered
+ * (grouped send/recv + ascending-rank sum, bitwise equal to in-process
+ * workers); SD_NCCL_ORDERED=0 selects ncclReduceScatter / ncclAllReduce. */
+sd_status sd_comm_wait(sd_comm c, sd_stream s);
 /* In-place sum all-reduce of n floats (data-sharded HVP, C1 of SURVEY §2.1). */
 sd_status sd_comm_allreduce_f32(sd_comm c, float* buf, uint64_t n, sd_stream s);
 /* All-gather of `bytes` per rank (ordered scalar partial exchange). */

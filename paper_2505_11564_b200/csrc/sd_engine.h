@@ -26,6 +26,8 @@ void comm_send_f32(sd_comm c, const float* buf, uint64_t n, int peer, cudaStream
 void comm_recv_f32(sd_comm c, float* buf, uint64_t n, int peer, cudaStream_t s);
 void comm_group_begin(sd_comm c);
 void comm_group_end(sd_comm c, cudaStream_t s);
+// stream wait that surfaces NCCL async errors / timeouts as SD_NCCL_ERROR
+void comm_wait(sd_comm c, cudaStream_t s);
 int comm_rank(sd_comm c);
 int comm_size(sd_comm c);
 void operator_apply(sd_operator op, const void* x, void* y, int prec, cudaStream_t s, uint64_t row_begin,

