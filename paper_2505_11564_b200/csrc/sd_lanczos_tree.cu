@@ -40,6 +40,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -48,7 +49,7 @@
 namespace sd {
 namespace tree {
 
-constexpr int kThreads = 256, kWarps = 8, kMaxCols = 256, kGrid = 148;
+constexpr int kThreads = 256, kWarps = 8, kMaxCols = 256, kSMs = 148, kMaxPerSM = 2, kGrid = kSMs * kMaxPerSM;
 constexpr uint64_t kChunk = uint64_t(1) << 30;  // elements per launch (TMA coordinates are int32)
 
 struct Params {
@@ -112,7 +113,7 @@ union VU {
 };
 
 template <typename T, int MODE, int EPL, int CPW>
-__global__ void __launch_bounds__(kThreads, 1) k_gs_tree(const __grid_constant__ CUtensorMap tq,
+__global__ void __launch_bounds__(kThreads, 2) k_gs_tree(const __grid_constant__ CUtensorMap tq,
                                                          const __grid_constant__ CUtensorMap tr, Params p) {
   constexpr int TE = 32 * EPL;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -428,6 +429,13 @@ static void pass_t(int mode, const void* Q, uint64_t ldq, int jb, void* r, uint6
   const Shape sh = pick<T>(jb);
   const size_t smem = smem_bytes<T>(sh, jb);
   const int cpw = (jb + kWarps - 1) / kWarps;
+  // two CTAs per SM when their rings fit (227 KB per SM): one CTA's update
+  // phase overlaps the other's dot phase and barriers
+  static const int max_per_sm = [] {
+    const char* e = std::getenv("SD_TREE_CTAS_PER_SM");
+    return e ? std::max(1, std::min(kMaxPerSM, std::atoi(e))) : kMaxPerSM;
+  }();
+  const int per_sm = (2 * (smem + 1024) <= 227 * 1024) ? max_per_sm : 1;
   const uint64_t nchunks = (n + kChunk - 1) / kChunk;
   // CTAs of every chunk launch, so the last one knows it is last
   std::vector<int> grids(nchunks), tiles(nchunks);
@@ -435,7 +443,7 @@ static void pass_t(int mode, const void* Q, uint64_t ldq, int jb, void* r, uint6
   for (uint64_t c = 0; c < nchunks; ++c) {
     const uint64_t len = std::min<uint64_t>(kChunk, n - c * kChunk);
     tiles[c] = int((len + sh.te - 1) / sh.te);
-    grids[c] = std::min(tiles[c], kGrid);
+    grids[c] = std::min(tiles[c], kSMs * per_sm);
     nparts += grids[c];
   }
   const CUtensorMapDataType dt = sizeof(T) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
