@@ -343,7 +343,7 @@ __global__ void __launch_bounds__(kThreadsFor<TA>(), 1)
   using Cf = Cfg<BN_>;
   constexpr int BN = Cf::BN, STAGES = Cf::STAGES, EC = Cf::EC;
   constexpr int A_BYTES = Cf::A_BYTES, B_BYTES = Cf::B_BYTES;
-  static_assert(!TA || (THREE && BN_ == 64), "TMEM-A: 3xTF32, 64-wide tiles");
+  static_assert(!TA || (THREE && (BN_ == 64 || BN_ == 128)), "TMEM-A: 3xTF32, 64- or 128-wide tiles");
   constexpr int CONV = TA ? 4 : kConvWarps;
   constexpr uint32_t TA_COL0 = 2 * BN_;                       // A slots after the two accumulators
   constexpr uint32_t TMEM_COLS = TA ? 512 : Cf::TMEM_COLS;   // TA: 128 + STAGES x (16 hi + 16 lo)
@@ -405,14 +405,16 @@ __global__ void __launch_bounds__(kThreadsFor<TA>(), 1)
           mbar_wait(&empty[s], ph ^ 1);
           unsigned char* st = smem + s * STAGE_BYTES;
           // dual source: the second product's k-blocks follow the first's
-          const bool src2 = kk >= ti.num_kb;
+          // (split pairs: interleaved, and source 2 multiplies B, not B2)
+          const bool src2 = ep.split ? (kk & 1) != 0 : kk >= ti.num_kb;
           const bool bex = THREE && !ep.res && ((ep.bexact >> (src2 ? 1 : 0)) & 1);
-          mbar_expect_tx_e(&full[s], ep.res ? A_BYTES + B_BYTES : STAGE_BYTES - (bex ? B_BYTES : 0));
-          const int kb = src2 ? kk - ti.num_kb : kk;
+          mbar_expect_tx_e(&full[s], ep.split ? A_BYTES + (src2 ? B_BYTES / 2 : B_BYTES)
+                                              : (ep.res ? A_BYTES + B_BYTES : STAGE_BYTES - (bex ? B_BYTES : 0)));
+          const int kb = ep.split ? kk >> 1 : (src2 ? kk - ti.num_kb : kk);
           const CUtensorMap* pA = src2 ? &mA2 : &mA;
           const CUtensorMap* pAs = src2 ? &mAs2 : &mAs;
-          const CUtensorMap* pB = src2 ? &mB2 : &mB;
-          const CUtensorMap* pBs = src2 ? &mBs2 : &mBs;
+          const CUtensorMap* pB = (src2 && !ep.split) ? &mB2 : &mB;
+          const CUtensorMap* pBs = (src2 && !ep.split) ? &mBs2 : &mBs;
           const int k0 = (ti.kb0 + kb) * BK;
           if (A_MN && (ep.mn5 & 1)) {
             tma_load_5d_e(pA, &full[s], st, 0, k0, ti.m0 / 32, z1, z2);
@@ -428,7 +430,11 @@ __global__ void __launch_bounds__(kThreadsFor<TA>(), 1)
             if (THREE && !ep.res) tma_load_4d_e(pAs, &full[s], st + A_BYTES, k0, ti.m0, z1, z2);
           }
           unsigned char* sb = st + (THREE ? 2 : 1) * A_BYTES;
-          if (B_MN && (ep.mn5 & 2)) {
+          if (B_MN && ep.split) {
+            // [B | B2] as two 64-wide 5-D boxes (2 chunks each); source 2: B only
+            tma_load_5d_e(pB, &full[s], sb, 0, k0, 0, z1, z2);
+            if (!src2) tma_load_5d_e(&mB2, &full[s], sb + B_BYTES / 2, 0, k0, 0, z1, z2);
+          } else if (B_MN && (ep.mn5 & 2)) {
             tma_load_5d_e(pB, &full[s], sb, 0, k0, ti.n0 / 32, z1, z2);
             if (THREE && !ep.res && !bex) tma_load_5d_e(pBs, &full[s], sb + B_BYTES, 0, k0, ti.n0 / 32, z1, z2);
           } else if (B_MN) {
@@ -520,6 +526,7 @@ __global__ void __launch_bounds__(kThreadsFor<TA>(), 1)
       }
   } else if (warp == 1) {
     constexpr uint32_t idesc = make_idesc(TA ? false : A_MN, B_MN, BN);  // TMEM A: lane = row, column = k
+    constexpr uint32_t idesc_half = make_idesc(TA ? false : A_MN, B_MN, BN / 2);  // split: source 2
     uint32_t g = 0, chunk = 0;
     for (int t = blockIdx.x; t < ep.n_tiles; t += gridDim.x) {
       const TileInfo ti = tile_info<BN, CAUSAL>(ep, t, K);
@@ -546,9 +553,13 @@ __global__ void __launch_bounds__(kThreadsFor<TA>(), 1)
             const uint32_t acc0 = (first && ks == 0) ? 0u : 1u;
             if (TA) {
               const uint32_t ta = tmem + TA_COL0 + uint32_t(s) * 32u + uint32_t(ks) * 8u;
-              mma_tf32_ta_e(d, ta + 16, tile_desc<B_MN>(b, ks), idesc, acc0);
-              mma_tf32_ta_e(d, ta, tile_desc<B_MN>(bs, ks), idesc, 1u);
-              mma_tf32_ta_e(d, ta, tile_desc<B_MN>(b, ks), idesc, 1u);
+              // split pair, source 2: N = BN/2 into accumulator columns BN/2.. (a chunk
+              // always starts with a source-1 k-block, so acc0 is 0 only there)
+              const bool half = ep.split && (kb & 1);
+              const uint32_t dd = half ? d + uint32_t(BN / 2) : d, id = half ? idesc_half : idesc;
+              mma_tf32_ta_e(dd, ta + 16, tile_desc<B_MN>(b, ks), id, acc0);
+              mma_tf32_ta_e(dd, ta, tile_desc<B_MN>(bs, ks), id, 1u);
+              mma_tf32_ta_e(dd, ta, tile_desc<B_MN>(b, ks), id, 1u);
             } else if (THREE) {
               mma_tf32_e(d, tile_desc<A_MN>(as, ks), tile_desc<B_MN>(b, ks), idesc, acc0);
               if (!bex) mma_tf32_e(d, tile_desc<A_MN>(a, ks), tile_desc<B_MN>(bs, ks), idesc, 1u);
@@ -601,6 +612,10 @@ __global__ void __launch_bounds__(kThreadsFor<TA>(), 1)
                            ep.bias, lane, ti.m0 + sub * 32, ti.n0 + cb, ti.z % ep.Z1, ti.z / ep.Z1);
         if (lane == 0) bulk_wait_read0();  // staging box free for the next tile
         __syncwarp();
+      } else if (ep.split && cb >= BN / 2) {
+        EpiParams e2 = ep;  // columns BN/2.. of the split pair: the second output
+        e2.C = ep.C2, e2.Cs = ep.Cs2;
+        store_row<EC>(e2, ti, row, ti.n0 + cb - BN / 2, acc);
       } else {
         store_row<EC>(ep, ti, row, ti.n0 + cb, acc);
       }
@@ -713,6 +728,59 @@ void launch(const GemmArgs& g, cudaStream_t s) {
   prof_end(s, (dual ? 4.0 : 2.0) * double(g.M) * g.N * g.K * g.Z1 * g.Z2);
 }
 
+// Merged pair of 64-wide products sharing A (GemmArgs::split): one 1-CTA
+// launch with a 128-wide TMEM accumulator and A from tensor memory. Per
+// k-block: source 1 (A) against [B | B2] (N = 128: 3 MMAs), source 2 (A2)
+// against B into columns 64-127 (N = 64: 3 MMAs) -- the MMA work of the two
+// separate products, but each A tile is staged and split once and every MMA
+// of source 1 is 128 wide (the 64-wide tf32 MMA is issue-bound).
+template <bool A_MN>
+void launch_split(const GemmArgs& g, cudaStream_t s) {
+  constexpr int BN = 128;
+  using Cf = Cfg<BN>;
+  if (g.N != 64 || !g.b_mn || !g.A2 || !g.B2 || !g.C2) fail(SD_ARGUMENT_ERROR, "split gemm: 64-wide MN-major pair");
+  GemmArgs m = g;  // maps: A, A2; B and B2 as 64-wide 5-D boxes
+  m.ldb2 = g.ldb, m.sb1_2 = g.sb1, m.sb2_2 = g.sb2;
+  m.As = m.Bs = m.A2s = m.B2s = nullptr;
+  m.onchip = true;
+  CUtensorMap maps[8];
+  int mn5 = 0;
+  operand_maps(m, A_MN, true, true, 64, maps, &mn5);
+  if (!(mn5 & 2)) fail(SD_ARGUMENT_ERROR, "split gemm: B needs 32-element chunks");
+  const int zc = g.Z1 * g.Z2;
+  const int tm = (g.M + BM - 1) / BM;
+  const int total_kb = (g.K + BK - 1) / BK;
+  EpiParams ep{g.C, g.ldc, g.sc1, g.sc2, g.M, g.N, g.Z1, g.alpha, g.beta, g.bias, g.Cs, g.dbg, zc, total_kb, nullptr,
+               g.causal, 1, tm, tm * zc, 2, 1};
+  ep.tma_store = 0;
+  ep.mn5 = mn5;
+  ep.bexact = 0;
+  ep.split = 1;
+  ep.C2 = g.C2, ep.Cs2 = g.Cs2;
+  ep.group = 0;
+  const size_t smem = 1024 + size_t(Cf::STAGES) * 2 * (Cf::A_BYTES + Cf::B_BYTES) + 8 * 4096 + 512;
+  auto kern = g.causal ? k_gemm_tf32<A_MN, true, true, BN, true, true> : k_gemm_tf32<A_MN, true, true, BN, false, true>;
+  static bool attr = false;
+  if (!attr) {
+    SD_CUDA(cudaFuncSetAttribute(k_gemm_tf32<A_MN, true, true, BN, true, true>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    SD_CUDA(cudaFuncSetAttribute(k_gemm_tf32<A_MN, true, true, BN, false, true>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    attr = true;
+  }
+  const int grid = std::min(ep.n_tiles, kNumSMs);
+  if (prof().on)
+    prof().next_tag = std::to_string(g.M) + "," + std::to_string(2 * g.N) + "," + std::to_string(g.K) + "," +
+                      std::to_string(zc) + "," + std::to_string(int(A_MN)) + ",1," + std::to_string(g.causal) +
+                      ",1,split";
+  prof_begin(s);
+  launch_gemm_kernel(kern, unsigned(grid), unsigned(kThreadsFor<true>()), smem, s, maps[0], maps[1], maps[2], maps[3],
+                     maps[4], maps[5], maps[6], maps[7], maps[0], maps[0], g.K, ep);
+  SD_LAUNCHED("k_gemm_tf32_split");
+  // algorithmic flops of the pair: A B + A B2 + A2 B
+  prof_end(s, 6.0 * double(g.M) * g.N * g.K * g.Z1 * g.Z2);
+}
+
 bool env_on(const char* name) {
   const char* e = std::getenv(name);
   return !(e && e[0] == '0');
@@ -736,6 +804,7 @@ void gemm(const GemmArgs& g_in, cudaStream_t s) {
   if (g.b_exact && g.As && !g.Bs) g.Bs = g.B;
   if (g.A2 && g.b2_exact && g.A2s && !g.B2s) g.B2s = g.B2;
   if (!g.A2) g.b2_exact = false;
+  if (g.split) return g.a_mn ? launch_split<true>(g, s) : launch_split<false>(g, s);
   const bool pair = g.causal == 0 && g.M >= 256 && g.N >= 256 && sd_gemm_pair_enabled();
   // On-chip residuals (onchip = allowed): they halve the operand bytes through
   // L2 and TMA but add a shared-memory read + write of every staged tile, and

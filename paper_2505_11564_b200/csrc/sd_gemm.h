@@ -30,6 +30,12 @@ struct GemmArgs {
   // B (B2) holds tf32-exact values (bf16-valued weights): its residual is zero,
   // so 3xTF32 needs neither its residual array nor the A . B_lo product
   bool b_exact = false, b2_exact = false;
+  // merged pair of 64-wide products sharing A (the per-head attention
+  // R-op products): C = alpha (A B), C2 = alpha (A B2 + A2 B), both N = 64,
+  // B and B2 MN-major with the same strides (ldb, sb1, sb2), C2 / Cs2 with C's
+  // strides; one launch with a 128-wide accumulator (A staged once for both)
+  bool split = false;
+  float *C2 = nullptr, *Cs2 = nullptr;
 };
 void gemm(const GemmArgs& g, cudaStream_t s);
 void split_tf32(const float* x, float* small, long long n, int mode, cudaStream_t s);

@@ -181,6 +181,10 @@ struct EpiParams {
   int mn5;                            // bit 0 / 1: MN-major A / B tile as one 5-D TMA box
   int bexact;                         // bit 0 / 1: source 1 / 2 B operand exact in tf32 (bf16-valued
                                       // weights): no B residual load, no A.B_lo MMA
+  int split;                          // merged 64-wide pair (GemmArgs::split): source 1 fills the
+                                      // 128 accumulator columns [A B | A B2], source 2 adds A2 B into
+                                      // columns 64-127; k-blocks interleave 1, 2, 1, 2, ...
+  float *C2, *Cs2;                    // split: output of columns 64-127
   int group;                          // grouped tile walk (raster_group): > 0 groups of `group` m tiles,
                                       // m fastest inside a group; < 0 groups of -group n tiles, n fastest
                                       // inside; 0 n fastest over the whole grid
@@ -348,6 +352,7 @@ __device__ __forceinline__ uint64_t tile_desc(uint32_t base, int ks) {
 // finished chunk into round-to-nearest fp32 registers while the MMA warp
 // fills the other buffer (chunks continue across the tiles of a CTA).
 constexpr int KC = 8;  // k-blocks (8 x 16 = 128 of K) per TMEM chunk
+static_assert(KC % 2 == 0, "split products interleave the two sources: a chunk must start with source 1");
 
 struct TileInfo {
   int n0, m0, z, split, kb0, num_kb;

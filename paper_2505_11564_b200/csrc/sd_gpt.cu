@@ -295,6 +295,34 @@ struct sd_gpt_s {
     onchip_residuals(g);
     sd::gemm(g, st);
   }
+  // merged pair of 64-wide per-head products sharing A (sd_gemm.cu launch_split):
+  // C = alpha A B, C2 = alpha (A B2 + A2 B) -- the [o | dO], [gv | gdv],
+  // [gq | gdq], [gk | gdk] pairs of the attention R-op in one launch each
+  void mm_pair(int M, int K, Op A, Op Bo, Op B2, Op A2, float* C, float* Cs, float* C2, float* Cs2, long long ldc,
+               float alpha, cudaStream_t st, int Z1, int Z2, long long c1, long long c2) {
+    sd::GemmArgs g;
+    g.M = M, g.N = 64, g.K = K;
+    g.A = A.p, g.lda = A.ld, g.a_mn = A.mn, g.sa1 = A.s1, g.sa2 = A.s2;
+    g.B = Bo.p, g.ldb = Bo.ld, g.b_mn = Bo.mn, g.sb1 = Bo.s1, g.sb2 = Bo.s2;
+    g.B2 = B2.p, g.ldb2 = B2.ld;
+    g.A2 = A2.p, g.lda2 = A2.ld, g.sa1_2 = A2.s1, g.sa2_2 = A2.s2;
+    if (A2.mn != A.mn || !Bo.mn || !B2.mn || B2.ld != Bo.ld || B2.s1 != Bo.s1 || B2.s2 != Bo.s2)
+      fail(SD_ARGUMENT_ERROR, "gpt: split pair operands differ in layout");
+    g.C = C, g.Cs = Cs, g.C2 = C2, g.Cs2 = Cs2, g.ldc = ldc, g.alpha = alpha, g.beta = 0.0f;
+    g.Z1 = Z1, g.Z2 = Z2, g.sc1 = c1, g.sc2 = c2;
+    g.causal = cmode;
+    g.onchip = true;
+    g.split = true;
+    sd::gemm(g, st);
+  }
+  static bool split_pairs() {
+    static const bool on = [] {  // SD_ATTN_SPLIT=0: the two products as separate launches
+      const char* e = std::getenv("SD_ATTN_SPLIT");
+      return !(e && e[0] == '0') && dh_ok;
+    }();
+    return on;
+  }
+  static constexpr bool dh_ok = true;
   int cmode = 0;  // causal tile/K skipping for the per-head S x S products (sd_gemm.cu)
   // Products with residual arrays use them (on-chip residuals for the MN-major-A
   // weight products measured neutral on the whole HVP: SD_GEMM_ONCHIP=1).
@@ -645,8 +673,12 @@ struct sd_gpt_s {
     const Op Pm{Ly.P, Ly.Ps, Sq, false, hs, bs}, dPm{Ly.dP, Ly.dPs, Sq, false, hs, bs};
     const Op vv{Ly.a + 2 * d, Ly.as + 2 * d, 3 * d, true, ha, ba}, dvv{Ly.da + 2 * d, Ly.das + 2 * d, 3 * d, true, ha, ba};
     cmode = 2;  // P, dP lower-triangular: keys k <= query i
-    mm(Sq, dh, Sq, Pm, vv, Ly.o, d, 1, 0, st, nullptr, Ly.os, H, B, ho, bo);
-    mm2(Sq, dh, Sq, dPm, vv, Pm, dvv, Ly.dO, d, 1, 0, st, nullptr, Ly.dOs, H, B, ho, bo);
+    if (dh == 64 && split_pairs()) {
+      mm_pair(Sq, Sq, Pm, vv, dvv, dPm, Ly.o, Ly.os, Ly.dO, Ly.dOs, d, 1.0f, st, H, B, ho, bo);
+    } else {
+      mm(Sq, dh, Sq, Pm, vv, Ly.o, d, 1, 0, st, nullptr, Ly.os, H, B, ho, bo);
+      mm2(Sq, dh, Sq, dPm, vv, Pm, dvv, Ly.dO, d, 1, 0, st, nullptr, Ly.dOs, H, B, ho, bo);
+    }
     cmode = 0;
   }
 
@@ -668,20 +700,34 @@ struct sd_gpt_s {
     const Op PT{Ly.P, Ly.Ps, Sq, true, hs, bs}, dPT{Ly.dP, Ly.dPs, Sq, true, hs, bs};
     const Op goM{go, gos, d, true, ho, bo}, gdoM{gdo, gdos, d, true, ho, bo};
     cmode = 3;  // P^T upper-triangular: queries i >= key j
-    mm(Sq, dh, Sq, PT, goM, ga + 2 * d, 3 * d, 1, 0, st, nullptr, gas + 2 * d, H, B, ha, ba);
-    mm2(Sq, dh, Sq, dPT, goM, PT, gdoM, gda + 2 * d, 3 * d, 1, 0, st, nullptr, gdas + 2 * d, H, B, ha, ba);
+    const bool pairs = dh == 64 && split_pairs();
+    if (pairs) {
+      mm_pair(Sq, Sq, PT, goM, gdoM, dPT, ga + 2 * d, gas + 2 * d, gda + 2 * d, gdas + 2 * d, 3 * d, 1.0f, st, H, B, ha,
+              ba);
+    } else {
+      mm(Sq, dh, Sq, PT, goM, ga + 2 * d, 3 * d, 1, 0, st, nullptr, gas + 2 * d, H, B, ha, ba);
+      mm2(Sq, dh, Sq, dPT, goM, PT, gdoM, gda + 2 * d, 3 * d, 1, 0, st, nullptr, gdas + 2 * d, H, B, ha, ba);
+    }
     // query adjoints
     const Op gS{gP, gPs, Sq, false, hs, bs}, gdS{gdP, gdPs, Sq, false, hs, bs};
     const Op kM{Ly.a + d, Ly.as + d, 3 * d, true, ha, ba}, dkM{Ly.da + d, Ly.das + d, 3 * d, true, ha, ba};
     cmode = 2;
-    mm(Sq, dh, Sq, gS, kM, ga, 3 * d, sc, 0, st, nullptr, gas, H, B, ha, ba);
-    mm2(Sq, dh, Sq, gdS, kM, gS, dkM, gda, 3 * d, sc, 0, st, nullptr, gdas, H, B, ha, ba);
+    if (pairs) {
+      mm_pair(Sq, Sq, gS, kM, dkM, gdS, ga, gas, gda, gdas, 3 * d, sc, st, H, B, ha, ba);
+    } else {
+      mm(Sq, dh, Sq, gS, kM, ga, 3 * d, sc, 0, st, nullptr, gas, H, B, ha, ba);
+      mm2(Sq, dh, Sq, gdS, kM, gS, dkM, gda, 3 * d, sc, 0, st, nullptr, gdas, H, B, ha, ba);
+    }
     // key adjoints
     const Op gST{gP, gPs, Sq, true, hs, bs}, gdST{gdP, gdPs, Sq, true, hs, bs};
     const Op qM{Ly.a, Ly.as, 3 * d, true, ha, ba}, dqM{Ly.da, Ly.das, 3 * d, true, ha, ba};
     cmode = 3;
-    mm(Sq, dh, Sq, gST, qM, ga + d, 3 * d, sc, 0, st, nullptr, gas + d, H, B, ha, ba);
-    mm2(Sq, dh, Sq, gdST, qM, gST, dqM, gda + d, 3 * d, sc, 0, st, nullptr, gdas + d, H, B, ha, ba);
+    if (pairs) {
+      mm_pair(Sq, Sq, gST, qM, dqM, gdST, ga + d, gas + d, gda + d, gdas + d, 3 * d, sc, st, H, B, ha, ba);
+    } else {
+      mm(Sq, dh, Sq, gST, qM, ga + d, 3 * d, sc, 0, st, nullptr, gas + d, H, B, ha, ba);
+      mm2(Sq, dh, Sq, gdST, qM, gST, dqM, gda + d, 3 * d, sc, 0, st, nullptr, gdas + d, H, B, ha, ba);
+    }
     cmode = 0;
   }
 };
