@@ -29,6 +29,7 @@ ap.add_argument("--ncu", action="store_true", help="run one HVP only (the ncu pa
 ap.add_argument("--summarise", default=None, help="ncu csv log to summarise")
 ap.add_argument("--shapes", default=str(ROOT / "gpurun_out" / "gemm_shapes.csv"))
 ap.add_argument("--out", default=str(ROOT / "profiles" / "gemm_traffic.json"))
+ap.add_argument("--batch", type=int, default=8, help="sequences of 1024 tokens (8 = the bench; 1 = one rank at N = 8)")
 a = ap.parse_args()
 
 if a.summarise:
@@ -61,7 +62,7 @@ import torch  # noqa: E402
 from paper_2505_11564_b200 import gpt  # noqa: E402
 from paper_2505_11564_b200._lib import check, lib  # noqa: E402
 
-eng = gpt.GptHvp(gpt.GPT2_SMALL, 8, 1024, init_seed=0)
+eng = gpt.GptHvp(gpt.GPT2_SMALL, a.batch, 1024, init_seed=0)
 v = torch.randn(eng.P, device="cuda", generator=torch.Generator(device="cuda").manual_seed(7)).contiguous()
 if a.ncu:
     eng.hvp(v)
