@@ -375,7 +375,20 @@ class WorkerPool {
     std::vector<std::promise<void>> ready(n);
     for (std::size_t w = 0; w < n; ++w)
       workers_[w]->thread = std::thread([this, w, p = &ready[w]] { worker_main(w, *p); });
-    for (auto& p : ready) p.get_future().get();  // streams exist before the first message
+    std::exception_ptr failed;
+    for (auto& p : ready) {  // streams exist before the first message
+      try {
+        p.get_future().get();
+      } catch (...) {
+        if (!failed) failed = std::current_exception();
+      }
+    }
+    if (failed) {  // release the workers that did start, then report the first failure
+      shut_down_ = true;
+      for (std::size_t w = 0; w < n; ++w) enqueue(w, MsgKind::Shutdown, nullptr);
+      for (auto& wk : workers_) wk->thread.join();
+      std::rethrow_exception(failed);
+    }
   }
   ~WorkerPool() {
     shut_down_ = true;

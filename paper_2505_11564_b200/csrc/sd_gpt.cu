@@ -22,6 +22,7 @@
 #include <algorithm>
 #include <cmath>
 #include <memory>
+#include <cstring>
 #include <numeric>
 #include <string>
 #include <vector>
@@ -165,7 +166,21 @@ struct sd_gpt_s {
   float* red = nullptr;  // column-reduction scratch
   // per micro-batch m: tok/tgt/upos at m T, uniq/ustart at m (T + 1)
   int *tok = nullptr, *tgt = nullptr, *uniq = nullptr, *ustart = nullptr, *upos = nullptr;
-  std::vector<int> n_uniq_mb;
+  int* nuniq = nullptr;  // [nmb] distinct tokens per micro-batch (device)
+  // pinned staging of the host tokens | targets (set_batch returns before the
+  // upload runs; the next call waits for the previous upload's event)
+  int* h_stage = nullptr;
+  cudaEvent_t ev_stage = nullptr;
+  void* csr_scratch = nullptr;  // device scratch of gpt_token_csr (allocated at the first set_batch)
+  size_t csr_bytes = 0;
+  ~sd_gpt_s() {
+    if (csr_scratch) cudaFree(csr_scratch);
+    if (ev_stage) {
+      cudaEventSynchronize(ev_stage);
+      cudaEventDestroy(ev_stage);
+    }
+    if (h_stage) cudaFreeHost(h_stage);
+  }
   float loss_scale = 1.0f;
   bool have_batch = false;
   std::vector<double> h_loss;
@@ -242,7 +257,7 @@ struct sd_gpt_s {
     red = p.take<float>(sd::kColredReserve + 2LL * 64 * std::max(3 * d, ff));
     if (first) {
       tok = p.take<int>(T_ * nmb), uniq = p.take<int>((T_ + 1) * nmb), ustart = p.take<int>((T_ + 1) * nmb);
-      upos = p.take<int>(T_ * nmb);
+      upos = p.take<int>(T_ * nmb), nuniq = p.take<int>(nmb);
     }
     if (last) tgt = p.take<int>(T_ * nmb);
     use_set(0);
@@ -441,7 +456,7 @@ struct sd_gpt_s {
     // embeddings (wte also carries the head contribution written above)
     if (!acc) SD_CUDA(cudaMemsetAsync(HV(1), 0, slots[1].rows * slots[1].cols * sizeof(float), st));
     sd::gpt_embed_bwd(uniq + (long long)m * (T + 1), ustart + (long long)m * (T + 1), upos + (long long)m * T,
-                      n_uniq_mb[m], B, S, d, gdx, HV(0), HV(1), st, int(acc));
+                      nuniq + m, B, S, d, gdx, HV(0), HV(1), st, int(acc));
   }
 
   void gpt2_layer_bwd(Layer& Ly, int l, float hb, cudaStream_t st) {
@@ -603,7 +618,7 @@ struct sd_gpt_s {
     if (first) {
       if (!acc) SD_CUDA(cudaMemsetAsync(HV(0), 0, slots[0].rows * slots[0].cols * sizeof(float), st));
       sd::gpt_embed_bwd(uniq + (long long)m * (T + 1), ustart + (long long)m * (T + 1), upos + (long long)m * T,
-                        n_uniq_mb[m], B, S, d, gdx, HV(0), nullptr, st);
+                        nuniq + m, B, S, d, gdx, HV(0), nullptr, st);
     }
   }
 
@@ -1001,30 +1016,29 @@ sd_status sd_gpt_set_batch(sd_gpt g, const int* tokens, const int* targets, floa
       if (tokens[t] < 0 || tokens[t] >= g->c.vocab || targets[t] < 0 || targets[t] >= g->c.vocab)
         fail(SD_ARGUMENT_ERROR, "token id out of range");
     cudaStream_t st = (cudaStream_t)s;
-    g->n_uniq_mb.assign(M, 0);
-    if (g->first) {
-      std::vector<int> uniq(size_t(T + 1) * M, 0), start(size_t(T + 1) * M, 0), order(size_t(T) * M);
-      for (int m = 0; m < M; ++m) {
-        const int* tk = tokens + (long long)m * T;
-        int* ord = order.data() + (long long)m * T;
-        std::iota(ord, ord + T, 0);
-        std::stable_sort(ord, ord + T, [&](int a, int b) { return tk[a] < tk[b]; });
-        int* u = uniq.data() + (long long)m * (T + 1);
-        int* st0 = start.data() + (long long)m * (T + 1);
-        int n = 0;
-        for (int i = 0; i < T; ++i)
-          if (i == 0 || tk[ord[i]] != tk[ord[i - 1]]) u[n] = tk[ord[i]], st0[n++] = i;
-        st0[n] = T;
-        g->n_uniq_mb[m] = n;
-      }
-      SD_CUDA(cudaMemcpyAsync(g->tok, tokens, size_t(T) * M * sizeof(int), cudaMemcpyHostToDevice, st));
-      SD_CUDA(cudaMemcpyAsync(g->uniq, uniq.data(), uniq.size() * sizeof(int), cudaMemcpyHostToDevice, st));
-      SD_CUDA(cudaMemcpyAsync(g->ustart, start.data(), start.size() * sizeof(int), cudaMemcpyHostToDevice, st));
-      SD_CUDA(cudaMemcpyAsync(g->upos, order.data(), order.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+    // tokens | targets through the engine's pinned staging buffer (the caller's
+    // buffers are free on return); the embedding backward's CSR is built on
+    // the device (gpt_token_csr), so the call never waits for the GPU's work
+    const size_t n = size_t(T) * M;
+    if (!g->h_stage) {
+      SD_CUDA(cudaMallocHost(&g->h_stage, 2 * n * sizeof(int)));
+      SD_CUDA(cudaEventCreateWithFlags(&g->ev_stage, cudaEventDisableTiming));
+    } else {
+      SD_CUDA(cudaEventSynchronize(g->ev_stage));  // the previous upload has read the staging buffer
     }
-    if (g->last)
-      SD_CUDA(cudaMemcpyAsync(g->tgt, targets, size_t(T) * M * sizeof(int), cudaMemcpyHostToDevice, st));
-    SD_CUDA(cudaStreamSynchronize(st));
+    std::memcpy(g->h_stage, tokens, n * sizeof(int));
+    std::memcpy(g->h_stage + n, targets, n * sizeof(int));
+    if (g->first) {
+      SD_CUDA(cudaMemcpyAsync(g->tok, g->h_stage, n * sizeof(int), cudaMemcpyHostToDevice, st));
+      if (!g->csr_scratch) {
+        g->csr_bytes = sd::gpt_token_csr_scratch(T, M, g->c.vocab);
+        SD_CUDA(cudaMalloc(&g->csr_scratch, g->csr_bytes));
+      }
+      sd::gpt_token_csr(g->tok, T, M, g->c.vocab, g->uniq, g->ustart, g->upos, g->nuniq, g->csr_scratch, g->csr_bytes,
+                        st);
+    }
+    if (g->last) SD_CUDA(cudaMemcpyAsync(g->tgt, g->h_stage + n, n * sizeof(int), cudaMemcpyHostToDevice, st));
+    SD_CUDA(cudaEventRecord(g->ev_stage, st));
     g->loss_scale = loss_scale;
     g->have_batch = true;
   });

@@ -59,8 +59,12 @@ void gpt_ce(float* z, float* dz, float* zs, float* dzs, const int* tgt, int T, i
             double* loss_rows, cudaStream_t s);
 // Hv of the embeddings: hv_wte rows += scattered adjoint tangents; hv_wpe
 // = (acc: +=) the per-position sums
-void gpt_embed_bwd(const int* uniq, const int* start, const int* pos, int n_uniq, int B, int S, int d,
+void gpt_embed_bwd(const int* uniq, const int* start, const int* pos, const int* n_uniq_dev, int B, int S, int d,
                    const float* gdx, float* hv_wte, float* hv_wpe, cudaStream_t s, int acc = 0);
+// device-side token -> positions CSR of M micro-batches of T tokens (see sd_gpt_kernels.cu)
+size_t gpt_token_csr_scratch(int T, int M, int V);
+void gpt_token_csr(const int* tok, int T, int M, int V, int* uniq, int* ustart, int* upos, int* nuniq,
+                   void* scratch, size_t scratch_bytes, cudaStream_t s);
 void gpt_residual(const float* x, float* xs, long long n, cudaStream_t s);
 void gpt_fill(float* x, float v, long long n, cudaStream_t s);
 // theta[i - th_base] for global flat indices i in [off, off + n)

@@ -8,6 +8,9 @@
 // Notation: X primal, dX tangent (R-op), gX adjoint, gdX adjoint tangent.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
+
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
 #include <math.h>
 #include <stdint.h>
 
@@ -893,11 +896,12 @@ __global__ void k_swiglu_bwd(const float* __restrict__ fu, const float* __restri
 // Hv_wte[v] += sum over positions with token v of gdx (CSR by token, fixed
 // order), one warp per (token, 32-column slab). Hv_wpe[s] = sum_b gdx[b,s].
 __global__ void k_embed_bwd_wte(const int* __restrict__ uniq, const int* __restrict__ start,
-                                const int* __restrict__ pos, int n_uniq, int d, const float* __restrict__ gdx,
-                                float* __restrict__ hv_wte) {
+                                const int* __restrict__ pos, const int* __restrict__ n_uniq_dev, int d,
+                                const float* __restrict__ gdx, float* __restrict__ hv_wte) {
   const long long w = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   const int slabs = (d + 31) / 32;
+  const int n_uniq = *n_uniq_dev;
   if (w >= (long long)n_uniq * slabs) return;
   const int u = int(w / slabs), slab = int(w % slabs);
   const int col = slab * 32 + lane;
@@ -1105,17 +1109,99 @@ void gpt_ce(float* z, float* dz, float* zs, float* dzs, const int* tgt, int T, i
   SD_LAUNCHED("k_ce");
 }
 
-void gpt_embed_bwd(const int* uniq, const int* start, const int* pos, int n_uniq, int B, int S, int d,
+void gpt_embed_bwd(const int* uniq, const int* start, const int* pos, const int* n_uniq_dev, int B, int S, int d,
                    const float* gdx, float* hv_wte, float* hv_wpe, cudaStream_t s, int acc) {
-  const long long warps = (long long)n_uniq * ((d + 31) / 32);
+  // one warp per (unique token, 32-column slab); the count of unique tokens
+  // is device-resident (built by gpt_token_csr): size the grid for all T rows
+  const long long warps = (long long)B * S * ((d + 31) / 32);
   if (warps > 0) {
-    k_embed_bwd_wte<<<g1(warps, 8), 256, 0, s>>>(uniq, start, pos, n_uniq, d, gdx, hv_wte);
+    k_embed_bwd_wte<<<g1(warps, 8), 256, 0, s>>>(uniq, start, pos, n_uniq_dev, d, gdx, hv_wte);
     SD_LAUNCHED("k_embed_bwd_wte");
   }
   if (hv_wpe) {
     k_embed_bwd_wpe<<<g1((long long)S * d), 256, 0, s>>>(gdx, B, S, d, hv_wpe, acc);
     SD_LAUNCHED("k_embed_bwd_wpe");
   }
+}
+
+// ---- token -> positions CSR of the deterministic embedding backward, built
+// on the device from the uploaded tokens (sd_gpt_set_batch): per micro-batch
+// the distinct tokens in ascending order (uniq), the start of each one's run
+// of positions (ustart, + T at n), the positions sorted stably by token
+// (upos), and the distinct-token count (nuniq). One stable radix sort of the
+// composite key m * V + token over all micro-batches, a head scan, a fill.
+__global__ void k_csr_keys(const int* __restrict__ tok, int T, long long n, int V, int* __restrict__ keys,
+                           int* __restrict__ vals) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int m = int(i / T);
+  keys[i] = m * V + tok[i];
+  vals[i] = int(i - (long long)m * T);
+}
+__global__ void k_csr_heads(const int* __restrict__ keys, int T, long long n, int* __restrict__ flag) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  flag[i] = (i % T == 0 || keys[i] != keys[i - 1]) ? 1 : 0;
+}
+__global__ void k_csr_fill(const int* __restrict__ keys, const int* __restrict__ flag, const int* __restrict__ scan,
+                           int T, long long n, int V, int* __restrict__ uniq, int* __restrict__ ustart,
+                           int* __restrict__ nuniq) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int m = int(i / T), li = int(i - (long long)m * T);
+  const long long seg = (long long)m * T;
+  const int u = scan[i] - scan[seg];
+  int* um = uniq + (long long)m * (T + 1);
+  int* sm = ustart + (long long)m * (T + 1);
+  if (flag[i]) {
+    um[u] = keys[i] - m * V;
+    sm[u] = li;
+  }
+  if (li == T - 1) {
+    const int cnt = u + flag[i];
+    nuniq[m] = cnt;
+    sm[cnt] = T;
+  }
+}
+
+size_t gpt_token_csr_scratch(int T, int M, int V) {
+  const long long n = (long long)T * M;
+  int end_bit = 1;
+  while ((1LL << end_bit) < (long long)M * V) ++end_bit;
+  size_t sort_bytes = 0, scan_bytes = 0;
+  SD_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, (const int*)nullptr, (int*)nullptr,
+                                          (const int*)nullptr, (int*)nullptr, int(n), 0, end_bit));
+  SD_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, (const int*)nullptr, (int*)nullptr, int(n)));
+  return size_t(n) * 5 * sizeof(int) + std::max(sort_bytes, scan_bytes) + 256;
+}
+
+void gpt_token_csr(const int* tok, int T, int M, int V, int* uniq, int* ustart, int* upos, int* nuniq,
+                   void* scratch, size_t scratch_bytes, cudaStream_t s) {
+  const long long n = (long long)T * M;
+  int end_bit = 1;
+  while ((1LL << end_bit) < (long long)M * V) ++end_bit;
+  size_t sort_bytes = 0, scan_bytes = 0;
+  SD_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, (const int*)nullptr, (int*)nullptr,
+                                          (const int*)nullptr, (int*)nullptr, int(n), 0, end_bit, s));
+  SD_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, (const int*)nullptr, (int*)nullptr, int(n), s));
+  const size_t ints = size_t(n) * 5;  // keys, vals, keys_sorted, flag, scan
+  if (scratch_bytes < ints * sizeof(int) + std::max(sort_bytes, scan_bytes) + 256)
+    fail(SD_ARGUMENT_ERROR, "token CSR scratch too small");
+  char* buf = static_cast<char*>(scratch);
+  int* keys = reinterpret_cast<int*>(buf);
+  int* vals = keys + n;
+  int* ksorted = vals + n;
+  int* flag = ksorted + n;
+  int* scan = flag + n;
+  void* temp = reinterpret_cast<void*>((reinterpret_cast<uintptr_t>(scan + n) + 255) & ~uintptr_t(255));
+  k_csr_keys<<<g1(n), 256, 0, s>>>(tok, T, n, V, keys, vals);
+  SD_LAUNCHED("k_csr_keys");
+  SD_CUDA(cub::DeviceRadixSort::SortPairs(temp, sort_bytes, keys, ksorted, vals, upos, int(n), 0, end_bit, s));
+  k_csr_heads<<<g1(n), 256, 0, s>>>(ksorted, T, n, flag);
+  SD_LAUNCHED("k_csr_heads");
+  SD_CUDA(cub::DeviceScan::ExclusiveSum(temp, scan_bytes, flag, scan, int(n), s));
+  k_csr_fill<<<g1(n), 256, 0, s>>>(ksorted, flag, scan, T, n, V, uniq, ustart, nuniq);
+  SD_LAUNCHED("k_csr_fill");
 }
 
 void llama_rope(float* a, float* as, float* da, float* das, int T, int S, int d, int dh, float base, int inverse,
