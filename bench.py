@@ -74,6 +74,14 @@ def workload_config(args):
             "k_max": args.k_max, "reorth": "full", "probes": 10}
 
 
+def probe_seed_plan(base: int, rank: int, world: int, probes: bool):
+    """(first probe seed, stride) of a rank's chains: with probe partitioning
+    rank r runs seeds base + r, base + r + N, ... -- together the ranks cover
+    base, base + 1, ... exactly once (the SLQ job's probes); otherwise every
+    rank drives the same sharded chains base, base + 1, ..."""
+    return (base + rank, world) if probes else (base, 1)
+
+
 def cpu_model() -> str:
     try:
         for line in open("/proc/cpuinfo"):
@@ -291,24 +299,31 @@ def run_ours(args):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    use_comm = world > 1 or args.comm
-    if use_comm:
+    c1, c3 = args.workload == "c1", args.workload == "c3"
+    # N > 1: C3 is data-sharded (the global batch over the ranks, Hv summed);
+    # C1/C2 -- one B200 each by BASELINE -- are SLQ jobs of independent probe
+    # chains, so their ranks run disjoint probes with no collective on the data
+    # path (--partition data runs the data-sharded variant instead)
+    partition = args.partition or ("data" if c3 else "probes")
+    probes = world > 1 and partition == "probes"
+    dworld, drank = (1, 0) if probes else (world, rank)
+    use_comm = (world > 1 and not probes) or args.comm
+    if world > 1 or args.comm:
         if world == 1:  # --comm: the multi-rank code path on one rank (NCCL, no peers)
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
             os.environ.setdefault("MASTER_PORT", "29541")
             dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", local))
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    c1, c3 = args.workload == "c1", args.workload == "c3"
     cfg = C1_MODEL if c1 else (C3_MODEL if c3 else GPT2_SMALL)
     B, S = (4, 32) if c1 else ((32, 2048) if c3 else (args.batch, args.seq))
     k_max = 32 if c1 else args.k_max
-    if B % world:
-        raise SystemExit(f"global batch {B} not divisible by {world} ranks")
-    b_loc = B // world
+    if B % dworld:
+        raise SystemExit(f"global batch {B} not divisible by {dworld} ranks")
+    b_loc = B // dworld
     T_glob = B * S
     tok_all, tgt_all = gpt.synthetic_tokens(cfg["vocab"], B, S, seed=1)
-    sl = slice(rank * b_loc * S, (rank + 1) * b_loc * S)
+    sl = slice(drank * b_loc * S, (drank + 1) * b_loc * S)
     if c3:  # b_loc sequences as micro-batches of one sequence, layers recomputed in the backward
         eng = gpt.GptHvp(cfg, 1, S, init_seed=0, tokens=tok_all[sl], targets=tgt_all[sl], loss_scale=1.0 / T_glob,
                          micro_batches=b_loc, recompute=args.c3_recompute)
@@ -319,23 +334,26 @@ def run_ours(args):
     P = eng.P
     # N > 1: Lanczos vectors parameter-sharded over the ranks (split_evenly);
     # each apply all-gathers q, runs the rank's batch HVP and reduce-scatters Hv
-    layout = sd.split_evenly(P, world) if use_comm else None
+    layout = sd.split_evenly(P, dworld) if use_comm else None
     op = eng.operator(comm, layout=layout)
-    P_local = (layout.shard_bounds[rank][1] - layout.shard_bounds[rank][0]) if layout else P
+    P_local = (layout.shard_bounds[drank][1] - layout.shard_bounds[drank][0]) if layout else P
     reduction = sd.REDUCE_TREE if args.reduction == "tree" else sd.REDUCE_ORDERED
     reorth = sd.REORTH_SELECTIVE if (c3 and args.c3_reorth == "selective") else sd.REORTH_FULL
     window = args.window if reorth == sd.REORTH_SELECTIVE else 0
     lcfg = lambda seed: sd.LanczosConfig(k_max=k_max, reorthogonalize=reorth, prec=sd.F32,  # noqa: E731
                                          probe=sd.ProbeSpec(seed=seed, distribution=sd.RADEMACHER),
                                          reduction=reduction, selective_window=window)
-    state = {"probe": 42 if c1 else 0, "L": None, "ws": None}
+    # probe chains: seeds base, base + 1, ...; with probe partitioning rank r
+    # takes seeds base + r, base + r + N, ... (its share of the SLQ job's probes)
+    first_seed, pstride = probe_seed_plan(42 if c1 else 0, rank, world, probes)
+    state = {"probe": first_seed, "L": None, "ws": None}
 
     def new_chain():
         if state["L"] is not None:
             state["L"].close()
         state["L"] = sd.Lanczos(op, lcfg(state["probe"]), layout=layout, comm=comm, workspace=state["ws"])
         state["ws"] = state["L"].workspace
-        state["probe"] += 1
+        state["probe"] += pstride
 
     def step():
         if state["L"] is None or state["L"].done:
@@ -375,7 +393,9 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_total = float(t.item())
     ms_step = ms_total / args.steps
-    value = 1000.0 / ms_step
+    # whole job: every rank advanced its own chain (probe partitioning) or all
+    # ranks advanced the one sharded chain together
+    value = (world if probes else 1) * 1000.0 / ms_step
 
     # ---- e2e: the public step API with host buffers, every step: H2D of the
     # step's batch tokens (pinned) + Lanczos step + D2H of (alpha, beta)
@@ -386,7 +406,7 @@ def run_ours(args):
     # window (full-reorth cost grows with the column): the timed chain's probe
     # is restarted and advanced, untimed, to e2e_steps steps centred on the
     # timed window's centre
-    state["probe"] -= 1
+    state["probe"] -= pstride
     new_chain()
     centre = (j_first + j_last) // 2
     for _ in range(max(0, centre - e2e_steps // 2 - 1)):
@@ -439,18 +459,20 @@ def run_ours(args):
     # columns + r, scale), ordered mode 4 P (7 + 3 j)
     j_eff = min(k_mid, window) if window else k_mid
     lanczos_bytes = 4.0 * P_local * ((3 * j_eff + 8) if reduction == sd.REDUCE_TREE else (7 + 3 * j_eff))
-    step_roof_ms = gemm_flops_per_step(cfg, B * S, S) / world / (tc_peak * 1e12) * 1e3 + lanczos_bytes / (hbm * 1e9) * 1e3
+    step_roof_ms = gemm_flops_per_step(cfg, B * S, S) / dworld / (tc_peak * 1e12) * 1e3 + lanczos_bytes / (hbm * 1e9) * 1e3
     cfgd = workload_config(args)
     line = {
         "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "weak" if probes else "strong",
         "vs_baseline": None, "dtype": "f32 (3xTF32 tensor-core GEMMs, fp32 storage, f64 Lanczos scalars)",
         "data": "synthetic (counter-keyed tokens, random-init weights)",
         "config": cfgd,
         "run": {"reorth_columns_timed": [j_first, j_last], "untimed_advance_steps": advance,
-                "reduction": args.reduction, "parallelism": (f"dp{world} batch x {world}-way sharded Lanczos "
-                                                             f"(all-gather q, reduce-scatter Hv)" if layout is not None
-                                                             else "dp1"),
+                "reduction": args.reduction,
+                "parallelism": (f"{world} ranks x independent probe chains (no data-path collective)" if probes else
+                                f"dp{world} batch x {world}-way sharded Lanczos (all-gather q, reduce-scatter Hv)"
+                                if layout is not None else "dp1"),
                 "l2": ("C1 fits in L2 (226 KB vectors)" if c1 else
                        "inputs larger than L2 (Lanczos vectors >= 0.5 GB, activations >= 10 GB)"),
                 "memory_gb": {"hvp_workspace": eng.workspace.numel() / 1e9,
@@ -470,7 +492,7 @@ def run_ours(args):
                      "gemm_launches_per_step": int(g_n.value) / prof_steps},
         "roofline_step": {"bound": "tensor+hbm", "roofline_ms": step_roof_ms, "measured_ms": ms_step,
                           "frac": step_roof_ms / ms_step, "lanczos_bytes": lanczos_bytes, "hbm_peak_gbs": hbm},
-        "e2e": {"value": 1000.0 / e2e_ms, "unit": "steps/s", "h2d_bytes_per_step": int(2 * tok_pin.numel() * 4),
+        "e2e": {"value": (world if probes else 1) * 1000.0 / e2e_ms, "unit": "steps/s", "h2d_bytes_per_step": int(2 * tok_pin.numel() * 4),
                 "d2h_bytes_per_step": 16, "steps": e2e_steps,
                 "reorth_columns": [e2e_first, e2e_first + e2e_steps - 1]},
         "gpu_launches": int(launches),
@@ -494,7 +516,7 @@ def run_ours(args):
     state["L"].close()
     if comm is not None:
         comm.close()
-    if use_comm:
+    if world > 1 or args.comm:
         dist.destroy_process_group()
 
 
@@ -611,6 +633,9 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--comm", action="store_true", help="use the NCCL/sharded path even on one rank")
+    ap.add_argument("--partition", default=None, choices=["probes", "data"],
+                    help="N > 1: probes (independent probe chains per rank; default for c1/c2) or data "
+                         "(data-sharded HVP + parameter-sharded Lanczos; default for c3)")
     ap.add_argument("--c3-reorth", default="selective", choices=["selective", "full"],
                     help="C3: selective (window --window, fits one GPU) or full (sharded basis, N >= 4)")
     ap.add_argument("--window", type=int, default=16, help="selective reorth window (C3)")

@@ -158,3 +158,17 @@ def test_parameter_sharded_lanczos_apply():
     for r in res.values():
         assert isinstance(r, dict), r
         assert r["gathered_exact"] and r["rel"] < 1e-12
+
+
+def test_bench_probe_partition_covers_every_probe_once():
+    # bench.py --gpus N (C1/C2): rank r runs probe chains r, r + N, ... -- the
+    # ranks together run the SLQ job's probes 0..n-1 exactly once, and the
+    # data-sharded partition drives the same chain on every rank
+    import bench
+    for world in (1, 2, 4, 8):
+        seen = []
+        for r in range(world):
+            first, stride = bench.probe_seed_plan(0, r, world, True)
+            seen += [first + i * stride for i in range(10 // world + 1) if first + i * stride < 10]
+        assert sorted(seen) == list(range(10))
+        assert all(bench.probe_seed_plan(42, r, world, False) == (42, 1) for r in range(world))
