@@ -113,3 +113,23 @@ def test_tree_rejects_too_many_columns(sd):
     op = sd.dense_operator(np.eye(512))
     with pytest.raises(sd.ConfigError):
         sd.lanczos_run(op, sd.LanczosConfig(k_max=300, reorthogonalize=sd.REORTH_FULL, reduction=sd.REDUCE_TREE))
+
+
+def test_tree_on_the_bench_operator(sd):
+    """The bench path itself: GPT-2-small (124M parameters, one 1024-token
+    sequence) HVP driving full-reorth Lanczos in tree mode vs ordered mode --
+    the same Hv (deterministic engine), only the reductions differ: alpha/beta
+    within 2e-6 of ||T|| over 10 steps, basis orthonormal."""
+    from paper_2505_11564_b200 import gpt
+    eng = gpt.GptHvp(gpt.GPT2_SMALL, 1, 1024, init_seed=0)
+    base = dict(k_max=10, reorthogonalize=sd.REORTH_FULL, prec=sd.F32,
+                probe=sd.ProbeSpec(seed=0, distribution=sd.RADEMACHER))
+    a = sd.lanczos_run(eng.operator(), sd.LanczosConfig(**base))
+    b = sd.lanczos_run(eng.operator(), sd.LanczosConfig(**base, reduction=sd.REDUCE_TREE))
+    assert tdiff(b, a) <= 2e-6, tdiff(b, a)
+    L = sd.Lanczos(eng.operator(), sd.LanczosConfig(**base, reduction=sd.REDUCE_TREE))
+    while not L.step():
+        pass
+    assert L.loss_of_orthogonality() < 1e-5
+    L.close()
+    eng.close()
