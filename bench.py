@@ -230,7 +230,7 @@ def cpu_c2_step(B, S, k_mid, seqs=(8, 64), full_recurrence=True):
 
 def cpu_baseline_c2(B, S, k_mid):
     from oracle.pyoracle import nthreads
-    sec, legs = cpu_c2_step(B, S, k_mid, seqs=(8, 64), full_recurrence=False)
+    sec, legs = cpu_c2_step(B, S, k_mid, seqs=(8, 32), full_recurrence=False)
     return {"value": 1.0 / sec, "unit": "steps/s", "cores": nthreads(), "kind": "port", "extrapolated": True,
             "cpu_model": cpu_model(), "legs": legs,
             "sample": "one C2 step extrapolated from bounded samples: " + legs["hvp"]["sample"] + "; "
