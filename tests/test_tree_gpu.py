@@ -133,3 +133,32 @@ def test_tree_on_the_bench_operator(sd):
     assert L.loss_of_orthogonality() < 1e-5
     L.close()
     eng.close()
+
+
+def test_tree_edge_cases(sd):
+    # SPEC.md:263 identity: alpha0 = 1, beta0 below eps -> benign breakdown at k = 1;
+    # diag(1,2,3) recovers its eigenvalues; a short vector (P < one 128-element tile)
+    for prec in (sd.F32, sd.F64):
+        r = sd.lanczos_run(sd.dense_operator(np.eye(64)),
+                           sd.LanczosConfig(k_max=10, reorthogonalize=sd.REORTH_FULL, prec=prec,
+                                            reduction=sd.REDUCE_TREE,
+                                            probe=sd.ProbeSpec(seed=1, distribution=sd.RADEMACHER)))
+        assert r.alphas.size == 1 and abs(r.alphas[0] - 1.0) < 1e-6 and r.breakdown
+    r = sd.lanczos_run(sd.dense_operator(np.diag([1.0, 2.0, 3.0])),
+                       sd.LanczosConfig(k_max=3, reorthogonalize=sd.REORTH_FULL, prec=sd.F64, reduction=sd.REDUCE_TREE,
+                                        probe=sd.ProbeSpec(seed=0, distribution=sd.RADEMACHER)))
+    ritz = sd.ritz_decompose(r.alphas, r.betas)
+    assert np.max(np.abs(ritz.values - [1, 2, 3])) < 1e-10
+    # a non-finite operator output -> NumericalError with the partial tridiagonal
+    import ctypes as C
+
+    def nan_apply(x, y, s):
+        t = torch.full((64,), float("nan"), dtype=torch.float64, device="cuda")
+        sd._lib.lib().sd_k_scale(C.c_void_p(t.data_ptr()), C.c_void_p(y), 64,
+                                 C.c_void_p(torch.ones(1, dtype=torch.float64, device="cuda").data_ptr()), 0, sd.F64,
+                                 C.c_void_p(s))
+        torch.cuda.synchronize()
+        return 0
+    with pytest.raises(sd.NumericalError):
+        sd.lanczos_run(sd.custom_operator(64, nan_apply, "nan"),
+                       sd.LanczosConfig(k_max=5, prec=sd.F64, reduction=sd.REDUCE_TREE))
