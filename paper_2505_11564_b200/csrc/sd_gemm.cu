@@ -809,7 +809,7 @@ void gemm(const GemmArgs& g_in, cudaStream_t s) {
   // On-chip residuals (onchip = allowed): they halve the operand bytes through
   // L2 and TMA but add a shared-memory read + write of every staged tile, and
   // measured slower wherever residual arrays exist (K-major pair products 258
-  // -> 162 TF/s; the dual weight products 176 -> 158, scratch/ab_wgrad.py).
+  // -> 162 TF/s; the dual weight products 176 -> 158, round-1 A/B, profiles/r01_*).
   // So they are used where arrays do not exist (attention P, dP, gS, gdS).
   (void)pair;
   if (g.onchip) {

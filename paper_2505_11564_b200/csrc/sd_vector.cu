@@ -645,7 +645,7 @@ static bool launch_cgs_fused(const void* Q, uint64_t ldq, uint64_t j, void* r, c
   if (!enabled || mode != 1 || j > uint64_t(kCgsMaxCols) || smem > kMaxSmem) return false;
   // the in-CTA update is a j-long dependent chain per element: beyond ~40
   // columns the element-parallel k_cgs_update followed by the block dots is
-  // faster than the fused single read (measured, scratch/bench_lanczos_kernels.py)
+  // faster than the fused single read (measured in round 1; the tree mode, sd_lanczos_tree.cu, is the fast path)
   if (coef != nullptr && j >= fused_update_max_cols()) {
     constexpr int W = V16<T>::W;
     const uint64_t threads = (local_end + W - 1) / W;
