@@ -112,3 +112,28 @@ def test_pdl_on_off_bitwise(gpt):
         assert r.returncode == 0, r.stderr[-2000:]
         out[tag] = r.stdout.strip().splitlines()[-1]
     assert out["pdl"] == out["nopdl"], out
+
+
+@pytest.mark.parametrize("micro_batches", [1, 2])
+def test_c3_width_vs_torch_f64(gpt, micro_batches):
+    """BASELINE configs[2] width (d 2048, 16 heads of 128, ff 8192, V 50257) at
+    S = 2048 with 4 of its 24 layers, whole or as micro-batches (the full
+    24-layer model gives 5.9e-6 / 6.1e-6 with tools/c3_parity.py, at 170 GB of
+    f64 reference memory: profiles/r02_c3_parity_full.json)."""
+    cfg = dict(n_layer=4, d=2048, n_head=16, ff=8192, vocab=50257, ctx=2048)
+    S = 2048 if micro_batches == 1 else 1024
+    import torch_gpt
+    eng = gpt.GptHvp(cfg, 1, S, init_seed=0, gain_scale=0.05, bias_scale=0.02, micro_batches=micro_batches)
+    v = _rademacher(eng.P, 5)
+    hv = eng.hvp(v).double().cpu()
+    theta = eng.theta.double()
+    tok = torch.tensor(eng._tok, device="cuda").long()
+    tgt = torch.tensor(eng._tgt, device="cuda").long()
+    B = eng.B
+    eng.close()
+    del eng
+    torch.cuda.empty_cache()
+    ref = torch_gpt.hvp(cfg, theta, tok, tgt, B, S, v.double()).cpu()
+    e = float((hv - ref).norm() / ref.norm())
+    print(f"C3 width, 4 layers, {B} x {S}: {e:.3e}")
+    assert e < TOL
