@@ -22,6 +22,13 @@ void diag_apply(const void* d, const void* x, void* y, uint64_t n, int prec, cud
 void comm_allgather(sd_comm c, const void* send, void* recv, uint64_t bytes, cudaStream_t s);
 void comm_allreduce_f32(sd_comm c, float* buf, uint64_t n, cudaStream_t s);
 void comm_reducescatter_f32(sd_comm c, const float* send, float* recv, uint64_t n, cudaStream_t s);
+// variable-length slices [rb[r], re[r]) of a full-length vector (the Lanczos
+// ShardLayout): all-gather of each rank's slice into `full`, and the
+// rank-ordered sum of every rank's `full` over this rank's slice into `mine`
+void comm_allgatherv_f32(sd_comm c, const float* mine, float* full, const uint64_t* rb, const uint64_t* re,
+                         cudaStream_t s);
+void comm_reducescatterv_f32(sd_comm c, const float* full, float* mine, const uint64_t* rb, const uint64_t* re,
+                             cudaStream_t s);
 void comm_send_f32(sd_comm c, const float* buf, uint64_t n, int peer, cudaStream_t s);
 void comm_recv_f32(sd_comm c, float* buf, uint64_t n, int peer, cudaStream_t s);
 void comm_group_begin(sd_comm c);

@@ -808,38 +808,26 @@ struct GptOpCtx {
 };
 
 // Parameter-sharded Lanczos over a data-sharded HVP: each rank
-// owns [begin_r, end_r) of the Lanczos vectors; per apply the shards of x are
-// all-gathered (fixed maxlen slots, compacted), the local batch's Hv runs on
-// the full vector, and Hv is reduce-scattered back into the owners' shards --
-// the replicated recurrence and reorthogonalisation shrink by the rank count.
+// owns [begin_r, end_r) of the Lanczos vectors; per apply the slices of x are
+// all-gathered straight into the full vector, the local batch's Hv runs on it,
+// and Hv's slices are reduce-scattered (rank-ordered sums) into the owners'
+// shards -- the replicated recurrence and reorthogonalisation shrink by the
+// rank count, and no padded slots or compaction copies sit on the data path.
 struct GptShardCtx {
   sd_gpt g;
   sd_comm comm;
   int nranks = 1, rank = 0;
   std::vector<uint64_t> rb, re;
-  uint64_t maxlen = 0;
-  float *slots = nullptr, *full = nullptr, *hv = nullptr, *mine = nullptr;
+  float *full = nullptr, *hv = nullptr;
 };
 
 sd_status gpt_shard_apply(void* ctx, const void* x, void* y, sd_stream st) {
   auto* c = static_cast<GptShardCtx*>(ctx);
   return sd::guard([&] {
     const cudaStream_t s = (cudaStream_t)st;
-    const uint64_t n = c->re[c->rank] - c->rb[c->rank], ml = c->maxlen;
-    float* my_slot = c->slots + uint64_t(c->rank) * ml;
-    SD_CUDA(cudaMemcpyAsync(my_slot, x, n * sizeof(float), cudaMemcpyDeviceToDevice, s));
-    sd::comm_allgather(c->comm, my_slot, c->slots, ml * sizeof(float), s);
-    for (int r = 0; r < c->nranks; ++r)
-      SD_CUDA(cudaMemcpyAsync(c->full + c->rb[r], c->slots + uint64_t(r) * ml, (c->re[r] - c->rb[r]) * sizeof(float),
-                              cudaMemcpyDeviceToDevice, s));
+    sd::comm_allgatherv_f32(c->comm, static_cast<const float*>(x), c->full, c->rb.data(), c->re.data(), s);
     c->g->hvp(c->full, c->hv, s);
-    // Hv into rank-major maxlen slots (zero tails), reduce-scatter the slots
-    SD_CUDA(cudaMemsetAsync(c->slots, 0, uint64_t(c->nranks) * ml * sizeof(float), s));
-    for (int r = 0; r < c->nranks; ++r)
-      SD_CUDA(cudaMemcpyAsync(c->slots + uint64_t(r) * ml, c->hv + c->rb[r], (c->re[r] - c->rb[r]) * sizeof(float),
-                              cudaMemcpyDeviceToDevice, s));
-    sd::comm_reducescatter_f32(c->comm, c->slots, c->mine, ml, s);
-    SD_CUDA(cudaMemcpyAsync(y, c->mine, n * sizeof(float), cudaMemcpyDeviceToDevice, s));
+    sd::comm_reducescatterv_f32(c->comm, c->hv, static_cast<float*>(y), c->rb.data(), c->re.data(), s);
   });
 }
 
@@ -1156,7 +1144,7 @@ sd_status sd_operator_gpt_pipeline(sd_gpt g, sd_comm comm, sd_operator* out) {
 }
 
 // Sharded operator: Lanczos vectors split by (begins, ends) over the comm's
-// ranks (f32 only); see GptShardCtx. Scratch (3 full vectors) is owned here.
+// ranks (f32 only); see GptShardCtx. Scratch (2 full vectors) is owned here.
 sd_status sd_operator_gpt_sharded(sd_gpt g, sd_comm comm, const uint64_t* begins, const uint64_t* ends,
                                   sd_operator* out) {
   return sd::guard([&] {
@@ -1172,20 +1160,16 @@ sd_status sd_operator_gpt_sharded(sd_gpt g, sd_comm comm, const uint64_t* begins
       if (begins[r] != at || ends[r] <= begins[r]) sd::fail(SD_LAYOUT_ERROR, "shard bounds leave a gap or overlap");
       c->rb.push_back(begins[r]);
       c->re.push_back(ends[r]);
-      c->maxlen = std::max<uint64_t>(c->maxlen, ends[r] - begins[r]);
       at = ends[r];
     }
     if (at != uint64_t(g->P)) sd::fail(SD_LAYOUT_ERROR, "shard bounds do not cover the parameter vector");
-    const uint64_t slots = uint64_t(c->nranks) * c->maxlen;
-    SD_CUDA(cudaMalloc(&c->slots, slots * sizeof(float)));
     SD_CUDA(cudaMalloc(&c->full, uint64_t(g->P) * sizeof(float)));
     SD_CUDA(cudaMalloc(&c->hv, uint64_t(g->P) * sizeof(float)));
-    SD_CUDA(cudaMalloc(&c->mine, c->maxlen * sizeof(float)));
     const sd_status st = sd_operator_custom(uint64_t(g->P), gpt_shard_apply, c, out);
     if (st != SD_OK) sd::fail(st, "operator_custom failed");
     sd::operator_set_dtor(*out, [](void* p) {
       auto* k = static_cast<GptShardCtx*>(p);
-      for (float* b : {k->slots, k->full, k->hv, k->mine})
+      for (float* b : {k->full, k->hv})
         if (b) cudaFree(b);
       delete k;
     });

@@ -461,6 +461,68 @@ void comm_reducescatter_f32(sd_comm c, const float* send, float* recv, uint64_t 
   nccl_check(nccl().ReduceScatter(send, recv, n, ncclFloat32, ncclSum, c->comm, s), "ncclReduceScatter");
 }
 
+// Variable-length exchanges of a sharded vector, straight between the slices
+// (no padded slots): NCCL moves each slice with one grouped send/recv round,
+// the in-process workers copy from the published buffers. The reduction sums
+// the ranks' contributions in ascending rank order like k_sum_ranks above.
+void comm_allgatherv_f32(sd_comm c, const float* mine, float* full, const uint64_t* rb, const uint64_t* re,
+                         cudaStream_t s) {
+  const int me = c ? c->rank : 0;
+  if (full + rb[me] != mine && re[me] > rb[me])
+    SD_CUDA(cudaMemcpyAsync(full + rb[me], mine, (re[me] - rb[me]) * sizeof(float), cudaMemcpyDeviceToDevice, s));
+  if (!c || c->nranks == 1) return;
+  if (c->local) {
+    local_publish(c, mine, s);
+    for (int q = 0; q < c->nranks; ++q)
+      if (q != me && re[q] > rb[q])
+        SD_CUDA(cudaMemcpyAsync(full + rb[q], c->local->slot[q], (re[q] - rb[q]) * sizeof(float),
+                                cudaMemcpyDeviceToDevice, s));
+    SD_CUDA(cudaStreamSynchronize(s));
+    c->local->barrier();  // every worker has read every slice
+    return;
+  }
+  nccl_check(nccl().GroupStart(), "ncclGroupStart");
+  for (int q = 0; q < c->nranks; ++q) {
+    if (q == me) continue;
+    if (re[me] > rb[me]) nccl_check(nccl().Send(mine, re[me] - rb[me], ncclFloat32, q, c->comm, s), "ncclSend");
+    if (re[q] > rb[q]) nccl_check(nccl().Recv(full + rb[q], re[q] - rb[q], ncclFloat32, q, c->comm, s), "ncclRecv");
+  }
+  nccl_check(nccl().GroupEnd(), "ncclGroupEnd");
+}
+
+void comm_reducescatterv_f32(sd_comm c, const float* full, float* mine, const uint64_t* rb, const uint64_t* re,
+                             cudaStream_t s) {
+  const int me = c ? c->rank : 0;
+  const uint64_t n = re[me] - rb[me];
+  if (!c || c->nranks == 1) {
+    if (n && full + rb[me] != mine)
+      SD_CUDA(cudaMemcpyAsync(mine, full + rb[me], n * sizeof(float), cudaMemcpyDeviceToDevice, s));
+    return;
+  }
+  if (c->local) {
+    local_publish(c, full, s);
+    local_sum(c, rb[me], n, mine, s);
+    SD_CUDA(cudaStreamSynchronize(s));
+    c->local->barrier();
+    return;
+  }
+  const int N = c->nranks;
+  float* slots = grow(c->ord_buf, c->ord_cap, uint64_t(N) * n);
+  nccl_check(nccl().GroupStart(), "ncclGroupStart");
+  for (int q = 0; q < N; ++q) {
+    if (q == me) continue;
+    if (re[q] > rb[q]) nccl_check(nccl().Send(full + rb[q], re[q] - rb[q], ncclFloat32, q, c->comm, s), "ncclSend");
+    if (n) nccl_check(nccl().Recv(slots + uint64_t(q) * n, n, ncclFloat32, q, c->comm, s), "ncclRecv");
+  }
+  nccl_check(nccl().GroupEnd(), "ncclGroupEnd");
+  if (!c->d_ptrs) SD_CUDA(cudaMalloc(&c->d_ptrs, sizeof(float*) * N));
+  std::vector<const float*> h(N);
+  for (int q = 0; q < N; ++q) h[q] = q == me ? full + rb[me] : slots + uint64_t(q) * n;
+  SD_CUDA(cudaMemcpyAsync(c->d_ptrs, h.data(), sizeof(float*) * N, cudaMemcpyHostToDevice, s));
+  if (n) k_sum_ranks<<<unsigned((n + 255) / 256), 256, 0, s>>>(c->d_ptrs, N, 0, n, mine);
+  SD_CUDA(cudaGetLastError());
+}
+
 // Point-to-point (pipeline stages): f32 payloads to/from a peer rank; between
 // group_begin/group_end the sends and receives progress together (NCCL group
 // semantics), which is what makes the 1F1B exchanges deadlock-free.

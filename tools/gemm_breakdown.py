@@ -19,8 +19,13 @@ shp = list(csv.DictReader(open(sys.argv[2])))
 agg = defaultdict(lambda: [0, 0.0, 0.0, 0.0])
 for i, s in zip(order, shp):
     v = by[i]
-    M, N, K, Z, ns = (int(float(s[k])) for k in ("M", "N", "K", "batch", "nsrc"))
-    alg = 4.0 * Z * (ns * (M * K + N * K) + M * N)
+    M, N, K, Z = (int(float(s[k])) for k in ("M", "N", "K", "batch"))
+    if s["nsrc"] == "split":  # A [B | B2] and A2 B: two A operands, B and B2 once, C and C2
+        ns = "split"
+        alg = 4.0 * Z * (2 * M * K + N * K + M * N)
+    else:
+        ns = int(float(s["nsrc"]))
+        alg = 4.0 * Z * (ns * (M * K + N * K) + M * N)
     a = agg[(M, N, K, Z, ns, s["a_mn"], s["b_mn"], s["causal"])]
     a[0] += 1
     a[1] += v["dram__bytes_read.sum"] + v["dram__bytes_write.sum"]
