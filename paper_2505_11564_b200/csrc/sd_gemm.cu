@@ -465,10 +465,10 @@ __global__ void __launch_bounds__(kThreadsFor<TA>(), 1)
         uint32_t hi[16], lo[16];
         if (!A_MN) {
           // row m of the K-major A tile: 64 B, SWIZZLE_64B (16 B chunk c at c ^ ((m >> 1) & 3))
-          const float4* row = reinterpret_cast<const float4*>(st + m * 64);
+          const uint32_t row = smem_u32(st + m * 64);
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
-            const float4 v = row[c ^ ((m >> 1) & 3)];
+            const float4 v = lds128(row + 16u * uint32_t(c ^ ((m >> 1) & 3)));
             const float e[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
@@ -480,10 +480,10 @@ __global__ void __launch_bounds__(kThreadsFor<TA>(), 1)
         } else {
           // MN-major A tile: 32-row chunk q (= this warp) at q * 2048, k-row k of
           // 128 B, 32 B granule (m % 32) / 8 swizzled with k & 3 (SWIZZLE_128B_ATOM_32B)
-          const unsigned char* ch = st + q * 2048 + (lane & 7) * 4;
+          const uint32_t ch = smem_u32(st + q * 2048 + (lane & 7) * 4);
 #pragma unroll
           for (int k = 0; k < 16; ++k) {
-            const float x = *reinterpret_cast<const float*>(ch + k * 128 + (((lane >> 3) ^ (k & 3)) << 5));
+            const float x = lds32(ch + uint32_t(k * 128 + (((lane >> 3) ^ (k & 3)) << 5)));
             const uint32_t h = __float_as_uint(x) & 0xFFFFE000u;
             hi[k] = h;
             lo[k] = __float_as_uint(x - __uint_as_float(h));

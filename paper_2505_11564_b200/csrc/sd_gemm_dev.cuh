@@ -258,6 +258,22 @@ __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.comm
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
+// explicit shared-space vector accesses (a generic pointer into the dynamic
+// smem ring compiles to LD.E / ST.E through the L1TEX long-scoreboard path)
+__device__ __forceinline__ float4 lds128(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts128(uint32_t a, float4 v) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
+}
+__device__ __forceinline__ float lds32(uint32_t a) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+  return v;
+}
+
 // One warp's 32 rows x EC columns (thread = row) of o = alpha*acc (+ bias)
 // -- and, if requested, the tf32 residual of o into Cs -- through a 4 KB
 // 128B-swizzled staging box and TMA stores (full lines; OOB clipped).
@@ -269,7 +285,7 @@ __device__ __forceinline__ void warp_tma_store(const CUtensorMap* mC, const CUte
                                                int row0, int col0, int z1, int z2) {
   constexpr int NQ = BOXC / 4;  // 16 B chunks per staged row
   const int sw = BOXC == 32 ? (lane & 7) : ((lane >> 1) & 3);
-  float4* rowp = reinterpret_cast<float4*>(stage + lane * BOXC);
+  const uint32_t rowa = smem_u32(stage + lane * BOXC);
   bool pending = false;
 #pragma unroll
   for (int c0 = 0; c0 < EC; c0 += BOXC) {
@@ -300,7 +316,7 @@ __device__ __forceinline__ void warp_tma_store(const CUtensorMap* mC, const CUte
           v.z -= __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
           v.w -= __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
         }
-        rowp[q ^ sw] = v;
+        sts128(rowa + 16u * uint32_t(q ^ sw), v);
       }
       fence_proxy_async_smem_decl();
       __syncwarp();
@@ -316,17 +332,16 @@ __device__ __forceinline__ void warp_tma_store(const CUtensorMap* mC, const CUte
 // x - trunc_tf32(x) over a staged operand tile (any smem layout: the residual
 // is elementwise), written to the tile's residual slot; threads t of nt.
 __device__ __forceinline__ void stage_residual(const unsigned char* src, unsigned char* dst, int bytes, int t, int nt) {
-  const float4* s4 = reinterpret_cast<const float4*>(src);
-  float4* d4 = reinterpret_cast<float4*>(dst);
+  const uint32_t s0 = smem_u32(src), d0 = smem_u32(dst);
 #pragma unroll 4
   for (int i = t; i < bytes / 16; i += nt) {
-    const float4 v = s4[i];
+    const float4 v = lds128(s0 + 16u * i);
     float4 r;
     r.x = v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
     r.y = v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
     r.z = v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
     r.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
-    d4[i] = r;
+    sts128(d0 + 16u * i, r);
   }
 }
 // generic-proxy smem writes -> visible to the tensor core (async proxy)
