@@ -255,17 +255,38 @@ __global__ void __launch_bounds__(128) k_splitk_reduce(const float* __restrict__
   }
 }
 
-// Split-K scratch: one lazily grown device buffer. GEMMs of this library are
-// issued on one stream in program order, so consecutive calls never overlap.
-float* splitk_workspace(size_t floats) {
-  static float* buf = nullptr;
-  static size_t cap = 0;
-  if (floats > cap) {
-    if (buf) SD_CUDA(cudaFree(buf));
-    SD_CUDA(cudaMalloc(&buf, floats * sizeof(float)));
-    cap = floats;
+// Split-K scratch: lazily grown device buffers per (issuing thread, device).
+// The GEMMs one thread issues go to one stream in program order, so its
+// consecutive calls never overlap; in-process workers (one thread each) get
+// their own buffers, released when the thread exits.
+namespace {
+struct SplitScratch {
+  float* ws = nullptr;
+  size_t cap = 0;
+};
+struct ThreadScratch {
+  std::vector<SplitScratch> per_dev;
+  ~ThreadScratch() {  // errors ignored: at process exit the runtime may be gone
+    for (size_t d = 0; d < per_dev.size(); ++d)
+      if (per_dev[d].ws && cudaSetDevice(int(d)) == cudaSuccess) (void)cudaFree(per_dev[d].ws);
   }
-  return buf;
+};
+SplitScratch& split_scratch() {
+  thread_local ThreadScratch t;
+  int dev = 0;
+  SD_CUDA(cudaGetDevice(&dev));
+  if (t.per_dev.size() <= size_t(dev)) t.per_dev.resize(dev + 1);
+  return t.per_dev[dev];
+}
+}  // namespace
+float* splitk_workspace(size_t floats) {
+  SplitScratch& sc = split_scratch();
+  if (floats > sc.cap) {
+    if (sc.ws) SD_CUDA(cudaFree(sc.ws));
+    SD_CUDA(cudaMalloc(&sc.ws, floats * sizeof(float)));
+    sc.cap = floats;
+  }
+  return sc.ws;
 }
 
 // Optional per-launch CUDA-event timing of every GEMM (bench.py roofline):

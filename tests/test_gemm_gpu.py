@@ -81,6 +81,46 @@ def test_gemm_split_k(G, a_t, b_t):
     assert torch.equal(C, first)  # deterministic split order
 
 
+def test_gemm_split_k_concurrent_threads(G):
+    """Split-K products issued concurrently from several threads on their own
+    streams (the in-process worker pool's pattern) use per-thread workspaces:
+    every thread's result equals the single-threaded one bitwise."""
+    import threading
+    M, N, K = 768, 768, 8192  # an Hv weight product: split 8 ways on the B200
+    g = torch.Generator(device="cuda").manual_seed(11)
+    ins = [(torch.randn(K, M, device="cuda", generator=g), torch.randn(K, N, device="cuda", generator=g))
+           for _ in range(4)]
+    sm = [(G.split(a), G.split(b)) for a, b in ins]
+
+    def one(i, out):
+        a, b = ins[i]
+        c = torch.empty(M, N, device="cuda")
+        for _ in range(3):
+            G.gemm(M, N, K, a, M, True, b, N, True, c, N, a_small=sm[i][0], b_small=sm[i][1])
+        out[i] = c
+
+    want = [None] * 4
+    for i in range(4):
+        one(i, want)
+    torch.cuda.synchronize()
+    got = [None] * 4
+    dev = torch.cuda.current_device()
+
+    def body(i):
+        torch.cuda.set_device(dev)
+        with torch.cuda.stream(torch.cuda.Stream()):
+            one(i, got)
+            torch.cuda.current_stream().synchronize()
+
+    ts = [threading.Thread(target=body, args=(i,)) for i in range(4)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    for i in range(4):
+        assert torch.equal(got[i], want[i]), i
+
+
 def test_gemm_wide_tiles(G):
     """Shapes that select the 256-wide tile path (enough output tiles)."""
     for (M, N, K, a_t, b_t) in [(4096, 2304, 256, False, False), (4096, 1024, 512, False, True),
