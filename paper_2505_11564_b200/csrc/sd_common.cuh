@@ -25,6 +25,7 @@ inline void cuda_check(cudaError_t e, const char* what) {
 // every kernel launch of the library passes through here: it is checked and
 // counted (sd_launch_count, reported as gpu_launches by bench.py)
 void count_launch();
+void add_launches(uint64_t n);  // kernels a replayed CUDA graph runs
 #define SD_LAUNCHED(name) (::sd::count_launch(), ::sd::cuda_check(cudaGetLastError(), name))
 
 void set_last_error(const std::string& m);

@@ -32,6 +32,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <atomic>
 #include <mutex>
 #include <vector>
 
@@ -279,9 +280,11 @@ SplitScratch& split_scratch() {
   return t.per_dev[dev];
 }
 }  // namespace
+std::atomic<uint64_t> g_scratch_gen{0};
 float* splitk_workspace(size_t floats) {
   SplitScratch& sc = split_scratch();
   if (floats > sc.cap) {
+    g_scratch_gen.fetch_add(1);
     if (sc.ws) SD_CUDA(cudaFree(sc.ws));
     SD_CUDA(cudaMalloc(&sc.ws, floats * sizeof(float)));
     sc.cap = floats;
@@ -871,6 +874,9 @@ void split_tf32(const float* x, float* small, long long n, int mode, cudaStream_
   k_split_tf32<<<unsigned((n + 255) / 256), 256, 0, s>>>(x, small, n, mode);
   SD_LAUNCHED("k_split_tf32");
 }
+
+uint64_t gemm_scratch_generation() { return gk::g_scratch_gen.load(); }
+bool gemm_profiling() { return gk::prof_on(); }
 
 }  // namespace sd
 

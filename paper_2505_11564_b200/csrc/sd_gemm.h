@@ -38,5 +38,10 @@ struct GemmArgs {
   float *C2 = nullptr, *Cs2 = nullptr;
 };
 void gemm(const GemmArgs& g, cudaStream_t s);
+// bumped whenever a split-K workspace is (re)allocated: a captured CUDA graph
+// holding the old pointer must be re-captured
+uint64_t gemm_scratch_generation();
+// per-GEMM event profiling on (events cannot sit inside a replayed graph)
+bool gemm_profiling();
 void split_tf32(const float* x, float* small, long long n, int mode, cudaStream_t s);
 }  // namespace sd

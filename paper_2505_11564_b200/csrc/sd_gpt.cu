@@ -25,6 +25,7 @@
 #include <cstring>
 #include <numeric>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "sd_common.cuh"
@@ -174,6 +175,9 @@ struct sd_gpt_s {
   void* csr_scratch = nullptr;  // device scratch of gpt_token_csr (allocated at the first set_batch)
   size_t csr_bytes = 0;
   ~sd_gpt_s() {
+    if (gexec) cudaGraphExecDestroy(gexec);
+    if (cap_stream) cudaStreamDestroy(cap_stream);
+    if (vfix) cudaFree(vfix);
     if (csr_scratch) cudaFree(csr_scratch);
     if (ev_stage) {
       cudaEventSynchronize(ev_stage);
@@ -362,7 +366,90 @@ struct sd_gpt_s {
   // forward + backward of each micro-batch (Hv of micro-batches after the
   // first accumulates: GEMM beta = 1, accumulate flags of the column and
   // embedding reductions; Alg. 1's h += u b over the loader)
+  // ---- CUDA graph of the whole-model HVP. The launch sequence of one HVP is
+  // fixed once the batch shape is, so it is captured once and replayed: v is
+  // first copied into the engine-owned vfix (the graph's fixed input) and the
+  // graph is keyed by everything else it captured by value -- the Hv pointer,
+  // loss_scale, the issuing thread (whose split-K workspace the GEMMs bound)
+  // and the workspace generation. A key seen for the first time runs eagerly
+  // (allocations happen there); its second occurrence is captured. Any
+  // capture failure falls back to eager launches for good. SD_GPT_GRAPH=0:
+  // always eager.
+  struct GraphKey {
+    const float* hv = nullptr;
+    float loss_scale = 0.0f;
+    std::thread::id tid;
+    uint64_t gen = 0;
+    bool operator==(const GraphKey& o) const {
+      return hv == o.hv && loss_scale == o.loss_scale && tid == o.tid && gen == o.gen;
+    }
+  };
+  float* vfix = nullptr;
+  cudaStream_t cap_stream = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  GraphKey gkey, gpending;
+  bool have_pending = false, graph_off = false;
+  uint64_t glaunches = 0;
+  static bool graphs_enabled() {
+    static const bool on = [] {
+      const char* e = std::getenv("SD_GPT_GRAPH");
+      return !(e && e[0] == '0');
+    }();
+    return on;
+  }
+  void drop_graph() {
+    if (gexec) cudaGraphExecDestroy(gexec);
+    gexec = nullptr;
+  }
+
   void hvp(const float* v, float* hv, cudaStream_t st) {
+    if (graph_off || !graphs_enabled() || !first || !last || sd::gemm_profiling()) {
+      hvp_eager(v, hv, st);
+      return;
+    }
+    if (!vfix) SD_CUDA(cudaMalloc(&vfix, size_t(Pst) * sizeof(float)));
+    SD_CUDA(cudaMemcpyAsync(vfix, v, size_t(Pst) * sizeof(float), cudaMemcpyDeviceToDevice, st));
+    const GraphKey k{hv, loss_scale, std::this_thread::get_id(), sd::gemm_scratch_generation()};
+    if (gexec && k == gkey) {
+      SD_CUDA(cudaGraphLaunch(gexec, st));
+      sd::add_launches(glaunches);
+      return;
+    }
+    if (!(have_pending && k == gpending)) {
+      hvp_eager(vfix, hv, st);  // first sighting: warm-up (workspaces grow here, outside any capture)
+      gpending = k, have_pending = true;
+      return;
+    }
+    drop_graph();
+    // captured on the engine's own stream (capture only records; the legacy
+    // default stream cannot capture), launched on st
+    if (!cap_stream) SD_CUDA(cudaStreamCreateWithFlags(&cap_stream, cudaStreamNonBlocking));
+    cudaGraph_t graph = nullptr;
+    const uint64_t n0 = sd_launch_count();
+    SD_CUDA(cudaStreamBeginCapture(cap_stream, cudaStreamCaptureModeThreadLocal));
+    bool ok = true;
+    try {
+      hvp_eager(vfix, hv, cap_stream);
+    } catch (...) {
+      ok = false;
+    }
+    const cudaError_t ce = cudaStreamEndCapture(cap_stream, &graph);
+    ok = ok && ce == cudaSuccess && graph && sd::gemm_scratch_generation() == k.gen;
+    if (ok) ok = cudaGraphInstantiateWithFlags(&gexec, graph, 0) == cudaSuccess;
+    if (graph) cudaGraphDestroy(graph);
+    if (!ok) {  // not capturable here: eager from now on
+      (void)cudaGetLastError();
+      gexec = nullptr;
+      graph_off = true;
+      hvp_eager(vfix, hv, st);
+      return;
+    }
+    glaunches = sd_launch_count() - n0;  // counted while capturing; they run now
+    gkey = k, have_pending = false;
+    SD_CUDA(cudaGraphLaunch(gexec, st));
+  }
+
+  void hvp_eager(const float* v, float* hv, cudaStream_t st) {
     stage_begin(v, hv, st);
     for (int m = 0; m < nmb; ++m) {
       if (c.arch == SD_ARCH_LLAMA) {

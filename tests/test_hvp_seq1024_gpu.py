@@ -137,3 +137,43 @@ def test_c3_width_vs_torch_f64(gpt, micro_batches):
     e = float((hv - ref).norm() / ref.norm())
     print(f"C3 width, 4 layers, {B} x {S}: {e:.3e}")
     assert e < TOL
+
+
+_GRAPH = r"""
+import sys, hashlib, json
+import torch
+sys.path.insert(0, sys.argv[1])
+from paper_2505_11564_b200 import gpt
+from paper_2505_11564_b200._lib import lib
+cfg = dict(gpt.GPT2_SMALL, n_layer=2)
+eng = gpt.GptHvp(cfg, 2, 1024, init_seed=2, gain_scale=0.1, bias_scale=0.1)
+out = torch.empty(eng.P, device="cuda")
+g = torch.Generator(device="cuda").manual_seed(7)
+res = []
+for i in range(4):  # eager warm-up, capture, replay, replay (fixed output pointer)
+    v = torch.randn(eng.P, device="cuda", generator=g).contiguous()
+    n0 = lib().sd_launch_count()
+    eng.hvp(v, out)
+    torch.cuda.synchronize()
+    res.append([hashlib.sha256(out.cpu().numpy().tobytes()).hexdigest(), lib().sd_launch_count() - n0])
+print(json.dumps(res))
+"""
+
+
+def test_cuda_graph_replay_bitwise(gpt):
+    """The whole-model HVP is captured into a CUDA graph at its second call with
+    the same output pointer and replayed afterwards: Hv of every call equals
+    the always-eager run (SD_GPT_GRAPH=0) bitwise, and every call reports the
+    same number of kernel launches (replays count the graph's kernels)."""
+    import json
+    out = {}
+    for tag, extra in (("graph", {}), ("eager", {"SD_GPT_GRAPH": "0"})):
+        env = dict(os.environ, **extra)
+        r = subprocess.run([sys.executable, "-c", _GRAPH, str(ROOT)], env=env, capture_output=True, text=True,
+                           timeout=900)
+        assert r.returncode == 0, r.stderr[-2000:]
+        out[tag] = json.loads(r.stdout.strip().splitlines()[-1])
+    assert [h for h, _ in out["graph"]] == [h for h, _ in out["eager"]]
+    counts = [n for _, n in out["graph"]] + [n for _, n in out["eager"]]
+    assert len(set(counts)) == 1 and counts[0] > 0, counts
+
