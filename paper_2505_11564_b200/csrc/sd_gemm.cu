@@ -820,8 +820,37 @@ bool sd_gemm_pair_enabled() {
 
 }  // namespace
 
+bool twin_enabled() {  // SD_GEMM_TWIN=0: twin products as two launches
+  static const bool on = [] {
+    const char* e = std::getenv("SD_GEMM_TWIN");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 void gemm(const GemmArgs& g_in, cudaStream_t s) {
   if (g_in.M <= 0 || g_in.N <= 0 || g_in.K <= 0) return;
+  if (g_in.twin) {
+    if (!g_in.A2 || !g_in.B2 || !g_in.C2 || g_in.split) fail(SD_ARGUMENT_ERROR, "twin gemm needs A2, B2 and C2");
+    // one launch for the weight products (K = d or ff); the LM-head adjoint
+    // (K = vocab: the logits-sized A operands dominate, and the twin walk
+    // re-streams them: 23 vs 15 GB measured) stays two launches
+    const bool one = g_in.causal == 0 && g_in.M >= 256 && g_in.N >= 256 && g_in.K <= 16384 &&
+                     sd_gemm_pair_enabled() && twin_enabled();
+    if (!one) {  // C = alpha A B + beta C ; C2 = alpha2 (A2 B + A B2) + beta2 C2
+      GemmArgs p = g_in;
+      p.twin = false, p.A2 = p.A2s = p.B2 = p.B2s = nullptr, p.b2_exact = false, p.C2 = p.Cs2 = nullptr;
+      gemm(p, s);
+      GemmArgs t = g_in;
+      t.twin = false;
+      t.A = g_in.A2, t.As = g_in.A2s, t.lda = g_in.lda2, t.sa1 = g_in.sa1_2, t.sa2 = g_in.sa2_2;
+      t.A2 = g_in.A, t.A2s = g_in.As, t.lda2 = g_in.lda, t.sa1_2 = g_in.sa1, t.sa2_2 = g_in.sa2;
+      t.C = g_in.C2, t.Cs = g_in.Cs2, t.alpha = g_in.alpha2, t.beta = g_in.beta2, t.bias = g_in.bias2;
+      t.C2 = t.Cs2 = nullptr;
+      gemm(t, s);
+      return;
+    }
+  }
   GemmArgs g = g_in;
   // tf32-exact B operands: their (zero) residual is never loaded; the B map
   // stands in for the residual map so the 3xTF32 path applies

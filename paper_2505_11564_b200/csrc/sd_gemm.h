@@ -36,6 +36,15 @@ struct GemmArgs {
   // strides; one launch with a 128-wide accumulator (A staged once for both)
   bool split = false;
   float *C2 = nullptr, *Cs2 = nullptr;
+  // twin products sharing A and B (the primal and tangent products of one
+  // weight in the R-op forward and adjoint): C = alpha A B + beta C (+bias,
+  // Cs) and C2 = alpha2 (A2 B + A B2) + beta2 C2 (+bias2, Cs2), C2 with C's
+  // strides; one launch whose tile list holds both outputs' tiles (C2's, the
+  // two-source ones, first), or two launches where the pair kernel does not
+  // apply
+  bool twin = false;
+  float alpha2 = 1.0f, beta2 = 0.0f;
+  const float* bias2 = nullptr;
 };
 void gemm(const GemmArgs& g, cudaStream_t s);
 // bumped whenever a split-K workspace is (re)allocated: a captured CUDA graph

@@ -188,6 +188,11 @@ struct EpiParams {
   int group;                          // grouped tile walk (raster_group): > 0 groups of `group` m tiles,
                                       // m fastest inside a group; < 0 groups of -group n tiles, n fastest
                                       // inside; 0 n fastest over the whole grid
+  int twin, tiles1;                   // twin products (GemmArgs::twin): tiles [0, tiles1) are C2's
+                                      // (sources A2 B, A B2), [tiles1, 2 tiles1) C's (source A B)
+  float alpha2, beta2;                // twin: C2's epilogue
+  const float* bias2;
+  float* ws2;                         // twin: C2's split-K partials
 };
 
 // Rasterisation. A persistent wave of clusters works on consecutive tile
@@ -372,6 +377,8 @@ static_assert(KC % 2 == 0, "split products interleave the two sources: a chunk m
 struct TileInfo {
   int n0, m0, z, split, kb0, num_kb;
   bool skip;
+  bool tan = false;  // twin: a C2 (two-source) tile
+  int nsrc = 1;      // sources of this tile
 };
 
 template <int BN, bool CAUSAL>
@@ -401,6 +408,7 @@ __device__ __forceinline__ TileInfo tile_info(const EpiParams& ep, int t, int K)
   } else {
     walk_tile(ep, t, mt, nt, zz);
   }
+  ti.nsrc = ep.nsrc;
   ti.n0 = nt * BN;
   ti.m0 = mt * BM;
   ti.z = zz % ep.zcount;

@@ -17,6 +17,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <string>
+#include <vector>
 
 #include "sd_gemm_dev.cuh"
 
@@ -110,7 +111,9 @@ template <int PN>
 __device__ __forceinline__ TileInfo pair_tile(const EpiParams& ep, int t, int K) {
   TileInfo ti;
   int mt, nt, zz;
-  walk_tile(ep, t, mt, nt, zz);
+  ti.tan = ep.twin && t < ep.tiles1;
+  ti.nsrc = ep.twin ? (ti.tan ? 2 : 1) : ep.nsrc;
+  walk_tile(ep, (ep.twin && !ti.tan) ? t - ep.tiles1 : t, mt, nt, zz);
   ti.n0 = nt * PN;
   ti.m0 = mt * kPairM;
   ti.z = zz % ep.zcount;
@@ -127,7 +130,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                 const __grid_constant__ CUtensorMap mB, const __grid_constant__ CUtensorMap mBs,
                 const __grid_constant__ CUtensorMap mA2, const __grid_constant__ CUtensorMap mAs2,
                 const __grid_constant__ CUtensorMap mB2, const __grid_constant__ CUtensorMap mBs2,
-                const __grid_constant__ CUtensorMap mC, const __grid_constant__ CUtensorMap mCs, int K, EpiParams ep) {
+                const __grid_constant__ CUtensorMap mC, const __grid_constant__ CUtensorMap mCs,
+                const __grid_constant__ CUtensorMap mC2, const __grid_constant__ CUtensorMap mCs2, int K,
+                EpiParams ep) {
   using PC = PairCfg<PN>;
   constexpr int STAGES = kPairStages, EC = PC::EC, kHalfB = PC::HALF, PB_BYTES = PC::PB_BYTES;
   constexpr int kPairN = PN;
@@ -185,7 +190,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         if (ti.skip) continue;
         const int z1 = ti.z % ep.Z1, z2 = ti.z / ep.Z1;
         const int m_own = ti.m0 + int(rank) * BM, n_own = ti.n0 + int(rank) * kHalfB;
-        for (int kk = 0; kk < ep.nsrc * ti.num_kb; ++kk, ++g) {
+        for (int kk = 0; kk < ti.nsrc * ti.num_kb; ++kk, ++g) {
           const int s = g % STAGES;
           const uint32_t ph = (g / STAGES) & 1;
           mbar_wait(&empty[s], ph ^ 1);
@@ -193,8 +198,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
           // residuals from memory: both CTAs' bytes land on the leader's full
           // barrier. On chip: each CTA's raw bytes land on its own barrier and
           // its residual warp releases the stage to the leader (conv[s]).
-          const bool src2 = kk >= ti.num_kb;
-          const bool bex = THREE && !ep.res && ((ep.bexact >> (src2 ? 1 : 0)) & 1);
+          // dual: (A, B) then (A2, B2); twin C2 tiles: (A2, B) then (A, B2)
+          const bool second = kk >= ti.num_kb;
+          const bool useA2 = ti.tan ? !second : second, useB2 = second;
+          const bool bex = THREE && !ep.res && ((ep.bexact >> (useB2 ? 1 : 0)) & 1);
           uint32_t bar;
           if (ep.res) {
             mbar_expect_tx_e(&full[s], PA_BYTES + PB_BYTES);
@@ -203,11 +210,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
             if (rank == 0) mbar_expect_tx_e(&full[s], 2 * (STAGE_BYTES - (bex ? PB_BYTES : 0)));
             bar = full_leader + 8u * s;
           }
-          const int kb = src2 ? kk - ti.num_kb : kk;
-          const CUtensorMap* pA = src2 ? &mA2 : &mA;
-          const CUtensorMap* pAs = src2 ? &mAs2 : &mAs;
-          const CUtensorMap* pB = src2 ? &mB2 : &mB;
-          const CUtensorMap* pBs = src2 ? &mBs2 : &mBs;
+          const int kb = second ? kk - ti.num_kb : kk;
+          const CUtensorMap* pA = useA2 ? &mA2 : &mA;
+          const CUtensorMap* pAs = useA2 ? &mAs2 : &mAs;
+          const CUtensorMap* pB = useB2 ? &mB2 : &mB;
+          const CUtensorMap* pBs = useB2 ? &mBs2 : &mBs;
           const int k0 = (ti.kb0 + kb) * BK;
           if (A_MN && (ep.mn5 & 1)) {
             tma_load_5d_pair_e(pA, bar, st, 0, k0, m_own / 32, z1, z2);
@@ -249,7 +256,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
       for (int t = cid; t < ep.n_tiles; t += ncl) {
         const TileInfo ti = pair_tile<PN>(ep, t, K);
         if (ti.skip) continue;
-        for (int kk = 0; kk < ep.nsrc * ti.num_kb; ++kk, ++g) {
+        for (int kk = 0; kk < ti.nsrc * ti.num_kb; ++kk, ++g) {
           if (int(g % kConvWarps) != cw) continue;
           const int s = g % STAGES;
           mbar_wait(&full[s], (g / STAGES) & 1);
@@ -268,7 +275,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
       for (int t = cid; t < ep.n_tiles; t += ncl) {
         const TileInfo ti = pair_tile<PN>(ep, t, K);
         if (ti.skip) continue;
-        const int nkb = ep.nsrc * ti.num_kb;
+        const int nkb = ti.nsrc * ti.num_kb;
         for (int kb = 0; kb < nkb; ++kb, ++g) {
           const int s = g % STAGES;
           const uint32_t ph = (g / STAGES) & 1;
@@ -317,7 +324,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
       float acc[EC];
 #pragma unroll
       for (int j = 0; j < EC; ++j) acc[j] = 0.0f;
-      const int nchunks = (ep.nsrc * ti.num_kb + KC - 1) / KC;
+      const int nchunks = (ti.nsrc * ti.num_kb + KC - 1) / KC;
       for (int c = 0; c < nchunks; ++c, ++chunk) {
         const uint32_t buf = chunk & 1;
         mbar_wait(&tfull[buf], (chunk >> 1) & 1);
@@ -336,10 +343,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
       }
       if (ep.tma_store) {
         const int ew = warp - 2 - kConvWarps;  // 0..15: its staging box
-        warp_tma_store<EC, 16>(&mC, ep.Cs ? &mCs : nullptr, epi_stage + ew * 512, acc, ep.alpha, ep.bias, lane,
-                               ti.m0 + int(rank) * BM + sub * 32, ti.n0 + cb, ti.z % ep.Z1, ti.z / ep.Z1);
+        const bool t2 = ti.tan;  // twin: C2's tile
+        const CUtensorMap* pcs = t2 ? (ep.Cs2 ? &mCs2 : nullptr) : (ep.Cs ? &mCs : nullptr);
+        warp_tma_store<EC, 16>(t2 ? &mC2 : &mC, pcs, epi_stage + ew * 512, acc, t2 ? ep.alpha2 : ep.alpha,
+                               t2 ? ep.bias2 : ep.bias, lane, ti.m0 + int(rank) * BM + sub * 32, ti.n0 + cb,
+                               ti.z % ep.Z1, ti.z / ep.Z1);
         if (lane == 0) bulk_wait_read0();  // staging box free for the next tile
         __syncwarp();
+      } else if (ti.tan) {
+        EpiParams e2 = ep;  // twin: C2's tile
+        e2.C = ep.C2, e2.Cs = ep.Cs2, e2.alpha = ep.alpha2, e2.beta = ep.beta2, e2.bias = ep.bias2, e2.ws = ep.ws2;
+        store_row<EC>(e2, ti, row, ti.n0 + cb, acc);
       } else {
         store_row<EC>(ep, ti, row, ti.n0 + cb, acc);
       }
@@ -371,6 +385,28 @@ int max_clusters(const void* kern, size_t smem) {
   return n;
 }
 
+// Split count of a twin launch: its units are the C2 tiles (two sources,
+// first) and the C tiles (one source) of every split, dealt round-robin to the
+// cluster slots; the modelled time is the busiest slot's k-blocks plus the
+// split-K partial traffic (as choose_splits).
+int choose_splits_twin(int tiles, int units, int total_kb, double t_kb, double out_bytes) {
+  int best_s = 1;
+  double best = 0.0;
+  std::vector<long long> load(units);
+  for (int s = 1; s <= 16 && (s == 1 || total_kb / s >= 16); ++s) {
+    const long long kb = (total_kb + s - 1) / s, n = (long long)tiles * s;
+    std::fill(load.begin(), load.end(), 0);
+    for (long long t = 0; t < 2 * n; ++t) load[t % units] += (t < n ? 2 : 1) * kb;
+    const double c = double(*std::max_element(load.begin(), load.end())) * t_kb +
+                     (s > 1 ? 2.0 * s * out_bytes / 6.0e12 + 5e-6 : 0.0);
+    if (s == 1 || c < best * 0.97) {
+      best = c;
+      best_s = s;
+    }
+  }
+  return best_s;
+}
+
 template <bool A_MN, bool B_MN, bool THREE, int PN>
 void launch_pair_t(const GemmArgs& g, cudaStream_t s) {
   using PC = PairCfg<PN>;
@@ -378,7 +414,8 @@ void launch_pair_t(const GemmArgs& g, cudaStream_t s) {
   CUtensorMap maps[8];
   int mn5 = 0;
   operand_maps(g, A_MN, B_MN, THREE, kHalfB, maps, &mn5);
-  const bool dual = g.A2 != nullptr;
+  const bool twin = g.twin;
+  const bool dual = g.A2 != nullptr && !twin;
   const int zc = g.Z1 * g.Z2;
   const int tn = (g.N + kPairN - 1) / kPairN, tm = (g.M + kPairM - 1) / kPairM;
   const int tiles = tn * tm * zc;
@@ -392,33 +429,49 @@ void launch_pair_t(const GemmArgs& g, cudaStream_t s) {
   // split-K as in the single-CTA launcher, over the cluster (pair) slots
   const int total_kb = (g.K + BK - 1) / BK;
   const double t_kb = 2.0 * kPairM * kPairN * BK / (2.0e14 / clusters) / (THREE ? 1.0 : 3.0);
-  int splits = choose_splits(tiles, clusters, total_kb, dual ? 2 : 1, t_kb, 4.0 * zc * g.M * g.N);
+  int splits = twin ? choose_splits_twin(tiles, clusters, total_kb, t_kb, 8.0 * zc * g.M * g.N)
+                    : choose_splits(tiles, clusters, total_kb, dual ? 2 : 1, t_kb, 4.0 * zc * g.M * g.N);
   const int kb_per = (total_kb + splits - 1) / splits;
   splits = (total_kb + kb_per - 1) / kb_per;
+  const size_t part = size_t(splits) * zc * size_t(g.M) * g.N;
   float* ws = nullptr;
-  if (splits > 1) ws = splitk_workspace(size_t(splits) * zc * size_t(g.M) * g.N);
+  if (splits > 1) ws = splitk_workspace((twin ? 2 : 1) * part);
   EpiParams ep{g.C, g.ldc, g.sc1, g.sc2, g.M, g.N, g.Z1, g.alpha, g.beta, g.bias, g.Cs, g.dbg, zc, kb_per, ws,
-               0, tn, tm, tiles * splits, dual ? 2 : 1, g.onchip ? 1 : 0};
+               0, tn, tm, tiles * splits * (twin ? 2 : 1), dual ? 2 : 1, g.onchip ? 1 : 0};
+  if (twin) {
+    ep.twin = 1, ep.tiles1 = tiles * splits;
+    ep.C2 = g.C2, ep.Cs2 = g.Cs2, ep.alpha2 = g.alpha2, ep.beta2 = g.beta2, ep.bias2 = g.bias2;
+    ep.ws2 = ws ? ws + part : nullptr;
+  }
   ep.group = walk_group(g, kPairM, PN, tm, tn, THREE);
   const int grid = 2 * std::min(ep.n_tiles, clusters);
   if (prof_on())
     prof_tag(std::to_string(g.M) + "," + std::to_string(g.N) + "," + std::to_string(g.K) + "," + std::to_string(zc) +
              "," + std::to_string(int(A_MN)) + "," + std::to_string(int(B_MN)) + ",pair," + std::to_string(splits) +
-             (dual ? ",2" : ",1"));
+             (twin ? ",twin" : dual ? ",2" : ",1"));
   prof_begin(s);
   ep.mn5 = mn5;
   ep.bexact = (g.b_exact ? 1 : 0) | (g.b2_exact ? 2 : 0);
-  CUtensorMap mC = maps[0], mCs = maps[0];
-  if (tma_store_ok(g, splits, 16)) {
+  CUtensorMap mC = maps[0], mCs = maps[0], mC2 = maps[0], mCs2 = maps[0];
+  GemmArgs g2 = g;  // twin: C2's epilogue
+  g2.C = g.C2, g2.Cs = g.Cs2, g2.alpha = g.alpha2, g2.beta = g.beta2, g2.bias = g.bias2;
+  if (tma_store_ok(g, splits, 16) && (!twin || tma_store_ok(g2, splits, 16))) {
     make_store_map(&mC, g.C, g, 16);
     if (g.Cs) make_store_map(&mCs, g.Cs, g, 16);
+    if (twin) {
+      make_store_map(&mC2, g2.C, g2, 16);
+      if (g2.Cs) make_store_map(&mCs2, g2.Cs, g2, 16);
+    }
     ep.tma_store = 1;
   }
   launch_gemm_kernel(kern, unsigned(grid), unsigned(kPairThreads), size_t(smem), s, maps[0], maps[1], maps[2], maps[3],
-                     maps[4], maps[5], maps[6], maps[7], mC, mCs, g.K, ep);
+                     maps[4], maps[5], maps[6], maps[7], mC, mCs, mC2, mCs2, g.K, ep);
   SD_LAUNCHED("k_gemm_pair");
-  if (splits > 1) launch_splitk_reduce(ws, splits, zc, g, s);
-  prof_end(s, (dual ? 4.0 : 2.0) * double(g.M) * g.N * g.K * g.Z1 * g.Z2);
+  if (splits > 1) {
+    launch_splitk_reduce(ws, splits, zc, g, s);
+    if (twin) launch_splitk_reduce(ws + part, splits, zc, g2, s);
+  }
+  prof_end(s, (twin ? 6.0 : dual ? 4.0 : 2.0) * double(g.M) * g.N * g.K * g.Z1 * g.Z2);
 }
 
 }  // namespace

@@ -314,6 +314,24 @@ struct sd_gpt_s {
     onchip_residuals(g);
     sd::gemm(g, st);
   }
+  // twin products of one weight (GemmArgs::twin): C = alpha A B + beta C (+bias,
+  // Cs) and its tangent C2 = alpha (A2 B + A B2) + beta C2 (+bias2, Cs2) -- the
+  // primal and tangent products of the R-op forward and adjoint -- as one
+  // launch over both outputs' tiles (SD_GEMM_TWIN=0: the two launches)
+  void mm_tw(int M, int N, int K, Op A, Op Bo, Op A2, Op B2, float* C, float* C2, long long ldc, float alpha,
+             float beta, cudaStream_t st, const float* bias, float* Cs, const float* bias2, float* Cs2) {
+    sd::GemmArgs g;
+    g.M = M, g.N = N, g.K = K;
+    g.A = A.p, g.As = A.s, g.lda = A.ld, g.a_mn = A.mn;
+    g.B = Bo.p, g.Bs = Bo.s, g.ldb = Bo.ld, g.b_mn = Bo.mn, g.b_exact = Bo.exact;
+    if (A2.mn != A.mn || B2.mn != Bo.mn) fail(SD_ARGUMENT_ERROR, "gpt: twin product majors differ");
+    g.A2 = A2.p, g.A2s = A2.s, g.lda2 = A2.ld, g.B2 = B2.p, g.B2s = B2.s, g.ldb2 = B2.ld, g.b2_exact = B2.exact;
+    g.C = C, g.ldc = ldc, g.alpha = alpha, g.beta = beta, g.bias = bias, g.Cs = Cs;
+    g.twin = true, g.C2 = C2, g.Cs2 = Cs2, g.alpha2 = alpha, g.beta2 = beta, g.bias2 = bias2;
+    g.causal = cmode;
+    onchip_residuals(g);
+    sd::gemm(g, st);
+  }
   // merged pair of 64-wide per-head products sharing A (sd_gemm.cu launch_split):
   // C = alpha A B, C2 = alpha (A B2 + A2 B) -- the [o | dO], [gv | gdv],
   // [gq | gdq], [gk | gdk] pairs of the attention R-op in one launch each
@@ -487,24 +505,16 @@ struct sd_gpt_s {
                   Ly.h1, Ly.h1s, Ly.dh1, Ly.dh1s, Ly.xh1, Ly.dxh1, Ly.r1, Ly.dr1};
     sd::gpt_ln_fwd(la, st);
     // qkv = h Wa + ba ; dqkv = dh Wa + h VWa + Vba
-    mm(T, 3 * d, d, {Ly.h1, Ly.h1s, d, false}, Wt(b + 2, 3 * d, true), Ly.a, 3 * d, 1, 0, st, th(b + 3), Ly.as);
-    mm2(T, 3 * d, d, {Ly.dh1, Ly.dh1s, d, false}, Wt(b + 2, 3 * d, true), {Ly.h1, Ly.h1s, d, false},
-        {V_(b + 2), Vs(b + 2), 3 * d, true}, Ly.da, 3 * d, 1, 0, st, V_(b + 3), Ly.das);
+    mm_tw(T, 3 * d, d, {Ly.h1, Ly.h1s, d, false}, Wt(b + 2, 3 * d, true), {Ly.dh1, Ly.dh1s, d, false}, {V_(b + 2), Vs(b + 2), 3 * d, true}, Ly.a, Ly.da, 3 * d, 1, 0, st, th(b + 3), Ly.as, V_(b + 3), Ly.das);
     attention_fwd(Ly, sc, st);
     // x += o Wp + bp ; dx += do Wp + o VWp + Vbp
-    mm(T, d, d, {Ly.o, Ly.os, d, false}, Wt(b + 4, d, true), x, d, 1, 1, st, th(b + 5));
-    mm2(T, d, d, {Ly.dO, Ly.dOs, d, false}, Wt(b + 4, d, true), {Ly.o, Ly.os, d, false},
-        {V_(b + 4), Vs(b + 4), d, true}, dx, d, 1, 1, st, V_(b + 5));
+    mm_tw(T, d, d, {Ly.o, Ly.os, d, false}, Wt(b + 4, d, true), {Ly.dO, Ly.dOs, d, false}, {V_(b + 4), Vs(b + 4), d, true}, x, dx, d, 1, 1, st, th(b + 5), nullptr, V_(b + 5), nullptr);
     sd::LnArgs lb{x, dx, th(b + 6), th(b + 7), V_(b + 6), V_(b + 7), T, d, 1e-5f,
                   Ly.h2, Ly.h2s, Ly.dh2, Ly.dh2s, Ly.xh2, Ly.dxh2, Ly.r2, Ly.dr2};
     sd::gpt_ln_fwd(lb, st);
-    mm(T, ff, d, {Ly.h2, Ly.h2s, d, false}, Wt(b + 8, ff, true), Ly.f, ff, 1, 0, st, th(b + 9));
-    mm2(T, ff, d, {Ly.dh2, Ly.dh2s, d, false}, Wt(b + 8, ff, true), {Ly.h2, Ly.h2s, d, false},
-        {V_(b + 8), Vs(b + 8), ff, true}, Ly.df, ff, 1, 0, st, V_(b + 9));
+    mm_tw(T, ff, d, {Ly.h2, Ly.h2s, d, false}, Wt(b + 8, ff, true), {Ly.dh2, Ly.dh2s, d, false}, {V_(b + 8), Vs(b + 8), ff, true}, Ly.f, Ly.df, ff, 1, 0, st, th(b + 9), nullptr, V_(b + 9), nullptr);
     sd::gpt_gelu_fwd(Ly.f, Ly.df, Ly.u, Ly.us, Ly.du, Ly.dus, (long long)T * ff, st);
-    mm(T, d, ff, {Ly.u, Ly.us, ff, false}, Wt(b + 10, d, true), x, d, 1, 1, st, th(b + 11));
-    mm2(T, d, ff, {Ly.du, Ly.dus, ff, false}, Wt(b + 10, d, true), {Ly.u, Ly.us, ff, false},
-        {V_(b + 10), Vs(b + 10), d, true}, dx, d, 1, 1, st, V_(b + 11));
+    mm_tw(T, d, ff, {Ly.u, Ly.us, ff, false}, Wt(b + 10, d, true), {Ly.du, Ly.dus, ff, false}, {V_(b + 10), Vs(b + 10), d, true}, x, dx, d, 1, 1, st, th(b + 11), nullptr, V_(b + 11), nullptr);
   }
 
   void gpt2_bwd(int m, cudaStream_t st) {
@@ -517,13 +527,10 @@ struct sd_gpt_s {
     sd::LnArgs lf{x, dx, th(fL), th(fL + 1), V_(fL), V_(fL + 1), T, d, 1e-5f, hf, hfs, dhf, dhfs, xhf, dxhf, rf, drf};
     sd::gpt_ln_fwd(lf, st);
     // logits z = hf wte^T ; dz = dhf wte^T + hf Vwte^T
-    mm(T, V, d, {hf, hfs, d, false}, Wt(0, d, false), z, Vp, 1, 0, st);
-    mm2(T, V, d, {dhf, dhfs, d, false}, Wt(0, d, false), {hf, hfs, d, false}, {V_(0), Vs(0), d, false}, dz, Vp, 1, 0,
-        st);
+    mm_tw(T, V, d, {hf, hfs, d, false}, Wt(0, d, false), {dhf, dhfs, d, false}, {V_(0), Vs(0), d, false}, z, dz, Vp, 1, 0, st, nullptr, nullptr, nullptr, nullptr);
     sd::gpt_ce(z, dz, zs, dzs, tgt + (long long)m * T, T, V, Vp, loss_scale, loss_rows + (long long)m * T, st);
     // ghf = gz wte ; gdhf = gdz wte + gz Vwte ; Hv_wte(head) (+)= gdz^T hf + gz^T dhf
-    mm(T, d, V, {z, zs, Vp, false}, Wt(0, d, true), gh, d, 1, 0, st);
-    mm2(T, d, V, {dz, dzs, Vp, false}, Wt(0, d, true), {z, zs, Vp, false}, {V_(0), Vs(0), d, true}, gdh, d, 1, 0, st);
+    mm_tw(T, d, V, {z, zs, Vp, false}, Wt(0, d, true), {dz, dzs, Vp, false}, {V_(0), Vs(0), d, true}, gh, gdh, d, 1, 0, st, nullptr, nullptr, nullptr, nullptr);
     mm2(V, d, T, {dz, dzs, Vp, true}, {hf, hfs, d, true}, {z, zs, Vp, true}, {dhf, dhfs, d, true}, HV(0), d, 1, hb,
         st);
     SD_CUDA(cudaMemsetAsync(gx, 0, 2 * Td * sizeof(float), st));
@@ -551,17 +558,13 @@ struct sd_gpt_s {
     const float sc = 1.0f / std::sqrt(float(dh));
     const int b = 2 + 12 * l;
     // MLP out: gu = gx Wq^T ; gdu = gdx Wq^T + gx VWq^T ; Hv_Wq = du^T gx + u^T gdx
-    mm(T, ff, d, {gx, gxs, d, false}, Wt(b + 10, d, false), gu, ff, 1, 0, st);
-    mm2(T, ff, d, {gdx, gdxs, d, false}, Wt(b + 10, d, false), {gx, gxs, d, false},
-        {V_(b + 10), Vs(b + 10), d, false}, gdu, ff, 1, 0, st);
+    mm_tw(T, ff, d, {gx, gxs, d, false}, Wt(b + 10, d, false), {gdx, gdxs, d, false}, {V_(b + 10), Vs(b + 10), d, false}, gu, gdu, ff, 1, 0, st, nullptr, nullptr, nullptr, nullptr);
     mm2(ff, d, T, {Ly.du, Ly.dus, ff, true}, {gx, gxs, d, true}, {Ly.u, Ly.us, ff, true}, {gdx, gdxs, d, true},
         HV(b + 10), d, 1, hb, st);
     sd::gpt_colsum(gdx, T, d, d, HV(b + 11), red, st, int(acc));
     sd::gpt_gelu_bwd(Ly.f, Ly.df, gu, gdu, gus, gdus, (long long)T * ff, st);
     // MLP in: gh = gf Wf^T ; gdh = gdf Wf^T + gf VWf^T ; Hv_Wf = dh2^T gf + h2^T gdf
-    mm(T, d, ff, {gu, gus, ff, false}, Wt(b + 8, ff, false), gh, d, 1, 0, st);
-    mm2(T, d, ff, {gdu, gdus, ff, false}, Wt(b + 8, ff, false), {gu, gus, ff, false},
-        {V_(b + 8), Vs(b + 8), ff, false}, gdh, d, 1, 0, st);
+    mm_tw(T, d, ff, {gu, gus, ff, false}, Wt(b + 8, ff, false), {gdu, gdus, ff, false}, {V_(b + 8), Vs(b + 8), ff, false}, gh, gdh, d, 1, 0, st, nullptr, nullptr, nullptr, nullptr);
     mm2(d, ff, T, {Ly.dh2, Ly.dh2s, d, true}, {gu, gus, ff, true}, {Ly.h2, Ly.h2s, d, true}, {gdu, gdus, ff, true},
         HV(b + 8), ff, 1, hb, st);
     sd::gpt_colsum(gdu, T, ff, ff, HV(b + 9), red, st, int(acc));
@@ -569,17 +572,13 @@ struct sd_gpt_s {
                      gx, gdx, gxs, gdxs, HV(b + 6), HV(b + 7), red, 0, int(acc)};
     sd::gpt_ln_bwd(b2, st);
     // attention out-projection
-    mm(T, d, d, {gx, gxs, d, false}, Wt(b + 4, d, false), go, d, 1, 0, st, nullptr, gos);
-    mm2(T, d, d, {gdx, gdxs, d, false}, Wt(b + 4, d, false), {gx, gxs, d, false},
-        {V_(b + 4), Vs(b + 4), d, false}, gdo, d, 1, 0, st, nullptr, gdos);
+    mm_tw(T, d, d, {gx, gxs, d, false}, Wt(b + 4, d, false), {gdx, gdxs, d, false}, {V_(b + 4), Vs(b + 4), d, false}, go, gdo, d, 1, 0, st, nullptr, gos, nullptr, gdos);
     mm2(d, d, T, {Ly.dO, Ly.dOs, d, true}, {gx, gxs, d, true}, {Ly.o, Ly.os, d, true}, {gdx, gdxs, d, true},
         HV(b + 4), d, 1, hb, st);
     sd::gpt_colsum(gdx, T, d, d, HV(b + 5), red, st, int(acc));
     attention_bwd(Ly, sc, st);
     // QKV: gh = ga Wa^T ; gdh = gda Wa^T + ga VWa^T ; Hv_Wa = dh1^T ga + h1^T gda
-    mm(T, d, 3 * d, {ga, gas, 3 * d, false}, Wt(b + 2, 3 * d, false), gh, d, 1, 0, st);
-    mm2(T, d, 3 * d, {gda, gdas, 3 * d, false}, Wt(b + 2, 3 * d, false), {ga, gas, 3 * d, false},
-        {V_(b + 2), Vs(b + 2), 3 * d, false}, gdh, d, 1, 0, st);
+    mm_tw(T, d, 3 * d, {ga, gas, 3 * d, false}, Wt(b + 2, 3 * d, false), {gda, gdas, 3 * d, false}, {V_(b + 2), Vs(b + 2), 3 * d, false}, gh, gdh, d, 1, 0, st, nullptr, nullptr, nullptr, nullptr);
     mm2(d, 3 * d, T, {Ly.dh1, Ly.dh1s, d, true}, {ga, gas, 3 * d, true}, {Ly.h1, Ly.h1s, d, true},
         {gda, gdas, 3 * d, true}, HV(b + 2), 3 * d, 1, hb, st);
     sd::gpt_colsum(gda, T, 3 * d, 3 * d, HV(b + 3), red, st, int(acc));
@@ -636,25 +635,17 @@ struct sd_gpt_s {
       // the KV heads to the MHA [T, 3d] layout the attention products use
       float *qa = gqa() ? Ly.qkv : Ly.a, *qas = gqa() ? Ly.qkvs : Ly.as;
       float *qd = gqa() ? Ly.dqkv : Ly.da, *qds = gqa() ? Ly.dqkvs : Ly.das;
-      mm(T, W, d, {Ly.h1, Ly.h1s, d, false}, Wt(b + 1, W, true), qa, W, 1, 0, st, nullptr, qas);
-      mm2(T, W, d, {Ly.dh1, Ly.dh1s, d, false}, Wt(b + 1, W, true), {Ly.h1, Ly.h1s, d, false},
-          {V_(b + 1), Vs(b + 1), W, true}, qd, W, 1, 0, st, nullptr, qds);
+      mm_tw(T, W, d, {Ly.h1, Ly.h1s, d, false}, Wt(b + 1, W, true), {Ly.dh1, Ly.dh1s, d, false}, {V_(b + 1), Vs(b + 1), W, true}, qa, qd, W, 1, 0, st, nullptr, qas, nullptr, qds);
       if (gqa()) sd::llama_gqa_expand(Ly.qkv, Ly.qkvs, Ly.dqkv, Ly.dqkvs, Ly.a, Ly.as, Ly.da, Ly.das, T, d, dh, KV, H, st);
       sd::llama_rope(Ly.a, Ly.as, Ly.da, Ly.das, T, S, d, dh, c.rope_base, 0, st);
       attention_fwd(Ly, sc, st);
-      mm(T, d, d, {Ly.o, Ly.os, d, false}, Wt(b + 2, d, true), x, d, 1, 1, st);
-      mm2(T, d, d, {Ly.dO, Ly.dOs, d, false}, Wt(b + 2, d, true), {Ly.o, Ly.os, d, false},
-          {V_(b + 2), Vs(b + 2), d, true}, dx, d, 1, 1, st);
+      mm_tw(T, d, d, {Ly.o, Ly.os, d, false}, Wt(b + 2, d, true), {Ly.dO, Ly.dOs, d, false}, {V_(b + 2), Vs(b + 2), d, true}, x, dx, d, 1, 1, st, nullptr, nullptr, nullptr, nullptr);
       sd::LnArgs lb{x, dx, th(b + 3), nullptr, V_(b + 3), nullptr, T, d, eps,
                     Ly.h2, Ly.h2s, Ly.dh2, Ly.dh2s, Ly.xh2, Ly.dxh2, Ly.r2, Ly.dr2, 1};
       sd::gpt_ln_fwd(lb, st);
-      mm(T, 2 * ff, d, {Ly.h2, Ly.h2s, d, false}, Wt(b + 4, 2 * ff, true), Ly.f, 2 * ff, 1, 0, st);
-      mm2(T, 2 * ff, d, {Ly.dh2, Ly.dh2s, d, false}, Wt(b + 4, 2 * ff, true),
-          {Ly.h2, Ly.h2s, d, false}, {V_(b + 4), Vs(b + 4), 2 * ff, true}, Ly.df, 2 * ff, 1, 0, st);
+      mm_tw(T, 2 * ff, d, {Ly.h2, Ly.h2s, d, false}, Wt(b + 4, 2 * ff, true), {Ly.dh2, Ly.dh2s, d, false}, {V_(b + 4), Vs(b + 4), 2 * ff, true}, Ly.f, Ly.df, 2 * ff, 1, 0, st, nullptr, nullptr, nullptr, nullptr);
       sd::llama_swiglu_fwd(Ly.f, Ly.df, Ly.u, Ly.us, Ly.du, Ly.dus, T, ff, st);
-      mm(T, d, ff, {Ly.u, Ly.us, ff, false}, Wt(b + 5, d, true), x, d, 1, 1, st);
-      mm2(T, d, ff, {Ly.du, Ly.dus, ff, false}, Wt(b + 5, d, true), {Ly.u, Ly.us, ff, false},
-          {V_(b + 5), Vs(b + 5), d, true}, dx, d, 1, 1, st);
+      mm_tw(T, d, ff, {Ly.u, Ly.us, ff, false}, Wt(b + 5, d, true), {Ly.du, Ly.dus, ff, false}, {V_(b + 5), Vs(b + 5), d, true}, x, dx, d, 1, 1, st, nullptr, nullptr, nullptr, nullptr);
     }
   }
 
@@ -675,13 +666,9 @@ struct sd_gpt_s {
       sd::LnArgs lf{x, dx, th(fL), nullptr, V_(fL), nullptr, T, d, eps, hf, hfs, dhf, dhfs, xhf, dxhf, rf, drf, 1};
       sd::gpt_ln_fwd(lf, st);
       // logits z = hf W_out^T ; dz = dhf W_out^T + hf VW_out^T
-      mm(T, V, d, {hf, hfs, d, false}, Wt(head, d, false), z, Vp, 1, 0, st);
-      mm2(T, V, d, {dhf, dhfs, d, false}, Wt(head, d, false), {hf, hfs, d, false},
-          {V_(head), Vs(head), d, false}, dz, Vp, 1, 0, st);
+      mm_tw(T, V, d, {hf, hfs, d, false}, Wt(head, d, false), {dhf, dhfs, d, false}, {V_(head), Vs(head), d, false}, z, dz, Vp, 1, 0, st, nullptr, nullptr, nullptr, nullptr);
       sd::gpt_ce(z, dz, zs, dzs, tgt + (long long)m * T, T, V, Vp, loss_scale, loss_rows + (long long)m * T, st);
-      mm(T, d, V, {z, zs, Vp, false}, Wt(head, d, true), gh, d, 1, 0, st);
-      mm2(T, d, V, {dz, dzs, Vp, false}, Wt(head, d, true), {z, zs, Vp, false},
-          {V_(head), Vs(head), d, true}, gdh, d, 1, 0, st);
+      mm_tw(T, d, V, {z, zs, Vp, false}, Wt(head, d, true), {dz, dzs, Vp, false}, {V_(head), Vs(head), d, true}, gh, gdh, d, 1, 0, st, nullptr, nullptr, nullptr, nullptr);
       mm2(V, d, T, {dz, dzs, Vp, true}, {hf, hfs, d, true}, {z, zs, Vp, true}, {dhf, dhfs, d, true}, HV(head), d, 1,
           hb, st);
       SD_CUDA(cudaMemsetAsync(gx, 0, 2 * Td * sizeof(float), st));
@@ -717,25 +704,19 @@ struct sd_gpt_s {
     {
       const int b = 1 + 6 * l;
       // down projection: ga = gx Wd^T ; gda = gdx Wd^T + gx VWd^T ; Hv_Wd = da^T gx + a^T gdx
-      mm(T, ff, d, {gx, gxs, d, false}, Wt(b + 5, d, false), ga_mlp, ff, 1, 0, st);
-      mm2(T, ff, d, {gdx, gdxs, d, false}, Wt(b + 5, d, false), {gx, gxs, d, false},
-          {V_(b + 5), Vs(b + 5), d, false}, gda_mlp, ff, 1, 0, st);
+      mm_tw(T, ff, d, {gx, gxs, d, false}, Wt(b + 5, d, false), {gdx, gdxs, d, false}, {V_(b + 5), Vs(b + 5), d, false}, ga_mlp, gda_mlp, ff, 1, 0, st, nullptr, nullptr, nullptr, nullptr);
       mm2(ff, d, T, {Ly.du, Ly.dus, ff, true}, {gx, gxs, d, true}, {Ly.u, Ly.us, ff, true}, {gdx, gdxs, d, true},
           HV(b + 5), d, 1, hb, st);
       sd::llama_swiglu_bwd(Ly.f, Ly.df, ga_mlp, gda_mlp, gu, gus, gdu, gdus, T, ff, st);
       // gate|up: gh = gfu Wgu^T ; gdh = gdfu Wgu^T + gfu VWgu^T ; Hv_Wgu = dh2^T gfu + h2^T gdfu
-      mm(T, d, 2 * ff, {gu, gus, 2 * ff, false}, Wt(b + 4, 2 * ff, false), gh, d, 1, 0, st);
-      mm2(T, d, 2 * ff, {gdu, gdus, 2 * ff, false}, Wt(b + 4, 2 * ff, false),
-          {gu, gus, 2 * ff, false}, {V_(b + 4), Vs(b + 4), 2 * ff, false}, gdh, d, 1, 0, st);
+      mm_tw(T, d, 2 * ff, {gu, gus, 2 * ff, false}, Wt(b + 4, 2 * ff, false), {gdu, gdus, 2 * ff, false}, {V_(b + 4), Vs(b + 4), 2 * ff, false}, gh, gdh, d, 1, 0, st, nullptr, nullptr, nullptr, nullptr);
       mm2(d, 2 * ff, T, {Ly.dh2, Ly.dh2s, d, true}, {gu, gus, 2 * ff, true}, {Ly.h2, Ly.h2s, d, true},
           {gdu, gdus, 2 * ff, true}, HV(b + 4), 2 * ff, 1, hb, st);
       sd::LnBwdArgs b2{gh, gdh, th(b + 3), V_(b + 3), Ly.xh2, Ly.dxh2, Ly.r2, Ly.dr2, T, d,
                        gx, gdx, gxs, gdxs, HV(b + 3), nullptr, red, 1, int(acc)};
       sd::gpt_ln_bwd(b2, st);
       // attention output projection
-      mm(T, d, d, {gx, gxs, d, false}, Wt(b + 2, d, false), go, d, 1, 0, st, nullptr, gos);
-      mm2(T, d, d, {gdx, gdxs, d, false}, Wt(b + 2, d, false), {gx, gxs, d, false},
-          {V_(b + 2), Vs(b + 2), d, false}, gdo, d, 1, 0, st, nullptr, gdos);
+      mm_tw(T, d, d, {gx, gxs, d, false}, Wt(b + 2, d, false), {gdx, gdxs, d, false}, {V_(b + 2), Vs(b + 2), d, false}, go, gdo, d, 1, 0, st, nullptr, gos, nullptr, gdos);
       mm2(d, d, T, {Ly.dO, Ly.dOs, d, true}, {gx, gxs, d, true}, {Ly.o, Ly.os, d, true}, {gdx, gdxs, d, true},
           HV(b + 2), d, 1, hb, st);
       attention_bwd(Ly, sc, st);
@@ -747,9 +728,7 @@ struct sd_gpt_s {
         sd::llama_gqa_reduce(ga, gda, gqkv, gqkvs, gdqkv, gdqkvs, T, d, dh, KV, H, st);
         qg = gqkv, qgs = gqkvs, qgd = gdqkv, qgds = gdqkvs;
       }
-      mm(T, d, W, {qg, qgs, W, false}, Wt(b + 1, W, false), gh, d, 1, 0, st);
-      mm2(T, d, W, {qgd, qgds, W, false}, Wt(b + 1, W, false), {qg, qgs, W, false},
-          {V_(b + 1), Vs(b + 1), W, false}, gdh, d, 1, 0, st);
+      mm_tw(T, d, W, {qg, qgs, W, false}, Wt(b + 1, W, false), {qgd, qgds, W, false}, {V_(b + 1), Vs(b + 1), W, false}, gh, gdh, d, 1, 0, st, nullptr, nullptr, nullptr, nullptr);
       mm2(d, W, T, {Ly.dh1, Ly.dh1s, d, true}, {qg, qgs, W, true}, {Ly.h1, Ly.h1s, d, true}, {qgd, qgds, W, true},
           HV(b + 1), W, 1, hb, st);
       sd::LnBwdArgs b1{gh, gdh, th(b), V_(b), Ly.xh1, Ly.dxh1, Ly.r1, Ly.dr1, T, d,

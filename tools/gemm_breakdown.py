@@ -23,6 +23,9 @@ for i, s in zip(order, shp):
     if s["nsrc"] == "split":  # A [B | B2] and A2 B: two A operands, B and B2 once, C and C2
         ns = "split"
         alg = 4.0 * Z * (2 * M * K + N * K + M * N)
+    elif s["nsrc"] == "twin":  # A B and A2 B + A B2: A, A2, B, B2 once, C and C2
+        ns = "twin"
+        alg = 4.0 * Z * (2 * M * K + 2 * N * K + 2 * M * N)
     else:
         ns = int(float(s["nsrc"]))
         alg = 4.0 * Z * (ns * (M * K + N * K) + M * N)
