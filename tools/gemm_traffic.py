@@ -45,14 +45,22 @@ if a.summarise:
     shp = list(csv.DictReader(open(a.shapes)))
     alg = 0.0
     for s in shp:
-        M, N, K, Z, ns = (int(float(s[k])) for k in ("M", "N", "K", "batch", "nsrc"))
-        alg += 4.0 * Z * (ns * (M * K + N * K) + M * N)
+        M, N, K, Z = (int(float(s[k])) for k in ("M", "N", "K", "batch"))
+        if s["nsrc"] == "split":  # [A B | A B2 + A2 B]: A, A2 once, B | B2 (N wide) once, C | C2
+            alg += 4.0 * Z * (2 * M * K + N * K + M * N)
+        elif s["nsrc"] == "twin":  # A B and A2 B + A B2: A, A2, B, B2 once, C and C2
+            alg += 4.0 * Z * (2 * M * K + 2 * N * K + 2 * M * N)
+        else:
+            ns = int(float(s["nsrc"]))
+            alg += 4.0 * Z * (ns * (M * K + N * K) + M * N)
     out = {"launches_ncu": len(gem), "launches_shapes": len(shp),
            "bytes_per_launch": (rd + wr) / max(1, len(gem)), "dram_read_bytes": rd, "dram_write_bytes": wr,
            "algorithmic_bytes_per_launch": alg / max(1, len(shp)),
            "ratio_measured_over_algorithmic": (rd + wr) / alg if alg else None,
            "how": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum over every k_gemm* launch of one "
-                  "GPT-2-small HVP (8x1024 tokens); algorithmic = 4*batch*(nsrc*(MK+NK)+MN) per launch"}
+                  "GPT-2-small HVP (8x1024 tokens); algorithmic = 4*batch*(nsrc*(MK+NK)+MN) per launch "
+                  "(each operand read once, each output written once; split pairs and twin products count "
+                  "their distinct operands and both outputs)"}
     Path(a.out).write_text(json.dumps(out, indent=1))
     print(json.dumps(out))
     sys.exit(0)
