@@ -211,6 +211,28 @@ int choose_splits(int tiles, int units, int total_kb, int nsrc, double t_kb, dou
   return best_s;
 }
 
+// Split count of a twin launch: its units are the C2 tiles (two sources,
+// first) and the C tiles (one source) of every split, dealt round-robin to the
+// cluster slots; the modelled time is the busiest slot's k-blocks plus the
+// split-K partial traffic (as choose_splits).
+int choose_splits_twin(int tiles, int units, int total_kb, double t_kb, double out_bytes) {
+  int best_s = 1;
+  double best = 0.0;
+  std::vector<long long> load(units);
+  for (int s = 1; s <= 16 && (s == 1 || total_kb / s >= 16); ++s) {
+    const long long kb = (total_kb + s - 1) / s, n = (long long)tiles * s;
+    std::fill(load.begin(), load.end(), 0);
+    for (long long t = 0; t < 2 * n; ++t) load[t % units] += (t < n ? 2 : 1) * kb;
+    const double c = double(*std::max_element(load.begin(), load.end())) * t_kb +
+                     (s > 1 ? 2.0 * s * out_bytes / 6.0e12 + 5e-6 : 0.0);
+    if (s == 1 || c < best * 0.97) {
+      best = c;
+      best_s = s;
+    }
+  }
+  return best_s;
+}
+
 // C = alpha * sum_split partial[split] + beta * C + bias (fixed split order)
 __device__ __forceinline__ float tf32_residual(float r) {
   return r - __uint_as_float(__float_as_uint(r) & 0xFFFFE000u);
@@ -362,7 +384,8 @@ __global__ void __launch_bounds__(kThreadsFor<TA>(), 1)
                 const __grid_constant__ CUtensorMap mB, const __grid_constant__ CUtensorMap mBs,
                 const __grid_constant__ CUtensorMap mA2, const __grid_constant__ CUtensorMap mAs2,
                 const __grid_constant__ CUtensorMap mB2, const __grid_constant__ CUtensorMap mBs2,
-                const __grid_constant__ CUtensorMap mC, const __grid_constant__ CUtensorMap mCs, int K,
+                const __grid_constant__ CUtensorMap mC, const __grid_constant__ CUtensorMap mCs,
+                const __grid_constant__ CUtensorMap mC2, const __grid_constant__ CUtensorMap mCs2, int K,
                 EpiParams ep) {
   using Cf = Cfg<BN_>;
   constexpr int BN = Cf::BN, STAGES = Cf::STAGES, EC = Cf::EC;
@@ -423,22 +446,24 @@ __global__ void __launch_bounds__(kThreadsFor<TA>(), 1)
         const TileInfo ti = tile_info<BN, CAUSAL>(ep, t, K);
         if (ti.skip) continue;
         const int z1 = ti.z % ep.Z1, z2 = ti.z / ep.Z1;
-        for (int kk = 0; kk < ep.nsrc * ti.num_kb; ++kk, ++g) {
+        for (int kk = 0; kk < ti.nsrc * ti.num_kb; ++kk, ++g) {
           const int s = g % STAGES;
           const uint32_t ph = (g / STAGES) & 1;
           mbar_wait(&empty[s], ph ^ 1);
           unsigned char* st = smem + s * STAGE_BYTES;
-          // dual source: the second product's k-blocks follow the first's
-          // (split pairs: interleaved, and source 2 multiplies B, not B2)
+          // dual source: the second product's k-blocks follow the first's, (A, B)
+          // then (A2, B2); twin C2 tiles: (A2, B) then (A, B2); split pairs:
+          // interleaved, and source 2 multiplies B, not B2
           const bool src2 = ep.split ? (kk & 1) != 0 : kk >= ti.num_kb;
+          const bool useA2 = ti.tan ? !src2 : src2, useB2 = src2 && !ep.split;
           const bool bex = THREE && !ep.res && ((ep.bexact >> (src2 ? 1 : 0)) & 1);
           mbar_expect_tx_e(&full[s], ep.split ? A_BYTES + (src2 ? B_BYTES / 2 : B_BYTES)
                                               : (ep.res ? A_BYTES + B_BYTES : STAGE_BYTES - (bex ? B_BYTES : 0)));
           const int kb = ep.split ? kk >> 1 : (src2 ? kk - ti.num_kb : kk);
-          const CUtensorMap* pA = src2 ? &mA2 : &mA;
-          const CUtensorMap* pAs = src2 ? &mAs2 : &mAs;
-          const CUtensorMap* pB = (src2 && !ep.split) ? &mB2 : &mB;
-          const CUtensorMap* pBs = (src2 && !ep.split) ? &mBs2 : &mBs;
+          const CUtensorMap* pA = useA2 ? &mA2 : &mA;
+          const CUtensorMap* pAs = useA2 ? &mAs2 : &mAs;
+          const CUtensorMap* pB = useB2 ? &mB2 : &mB;
+          const CUtensorMap* pBs = useB2 ? &mBs2 : &mBs;
           const int k0 = (ti.kb0 + kb) * BK;
           if (A_MN && (ep.mn5 & 1)) {
             tma_load_5d_e(pA, &full[s], st, 0, k0, ti.m0 / 32, z1, z2);
@@ -482,7 +507,7 @@ __global__ void __launch_bounds__(kThreadsFor<TA>(), 1)
     for (int t = blockIdx.x; t < ep.n_tiles; t += gridDim.x) {
       const TileInfo ti = tile_info<BN, CAUSAL>(ep, t, K);
       if (ti.skip) continue;
-      for (int kk = 0; kk < ep.nsrc * ti.num_kb; ++kk, ++g) {
+      for (int kk = 0; kk < ti.nsrc * ti.num_kb; ++kk, ++g) {
         const int s = g % STAGES;
         mbar_wait(&full[s], (g / STAGES) & 1);
         unsigned char* st = smem + s * STAGE_BYTES;
@@ -536,7 +561,7 @@ __global__ void __launch_bounds__(kThreadsFor<TA>(), 1)
       for (int t = blockIdx.x; t < ep.n_tiles; t += gridDim.x) {
         const TileInfo ti = tile_info<BN, CAUSAL>(ep, t, K);
         if (ti.skip) continue;
-        for (int kk = 0; kk < ep.nsrc * ti.num_kb; ++kk, ++g) {
+        for (int kk = 0; kk < ti.nsrc * ti.num_kb; ++kk, ++g) {
           if (int(g % kConvWarps) != cw) continue;
           const int s = g % STAGES;
           mbar_wait(&full[s], (g / STAGES) & 1);
@@ -555,7 +580,7 @@ __global__ void __launch_bounds__(kThreadsFor<TA>(), 1)
     for (int t = blockIdx.x; t < ep.n_tiles; t += gridDim.x) {
       const TileInfo ti = tile_info<BN, CAUSAL>(ep, t, K);
       if (ti.skip) continue;
-      const int nkb = ep.nsrc * ti.num_kb;
+      const int nkb = ti.nsrc * ti.num_kb;
       for (int kb = 0; kb < nkb; ++kb, ++g) {
         const int s = g % STAGES;
         const uint32_t ph = (g / STAGES) & 1;
@@ -613,7 +638,7 @@ __global__ void __launch_bounds__(kThreadsFor<TA>(), 1)
       float acc[EC];
 #pragma unroll
       for (int j = 0; j < EC; ++j) acc[j] = 0.0f;
-      const int nchunks = (ep.nsrc * ti.num_kb + KC - 1) / KC;
+      const int nchunks = (ti.nsrc * ti.num_kb + KC - 1) / KC;
       for (int c = 0; c < nchunks; ++c, ++chunk) {
         const uint32_t buf = chunk & 1;
         mbar_wait(&tfull[buf], (chunk >> 1) & 1);
@@ -632,10 +657,16 @@ __global__ void __launch_bounds__(kThreadsFor<TA>(), 1)
       }
       if (ep.tma_store) {
         const int ew = warp - 2 - CONV;  // 0..7: its staging box
-        warp_tma_store<EC>(&mC, ep.Cs ? &mCs : nullptr, epi_stage + ew * 1024, acc, ep.alpha,
-                           ep.bias, lane, ti.m0 + sub * 32, ti.n0 + cb, ti.z % ep.Z1, ti.z / ep.Z1);
+        const bool t2 = ti.tan;          // twin: C2's tile
+        const CUtensorMap* pcs = t2 ? (ep.Cs2 ? &mCs2 : nullptr) : (ep.Cs ? &mCs : nullptr);
+        warp_tma_store<EC>(t2 ? &mC2 : &mC, pcs, epi_stage + ew * 1024, acc, t2 ? ep.alpha2 : ep.alpha,
+                           t2 ? ep.bias2 : ep.bias, lane, ti.m0 + sub * 32, ti.n0 + cb, ti.z % ep.Z1, ti.z / ep.Z1);
         if (lane == 0) bulk_wait_read0();  // staging box free for the next tile
         __syncwarp();
+      } else if (ti.tan) {
+        EpiParams e2 = ep;  // twin: C2's tile
+        e2.C = ep.C2, e2.Cs = ep.Cs2, e2.alpha = ep.alpha2, e2.beta = ep.beta2, e2.bias = ep.bias2, e2.ws = ep.ws2;
+        store_row<EC>(e2, ti, row, ti.n0 + cb, acc);
       } else if (ep.split && cb >= BN / 2) {
         EpiParams e2 = ep;  // columns BN/2.. of the split pair: the second output
         e2.C = ep.C2, e2.Cs = ep.Cs2;
@@ -693,20 +724,35 @@ void launch(const GemmArgs& g, cudaStream_t s) {
   // ceil(tiles*s/148)/s (each split keeps >= 16 k-blocks), smallest s on ties.
   // one worker: 128 x BN x BK per k-block at ~200 TF/s (algorithmic) per 148 SMs
   const double t_kb = 2.0 * BM * BN * BK / (2.0e14 / kNumSMs) / (THREE ? 1.0 : 3.0);
-  int splits = g.causal == 0 ? choose_splits(tiles, kNumSMs, total_kb, dual ? 2 : 1, t_kb, 4.0 * zc * g.M * g.N) : 1;
+  const bool twin = g.twin;
+  int splits = g.causal == 0 ? (twin ? choose_splits_twin(tiles, kNumSMs, total_kb, t_kb, 8.0 * zc * g.M * g.N)
+                                     : choose_splits(tiles, kNumSMs, total_kb, dual ? 2 : 1, t_kb, 4.0 * zc * g.M * g.N))
+                             : 1;
   const int kb_per = (total_kb + splits - 1) / splits;
   splits = (total_kb + kb_per - 1) / kb_per;
+  const size_t part = size_t(splits) * zc * size_t(g.M) * g.N;
   float* ws = nullptr;
-  if (splits > 1) ws = splitk_workspace(size_t(splits) * zc * size_t(g.M) * g.N);
+  if (splits > 1) ws = splitk_workspace((twin ? 2 : 1) * part);
   EpiParams ep{g.C, g.ldc, g.sc1, g.sc2, g.M, g.N, g.Z1, g.alpha, g.beta, g.bias, g.Cs, g.dbg, zc, kb_per, ws,
-               g.causal, tn, tm, tiles * splits, dual ? 2 : 1, g.onchip ? 1 : 0};
+               g.causal, tn, tm, tiles * splits * (twin ? 2 : 1), dual ? 2 : 1, g.onchip ? 1 : 0};
+  GemmArgs g2 = g;  // twin: C2's epilogue
+  g2.C = g.C2, g2.Cs = g.Cs2, g2.alpha = g.alpha2, g2.beta = g.beta2, g2.bias = g.bias2;
+  if (twin) {
+    ep.twin = 1, ep.tiles1 = tiles * splits;
+    ep.C2 = g.C2, ep.Cs2 = g.Cs2, ep.alpha2 = g.alpha2, ep.beta2 = g.beta2, ep.bias2 = g.bias2;
+    ep.ws2 = ws ? ws + part : nullptr;
+  }
   const size_t smem = 1024 + size_t(Cf::STAGES) * (THREE ? 2 : 1) * (Cf::A_BYTES + Cf::B_BYTES) + 8 * 4096 + 512;
   // TMA-store epilogue: plain C = alpha op(A) op(B) tiles (no accumulate/bias/residual/split)
-  CUtensorMap mC = maps[0], mCs = maps[0];
-  const bool tma_store = tma_store_ok(g, splits, 32);
+  CUtensorMap mC = maps[0], mCs = maps[0], mC2 = maps[0], mCs2 = maps[0];
+  const bool tma_store = tma_store_ok(g, splits, 32) && (!twin || tma_store_ok(g2, splits, 32));
   if (tma_store) {
     make_store_map(&mC, g.C, g);
     if (g.Cs) make_store_map(&mCs, g.Cs, g);
+    if (twin) {
+      make_store_map(&mC2, g2.C, g2);
+      if (g2.Cs) make_store_map(&mCs2, g2.Cs, g2);
+    }
   }
   ep.tma_store = tma_store ? 1 : 0;
   ep.mn5 = mn5;
@@ -741,15 +787,16 @@ void launch(const GemmArgs& g, cudaStream_t s) {
   if (prof().on)
     prof().next_tag = std::to_string(g.M) + "," + std::to_string(g.N) + "," + std::to_string(g.K) + "," +
                       std::to_string(zc) + "," + std::to_string(int(A_MN)) + "," + std::to_string(int(B_MN)) + "," +
-                      std::to_string(g.causal) + "," + std::to_string(splits) + (dual ? ",2" : ",1");
+                      std::to_string(g.causal) + "," + std::to_string(splits) + (twin ? ",twin" : dual ? ",2" : ",1");
   prof_begin(s);
   launch_gemm_kernel(kern, unsigned(grid), unsigned(threads), smem, s, maps[0], maps[1], maps[2], maps[3], maps[4],
-                     maps[5], maps[6], maps[7], mC, mCs, g.K, ep);
+                     maps[5], maps[6], maps[7], mC, mCs, mC2, mCs2, g.K, ep);
   SD_LAUNCHED("k_gemm_tf32");
   if (splits > 1) {
     launch_splitk_reduce(ws, splits, zc, g, s);
+    if (twin) launch_splitk_reduce(ws + part, splits, zc, g2, s);
   }
-  prof_end(s, (dual ? 4.0 : 2.0) * double(g.M) * g.N * g.K * g.Z1 * g.Z2);
+  prof_end(s, (twin ? 6.0 : dual ? 4.0 : 2.0) * double(g.M) * g.N * g.K * g.Z1 * g.Z2);
 }
 
 // Merged pair of 64-wide products sharing A (GemmArgs::split): one 1-CTA
@@ -799,7 +846,7 @@ void launch_split(const GemmArgs& g, cudaStream_t s) {
                       ",1,split";
   prof_begin(s);
   launch_gemm_kernel(kern, unsigned(grid), unsigned(kThreadsFor<true>()), smem, s, maps[0], maps[1], maps[2], maps[3],
-                     maps[4], maps[5], maps[6], maps[7], maps[0], maps[0], g.K, ep);
+                     maps[4], maps[5], maps[6], maps[7], maps[0], maps[0], maps[0], maps[0], g.K, ep);
   SD_LAUNCHED("k_gemm_tf32_split");
   // algorithmic flops of the pair: A B + A B2 + A2 B
   prof_end(s, 6.0 * double(g.M) * g.N * g.K * g.Z1 * g.Z2);
@@ -832,11 +879,14 @@ void gemm(const GemmArgs& g_in, cudaStream_t s) {
   if (g_in.M <= 0 || g_in.N <= 0 || g_in.K <= 0) return;
   if (g_in.twin) {
     if (!g_in.A2 || !g_in.B2 || !g_in.C2 || g_in.split) fail(SD_ARGUMENT_ERROR, "twin gemm needs A2, B2 and C2");
-    // one launch for the weight products (K = d or ff); the LM-head adjoint
-    // (K = vocab: the logits-sized A operands dominate, and the twin walk
-    // re-streams them: 23 vs 15 GB measured) stays two launches
-    const bool one = g_in.causal == 0 && g_in.M >= 256 && g_in.N >= 256 && g_in.K <= 16384 &&
-                     sd_gemm_pair_enabled() && twin_enabled();
+    // one launch for the weight products (K = d or ff; pair kernel) and the
+    // per-head score products (causal 1, 128-wide tiles; k_gemm_tf32); the
+    // LM-head adjoint (K = vocab: the logits-sized A operands dominate, and
+    // the twin walk re-streams them: 23 vs 15 GB measured) stays two launches
+    const bool pair_ok = g_in.causal == 0 && g_in.M >= 256 && g_in.N >= 256 && g_in.K <= 16384 &&
+                         sd_gemm_pair_enabled();
+    const bool score_ok = g_in.causal == 1 && g_in.N > 64 && g_in.M == g_in.N;
+    const bool one = twin_enabled() && (pair_ok || score_ok);
     if (!one) {  // C = alpha A B + beta C ; C2 = alpha2 (A2 B + A B2) + beta2 C2
       GemmArgs p = g_in;
       p.twin = false, p.A2 = p.A2s = p.B2 = p.B2s = nullptr, p.b2_exact = false, p.C2 = p.Cs2 = nullptr;

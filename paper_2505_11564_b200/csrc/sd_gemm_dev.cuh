@@ -385,6 +385,9 @@ template <int BN, bool CAUSAL>
 __device__ __forceinline__ TileInfo tile_info(const EpiParams& ep, int t, int K) {
   TileInfo ti;
   int nt, mt, zz;
+  // twin (causal 0 / 1 only): tiles [0, tiles1) are C2's, then C's
+  ti.tan = ep.twin && t < ep.tiles1;
+  if (ep.twin && !ti.tan) t -= ep.tiles1;
   if (CAUSAL && ep.causal == 1 && BN == BM) {
     // only the tm (tm + 1) / 2 lower-triangle tiles of each square head are
     // enumerated: every CTA of the round-robin gets equal work
@@ -408,7 +411,7 @@ __device__ __forceinline__ TileInfo tile_info(const EpiParams& ep, int t, int K)
   } else {
     walk_tile(ep, t, mt, nt, zz);
   }
-  ti.nsrc = ep.nsrc;
+  ti.nsrc = ep.twin ? (ti.tan ? 2 : 1) : ep.nsrc;
   ti.n0 = nt * BN;
   ti.m0 = mt * BM;
   ti.z = zz % ep.zcount;
@@ -514,6 +517,7 @@ void make_store_map(CUtensorMap* m, float* C, const GemmArgs& g, int box_cols = 
 bool tma_store_ok(const GemmArgs& g, int splits, int bias_cols);
 float* splitk_workspace(size_t floats);
 int choose_splits(int tiles, int units, int total_kb, int nsrc, double t_kb, double out_bytes);
+int choose_splits_twin(int tiles, int units, int total_kb, double t_kb, double out_bytes);
 void operand_maps(const GemmArgs& g, bool a_mn, bool b_mn, bool three, int box_n, CUtensorMap* m, int* mn5);
 bool prof_on();
 void prof_tag(const std::string& tag);

@@ -385,28 +385,6 @@ int max_clusters(const void* kern, size_t smem) {
   return n;
 }
 
-// Split count of a twin launch: its units are the C2 tiles (two sources,
-// first) and the C tiles (one source) of every split, dealt round-robin to the
-// cluster slots; the modelled time is the busiest slot's k-blocks plus the
-// split-K partial traffic (as choose_splits).
-int choose_splits_twin(int tiles, int units, int total_kb, double t_kb, double out_bytes) {
-  int best_s = 1;
-  double best = 0.0;
-  std::vector<long long> load(units);
-  for (int s = 1; s <= 16 && (s == 1 || total_kb / s >= 16); ++s) {
-    const long long kb = (total_kb + s - 1) / s, n = (long long)tiles * s;
-    std::fill(load.begin(), load.end(), 0);
-    for (long long t = 0; t < 2 * n; ++t) load[t % units] += (t < n ? 2 : 1) * kb;
-    const double c = double(*std::max_element(load.begin(), load.end())) * t_kb +
-                     (s > 1 ? 2.0 * s * out_bytes / 6.0e12 + 5e-6 : 0.0);
-    if (s == 1 || c < best * 0.97) {
-      best = c;
-      best_s = s;
-    }
-  }
-  return best_s;
-}
-
 template <bool A_MN, bool B_MN, bool THREE, int PN>
 void launch_pair_t(const GemmArgs& g, cudaStream_t s) {
   using PC = PairCfg<PN>;

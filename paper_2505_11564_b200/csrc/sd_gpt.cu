@@ -319,7 +319,8 @@ struct sd_gpt_s {
   // primal and tangent products of the R-op forward and adjoint -- as one
   // launch over both outputs' tiles (SD_GEMM_TWIN=0: the two launches)
   void mm_tw(int M, int N, int K, Op A, Op Bo, Op A2, Op B2, float* C, float* C2, long long ldc, float alpha,
-             float beta, cudaStream_t st, const float* bias, float* Cs, const float* bias2, float* Cs2) {
+             float beta, cudaStream_t st, const float* bias, float* Cs, const float* bias2, float* Cs2, int Z1 = 1,
+             int Z2 = 1, long long c1 = 0, long long c2 = 0) {
     sd::GemmArgs g;
     g.M = M, g.N = N, g.K = K;
     g.A = A.p, g.As = A.s, g.lda = A.ld, g.a_mn = A.mn;
@@ -328,6 +329,8 @@ struct sd_gpt_s {
     g.A2 = A2.p, g.A2s = A2.s, g.lda2 = A2.ld, g.B2 = B2.p, g.B2s = B2.s, g.ldb2 = B2.ld, g.b2_exact = B2.exact;
     g.C = C, g.ldc = ldc, g.alpha = alpha, g.beta = beta, g.bias = bias, g.Cs = Cs;
     g.twin = true, g.C2 = C2, g.Cs2 = Cs2, g.alpha2 = alpha, g.beta2 = beta, g.bias2 = bias2;
+    g.Z1 = Z1, g.Z2 = Z2, g.sa1 = A.s1, g.sa2 = A.s2, g.sb1 = Bo.s1, g.sb2 = Bo.s2, g.sc1 = c1, g.sc2 = c2;
+    g.sa1_2 = A2.s1, g.sa2_2 = A2.s2, g.sb1_2 = B2.s1, g.sb2_2 = B2.s2;
     g.causal = cmode;
     onchip_residuals(g);
     sd::gemm(g, st);
@@ -746,10 +749,10 @@ struct sd_gpt_s {
     const long long ho = dh, bo = (long long)Sq * d;          // in o [T, d]
     auto q = [&](float* base, float* res) { return Op{base, res, 3 * d, false, ha, ba}; };
     cmode = 1;  // scores: only j <= i tiles
-    mm(Sq, Sq, dh, q(Ly.a, Ly.as), {Ly.a + d, Ly.as + d, 3 * d, false, ha, ba}, Ly.P, Sq, sc, 0, st, nullptr,
-       nullptr, H, B, hs, bs);
-    mm2(Sq, Sq, dh, q(Ly.da, Ly.das), {Ly.a + d, Ly.as + d, 3 * d, false, ha, ba}, q(Ly.a, Ly.as),
-        {Ly.da + d, Ly.das + d, 3 * d, false, ha, ba}, Ly.dP, Sq, sc, 0, st, nullptr, nullptr, H, B, hs, bs);
+    // S = sc q k^T and dS = sc (dq k^T + q dk^T): one twin launch
+    mm_tw(Sq, Sq, dh, q(Ly.a, Ly.as), {Ly.a + d, Ly.as + d, 3 * d, false, ha, ba}, q(Ly.da, Ly.das),
+          {Ly.da + d, Ly.das + d, 3 * d, false, ha, ba}, Ly.P, Ly.dP, Sq, sc, 0, st, nullptr, nullptr, nullptr, nullptr,
+          H, B, hs, bs);
     sd::gpt_attn_softmax_fwd(Ly.P, Ly.dP, Ly.Ps, Ly.dPs, Sq, (long long)B * H * Sq, st);
     const Op Pm{Ly.P, Ly.Ps, Sq, false, hs, bs}, dPm{Ly.dP, Ly.dPs, Sq, false, hs, bs};
     const Op vv{Ly.a + 2 * d, Ly.as + 2 * d, 3 * d, true, ha, ba}, dvv{Ly.da + 2 * d, Ly.das + 2 * d, 3 * d, true, ha, ba};
@@ -774,8 +777,7 @@ struct sd_gpt_s {
     const Op goK{go, gos, d, false, ho, bo}, gdoK{gdo, gdos, d, false, ho, bo};
     const Op vK{Ly.a + 2 * d, Ly.as + 2 * d, 3 * d, false, ha, ba}, dvK{Ly.da + 2 * d, Ly.das + 2 * d, 3 * d, false, ha, ba};
     cmode = 1;
-    mm(Sq, Sq, dh, goK, vK, gP, Sq, 1, 0, st, nullptr, nullptr, H, B, hs, bs);
-    mm2(Sq, Sq, dh, gdoK, vK, goK, dvK, gdP, Sq, 1, 0, st, nullptr, nullptr, H, B, hs, bs);
+    mm_tw(Sq, Sq, dh, goK, vK, gdoK, dvK, gP, gdP, Sq, 1, 0, st, nullptr, nullptr, nullptr, nullptr, H, B, hs, bs);
     sd::gpt_attn_softmax_bwd(Ly.P, Ly.dP, gP, gdP, gPs, gdPs, Sq, (long long)B * H * Sq, st);
     // value adjoints
     const Op PT{Ly.P, Ly.Ps, Sq, true, hs, bs}, dPT{Ly.dP, Ly.dPs, Sq, true, hs, bs};
