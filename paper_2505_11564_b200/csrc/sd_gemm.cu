@@ -883,10 +883,16 @@ void gemm(const GemmArgs& g_in, cudaStream_t s) {
     // per-head score products (causal 1, 128-wide tiles; k_gemm_tf32); the
     // LM-head adjoint (K = vocab: the logits-sized A operands dominate, and
     // the twin walk re-streams them: 23 vs 15 GB measured) stays two launches
-    const bool pair_ok = g_in.causal == 0 && g_in.M >= 256 && g_in.N >= 256 && g_in.K <= 16384 &&
+    // (measured: GPT-2-small at 8192 tokens -1.5 ms of GEMM per HVP; the C4
+    // stage's 1024-token micro-batches +2% per step, so short token panels
+    // keep two launches)
+    const bool pair_ok = g_in.causal == 0 && g_in.M >= 4096 && g_in.N >= 256 && g_in.K <= 16384 &&
                          sd_gemm_pair_enabled();
     const bool score_ok = g_in.causal == 1 && g_in.N > 64 && g_in.M == g_in.N;
-    const bool one = twin_enabled() && (pair_ok || score_ok);
+    // on-chip residuals (an operand without its residual array, e.g. the probe
+    // under SD_GPT_NO_PROBE_RESIDUAL) would extend to the primal product and
+    // drop its exact-B 2-MMA path: two launches then
+    const bool one = twin_enabled() && (pair_ok || score_ok) && !g_in.onchip;
     if (!one) {  // C = alpha A B + beta C ; C2 = alpha2 (A2 B + A B2) + beta2 C2
       GemmArgs p = g_in;
       p.twin = false, p.A2 = p.A2s = p.B2 = p.B2s = nullptr, p.b2_exact = false, p.C2 = p.Cs2 = nullptr;
