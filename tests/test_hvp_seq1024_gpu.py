@@ -150,12 +150,22 @@ eng = gpt.GptHvp(cfg, 2, 1024, init_seed=2, gain_scale=0.1, bias_scale=0.1)
 out = torch.empty(eng.P, device="cuda")
 g = torch.Generator(device="cuda").manual_seed(7)
 res = []
-for i in range(4):  # eager warm-up, capture, replay, replay (fixed output pointer)
-    v = torch.randn(eng.P, device="cuda", generator=g).contiguous()
+def call(v):
     n0 = lib().sd_launch_count()
     eng.hvp(v, out)
     torch.cuda.synchronize()
     res.append([hashlib.sha256(out.cpu().numpy().tobytes()).hexdigest(), lib().sd_launch_count() - n0])
+for i in range(4):  # eager warm-up, capture, replay, replay (fixed output pointer)
+    call(torch.randn(eng.P, device="cuda", generator=g).contiguous())
+# a new batch (same loss scale: replayed with the new token contents), then a
+# new loss scale (a captured kernel argument: eager, recapture, replay)
+tok, tgt = gpt.synthetic_tokens(cfg["vocab"], 2, 1024, seed=9)
+eng.set_batch(tok, tgt)
+v = torch.randn(eng.P, device="cuda", generator=g).contiguous()
+call(v)
+eng.set_batch(tok, tgt, loss_scale=0.25 / 2048)
+for i in range(3):
+    call(v)
 print(json.dumps(res))
 """
 
