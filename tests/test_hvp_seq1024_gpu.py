@@ -187,3 +187,35 @@ def test_cuda_graph_replay_bitwise(gpt):
     counts = [n for _, n in out["graph"]] + [n for _, n in out["eager"]]
     assert len(set(counts)) == 1 and counts[0] > 0, counts
 
+
+_HV_NPY = r"""
+import sys
+import numpy as np
+import torch
+sys.path.insert(0, sys.argv[1])
+from paper_2505_11564_b200 import gpt
+eng = gpt.GptHvp(gpt.GPT2_SMALL, 4, 1024, init_seed=4, gain_scale=0.1, bias_scale=0.1)
+g = torch.Generator(device="cuda").manual_seed(3)
+v = torch.randn(eng.P, device="cuda", generator=g).contiguous()
+np.save(sys.argv[2], eng.hvp(v).cpu().numpy())
+"""
+
+
+def test_twin_products_match_two_launches(gpt, tmp_path):
+    """Twin launches (a weight's primal and tangent products in one launch,
+    the score products S / dS and gP / gdP likewise) against the two-launch
+    path (SD_GEMM_TWIN=0) on GPT-2-small at 4 x 1024 tokens: identical where
+    the split counts agree, else the same sums in another split partition --
+    within 2e-6 (the parity tests above bound both against float64)."""
+    import numpy as np
+    out = {}
+    for tag, extra in (("twin", {}), ("two", {"SD_GEMM_TWIN": "0"})):
+        f = tmp_path / f"{tag}.npy"
+        r = subprocess.run([sys.executable, "-c", _HV_NPY, str(ROOT), str(f)], env=dict(os.environ, **extra),
+                           capture_output=True, text=True, timeout=900)
+        assert r.returncode == 0, r.stderr[-2000:]
+        out[tag] = np.load(f).astype(np.float64)
+    e = float(np.linalg.norm(out["twin"] - out["two"]) / np.linalg.norm(out["two"]))
+    print(f"twin vs two launches: {e:.3e}")  # 5.1e-7 on the B200
+    assert e < 2e-6
+
