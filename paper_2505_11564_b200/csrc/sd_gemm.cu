@@ -20,6 +20,10 @@
 //   warps 4-11: epilogue: drain TMEM chunks (tcgen05.ld 32x32b) into
 //              round-to-nearest fp32 registers, then alpha/beta/bias,
 //              residual and store — overlapped with the next tile's MMAs.
+// Source structures per launch: one product; dual (C = A B + A2 B2, one
+// accumulator); twin (C = A B and C2 = A2 B + A B2 -- a weight's primal and
+// tangent products -- as two tile sets of one launch, C2's first); split
+// (the 64-wide attention pairs, below).
 // Operand majors: A is K-major (row-major M x K) or MN-major (row-major K x M);
 // B is K-major (row-major N x K) or MN-major (row-major K x N). A batch index
 // z decomposes as (z1 = z % Z1, z2 = z / Z1) with independent strides, which

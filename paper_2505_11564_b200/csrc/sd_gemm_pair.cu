@@ -12,8 +12,8 @@
 // TMEM allocator + (leader only) MMA issuer, warps 2-3 residual warps (write
 // the tf32 residual tiles on chip, then arrive on the leader's conv barrier),
 // warps 4..19 epilogue (16 warps: lane quadrant warp % 4, 64 columns each).
-// Same 3xTF32 scheme, chunked round-to-nearest drain (KC), dual-source and
-// split-K support as the single-CTA kernel in sd_gemm.cu.
+// Same 3xTF32 scheme, chunked round-to-nearest drain (KC), dual-source, twin
+// and split-K support as the single-CTA kernel in sd_gemm.cu.
 #include <algorithm>
 #include <cstdlib>
 #include <string>
