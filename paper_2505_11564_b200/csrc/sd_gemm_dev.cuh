@@ -193,7 +193,23 @@ struct EpiParams {
   float alpha2, beta2;                // twin: C2's epilogue
   const float* bias2;
   float* ws2;                         // twin: C2's split-K partials
+  int ncl;                            // twin: worker slots of the launch (CTAs / clusters); the
+                                      // n_tiles slot indices (padded to whole rounds) are dealt
+                                      // boustrophedon (twin_unit); 0: plain round robin
 };
+
+// Twin launches deal their units -- C2's two-source tiles, then C's -- to the
+// persistent workers in boustrophedon order (round r of the static round robin
+// walks the workers forward for even r, backward for odd r), so the workers
+// that drew the last two-source units draw the first one-source units: e.g.
+// 96 + 96 units on 74 clusters, busiest worker 4 instead of 5 unit-costs.
+// Returns the unit of slot t, or -1 past the last unit.
+__device__ __forceinline__ int twin_unit(const EpiParams& ep, int t) {
+  if (ep.ncl == 0) return t;  // plain round robin
+  const int r = t / ep.ncl, p = t - r * ep.ncl;
+  const int u = r * ep.ncl + ((r & 1) ? ep.ncl - 1 - p : p);
+  return u < 2 * ep.tiles1 ? u : -1;
+}
 
 // Rasterisation. A persistent wave of clusters works on consecutive tile
 // indices, so the walk order decides which operand stays in L2: with n
@@ -385,7 +401,14 @@ template <int BN, bool CAUSAL>
 __device__ __forceinline__ TileInfo tile_info(const EpiParams& ep, int t, int K) {
   TileInfo ti;
   int nt, mt, zz;
-  // twin (causal 0 / 1 only): tiles [0, tiles1) are C2's, then C's
+  // twin (causal 0 / 1 only): units [0, tiles1) are C2's tiles, then C's
+  if (ep.twin) {
+    t = twin_unit(ep, t);
+    if (t < 0) {
+      ti.skip = true;
+      return ti;
+    }
+  }
   ti.tan = ep.twin && t < ep.tiles1;
   if (ep.twin && !ti.tan) t -= ep.tiles1;
   if (CAUSAL && ep.causal == 1 && BN == BM) {
