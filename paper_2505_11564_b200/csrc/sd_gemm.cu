@@ -847,6 +847,10 @@ void launch_split(const GemmArgs& g, cudaStream_t s) {
     attr = true;
   }
   const int grid = std::min(ep.n_tiles, kNumSMs);
+  if (g.causal == 2 || g.causal == 3) {  // K-trimmed row tiles, longest first: boustrophedon deal
+    ep.ncl = grid, ep.units = ep.n_tiles;
+    ep.n_tiles = (ep.n_tiles + ep.ncl - 1) / ep.ncl * ep.ncl;
+  }
   if (prof().on)
     prof().next_tag = std::to_string(g.M) + "," + std::to_string(2 * g.N) + "," + std::to_string(g.K) + "," +
                       std::to_string(zc) + "," + std::to_string(int(A_MN)) + ",1," + std::to_string(g.causal) +

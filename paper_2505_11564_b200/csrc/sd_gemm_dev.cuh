@@ -193,22 +193,24 @@ struct EpiParams {
   float alpha2, beta2;                // twin: C2's epilogue
   const float* bias2;
   float* ws2;                         // twin: C2's split-K partials
-  int ncl;                            // twin: worker slots of the launch (CTAs / clusters); the
-                                      // n_tiles slot indices (padded to whole rounds) are dealt
-                                      // boustrophedon (twin_unit); 0: plain round robin
+  int ncl, units;                     // boustrophedon deal (deal_unit): worker slots of the launch
+                                      // (CTAs / clusters) and the real units; n_tiles is then padded
+                                      // to whole rounds; ncl 0: plain round robin
 };
 
-// Twin launches deal their units -- C2's two-source tiles, then C's -- to the
-// persistent workers in boustrophedon order (round r of the static round robin
-// walks the workers forward for even r, backward for odd r), so the workers
-// that drew the last two-source units draw the first one-source units: e.g.
-// 96 + 96 units on 74 clusters, busiest worker 4 instead of 5 unit-costs.
-// Returns the unit of slot t, or -1 past the last unit.
-__device__ __forceinline__ int twin_unit(const EpiParams& ep, int t) {
-  if (ep.ncl == 0) return t;  // plain round robin
+// Launches whose units differ in cost -- a twin launch's two-source C2 tiles
+// then one-source C tiles, the causal K-trimmed attention products' row tiles
+// from the longest to the shortest -- deal them to the persistent workers in
+// boustrophedon order: round r of the static round robin walks the workers
+// forward for even r and backward for odd r, so the workers that drew the
+// last expensive units draw the first cheap ones (e.g. 96 + 96 twin units on
+// 74 clusters: busiest worker 4 instead of 5 unit-costs). Returns the unit of
+// slot t, or -1 past the last unit.
+__device__ __forceinline__ int deal_unit(const EpiParams& ep, int t) {
+  if (ep.ncl == 0) return t;
   const int r = t / ep.ncl, p = t - r * ep.ncl;
   const int u = r * ep.ncl + ((r & 1) ? ep.ncl - 1 - p : p);
-  return u < 2 * ep.tiles1 ? u : -1;
+  return u < ep.units ? u : -1;
 }
 
 // Rasterisation. A persistent wave of clusters works on consecutive tile
@@ -401,14 +403,12 @@ template <int BN, bool CAUSAL>
 __device__ __forceinline__ TileInfo tile_info(const EpiParams& ep, int t, int K) {
   TileInfo ti;
   int nt, mt, zz;
-  // twin (causal 0 / 1 only): units [0, tiles1) are C2's tiles, then C's
-  if (ep.twin) {
-    t = twin_unit(ep, t);
-    if (t < 0) {
-      ti.skip = true;
-      return ti;
-    }
+  t = deal_unit(ep, t);
+  if (t < 0) {
+    ti.skip = true;
+    return ti;
   }
+  // twin (causal 0 / 1 only): units [0, tiles1) are C2's tiles, then C's
   ti.tan = ep.twin && t < ep.tiles1;
   if (ep.twin && !ti.tan) t -= ep.tiles1;
   if (CAUSAL && ep.causal == 1 && BN == BM) {
@@ -426,7 +426,7 @@ __device__ __forceinline__ TileInfo tile_info(const EpiParams& ep, int t, int K)
     // K range grows (2) / shrinks (3) with the row tile: walk the row tiles
     // from the longest to the shortest, so that each round-robin wave holds
     // tiles of (nearly) equal cost
-    const int per = ep.n_tiles / ep.n_tiles_m;  // n tiles x (split, z)
+    const int per = (ep.ncl ? ep.units : ep.n_tiles) / ep.n_tiles_m;  // n tiles x (split, z)
     const int mi = t / per, rem = t % per;
     mt = ep.causal == 2 ? ep.n_tiles_m - 1 - mi : mi;
     nt = rem % ep.n_tiles_n;

@@ -111,12 +111,10 @@ template <int PN>
 __device__ __forceinline__ TileInfo pair_tile(const EpiParams& ep, int t, int K) {
   TileInfo ti;
   int mt, nt, zz;
-  if (ep.twin) {
-    t = twin_unit(ep, t);
-    if (t < 0) {
-      ti.skip = true;
-      return ti;
-    }
+  t = deal_unit(ep, t);
+  if (t < 0) {
+    ti.skip = true;
+    return ti;
   }
   ti.tan = ep.twin && t < ep.tiles1;
   ti.nsrc = ep.twin ? (ti.tan ? 2 : 1) : ep.nsrc;
@@ -430,8 +428,8 @@ void launch_pair_t(const GemmArgs& g, cudaStream_t s) {
   }
   ep.group = walk_group(g, kPairM, PN, tm, tn, THREE);
   const int grid = 2 * std::min(ep.n_tiles, clusters);
-  if (twin) {  // whole boustrophedon rounds over the cluster slots (twin_unit)
-    ep.ncl = grid / 2;
+  if (twin) {  // boustrophedon deal over the cluster slots (deal_unit)
+    ep.ncl = grid / 2, ep.units = ep.n_tiles;
     ep.n_tiles = (ep.n_tiles + ep.ncl - 1) / ep.ncl * ep.ncl;
   }
   if (prof_on())
