@@ -216,8 +216,8 @@ int choose_splits(int tiles, int units, int total_kb, int nsrc, double t_kb, dou
 }
 
 // Split count of a twin launch: its units are the C2 tiles (two sources,
-// first) and the C tiles (one source) of every split, dealt round-robin to the
-// cluster slots; the modelled time is the busiest slot's k-blocks plus the
+// first) and the C tiles (one source) of every split, dealt boustrophedon to
+// the cluster slots (deal_unit); the modelled time is the busiest slot's k-blocks plus the
 // split-K partial traffic (as choose_splits).
 int choose_splits_twin(int tiles, int units, int total_kb, double t_kb, double out_bytes) {
   int best_s = 1;
@@ -226,7 +226,10 @@ int choose_splits_twin(int tiles, int units, int total_kb, double t_kb, double o
   for (int s = 1; s <= 16 && (s == 1 || total_kb / s >= 16); ++s) {
     const long long kb = (total_kb + s - 1) / s, n = (long long)tiles * s;
     std::fill(load.begin(), load.end(), 0);
-    for (long long t = 0; t < 2 * n; ++t) load[t % units] += (t < n ? 2 : 1) * kb;
+    for (long long t = 0; t < 2 * n; ++t) {  // the boustrophedon deal of deal_unit
+      const long long r = t / units, p = t % units;
+      load[(r & 1) ? units - 1 - p : p] += (t < n ? 2 : 1) * kb;
+    }
     const double c = double(*std::max_element(load.begin(), load.end())) * t_kb +
                      (s > 1 ? 2.0 * s * out_bytes / 6.0e12 + 5e-6 : 0.0);
     if (s == 1 || c < best * 0.97) {
