@@ -897,10 +897,14 @@ void gemm(const GemmArgs& g_in, cudaStream_t s) {
     // per-head score products (causal 1, 128-wide tiles; k_gemm_tf32); the
     // LM-head adjoint (K = vocab: the logits-sized A operands dominate, and
     // the twin walk re-streams them: 23 vs 15 GB measured) stays two launches
-    // (measured: GPT-2-small at 8192 tokens -1.5 ms of GEMM per HVP; the C4
-    // stage's 1024-token micro-batches +2% per step, so short token panels
-    // keep two launches)
-    const bool pair_ok = g_in.causal == 0 && g_in.M >= 4096 && g_in.N >= 256 && g_in.K <= 16384 &&
+    // (measured with the boustrophedon deal: GPT-2-small at 8192 tokens
+    // -3.5 ms per step, the C3 micro-batches of 2048 tokens -1.5%, the C4
+    // stage's 1024-token micro-batches -0.3%)
+    static const int min_m = [] {  // SD_GEMM_TWIN_MIN_M: shortest token panel for pair twins
+      const char* e = std::getenv("SD_GEMM_TWIN_MIN_M");
+      return e ? std::atoi(e) : 1024;
+    }();
+    const bool pair_ok = g_in.causal == 0 && g_in.M >= std::max(256, min_m) && g_in.N >= 256 && g_in.K <= 16384 &&
                          sd_gemm_pair_enabled();
     const bool score_ok = g_in.causal == 1 && g_in.N > 64 && g_in.M == g_in.N;
     // on-chip residuals (an operand without its residual array, e.g. the probe
