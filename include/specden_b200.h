@@ -284,6 +284,10 @@ sd_status sd_gpt_stage_forward(sd_gpt g, int m, const float* x_in, const float* 
                                sd_stream s);
 sd_status sd_gpt_stage_backward(sd_gpt g, int m, const float* gx_in, const float* gdx_in, float* gx_out,
                                 float* gdx_out, sd_stream s);
+/* whole-model Hv = H v on stream s. v is first copied into an engine-owned
+ * buffer; from the second call with the same hv pointer and loss scale the
+ * HVP's kernels replay as one CUDA graph (SD_GPT_GRAPH=0: always launched
+ * one by one); results are bit-identical either way */
 sd_status sd_gpt_hvp(sd_gpt g, const float* v, float* hv, sd_stream s);
 sd_status sd_gpt_last_loss(sd_gpt g, double* loss, sd_stream s);
 sd_status sd_gpt_destroy(sd_gpt g);
