@@ -663,11 +663,13 @@ __global__ void __launch_bounds__(kThreadsFor<TA>(), 1)
         if (lane == 0) mbar_arrive(&tempty[buf]);
       }
       if (ep.tma_store) {
-        const int ew = warp - 2 - CONV;  // 0..7: its staging box
-        const bool t2 = ti.tan;          // twin: C2's tile
+        const int ew = warp - 2 - CONV;                 // 0..7: its staging box
+        const bool second = ep.split && cb >= BN / 2;  // split pair: columns BN/2.. are C2's
+        const bool t2 = ti.tan || second;               // twin: C2's tile
         const CUtensorMap* pcs = t2 ? (ep.Cs2 ? &mCs2 : nullptr) : (ep.Cs ? &mCs : nullptr);
-        warp_tma_store<EC>(t2 ? &mC2 : &mC, pcs, epi_stage + ew * 1024, acc, t2 ? ep.alpha2 : ep.alpha,
-                           t2 ? ep.bias2 : ep.bias, lane, ti.m0 + sub * 32, ti.n0 + cb, ti.z % ep.Z1, ti.z / ep.Z1);
+        warp_tma_store<EC>(t2 ? &mC2 : &mC, pcs, epi_stage + ew * 1024, acc, ti.tan ? ep.alpha2 : ep.alpha,
+                           ti.tan ? ep.bias2 : ep.bias, lane, ti.m0 + sub * 32, ti.n0 + cb - (second ? BN / 2 : 0),
+                           ti.z % ep.Z1, ti.z / ep.Z1);
         if (lane == 0) bulk_wait_read0();  // staging box free for the next tile
         __syncwarp();
       } else if (ti.tan) {
@@ -833,12 +835,27 @@ void launch_split(const GemmArgs& g, cudaStream_t s) {
   const int total_kb = (g.K + BK - 1) / BK;
   EpiParams ep{g.C, g.ldc, g.sc1, g.sc2, g.M, g.N, g.Z1, g.alpha, g.beta, g.bias, g.Cs, g.dbg, zc, total_kb, nullptr,
                g.causal, 1, tm, tm * zc, 2, 1};
-  ep.tma_store = 0;
   ep.mn5 = mn5;
   ep.bexact = 0;
   ep.split = 1;
   ep.C2 = g.C2, ep.Cs2 = g.Cs2;
   ep.group = 0;
+  // TMA-store epilogue: each output's 64 columns as two 32-wide boxes
+  // (SD_SPLIT_TMA_STORE=0: row stores)
+  static const bool tma_on = [] {
+    const char* e = std::getenv("SD_SPLIT_TMA_STORE");
+    return !(e && e[0] == '0');
+  }();
+  GemmArgs g2 = g;
+  g2.C = g.C2, g2.Cs = g.Cs2;
+  CUtensorMap mC = maps[0], mCs = maps[0], mC2 = maps[0], mCs2 = maps[0];
+  ep.tma_store = tma_on && tma_store_ok(g, 1, 32) && tma_store_ok(g2, 1, 32);
+  if (ep.tma_store) {
+    make_store_map(&mC, g.C, g);
+    make_store_map(&mC2, g.C2, g2);
+    if (g.Cs) make_store_map(&mCs, g.Cs, g);
+    if (g.Cs2) make_store_map(&mCs2, g.Cs2, g2);
+  }
   const size_t smem = 1024 + size_t(Cf::STAGES) * 2 * (Cf::A_BYTES + Cf::B_BYTES) + 8 * 4096 + 512;
   auto kern = g.causal ? k_gemm_tf32<A_MN, true, true, BN, true, true> : k_gemm_tf32<A_MN, true, true, BN, false, true>;
   static bool attr = false;
@@ -860,7 +877,7 @@ void launch_split(const GemmArgs& g, cudaStream_t s) {
                       ",1,split";
   prof_begin(s);
   launch_gemm_kernel(kern, unsigned(grid), unsigned(kThreadsFor<true>()), smem, s, maps[0], maps[1], maps[2], maps[3],
-                     maps[4], maps[5], maps[6], maps[7], maps[0], maps[0], maps[0], maps[0], g.K, ep);
+                     maps[4], maps[5], maps[6], maps[7], mC, mCs, mC2, mCs2, g.K, ep);
   SD_LAUNCHED("k_gemm_tf32_split");
   // algorithmic flops of the pair: A B + A B2 + A2 B
   prof_end(s, 6.0 * double(g.M) * g.N * g.K * g.Z1 * g.Z2);
