@@ -98,8 +98,10 @@ bool sd_gemm_tmem_a_enabled() {
   return on;
 }
 
-bool tma_store_ok(const GemmArgs& g, int splits, int bias_cols) {
-  return sd_gemm_tma_store_enabled() && splits == 1 && g.beta == 0.0f &&
+bool tma_store_ok(const GemmArgs& g, int splits, int bias_cols, bool allow_add) {
+  // beta 1 without a residual output: the tile is added in place by a TMA reduce-add store
+  const bool beta_ok = g.beta == 0.0f || (allow_add && g.beta == 1.0f && !g.Cs);
+  return sd_gemm_tma_store_enabled() && splits == 1 && beta_ok &&
          (reinterpret_cast<uintptr_t>(g.C) & 15) == 0 && (g.ldc % 4) == 0 &&
          (!g.Cs || (reinterpret_cast<uintptr_t>(g.Cs) & 15) == 0) &&
          (!g.bias || ((reinterpret_cast<uintptr_t>(g.bias) & 15) == 0 && g.N % bias_cols == 0)) &&
@@ -669,7 +671,7 @@ __global__ void __launch_bounds__(kThreadsFor<TA>(), 1)
         const CUtensorMap* pcs = t2 ? (ep.Cs2 ? &mCs2 : nullptr) : (ep.Cs ? &mCs : nullptr);
         warp_tma_store<EC>(t2 ? &mC2 : &mC, pcs, epi_stage + ew * 1024, acc, ti.tan ? ep.alpha2 : ep.alpha,
                            ti.tan ? ep.bias2 : ep.bias, lane, ti.m0 + sub * 32, ti.n0 + cb - (second ? BN / 2 : 0),
-                           ti.z % ep.Z1, ti.z / ep.Z1);
+                           ti.z % ep.Z1, ti.z / ep.Z1, false);
         if (lane == 0) bulk_wait_read0();  // staging box free for the next tile
         __syncwarp();
       } else if (ti.tan) {

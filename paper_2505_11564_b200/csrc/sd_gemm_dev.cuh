@@ -185,6 +185,7 @@ struct EpiParams {
                                       // 128 accumulator columns [A B | A B2], source 2 adds A2 B into
                                       // columns 64-127; k-blocks interleave 1, 2, 1, 2, ...
   float *C2, *Cs2;                    // split: output of columns 64-127
+  int tma_add;                        // TMA-store epilogue, bit 0 / 1: C / C2 accumulate (beta 1) by reduce-add
   int group;                          // grouped tile walk (raster_group): > 0 groups of `group` m tiles,
                                       // m fastest inside a group; < 0 groups of -group n tiles, n fastest
                                       // inside; 0 n fastest over the whole grid
@@ -277,6 +278,13 @@ __device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, const void*
                "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
                : "memory");
 }
+// ... or added element-wise to C in place (fp32 reduce-add, one writer per element)
+__device__ __forceinline__ void tma_store_add_4d(const CUtensorMap* map, const void* src, int c0, int c1, int c2,
+                                                 int c3) {
+  asm volatile("cp.reduce.async.bulk.tensor.4d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(map),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+               : "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
@@ -305,7 +313,7 @@ __device__ __forceinline__ float lds32(uint32_t a) {
 template <int EC, int BOXC = 32>
 __device__ __forceinline__ void warp_tma_store(const CUtensorMap* mC, const CUtensorMap* mCs, float* stage,
                                                const float (&acc)[EC], float alpha, const float* bias, int lane,
-                                               int row0, int col0, int z1, int z2) {
+                                               int row0, int col0, int z1, int z2, bool add) {
   constexpr int NQ = BOXC / 4;  // 16 B chunks per staged row
   const int sw = BOXC == 32 ? (lane & 7) : ((lane >> 1) & 3);
   const uint32_t rowa = smem_u32(stage + lane * BOXC);
@@ -344,7 +352,8 @@ __device__ __forceinline__ void warp_tma_store(const CUtensorMap* mC, const CUte
       fence_proxy_async_smem_decl();
       __syncwarp();
       if (lane == 0) {
-        tma_store_4d(pass ? mCs : mC, stage, col0 + c0, row0, z1, z2);
+        if (add && pass == 0) tma_store_add_4d(mC, stage, col0 + c0, row0, z1, z2);  // C += o (beta 1)
+        else tma_store_4d(pass ? mCs : mC, stage, col0 + c0, row0, z1, z2);
         bulk_commit();
       }
       pending = true;
@@ -537,7 +546,7 @@ void make_map(CUtensorMap* m, const float* base, long long inner, long long oute
 // box_cols x 32 fp32 boxes (32: 128B swizzle, 16: 64B): the epilogue's TMA store map of C
 void make_store_map(CUtensorMap* m, float* C, const GemmArgs& g, int box_cols = 32);
 // whether a product may take the TMA-store epilogue (beta 0, aligned C/Cs/bias, no split)
-bool tma_store_ok(const GemmArgs& g, int splits, int bias_cols);
+bool tma_store_ok(const GemmArgs& g, int splits, int bias_cols, bool allow_add = false);
 float* splitk_workspace(size_t floats);
 int choose_splits(int tiles, int units, int total_kb, int nsrc, double t_kb, double out_bytes);
 int choose_splits_twin(int tiles, int units, int total_kb, double t_kb, double out_bytes);

@@ -352,7 +352,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         const CUtensorMap* pcs = t2 ? (ep.Cs2 ? &mCs2 : nullptr) : (ep.Cs ? &mCs : nullptr);
         warp_tma_store<EC, 16>(t2 ? &mC2 : &mC, pcs, epi_stage + ew * 512, acc, t2 ? ep.alpha2 : ep.alpha,
                                t2 ? ep.bias2 : ep.bias, lane, ti.m0 + int(rank) * BM + sub * 32, ti.n0 + cb,
-                               ti.z % ep.Z1, ti.z / ep.Z1);
+                               ti.z % ep.Z1, ti.z / ep.Z1, (ep.tma_add >> (t2 ? 1 : 0)) & 1);
         if (lane == 0) bulk_wait_read0();  // staging box free for the next tile
         __syncwarp();
       } else if (ti.tan) {
@@ -442,7 +442,8 @@ void launch_pair_t(const GemmArgs& g, cudaStream_t s) {
   CUtensorMap mC = maps[0], mCs = maps[0], mC2 = maps[0], mCs2 = maps[0];
   GemmArgs g2 = g;  // twin: C2's epilogue
   g2.C = g.C2, g2.Cs = g.Cs2, g2.alpha = g.alpha2, g2.beta = g.beta2, g2.bias = g.bias2;
-  if (tma_store_ok(g, splits, 16) && (!twin || tma_store_ok(g2, splits, 16))) {
+  if (tma_store_ok(g, splits, 16, true) && (!twin || tma_store_ok(g2, splits, 16, true))) {
+    ep.tma_add = (g.beta != 0.0f ? 1 : 0) | (twin && g2.beta != 0.0f ? 2 : 0);
     make_store_map(&mC, g.C, g, 16);
     if (g.Cs) make_store_map(&mCs, g.Cs, g, 16);
     if (twin) {
