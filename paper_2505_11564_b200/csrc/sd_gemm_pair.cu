@@ -346,7 +346,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive_remote(tempty_leader + 8u * buf);
       }
-      if (ep.tma_store) {
+      if (ep.tma_store && ep.ws) {
+        // split-K partial (raw accumulator) through the workspace maps: [split][z][M][N]
+        const int ew = warp - 2 - kConvWarps;
+        warp_tma_store<EC, 16>(ti.tan ? &mC2 : &mC, nullptr, epi_stage + ew * 512, acc, 1.0f, nullptr, lane,
+                               ti.m0 + int(rank) * BM + sub * 32, ti.n0 + cb, ti.split * ep.zcount + ti.z, 0, false);
+        if (lane == 0) bulk_wait_read0();
+        __syncwarp();
+      } else if (ep.tma_store) {
         const int ew = warp - 2 - kConvWarps;  // 0..15: its staging box
         const bool t2 = ti.tan;  // twin: C2's tile
         const CUtensorMap* pcs = t2 ? (ep.Cs2 ? &mCs2 : nullptr) : (ep.Cs ? &mCs : nullptr);
@@ -388,6 +395,14 @@ int max_clusters(const void* kern, size_t smem) {
   int n = 0;
   SD_CUDA(cudaOccupancyMaxActiveClusters(&n, kern, &cfg));
   return n;
+}
+
+bool sd_gemm_partials_tma() {  // SD_GEMM_PARTIALS_TMA=0: split-K partials by row stores
+  static const bool on = [] {
+    const char* e = std::getenv("SD_GEMM_PARTIALS_TMA");
+    return !(e && e[0] == '0');
+  }();
+  return on;
 }
 
 template <bool A_MN, bool B_MN, bool THREE, int PN>
@@ -450,6 +465,13 @@ void launch_pair_t(const GemmArgs& g, cudaStream_t s) {
       make_store_map(&mC2, g2.C, g2, 16);
       if (g2.Cs) make_store_map(&mCs2, g2.Cs, g2, 16);
     }
+    ep.tma_store = 1;
+  } else if (splits > 1 && g.N % 4 == 0 && sd_gemm_partials_tma()) {
+    // split-K partials through TMA stores: the workspace as a [split * z][M][N] tensor
+    GemmArgs gw = g;
+    gw.ldc = g.N, gw.Z1 = splits * zc, gw.sc1 = (long long)g.M * g.N, gw.Z2 = 1, gw.sc2 = 0;
+    make_store_map(&mC, ws, gw, 16);
+    if (twin) make_store_map(&mC2, ws + part, gw, 16);
     ep.tma_store = 1;
   }
   launch_gemm_kernel(kern, unsigned(grid), unsigned(kPairThreads), size_t(smem), s, maps[0], maps[1], maps[2], maps[3],
